@@ -1,0 +1,100 @@
+/* Plain-C restatement of the reference's posit/quire hot path.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline leg may load this library, and only as the checker
+ * -- never as the thing measured or shipped.  The product path
+ * (paper_2105_00053_b200/) never links or calls it.
+ *
+ * Parity pinning: tests/test_oracle_pin.py checks every function here
+ * against (a) the reference's own known-answer tests (proj/tests/
+ * test_quire.cpp, test_tensor.cpp, test_posit.cpp), (b) committed golden
+ * fixtures generated from the unmodified reference (tests/golden/,
+ * tests/golden/make_golden.py), and (c) the reference library itself built
+ * from its sources (oracle/_ref/libpnn_ref.so) on random inputs.
+ *
+ * Codes are right-aligned posit bit patterns in uint64 (reference
+ * tensor.hpp:10-14).  Tensor functions implement the quire (use_quire=true)
+ * semantics of proj/src/tensor_ops.cpp for nbits <= 32.
+ */
+#ifndef POSIT_ORACLE_H
+#define POSIT_ORACLE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Format descriptor: posit.hpp:17-42. */
+int po_max_scale(int nbits, int es);  /* R = (nbits-2) << es */
+int po_quire_bits(int nbits, int es); /* W = 4R + nbits      */
+
+/* detail::unpack, posit.cpp:67-91.  cls: 0 zero, 1 NaR, 2 finite. */
+typedef struct {
+    int cls, neg, scale, fbits;
+    uint64_t sig;  /* normalized: bit 63 set */
+    uint64_t frac; /* fbits-bit fraction field */
+} po_unpacked;
+po_unpacked po_unpack(int nbits, int es, uint64_t code);
+
+/* DecodeTables::Fixed, posit_tables.cpp:43-64. */
+void po_decode_fixed(int nbits, int es, uint64_t code, int32_t* lsb_scale, uint32_t* sig,
+                     uint8_t* neg, uint8_t* nar);
+
+/* detail::pack_round, posit.cpp:93-132. */
+uint64_t po_pack_round(int nbits, int es, int neg, int scale, uint64_t sig, int sticky);
+
+/* Scalar ops: posit.cpp:437-485 (op 0 add, 1 sub, 2 mul, 3 div). */
+uint64_t po_scalar_op(int nbits, int es, int op, uint64_t a, uint64_t b);
+uint64_t po_convert(int sn, int se, int dn, int de, uint64_t code); /* posit.cpp:487-495 */
+int po_compare(int nbits, int es, uint64_t a, uint64_t b);          /* posit.cpp:514-520 */
+uint64_t po_from_float64(int nbits, int es, double x);              /* posit.cpp:502-508 */
+double po_to_float64(int nbits, int es, uint64_t code);             /* posit.cpp:228-236 */
+uint64_t po_ldexp(int nbits, int es, uint64_t code, int k);         /* posit.cpp:522-532 */
+uint64_t po_round_to_int(int nbits, int es, uint64_t code);         /* posit.cpp:534-555 */
+int64_t po_to_int64(int nbits, int es, uint64_t code);              /* posit.cpp:557-563 */
+uint64_t po_from_int64(int nbits, int es, int64_t v);               /* posit_math.cpp:51-57 */
+uint64_t po_exp(int nbits, int es, uint64_t code);                  /* posit_math.cpp:67-85 */
+uint64_t po_log(int nbits, int es, uint64_t code);                  /* posit_math.cpp:87-107 */
+
+/* Quire as an opaque accumulator: quire.hpp:18-86, quire.cpp. */
+typedef struct po_quire po_quire;
+po_quire* po_quire_new(int nbits, int es);
+void po_quire_free(po_quire* q);
+void po_quire_clear(po_quire* q);
+void po_quire_add_posit(po_quire* q, uint64_t a);
+void po_quire_add_product(po_quire* q, uint64_t a, uint64_t b);
+void po_quire_sub_product(po_quire* q, uint64_t a, uint64_t b);
+uint64_t po_quire_to_posit(const po_quire* q);
+/* Raw quire words (little-endian uint64 limbs, W bits, two's complement). */
+int po_quire_words(const po_quire* q, uint64_t* out, int max_words, int* nar);
+
+/* Tensor kernels, quire mode (tensor_ops.cpp).  Return 0 on success. */
+int po_matmul(int nbits, int es, const uint64_t* A, const uint64_t* B, uint64_t* C,
+              int64_t m, int64_t k, int64_t n);
+int po_conv2d(int nbits, int es, const uint64_t* x, int64_t N, int64_t C, int64_t H,
+              int64_t W, const uint64_t* w, int64_t F, int64_t KH, int64_t KW,
+              const uint64_t* bias, int stride, int pad, uint64_t* y);
+int po_conv2d_input_grad(int nbits, int es, const uint64_t* dy, int64_t N, int64_t F,
+                         int64_t OH, int64_t OW, const uint64_t* w, int64_t C, int64_t KH,
+                         int64_t KW, int64_t H, int64_t W, int stride, int pad,
+                         uint64_t* dx);
+int po_conv2d_weight_grad(int nbits, int es, const uint64_t* dy, int64_t N, int64_t F,
+                          int64_t OH, int64_t OW, const uint64_t* x, int64_t C, int64_t H,
+                          int64_t W, int64_t KH, int64_t KW, int stride, int pad,
+                          uint64_t* dw);
+int po_conv2d_bias_grad(int nbits, int es, const uint64_t* dy, int64_t N, int64_t F,
+                        int64_t OH, int64_t OW, uint64_t* db);
+int po_column_sum(int nbits, int es, const uint64_t* x, int64_t B, int64_t N, uint64_t* out);
+int po_maxpool2d(int nbits, int es, const uint64_t* x, int64_t N, int64_t C, int64_t H,
+                 int64_t W, int k, int stride, uint64_t* y, int64_t* argmax);
+int po_maxpool2d_backward(int nbits, int es, const uint64_t* dy, int64_t ny,
+                          const int64_t* argmax, int64_t nx, uint64_t* dx);
+int po_convert_tensor(int sn, int se, int dn, int de, const uint64_t* x, int64_t n,
+                      uint64_t* y);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif
