@@ -1,0 +1,80 @@
+/* pnn_b200 -- C-ABI of the B200-native posit/quire kernels.
+ *
+ * Drop-in boundary for the reference's operator API
+ * (/root/reference/proj/include/pnn/tensor_ops.hpp:17-61, quire.hpp:18-86).
+ * Plain pointers, sizes and int status codes only; no C++ or torch types.
+ *
+ * Conventions (mirroring the reference):
+ *   - A posit format is (nbits, es); every kernel implements the reference's
+ *     use_quire=true path: one exact quire accumulation per output element,
+ *     rounded once (tensor_ops.cpp header comment, lines 10-14).
+ *   - Device entry points (suffix-free) take DEVICE pointers to PACKED codes:
+ *     uint8_t per element for nbits <= 8, uint16_t for 9..16, row-major
+ *     (NCHW activations, FCKK weights), plus a cudaStream_t passed as void*.
+ *     They are asynchronous on that stream.
+ *   - Host entry points (suffix _host) take HOST uint64_t code arrays -- the
+ *     reference Tensor storage (tensor.hpp:10-14, one code per 64-bit slot) --
+ *     and are synchronous, like the reference functions they replace.
+ *   - Status: 0 = ok; nonzero = error, message via pnn_last_error().  The C++
+ *     wrapper (include/pnn_b200/tensor_ops.hpp) rethrows nonzero status as
+ *     std::invalid_argument, the reference's error type (tensor_ops.cpp:17-27).
+ *   - Supported device formats: nbits in [2,16] with 2*max_scale <= 56
+ *     (all of posit(8,0), (8,1), (8,2), (12,1), (16,1)).
+ */
+#ifndef PNN_B200_H
+#define PNN_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PNN_OK 0
+#define PNN_EINVAL 1         /* bad shape / argument (reference: std::invalid_argument) */
+#define PNN_EUNSUPPORTED 2   /* format not supported on device */
+#define PNN_EWORKSPACE 3     /* workspace too small */
+#define PNN_ECUDA 4          /* CUDA runtime error */
+
+const char* pnn_last_error(void);
+int pnn_abi_version(void);
+/* 1 if (nbits, es) runs on the device kernels. */
+int pnn_format_supported(int nbits, int es);
+/* Bytes per packed code on device for nbits (1 or 2). */
+int pnn_code_bytes(int nbits);
+
+/* ---- quire GEMM ---------------------------------------------------------
+ * Replaces matmul(a, b, use_quire=true) -> matmul_quire
+ * (tensor_ops.cpp:461-487, 166-185): C[M,N] = round(A[M,K] . B[K,N]). */
+int pnn_quire_gemm_workspace(int nbits, int es, int64_t M, int64_t N, int64_t K, size_t* bytes);
+int pnn_quire_gemm(int nbits, int es, const void* A, const void* B, void* C, int64_t M, int64_t N,
+                   int64_t K, void* workspace, size_t workspace_bytes, void* stream);
+/* Same, forcing split-K with at most max_kblocks k-blocks per split (tests). */
+int pnn_quire_gemm_splitk(int nbits, int es, const void* A, const void* B, void* C, int64_t M,
+                          int64_t N, int64_t K, int64_t max_kblocks, void* workspace,
+                          size_t workspace_bytes, void* stream);
+/* Host Tensor-storage entry: matmul(a, b, true) on uint64 code arrays. */
+int pnn_matmul_host(int nbits, int es, const uint64_t* A, const uint64_t* B, uint64_t* C,
+                    int64_t M, int64_t K, int64_t N);
+
+/* ---- device posit core (parity / diagnostics) ----------------------------
+ * pnn_decode_x: code -> exact integer image X = value * 2^max_scale and NaR
+ *   flag (detail::unpack posit.cpp:67-91 / DecodeTables::Fixed).
+ * pnn_quire_round: raw W-bit quire words (lo, hi pairs, two's complement,
+ *   LSB 2^-2R) -> posit code (Quire::to_posit, quire.cpp:105-146).
+ * pnn_pack_round: (neg, scale, sig, sticky) -> code (detail::pack_round,
+ *   posit.cpp:93-132). */
+int pnn_decode_x(int nbits, int es, const uint32_t* codes, int64_t n, int64_t* X, uint8_t* nar,
+                 void* stream);
+int pnn_quire_round(int nbits, int es, const uint64_t* q, int64_t n, uint32_t* codes,
+                    void* stream);
+int pnn_pack_round(int nbits, int es, const int32_t* neg, const int32_t* scale,
+                   const uint64_t* sig, const int32_t* sticky, int64_t n, uint32_t* codes,
+                   void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PNN_B200_H */

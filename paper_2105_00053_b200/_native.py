@@ -1,0 +1,79 @@
+"""ctypes binding of libpnn_b200.so (the C-ABI declared in include/pnn_b200.h).
+
+The product path.  There is deliberately no CPU fallback: if the shared
+library is missing or a call returns a nonzero status, we raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import re
+import threading
+
+PKG_DIR = os.path.dirname(os.path.abspath(__file__))
+REPO_DIR = os.path.dirname(PKG_DIR)
+LIB_PATH = os.path.join(PKG_DIR, "libpnn_b200.so")
+HEADER_PATH = os.path.join(REPO_DIR, "include", "pnn_b200.h")
+
+_lock = threading.Lock()
+_lib: C.CDLL | None = None
+
+_i64 = C.c_int64
+_vp = C.c_void_p
+_SIGS = {
+    "pnn_last_error": (C.c_char_p, []),
+    "pnn_abi_version": (C.c_int, []),
+    "pnn_format_supported": (C.c_int, [C.c_int, C.c_int]),
+    "pnn_code_bytes": (C.c_int, [C.c_int]),
+    "pnn_quire_gemm_workspace": (C.c_int, [C.c_int, C.c_int, _i64, _i64, _i64, C.POINTER(C.c_size_t)]),
+    "pnn_quire_gemm": (C.c_int, [C.c_int, C.c_int, _vp, _vp, _vp, _i64, _i64, _i64, _vp, C.c_size_t, _vp]),
+    "pnn_quire_gemm_splitk": (C.c_int, [C.c_int, C.c_int, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _vp,
+                                        C.c_size_t, _vp]),
+    "pnn_matmul_host": (C.c_int, [C.c_int, C.c_int, _vp, _vp, _vp, _i64, _i64, _i64]),
+    "pnn_decode_x": (C.c_int, [C.c_int, C.c_int, _vp, _i64, _vp, _vp, _vp]),
+    "pnn_quire_round": (C.c_int, [C.c_int, C.c_int, _vp, _i64, _vp, _vp]),
+    "pnn_pack_round": (C.c_int, [C.c_int, C.c_int, _vp, _vp, _vp, _vp, _i64, _vp, _vp]),
+}
+
+
+class PnnError(RuntimeError):
+    """A nonzero status from the C-ABI (message from pnn_last_error())."""
+
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"[pnn status {code}] {msg}")
+        self.code = code
+
+
+class PnnInvalidArgument(PnnError, ValueError):
+    """PNN_EINVAL -- the reference raises std::invalid_argument here."""
+
+
+def lib() -> C.CDLL:
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise RuntimeError(
+                    f"{LIB_PATH} is missing: build it with __graft_entry__.build() "
+                    "(there is no CPU fallback)")
+            L = C.CDLL(LIB_PATH)
+            for name, (res, args) in _SIGS.items():
+                fn = getattr(L, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = L
+    return _lib
+
+
+def header_symbols() -> list[str]:
+    """Every function the public C header declares."""
+    txt = open(HEADER_PATH).read()
+    return sorted(set(re.findall(r"\b(pnn_[a-z0-9_]+)\s*\(", txt)))
+
+
+def check(rc: int) -> None:
+    if rc != 0:
+        msg = lib().pnn_last_error().decode(errors="replace")
+        if rc == 1:
+            raise PnnInvalidArgument(rc, msg)
+        raise PnnError(rc, msg)

@@ -1,0 +1,254 @@
+// C-ABI entry points (include/pnn_b200.h).  Argument validation mirrors the
+// reference's checks (tensor_ops.cpp:17-27, 461-466); every error is a status
+// code plus a thread-local message.  There is no CPU fallback: if the device
+// or a kernel fails, the call fails.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "../../include/pnn_b200.h"
+#include "posit_device.cuh"
+#include "quire_gemm.h"
+
+using namespace pnn_b200;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+    return fail(PNN_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+bool fmt_ok(int nbits, int es) {
+    if (nbits < 2 || nbits > 16 || es < 0 || es > 4) return false;
+    const PositFmt f = make_fmt(nbits, es);
+    return 2 * f.R <= 56;
+}
+
+int check_fmt(int nbits, int es) {
+    if (!fmt_ok(nbits, es))
+        return fail(PNN_EUNSUPPORTED, "posit(" + std::to_string(nbits) + "," + std::to_string(es) +
+                                          ") is not supported by the device kernels");
+    return PNN_OK;
+}
+
+cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+// Grow-only device scratch for the synchronous host entry points.
+struct Scratch {
+    std::mutex mu;
+    void* ptr = nullptr;
+    size_t bytes = 0;
+    cudaStream_t stream = nullptr;
+    void* reserve(size_t n) {
+        if (n <= bytes) return ptr;
+        if (ptr) cudaFree(ptr);
+        ptr = nullptr;
+        bytes = 0;
+        if (cudaMalloc(&ptr, n) != cudaSuccess) return nullptr;
+        bytes = n;
+        return ptr;
+    }
+};
+Scratch g_scratch;
+
+__global__ void narrow_codes_kernel(const uint64_t* __restrict__ src, void* __restrict__ dst,
+                                    int64_t n, int code_bytes, uint64_t mask) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        const uint64_t c = src[i] & mask;
+        if (code_bytes == 1) static_cast<uint8_t*>(dst)[i] = uint8_t(c);
+        else static_cast<uint16_t*>(dst)[i] = uint16_t(c);
+    }
+}
+
+__global__ void widen_codes_kernel(const void* __restrict__ src, uint64_t* __restrict__ dst,
+                                   int64_t n, int code_bytes) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        dst[i] = code_bytes == 1 ? uint64_t(static_cast<const uint8_t*>(src)[i])
+                                 : uint64_t(static_cast<const uint16_t*>(src)[i]);
+    }
+}
+
+int blocks_for(int64_t n) {
+    int64_t b = (n + 255) / 256;
+    if (b > 148 * 32) b = 148 * 32;
+    return int(b < 1 ? 1 : b);
+}
+
+__global__ void decode_x_kernel(const uint32_t* codes, int64_t n, PositFmt f, int64_t* X,
+                                uint8_t* nar) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        int64_t x;
+        nar[i] = decode_x(codes[i], f, x) ? 1 : 0;
+        X[i] = x;
+    }
+}
+
+__global__ void quire_round_kernel(const uint64_t* q, int64_t n, PositFmt f, uint32_t* codes) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        const unsigned __int128 v = (unsigned __int128)q[2 * i] | ((unsigned __int128)q[2 * i + 1] << 64);
+        codes[i] = quire_to_posit(f, v);
+    }
+}
+
+__global__ void pack_round_kernel(const int32_t* neg, const int32_t* scale, const uint64_t* sig,
+                                  const int32_t* sticky, int64_t n, PositFmt f, uint32_t* codes) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        codes[i] = pack_round(f, neg[i] != 0, scale[i], sig[i], sticky[i] != 0);
+    }
+}
+
+int gemm_common(int nbits, int es, const void* A, const void* B, void* C, int64_t M, int64_t N,
+                int64_t K, int64_t max_kb, void* ws, size_t ws_bytes, void* stream) {
+    if (int rc = check_fmt(nbits, es)) return rc;
+    if (M < 0 || N < 0 || K < 0) return fail(PNN_EINVAL, "matmul: negative dimension");
+    if (M == 0 || N == 0) return PNN_OK;
+    const int cb = nbits <= 8 ? 1 : 2;
+    if (K == 0) {  // reference returns an all-zero tensor (tensor_ops.cpp:467)
+        cudaError_t e = cudaMemsetAsync(C, 0, size_t(M * N) * cb, as_stream(stream));
+        return e == cudaSuccess ? PNN_OK : cuda_fail(e, "matmul memset");
+    }
+    if (!A || !B || !C) return fail(PNN_EINVAL, "matmul: null pointer");
+    int rc = quire_gemm_launch(nbits, es, A, B, C, M, N, K, K, N, N, ws, ws_bytes, max_kb,
+                               as_stream(stream), nullptr);
+    if (rc == 3) return fail(PNN_EWORKSPACE, "matmul: workspace too small");
+    if (rc == 2) return fail(PNN_EUNSUPPORTED, "matmul: format not supported");
+    if (rc == 4) return cuda_fail(cudaGetLastError(), "matmul launch");
+    return rc;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* pnn_last_error(void) { return g_err.c_str(); }
+
+int pnn_abi_version(void) { return 1; }
+
+int pnn_format_supported(int nbits, int es) { return fmt_ok(nbits, es) ? 1 : 0; }
+
+int pnn_code_bytes(int nbits) { return nbits <= 8 ? 1 : 2; }
+
+int pnn_quire_gemm_workspace(int nbits, int es, int64_t M, int64_t N, int64_t K, size_t* bytes) {
+    if (int rc = check_fmt(nbits, es)) return rc;
+    if (M < 0 || N < 0 || K < 0 || !bytes) return fail(PNN_EINVAL, "matmul: bad arguments");
+    QuireGemmPlan p;
+    if (M == 0 || N == 0 || K == 0) {
+        *bytes = 0;
+        return PNN_OK;
+    }
+    if (quire_gemm_plan(nbits, es, M, N, K, 0, &p)) return fail(PNN_EUNSUPPORTED, "format");
+    *bytes = p.workspace_bytes;
+    return PNN_OK;
+}
+
+int pnn_quire_gemm(int nbits, int es, const void* A, const void* B, void* C, int64_t M, int64_t N,
+                   int64_t K, void* workspace, size_t workspace_bytes, void* stream) {
+    return gemm_common(nbits, es, A, B, C, M, N, K, 0, workspace, workspace_bytes, stream);
+}
+
+int pnn_quire_gemm_splitk(int nbits, int es, const void* A, const void* B, void* C, int64_t M,
+                          int64_t N, int64_t K, int64_t max_kblocks, void* workspace,
+                          size_t workspace_bytes, void* stream) {
+    if (max_kblocks < 1) return fail(PNN_EINVAL, "splitk: max_kblocks must be >= 1");
+    return gemm_common(nbits, es, A, B, C, M, N, K, max_kblocks, workspace, workspace_bytes,
+                       stream);
+}
+
+int pnn_matmul_host(int nbits, int es, const uint64_t* A, const uint64_t* B, uint64_t* C,
+                    int64_t M, int64_t K, int64_t N) {
+    if (int rc = check_fmt(nbits, es)) return rc;
+    if (M < 0 || N < 0 || K < 0) return fail(PNN_EINVAL, "matmul: negative dimension");
+    if (M == 0 || N == 0) return PNN_OK;
+    if (K == 0) {
+        std::memset(C, 0, size_t(M * N) * 8);
+        return PNN_OK;
+    }
+    std::lock_guard<std::mutex> lock(g_scratch.mu);
+    if (!g_scratch.stream) {
+        if (cudaError_t e = cudaStreamCreateWithFlags(&g_scratch.stream, cudaStreamNonBlocking))
+            return cuda_fail(e, "stream");
+    }
+    cudaStream_t st = g_scratch.stream;
+    QuireGemmPlan p;
+    if (quire_gemm_plan(nbits, es, M, N, K, 0, &p)) return fail(PNN_EUNSUPPORTED, "format");
+    const int cb = nbits <= 8 ? 1 : 2;
+    auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+    const size_t wide_a = al(size_t(M * K) * 8), wide_b = al(size_t(K * N) * 8),
+                 wide_c = al(size_t(M * N) * 8);
+    const size_t pa = al(size_t(M * K) * cb), pb = al(size_t(K * N) * cb), pc = al(size_t(M * N) * cb);
+    uint8_t* base = static_cast<uint8_t*>(
+        g_scratch.reserve(wide_a + wide_b + wide_c + pa + pb + pc + p.workspace_bytes));
+    if (!base) return fail(PNN_ECUDA, "matmul_host: device allocation failed");
+    uint64_t* dA64 = reinterpret_cast<uint64_t*>(base);
+    uint64_t* dB64 = reinterpret_cast<uint64_t*>(base + wide_a);
+    uint64_t* dC64 = reinterpret_cast<uint64_t*>(base + wide_a + wide_b);
+    uint8_t* dA = base + wide_a + wide_b + wide_c;
+    uint8_t* dB = dA + pa;
+    uint8_t* dC = dB + pb;
+    uint8_t* ws = dC + pc;
+    const uint64_t mask = (uint64_t(1) << nbits) - 1;
+    cudaError_t e;
+    if ((e = cudaMemcpyAsync(dA64, A, size_t(M * K) * 8, cudaMemcpyHostToDevice, st)))
+        return cuda_fail(e, "H2D A");
+    if ((e = cudaMemcpyAsync(dB64, B, size_t(K * N) * 8, cudaMemcpyHostToDevice, st)))
+        return cuda_fail(e, "H2D B");
+    narrow_codes_kernel<<<blocks_for(M * K), 256, 0, st>>>(dA64, dA, M * K, cb, mask);
+    narrow_codes_kernel<<<blocks_for(K * N), 256, 0, st>>>(dB64, dB, K * N, cb, mask);
+    int rc = quire_gemm_launch(nbits, es, dA, dB, dC, M, N, K, K, N, N, ws, p.workspace_bytes, 0,
+                               st, nullptr);
+    if (rc) return rc == 4 ? cuda_fail(cudaGetLastError(), "matmul launch") : fail(rc, "matmul");
+    widen_codes_kernel<<<blocks_for(M * N), 256, 0, st>>>(dC, dC64, M * N, cb);
+    if ((e = cudaMemcpyAsync(C, dC64, size_t(M * N) * 8, cudaMemcpyDeviceToHost, st)))
+        return cuda_fail(e, "D2H C");
+    if ((e = cudaStreamSynchronize(st))) return cuda_fail(e, "matmul_host sync");
+    return PNN_OK;
+}
+
+int pnn_decode_x(int nbits, int es, const uint32_t* codes, int64_t n, int64_t* X, uint8_t* nar,
+                 void* stream) {
+    if (int rc = check_fmt(nbits, es)) return rc;
+    if (n <= 0) return PNN_OK;
+    decode_x_kernel<<<blocks_for(n), 256, 0, as_stream(stream)>>>(codes, n, make_fmt(nbits, es), X,
+                                                                   nar);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? PNN_OK : cuda_fail(e, "decode_x");
+}
+
+int pnn_quire_round(int nbits, int es, const uint64_t* q, int64_t n, uint32_t* codes,
+                    void* stream) {
+    if (int rc = check_fmt(nbits, es)) return rc;
+    if (n <= 0) return PNN_OK;
+    quire_round_kernel<<<blocks_for(n), 256, 0, as_stream(stream)>>>(q, n, make_fmt(nbits, es),
+                                                                      codes);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? PNN_OK : cuda_fail(e, "quire_round");
+}
+
+int pnn_pack_round(int nbits, int es, const int32_t* neg, const int32_t* scale,
+                   const uint64_t* sig, const int32_t* sticky, int64_t n, uint32_t* codes,
+                   void* stream) {
+    if (nbits < 2 || nbits > 32 || es < 0 || es > 4)
+        return fail(PNN_EUNSUPPORTED, "pack_round: bad format");
+    if (n <= 0) return PNN_OK;
+    pack_round_kernel<<<blocks_for(n), 256, 0, as_stream(stream)>>>(neg, scale, sig, sticky, n,
+                                                                     make_fmt(nbits, es), codes);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? PNN_OK : cuda_fail(e, "pack_round");
+}
+
+}  // extern "C"

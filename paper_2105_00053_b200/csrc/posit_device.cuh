@@ -1,0 +1,147 @@
+// Device posit core: decode to the exact integer image, balanced int8 digit
+// split, and quire -> posit rounding.  sm_100a only.
+//
+// Reference semantics:
+//   decode        : detail::unpack            proj/src/posit.cpp:67-91
+//                   DecodeTables::Fixed        proj/src/posit_tables.cpp:43-64
+//   pack_round    : detail::pack_round         proj/src/posit.cpp:93-132
+//   quire readout : Quire::to_posit            proj/src/quire.cpp:105-146
+//
+// Integer image.  For format (n, es) with R = (n-2)<<es every posit x is
+// x = X * 2^-R with X an exact integer, |X| <= 2^(2R).  The reference quire
+// (W = 4R + n bits, LSB weight 2^-2R, quire.hpp:20-30) after accumulating
+// products holds exactly  sum(X_a * X_b) mod 2^W.  Everything below works on X.
+#pragma once
+
+#include <cstdint>
+
+namespace pnn_b200 {
+
+struct PositFmt {
+    int nbits;
+    int es;
+    int R;  // max_scale
+    int W;  // quire bits
+};
+
+__host__ __device__ inline PositFmt make_fmt(int nbits, int es) {
+    PositFmt f;
+    f.nbits = nbits;
+    f.es = es;
+    f.R = (nbits - 2) << es;
+    f.W = 4 * f.R + nbits;
+    return f;
+}
+
+// Decode one code into X (two's complement int64).  Returns true for NaR.
+// Valid for 2 <= nbits <= 32 and 2R <= 62 (X fits int64).
+__device__ __forceinline__ bool decode_x(uint32_t code, const PositFmt& f, int64_t& X) {
+    const uint32_t mask = f.nbits == 32 ? 0xFFFFFFFFu : ((1u << f.nbits) - 1u);
+    code &= mask;
+    X = 0;
+    if (code == 0) return false;
+    const uint32_t nar = 1u << (f.nbits - 1);
+    if (code == nar) return true;
+    const bool neg = (code & nar) != 0;
+    const uint32_t mag = neg ? ((0u - code) & mask) : code;
+    // payload (nbits-1 bits) left-aligned in 32 bits; low bits are zero
+    const uint32_t p = mag << (33 - f.nbits);
+    const bool first = (p >> 31) != 0;
+    int run = first ? __clz(~p) : __clz(p);
+    if (run > f.nbits - 1) run = f.nbits - 1;
+    const int k = first ? run - 1 : -run;
+    const int used = run + 1;
+    int rem = f.nbits - 1 - used;
+    if (rem < 0) rem = 0;
+    const uint32_t tail = used < 32 ? (p << used) : 0u;
+    const int ebits = f.es < rem ? f.es : rem;
+    uint32_t e = ebits > 0 ? (tail >> (32 - ebits)) : 0u;
+    e <<= (f.es - ebits);
+    const int fb = rem - ebits;
+    const uint32_t frac = fb > 0 ? ((tail << ebits) >> (32 - fb)) : 0u;
+    const int scale = k * (1 << f.es) + int(e);
+    const uint64_t sig = (uint64_t(1) << fb) | frac;
+    const int pos = scale - fb + f.R;  // >= 0 for every finite posit
+    const int64_t mx = int64_t(sig << pos);
+    X = neg ? -mx : mx;
+    return false;
+}
+
+// Balanced base-256 digits: X = sum_d digit[d] * 256^d, digit in [-128, 127].
+template <int D>
+__device__ __forceinline__ void balanced_digits(int64_t X, int8_t (&dig)[D]) {
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+        const int8_t t = int8_t(uint8_t(uint64_t(X) & 0xFF));
+        dig[d] = t;
+        X = (X - int64_t(t)) >> 8;
+    }
+}
+
+// detail::pack_round restated with a 64-bit window (nbits <= 32, so regime +
+// exponent + guard always fit): round-to-nearest, ties to the even pattern,
+// saturate at maxpos, never round to zero.
+__device__ __forceinline__ uint32_t pack_round(const PositFmt& f, bool neg, int scale,
+                                               uint64_t sig, bool sticky) {
+    if (sig == 0) return 0;
+    uint32_t pat;
+    if (scale >= f.R) {
+        pat = (1u << (f.nbits - 1)) - 1u;
+    } else if (scale < -f.R) {
+        pat = 1u;
+    } else {
+        const int k = scale >> f.es;                  // floor division
+        const int e = scale - (k << f.es);
+        const int rl = k >= 0 ? k + 2 : 1 - k;        // regime incl. terminator
+        const uint64_t regime = k >= 0 ? (((uint64_t(1) << (k + 1)) - 1) << 1) : 1;
+        const int head = rl + f.es;                   // < 64
+        uint64_t w = regime << (64 - rl);
+        if (f.es > 0) w |= uint64_t(e) << (64 - head);
+        const uint64_t frac = sig << 1;               // 63 fraction bits, left-aligned
+        w |= frac >> head;
+        bool st = sticky || (frac << (64 - head)) != 0;
+        pat = uint32_t(w >> (65 - f.nbits));
+        const bool guard = (w >> (64 - f.nbits)) & 1;
+        st = st || (w << f.nbits) != 0;
+        if (guard && (st || (pat & 1))) ++pat;
+    }
+    const uint32_t mask = f.nbits == 32 ? 0xFFFFFFFFu : ((1u << f.nbits) - 1u);
+    return neg ? ((0u - pat) & mask) : pat;
+}
+
+// Quire::to_posit on a W-bit two's complement value held in 128 bits
+// (W <= 128).  LSB weight 2^-2R.
+__device__ __forceinline__ uint32_t quire_to_posit(const PositFmt& f, unsigned __int128 q) {
+    const unsigned __int128 one = 1;
+    const unsigned __int128 m = f.W >= 128 ? ~(unsigned __int128)0 : ((one << f.W) - 1);
+    q &= m;
+    const bool neg = ((q >> (f.W - 1)) & 1) != 0;
+    const unsigned __int128 mag = neg ? ((0 - q) & m) : q;
+    if (mag == 0) return 0;
+    const uint64_t hi = uint64_t(mag >> 64), lo = uint64_t(mag);
+    const int top = hi ? 127 - __clzll(hi) : 63 - __clzll(lo);
+    uint64_t sig;
+    bool sticky;
+    if (top >= 63) {
+        const int drop = top - 63;
+        sig = uint64_t(mag >> drop);
+        sticky = drop > 0 && (mag & ((one << drop) - 1)) != 0;
+    } else {
+        sig = lo << (63 - top);
+        sticky = false;
+    }
+    return pack_round(f, neg, top - 2 * f.R, sig, sticky);
+}
+
+// 64-bit variant for W <= 64 (e.g. posit(8,0) W=32, posit(8,1) W=56).
+__device__ __forceinline__ uint32_t quire_to_posit64(const PositFmt& f, uint64_t q) {
+    const uint64_t m = f.W >= 64 ? ~uint64_t(0) : ((uint64_t(1) << f.W) - 1);
+    q &= m;
+    const bool neg = ((q >> (f.W - 1)) & 1) != 0;
+    const uint64_t mag = neg ? ((0 - q) & m) : q;
+    if (mag == 0) return 0;
+    const int top = 63 - __clzll(mag);
+    return pack_round(f, neg, top - 2 * f.R, mag << (63 - top), false);
+}
+
+}  // namespace pnn_b200
