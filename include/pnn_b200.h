@@ -54,6 +54,13 @@ int pnn_quire_gemm(int nbits, int es, const void* A, const void* B, void* C, int
 int pnn_quire_gemm_splitk(int nbits, int es, const void* A, const void* B, void* C, int64_t M,
                           int64_t N, int64_t K, int64_t max_kblocks, void* workspace,
                           size_t workspace_bytes, void* stream);
+/* Same as pnn_quire_gemm, then synchronizes the stream and reports the
+ * device time (CUDA events on that stream) of each phase in milliseconds:
+ * ms[0] operand decode/pack, ms[1] tcgen05 MMA kernel, ms[2] split-K finalize.
+ * For benchmarking / roofline accounting only. */
+int pnn_quire_gemm_profiled(int nbits, int es, const void* A, const void* B, void* C, int64_t M,
+                            int64_t N, int64_t K, void* workspace, size_t workspace_bytes,
+                            void* stream, float* ms);
 /* Host Tensor-storage entry: matmul(a, b, true) on uint64 code arrays. */
 int pnn_matmul_host(int nbits, int es, const uint64_t* A, const uint64_t* B, uint64_t* C,
                     int64_t M, int64_t K, int64_t N);

@@ -29,6 +29,8 @@ _SIGS = {
     "pnn_quire_gemm": (C.c_int, [C.c_int, C.c_int, _vp, _vp, _vp, _i64, _i64, _i64, _vp, C.c_size_t, _vp]),
     "pnn_quire_gemm_splitk": (C.c_int, [C.c_int, C.c_int, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _vp,
                                         C.c_size_t, _vp]),
+    "pnn_quire_gemm_profiled": (C.c_int, [C.c_int, C.c_int, _vp, _vp, _vp, _i64, _i64, _i64, _vp,
+                                          C.c_size_t, _vp, C.POINTER(C.c_float)]),
     "pnn_matmul_host": (C.c_int, [C.c_int, C.c_int, _vp, _vp, _vp, _i64, _i64, _i64]),
     "pnn_decode_x": (C.c_int, [C.c_int, C.c_int, _vp, _i64, _vp, _vp, _vp]),
     "pnn_quire_round": (C.c_int, [C.c_int, C.c_int, _vp, _i64, _vp, _vp]),

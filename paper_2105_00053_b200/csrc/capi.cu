@@ -169,6 +169,29 @@ int pnn_quire_gemm_splitk(int nbits, int es, const void* A, const void* B, void*
                        stream);
 }
 
+int pnn_quire_gemm_profiled(int nbits, int es, const void* A, const void* B, void* C, int64_t M,
+                            int64_t N, int64_t K, void* workspace, size_t workspace_bytes,
+                            void* stream, float* ms) {
+    if (int rc = check_fmt(nbits, es)) return rc;
+    if (M <= 0 || N <= 0 || K <= 0 || !A || !B || !C || !ms)
+        return fail(PNN_EINVAL, "profiled gemm: bad arguments");
+    QuireGemmStats stats;
+    for (auto& e : stats.ev) cudaEventCreate(&e);
+    cudaStream_t st = as_stream(stream);
+    int rc = quire_gemm_launch(nbits, es, A, B, C, M, N, K, K, N, N, workspace, workspace_bytes, 0,
+                               st, &stats);
+    if (rc == 0) {
+        cudaError_t e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) rc = cuda_fail(e, "profiled gemm sync");
+        else
+            for (int i = 0; i < 3; ++i) cudaEventElapsedTime(&ms[i], stats.ev[i], stats.ev[i + 1]);
+    } else {
+        rc = fail(rc, "profiled gemm launch failed");
+    }
+    for (auto& e : stats.ev) cudaEventDestroy(e);
+    return rc;
+}
+
 int pnn_matmul_host(int nbits, int es, const uint64_t* A, const uint64_t* B, uint64_t* C,
                     int64_t M, int64_t K, int64_t N) {
     if (int rc = check_fmt(nbits, es)) return rc;
