@@ -100,7 +100,7 @@ __global__ void quire_round_kernel(const uint64_t* q, int64_t n, PositFmt f, uin
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
          i += int64_t(gridDim.x) * blockDim.x) {
         const unsigned __int128 v = (unsigned __int128)q[2 * i] | ((unsigned __int128)q[2 * i + 1] << 64);
-        codes[i] = quire_to_posit(f, v);
+        codes[i] = f.nbits <= 16 ? quire_word_to_posit(f, v) : quire_to_posit(f, v);
     }
 }
 
@@ -108,7 +108,11 @@ __global__ void pack_round_kernel(const int32_t* neg, const int32_t* scale, cons
                                   const int32_t* sticky, int64_t n, PositFmt f, uint32_t* codes) {
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
          i += int64_t(gridDim.x) * blockDim.x) {
-        codes[i] = pack_round(f, neg[i] != 0, scale[i], sig[i], sticky[i] != 0);
+        if (f.nbits <= 16)
+            codes[i] = pack_round32(f, neg[i] != 0, scale[i], uint32_t(sig[i] >> 32),
+                                    sticky[i] != 0 || uint32_t(sig[i]) != 0);
+        else
+            codes[i] = pack_round(f, neg[i] != 0, scale[i], sig[i], sticky[i] != 0);
     }
 }
 

@@ -109,6 +109,81 @@ __device__ __forceinline__ uint32_t pack_round(const PositFmt& f, bool neg, int 
     return neg ? ((0u - pat) & mask) : pat;
 }
 
+// pack_round with a 32-bit window for nbits <= 16 (regime <= 15 bits, es <= 4):
+// identical results to pack_round with sig = sig32 << 32 | low, sticky |= low != 0.
+__device__ __forceinline__ uint32_t pack_round32(const PositFmt& f, bool neg, int scale,
+                                                 uint32_t sig32, bool sticky) {
+    uint32_t pat;
+    if (scale >= f.R) {
+        pat = (1u << (f.nbits - 1)) - 1u;
+    } else if (scale < -f.R) {
+        pat = 1u;
+    } else {
+        const int k = scale >> f.es;
+        const int e = scale - (k << f.es);
+        const int rl = k >= 0 ? k + 2 : 1 - k;
+        const uint32_t regime = k >= 0 ? (((1u << (k + 1)) - 1u) << 1) : 1u;
+        const int head = rl + f.es;  // in [2, 19]
+        uint32_t w = regime << (32 - rl);
+        if (f.es > 0) w |= uint32_t(e) << (32 - head);
+        const uint32_t frac = sig32 << 1;
+        w |= frac >> head;
+        bool st = sticky || (frac << (32 - head)) != 0;
+        pat = w >> (33 - f.nbits);
+        const bool guard = (w >> (32 - f.nbits)) & 1u;
+        st = st || (w << f.nbits) != 0;
+        if (guard && (st || (pat & 1u))) ++pat;
+    }
+    const uint32_t mask = (1u << f.nbits) - 1u;
+    return neg ? ((0u - pat) & mask) : pat;
+}
+
+// Quire word (W <= 32 / 64 / 128 bits held in uint32 / uint64 / u128) -> posit,
+// nbits <= 16.  Same result as quire_to_posit.
+__device__ __forceinline__ uint32_t quire_word_to_posit(const PositFmt& f, uint32_t q) {
+    const uint32_t m = f.W >= 32 ? 0xFFFFFFFFu : ((1u << f.W) - 1u);
+    q &= m;
+    const bool neg = ((q >> (f.W - 1)) & 1u) != 0;
+    const uint32_t mag = neg ? ((0u - q) & m) : q;
+    if (mag == 0) return 0;
+    const int top = 31 - __clz(mag);
+    return pack_round32(f, neg, top - 2 * f.R, mag << (31 - top), false);
+}
+__device__ __forceinline__ uint32_t quire_word_to_posit(const PositFmt& f, uint64_t q) {
+    const uint64_t m = f.W >= 64 ? ~uint64_t(0) : ((uint64_t(1) << f.W) - 1);
+    q &= m;
+    const bool neg = ((q >> (f.W - 1)) & 1) != 0;
+    const uint64_t mag = neg ? ((0 - q) & m) : q;
+    if (mag == 0) return 0;
+    const int top = 63 - __clzll(mag);
+    const uint64_t sig = mag << (63 - top);
+    return pack_round32(f, neg, top - 2 * f.R, uint32_t(sig >> 32), uint32_t(sig) != 0);
+}
+__device__ __forceinline__ uint32_t quire_word_to_posit(const PositFmt& f, unsigned __int128 q) {
+    const unsigned __int128 one = 1;
+    const unsigned __int128 m = f.W >= 128 ? ~(unsigned __int128)0 : ((one << f.W) - 1);
+    q &= m;
+    const bool neg = ((q >> (f.W - 1)) & 1) != 0;
+    const unsigned __int128 mag = neg ? ((0 - q) & m) : q;
+    if (mag == 0) return 0;
+    const uint64_t hi = uint64_t(mag >> 64), lo = uint64_t(mag);
+    int top;
+    uint64_t sig;
+    bool sticky;
+    if (hi) {
+        const int lz = __clzll(hi);
+        top = 127 - lz;
+        sig = lz ? ((hi << lz) | (lo >> (64 - lz))) : hi;
+        sticky = lz ? (lo << lz) != 0 : lo != 0;
+    } else {
+        const int lz = __clzll(lo);
+        top = 63 - lz;
+        sig = lo << lz;
+        sticky = false;
+    }
+    return pack_round32(f, neg, top - 2 * f.R, uint32_t(sig >> 32), sticky || uint32_t(sig) != 0);
+}
+
 // Quire::to_posit on a W-bit two's complement value held in 128 bits
 // (W <= 128).  LSB weight 2^-2R.
 __device__ __forceinline__ uint32_t quire_to_posit(const PositFmt& f, unsigned __int128 q) {

@@ -47,7 +47,8 @@ template <> struct TileCfg<7> { static constexpr int NT = 32, KB = 32, STAGES = 
 template <> struct TileCfg<8> { static constexpr int NT = 32, KB = 32, STAGES = 5; };
 
 constexpr int kBM = 128;          // output rows per CTA (UMMA M)
-constexpr int kThreads = 192;     // 6 warps
+constexpr int kEpiWarps = 8;      // epilogue warps (2 per TMEM lane quarter)
+constexpr int kThreads = 64 + 32 * kEpiWarps;  // producer + MMA + epilogue
 constexpr int kZeroBytes = kBM * 32;
 
 template <int D>
@@ -61,6 +62,7 @@ struct Geometry {
     static constexpr int B_BYTES = D * NT * KB;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
     static constexpr int SMEM = STAGES * STAGE_BYTES + kZeroBytes + 256;
+    static_assert((NT / 2) % 8 == 0, "epilogue column split");
     static constexpr uint32_t TMEM_COLS = 512;
     static_assert(G * NT <= 512, "TMEM overflow");
     static_assert(NMMA % 16 == 0 && NMMA <= 256, "bad UMMA N");
@@ -188,28 +190,65 @@ __device__ __forceinline__ void store_codes8(CodeT* dst, const uint32_t (&c)[8],
     }
 }
 
-template <int D, bool kWide, typename CodeT>
+template <int QW>
+struct QuireWord;
+template <> struct QuireWord<1> { using T = uint32_t; };
+template <> struct QuireWord<2> { using T = uint64_t; };
+template <> struct QuireWord<4> { using T = unsigned __int128; };
+
+// Sign-extend an int32 group sum and weight it by 256^g, modulo the word size
+// (the quire itself is only defined mod 2^W <= word bits).
+template <typename T>
+__device__ __forceinline__ T group_term(uint32_t acc, int sh) {
+    if constexpr (sizeof(T) == 4) return T(acc) << sh;
+    else if constexpr (sizeof(T) == 8) return T(int64_t(int32_t(acc))) << sh;
+    else return T(__int128(int32_t(acc))) << sh;
+}
+
+// Raster: tiles grouped by kGroupM m-tiles so the ~148 tiles in flight share
+// A and B digit planes in L2.
+constexpr int kGroupM = 8;
+
+__device__ __forceinline__ void tile_coords(int64_t t, int64_t mtiles, int64_t ntiles,
+                                            int64_t& split, int64_t& mt, int64_t& nt) {
+    const int64_t per_split = mtiles * ntiles;
+    split = t / per_split;
+    const int64_t r = t - split * per_split;
+    const int64_t group = r / (kGroupM * ntiles);
+    const int64_t within = r - group * (kGroupM * ntiles);
+    const int64_t gm = min(int64_t(kGroupM), mtiles - group * kGroupM);
+    mt = group * kGroupM + within % gm;
+    nt = within / gm;
+}
+
+// Persistent, warp-specialized: warp 0 = bulk-copy producer, warp 1 = MMA
+// issuer, warps 2..9 = epilogue (2 warps per TMEM lane quarter, each owning
+// half of the tile's columns).  The epilogue drains TMEM into registers,
+// releases it (tmem_empty), and rounds/stores while the next tile's MMAs run.
+template <int D, int QW, typename CodeT>
 __global__ void __launch_bounds__(kThreads, 1)
     quire_gemm_tc_kernel(const int8_t* __restrict__ a_img, const int8_t* __restrict__ b_img,
                          int64_t kbt, int64_t kb_per_split, const uint8_t* __restrict__ row_nar,
                          const uint8_t* __restrict__ col_nar, CodeT* __restrict__ C, int64_t M,
                          int64_t N, int64_t ldc, PositFmt f,
-                         unsigned __int128* __restrict__ partial) {
+                         unsigned __int128* __restrict__ partial, int64_t mtiles, int64_t ntiles,
+                         int64_t splits) {
     using Geo = Geometry<D>;
+    using QT = typename QuireWord<QW>::T;
     constexpr int NT = Geo::NT, KB = Geo::KB, STAGES = Geo::STAGES, G = Geo::G;
+    constexpr int COLS = NT / 2;                 // columns per epilogue thread
+    constexpr int GB = G < 8 ? G : 8;            // TMEM loads batched per wait
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* zero_tile = smem + STAGES * Geo::STAGE_BYTES;
     uint64_t* full = reinterpret_cast<uint64_t*>(zero_tile + kZeroBytes);
     uint64_t* empty = full + STAGES;
     uint64_t* tmem_full = empty + STAGES;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+    uint64_t* tmem_empty = tmem_full + 1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 1);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    const int64_t nt = blockIdx.x, mt = blockIdx.y, split = blockIdx.z;
-    const int64_t kb0 = split * kb_per_split;
-    const int64_t kb1 = min(kbt, kb0 + kb_per_split);
-    const int nkb = int(kb1 - kb0);
+    const int64_t tiles = mtiles * ntiles * splits;
 
     for (int i = threadIdx.x; i < kZeroBytes / 16; i += kThreads)
         reinterpret_cast<int4*>(zero_tile)[i] = make_int4(0, 0, 0, 0);
@@ -219,6 +258,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::mbar_init(&empty[s], 1);
         }
         ptx::mbar_init(tmem_full, 1);
+        ptx::mbar_init(tmem_empty, kEpiWarps);
         ptx::fence_barrier_init();
     }
     if (warp == 1) ptx::tmem_alloc<Geo::TMEM_COLS>(tmem_slot);
@@ -231,17 +271,24 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 0) {
         if (lane == 0) {
             // ===== producer: one bulk copy per operand per stage =====
-            const int8_t* a_src = a_img + (mt * kbt + kb0) * int64_t(Geo::A_BYTES);
-            const int8_t* b_src = b_img + (nt * kbt + kb0) * int64_t(Geo::B_BYTES);
-            for (int i = 0; i < nkb; ++i) {
-                const int s = i % STAGES;
-                const uint32_t ph = (i / STAGES) & 1;
-                ptx::mbar_wait(&empty[s], ph ^ 1);
-                uint8_t* sa = smem + s * Geo::STAGE_BYTES;
-                ptx::mbar_arrive_expect_tx(&full[s], Geo::STAGE_BYTES);
-                ptx::bulk_g2s(sa, a_src + int64_t(i) * Geo::A_BYTES, Geo::A_BYTES, &full[s]);
-                ptx::bulk_g2s(sa + Geo::A_BYTES, b_src + int64_t(i) * Geo::B_BYTES, Geo::B_BYTES,
-                              &full[s]);
+            uint32_t it = 0;
+            for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+                int64_t split, mt, nt;
+                tile_coords(t, mtiles, ntiles, split, mt, nt);
+                const int64_t kb0 = split * kb_per_split;
+                const int nkb = int(min(kbt, kb0 + kb_per_split) - kb0);
+                const int8_t* a_src = a_img + (mt * kbt + kb0) * int64_t(Geo::A_BYTES);
+                const int8_t* b_src = b_img + (nt * kbt + kb0) * int64_t(Geo::B_BYTES);
+                for (int i = 0; i < nkb; ++i, ++it) {
+                    const int s = it % STAGES;
+                    const uint32_t ph = (it / STAGES) & 1;
+                    ptx::mbar_wait(&empty[s], ph ^ 1);
+                    uint8_t* sa = smem + s * Geo::STAGE_BYTES;
+                    ptx::mbar_arrive_expect_tx(&full[s], Geo::STAGE_BYTES);
+                    ptx::bulk_g2s(sa, a_src + int64_t(i) * Geo::A_BYTES, Geo::A_BYTES, &full[s]);
+                    ptx::bulk_g2s(sa + Geo::A_BYTES, b_src + int64_t(i) * Geo::B_BYTES,
+                                  Geo::B_BYTES, &full[s]);
+                }
             }
         }
     } else if (warp == 1) {
@@ -250,80 +297,99 @@ __global__ void __launch_bounds__(kThreads, 1)
             constexpr uint32_t idesc = ptx::idesc_i8(kBM, Geo::NMMA);
             constexpr uint32_t SBO = 8 * KB, LBO = 128;
             const uint64_t zdesc = ptx::smem_desc_kmajor(ptx::smem_u32(zero_tile), LBO, 8 * 32);
-            for (int i = 0; i < nkb; ++i) {
-                const int s = i % STAGES;
-                const uint32_t ph = (i / STAGES) & 1;
-                ptx::mbar_wait(&full[s], ph);
+            uint32_t it = 0, j = 0;
+            for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++j) {
+                int64_t split, mt, nt;
+                tile_coords(t, mtiles, ntiles, split, mt, nt);
+                const int64_t kb0 = split * kb_per_split;
+                const int nkb = int(min(kbt, kb0 + kb_per_split) - kb0);
+                ptx::mbar_wait(tmem_empty, (j & 1) ^ 1);  // epilogue drained the previous tile
                 ptx::tc_fence_after();
-                const uint32_t a_base = ptx::smem_u32(smem + s * Geo::STAGE_BYTES);
-                const uint32_t b_base = a_base + Geo::A_BYTES;
+                for (int i = 0; i < nkb; ++i, ++it) {
+                    const int s = it % STAGES;
+                    const uint32_t ph = (it / STAGES) & 1;
+                    ptx::mbar_wait(&full[s], ph);
+                    ptx::tc_fence_after();
+                    const uint32_t a_base = ptx::smem_u32(smem + s * Geo::STAGE_BYTES);
+                    const uint32_t b_base = a_base + Geo::A_BYTES;
 #pragma unroll
-                for (int ks = 0; ks < KB / 32; ++ks) {
-                    const uint64_t bdesc = ptx::smem_desc_kmajor(b_base + ks * 256, LBO, SBO);
-                    const bool first = (i == 0 && ks == 0);
-                    if (first)  // zero groups D-1 .. 2D-2 (plane 0 initialises 0 .. D-1)
-                        ptx::mma_i8(tmem + (D - 1) * NT, zdesc, bdesc, idesc, 0);
+                    for (int ks = 0; ks < KB / 32; ++ks) {
+                        const uint64_t bdesc = ptx::smem_desc_kmajor(b_base + ks * 256, LBO, SBO);
+                        const bool first = (i == 0 && ks == 0);
+                        if (first)  // zero groups D-1 .. 2D-2 (plane 0 initialises 0 .. D-1)
+                            ptx::mma_i8(tmem + (D - 1) * NT, zdesc, bdesc, idesc, 0);
 #pragma unroll
-                    for (int p = 0; p < D; ++p) {
-                        const uint64_t adesc =
-                            ptx::smem_desc_kmajor(a_base + p * (kBM * KB) + ks * 256, LBO, SBO);
-                        ptx::mma_i8(tmem + p * NT, adesc, bdesc, idesc, (first && p == 0) ? 0u : 1u);
+                        for (int p = 0; p < D; ++p) {
+                            const uint64_t adesc = ptx::smem_desc_kmajor(
+                                a_base + p * (kBM * KB) + ks * 256, LBO, SBO);
+                            ptx::mma_i8(tmem + p * NT, adesc, bdesc, idesc,
+                                        (first && p == 0) ? 0u : 1u);
+                        }
                     }
+                    ptx::mma_commit(&empty[s]);
                 }
-                ptx::mma_commit(&empty[s]);
+                ptx::mma_commit(tmem_full);
             }
-            ptx::mma_commit(tmem_full);
         }
     } else {
-        // ===== epilogue: TMEM -> 128-bit quire -> posit =====
+        // ===== epilogue: TMEM -> quire words (registers) -> posit codes =====
         const int quarter = warp & 3;
-        const int64_t row = mt * kBM + quarter * 32 + lane;
-        ptx::mbar_wait(tmem_full, 0);
-        ptx::tc_fence_after();
-        const uint32_t trow = tmem + (uint32_t(quarter * 32) << 16);
-        const bool rnar = (row < M) && row_nar[row];
+        const int half = (warp - 2) >> 2;
+        const uint32_t trow = tmem + (uint32_t(quarter * 32) << 16) + half * COLS;
         const bool vec_ok = (ldc % 8) == 0;
-        for (int c0 = 0; c0 < NT; c0 += 8) {
-            uint32_t r[G][8];
+        uint32_t j = 0;
+        for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++j) {
+            int64_t split, mt, nt;
+            tile_coords(t, mtiles, ntiles, split, mt, nt);
+            ptx::mbar_wait(tmem_full, j & 1);
+            ptx::tc_fence_after();
+            QT q[COLS];
 #pragma unroll
-            for (int g = 0; g < G; ++g) ptx::tmem_ld8(trow + g * NT + c0, r[g]);
-            ptx::tmem_wait_ld();
-            const int64_t col0 = nt * NT + c0;
-            if (row >= M || col0 >= N) continue;
-            const int valid = int(N - col0 < 8 ? N - col0 : 8);
-            if (partial != nullptr) {
-                unsigned __int128* dst = partial + (split * M + row) * N + col0;
-                for (int j = 0; j < valid; ++j) {
-                    unsigned __int128 q = 0;
+            for (int c = 0; c < COLS; ++c) q[c] = 0;
 #pragma unroll
-                    for (int g = 0; g < G; ++g)
-                        q += (unsigned __int128)(__int128)int32_t(r[g][j]) << (8 * g);
-                    dst[j] = q;
+            for (int c0 = 0; c0 < COLS; c0 += 8) {
+#pragma unroll
+                for (int g0 = 0; g0 < G; g0 += GB) {
+                    uint32_t r[GB][8];
+#pragma unroll
+                    for (int g = 0; g < GB; ++g)
+                        if (g0 + g < G) ptx::tmem_ld8(trow + (g0 + g) * NT + c0, r[g]);
+                    ptx::tmem_wait_ld();
+#pragma unroll
+                    for (int g = 0; g < GB; ++g)
+                        if (g0 + g < G)
+#pragma unroll
+                            for (int x = 0; x < 8; ++x) q[c0 + x] += group_term<QT>(r[g][x], 8 * (g0 + g));
                 }
-                continue;
             }
-            uint32_t codes[8];
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(tmem_empty);
+
+            const int64_t row = mt * kBM + quarter * 32 + lane;
+            if (row >= M) continue;
+            const bool rnar = row_nar[row] != 0;
+            const int64_t colbase = nt * NT + half * COLS;
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                const bool nar = rnar || (col0 + j < N && col_nar[col0 + j]);
-                if (nar) {
-                    codes[j] = 1u << (f.nbits - 1);
+            for (int c0 = 0; c0 < COLS; c0 += 8) {
+                const int64_t col0 = colbase + c0;
+                if (col0 >= N) break;
+                const int valid = int(N - col0 < 8 ? N - col0 : 8);
+                if (partial != nullptr) {
+                    unsigned __int128* dst = partial + (split * M + row) * N + col0;
+#pragma unroll
+                    for (int x = 0; x < 8; ++x)
+                        if (x < valid) dst[x] = (unsigned __int128)q[c0 + x];
                     continue;
                 }
-                if constexpr (kWide) {
-                    unsigned __int128 q = 0;
+                uint32_t codes[8];
 #pragma unroll
-                    for (int g = 0; g < G; ++g)
-                        q += (unsigned __int128)(__int128)int32_t(r[g][j]) << (8 * g);
-                    codes[j] = quire_to_posit(f, q);
-                } else {
-                    uint64_t q = 0;
-#pragma unroll
-                    for (int g = 0; g < G; ++g) q += uint64_t(int64_t(int32_t(r[g][j]))) << (8 * g);
-                    codes[j] = quire_to_posit64(f, q);
+                for (int x = 0; x < 8; ++x) {
+                    const bool nar = rnar || (x < valid && col_nar[col0 + x]);
+                    codes[x] = nar ? (1u << (f.nbits - 1)) : quire_word_to_posit(f, q[c0 + x]);
                 }
+                store_codes8(C + row * ldc + col0, codes, valid, vec_ok);
             }
-            store_codes8(C + row * ldc + col0, codes, valid, vec_ok);
         }
     }
     __syncwarp();
@@ -351,7 +417,7 @@ __global__ void quire_finalize_kernel(const unsigned __int128* __restrict__ part
         } else {
             unsigned __int128 q = 0;
             for (int s = 0; s < splits; ++s) q += partial[s * total + idx];
-            code = quire_to_posit(f, q);
+            code = quire_word_to_posit(f, q);
         }
         C[i * ldc + j] = CodeT(code);
     }
@@ -425,6 +491,17 @@ int quire_gemm_plan(int nbits, int es, int64_t M, int64_t N, int64_t K, int64_t 
     return 0;
 }
 
+static int num_sms() {
+    static int n = 0;
+    if (n == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
 static int grid_for(int64_t items, int threads) {
     int64_t b = (items + threads - 1) / threads;
     if (b > 148 * 64) b = 148 * 64;
@@ -454,14 +531,21 @@ static cudaError_t launch_typed(const QuireGemmPlan& p, const PositFmt& f, const
     pack_b_kernel<D, CodeT><<<grid_for(b_items, 256), 256, 0, st>>>(B, K, N, ldb, f, b_img, cnar,
                                                                      p.kbt);
     if (stats) cudaEventRecord(stats->ev[1], st);
-    const bool wide = f.W > 64;
-    auto kern = wide ? quire_gemm_tc_kernel<D, true, CodeT> : quire_gemm_tc_kernel<D, false, CodeT>;
+    // D <= 3 implies R <= 11, hence W <= 64: no 128-bit instantiation needed.
+    void (*kern)(const int8_t*, const int8_t*, int64_t, int64_t, const uint8_t*, const uint8_t*,
+                 CodeT*, int64_t, int64_t, int64_t, PositFmt, unsigned __int128*, int64_t, int64_t,
+                 int64_t);
+    if constexpr (D <= 3)
+        kern = f.W <= 32 ? quire_gemm_tc_kernel<D, 1, CodeT> : quire_gemm_tc_kernel<D, 2, CodeT>;
+    else
+        kern = f.W <= 64 ? quire_gemm_tc_kernel<D, 2, CodeT> : quire_gemm_tc_kernel<D, 4, CodeT>;
     if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Geo::SMEM)) !=
         cudaSuccess)
         return e;
-    dim3 grid(unsigned(p.ntiles), unsigned(p.mtiles), unsigned(p.splits));
+    const int64_t tiles = p.mtiles * p.ntiles * p.splits;
+    const int grid = int(tiles < num_sms() ? tiles : num_sms());
     kern<<<grid, kThreads, Geo::SMEM, st>>>(a_img, b_img, p.kbt, p.kb_per_split, rnar, cnar, C, M,
-                                            N, ldc, f, partial);
+                                            N, ldc, f, partial, p.mtiles, p.ntiles, p.splits);
     if (stats) cudaEventRecord(stats->ev[2], st);
     if (p.splits > 1) {
         quire_finalize_kernel<CodeT><<<grid_for(M * N, 256), 256, 0, st>>>(
