@@ -124,9 +124,16 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def int8_peak():
-    """Measured dense int8 tensor peak (TOPS): profiles/int8_peak.json if the
-    measurement exists, else 2x the measured bf16 burst figure."""
+def int8_peak(L=None):
+    """Dense int8 tensor-pipe peak (TOPS) measured on this GPU: the tcgen05
+    kind::i8 probe (pnn_probe_int8_peak: back-to-back 128x256x32 MMAs from
+    shared memory on every SM, CUDA events), else profiles/int8_peak.json
+    (cuBLASLt int8 GEMM), else 2x the measured bf16 burst figure."""
+    if L is not None:
+        tops, ms = C.c_double(), C.c_double()
+        if L.pnn_probe_int8_peak(20000, C.byref(tops), C.byref(ms)) == 0:
+            return tops.value, (f"measured tensor-pipe ceiling: tcgen05 kind::i8 probe, 148 SMs x "
+                                f"20000 MMAs 128x256x32, {ms.value:.2f} ms")
     p = os.path.join(REPO, "profiles", "int8_peak.json")
     if os.path.exists(p):
         d = json.load(open(p))
@@ -276,7 +283,7 @@ def main():
     D = {8: 2, 16: 8}[ncfg.nbits] if ncfg.es <= 1 else None
     int8_ops = 2.0 * M * N * K * D * D  # algorithmic int8 ops per launch (D^2 digit MMAs / MAC)
     achieved = int8_ops / (per_fmt[dom]["mma_ms"] / 1000.0) / 1e12
-    peak, peak_src = int8_peak()
+    peak, peak_src = int8_peak(L)
 
     # ---- e2e through the reference-facing host API (uint64 Tensor storage) ----
     e2e = None

@@ -65,6 +65,37 @@ int pnn_quire_gemm_profiled(int nbits, int es, const void* A, const void* B, voi
 int pnn_matmul_host(int nbits, int es, const uint64_t* A, const uint64_t* B, uint64_t* C,
                     int64_t M, int64_t K, int64_t N);
 
+/* ---- Conv2d / Linear passes (implicit GEMMs on the same tcgen05 core) -----
+ * Shapes follow the reference: x [N,C,H,W], w [F,C,KH,KW], bias [F] or NULL,
+ * y/dy [N,F,OH,OW] with OH = (H+2pad-KH)/stride+1.  A Linear layer is the
+ * 1x1 convolution of x [B,in,1,1] with w [out,in,1,1].
+ * pass: 0 forward (conv2d, tensor_ops.cpp:494-525 -- bias inside the quire),
+ *       1 input grad (conv2d_input_grad, :527-574),
+ *       2 weight grad (conv2d_weight_grad, :576-603). */
+int pnn_conv2d_workspace(int pass, int nbits, int es, int64_t N, int64_t C, int64_t H, int64_t W,
+                         int64_t F, int64_t KH, int64_t KW, int stride, int pad, int has_bias,
+                         size_t* bytes);
+int pnn_conv2d_fwd(int nbits, int es, const void* x, int64_t N, int64_t C, int64_t H, int64_t W,
+                   const void* w, int64_t F, int64_t KH, int64_t KW, const void* bias, int stride,
+                   int pad, void* y, void* workspace, size_t workspace_bytes, void* stream);
+int pnn_conv2d_dgrad(int nbits, int es, const void* dy, int64_t N, int64_t F, int64_t OH,
+                     int64_t OW, const void* w, int64_t C, int64_t KH, int64_t KW, int64_t H,
+                     int64_t W, int stride, int pad, void* dx, void* workspace,
+                     size_t workspace_bytes, void* stream);
+/* dw codes [F,C,KH,KW] (may be NULL) and/or the exact unrounded quire words
+ * (16 bytes each, W-bit two's complement, same layout) + NaR mask -- the
+ * data-parallel reduction input. */
+int pnn_conv2d_wgrad(int nbits, int es, const void* dy, int64_t N, int64_t F, int64_t OH,
+                     int64_t OW, const void* x, int64_t C, int64_t H, int64_t W, int64_t KH,
+                     int64_t KW, int stride, int pad, void* dw, void* raw_words, void* raw_nar,
+                     void* workspace, size_t workspace_bytes, void* stream);
+/* conv2d_bias_grad (tensor_ops.cpp:605-618) for dy [N,F,P] with P = OH*OW,
+ * and column_sum (:722-731) with P = 1: db[f] = round(quire sum of dy[:,f,:]). */
+int pnn_bias_grad_workspace(int64_t F, size_t* bytes);
+int pnn_bias_grad(int nbits, int es, const void* dy, int64_t N, int64_t F, int64_t P, void* db,
+                  void* raw_words, void* raw_nar, void* workspace, size_t workspace_bytes,
+                  void* stream);
+
 /* ---- device posit core (parity / diagnostics) ----------------------------
  * pnn_decode_x: code -> exact integer image X = value * 2^max_scale and NaR
  *   flag (detail::unpack posit.cpp:67-91 / DecodeTables::Fixed).
@@ -79,6 +110,13 @@ int pnn_quire_round(int nbits, int es, const uint64_t* q, int64_t n, uint32_t* c
 int pnn_pack_round(int nbits, int es, const int32_t* neg, const int32_t* scale,
                    const uint64_t* sig, const int32_t* sticky, int64_t n, uint32_t* codes,
                    void* stream);
+
+/* ---- measurement ---------------------------------------------------------
+ * Tensor-pipe ceiling for the kind::i8 MMA shape the quire GEMM issues
+ * (M=128, N=256, K=32 from shared memory), one CTA per SM, `iters` MMAs each;
+ * returns int8 TOPS (2 ops per MAC) and the launch time.  Roofline
+ * denominator for bench.py. */
+int pnn_probe_int8_peak(int iters, double* tops, double* ms);
 
 #ifdef __cplusplus
 }

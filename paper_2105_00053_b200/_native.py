@@ -35,6 +35,18 @@ _SIGS = {
     "pnn_decode_x": (C.c_int, [C.c_int, C.c_int, _vp, _i64, _vp, _vp, _vp]),
     "pnn_quire_round": (C.c_int, [C.c_int, C.c_int, _vp, _i64, _vp, _vp]),
     "pnn_pack_round": (C.c_int, [C.c_int, C.c_int, _vp, _vp, _vp, _vp, _i64, _vp, _vp]),
+    "pnn_conv2d_workspace": (C.c_int, [C.c_int, C.c_int, C.c_int] + [_i64] * 7 + [C.c_int, C.c_int, C.c_int,
+                                                                           C.POINTER(C.c_size_t)]),
+    "pnn_conv2d_fwd": (C.c_int, [C.c_int, C.c_int, _vp] + [_i64] * 4 + [_vp] + [_i64] * 3 +
+                       [_vp, C.c_int, C.c_int, _vp, _vp, C.c_size_t, _vp]),
+    "pnn_conv2d_dgrad": (C.c_int, [C.c_int, C.c_int, _vp] + [_i64] * 4 + [_vp] + [_i64] * 5 +
+                         [C.c_int, C.c_int, _vp, _vp, C.c_size_t, _vp]),
+    "pnn_conv2d_wgrad": (C.c_int, [C.c_int, C.c_int, _vp] + [_i64] * 4 + [_vp] + [_i64] * 5 +
+                         [C.c_int, C.c_int, _vp, _vp, _vp, _vp, C.c_size_t, _vp]),
+    "pnn_bias_grad_workspace": (C.c_int, [_i64, C.POINTER(C.c_size_t)]),
+    "pnn_bias_grad": (C.c_int, [C.c_int, C.c_int, _vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp, C.c_size_t,
+                                _vp]),
+    "pnn_probe_int8_peak": (C.c_int, [C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
 }
 
 

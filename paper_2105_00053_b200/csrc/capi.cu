@@ -12,6 +12,7 @@
 #include "../../include/pnn_b200.h"
 #include "posit_device.cuh"
 #include "quire_gemm.h"
+#include "status.h"
 
 using namespace pnn_b200;
 
@@ -23,6 +24,18 @@ int fail(int code, const std::string& msg) {
     g_err = msg;
     return code;
 }
+
+}  // namespace
+
+namespace pnn_b200 {
+void set_last_error(const std::string& msg) { g_err = msg; }
+int set_status(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+}  // namespace pnn_b200
+
+namespace {
 
 int cuda_fail(cudaError_t e, const char* where) {
     return fail(PNN_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));

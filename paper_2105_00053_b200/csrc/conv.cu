@@ -1,0 +1,440 @@
+// Conv2d / Linear passes as implicit GEMMs on the tcgen05 quire core.
+//
+//   forward      conv2d -> conv_quire            proj/src/tensor_ops.cpp:494-525, 266-297
+//                  GEMM  M = N*OH*OW pixels, N = F, K = C*KH*KW (+1: bias * 1.0 inside the quire, :292)
+//   input grad   conv2d_input_grad               tensor_ops.cpp:527-574
+//                  GEMM  M = N*H*W, N = C, K = F*KH*KW (taps that fail the divisibility /
+//                        range tests of :546-554 are zero and carry no NaR)
+//   weight grad  conv2d_weight_grad              tensor_ops.cpp:576-603
+//                  GEMM  M = C*KH*KW, N = F, K = N*OH*OW (batch reduction; split-K)
+//   bias grad    conv2d_bias_grad / column_sum   tensor_ops.cpp:605-618, 722-731
+//                  CUDA-core exact 128-bit reduction (quire sum of X * 2^R)
+//
+// A Linear layer is the 1x1 convolution of [B, in, 1, 1].
+// NaR: an output is NaR iff one of ITS terms has a NaR operand (quire.hpp:55,
+// NaR * 0 included).  For forward and weight-grad every k of the GEMM is a
+// term, so operand row/column flags are exact; for input-grad the weight-side
+// flag is applied per output over its valid taps only (dgrad_weight_nar).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "../../include/pnn_b200.h"
+#include "quire_gemm_core.cuh"
+#include "status.h"
+
+namespace pnn_b200 {
+
+struct ConvGeom {
+    int64_t N, C, H, W, F, KH, KW, OH, OW;
+    int stride, pad;
+};
+
+// ---- forward ---------------------------------------------------------------
+
+template <typename CodeT>
+struct FetchIm2colFwd {  // X[r = (n,oy,ox)][k = (c,ky,kx) | bias col]
+    const CodeT* x;
+    ConvGeom g;
+    int64_t kconv;
+    uint32_t one_code;
+    static constexpr bool kRowFastest = true;
+    __device__ __forceinline__ uint32_t operator()(int64_t r, int64_t k) const {
+        if (k >= kconv) return one_code;
+        const int64_t ohw = g.OH * g.OW;
+        const int64_t n = r / ohw, p = r - n * ohw, oy = p / g.OW, ox = p - oy * g.OW;
+        const int64_t khw = g.KH * g.KW;
+        const int64_t c = k / khw, t = k - c * khw, ky = t / g.KW, kx = t - ky * g.KW;
+        const int64_t iy = oy * g.stride + ky - g.pad, ix = ox * g.stride + kx - g.pad;
+        if (iy < 0 || iy >= g.H || ix < 0 || ix >= g.W) return 0;
+        return uint32_t(x[((n * g.C + c) * g.H + iy) * g.W + ix]);
+    }
+};
+
+template <typename CodeT>
+struct FetchWeightFwd {  // X[r = f][k = (c,ky,kx) | bias col]
+    const CodeT* w;
+    const CodeT* bias;
+    int64_t kconv;
+    static constexpr bool kRowFastest = false;
+    __device__ __forceinline__ uint32_t operator()(int64_t r, int64_t k) const {
+        return k < kconv ? uint32_t(w[r * kconv + k]) : uint32_t(bias[r]);
+    }
+};
+
+// ---- input grad --------------------------------------------------------------
+
+template <typename CodeT>
+struct FetchDgradDy {  // X[r = (n,iy,ix)][k = (f,ky,kx)]
+    const CodeT* dy;
+    ConvGeom g;
+    static constexpr bool kRowFastest = true;
+    __device__ __forceinline__ uint32_t operator()(int64_t r, int64_t k) const {
+        const int64_t hw = g.H * g.W;
+        const int64_t n = r / hw, p = r - n * hw, iy = p / g.W, ix = p - iy * g.W;
+        const int64_t khw = g.KH * g.KW;
+        const int64_t f = k / khw, t = k - f * khw, ky = t / g.KW, kx = t - ky * g.KW;
+        const int64_t ty = iy + g.pad - ky, tx = ix + g.pad - kx;
+        if (ty < 0 || tx < 0 || ty % g.stride || tx % g.stride) return 0;
+        const int64_t oy = ty / g.stride, ox = tx / g.stride;
+        if (oy >= g.OH || ox >= g.OW) return 0;
+        return uint32_t(dy[((n * g.F + f) * g.OH + oy) * g.OW + ox]);
+    }
+};
+
+template <typename CodeT>
+struct FetchDgradW {  // X[r = c][k = (f,ky,kx)] = w[f][c][ky][kx]
+    const CodeT* w;
+    ConvGeom g;
+    static constexpr bool kRowFastest = false;
+    __device__ __forceinline__ uint32_t operator()(int64_t r, int64_t k) const {
+        const int64_t khw = g.KH * g.KW;
+        const int64_t f = k / khw, t = k - f * khw;
+        return uint32_t(w[(f * g.C + r) * khw + t]);
+    }
+};
+
+// Weight-side NaR of the input gradient, exact per output over its valid taps.
+// Runs only when the pack pass saw a NaR weight (flag set on device).
+template <typename CodeT>
+__global__ void dgrad_weight_nar_kernel(CodeT* __restrict__ dx, const CodeT* __restrict__ w,
+                                        ConvGeom g, const uint8_t* __restrict__ any_nar_w,
+                                        uint32_t nar) {
+    if (*any_nar_w == 0) return;
+    const int64_t total = g.N * g.C * g.H * g.W;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t ix = i % g.W, iy = (i / g.W) % g.H, c = (i / (g.W * g.H)) % g.C;
+        bool hit = false;
+        for (int64_t f = 0; f < g.F && !hit; ++f)
+            for (int64_t ky = 0; ky < g.KH && !hit; ++ky) {
+                const int64_t ty = iy + g.pad - ky;
+                if (ty < 0 || ty % g.stride || ty / g.stride >= g.OH) continue;
+                for (int64_t kx = 0; kx < g.KW; ++kx) {
+                    const int64_t tx = ix + g.pad - kx;
+                    if (tx < 0 || tx % g.stride || tx / g.stride >= g.OW) continue;
+                    if (uint32_t(w[((f * g.C + c) * g.KH + ky) * g.KW + kx]) == nar) {
+                        hit = true;
+                        break;
+                    }
+                }
+            }
+        if (hit) dx[i] = CodeT(nar);
+    }
+}
+
+// ---- weight grad -------------------------------------------------------------
+
+template <typename CodeT>
+struct FetchWgradX {  // X[r = (c,ky,kx)][k = (n,oy,ox)] = x_pad[n][c][oy*s+ky][ox*s+kx]
+    const CodeT* x;
+    ConvGeom g;
+    static constexpr bool kRowFastest = false;
+    __device__ __forceinline__ uint32_t operator()(int64_t r, int64_t k) const {
+        const int64_t khw = g.KH * g.KW;
+        const int64_t c = r / khw, t = r - c * khw, ky = t / g.KW, kx = t - ky * g.KW;
+        const int64_t ohw = g.OH * g.OW;
+        const int64_t n = k / ohw, p = k - n * ohw, oy = p / g.OW, ox = p - oy * g.OW;
+        const int64_t iy = oy * g.stride + ky - g.pad, ix = ox * g.stride + kx - g.pad;
+        if (iy < 0 || iy >= g.H || ix < 0 || ix >= g.W) return 0;
+        return uint32_t(x[((n * g.C + c) * g.H + iy) * g.W + ix]);
+    }
+};
+
+template <typename CodeT>
+struct FetchWgradDy {  // X[r = f][k = (n,o)] = dy[n][f][o]
+    const CodeT* dy;
+    ConvGeom g;
+    static constexpr bool kRowFastest = false;
+    __device__ __forceinline__ uint32_t operator()(int64_t r, int64_t k) const {
+        const int64_t ohw = g.OH * g.OW;
+        const int64_t n = k / ohw, p = k - n * ohw;
+        return uint32_t(dy[(n * g.F + r) * ohw + p]);
+    }
+};
+
+// ---- bias grad / column sum -------------------------------------------------
+
+// Exact quire sum of dy over (n, pixel) per channel: Q_f = 2^R * sum X (mod
+// 2^W).  Stage 1: each block reduces a slice of (n) for one f into a 128-bit
+// partial (|sum X| < 2^56 * 2^31 fits); stage 2 sums partials and rounds.
+template <typename CodeT>
+__global__ void __launch_bounds__(256) bias_grad_partial_kernel(
+    const CodeT* __restrict__ dy, int64_t N, int64_t F, int64_t P, PositFmt f, int slices,
+    unsigned __int128* __restrict__ partial, uint8_t* __restrict__ nar_out) {
+    const int64_t ch = blockIdx.x, slice = blockIdx.y;
+    const int64_t per = (N + slices - 1) / slices;
+    const int64_t n0 = slice * per, n1 = min(N, n0 + per);
+    __int128 acc = 0;
+    bool nar = false;
+    for (int64_t n = n0; n < n1; ++n) {
+        const CodeT* row = dy + (n * F + ch) * P;
+        for (int64_t o = threadIdx.x; o < P; o += blockDim.x) {
+            int64_t X;
+            nar |= decode_x(uint32_t(row[o]), f, X);
+            acc += X;
+        }
+    }
+    __shared__ unsigned long long lo_s[256], hi_s[256];
+    __shared__ int nar_s;
+    if (threadIdx.x == 0) nar_s = 0;
+    __syncthreads();
+    if (nar) nar_s = 1;
+    lo_s[threadIdx.x] = (unsigned long long)(uint64_t(acc));
+    hi_s[threadIdx.x] = (unsigned long long)(uint64_t((unsigned __int128)acc >> 64));
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned __int128 s = 0;
+        for (int i = 0; i < blockDim.x; ++i)
+            s += (unsigned __int128)lo_s[i] | ((unsigned __int128)hi_s[i] << 64);
+        partial[ch * slices + slice] = s;
+        if (nar_s) nar_out[ch] = 1;
+    }
+}
+
+template <typename CodeT>
+__global__ void bias_grad_final_kernel(const unsigned __int128* __restrict__ partial, int slices,
+                                       const uint8_t* __restrict__ nar_in, int64_t F, PositFmt f,
+                                       CodeT* __restrict__ out, unsigned __int128* raw_words,
+                                       uint8_t* raw_nar) {
+    const unsigned __int128 one = 1;
+    const unsigned __int128 wmask = f.W >= 128 ? ~(unsigned __int128)0 : ((one << f.W) - 1);
+    for (int64_t ch = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; ch < F;
+         ch += int64_t(gridDim.x) * blockDim.x) {
+        unsigned __int128 s = 0;
+        for (int i = 0; i < slices; ++i) s += partial[ch * slices + i];
+        const unsigned __int128 q = (s << f.R) & wmask;  // accumulate_value: X * 2^R
+        if (raw_words) {
+            raw_words[ch] = q;
+            raw_nar[ch] = nar_in[ch];
+        }
+        if (out) out[ch] = CodeT(nar_in[ch] ? (1u << (f.nbits - 1)) : quire_word_to_posit(f, q));
+    }
+}
+
+}  // namespace pnn_b200
+
+// =========================================================================
+// C-ABI
+// =========================================================================
+
+using namespace pnn_b200;
+
+namespace {
+
+bool conv_fmt_ok(int nbits, int es) {
+    if (nbits < 2 || nbits > 16 || es < 0 || es > 4) return false;
+    return 2 * make_fmt(nbits, es).R <= 56;
+}
+
+int conv_geom(int64_t N, int64_t C, int64_t H, int64_t W, int64_t F, int64_t KH, int64_t KW,
+              int stride, int pad, ConvGeom* g) {
+    if (N < 0 || C < 1 || H < 1 || W < 1 || F < 1 || KH < 1 || KW < 1 || stride < 1 || pad < 0)
+        return set_status(PNN_EINVAL, "conv: invalid shape or argument");
+    if (H + 2 * pad < KH || W + 2 * pad < KW) return set_status(PNN_EINVAL, "conv: invalid shape or argument");  // tensor_ops.cpp:215
+    g->N = N; g->C = C; g->H = H; g->W = W; g->F = F; g->KH = KH; g->KW = KW;
+    g->stride = stride;
+    g->pad = pad;
+    g->OH = (H + 2 * pad - KH) / stride + 1;
+    g->OW = (W + 2 * pad - KW) / stride + 1;
+    return PNN_OK;
+}
+
+// Logical GEMM sizes per pass.
+void pass_dims(int pass, const ConvGeom& g, bool has_bias, int64_t* M, int64_t* Nn, int64_t* K) {
+    const int64_t kconv = g.C * g.KH * g.KW;
+    if (pass == 0) {
+        *M = g.N * g.OH * g.OW; *Nn = g.F; *K = kconv + (has_bias ? 1 : 0);
+    } else if (pass == 1) {
+        *M = g.N * g.H * g.W; *Nn = g.C; *K = g.F * g.KH * g.KW;
+    } else {
+        *M = kconv; *Nn = g.F; *K = g.N * g.OH * g.OW;
+    }
+}
+
+int status_of(int rc, const char* what) {
+    if (rc == 0) return PNN_OK;
+    set_last_error(std::string(what) + (rc == 2 ? ": format not supported"
+                                        : rc == 3 ? ": workspace too small"
+                                                  : ": CUDA launch failed"));
+    return rc == 2 ? PNN_EUNSUPPORTED : rc == 3 ? PNN_EWORKSPACE : PNN_ECUDA;
+}
+
+uint32_t one_code(const PositFmt& f) { return 1u << (f.nbits - 2); }  // 0b01000.. = 1.0
+
+}  // namespace
+
+extern "C" {
+
+int pnn_conv2d_workspace(int pass, int nbits, int es, int64_t N, int64_t C, int64_t H, int64_t W,
+                         int64_t F, int64_t KH, int64_t KW, int stride, int pad, int has_bias,
+                         size_t* bytes) {
+    if (!conv_fmt_ok(nbits, es)) return set_status(PNN_EUNSUPPORTED, "conv: format not supported");
+    ConvGeom g;
+    if (!bytes || pass < 0 || pass > 2 || conv_geom(N, C, H, W, F, KH, KW, stride, pad, &g))
+        return set_status(PNN_EINVAL, "conv: invalid shape or argument");
+    int64_t M, Nn, K;
+    pass_dims(pass, g, has_bias != 0, &M, &Nn, &K);
+    if (M == 0 || K == 0) {
+        *bytes = 0;
+        return PNN_OK;
+    }
+    QuireGemmPlan p;
+    if (plan_quire_gemm(make_fmt(nbits, es), M, Nn, K, 0, pass == 2, &p)) return PNN_EUNSUPPORTED;
+    *bytes = p.workspace_bytes;
+    return PNN_OK;
+}
+
+int pnn_conv2d_fwd(int nbits, int es, const void* x, int64_t N, int64_t C, int64_t H, int64_t W,
+                   const void* w, int64_t F, int64_t KH, int64_t KW, const void* bias, int stride,
+                   int pad, void* y, void* workspace, size_t workspace_bytes, void* stream) {
+    if (!conv_fmt_ok(nbits, es)) return set_status(PNN_EUNSUPPORTED, "conv: format not supported");
+    ConvGeom g;
+    if (conv_geom(N, C, H, W, F, KH, KW, stride, pad, &g) || !x || !w || !y) return set_status(PNN_EINVAL, "conv: invalid shape or argument");
+    if (N == 0) return PNN_OK;
+    GemmArgs a;
+    a.f = make_fmt(nbits, es);
+    pass_dims(0, g, bias != nullptr, &a.M, &a.N, &a.K);
+    a.max_kb_per_split = 0;
+    a.row_nar = a.col_nar = true;
+    const int64_t kconv = C * KH * KW;
+    auto st = static_cast<cudaStream_t>(stream);
+    int rc;
+    if (nbits <= 8) {
+        using T = uint8_t;
+        rc = run_quire_gemm<T>(a, FetchIm2colFwd<T>{(const T*)x, g, kconv, one_code(a.f)},
+                               FetchWeightFwd<T>{(const T*)w, (const T*)bias, kconv},
+                               out_nchw<T>(y, g.OH * g.OW, F), workspace, workspace_bytes, st,
+                               nullptr);
+    } else {
+        using T = uint16_t;
+        rc = run_quire_gemm<T>(a, FetchIm2colFwd<T>{(const T*)x, g, kconv, one_code(a.f)},
+                               FetchWeightFwd<T>{(const T*)w, (const T*)bias, kconv},
+                               out_nchw<T>(y, g.OH * g.OW, F), workspace, workspace_bytes, st,
+                               nullptr);
+    }
+    return status_of(rc, "conv2d_fwd");
+}
+
+int pnn_conv2d_dgrad(int nbits, int es, const void* dy, int64_t N, int64_t F, int64_t OH,
+                     int64_t OW, const void* w, int64_t C, int64_t KH, int64_t KW, int64_t H,
+                     int64_t W, int stride, int pad, void* dx, void* workspace,
+                     size_t workspace_bytes, void* stream) {
+    if (!conv_fmt_ok(nbits, es)) return set_status(PNN_EUNSUPPORTED, "conv: format not supported");
+    ConvGeom g;
+    if (conv_geom(N, C, H, W, F, KH, KW, stride, pad, &g) || !dy || !w || !dx) return set_status(PNN_EINVAL, "conv: invalid shape or argument");
+    if (g.OH != OH || g.OW != OW) return set_status(PNN_EINVAL, "conv: invalid shape or argument");
+    if (N == 0) return PNN_OK;
+    GemmArgs a;
+    a.f = make_fmt(nbits, es);
+    pass_dims(1, g, false, &a.M, &a.N, &a.K);
+    a.max_kb_per_split = 0;
+    a.row_nar = true;
+    a.col_nar = false;  // weight NaR applied per valid tap below
+    QuireGemmPlan p;
+    if (plan_quire_gemm(a.f, a.M, a.N, a.K, 0, false, &p)) return PNN_EUNSUPPORTED;
+    auto st = static_cast<cudaStream_t>(stream);
+    const uint8_t* flag_w = static_cast<const uint8_t*>(workspace) + p.off_flags + 1;
+    int rc;
+    const uint32_t nar = 1u << (nbits - 1);
+    const int64_t total = N * C * H * W;
+    if (nbits <= 8) {
+        using T = uint8_t;
+        rc = run_quire_gemm<T>(a, FetchDgradDy<T>{(const T*)dy, g}, FetchDgradW<T>{(const T*)w, g},
+                               out_nchw<T>(dx, H * W, C), workspace, workspace_bytes, st, nullptr);
+        if (rc == 0)
+            dgrad_weight_nar_kernel<T><<<grid_for(total, 256), 256, 0, st>>>((T*)dx, (const T*)w, g,
+                                                                             flag_w, nar);
+    } else {
+        using T = uint16_t;
+        rc = run_quire_gemm<T>(a, FetchDgradDy<T>{(const T*)dy, g}, FetchDgradW<T>{(const T*)w, g},
+                               out_nchw<T>(dx, H * W, C), workspace, workspace_bytes, st, nullptr);
+        if (rc == 0)
+            dgrad_weight_nar_kernel<T><<<grid_for(total, 256), 256, 0, st>>>((T*)dx, (const T*)w, g,
+                                                                             flag_w, nar);
+    }
+    if (rc == 0 && cudaGetLastError() != cudaSuccess) rc = 4;
+    return status_of(rc, "conv2d_dgrad");
+}
+
+int pnn_conv2d_wgrad(int nbits, int es, const void* dy, int64_t N, int64_t F, int64_t OH,
+                     int64_t OW, const void* x, int64_t C, int64_t H, int64_t W, int64_t KH,
+                     int64_t KW, int stride, int pad, void* dw, void* raw_words, void* raw_nar,
+                     void* workspace, size_t workspace_bytes, void* stream) {
+    if (!conv_fmt_ok(nbits, es)) return set_status(PNN_EUNSUPPORTED, "conv: format not supported");
+    ConvGeom g;
+    if (conv_geom(N, C, H, W, F, KH, KW, stride, pad, &g) || !dy || !x) return set_status(PNN_EINVAL, "conv: invalid shape or argument");
+    if (g.OH != OH || g.OW != OW) return set_status(PNN_EINVAL, "conv: invalid shape or argument");
+    if (!dw && !raw_words) return set_status(PNN_EINVAL, "conv: invalid shape or argument");
+    if ((raw_words != nullptr) != (raw_nar != nullptr)) return set_status(PNN_EINVAL, "conv: invalid shape or argument");
+    GemmArgs a;
+    a.f = make_fmt(nbits, es);
+    pass_dims(2, g, false, &a.M, &a.N, &a.K);
+    auto st = static_cast<cudaStream_t>(stream);
+    if (a.K == 0) {  // empty batch: all-zero gradient
+        if (dw) cudaMemsetAsync(dw, 0, size_t(a.M * a.N) * (nbits <= 8 ? 1 : 2), st);
+        if (raw_words) {
+            cudaMemsetAsync(raw_words, 0, size_t(a.M * a.N) * 16, st);
+            cudaMemsetAsync(raw_nar, 0, size_t(a.M * a.N), st);
+        }
+        return PNN_OK;
+    }
+    a.max_kb_per_split = 0;
+    a.row_nar = a.col_nar = true;
+    a.raw_words = static_cast<unsigned __int128*>(raw_words);
+    a.raw_nar = static_cast<uint8_t*>(raw_nar);
+    // dw[f][(c,ky,kx)]: output (m=(c,ky,kx), n=f) -> f*M + m  (NCHW map with one "image")
+    int rc;
+    if (nbits <= 8) {
+        using T = uint8_t;
+        rc = run_quire_gemm<T>(a, FetchWgradX<T>{(const T*)x, g}, FetchWgradDy<T>{(const T*)dy, g},
+                               out_nchw<T>(dw, a.M, F), workspace, workspace_bytes, st, nullptr);
+    } else {
+        using T = uint16_t;
+        rc = run_quire_gemm<T>(a, FetchWgradX<T>{(const T*)x, g}, FetchWgradDy<T>{(const T*)dy, g},
+                               out_nchw<T>(dw, a.M, F), workspace, workspace_bytes, st, nullptr);
+    }
+    return status_of(rc, "conv2d_wgrad");
+}
+
+int pnn_bias_grad_workspace(int64_t F, size_t* bytes) {
+    if (F < 0 || !bytes) return set_status(PNN_EINVAL, "conv: invalid shape or argument");
+    *bytes = size_t(F) * 16 * 64 + size_t(F) + 256;
+    return PNN_OK;
+}
+
+int pnn_bias_grad(int nbits, int es, const void* dy, int64_t N, int64_t F, int64_t P, void* db,
+                  void* raw_words, void* raw_nar, void* workspace, size_t workspace_bytes,
+                  void* stream) {
+    if (!conv_fmt_ok(nbits, es)) return set_status(PNN_EUNSUPPORTED, "conv: format not supported");
+    if (N < 0 || F < 1 || P < 1 || !dy || (!db && !raw_words)) return set_status(PNN_EINVAL, "conv: invalid shape or argument");
+    if ((raw_words != nullptr) != (raw_nar != nullptr)) return set_status(PNN_EINVAL, "conv: invalid shape or argument");
+    size_t need;
+    pnn_bias_grad_workspace(F, &need);
+    if (workspace_bytes < need) return PNN_EWORKSPACE;
+    const PositFmt f = make_fmt(nbits, es);
+    int slices = int(N < 64 ? (N < 1 ? 1 : N) : 64);
+    auto* partial = static_cast<unsigned __int128*>(workspace);
+    auto* nar = static_cast<uint8_t*>(workspace) + size_t(F) * 16 * 64;
+    auto st = static_cast<cudaStream_t>(stream);
+    cudaMemsetAsync(nar, 0, size_t(F), st);
+    cudaMemsetAsync(partial, 0, size_t(F) * 16 * slices, st);
+    const dim3 grid{unsigned(F), unsigned(slices), 1u};
+    if (nbits <= 8) {
+        bias_grad_partial_kernel<uint8_t><<<grid, 256, 0, st>>>((const uint8_t*)dy, N, F, P, f,
+                                                                 slices, partial, nar);
+        bias_grad_final_kernel<uint8_t><<<grid_for(F, 128), 128, 0, st>>>(
+            partial, slices, nar, F, f, (uint8_t*)db, (unsigned __int128*)raw_words,
+            (uint8_t*)raw_nar);
+    } else {
+        bias_grad_partial_kernel<uint16_t><<<grid, 256, 0, st>>>((const uint16_t*)dy, N, F, P, f,
+                                                                  slices, partial, nar);
+        bias_grad_final_kernel<uint16_t><<<grid_for(F, 128), 128, 0, st>>>(
+            partial, slices, nar, F, f, (uint16_t*)db, (unsigned __int128*)raw_words,
+            (uint8_t*)raw_nar);
+    }
+    return cudaGetLastError() == cudaSuccess ? PNN_OK : PNN_ECUDA;
+}
+
+}  // extern "C"

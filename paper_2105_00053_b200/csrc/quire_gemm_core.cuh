@@ -1,0 +1,709 @@
+// Exact posit-quire GEMM core on the 5th-gen tensor cores (tcgen05 kind::i8).
+// Templated on operand-fetch functors and an output map, so the matmul, the
+// Conv2d forward / input-grad / weight-grad and the Linear passes all run
+// through the same pack -> tcgen05 -> epilogue pipeline (implicit GEMM with
+// the im2col gather done once per element in the pack stage).
+//
+// Replaces matmul_quire (proj/src/tensor_ops.cpp:166-185, via matmul :461-487):
+//   C[i,j] = round( sum_k A[i,k] * B[k,j] )  with one exact quire per output.
+//
+// Method.  Each operand is decoded to its exact
+// integer image X (posit_device.cuh) and split into D balanced int8 digits,
+// X = sum_d x_d 256^d.  Then
+//     Q[i,j] = sum_k X_A[i,k] X_B[k,j] = sum_g 256^g * S_g[i,j],
+//     S_g    = sum_{p+q=g} A_p . B_q           (int8 x int8 -> int32 GEMMs)
+// and Q mod 2^W is exactly the reference quire (quire.cpp:26-53).  Every S_g
+// is computed exactly by tcgen05.mma.kind::i8 as long as it stays inside
+// int32: |S_g| <= D * 128^2 * K, so K is processed in chunks of at most
+// 131071/D (split-K with raw quire partials) whenever W > 32.
+//
+// Tensor-core mapping.  One CTA owns a 128 x NT output tile.  B's D digit
+// planes for the tile are concatenated along N (N_mma = D*NT <= 256); the MMA
+// for A-plane p writes TMEM columns [p*NT, p*NT + D*NT), so the product
+// A_p . B_q lands in columns (p+q)*NT -- group S_{p+q} -- without any
+// data movement.  TMEM holds (2D-1)*NT int32 columns.
+//
+// Data path.  pack_a / pack_b write the digit planes in HBM already in the
+// canonical no-swizzle K-major UMMA shared-memory image, chunked per
+// (tile, k-block), so the producer warp moves each stage with one
+// cp.async.bulk per operand (TMA engine) into a STAGES-deep mbarrier ring.
+// Warp roles: warp 0 producer, warp 1 MMA issuer (+TMEM owner), warps 2-5
+// epilogue (TMEM -> registers -> 128-bit quire -> posit code).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+
+#include "posit_device.cuh"
+#include "quire_gemm.h"
+#include "sm100_ptx.cuh"
+
+namespace pnn_b200 {
+
+template <int D>
+struct TileCfg;
+template <> struct TileCfg<2> { static constexpr int NT = 128, KB = 128, STAGES = 3; };
+template <> struct TileCfg<3> { static constexpr int NT = 64, KB = 64, STAGES = 5; };
+template <> struct TileCfg<4> { static constexpr int NT = 64, KB = 64, STAGES = 4; };
+template <> struct TileCfg<5> { static constexpr int NT = 32, KB = 32, STAGES = 6; };
+template <> struct TileCfg<6> { static constexpr int NT = 32, KB = 32, STAGES = 6; };
+template <> struct TileCfg<7> { static constexpr int NT = 32, KB = 32, STAGES = 5; };
+template <> struct TileCfg<8> { static constexpr int NT = 32, KB = 32, STAGES = 5; };
+
+constexpr int kBM = 128;          // output rows per CTA (UMMA M)
+constexpr int kEpiWarps = 8;      // epilogue warps (2 per TMEM lane quarter)
+constexpr int kThreads = 64 + 32 * kEpiWarps;  // producer + MMA + epilogue
+constexpr int kZeroBytes = kBM * 32;
+
+template <int D>
+struct Geometry {
+    static constexpr int NT = TileCfg<D>::NT;
+    static constexpr int KB = TileCfg<D>::KB;
+    static constexpr int STAGES = TileCfg<D>::STAGES;
+    static constexpr int G = 2 * D - 1;
+    static constexpr int NMMA = D * NT;
+    static constexpr int A_BYTES = D * kBM * KB;
+    static constexpr int B_BYTES = D * NT * KB;
+    static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+    static constexpr int SMEM = STAGES * STAGE_BYTES + kZeroBytes + 256;
+    static_assert((NT / 2) % 8 == 0, "epilogue column split");
+    static constexpr uint32_t TMEM_COLS = 512;
+    static_assert(G * NT <= 512, "TMEM overflow");
+    static_assert(NMMA % 16 == 0 && NMMA <= 256, "bad UMMA N");
+    static_assert(KB % 32 == 0, "KB must hold whole i8 MMA k-steps");
+};
+
+// ---------------------------------------------------------------- packing
+
+template <int D>
+__device__ __forceinline__ void digit_words(uint32_t code, const PositFmt& f, uint32_t& lo,
+                                            uint32_t& hi, bool& nar) {
+    int64_t X;
+    nar = decode_x(code, f, X);
+    int8_t d[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    int8_t dd[D];
+    balanced_digits<D>(X, dd);
+#pragma unroll
+    for (int i = 0; i < D; ++i) d[i] = dd[i];
+    lo = uint32_t(uint8_t(d[0])) | (uint32_t(uint8_t(d[1])) << 8) | (uint32_t(uint8_t(d[2])) << 16) |
+         (uint32_t(uint8_t(d[3])) << 24);
+    hi = uint32_t(uint8_t(d[4])) | (uint32_t(uint8_t(d[5])) << 8) | (uint32_t(uint8_t(d[6])) << 16) |
+         (uint32_t(uint8_t(d[7])) << 24);
+}
+
+constexpr int kLutMaxBits = 10;  // shared-memory decode LUT up to 1024 codes (8 KB)
+
+// Operand fetch functors: X[r][k] for r < rows, k < K (bounds checked by the
+// caller).  kRowFastest picks the coalesced load order of the pack kernel.
+template <typename CodeT>
+struct FetchRowMajor {  // X[r][k] = p[r*ld + k]
+    const CodeT* p;
+    int64_t ld;
+    static constexpr bool kRowFastest = false;
+    __device__ __forceinline__ uint32_t operator()(int64_t r, int64_t k) const {
+        return uint32_t(p[r * ld + k]);
+    }
+};
+template <typename CodeT>
+struct FetchColMajor {  // X[r][k] = p[k*ld + r]
+    const CodeT* p;
+    int64_t ld;
+    static constexpr bool kRowFastest = true;
+    __device__ __forceinline__ uint32_t operator()(int64_t r, int64_t k) const {
+        return uint32_t(p[k * ld + r]);
+    }
+};
+
+// One CTA packs (tile, k-block) chunks of the logical operand X[r][k] (A: rows
+// are output rows m; B: rows are output columns n) into the canonical K-major
+// no-swizzle UMMA image [D][ROWS/8][KB/16][8][16], and flags X rows that
+// contain a NaR.  Loads go through a shared-memory tile (coalesced for either
+// fetch order), decode is a shared-memory LUT for nbits <= 10.
+template <int D, int ROWS, typename CodeT, class Fetch>
+__global__ void __launch_bounds__(256) pack_kernel(Fetch fetch, int64_t rows_total, int64_t K,
+                                                   PositFmt f,
+                                                   int8_t* __restrict__ img,
+                                                   uint8_t* __restrict__ nar_flags,
+                                                   uint8_t* __restrict__ any_nar_flag, int64_t tiles,
+                                                   int64_t kbt) {
+    constexpr int KB = Geometry<D>::KB;
+    constexpr int KC = KB / 16;
+    // k-blocks per pass, so that every thread owns at least one 16-code unit
+    constexpr int KBS = ROWS * KC >= 256 ? 1 : 256 / (ROWS * KC);
+    constexpr int KW = KB * KBS;             // codes per tile row per pass
+    constexpr int PADC = 4 / sizeof(CodeT);  // row stride = odd multiple of 4 bytes
+    constexpr int LD = KW + PADC;
+    __shared__ __align__(16) CodeT tile[ROWS * LD];
+    __shared__ uint32_t lut[2 << kLutMaxBits];
+    const bool use_lut = f.nbits <= kLutMaxBits;
+    if (use_lut) {
+        for (int c = threadIdx.x; c < (1 << f.nbits); c += blockDim.x) {
+            uint32_t lo, hi;
+            bool nar;
+            digit_words<D>(uint32_t(c), f, lo, hi, nar);
+            lut[2 * c] = lo;
+            lut[2 * c + 1] = hi;
+        }
+    }
+    const uint32_t nar_code = 1u << (f.nbits - 1);
+    const int64_t groups_per_tile = (kbt + KBS - 1) / KBS;
+    const int64_t work = tiles * groups_per_tile;
+    for (int64_t wi = blockIdx.x; wi < work; wi += gridDim.x) {
+        const int64_t t = wi / groups_per_tile;
+        const int64_t kb0 = (wi - t * groups_per_tile) * KBS;
+        const int nkb = int(kbt - kb0 < KBS ? kbt - kb0 : KBS);
+        const int64_t r0 = t * ROWS, k0 = kb0 * KB;
+        __syncthreads();  // previous pass's readers are done with `tile` (and LUT is built)
+        if constexpr (!Fetch::kRowFastest) {
+            for (int i = threadIdx.x; i < ROWS * KW; i += blockDim.x) {
+                const int r = i / KW, k = i % KW;  // k fastest: coalesced along a row of X
+                const int64_t gr = r0 + r, gk = k0 + k;
+                tile[r * LD + k] = (gr < rows_total && gk < K) ? CodeT(fetch(gr, gk)) : CodeT(0);
+            }
+        } else {
+            for (int i = threadIdx.x; i < ROWS * KW; i += blockDim.x) {
+                const int k = i / ROWS, r = i % ROWS;  // r fastest: coalesced along X's column
+                const int64_t gr = r0 + r, gk = k0 + k;
+                tile[r * LD + k] = (gr < rows_total && gk < K) ? CodeT(fetch(gr, gk)) : CodeT(0);
+            }
+        }
+        __syncthreads();
+        for (int u = threadIdx.x; u < ROWS * KC * nkb; u += blockDim.x) {
+            const int r8 = u & 7;
+            const int rest = u >> 3;
+            const int kc = rest % KC;
+            const int rg = (rest / KC) % (ROWS / 8);
+            const int kbl = rest / (KC * (ROWS / 8));
+            const int r = rg * 8 + r8;
+            uint32_t lo[16], hi[16];
+            bool any_nar = false;
+            const CodeT* tr = tile + r * LD + kbl * KB + kc * 16;
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                const uint32_t code = uint32_t(tr[j]);
+                if (use_lut) {
+                    lo[j] = lut[2 * code];
+                    hi[j] = lut[2 * code + 1];
+                    any_nar |= code == nar_code;
+                } else {
+                    bool nar;
+                    digit_words<D>(code, f, lo[j], hi[j], nar);
+                    any_nar |= nar;
+                }
+            }
+            if (any_nar && r0 + r < rows_total) {
+                nar_flags[r0 + r] = 1;
+                *any_nar_flag = 1;
+            }
+            int8_t* chunk = img + (t * kbt + kb0 + kbl) * int64_t(D * ROWS * KB);
+#pragma unroll
+            for (int p = 0; p < D; ++p) {
+                const uint32_t* w = p < 4 ? lo : hi;
+                const uint32_t q = p & 3;
+                const uint32_t sel = q | ((q + 4) << 4);
+                uint4 v;
+                uint32_t* vv = reinterpret_cast<uint32_t*>(&v);
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj) {
+                    const uint32_t a = __byte_perm(w[4 * jj], w[4 * jj + 1], sel);
+                    const uint32_t b = __byte_perm(w[4 * jj + 2], w[4 * jj + 3], sel);
+                    vv[jj] = __byte_perm(a, b, 0x5410);
+                }
+                *reinterpret_cast<uint4*>(chunk + p * (ROWS * KB) + rg * (8 * KB) + kc * 128 +
+                                          r8 * 16) = v;
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------- main kernel
+
+// Where output element (m, n) lives: mode 0 row-major (m*ldc + n); mode 1
+// NCHW scatter for convolutions (m = img*inner + pixel, n = channel).
+template <typename CodeT>
+struct OutMap {
+    CodeT* base;
+    int64_t ldc;
+    int64_t inner;
+    int64_t ncols;
+    int mode;
+    __device__ __forceinline__ int64_t index(int64_t m, int64_t n) const {
+        if (mode == 0) return m * ldc + n;
+        const int64_t img = m / inner, pix = m - img * inner;
+        return (img * ncols + n) * inner + pix;
+    }
+};
+
+template <typename CodeT>
+__device__ __forceinline__ void store_codes8(CodeT* dst, const uint32_t (&c)[8], int valid,
+                                             bool vec_ok) {
+    if (vec_ok && valid == 8) {
+        if constexpr (sizeof(CodeT) == 1) {
+            uint2 v;
+            v.x = (c[0] & 0xFF) | ((c[1] & 0xFF) << 8) | ((c[2] & 0xFF) << 16) | (c[3] << 24);
+            v.y = (c[4] & 0xFF) | ((c[5] & 0xFF) << 8) | ((c[6] & 0xFF) << 16) | (c[7] << 24);
+            *reinterpret_cast<uint2*>(dst) = v;
+        } else {
+            uint4 v;
+            v.x = (c[0] & 0xFFFF) | (c[1] << 16);
+            v.y = (c[2] & 0xFFFF) | (c[3] << 16);
+            v.z = (c[4] & 0xFFFF) | (c[5] << 16);
+            v.w = (c[6] & 0xFFFF) | (c[7] << 16);
+            *reinterpret_cast<uint4*>(dst) = v;
+        }
+    } else {
+        for (int j = 0; j < valid; ++j) dst[j] = CodeT(c[j]);
+    }
+}
+
+template <int QW>
+struct QuireWord;
+template <> struct QuireWord<1> { using T = uint32_t; };
+template <> struct QuireWord<2> { using T = uint64_t; };
+template <> struct QuireWord<4> { using T = unsigned __int128; };
+
+// Sign-extend an int32 group sum and weight it by 256^g, modulo the word size
+// (the quire itself is only defined mod 2^W <= word bits).
+template <typename T>
+__device__ __forceinline__ T group_term(uint32_t acc, int sh) {
+    if constexpr (sizeof(T) == 4) return T(acc) << sh;
+    else if constexpr (sizeof(T) == 8) return T(int64_t(int32_t(acc))) << sh;
+    else return T(__int128(int32_t(acc))) << sh;
+}
+
+// Raster: tiles grouped by kGroupM m-tiles so the ~148 tiles in flight share
+// A and B digit planes in L2.
+constexpr int kGroupM = 8;
+
+__device__ __forceinline__ void tile_coords(int64_t t, int64_t mtiles, int64_t ntiles,
+                                            int64_t& split, int64_t& mt, int64_t& nt) {
+    const int64_t per_split = mtiles * ntiles;
+    split = t / per_split;
+    const int64_t r = t - split * per_split;
+    const int64_t group = r / (kGroupM * ntiles);
+    const int64_t within = r - group * (kGroupM * ntiles);
+    const int64_t gm = min(int64_t(kGroupM), mtiles - group * kGroupM);
+    mt = group * kGroupM + within % gm;
+    nt = within / gm;
+}
+
+// Persistent, warp-specialized: warp 0 = bulk-copy producer, warp 1 = MMA
+// issuer, warps 2..9 = epilogue (2 warps per TMEM lane quarter, each owning
+// half of the tile's columns).  The epilogue drains TMEM into registers,
+// releases it (tmem_empty), and rounds/stores while the next tile's MMAs run.
+template <int D, int QW, typename CodeT>
+__global__ void __launch_bounds__(kThreads, 1)
+    quire_gemm_tc_kernel(const int8_t* __restrict__ a_img, const int8_t* __restrict__ b_img,
+                         int64_t kbt, int64_t kb_per_split, const uint8_t* __restrict__ row_nar,
+                         const uint8_t* __restrict__ col_nar, OutMap<CodeT> out, int64_t M,
+                         int64_t N, PositFmt f,
+                         unsigned __int128* __restrict__ partial, int64_t mtiles, int64_t ntiles,
+                         int64_t splits) {
+    using Geo = Geometry<D>;
+    using QT = typename QuireWord<QW>::T;
+    constexpr int NT = Geo::NT, KB = Geo::KB, STAGES = Geo::STAGES, G = Geo::G;
+    constexpr int COLS = NT / 2;                 // columns per epilogue thread
+    constexpr int GB = G < 8 ? G : 8;            // TMEM loads batched per wait
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint8_t* zero_tile = smem + STAGES * Geo::STAGE_BYTES;
+    uint64_t* full = reinterpret_cast<uint64_t*>(zero_tile + kZeroBytes);
+    uint64_t* empty = full + STAGES;
+    uint64_t* tmem_full = empty + STAGES;
+    uint64_t* tmem_empty = tmem_full + 1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 1);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int64_t tiles = mtiles * ntiles * splits;
+
+    for (int i = threadIdx.x; i < kZeroBytes / 16; i += kThreads)
+        reinterpret_cast<int4*>(zero_tile)[i] = make_int4(0, 0, 0, 0);
+    if (warp == 0 && lane == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            ptx::mbar_init(&full[s], 1);
+            ptx::mbar_init(&empty[s], 1);
+        }
+        ptx::mbar_init(tmem_full, 1);
+        ptx::mbar_init(tmem_empty, kEpiWarps);
+        ptx::fence_barrier_init();
+    }
+    if (warp == 1) ptx::tmem_alloc<Geo::TMEM_COLS>(tmem_slot);
+    ptx::fence_proxy_async_smem();
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ===== producer: one bulk copy per operand per stage =====
+            uint32_t it = 0;
+            for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+                int64_t split, mt, nt;
+                tile_coords(t, mtiles, ntiles, split, mt, nt);
+                const int64_t kb0 = split * kb_per_split;
+                const int nkb = int(min(kbt, kb0 + kb_per_split) - kb0);
+                const int8_t* a_src = a_img + (mt * kbt + kb0) * int64_t(Geo::A_BYTES);
+                const int8_t* b_src = b_img + (nt * kbt + kb0) * int64_t(Geo::B_BYTES);
+                for (int i = 0; i < nkb; ++i, ++it) {
+                    const int s = it % STAGES;
+                    const uint32_t ph = (it / STAGES) & 1;
+                    ptx::mbar_wait(&empty[s], ph ^ 1);
+                    uint8_t* sa = smem + s * Geo::STAGE_BYTES;
+                    ptx::mbar_arrive_expect_tx(&full[s], Geo::STAGE_BYTES);
+                    ptx::bulk_g2s(sa, a_src + int64_t(i) * Geo::A_BYTES, Geo::A_BYTES, &full[s]);
+                    ptx::bulk_g2s(sa + Geo::A_BYTES, b_src + int64_t(i) * Geo::B_BYTES,
+                                  Geo::B_BYTES, &full[s]);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            // ===== MMA issuer =====
+            constexpr uint32_t idesc = ptx::idesc_i8(kBM, Geo::NMMA);
+            constexpr uint32_t SBO = 8 * KB, LBO = 128;
+            const uint64_t zdesc = ptx::smem_desc_kmajor(ptx::smem_u32(zero_tile), LBO, 8 * 32);
+            uint32_t it = 0, j = 0;
+            for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++j) {
+                int64_t split, mt, nt;
+                tile_coords(t, mtiles, ntiles, split, mt, nt);
+                const int64_t kb0 = split * kb_per_split;
+                const int nkb = int(min(kbt, kb0 + kb_per_split) - kb0);
+                ptx::mbar_wait(tmem_empty, (j & 1) ^ 1);  // epilogue drained the previous tile
+                ptx::tc_fence_after();
+                for (int i = 0; i < nkb; ++i, ++it) {
+                    const int s = it % STAGES;
+                    const uint32_t ph = (it / STAGES) & 1;
+                    ptx::mbar_wait(&full[s], ph);
+                    ptx::tc_fence_after();
+                    const uint32_t a_base = ptx::smem_u32(smem + s * Geo::STAGE_BYTES);
+                    const uint32_t b_base = a_base + Geo::A_BYTES;
+#pragma unroll
+                    for (int ks = 0; ks < KB / 32; ++ks) {
+                        const uint64_t bdesc = ptx::smem_desc_kmajor(b_base + ks * 256, LBO, SBO);
+                        const bool first = (i == 0 && ks == 0);
+                        if (first)  // zero groups D-1 .. 2D-2 (plane 0 initialises 0 .. D-1)
+                            ptx::mma_i8(tmem + (D - 1) * NT, zdesc, bdesc, idesc, 0);
+#pragma unroll
+                        for (int p = 0; p < D; ++p) {
+                            const uint64_t adesc = ptx::smem_desc_kmajor(
+                                a_base + p * (kBM * KB) + ks * 256, LBO, SBO);
+                            ptx::mma_i8(tmem + p * NT, adesc, bdesc, idesc,
+                                        (first && p == 0) ? 0u : 1u);
+                        }
+                    }
+                    ptx::mma_commit(&empty[s]);
+                }
+                ptx::mma_commit(tmem_full);
+            }
+        }
+    } else {
+        // ===== epilogue: TMEM -> quire words (registers) -> posit codes =====
+        const int quarter = warp & 3;
+        const int half = (warp - 2) >> 2;
+        const uint32_t trow = tmem + (uint32_t(quarter * 32) << 16) + half * COLS;
+        const bool vec_ok = out.mode == 0 && (out.ldc % 8) == 0;
+        uint32_t j = 0;
+        for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++j) {
+            int64_t split, mt, nt;
+            tile_coords(t, mtiles, ntiles, split, mt, nt);
+            ptx::mbar_wait(tmem_full, j & 1);
+            ptx::tc_fence_after();
+            QT q[COLS];
+#pragma unroll
+            for (int c = 0; c < COLS; ++c) q[c] = 0;
+#pragma unroll
+            for (int c0 = 0; c0 < COLS; c0 += 8) {
+#pragma unroll
+                for (int g0 = 0; g0 < G; g0 += GB) {
+                    uint32_t r[GB][8];
+#pragma unroll
+                    for (int g = 0; g < GB; ++g)
+                        if (g0 + g < G) ptx::tmem_ld8(trow + (g0 + g) * NT + c0, r[g]);
+                    ptx::tmem_wait_ld();
+#pragma unroll
+                    for (int g = 0; g < GB; ++g)
+                        if (g0 + g < G)
+#pragma unroll
+                            for (int x = 0; x < 8; ++x) q[c0 + x] += group_term<QT>(r[g][x], 8 * (g0 + g));
+                }
+            }
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(tmem_empty);
+
+            const int64_t row = mt * kBM + quarter * 32 + lane;
+            if (row >= M) continue;
+            const bool rnar = row_nar != nullptr && row_nar[row] != 0;
+            const int64_t colbase = nt * NT + half * COLS;
+#pragma unroll
+            for (int c0 = 0; c0 < COLS; c0 += 8) {
+                const int64_t col0 = colbase + c0;
+                if (col0 >= N) break;
+                const int valid = int(N - col0 < 8 ? N - col0 : 8);
+                if (partial != nullptr) {
+                    unsigned __int128* dst = partial + (split * M + row) * N + col0;
+#pragma unroll
+                    for (int x = 0; x < 8; ++x)
+                        if (x < valid) dst[x] = (unsigned __int128)q[c0 + x];
+                    continue;
+                }
+                uint32_t codes[8];
+#pragma unroll
+                for (int x = 0; x < 8; ++x) {
+                    const bool nar = rnar || (col_nar != nullptr && x < valid && col_nar[col0 + x]);
+                    codes[x] = nar ? (1u << (f.nbits - 1)) : quire_word_to_posit(f, q[c0 + x]);
+                }
+                if (vec_ok) {
+                    store_codes8(out.base + row * out.ldc + col0, codes, valid, true);
+                } else {
+#pragma unroll
+                    for (int x = 0; x < 8; ++x)
+                        if (x < valid) out.base[out.index(row, col0 + x)] = CodeT(codes[x]);
+                }
+            }
+        }
+    }
+    __syncwarp();
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc<Geo::TMEM_COLS>(tmem);
+    }
+}
+
+// Sum split-K quire partials (mod 2^W), apply NaR, round once -- or, in raw
+// mode, emit the exact W-bit quire words and NaR mask (data-parallel
+// gradient reduction input).
+template <typename CodeT>
+__global__ void quire_finalize_kernel(const unsigned __int128* __restrict__ partial, int splits,
+                                      const uint8_t* __restrict__ row_nar,
+                                      const uint8_t* __restrict__ col_nar, OutMap<CodeT> out,
+                                      int64_t M, int64_t N, PositFmt f,
+                                      unsigned __int128* __restrict__ raw_words,
+                                      uint8_t* __restrict__ raw_nar) {
+    const int64_t total = M * N;
+    const unsigned __int128 one = 1;
+    const unsigned __int128 wmask = f.W >= 128 ? ~(unsigned __int128)0 : ((one << f.W) - 1);
+    for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total;
+         idx += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t i = idx / N, j = idx % N;
+        const bool nar = (row_nar != nullptr && row_nar[i]) || (col_nar != nullptr && col_nar[j]);
+        unsigned __int128 q = 0;
+        for (int s = 0; s < splits; ++s) q += partial[s * total + idx];
+        if (raw_words != nullptr) {  // raw words/NaR mask land in the output's layout
+            const int64_t o = out.index(i, j);
+            raw_words[o] = q & wmask;
+            raw_nar[o] = nar ? 1 : 0;
+        } else {
+            out.base[out.index(i, j)] = CodeT(nar ? (1u << (f.nbits - 1)) : quire_word_to_posit(f, q));
+        }
+    }
+}
+
+// ------------------------------------------------------------------ host
+
+inline int digits_for(const PositFmt& f) {
+    // smallest D with balanced capacity 127*(256^D-1)/255 >= 2^(2R)
+    for (int D = 1; D <= 8; ++D) {
+        const long double cap = 127.0L * (powl(256.0L, D) - 1.0L) / 255.0L;
+        if (cap >= powl(2.0L, 2 * f.R)) return D < 2 ? 2 : D;
+    }
+    return -1;
+}
+
+
+inline int num_sms() {
+    static int n = 0;
+    if (n == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
+inline int grid_for(int64_t items, int threads) {
+    int64_t b = (items + threads - 1) / threads;
+    if (b > 148 * 64) b = 148 * 64;
+    if (b < 1) b = 1;
+    return int(b);
+}
+
+// Arguments of one logical quire GEMM  C[m][n] = round(sum_k A[m][k] B[k][n]).
+struct GemmArgs {
+    PositFmt f;
+    int64_t M, N, K;
+    int64_t max_kb_per_split;  // 0: automatic (int32 exactness + SM fill)
+    bool row_nar, col_nar;     // apply operand NaR flags in the epilogue
+    unsigned __int128* raw_words = nullptr;  // raw mode: exact W-bit quire words out
+    uint8_t* raw_nar = nullptr;              //           and the NaR mask
+};
+
+template <int D>
+inline QuireGemmPlan plan_for(const PositFmt& f, int64_t M, int64_t N, int64_t K,
+                              int64_t max_kb_per_split, bool raw) {
+    using Geo = Geometry<D>;
+    QuireGemmPlan p{};
+    p.D = D;
+    p.NT = Geo::NT;
+    p.KB = Geo::KB;
+    p.mtiles = (M + kBM - 1) / kBM;
+    p.ntiles = (N + Geo::NT - 1) / Geo::NT;
+    p.kbt = (K + Geo::KB - 1) / Geo::KB;
+    // int32 group sums stay exact for K <= 131071 / D (|digit| <= 128); a
+    // quire of W <= 32 bits is itself mod 2^32, so wrapping is exact there.
+    int64_t kbps = f.W <= 32 ? p.kbt : (131071 / D) / Geo::KB;
+    if (max_kb_per_split > 0) {
+        kbps = kbps < max_kb_per_split ? kbps : max_kb_per_split;
+    } else {
+        const int64_t tiles = p.mtiles * p.ntiles;
+        const int sms = num_sms();
+        if (tiles < sms && p.kbt >= 8) {  // few output tiles, long K: split for SM fill
+            int64_t want = (sms + tiles - 1) / tiles;
+            if (want > p.kbt / 4) want = p.kbt / 4;
+            if (want > 1) {
+                const int64_t per = (p.kbt + want - 1) / want;
+                kbps = kbps < per ? kbps : per;
+            }
+        }
+    }
+    if (kbps < 1) kbps = 1;
+    p.kb_per_split = p.kbt < kbps ? p.kbt : kbps;
+    p.splits = (p.kbt + p.kb_per_split - 1) / p.kb_per_split;
+    p.a_img_bytes = size_t(p.mtiles) * p.kbt * Geo::A_BYTES;
+    p.b_img_bytes = size_t(p.ntiles) * p.kbt * Geo::B_BYTES;
+    p.row_nar_bytes = size_t(p.mtiles) * kBM;
+    p.col_nar_bytes = size_t(p.ntiles) * Geo::NT;
+    p.partial_bytes = (p.splits > 1 || raw) ? size_t(p.splits) * M * N * 16 : 0;
+    p.smem_bytes = Geo::SMEM;
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        size_t o = off;
+        off += (bytes + 255) & ~size_t(255);
+        return o;
+    };
+    p.off_a = take(p.a_img_bytes);
+    p.off_b = take(p.b_img_bytes);
+    p.off_row_nar = take(p.row_nar_bytes);
+    p.off_col_nar = take(p.col_nar_bytes);
+    p.off_flags = take(16);
+    p.off_partial = take(p.partial_bytes);
+    p.workspace_bytes = off;
+    return p;
+}
+
+inline int plan_quire_gemm(const PositFmt& f, int64_t M, int64_t N, int64_t K,
+                           int64_t max_kb_per_split, bool raw, QuireGemmPlan* plan) {
+    if (f.nbits < 2 || f.nbits > 16 || f.es < 0 || 2 * f.R > 56) return 2;
+    switch (digits_for(f)) {
+        case 2: *plan = plan_for<2>(f, M, N, K, max_kb_per_split, raw); break;
+        case 3: *plan = plan_for<3>(f, M, N, K, max_kb_per_split, raw); break;
+        case 4: *plan = plan_for<4>(f, M, N, K, max_kb_per_split, raw); break;
+        case 5: *plan = plan_for<5>(f, M, N, K, max_kb_per_split, raw); break;
+        case 6: *plan = plan_for<6>(f, M, N, K, max_kb_per_split, raw); break;
+        case 7: *plan = plan_for<7>(f, M, N, K, max_kb_per_split, raw); break;
+        case 8: *plan = plan_for<8>(f, M, N, K, max_kb_per_split, raw); break;
+        default: return 2;
+    }
+    return 0;
+}
+
+template <int D, typename CodeT, class FA, class FB>
+cudaError_t launch_generic(const QuireGemmPlan& p, const GemmArgs& g, FA fa, FB fb,
+                           OutMap<CodeT> out, uint8_t* ws, cudaStream_t st,
+                           QuireGemmStats* stats) {
+    using Geo = Geometry<D>;
+    const PositFmt& f = g.f;
+    int8_t* a_img = reinterpret_cast<int8_t*>(ws + p.off_a);
+    int8_t* b_img = reinterpret_cast<int8_t*>(ws + p.off_b);
+    uint8_t* rnar = ws + p.off_row_nar;
+    uint8_t* cnar = ws + p.off_col_nar;
+    uint8_t* flags = ws + p.off_flags;  // [0] any NaR in A, [1] any NaR in B
+    const bool use_partial = p.splits > 1 || g.raw_words != nullptr;
+    auto* partial = use_partial ? reinterpret_cast<unsigned __int128*>(ws + p.off_partial) : nullptr;
+    cudaError_t e;
+    if ((e = cudaMemsetAsync(rnar, 0, p.off_flags + 16 - p.off_row_nar, st)) != cudaSuccess) return e;
+    if (stats) cudaEventRecord(stats->ev[0], st);
+    const int64_t a_work = p.mtiles * p.kbt, b_work = p.ntiles * p.kbt;  // upper bounds
+    pack_kernel<D, kBM, CodeT, FA><<<int(a_work < 148 * 8 ? a_work : 148 * 8), 256, 0, st>>>(
+        fa, g.M, g.K, f, a_img, rnar, flags, p.mtiles, p.kbt);
+    pack_kernel<D, Geo::NT, CodeT, FB><<<int(b_work < 148 * 8 ? b_work : 148 * 8), 256, 0, st>>>(
+        fb, g.N, g.K, f, b_img, cnar, flags + 1, p.ntiles, p.kbt);
+    if (stats) cudaEventRecord(stats->ev[1], st);
+    // D <= 3 implies R <= 11, hence W <= 64: no 128-bit instantiation needed.
+    void (*kern)(const int8_t*, const int8_t*, int64_t, int64_t, const uint8_t*, const uint8_t*,
+                 OutMap<CodeT>, int64_t, int64_t, PositFmt, unsigned __int128*, int64_t, int64_t,
+                 int64_t);
+    if constexpr (D <= 3)
+        kern = f.W <= 32 ? quire_gemm_tc_kernel<D, 1, CodeT> : quire_gemm_tc_kernel<D, 2, CodeT>;
+    else
+        kern = f.W <= 64 ? quire_gemm_tc_kernel<D, 2, CodeT> : quire_gemm_tc_kernel<D, 4, CodeT>;
+    if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Geo::SMEM)) !=
+        cudaSuccess)
+        return e;
+    const int64_t tiles = p.mtiles * p.ntiles * p.splits;
+    const int grid = int(tiles < num_sms() ? tiles : num_sms());
+    kern<<<grid, kThreads, Geo::SMEM, st>>>(a_img, b_img, p.kbt, p.kb_per_split,
+                                            g.row_nar ? rnar : nullptr, g.col_nar ? cnar : nullptr,
+                                            out, g.M, g.N, f, partial, p.mtiles, p.ntiles, p.splits);
+    if (stats) cudaEventRecord(stats->ev[2], st);
+    if (use_partial) {
+        quire_finalize_kernel<CodeT><<<grid_for(g.M * g.N, 256), 256, 0, st>>>(
+            partial, int(p.splits), g.row_nar ? rnar : nullptr, g.col_nar ? cnar : nullptr, out,
+            g.M, g.N, f, g.raw_words, g.raw_nar);
+    }
+    if (stats) cudaEventRecord(stats->ev[3], st);
+    return cudaGetLastError();
+}
+
+// 0 ok, 2 unsupported format, 3 workspace too small, 4 CUDA error.
+template <typename CodeT, class FA, class FB>
+int run_quire_gemm(const GemmArgs& g, FA fa, FB fb, OutMap<CodeT> out, void* workspace,
+                   size_t workspace_bytes, cudaStream_t st, QuireGemmStats* stats) {
+    QuireGemmPlan p;
+    if (plan_quire_gemm(g.f, g.M, g.N, g.K, g.max_kb_per_split, g.raw_words != nullptr, &p))
+        return 2;
+    if (workspace_bytes < p.workspace_bytes) return 3;
+    auto* ws = static_cast<uint8_t*>(workspace);
+    cudaError_t e = cudaSuccess;
+    switch (p.D) {
+        case 2: e = launch_generic<2, CodeT>(p, g, fa, fb, out, ws, st, stats); break;
+        case 3: e = launch_generic<3, CodeT>(p, g, fa, fb, out, ws, st, stats); break;
+        case 4: e = launch_generic<4, CodeT>(p, g, fa, fb, out, ws, st, stats); break;
+        case 5: e = launch_generic<5, CodeT>(p, g, fa, fb, out, ws, st, stats); break;
+        case 6: e = launch_generic<6, CodeT>(p, g, fa, fb, out, ws, st, stats); break;
+        case 7: e = launch_generic<7, CodeT>(p, g, fa, fb, out, ws, st, stats); break;
+        case 8: e = launch_generic<8, CodeT>(p, g, fa, fb, out, ws, st, stats); break;
+        default: return 2;
+    }
+    return e == cudaSuccess ? 0 : 4;
+}
+
+template <typename CodeT>
+inline OutMap<CodeT> out_rowmajor(void* base, int64_t ldc) {
+    OutMap<CodeT> o;
+    o.base = static_cast<CodeT*>(base);
+    o.ldc = ldc;
+    o.inner = 1;
+    o.ncols = 0;
+    o.mode = 0;
+    return o;
+}
+
+template <typename CodeT>
+inline OutMap<CodeT> out_nchw(void* base, int64_t pixels, int64_t channels) {
+    OutMap<CodeT> o;
+    o.base = static_cast<CodeT*>(base);
+    o.ldc = 0;
+    o.inner = pixels;
+    o.ncols = channels;
+    o.mode = 1;
+    return o;
+}
+
+}  // namespace pnn_b200

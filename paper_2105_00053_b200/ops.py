@@ -191,3 +191,118 @@ def pack_round(cfg, neg, scale, sig, sticky):
                                                sticky.contiguous().data_ptr(), n, out.data_ptr(),
                                                _stream_ptr(neg.device)))
     return out
+
+
+# ---- Conv2d / Linear passes (tensor_ops.hpp:34-42, 61) ----------------------
+
+def _conv_ws(pass_, cfg, N, Cc, H, W, F, KH, KW, stride, pad, has_bias):
+    n = C.c_size_t()
+    _native.check(_native.lib().pnn_conv2d_workspace(pass_, cfg.nbits, cfg.es, N, Cc, H, W, F, KH, KW,
+                                                      stride, pad, int(has_bias), C.byref(n)))
+    return n.value
+
+
+def _check_codes(cfg, *ts):
+    for t in ts:
+        if t is not None and t.dtype != cfg.code_dtype:
+            raise _native.PnnInvalidArgument(1, "dtype mismatch")
+
+
+def conv2d(cfg, x, w, bias, stride: int, pad: int, use_quire: bool = True, pool=None):
+    """tensor_ops.hpp:34-35: y = round(conv(x_pad, w) + bias), bias inside the quire."""
+    if not use_quire:
+        raise NotImplementedError("non-quire conv is outside this path (SURVEY.md §8f)")
+    cfg = _cfg(cfg)
+    if x.dim() != 4 or w.dim() != 4:
+        raise _native.PnnInvalidArgument(1, "conv2d: NCHW/FCKK tensors required")
+    if x.shape[1] != w.shape[1]:
+        raise _native.PnnInvalidArgument(1, "conv2d: channel mismatch")
+    _check_codes(cfg, x, w, bias)
+    x, w = x.contiguous(), w.contiguous()
+    bias = bias.contiguous() if bias is not None else None
+    N, Cc, H, W = x.shape
+    F, _, KH, KW = w.shape
+    OH, OW = (H + 2 * pad - KH) // stride + 1, (W + 2 * pad - KW) // stride + 1
+    y = torch.empty((N, F, OH, OW), dtype=cfg.code_dtype, device=x.device)
+    ws = _ws.get(x.device, _conv_ws(0, cfg, N, Cc, H, W, F, KH, KW, stride, pad, bias is not None))
+    _native.check(_native.lib().pnn_conv2d_fwd(
+        cfg.nbits, cfg.es, x.data_ptr(), N, Cc, H, W, w.data_ptr(), F, KH, KW,
+        bias.data_ptr() if bias is not None else None, stride, pad, y.data_ptr(), ws.data_ptr(),
+        ws.numel(), _stream_ptr(x.device)))
+    return y
+
+
+def conv2d_input_grad(cfg, dy, w, x_shape, stride: int, pad: int, use_quire: bool = True, pool=None):
+    """tensor_ops.hpp:36-38."""
+    cfg = _cfg(cfg)
+    _check_codes(cfg, dy, w)
+    dy, w = dy.contiguous(), w.contiguous()
+    N, Cc, H, W = (int(v) for v in x_shape)
+    _, F, OH, OW = dy.shape
+    _, _, KH, KW = w.shape
+    dx = torch.empty((N, Cc, H, W), dtype=cfg.code_dtype, device=dy.device)
+    ws = _ws.get(dy.device, _conv_ws(1, cfg, N, Cc, H, W, F, KH, KW, stride, pad, False))
+    _native.check(_native.lib().pnn_conv2d_dgrad(
+        cfg.nbits, cfg.es, dy.data_ptr(), N, F, OH, OW, w.data_ptr(), Cc, KH, KW, H, W, stride, pad,
+        dx.data_ptr(), ws.data_ptr(), ws.numel(), _stream_ptr(dy.device)))
+    return dx
+
+
+def conv2d_weight_grad(cfg, dy, x, w_shape, stride: int, pad: int, use_quire: bool = True, pool=None,
+                       raw: bool = False):
+    """tensor_ops.hpp:39-41.  raw=True also returns the exact unrounded quire
+    words (int64 [..., 2]: lo, hi) and NaR mask -- the data-parallel reduction input."""
+    cfg = _cfg(cfg)
+    _check_codes(cfg, dy, x)
+    dy, x = dy.contiguous(), x.contiguous()
+    N, F, OH, OW = dy.shape
+    _, Cc, H, W = x.shape
+    KH, KW = int(w_shape[2]), int(w_shape[3])
+    dw = torch.empty((F, Cc, KH, KW), dtype=cfg.code_dtype, device=dy.device)
+    words = nar = None
+    if raw:
+        words = torch.empty((F, Cc, KH, KW, 2), dtype=torch.int64, device=dy.device)
+        nar = torch.empty((F, Cc, KH, KW), dtype=torch.uint8, device=dy.device)
+    ws = _ws.get(dy.device, _conv_ws(2, cfg, N, Cc, H, W, F, KH, KW, stride, pad, False))
+    _native.check(_native.lib().pnn_conv2d_wgrad(
+        cfg.nbits, cfg.es, dy.data_ptr(), N, F, OH, OW, x.data_ptr(), Cc, H, W, KH, KW, stride, pad,
+        dw.data_ptr(), words.data_ptr() if raw else None, nar.data_ptr() if raw else None,
+        ws.data_ptr(), ws.numel(), _stream_ptr(dy.device)))
+    return (dw, words, nar) if raw else dw
+
+
+def _bias_grad(cfg, dy3, raw=False):
+    N, F, P = dy3.shape
+    db = torch.empty((F,), dtype=cfg.code_dtype, device=dy3.device)
+    words = nar = None
+    if raw:
+        words = torch.empty((F, 2), dtype=torch.int64, device=dy3.device)
+        nar = torch.empty((F,), dtype=torch.uint8, device=dy3.device)
+    n = C.c_size_t()
+    _native.check(_native.lib().pnn_bias_grad_workspace(F, C.byref(n)))
+    ws = _ws.get(dy3.device, n.value)
+    _native.check(_native.lib().pnn_bias_grad(cfg.nbits, cfg.es, dy3.data_ptr(), N, F, P, db.data_ptr(),
+                                              words.data_ptr() if raw else None,
+                                              nar.data_ptr() if raw else None, ws.data_ptr(), ws.numel(),
+                                              _stream_ptr(dy3.device)))
+    return (db, words, nar) if raw else db
+
+
+def conv2d_bias_grad(cfg, dy, use_quire: bool = True, raw: bool = False):
+    """tensor_ops.hpp:42: db[f] = round(quire sum over (n, oy, ox) of dy)."""
+    cfg = _cfg(cfg)
+    _check_codes(cfg, dy)
+    if dy.dim() != 4:
+        raise _native.PnnInvalidArgument(1, "conv2d_bias_grad: bad rank")
+    N, F, OH, OW = dy.shape
+    return _bias_grad(cfg, dy.contiguous().view(N, F, OH * OW), raw)
+
+
+def column_sum(cfg, x, use_quire: bool = True, raw: bool = False):
+    """tensor_ops.hpp:61: [B,N] -> [N] quire column sums."""
+    cfg = _cfg(cfg)
+    _check_codes(cfg, x)
+    if x.dim() != 2:
+        raise _native.PnnInvalidArgument(1, "column_sum: rank-2 tensor required")
+    B, N = x.shape
+    return _bias_grad(cfg, x.contiguous().view(B, N, 1), raw)
