@@ -498,9 +498,9 @@ __global__ void quire_finalize_kernel(const unsigned __int128* __restrict__ part
             const int64_t o = out.index(i, j);
             raw_words[o] = q & wmask;
             raw_nar[o] = nar ? 1 : 0;
-        } else {
-            out.base[out.index(i, j)] = CodeT(nar ? (1u << (f.nbits - 1)) : quire_word_to_posit(f, q));
         }
+        if (out.base != nullptr)
+            out.base[out.index(i, j)] = CodeT(nar ? (1u << (f.nbits - 1)) : quire_word_to_posit(f, q));
     }
 }
 
