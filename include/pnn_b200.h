@@ -96,6 +96,39 @@ int pnn_bias_grad(int nbits, int es, const void* dy, int64_t N, int64_t F, int64
                   void* raw_words, void* raw_nar, void* workspace, size_t workspace_bytes,
                   void* stream);
 
+/* ---- elementwise kernels of the training step -----------------------------
+ * Semantics: convert = convert_tensor (tensor_ops.cpp:807-821); maxpool =
+ * maxpool2d / maxpool2d_backward (:620-670, argmax = flat input index, int64);
+ * ReLU, softmax cross-entropy and SGD have no reference code (placeholders,
+ * SURVEY.md §0.3) and follow SURVEY.md Appendix A.2 / A.5 / A.7 exactly as the
+ * CPU oracle step (oracle/step.py) does. */
+int pnn_convert(int src_nbits, int src_es, int dst_nbits, int dst_es, const void* src, void* dst,
+                int64_t n, void* stream);
+int pnn_relu_fwd(int nbits, int es, const void* x, void* y, int64_t n, void* stream);
+/* dx = x > 0 ? dy : 0 with x in (x_nbits, x_es) and dy/dx in (g_nbits, g_es). */
+int pnn_relu_bwd(int x_nbits, int x_es, const void* x, int g_nbits, int g_es, const void* dy,
+                 void* dx, int64_t n, void* stream);
+int pnn_maxpool2d_fwd(int nbits, int es, const void* x, int64_t N, int64_t C, int64_t H,
+                      int64_t W, int k, int stride, void* y, int64_t* argmax, void* stream);
+int pnn_maxpool2d_bwd(int nbits, int es, const void* dy, const int64_t* argmax, int64_t N,
+                      int64_t C, int64_t H, int64_t W, int k, int stride, void* dx, void* stream);
+/* logits [B, classes] in the loss format; labels int32 [B]; outputs dlogits
+ * [B, classes] (already scaled by 2^-log2_batch), per-row losses [B], the
+ * batch loss (1 code, may be NULL) and/or the raw quire word (16 bytes) + NaR
+ * byte of sum(loss_i) for the data-parallel reduction (may be NULL). */
+int pnn_softmax_xent(int nbits, int es, const void* logits, const int32_t* labels, int64_t B,
+                     int64_t classes, int log2_batch, void* dlogits, void* loss_rows,
+                     void* loss_out, void* raw_word, void* raw_nar, void* stream);
+/* master = sub(master, mul(lr, convert(grad -> opt))) in the optimizer
+ * format; copy1/copy2 (may be NULL) receive convert(master -> their format). */
+int pnn_sgd_step(int opt_nbits, int opt_es, void* master, int g_nbits, int g_es, const void* grad,
+                 int64_t n, uint32_t lr_code, int c1_nbits, int c1_es, void* copy1, int c2_nbits,
+                 int c2_es, void* copy2, void* stream);
+/* Scalar ALU on device (parity): op 0 add 1 sub 2 mul 3 div 4 exp 5 log
+ * 6 round_to_int 7 ldexp(a, (int)b) 8 compare 9 to_int64 (low 32 bits). */
+int pnn_scalar_eval(int nbits, int es, int op, const uint32_t* a, const uint32_t* b,
+                    uint32_t* out, int64_t n, void* stream);
+
 /* ---- device posit core (parity / diagnostics) ----------------------------
  * pnn_decode_x: code -> exact integer image X = value * 2^max_scale and NaR
  *   flag (detail::unpack posit.cpp:67-91 / DecodeTables::Fixed).

@@ -253,6 +253,41 @@ class Restatement(_Base):
                                                  _p(dx)), "maxpool2d_backward")
         return dx.reshape(x_shape)
 
+    def ew(self, n, es, op, a, b):
+        a, b = _codes(a), _codes(b)
+        out = np.zeros(a.shape, np.uint64)
+        self.lib.po_ew(n, es, op, _p(a), _p(b), _p(out), i64(a.size))
+        return out
+
+    def relu_fwd(self, n, es, x):
+        x = _codes(x)
+        y = np.zeros(x.shape, np.uint64)
+        self.lib.po_relu_fwd(n, es, _p(x), _p(y), i64(x.size))
+        return y
+
+    def relu_bwd(self, xn, xes, x, dy):
+        x, dy = _codes(x), _codes(dy)
+        dx = np.zeros(dy.shape, np.uint64)
+        self.lib.po_relu_bwd(xn, xes, _p(x), _p(dy), _p(dx), i64(x.size))
+        return dx
+
+    def softmax_xent(self, n, es, logits, labels, log2_batch):
+        z = _codes(logits)
+        B, Cn = z.shape
+        lab = np.ascontiguousarray(np.asarray(labels, np.int32))
+        d = np.zeros(z.shape, np.uint64)
+        rows = np.zeros((B,), np.uint64)
+        self.lib.po_softmax_xent.restype = C.c_uint64
+        loss = self.lib.po_softmax_xent(n, es, _p(z), lab.ctypes.data_as(C.POINTER(C.c_int32)), i64(B),
+                                        i64(Cn), int(log2_batch), _p(d), _p(rows))
+        return int(loss), d, rows
+
+    def sgd(self, on, oes, w, gn, ges, g, lr):
+        w = _codes(w).copy()
+        g = _codes(g)
+        self.lib.po_sgd(on, oes, _p(w), gn, ges, _p(g), i64(w.size), C.c_uint64(int(lr)))
+        return w
+
     def convert_tensor(self, sn, se, dn, de, x):
         x = _codes(x)
         y = np.zeros(x.shape, np.uint64)

@@ -729,3 +729,60 @@ int po_convert_tensor(int sn, int se, int dn, int de, const uint64_t* x, int64_t
         y[i] = (sn == dn && se == de) ? x[i] : po_convert(sn, se, dn, de, x[i]);
     return 0;
 }
+
+/* ------------------------------------------------ training-step semantics */
+
+void po_ew(int nbits, int es, int op, const uint64_t* a, const uint64_t* b, uint64_t* out,
+           int64_t n) {
+    for (int64_t i = 0; i < n; ++i) out[i] = po_scalar_op(nbits, es, op, a[i], b[i]);
+}
+
+void po_relu_fwd(int nbits, int es, const uint64_t* x, uint64_t* y, int64_t n) {
+    for (int64_t i = 0; i < n; ++i) y[i] = po_compare(nbits, es, x[i], 0) > 0 ? x[i] : 0;
+}
+
+void po_relu_bwd(int x_nbits, int x_es, const uint64_t* x, const uint64_t* dy, uint64_t* dx,
+                 int64_t n) {
+    for (int64_t i = 0; i < n; ++i) dx[i] = po_compare(x_nbits, x_es, x[i], 0) > 0 ? dy[i] : 0;
+}
+
+/* m = max z (signed-pattern compare); e_j =
+ * exp(sub(z_j, m)); S = quire sum of e_j rounded once; p_j = div(e_j, S);
+ * loss_i = sub(log(S), sub(z_y, m)); batch loss = quire sum of loss_i rounded
+ * once then ldexp by -log2(B); dlogits = ldexp(sub(p_j, [j==y]), -log2(B)). */
+uint64_t po_softmax_xent(int nbits, int es, const uint64_t* logits, const int32_t* labels,
+                         int64_t B, int64_t C, int log2_batch, uint64_t* dlogits,
+                         uint64_t* loss_rows) {
+    const uint64_t one = po_from_int64(nbits, es, 1);
+    po_quire* tot = po_quire_new(nbits, es);
+    po_quire* q = po_quire_new(nbits, es);
+    for (int64_t i = 0; i < B; ++i) {
+        const uint64_t* z = logits + i * C;
+        uint64_t m = z[0];
+        for (int64_t j = 1; j < C; ++j)
+            if (po_compare(nbits, es, z[j], m) > 0) m = z[j];
+        po_quire_clear(q);
+        for (int64_t j = 0; j < C; ++j) po_quire_add_posit(q, po_exp(nbits, es, OP_SUB(z[j], m)));
+        const uint64_t S = po_quire_to_posit(q);
+        const int32_t y = labels[i];
+        for (int64_t j = 0; j < C; ++j) {
+            const uint64_t p = OP_DIV(po_exp(nbits, es, OP_SUB(z[j], m)), S);
+            dlogits[i * C + j] = po_ldexp(nbits, es, OP_SUB(p, j == y ? one : 0), -log2_batch);
+        }
+        loss_rows[i] = OP_SUB(po_log(nbits, es, S), OP_SUB(z[y], m));
+        po_quire_add_posit(tot, loss_rows[i]);
+    }
+    const uint64_t loss = po_ldexp(nbits, es, po_quire_to_posit(tot), -log2_batch);
+    po_quire_free(q);
+    po_quire_free(tot);
+    return loss;
+}
+
+void po_sgd(int opt_nbits, int opt_es, uint64_t* w, int g_nbits, int g_es, const uint64_t* g,
+            int64_t n, uint64_t lr) {
+    for (int64_t i = 0; i < n; ++i) {
+        const uint64_t gg = po_convert(g_nbits, g_es, opt_nbits, opt_es, g[i]);
+        w[i] = po_scalar_op(opt_nbits, opt_es, 1, w[i],
+                            po_scalar_op(opt_nbits, opt_es, 2, lr, gg));
+    }
+}

@@ -93,6 +93,25 @@ int po_maxpool2d_backward(int nbits, int es, const uint64_t* dy, int64_t ny,
 int po_convert_tensor(int sn, int se, int dn, int de, const uint64_t* x, int64_t n,
                       uint64_t* y);
 
+/* ---- training-step semantics the reference leaves open (placeholders in
+ * layers.cpp / losses.cpp / optimizer.cpp), pinned per SURVEY.md Appendix A
+ * and restated here as the single CPU definition the GPU step must match. */
+/* Vector scalar op over n elements (op 0 add 1 sub 2 mul 3 div). */
+void po_ew(int nbits, int es, int op, const uint64_t* a, const uint64_t* b, uint64_t* out,
+           int64_t n);
+/* A.2 ReLU: x > 0 ? x : 0 by signed-pattern compare (NaR sorts lowest -> 0). */
+void po_relu_fwd(int nbits, int es, const uint64_t* x, uint64_t* y, int64_t n);
+/* dx = x > 0 ? dy : 0 (x in the forward format, dy in the backward format). */
+void po_relu_bwd(int x_nbits, int x_es, const uint64_t* x, const uint64_t* dy, uint64_t* dx,
+                 int64_t n);
+/* A.5 softmax cross-entropy in the loss format; returns the batch loss code. */
+uint64_t po_softmax_xent(int nbits, int es, const uint64_t* logits, const int32_t* labels,
+                         int64_t B, int64_t C, int log2_batch, uint64_t* dlogits,
+                         uint64_t* loss_rows);
+/* A.7 SGD: w = sub(w, mul(lr, convert(g -> opt))) in the optimizer format. */
+void po_sgd(int opt_nbits, int opt_es, uint64_t* w, int g_nbits, int g_es, const uint64_t* g,
+            int64_t n, uint64_t lr);
+
 #ifdef __cplusplus
 }
 #endif

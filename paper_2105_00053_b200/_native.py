@@ -46,6 +46,16 @@ _SIGS = {
     "pnn_bias_grad_workspace": (C.c_int, [_i64, C.POINTER(C.c_size_t)]),
     "pnn_bias_grad": (C.c_int, [C.c_int, C.c_int, _vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp, C.c_size_t,
                                 _vp]),
+    "pnn_convert": (C.c_int, [C.c_int] * 4 + [_vp, _vp, _i64, _vp]),
+    "pnn_relu_fwd": (C.c_int, [C.c_int, C.c_int, _vp, _vp, _i64, _vp]),
+    "pnn_relu_bwd": (C.c_int, [C.c_int, C.c_int, _vp, C.c_int, C.c_int, _vp, _vp, _i64, _vp]),
+    "pnn_maxpool2d_fwd": (C.c_int, [C.c_int, C.c_int, _vp] + [_i64] * 4 + [C.c_int, C.c_int, _vp, _vp, _vp]),
+    "pnn_maxpool2d_bwd": (C.c_int, [C.c_int, C.c_int, _vp, _vp] + [_i64] * 4 + [C.c_int, C.c_int, _vp, _vp]),
+    "pnn_softmax_xent": (C.c_int, [C.c_int, C.c_int, _vp, _vp, _i64, _i64, C.c_int, _vp, _vp, _vp, _vp, _vp,
+                                   _vp]),
+    "pnn_sgd_step": (C.c_int, [C.c_int, C.c_int, _vp, C.c_int, C.c_int, _vp, _i64, C.c_uint32, C.c_int,
+                               C.c_int, _vp, C.c_int, C.c_int, _vp, _vp]),
+    "pnn_scalar_eval": (C.c_int, [C.c_int, C.c_int, C.c_int, _vp, _vp, _vp, _i64, _vp]),
     "pnn_probe_int8_peak": (C.c_int, [C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
 }
 

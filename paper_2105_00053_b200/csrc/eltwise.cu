@@ -1,0 +1,349 @@
+// Elementwise / small kernels of the training step (HBM-roofline kernels):
+// stage conversion, ReLU, max-pool, softmax cross-entropy, SGD update.
+//
+//   convert_tensor       proj/src/tensor_ops.cpp:807-821
+//   maxpool2d (+bwd)     tensor_ops.cpp:620-656, 658-670 (first strict max; the
+//                        backward accumulates with scalar add in output order)
+//   ReLU / CE / SGD      no reference code (layers are placeholders, SURVEY.md
+//                        §0.3); semantics pinned in SURVEY.md Appendix A.2/A.5/A.7
+//                        and mirrored by the CPU oracle step (oracle/step.py)
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "../../include/pnn_b200.h"
+#include "posit_scalar.cuh"
+#include "status.h"
+
+namespace pnn_b200 {
+
+template <typename T>
+__device__ __forceinline__ uint32_t ld_code(const void* p, int64_t i) {
+    return uint32_t(static_cast<const T*>(p)[i]);
+}
+
+__device__ __forceinline__ uint32_t load_any(const void* p, int64_t i, int bytes) {
+    return bytes == 1 ? uint32_t(static_cast<const uint8_t*>(p)[i])
+                      : uint32_t(static_cast<const uint16_t*>(p)[i]);
+}
+__device__ __forceinline__ void store_any(void* p, int64_t i, int bytes, uint32_t c) {
+    if (bytes == 1) static_cast<uint8_t*>(p)[i] = uint8_t(c);
+    else static_cast<uint16_t*>(p)[i] = uint16_t(c);
+}
+
+#define GRID_STRIDE(i, n)                                                        \
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < (n); \
+         i += int64_t(gridDim.x) * blockDim.x)
+
+__global__ void convert_kernel(PositFmt s, int sb, const void* src, PositFmt d, int db, void* dst,
+                               int64_t n) {
+    GRID_STRIDE(i, n) { store_any(dst, i, db, p_convert(s, d, load_any(src, i, sb))); }
+}
+
+// ReLU: x > 0 ? x : 0 by signed-pattern compare (NaR sorts lowest -> 0).
+__global__ void relu_fwd_kernel(PositFmt f, int b, const void* x, void* y, int64_t n) {
+    GRID_STRIDE(i, n) {
+        const uint32_t c = load_any(x, i, b);
+        store_any(y, i, b, p_compare(f, c, 0) > 0 ? c : 0u);
+    }
+}
+
+// dx = x > 0 ? dy : 0 (x in the forward format, dy/dx in the backward format).
+__global__ void relu_bwd_kernel(PositFmt fx, int bx, const void* x, int bg, const void* dy,
+                                void* dx, int64_t n) {
+    GRID_STRIDE(i, n) {
+        const uint32_t c = load_any(x, i, bx);
+        store_any(dx, i, bg, p_compare(fx, c, 0) > 0 ? load_any(dy, i, bg) : 0u);
+    }
+}
+
+__global__ void maxpool_fwd_kernel(PositFmt f, int b, const void* x, int64_t NC, int64_t H,
+                                   int64_t W, int k, int s, int64_t OH, int64_t OW, void* y,
+                                   int64_t* argmax) {
+    GRID_STRIDE(o, NC * OH * OW) {
+        const int64_t ox = o % OW, oy = (o / OW) % OH, nc = o / (OW * OH);
+        const int64_t base = nc * H * W;
+        int64_t best = base + (oy * s) * W + ox * s;
+        uint32_t bv = load_any(x, best, b);
+        for (int ky = 0; ky < k; ++ky)
+            for (int kx = 0; kx < k; ++kx) {
+                const int64_t idx = base + (oy * s + ky) * W + ox * s + kx;
+                const uint32_t v = load_any(x, idx, b);
+                if (p_compare(f, v, bv) > 0) {
+                    best = idx;
+                    bv = v;
+                }
+            }
+        store_any(y, o, b, bv);
+        argmax[o] = best;
+    }
+}
+
+// dx[t] = add(...add(add(0, dy[i1]), dy[i2])...) over outputs i with
+// argmax[i] == t in increasing i -- the reference's sequential order.
+__global__ void maxpool_bwd_kernel(PositFmt f, int b, const void* dy, const int64_t* argmax,
+                                   int64_t NC, int64_t H, int64_t W, int k, int s, int64_t OH,
+                                   int64_t OW, void* dx) {
+    GRID_STRIDE(t, NC * H * W) {
+        const int64_t ix = t % W, iy = (t / W) % H, nc = t / (W * H);
+        const int64_t oy0 = iy - k + 1 > 0 ? (iy - k + 1 + s - 1) / s : 0;
+        const int64_t ox0 = ix - k + 1 > 0 ? (ix - k + 1 + s - 1) / s : 0;
+        const int64_t oy1 = min(OH - 1, iy / s), ox1 = min(OW - 1, ix / s);
+        uint32_t acc = 0;
+        for (int64_t oy = oy0; oy <= oy1; ++oy)
+            for (int64_t ox = ox0; ox <= ox1; ++ox) {
+                const int64_t o = (nc * OH + oy) * OW + ox;
+                if (argmax[o] == t) acc = p_add(f, acc, load_any(dy, o, b));
+            }
+        store_any(dx, t, b, acc);
+    }
+}
+
+// Softmax cross-entropy in the loss format, one row
+// per thread:  m = max z;  e_j = exp(z_j - m);  S = round(quire sum e_j);
+// p_j = e_j / S;  loss_i = log(S) - (z_y - m);
+// dlogits_j = ldexp(p_j - [j==y], -log2_batch).
+__global__ void softmax_xent_kernel(PositFmt f, int b, const void* logits, const int32_t* labels,
+                                    int64_t B, int64_t Cn, int log2_batch, void* dlogits,
+                                    void* loss_rows) {
+    GRID_STRIDE(i, B) {
+        const int64_t row = i * Cn;
+        uint32_t m = load_any(logits, row, b);
+        for (int64_t j = 1; j < Cn; ++j) {
+            const uint32_t v = load_any(logits, row + j, b);
+            if (p_compare(f, v, m) > 0) m = v;
+        }
+        // S = quire sum of e_j: exact in the integer image, one rounding
+        __int128 sx = 0;
+        bool nar = false;
+        for (int64_t j = 0; j < Cn; ++j) {
+            const uint32_t e = p_exp(f, p_sub(f, load_any(logits, row + j, b), m));
+            int64_t X;
+            nar |= decode_x(e, f, X);
+            sx += X;
+        }
+        uint32_t S;
+        if (nar) {
+            S = nar_of(f);
+        } else {
+            const bool neg = sx < 0;
+            S = round_mag128(f, neg, (unsigned __int128)(neg ? -sx : sx), -f.R);
+        }
+        const int32_t y = labels[i];
+        const uint32_t one = p_from_int64(f, 1);
+        for (int64_t j = 0; j < Cn; ++j) {
+            const uint32_t e = p_exp(f, p_sub(f, load_any(logits, row + j, b), m));
+            const uint32_t pj = p_div(f, e, S);
+            const uint32_t g = p_sub(f, pj, j == y ? one : 0u);
+            store_any(dlogits, row + j, b, p_ldexp(f, g, -log2_batch));
+        }
+        const uint32_t zy = load_any(logits, row + y, b);
+        store_any(loss_rows, i, b, p_sub(f, p_log(f, S), p_sub(f, zy, m)));
+    }
+}
+
+// Batch loss: quire sum of loss_i (optionally returned as a raw W-bit word
+// for the data-parallel reduction), rounded once, then ldexp by -log2_batch.
+__global__ void loss_reduce_kernel(PositFmt f, int b, const void* loss_rows, int64_t B,
+                                   int log2_batch, void* loss_out, unsigned __int128* raw_word,
+                                   uint8_t* raw_nar) {
+    __shared__ unsigned long long lo_s[256], hi_s[256];
+    __shared__ int nar_s;
+    if (threadIdx.x == 0) nar_s = 0;
+    __syncthreads();
+    __int128 acc = 0;
+    for (int64_t i = threadIdx.x; i < B; i += blockDim.x) {
+        int64_t X;
+        if (decode_x(load_any(loss_rows, i, b), f, X)) nar_s = 1;
+        acc += X;
+    }
+    lo_s[threadIdx.x] = (unsigned long long)uint64_t(acc);
+    hi_s[threadIdx.x] = (unsigned long long)uint64_t((unsigned __int128)acc >> 64);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned __int128 s = 0;
+        for (int t = 0; t < blockDim.x; ++t)
+            s += (unsigned __int128)lo_s[t] | ((unsigned __int128)hi_s[t] << 64);
+        const unsigned __int128 one = 1;
+        const unsigned __int128 wmask = f.W >= 128 ? ~(unsigned __int128)0 : ((one << f.W) - 1);
+        const unsigned __int128 q = (s << f.R) & wmask;
+        if (raw_word) {
+            *raw_word = q;
+            *raw_nar = nar_s ? 1 : 0;
+        }
+        if (loss_out) {
+            const uint32_t c = nar_s ? nar_of(f) : quire_to_posit(f, q);
+            store_any(loss_out, 0, b, p_ldexp(f, c, -log2_batch));
+        }
+    }
+}
+
+// SGD: w = sub(w, mul(lr, convert(g -> p_opt))) in
+// the optimizer format, then refresh the stage copies (convert, SPEC §3.3).
+__global__ void sgd_kernel(PositFmt fo, int bo, void* master, PositFmt fg, int bg, const void* grad,
+                           int64_t n, uint32_t lr, PositFmt f1, int b1, void* copy1, PositFmt f2,
+                           int b2, void* copy2) {
+    GRID_STRIDE(i, n) {
+        const uint32_t g = p_convert(fg, fo, load_any(grad, i, bg));
+        const uint32_t w = p_sub(fo, load_any(master, i, bo), p_mul(fo, lr, g));
+        store_any(master, i, bo, w);
+        if (copy1) store_any(copy1, i, b1, p_convert(fo, f1, w));
+        if (copy2) store_any(copy2, i, b2, p_convert(fo, f2, w));
+    }
+}
+
+__global__ void scalar_eval_kernel(PositFmt f, int op, const uint32_t* a, const uint32_t* b,
+                                   uint32_t* out, int64_t n) {
+    GRID_STRIDE(i, n) {
+        const uint32_t x = a[i], y = b ? b[i] : 0u;
+        uint32_t r;
+        switch (op) {
+            case 0: case 1: case 2: case 3: r = p_op(f, op, x, y); break;
+            case 4: r = p_exp(f, x); break;
+            case 5: r = p_log(f, x); break;
+            case 6: r = p_round_to_int(f, x); break;
+            case 7: r = p_ldexp(f, x, int32_t(y)); break;
+            case 8: r = uint32_t(p_compare(f, x, y)); break;
+            default: r = uint32_t(p_to_int64(f, x)); break;
+        }
+        out[i] = r;
+    }
+}
+
+}  // namespace pnn_b200
+
+// =========================================================================
+// C-ABI
+// =========================================================================
+
+using namespace pnn_b200;
+
+namespace {
+
+bool elt_fmt_ok(int nbits, int es) {
+    if (nbits < 2 || nbits > 16 || es < 0 || es > 4) return false;
+    return 2 * make_fmt(nbits, es).R <= 56;
+}
+
+int bytes_of(int nbits) { return nbits <= 8 ? 1 : 2; }
+
+int grid1(int64_t n) {
+    int64_t b = (n + 255) / 256;
+    if (b > 148 * 16) b = 148 * 16;
+    return int(b < 1 ? 1 : b);
+}
+
+int launched(const char* what) {
+    const cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) return PNN_OK;
+    return set_status(PNN_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define CHECK_FMT(n, e)                                                               \
+    if (!elt_fmt_ok(n, e)) return set_status(PNN_EUNSUPPORTED, "format not supported")
+
+}  // namespace
+
+extern "C" {
+
+int pnn_convert(int src_nbits, int src_es, int dst_nbits, int dst_es, const void* src, void* dst,
+                int64_t n, void* stream) {
+    CHECK_FMT(src_nbits, src_es);
+    CHECK_FMT(dst_nbits, dst_es);
+    if (n < 0 || (n > 0 && (!src || !dst))) return set_status(PNN_EINVAL, "convert: bad arguments");
+    if (n == 0) return PNN_OK;
+    convert_kernel<<<grid1(n), 256, 0, (cudaStream_t)stream>>>(
+        make_fmt(src_nbits, src_es), bytes_of(src_nbits), src, make_fmt(dst_nbits, dst_es),
+        bytes_of(dst_nbits), dst, n);
+    return launched("convert");
+}
+
+int pnn_relu_fwd(int nbits, int es, const void* x, void* y, int64_t n, void* stream) {
+    CHECK_FMT(nbits, es);
+    if (n < 0) return set_status(PNN_EINVAL, "relu: bad size");
+    if (n == 0) return PNN_OK;
+    relu_fwd_kernel<<<grid1(n), 256, 0, (cudaStream_t)stream>>>(make_fmt(nbits, es),
+                                                                bytes_of(nbits), x, y, n);
+    return launched("relu_fwd");
+}
+
+int pnn_relu_bwd(int x_nbits, int x_es, const void* x, int g_nbits, int g_es, const void* dy,
+                 void* dx, int64_t n, void* stream) {
+    CHECK_FMT(x_nbits, x_es);
+    CHECK_FMT(g_nbits, g_es);
+    if (n < 0) return set_status(PNN_EINVAL, "relu: bad size");
+    if (n == 0) return PNN_OK;
+    relu_bwd_kernel<<<grid1(n), 256, 0, (cudaStream_t)stream>>>(
+        make_fmt(x_nbits, x_es), bytes_of(x_nbits), x, bytes_of(g_nbits), dy, dx, n);
+    return launched("relu_bwd");
+}
+
+int pnn_maxpool2d_fwd(int nbits, int es, const void* x, int64_t N, int64_t C, int64_t H,
+                      int64_t W, int k, int stride, void* y, int64_t* argmax, void* stream) {
+    CHECK_FMT(nbits, es);
+    if (N < 0 || C < 1 || k < 1 || stride < 1 || H < k || W < k)
+        return set_status(PNN_EINVAL, "maxpool2d: window larger than input");
+    const int64_t OH = (H - k) / stride + 1, OW = (W - k) / stride + 1;
+    if (N == 0) return PNN_OK;
+    maxpool_fwd_kernel<<<grid1(N * C * OH * OW), 256, 0, (cudaStream_t)stream>>>(
+        make_fmt(nbits, es), bytes_of(nbits), x, N * C, H, W, k, stride, OH, OW, y, argmax);
+    return launched("maxpool2d_fwd");
+}
+
+int pnn_maxpool2d_bwd(int nbits, int es, const void* dy, const int64_t* argmax, int64_t N,
+                      int64_t C, int64_t H, int64_t W, int k, int stride, void* dx, void* stream) {
+    CHECK_FMT(nbits, es);
+    if (N < 0 || C < 1 || k < 1 || stride < 1 || H < k || W < k)
+        return set_status(PNN_EINVAL, "maxpool2d_backward: bad shape");
+    const int64_t OH = (H - k) / stride + 1, OW = (W - k) / stride + 1;
+    if (N == 0) return PNN_OK;
+    maxpool_bwd_kernel<<<grid1(N * C * H * W), 256, 0, (cudaStream_t)stream>>>(
+        make_fmt(nbits, es), bytes_of(nbits), dy, argmax, N * C, H, W, k, stride, OH, OW, dx);
+    return launched("maxpool2d_bwd");
+}
+
+int pnn_softmax_xent(int nbits, int es, const void* logits, const int32_t* labels, int64_t B,
+                     int64_t classes, int log2_batch, void* dlogits, void* loss_rows,
+                     void* loss_out, void* raw_word, void* raw_nar, void* stream) {
+    CHECK_FMT(nbits, es);
+    if (B < 1 || classes < 1 || !logits || !labels || !dlogits || !loss_rows)
+        return set_status(PNN_EINVAL, "softmax_xent: bad arguments");
+    const PositFmt f = make_fmt(nbits, es);
+    auto st = (cudaStream_t)stream;
+    softmax_xent_kernel<<<grid1(B), 256, 0, st>>>(f, bytes_of(nbits), logits, labels, B, classes,
+                                                  log2_batch, dlogits, loss_rows);
+    if (loss_out || raw_word)
+        loss_reduce_kernel<<<1, 256, 0, st>>>(f, bytes_of(nbits), loss_rows, B, log2_batch,
+                                              loss_out, (unsigned __int128*)raw_word,
+                                              (uint8_t*)raw_nar);
+    return launched("softmax_xent");
+}
+
+int pnn_sgd_step(int opt_nbits, int opt_es, void* master, int g_nbits, int g_es, const void* grad,
+                 int64_t n, uint32_t lr_code, int c1_nbits, int c1_es, void* copy1, int c2_nbits,
+                 int c2_es, void* copy2, void* stream) {
+    CHECK_FMT(opt_nbits, opt_es);
+    CHECK_FMT(g_nbits, g_es);
+    if (copy1) CHECK_FMT(c1_nbits, c1_es);
+    if (copy2) CHECK_FMT(c2_nbits, c2_es);
+    if (n < 0 || (n > 0 && (!master || !grad))) return set_status(PNN_EINVAL, "sgd: bad arguments");
+    if (n == 0) return PNN_OK;
+    const PositFmt f1 = copy1 ? make_fmt(c1_nbits, c1_es) : make_fmt(opt_nbits, opt_es);
+    const PositFmt f2 = copy2 ? make_fmt(c2_nbits, c2_es) : make_fmt(opt_nbits, opt_es);
+    sgd_kernel<<<grid1(n), 256, 0, (cudaStream_t)stream>>>(
+        make_fmt(opt_nbits, opt_es), bytes_of(opt_nbits), master, make_fmt(g_nbits, g_es),
+        bytes_of(g_nbits), grad, n, lr_code, f1, bytes_of(f1.nbits), copy1, f2,
+        bytes_of(f2.nbits), copy2);
+    return launched("sgd_step");
+}
+
+int pnn_scalar_eval(int nbits, int es, int op, const uint32_t* a, const uint32_t* b,
+                    uint32_t* out, int64_t n, void* stream) {
+    CHECK_FMT(nbits, es);
+    if (n <= 0) return PNN_OK;
+    scalar_eval_kernel<<<grid1(n), 256, 0, (cudaStream_t)stream>>>(make_fmt(nbits, es), op, a, b,
+                                                                   out, n);
+    return launched("scalar_eval");
+}
+
+}  // extern "C"

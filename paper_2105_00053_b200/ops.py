@@ -306,3 +306,106 @@ def column_sum(cfg, x, use_quire: bool = True, raw: bool = False):
         raise _native.PnnInvalidArgument(1, "column_sum: rank-2 tensor required")
     B, N = x.shape
     return _bias_grad(cfg, x.contiguous().view(B, N, 1), raw)
+
+
+# ---- elementwise kernels of the training step -------------------------------
+
+def convert_tensor(t, src_cfg, dst_cfg):
+    """tensor_ops.hpp:26 convert_tensor (same dtype returns the input, :808)."""
+    s, d = _cfg(src_cfg), _cfg(dst_cfg)
+    if s == d:
+        return t
+    t = t.contiguous()
+    out = torch.empty(t.shape, dtype=d.code_dtype, device=t.device)
+    _native.check(_native.lib().pnn_convert(s.nbits, s.es, d.nbits, d.es, t.data_ptr(), out.data_ptr(),
+                                            t.numel(), _stream_ptr(t.device)))
+    return out
+
+
+def relu_fwd(cfg, x):
+    cfg = _cfg(cfg)
+    x = x.contiguous()
+    y = torch.empty_like(x)
+    _native.check(_native.lib().pnn_relu_fwd(cfg.nbits, cfg.es, x.data_ptr(), y.data_ptr(), x.numel(),
+                                             _stream_ptr(x.device)))
+    return y
+
+
+def relu_bwd(x_cfg, x, g_cfg, dy):
+    xc, gc = _cfg(x_cfg), _cfg(g_cfg)
+    x, dy = x.contiguous(), dy.contiguous()
+    if x.numel() != dy.numel():
+        raise _native.PnnInvalidArgument(1, "relu_bwd: shape mismatch")
+    dx = torch.empty_like(dy)
+    _native.check(_native.lib().pnn_relu_bwd(xc.nbits, xc.es, x.data_ptr(), gc.nbits, gc.es, dy.data_ptr(),
+                                             dx.data_ptr(), x.numel(), _stream_ptr(x.device)))
+    return dx
+
+
+def maxpool2d(cfg, x, k: int, stride: int, pool=None):
+    """tensor_ops.hpp:44-49: (out, argmax as flat input indices)."""
+    cfg = _cfg(cfg)
+    x = x.contiguous()
+    N, Cc, H, W = x.shape
+    if H < k or W < k:
+        raise _native.PnnInvalidArgument(1, "maxpool2d: window larger than input")
+    OH, OW = (H - k) // stride + 1, (W - k) // stride + 1
+    y = torch.empty((N, Cc, OH, OW), dtype=x.dtype, device=x.device)
+    am = torch.empty((N, Cc, OH, OW), dtype=torch.int64, device=x.device)
+    _native.check(_native.lib().pnn_maxpool2d_fwd(cfg.nbits, cfg.es, x.data_ptr(), N, Cc, H, W, k, stride,
+                                                  y.data_ptr(), am.data_ptr(), _stream_ptr(x.device)))
+    return y, am
+
+
+def maxpool2d_backward(cfg, dy, argmax, x_shape, k: int = 2, stride: int = 2):
+    """tensor_ops.hpp:50-51 (window geometry passed explicitly)."""
+    cfg = _cfg(cfg)
+    N, Cc, H, W = (int(v) for v in x_shape)
+    dx = torch.empty((N, Cc, H, W), dtype=cfg.code_dtype, device=dy.device)
+    _native.check(_native.lib().pnn_maxpool2d_bwd(cfg.nbits, cfg.es, dy.contiguous().data_ptr(),
+                                                  argmax.contiguous().data_ptr(), N, Cc, H, W, k, stride,
+                                                  dx.data_ptr(), _stream_ptr(dy.device)))
+    return dx
+
+
+def softmax_xent(cfg, logits, labels, log2_batch: int, raw: bool = False):
+    """SURVEY.md Appendix A.5 -> (loss code tensor [1], dlogits, loss_rows[, raw word, raw nar])."""
+    cfg = _cfg(cfg)
+    logits = logits.contiguous()
+    B, Cn = logits.shape
+    labels = labels.to(torch.int32).contiguous()
+    d = torch.empty_like(logits)
+    rows = torch.empty((B,), dtype=logits.dtype, device=logits.device)
+    loss = torch.empty((1,), dtype=logits.dtype, device=logits.device)
+    word = torch.empty((2,), dtype=torch.int64, device=logits.device) if raw else None
+    nar = torch.empty((1,), dtype=torch.uint8, device=logits.device) if raw else None
+    _native.check(_native.lib().pnn_softmax_xent(cfg.nbits, cfg.es, logits.data_ptr(), labels.data_ptr(), B, Cn,
+                                                 int(log2_batch), d.data_ptr(), rows.data_ptr(),
+                                                 loss.data_ptr(), word.data_ptr() if raw else None,
+                                                 nar.data_ptr() if raw else None, _stream_ptr(logits.device)))
+    return (loss, d, rows, word, nar) if raw else (loss, d, rows)
+
+
+def sgd_step(opt_cfg, master, g_cfg, grad, lr_code: int, copies=()):
+    """SURVEY.md Appendix A.7, in place on master; copies = [(cfg, tensor), ...] (<= 2)."""
+    oc, gc = _cfg(opt_cfg), _cfg(g_cfg)
+    cps = [(_cfg(c), t) for c, t in copies] + [(oc, None)] * (2 - len(copies))
+    (c1, t1), (c2, t2) = cps[0], cps[1]
+    _native.check(_native.lib().pnn_sgd_step(oc.nbits, oc.es, master.data_ptr(), gc.nbits, gc.es,
+                                             grad.contiguous().data_ptr(), master.numel(), int(lr_code),
+                                             c1.nbits, c1.es, t1.data_ptr() if t1 is not None else None,
+                                             c2.nbits, c2.es, t2.data_ptr() if t2 is not None else None,
+                                             _stream_ptr(master.device)))
+    return master
+
+
+def scalar_eval(cfg, op: int, a, b=None):
+    """Device scalar ALU (parity): a, b CUDA int32 code tensors."""
+    cfg = _cfg(cfg)
+    a = a.to(torch.int32).contiguous()
+    b = b.to(torch.int32).contiguous() if b is not None else None
+    out = torch.empty_like(a)
+    _native.check(_native.lib().pnn_scalar_eval(cfg.nbits, cfg.es, op, a.data_ptr(),
+                                                b.data_ptr() if b is not None else None, out.data_ptr(),
+                                                a.numel(), _stream_ptr(a.device)))
+    return out
