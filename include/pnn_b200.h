@@ -124,6 +124,9 @@ int pnn_softmax_xent(int nbits, int es, const void* logits, const int32_t* label
 int pnn_sgd_step(int opt_nbits, int opt_es, void* master, int g_nbits, int g_es, const void* grad,
                  int64_t n, uint32_t lr_code, int c1_nbits, int c1_es, void* copy1, int c2_nbits,
                  int c2_es, void* copy2, void* stream);
+/* Data ingestion: from_float64 (posit.cpp:502-508) of device doubles into
+ * packed codes -- inputs, labels-free data and initial weights. */
+int pnn_from_float64(int nbits, int es, const double* x, void* codes, int64_t n, void* stream);
 /* Scalar ALU on device (parity): op 0 add 1 sub 2 mul 3 div 4 exp 5 log
  * 6 round_to_int 7 ldexp(a, (int)b) 8 compare 9 to_int64 (low 32 bits). */
 int pnn_scalar_eval(int nbits, int es, int op, const uint32_t* a, const uint32_t* b,

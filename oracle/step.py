@@ -1,0 +1,126 @@
+"""CPU oracle of one training step (TEST INFRASTRUCTURE ONLY).
+
+The reference has no layer / loss / optimizer code (layers.cpp, losses.cpp,
+optimizer.cpp, model.cpp are placeholders), so a training
+step's semantics are pinned once, here, from SURVEY.md Appendix A and
+composed purely from the oracle's restatement of the reference's tensor
+kernels (oracle/posit_oracle.c -- conv2d / conv2d_input_grad /
+conv2d_weight_grad / conv2d_bias_grad / maxpool2d(+backward) /
+convert_tensor, tensor_ops.cpp) plus the Appendix-A scalar pieces (ReLU,
+softmax cross-entropy, SGD) restated in the same C file.
+
+A layer description is a list of tuples:
+    ("conv", cin, cout, k, stride, pad, first_layer)   ("linear", fin, fout, first_layer)
+    ("relu",)   ("pool", k, stride)   ("flatten",)
+Params are host uint64 code arrays in the optimizer format, one (w, b) pair
+per conv / linear, in order.
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+LENET5 = [("conv", 1, 6, 5, 1, 0, True), ("relu",), ("pool", 2, 2),
+          ("conv", 6, 16, 5, 1, 0, False), ("relu",), ("pool", 2, 2), ("flatten",),
+          ("linear", 400, 120, False), ("relu",), ("linear", 120, 84, False), ("relu",),
+          ("linear", 84, 10, False)]
+
+CIFAR_CNN = [("conv", 3, 32, 3, 1, 1, True), ("relu",), ("conv", 32, 32, 3, 1, 1, False), ("relu",),
+             ("pool", 2, 2), ("conv", 32, 64, 3, 1, 1, False), ("relu",),
+             ("conv", 64, 64, 3, 1, 1, False), ("relu",), ("pool", 2, 2), ("flatten",),
+             ("linear", 4096, 512, False), ("relu",), ("linear", 512, 10, False)]
+
+
+def _cv(po, src, dst, x):
+    """convert_tensor (same format returns the input, tensor_ops.cpp:808)."""
+    if tuple(src) == tuple(dst):
+        return x
+    return po.convert_tensor(*src, *dst, x)
+
+
+def oracle_step(po, layers, st, params, x, labels, lr, global_batch, record=None):
+    """One SGD step.  st = dict(forward, backward, gradient, optimizer, loss) of
+    (nbits, es); x = input codes in the forward format; returns (loss_code,
+    new_params, grads) and fills ``record`` (if given) with every activation
+    and gradient, keyed like the GPU model's recording."""
+    f, b, g, o, lf = (tuple(st[k]) for k in ("forward", "backward", "gradient", "optimizer", "loss"))
+    lb = int(round(math.log2(global_batch)))
+    rec = record if record is not None else {}
+    caches = []
+    h = x
+    pi = 0
+    for li, L in enumerate(layers):
+        kind = L[0]
+        if kind in ("conv", "linear"):
+            w, bias = params[pi]
+            pi += 1
+            if kind == "conv":
+                _, cin, cout, k, s, p, first = L
+                xin = h
+            else:
+                _, fin, fout, first = L
+                k, s, p = 1, 1, 0
+                xin = h.reshape(h.shape[0], -1, 1, 1)
+            y = po.conv2d(*f, xin, _cv(po, o, f, w), _cv(po, o, f, bias), s, p)
+            caches.append((kind, xin, w, (k, s, p), first, h.shape))
+            h = y if kind == "conv" else y.reshape(y.shape[0], -1)
+        elif kind == "relu":
+            caches.append(("relu", h))
+            h = po.relu_fwd(*f, h)
+        elif kind == "pool":
+            _, k, s = L
+            y, am = po.maxpool2d(*f, h, k, s)
+            caches.append(("pool", h.shape, am))
+            h = y
+        elif kind == "flatten":
+            caches.append(("flatten", h.shape))
+            h = h.reshape(h.shape[0], -1)
+        rec[f"act{li}"] = h
+    z = _cv(po, f, lf, h)
+    loss, d, rows = po.softmax_xent(*lf, z, labels, lb)
+    rec["loss_rows"] = rows
+    dy = _cv(po, lf, b, d)
+    rec["dlogits"] = dy
+    grads = [None] * len(params)
+    pi = len(params)
+    for li in range(len(layers) - 1, -1, -1):
+        c = caches[li]
+        kind = c[0]
+        if kind in ("conv", "linear"):
+            pi -= 1
+            _, xin, w, (k, s, p), first, in_shape = c
+            dy4 = dy if kind == "conv" else dy.reshape(dy.shape[0], -1, 1, 1)
+            dyg = _cv(po, b, g, dy4)
+            xg = _cv(po, f, g, xin)
+            dw = po.conv2d_weight_grad(*g, dyg, xg, w.shape, s, p)
+            db = po.conv2d_bias_grad(*g, dyg)
+            grads[pi] = (dw, db)
+            rec[f"grad_w{pi}"], rec[f"grad_b{pi}"] = dw, db
+            if first:
+                break
+            dx = po.conv2d_input_grad(*b, dy4, _cv(po, o, b, w), xin.shape, s, p)
+            dy = dx if kind == "conv" else dx.reshape(in_shape)
+        elif kind == "relu":
+            dy = po.relu_bwd(*f, c[1], dy)
+        elif kind == "pool":
+            dy = po.maxpool2d_backward(*b, dy, c[2], c[1])
+        elif kind == "flatten":
+            dy = dy.reshape(c[1])
+        rec[f"dact{li}"] = dy
+    lr_code = po.from_float64(*o, lr)
+    new_params = []
+    for (w, bias), (dw, db) in zip(params, grads):
+        new_params.append((po.sgd(*o, w, *g, dw, lr_code), po.sgd(*o, bias, *g, db, lr_code)))
+    return loss, new_params, grads
+
+
+def blob_images(seed: int, n: int, classes: int = 10, shape=(1, 32, 32), sigma: float = 0.3):
+    """Config-2 synthetic data: per-class Gaussian blobs (sigma 0.3) clipped to
+    [0, 1): class centres uniform in [0,1)^shape from the seed."""
+    rng = np.random.default_rng(seed)
+    centres = rng.random((classes,) + tuple(shape))
+    labels = rng.integers(0, classes, n)
+    x = centres[labels] + sigma * rng.standard_normal((n,) + tuple(shape))
+    x = np.clip(x, 0.0, np.nextafter(1.0, 0.0))
+    return x, labels.astype(np.int32)

@@ -55,6 +55,7 @@ _SIGS = {
                                    _vp]),
     "pnn_sgd_step": (C.c_int, [C.c_int, C.c_int, _vp, C.c_int, C.c_int, _vp, _i64, C.c_uint32, C.c_int,
                                C.c_int, _vp, C.c_int, C.c_int, _vp, _vp]),
+    "pnn_from_float64": (C.c_int, [C.c_int, C.c_int, _vp, _vp, _i64, _vp]),
     "pnn_scalar_eval": (C.c_int, [C.c_int, C.c_int, C.c_int, _vp, _vp, _vp, _i64, _vp]),
     "pnn_probe_int8_peak": (C.c_int, [C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
 }

@@ -192,6 +192,10 @@ __global__ void sgd_kernel(PositFmt fo, int bo, void* master, PositFmt fg, int b
     }
 }
 
+__global__ void from_float64_kernel(PositFmt f, int b, const double* x, void* out, int64_t n) {
+    GRID_STRIDE(i, n) { store_any(out, i, b, p_from_float64(f, x[i])); }
+}
+
 __global__ void scalar_eval_kernel(PositFmt f, int op, const uint32_t* a, const uint32_t* b,
                                    uint32_t* out, int64_t n) {
     GRID_STRIDE(i, n) {
@@ -335,6 +339,15 @@ int pnn_sgd_step(int opt_nbits, int opt_es, void* master, int g_nbits, int g_es,
         bytes_of(g_nbits), grad, n, lr_code, f1, bytes_of(f1.nbits), copy1, f2,
         bytes_of(f2.nbits), copy2);
     return launched("sgd_step");
+}
+
+int pnn_from_float64(int nbits, int es, const double* x, void* codes, int64_t n, void* stream) {
+    CHECK_FMT(nbits, es);
+    if (n < 0 || (n > 0 && (!x || !codes))) return set_status(PNN_EINVAL, "from_float64: bad args");
+    if (n == 0) return PNN_OK;
+    from_float64_kernel<<<grid1(n), 256, 0, (cudaStream_t)stream>>>(make_fmt(nbits, es),
+                                                                    bytes_of(nbits), x, codes, n);
+    return launched("from_float64");
 }
 
 int pnn_scalar_eval(int nbits, int es, int op, const uint32_t* a, const uint32_t* b,

@@ -1,0 +1,317 @@
+"""PyTorch-like layer / loss / optimizer API over the B200 quire kernels.
+
+The reference ships this layer only as specification (the
+files proj/src/layers.cpp, losses.cpp, optimizer.cpp, model.cpp are one-line
+placeholders), so the semantics are the ones pinned in
+SURVEY.md Appendix A and restated identically by the CPU oracle step
+(oracle/step.py):
+
+* StagePrecisions: p_forward, p_backward, p_gradient,
+  p_optimizer, p_loss -- quires everywhere.
+* MixedParam: master copy in p_optimizer, stage copies
+  refreshed with convert after every update (Appendix A.6/A.7).
+* Conv2d / Linear: bias inside the forward quire (tensor_ops.cpp:292,
+  Appendix A.1); input grad in p_backward; weight / bias grads accumulated in
+  p_gradient quires (operands converted to p_gradient).
+* ReLU (A.2), MaxPool2d (A.3, reference kernel), Flatten (A.4),
+  CrossEntropyLoss (A.5), SGD lr, momentum 0 (A.7), no input grad for the
+  first layer (A.8).
+
+Every tensor is a CUDA tensor of packed posit codes; every operation is a
+libpnn_b200.so kernel.  Data-parallel training (dp.py) reuses the same layers
+with the gradient reductions deferred to raw quire words.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import ops
+from .ops import PositConfig
+
+
+@dataclass(frozen=True)
+class StagePrecisions:
+    forward: PositConfig
+    backward: PositConfig
+    gradient: PositConfig
+    optimizer: PositConfig
+    loss: PositConfig
+
+    @staticmethod
+    def uniform(cfg) -> "StagePrecisions":
+        c = ops._cfg(cfg)
+        return StagePrecisions(c, c, c, c, c)
+
+
+class MixedParam:
+    """Master copy in p_optimizer plus converted copies per stage format."""
+
+    def __init__(self, master_codes: torch.Tensor, st: StagePrecisions):
+        self.st = st
+        self.master = master_codes
+        self.copies: dict[PositConfig, torch.Tensor] = {}
+        self.grad: torch.Tensor | None = None      # codes in p_gradient
+        self.grad_words = None                      # raw quire words (data-parallel)
+        self.grad_nar = None
+        self.refresh()
+
+    def stage_formats(self):
+        st = self.st
+        return sorted({st.forward, st.backward, st.gradient} - {st.optimizer},
+                      key=lambda c: (c.nbits, c.es))
+
+    def refresh(self):
+        for cfg in self.stage_formats():
+            self.copies[cfg] = ops.convert_tensor(self.master, self.st.optimizer, cfg)
+
+    def as_(self, cfg: PositConfig) -> torch.Tensor:
+        if cfg == self.st.optimizer:
+            return self.master
+        return self.copies[cfg]
+
+    @property
+    def shape(self):
+        return tuple(self.master.shape)
+
+
+def kaiming_uniform_codes(shape, fan_in, cfg: PositConfig, rng: np.random.Generator):
+    """fp32 Kaiming-uniform U(-sqrt(6/fan_in), +sqrt(6/fan_in)) rounded to posit
+    codes (Appendix A.9); generated on the host once, identical for the oracle."""
+    from .codec import from_float64_array
+
+    bound = np.float32(math.sqrt(6.0 / fan_in))
+    w = rng.uniform(-1.0, 1.0, size=shape).astype(np.float32) * bound
+    return from_float64_array(w.astype(np.float64), cfg)
+
+
+class Module:
+    training = True
+
+    def params(self):
+        return []
+
+
+class Conv2d(Module):
+    def __init__(self, cin, cout, k, st: StagePrecisions, stride=1, pad=0, rng=None,
+                 first_layer=False, device="cuda"):
+        self.cin, self.cout, self.k, self.stride, self.pad = cin, cout, k, stride, pad
+        self.st = st
+        self.first_layer = first_layer
+        rng = rng or np.random.default_rng(0)
+        fan_in = cin * k * k
+        w = kaiming_uniform_codes((cout, cin, k, k), fan_in, st.optimizer, rng)
+        b = np.zeros((cout,), np.uint64)
+        dt = st.optimizer.np_code_dtype
+        self.w = MixedParam(torch.from_numpy(w.astype(dt)).to(device), st)
+        self.b = MixedParam(torch.from_numpy(b.astype(dt)).to(device), st)
+        self.x = None
+
+    def params(self):
+        return [self.w, self.b]
+
+    def forward(self, x):
+        f = self.st.forward
+        self.x = x
+        return ops.conv2d(f, x, self.w.as_(f), self.b.as_(f), self.stride, self.pad)
+
+    def backward(self, dy, raw=False):
+        """dy in p_backward -> dx in p_backward (None for the first layer)."""
+        st = self.st
+        g = st.gradient
+        dyg = ops.convert_tensor(dy, st.backward, g)
+        xg = ops.convert_tensor(self.x, st.forward, g)
+        if raw:
+            _, self.w.grad_words, self.w.grad_nar = ops.conv2d_weight_grad(
+                g, dyg, xg, self.w.shape, self.stride, self.pad, raw=True)
+            _, self.b.grad_words, self.b.grad_nar = ops.conv2d_bias_grad(g, dyg, raw=True)
+        else:
+            self.w.grad = ops.conv2d_weight_grad(g, dyg, xg, self.w.shape, self.stride, self.pad)
+            self.b.grad = ops.conv2d_bias_grad(g, dyg)
+        if self.first_layer:
+            return None
+        return ops.conv2d_input_grad(st.backward, dy, self.w.as_(st.backward), self.x.shape,
+                                     self.stride, self.pad)
+
+
+class Linear(Conv2d):
+    """y = round(x W^T + b): the 1x1 convolution of [B, in, 1, 1] (Appendix A.1)."""
+
+    def __init__(self, fin, fout, st, rng=None, first_layer=False, device="cuda"):
+        super().__init__(fin, fout, 1, st, rng=rng, first_layer=first_layer, device=device)
+
+    def forward(self, x):
+        B = x.shape[0]
+        return super().forward(x.reshape(B, -1, 1, 1)).reshape(B, -1)
+
+    def backward(self, dy, raw=False):
+        B = dy.shape[0]
+        dx = super().backward(dy.reshape(B, -1, 1, 1), raw=raw)
+        return None if dx is None else dx.reshape(B, -1)
+
+
+class ReLU(Module):
+    def __init__(self, st: StagePrecisions):
+        self.st = st
+        self.x = None
+
+    def forward(self, x):
+        self.x = x
+        return ops.relu_fwd(self.st.forward, x)
+
+    def backward(self, dy, raw=False):
+        return ops.relu_bwd(self.st.forward, self.x, self.st.backward, dy)
+
+
+class MaxPool2d(Module):
+    def __init__(self, k, st: StagePrecisions, stride=None):
+        self.k, self.stride, self.st = k, stride or k, st
+        self.argmax = None
+        self.x_shape = None
+
+    def forward(self, x):
+        self.x_shape = x.shape
+        y, self.argmax = ops.maxpool2d(self.st.forward, x, self.k, self.stride)
+        return y
+
+    def backward(self, dy, raw=False):
+        return ops.maxpool2d_backward(self.st.backward, dy, self.argmax, self.x_shape, self.k,
+                                      self.stride)
+
+
+class Flatten(Module):
+    def __init__(self):
+        self.shape = None
+
+    def forward(self, x):
+        self.shape = x.shape
+        return x.reshape(x.shape[0], -1)
+
+    def backward(self, dy, raw=False):
+        return dy.reshape(self.shape)
+
+
+class CrossEntropyLoss(Module):
+    """Softmax cross-entropy in p_loss (Appendix A.5); the gradient is already
+    divided by the GLOBAL batch (2^-log2_batch)."""
+
+    def __init__(self, st: StagePrecisions):
+        self.st = st
+
+    def __call__(self, logits_fwd, labels, global_batch: int, raw=False):
+        lb = int(round(math.log2(global_batch)))
+        if 1 << lb != global_batch:
+            raise ValueError("global batch must be a power of two (Appendix A.5)")
+        z = ops.convert_tensor(logits_fwd, self.st.forward, self.st.loss)
+        out = ops.softmax_xent(self.st.loss, z, labels, lb, raw=raw)
+        dz = ops.convert_tensor(out[1], self.st.loss, self.st.backward)
+        if raw:
+            loss, _, rows, word, nar = out
+            return loss, dz, word, nar
+        return out[0], dz
+
+
+class Sequential(Module):
+    def __init__(self, *layers):
+        self.layers = list(layers)
+
+    def params(self):
+        return [p for l in self.layers for p in l.params()]
+
+    def forward(self, x, record=None):
+        for i, l in enumerate(self.layers):
+            x = l.forward(x)
+            if record is not None:
+                record[f"act{i}"] = x
+        return x
+
+    def backward(self, dy, raw=False, record=None):
+        for i in range(len(self.layers) - 1, -1, -1):
+            dy = self.layers[i].backward(dy, raw=raw)
+            if dy is None:
+                break
+            if record is not None:
+                record[f"dact{i}"] = dy
+        return dy
+
+
+class SGD:
+    """master = sub(master, mul(lr, convert(grad -> p_opt))), copies refreshed
+    (Appendix A.7; momentum 0)."""
+
+    def __init__(self, params, lr: float, st: StagePrecisions):
+        from .codec import from_float64_array
+
+        self.params = params
+        self.st = st
+        self.lr_code = int(from_float64_array(np.array([lr]), st.optimizer)[0])
+
+    def step(self):
+        st = self.st
+        for p in self.params:
+            fmts = p.stage_formats()
+            fused = [(c, p.copies[c]) for c in fmts[:2]]  # refreshed inside the SGD kernel
+            ops.sgd_step(st.optimizer, p.master, st.gradient, p.grad, self.lr_code, fused)
+            for c in fmts[2:]:
+                p.copies[c] = ops.convert_tensor(p.master, st.optimizer, c)
+
+
+def lenet5(st: StagePrecisions, seed: int = 0, device="cuda") -> Sequential:
+    """LeNet-5 of BASELINE configs 0/2: conv 1->6 5x5, ReLU, maxpool 2, conv
+    6->16 5x5, ReLU, maxpool 2, Linear 400->120->84->10 with ReLU."""
+    rng = np.random.default_rng(seed)
+    return Sequential(
+        Conv2d(1, 6, 5, st, rng=rng, first_layer=True, device=device), ReLU(st), MaxPool2d(2, st),
+        Conv2d(6, 16, 5, st, rng=rng, device=device), ReLU(st), MaxPool2d(2, st), Flatten(),
+        Linear(400, 120, st, rng=rng, device=device), ReLU(st),
+        Linear(120, 84, st, rng=rng, device=device), ReLU(st),
+        Linear(84, 10, st, rng=rng, device=device))
+
+
+def cifar_cnn(st: StagePrecisions, seed: int = 0, device="cuda") -> Sequential:
+    """CIFAR-shape CNN of BASELINE configs 3/4 (Appendix A.10): conv 3->32 3x3
+    pad 1, ReLU, conv 32->32, ReLU, maxpool; conv 32->64, ReLU, conv 64->64,
+    ReLU, maxpool; Linear 4096->512, ReLU, 512->10."""
+    rng = np.random.default_rng(seed)
+    return Sequential(
+        Conv2d(3, 32, 3, st, pad=1, rng=rng, first_layer=True, device=device), ReLU(st),
+        Conv2d(32, 32, 3, st, pad=1, rng=rng, device=device), ReLU(st), MaxPool2d(2, st),
+        Conv2d(32, 64, 3, st, pad=1, rng=rng, device=device), ReLU(st),
+        Conv2d(64, 64, 3, st, pad=1, rng=rng, device=device), ReLU(st), MaxPool2d(2, st),
+        Flatten(), Linear(4096, 512, st, rng=rng, device=device), ReLU(st),
+        Linear(512, 10, st, rng=rng, device=device))
+
+
+def train_step(model: Sequential, loss_fn: CrossEntropyLoss, opt: SGD, x_fwd, labels,
+               global_batch: int, record=None):
+    """One SGD step on one device; returns the loss code tensor [1] (p_loss)."""
+    logits = model.forward(x_fwd, record)
+    loss, dz = loss_fn(logits, labels, global_batch)
+    if record is not None:
+        record["dlogits"] = dz
+    model.backward(dz, record=record)
+    if record is not None:
+        for i, p in enumerate([q for q in model.params()]):
+            record[f"grad_{'wb'[i % 2]}{i // 2}"] = p.grad
+    opt.step()
+    return loss
+
+
+def layer_description(model: Sequential):
+    """The oracle-step layer list (oracle/step.py) of a model."""
+    out = []
+    for l in model.layers:
+        if isinstance(l, Linear):
+            out.append(("linear", l.cin, l.cout, l.first_layer))
+        elif isinstance(l, Conv2d):
+            out.append(("conv", l.cin, l.cout, l.k, l.stride, l.pad, l.first_layer))
+        elif isinstance(l, ReLU):
+            out.append(("relu",))
+        elif isinstance(l, MaxPool2d):
+            out.append(("pool", l.k, l.stride))
+        elif isinstance(l, Flatten):
+            out.append(("flatten",))
+    return out
