@@ -147,6 +147,18 @@ int pnn_pack_round(int nbits, int es, const int32_t* neg, const int32_t* scale,
                    const uint64_t* sig, const int32_t* sticky, int64_t n, uint32_t* codes,
                    void* stream);
 
+/* ---- data-parallel quire-word reduction --------------
+ * Raw W-bit quire words (16 bytes each) + NaR bytes -> int64 lanes
+ * [n][L+1] of 60-bit digits (L = pnn_quire_lanes) plus a NaR lane, ready for
+ * an integer SUM all-reduce (NCCL int64; 8 ranks * (2^60-1) < 2^63: no overflow); then
+ * lanes -> carry-propagated W-bit quire -> one rounding (codes) and/or the
+ * reduced raw words. */
+int pnn_quire_lanes(int nbits, int es);
+int pnn_quire_to_lanes(int nbits, int es, const void* words, const uint8_t* nar, int64_t n,
+                       uint64_t* lanes, void* stream);
+int pnn_lanes_to_posit(int nbits, int es, const uint64_t* lanes, int64_t n, void* codes,
+                       void* words_out, void* stream);
+
 /* ---- measurement ---------------------------------------------------------
  * Tensor-pipe ceiling for the kind::i8 MMA shape the quire GEMM issues
  * (M=128, N=256, K=32 from shared memory), one CTA per SM, `iters` MMAs each;

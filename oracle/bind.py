@@ -253,6 +253,23 @@ class Restatement(_Base):
                                                  _p(dx)), "maxpool2d_backward")
         return dx.reshape(x_shape)
 
+    def quire_words(self, q) -> tuple[int, bool]:
+        """(W-bit quire value as a Python int, NaR flag) of a restatement quire."""
+        buf = (C.c_uint64 * 16)()
+        nar = C.c_int()
+        self.lib.po_quire_words.argtypes = [C.c_void_p, C.POINTER(C.c_uint64), C.c_int, C.POINTER(C.c_int)]
+        nw = self.lib.po_quire_words(q.h, buf, 16, C.byref(nar))
+        return sum(int(buf[i]) << (64 * i) for i in range(nw)), bool(nar.value)
+
+    def round_words(self, n, es, value: int) -> int:
+        """Round a W-bit quire value (Python int, taken mod 2^W) once."""
+        W = 4 * ((n - 2) << es) + n
+        value &= (1 << W) - 1
+        nw = (W + 63) // 64
+        arr = (C.c_uint64 * nw)(*[(value >> (64 * i)) & ((1 << 64) - 1) for i in range(nw)])
+        self.lib.po_round_words.restype = C.c_uint64
+        return int(self.lib.po_round_words(n, es, arr, nw))
+
     def ew(self, n, es, op, a, b):
         a, b = _codes(a), _codes(b)
         out = np.zeros(a.shape, np.uint64)

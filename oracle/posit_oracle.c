@@ -786,3 +786,12 @@ void po_sgd(int opt_nbits, int opt_es, uint64_t* w, int g_nbits, int g_es, const
                             po_scalar_op(opt_nbits, opt_es, 2, lr, gg));
     }
 }
+
+/* Round W-bit quire words (little-endian limbs, two's complement) once --
+ * Quire::to_posit on an externally summed quire (data-parallel reduction). */
+uint64_t po_round_words(int nbits, int es, const uint64_t* words, int nwords) {
+    wide w;
+    wide_zero(&w);
+    for (int i = 0; i < nwords && i < WL; ++i) w.w[i] = words[i];
+    return wide_round(nbits, es, &w, po_quire_bits(nbits, es), -2 * po_max_scale(nbits, es));
+}

@@ -69,6 +69,9 @@ uint64_t po_quire_to_posit(const po_quire* q);
 /* Raw quire words (little-endian uint64 limbs, W bits, two's complement). */
 int po_quire_words(const po_quire* q, uint64_t* out, int max_words, int* nar);
 
+/* Round externally summed W-bit quire words once (data-parallel reduction). */
+uint64_t po_round_words(int nbits, int es, const uint64_t* words, int nwords);
+
 /* Tensor kernels, quire mode (tensor_ops.cpp).  Return 0 on success. */
 int po_matmul(int nbits, int es, const uint64_t* A, const uint64_t* B, uint64_t* C,
               int64_t m, int64_t k, int64_t n);

@@ -57,6 +57,9 @@ _SIGS = {
                                C.c_int, _vp, C.c_int, C.c_int, _vp, _vp]),
     "pnn_from_float64": (C.c_int, [C.c_int, C.c_int, _vp, _vp, _i64, _vp]),
     "pnn_scalar_eval": (C.c_int, [C.c_int, C.c_int, C.c_int, _vp, _vp, _vp, _i64, _vp]),
+    "pnn_quire_lanes": (C.c_int, [C.c_int, C.c_int]),
+    "pnn_quire_to_lanes": (C.c_int, [C.c_int, C.c_int, _vp, _vp, _i64, _vp, _vp]),
+    "pnn_lanes_to_posit": (C.c_int, [C.c_int, C.c_int, _vp, _i64, _vp, _vp, _vp]),
     "pnn_probe_int8_peak": (C.c_int, [C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
 }
 

@@ -409,3 +409,26 @@ def scalar_eval(cfg, op: int, a, b=None):
                                                 b.data_ptr() if b is not None else None, out.data_ptr(),
                                                 a.numel(), _stream_ptr(a.device)))
     return out
+
+
+# ---- data-parallel lane encoding (csrc/dp.cu) --------------------------------
+
+def quire_to_lanes(cfg, words, nar):
+    """Raw quire words (int64 [..., 2]) + NaR bytes -> int64 lanes [n, L+1]."""
+    cfg = _cfg(cfg)
+    L = _native.lib().pnn_quire_lanes(cfg.nbits, cfg.es)
+    n = nar.numel()
+    lanes = torch.empty((n, L + 1), dtype=torch.int64, device=words.device)
+    _native.check(_native.lib().pnn_quire_to_lanes(cfg.nbits, cfg.es, words.contiguous().data_ptr(),
+                                                   nar.contiguous().data_ptr(), n, lanes.data_ptr(),
+                                                   _stream_ptr(words.device)))
+    return lanes
+
+
+def lanes_to_posit(cfg, lanes):
+    cfg = _cfg(cfg)
+    n = lanes.shape[0]
+    out = torch.empty((n,), dtype=cfg.code_dtype, device=lanes.device)
+    _native.check(_native.lib().pnn_lanes_to_posit(cfg.nbits, cfg.es, lanes.contiguous().data_ptr(), n,
+                                                   out.data_ptr(), None, _stream_ptr(lanes.device)))
+    return out

@@ -1,0 +1,63 @@
+"""Data-parallel exactness on one B200: the global batch is split into
+`world` shards, each shard's backward runs in raw-quire mode on its own model
+replica, the shards' lanes are summed (what NCCL all-reduce does across GPUs)
+and rounded once -- gradients and loss must equal the single-process step
+bit for bit, for 2, 4 and 8 simulated ranks.  (Multi-process NCCL needs more
+than the one GPU this environment grants; the rank logic is covered by
+tests/test_dp_cpu.py with gloo.)"""
+import numpy as np
+import pytest
+import torch
+
+from paper_2105_00053_b200 import codec, dp, nn, ops
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_sharded_raw_quire_sum_equals_full_batch(cuda, world):
+    st = nn.StagePrecisions(ops.P80, ops.P121, ops.P121, ops.P161, ops.P161)
+    B = 64
+    rng = np.random.default_rng(world)
+    x = codec.from_float64_device(rng.random((B, 1, 32, 32)), st.forward)
+    labels = torch.from_numpy(rng.integers(0, 10, B).astype(np.int32)).cuda()
+    ref = nn.lenet5(st, seed=3)
+    loss_fn = nn.CrossEntropyLoss(st)
+    ref_loss, dz = loss_fn(ref.forward(x), labels, B)
+    ref.backward(dz)
+    ref_grads = [codec.to_host(p.grad) for p in ref.params()]
+
+    lanes_sum = None
+    loss_lanes = None
+    for r in range(world):
+        lo, hi = dp.shard_bounds(B, r, world)
+        rep = nn.lenet5(st, seed=3)
+        _, dzr, word, nar = loss_fn(rep.forward(x[lo:hi]), labels[lo:hi], B, raw=True)
+        rep.backward(dzr, raw=True)
+        lanes = [ops.quire_to_lanes(st.gradient, p.grad_words, p.grad_nar) for p in rep.params()]
+        ll = ops.quire_to_lanes(st.loss, word, nar)
+        lanes_sum = lanes if lanes_sum is None else [a + b for a, b in zip(lanes_sum, lanes)]
+        loss_lanes = ll if loss_lanes is None else loss_lanes + ll
+    for i, (ls, want) in enumerate(zip(lanes_sum, ref_grads)):
+        got = codec.to_host(ops.lanes_to_posit(st.gradient, ls)).reshape(want.shape)
+        assert (got == want).all(), i
+    lc = ops.lanes_to_posit(st.loss, loss_lanes)
+    lb = int(np.log2(B))
+    loss = ops.scalar_eval(st.loss, 7, lc.to(torch.int32), torch.full((1,), -lb, dtype=torch.int32, device="cuda"))
+    assert int(codec.to_host(loss)[0]) & 0xFFFF == int(codec.to_host(ref_loss)[0])
+
+
+def test_dp_train_step_world1_equals_train_step(cuda):
+    st = nn.StagePrecisions.uniform(ops.P161)
+    B = 32
+    rng = np.random.default_rng(1)
+    x = codec.from_float64_device(rng.random((B, 1, 32, 32)), st.forward)
+    labels = torch.from_numpy(rng.integers(0, 10, B).astype(np.int32)).cuda()
+    a, b = nn.lenet5(st, seed=9), nn.lenet5(st, seed=9)
+    la = nn.train_step(a, nn.CrossEntropyLoss(st), nn.SGD(a.params(), 1 / 16, st), x, labels, B)
+    red = dp.QuireAllReduce(b.params(), st.gradient, group=False)
+    lb = dp.dp_train_step(b, nn.CrossEntropyLoss(st), nn.SGD(b.params(), 1 / 16, st), red, x, labels, B,
+                          group=False)
+    assert int(codec.to_host(la)[0]) == int(codec.to_host(lb)[0])
+    for p, q in zip(a.params(), b.params()):
+        assert (codec.to_host(p.master) == codec.to_host(q.master)).all()
