@@ -1,6 +1,7 @@
 """C-ABI library checks that need no GPU: it loads, exports every symbol the
 public header declares, and validates arguments before touching the device."""
 import ctypes as C
+import os
 
 import pytest
 
@@ -50,3 +51,12 @@ def test_invalid_arguments_fail_loudly_without_gpu():
 def test_non_quire_path_is_out_of_scope():
     with pytest.raises(NotImplementedError):
         ops.matmul(None, None, use_quire=False, cfg=(8, 0))
+
+
+def test_cpp_host_mirror_compiles_and_links(tmp_path):
+    """include/pnn_b200/tensor_ops.hpp + libpnn_b200.so build into a C++
+    program here (running it needs the GPU: tests/test_cpp_host_gpu.py)."""
+    from test_cpp_host_gpu import build_host_ops_test
+
+    exe = build_host_ops_test(str(tmp_path))
+    assert os.path.exists(exe)
