@@ -40,6 +40,8 @@ struct FetchIm2colFwd {  // X[r = (n,oy,ox)][k = (c,ky,kx) | bias col]
     int64_t kconv;
     uint32_t one_code;
     static constexpr bool kRowFastest = true;
+    static constexpr bool kVecK = false, kVecR = false;
+    __device__ const CodeT* ptr(int64_t, int64_t) const { return nullptr; }
     __device__ __forceinline__ uint32_t operator()(int64_t r, int64_t k) const {
         if (k >= kconv) return one_code;
         const int64_t ohw = g.OH * g.OW;
@@ -58,6 +60,8 @@ struct FetchWeightFwd {  // X[r = f][k = (c,ky,kx) | bias col]
     const CodeT* bias;
     int64_t kconv;
     static constexpr bool kRowFastest = false;
+    static constexpr bool kVecK = false, kVecR = false;
+    __device__ const CodeT* ptr(int64_t, int64_t) const { return nullptr; }
     __device__ __forceinline__ uint32_t operator()(int64_t r, int64_t k) const {
         return k < kconv ? uint32_t(w[r * kconv + k]) : uint32_t(bias[r]);
     }
@@ -70,6 +74,8 @@ struct FetchDgradDy {  // X[r = (n,iy,ix)][k = (f,ky,kx)]
     const CodeT* dy;
     ConvGeom g;
     static constexpr bool kRowFastest = true;
+    static constexpr bool kVecK = false, kVecR = false;
+    __device__ const CodeT* ptr(int64_t, int64_t) const { return nullptr; }
     __device__ __forceinline__ uint32_t operator()(int64_t r, int64_t k) const {
         const int64_t hw = g.H * g.W;
         const int64_t n = r / hw, p = r - n * hw, iy = p / g.W, ix = p - iy * g.W;
@@ -88,6 +94,8 @@ struct FetchDgradW {  // X[r = c][k = (f,ky,kx)] = w[f][c][ky][kx]
     const CodeT* w;
     ConvGeom g;
     static constexpr bool kRowFastest = false;
+    static constexpr bool kVecK = false, kVecR = false;
+    __device__ const CodeT* ptr(int64_t, int64_t) const { return nullptr; }
     __device__ __forceinline__ uint32_t operator()(int64_t r, int64_t k) const {
         const int64_t khw = g.KH * g.KW;
         const int64_t f = k / khw, t = k - f * khw;
@@ -131,6 +139,8 @@ struct FetchWgradX {  // X[r = (c,ky,kx)][k = (n,oy,ox)] = x_pad[n][c][oy*s+ky][
     const CodeT* x;
     ConvGeom g;
     static constexpr bool kRowFastest = false;
+    static constexpr bool kVecK = false, kVecR = false;
+    __device__ const CodeT* ptr(int64_t, int64_t) const { return nullptr; }
     __device__ __forceinline__ uint32_t operator()(int64_t r, int64_t k) const {
         const int64_t khw = g.KH * g.KW;
         const int64_t c = r / khw, t = r - c * khw, ky = t / g.KW, kx = t - ky * g.KW;
@@ -147,6 +157,8 @@ struct FetchWgradDy {  // X[r = f][k = (n,o)] = dy[n][f][o]
     const CodeT* dy;
     ConvGeom g;
     static constexpr bool kRowFastest = false;
+    static constexpr bool kVecK = false, kVecR = false;
+    __device__ const CodeT* ptr(int64_t, int64_t) const { return nullptr; }
     __device__ __forceinline__ uint32_t operator()(int64_t r, int64_t k) const {
         const int64_t ohw = g.OH * g.OW;
         const int64_t n = k / ohw, p = k - n * ohw;

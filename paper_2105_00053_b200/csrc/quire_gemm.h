@@ -14,6 +14,8 @@ struct QuireGemmPlan {
     size_t a_img_bytes, b_img_bytes, row_nar_bytes, col_nar_bytes, partial_bytes;
     size_t off_a, off_b, off_row_nar, off_col_nar, off_flags, off_partial, workspace_bytes;
     int smem_bytes;
+    int pair;               // 1: CTA-pair (cta_group::2) kernel
+    int64_t mtiles_alloc;   // A image m-tiles (even in pair mode)
 };
 
 // Optional per-phase CUDA events (pack start, pack end / GEMM start, GEMM end,

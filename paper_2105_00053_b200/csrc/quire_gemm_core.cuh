@@ -35,6 +35,7 @@
 
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 
 #include "posit_device.cuh"
 #include "quire_gemm.h"
@@ -82,15 +83,13 @@ __device__ __forceinline__ void digit_words(uint32_t code, const PositFmt& f, ui
                                             uint32_t& hi, bool& nar) {
     int64_t X;
     nar = decode_x(code, f, X);
-    int8_t d[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    int8_t dd[D];
-    balanced_digits<D>(X, dd);
-#pragma unroll
-    for (int i = 0; i < D; ++i) d[i] = dd[i];
-    lo = uint32_t(uint8_t(d[0])) | (uint32_t(uint8_t(d[1])) << 8) | (uint32_t(uint8_t(d[2])) << 16) |
-         (uint32_t(uint8_t(d[3])) << 24);
-    hi = uint32_t(uint8_t(d[4])) | (uint32_t(uint8_t(d[5])) << 8) | (uint32_t(uint8_t(d[6])) << 16) |
-         (uint32_t(uint8_t(d[7])) << 24);
+    // Balanced digits in two instructions: with bias = sum_{i<D} 128*256^i,
+    // Y = X + bias has plain bytes (d_i + 128) in [0, 255] (|X| is within the
+    // D-digit balanced capacity, so Y < 256^D), and d_i = byte_i(Y) ^ 0x80.
+    constexpr uint64_t bias = 0x8080808080808080ull >> (8 * (8 - D));
+    const uint64_t y = (uint64_t(X) + bias) ^ bias;
+    lo = uint32_t(y);
+    hi = uint32_t(y >> 32);
 }
 
 constexpr int kLutMaxBits = 10;  // shared-memory decode LUT up to 1024 codes (8 KB)
@@ -102,6 +101,8 @@ struct FetchRowMajor {  // X[r][k] = p[r*ld + k]
     const CodeT* p;
     int64_t ld;
     static constexpr bool kRowFastest = false;
+    static constexpr bool kVecK = true, kVecR = false;
+    __device__ __forceinline__ const CodeT* ptr(int64_t r, int64_t k) const { return p + r * ld + k; }
     __device__ __forceinline__ uint32_t operator()(int64_t r, int64_t k) const {
         return uint32_t(p[r * ld + k]);
     }
@@ -111,6 +112,8 @@ struct FetchColMajor {  // X[r][k] = p[k*ld + r]
     const CodeT* p;
     int64_t ld;
     static constexpr bool kRowFastest = true;
+    static constexpr bool kVecK = false, kVecR = true;
+    __device__ __forceinline__ const CodeT* ptr(int64_t r, int64_t k) const { return p + k * ld + r; }
     __device__ __forceinline__ uint32_t operator()(int64_t r, int64_t k) const {
         return uint32_t(p[k * ld + r]);
     }
@@ -156,7 +159,45 @@ __global__ void __launch_bounds__(256) pack_kernel(Fetch fetch, int64_t rows_tot
         const int nkb = int(kbt - kb0 < KBS ? kbt - kb0 : KBS);
         const int64_t r0 = t * ROWS, k0 = kb0 * KB;
         __syncthreads();  // previous pass's readers are done with `tile` (and LUT is built)
-        if constexpr (!Fetch::kRowFastest) {
+        constexpr int VE = 16 / int(sizeof(CodeT));  // codes per 16-byte vector
+        if constexpr (Fetch::kVecK) {
+            // X rows contiguous in memory: 16-byte loads along k
+            constexpr int VPR = KW / VE;
+            for (int i = threadIdx.x; i < ROWS * VPR; i += blockDim.x) {
+                const int r = i / VPR, v = i % VPR;
+                const int64_t gr = r0 + r, gk = k0 + int64_t(v) * VE;
+                alignas(16) CodeT vals[VE];
+                const CodeT* src = (gr < rows_total) ? fetch.ptr(gr, gk) : nullptr;
+                if (src && gk + VE <= K && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+                    *reinterpret_cast<uint4*>(vals) = __ldg(reinterpret_cast<const uint4*>(src));
+                } else {
+#pragma unroll
+                    for (int j = 0; j < VE; ++j)
+                        vals[j] = (gr < rows_total && gk + j < K) ? CodeT(fetch(gr, gk + j)) : CodeT(0);
+                }
+                uint32_t* dst = reinterpret_cast<uint32_t*>(tile + r * LD + v * VE);
+#pragma unroll
+                for (int w = 0; w < 4; ++w) dst[w] = reinterpret_cast<const uint32_t*>(vals)[w];
+            }
+        } else if constexpr (Fetch::kVecR) {
+            // X columns contiguous in memory (B row-major): 16-byte loads along r
+            constexpr int VPC = ROWS / VE;
+            for (int i = threadIdx.x; i < KW * VPC; i += blockDim.x) {
+                const int k = i / VPC, v = i % VPC;
+                const int64_t gr = r0 + int64_t(v) * VE, gk = k0 + k;
+                alignas(16) CodeT vals[VE];
+                const CodeT* src = (gk < K) ? fetch.ptr(gr, gk) : nullptr;
+                if (src && gr + VE <= rows_total && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+                    *reinterpret_cast<uint4*>(vals) = __ldg(reinterpret_cast<const uint4*>(src));
+                } else {
+#pragma unroll
+                    for (int j = 0; j < VE; ++j)
+                        vals[j] = (gr + j < rows_total && gk < K) ? CodeT(fetch(gr + j, gk)) : CodeT(0);
+                }
+#pragma unroll
+                for (int j = 0; j < VE; ++j) tile[(v * VE + j) * LD + k] = vals[j];
+            }
+        } else if constexpr (!Fetch::kRowFastest) {
             for (int i = threadIdx.x; i < ROWS * KW; i += blockDim.x) {
                 const int r = i / KW, k = i % KW;  // k fastest: coalesced along a row of X
                 const int64_t gr = r0 + r, gk = k0 + k;
@@ -180,12 +221,17 @@ __global__ void __launch_bounds__(256) pack_kernel(Fetch fetch, int64_t rows_tot
             uint32_t lo[16], hi[16];
             bool any_nar = false;
             const CodeT* tr = tile + r * LD + kbl * KB + kc * 16;
+            uint32_t wv[16 * sizeof(CodeT) / 4];
+#pragma unroll
+            for (int w = 0; w < int(16 * sizeof(CodeT) / 4); ++w)
+                wv[w] = reinterpret_cast<const uint32_t*>(tr)[w];
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
-                const uint32_t code = uint32_t(tr[j]);
+                const uint32_t code = sizeof(CodeT) == 1 ? (wv[j >> 2] >> (8 * (j & 3))) & 0xFFu
+                                                         : (wv[j >> 1] >> (16 * (j & 1))) & 0xFFFFu;
                 if (use_lut) {
                     lo[j] = lut[2 * code];
-                    hi[j] = lut[2 * code + 1];
+                    hi[j] = D > 4 ? lut[2 * code + 1] : 0u;
                     any_nar |= code == nar_code;
                 } else {
                     bool nar;
@@ -293,7 +339,7 @@ __device__ __forceinline__ void tile_coords(int64_t t, int64_t mtiles, int64_t n
 // issuer, warps 2..9 = epilogue (2 warps per TMEM lane quarter, each owning
 // half of the tile's columns).  The epilogue drains TMEM into registers,
 // releases it (tmem_empty), and rounds/stores while the next tile's MMAs run.
-template <int D, int QW, typename CodeT>
+template <int D, int QW, typename CodeT, bool kPair>
 __global__ void __launch_bounds__(kThreads, 1)
     quire_gemm_tc_kernel(const int8_t* __restrict__ a_img, const int8_t* __restrict__ b_img,
                          int64_t kbt, int64_t kb_per_split, const uint8_t* __restrict__ row_nar,
@@ -301,11 +347,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                          int64_t N, PositFmt f,
                          unsigned __int128* __restrict__ partial, int64_t mtiles, int64_t ntiles,
                          int64_t splits) {
+    // kPair: clusters of 2 CTAs run one M=256 tcgen05.mma.cta_group::2 per
+    // digit plane; each CTA stages its own 128-row A tile and HALF of the
+    // concatenated B rows, halving each SM's shared-memory operand traffic.
     using Geo = Geometry<D>;
     using QT = typename QuireWord<QW>::T;
     constexpr int NT = Geo::NT, KB = Geo::KB, STAGES = Geo::STAGES, G = Geo::G;
     constexpr int COLS = NT / 2;                 // columns per epilogue thread
     constexpr int GB = G < 8 ? G : 8;            // TMEM loads batched per wait
+    constexpr int B_LOCAL = kPair ? Geo::B_BYTES / 2 : Geo::B_BYTES;
+    constexpr int STAGE_TX = Geo::A_BYTES + B_LOCAL;
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* zero_tile = smem + STAGES * Geo::STAGE_BYTES;
     uint64_t* full = reinterpret_cast<uint64_t*>(zero_tile + kZeroBytes);
@@ -316,23 +367,34 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    const int64_t tiles = mtiles * ntiles * splits;
+    const uint32_t rank = kPair ? ptx::cluster_ctarank() : 0u;
+    const bool leader = rank == 0;
+    // work units: pair-tiles (2 m-tiles x 1 n-tile) in pair mode
+    const int64_t unit_m = kPair ? (mtiles + 1) / 2 : mtiles;
+    const int64_t tiles = unit_m * ntiles * splits;
+    const int64_t unit0 = kPair ? blockIdx.x / 2 : blockIdx.x;
+    const int64_t ustride = kPair ? gridDim.x / 2 : gridDim.x;
 
     for (int i = threadIdx.x; i < kZeroBytes / 16; i += kThreads)
         reinterpret_cast<int4*>(zero_tile)[i] = make_int4(0, 0, 0, 0);
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < STAGES; ++s) {
-            ptx::mbar_init(&full[s], 1);
+            // leader: own expect_tx arrive + the follower's "landed" forward
+            ptx::mbar_init(&full[s], (kPair && leader) ? 2 : 1);
             ptx::mbar_init(&empty[s], 1);
         }
         ptx::mbar_init(tmem_full, 1);
-        ptx::mbar_init(tmem_empty, kEpiWarps);
+        ptx::mbar_init(tmem_empty, kPair ? 2 * kEpiWarps : kEpiWarps);
         ptx::fence_barrier_init();
     }
-    if (warp == 1) ptx::tmem_alloc<Geo::TMEM_COLS>(tmem_slot);
+    if (warp == 1) {
+        if constexpr (kPair) ptx::tmem_alloc2<Geo::TMEM_COLS>(tmem_slot);
+        else ptx::tmem_alloc<Geo::TMEM_COLS>(tmem_slot);
+    }
     ptx::fence_proxy_async_smem();
     ptx::tc_fence_before();
-    __syncthreads();
+    if constexpr (kPair) ptx::cluster_sync();
+    else __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
@@ -340,38 +402,55 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) {
             // ===== producer: one bulk copy per operand per stage =====
             uint32_t it = 0;
-            for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
-                int64_t split, mt, nt;
-                tile_coords(t, mtiles, ntiles, split, mt, nt);
+            for (int64_t t = unit0; t < tiles; t += ustride) {
+                int64_t split, um, nt;
+                tile_coords(t, unit_m, ntiles, split, um, nt);
+                const int64_t mt = kPair ? 2 * um + rank : um;
                 const int64_t kb0 = split * kb_per_split;
                 const int nkb = int(min(kbt, kb0 + kb_per_split) - kb0);
                 const int8_t* a_src = a_img + (mt * kbt + kb0) * int64_t(Geo::A_BYTES);
-                const int8_t* b_src = b_img + (nt * kbt + kb0) * int64_t(Geo::B_BYTES);
+                const int8_t* b_src = b_img + (nt * kbt + kb0) * int64_t(Geo::B_BYTES) +
+                                      (kPair ? rank * B_LOCAL : 0);
                 for (int i = 0; i < nkb; ++i, ++it) {
                     const int s = it % STAGES;
                     const uint32_t ph = (it / STAGES) & 1;
                     ptx::mbar_wait(&empty[s], ph ^ 1);
                     uint8_t* sa = smem + s * Geo::STAGE_BYTES;
-                    ptx::mbar_arrive_expect_tx(&full[s], Geo::STAGE_BYTES);
+                    ptx::mbar_arrive_expect_tx(&full[s], STAGE_TX);
                     ptx::bulk_g2s(sa, a_src + int64_t(i) * Geo::A_BYTES, Geo::A_BYTES, &full[s]);
-                    ptx::bulk_g2s(sa + Geo::A_BYTES, b_src + int64_t(i) * Geo::B_BYTES,
-                                  Geo::B_BYTES, &full[s]);
+                    ptx::bulk_g2s(sa + Geo::A_BYTES, b_src + int64_t(i) * Geo::B_BYTES, B_LOCAL,
+                                  &full[s]);
                 }
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
+        if (lane == 0 && kPair && !leader) {
+            // ===== follower: forward "stage landed" to the leader's barrier =====
+            uint32_t it = 0;
+            for (int64_t t = unit0; t < tiles; t += ustride) {
+                int64_t split, um, nt;
+                tile_coords(t, unit_m, ntiles, split, um, nt);
+                const int64_t kb0 = split * kb_per_split;
+                const int nkb = int(min(kbt, kb0 + kb_per_split) - kb0);
+                for (int i = 0; i < nkb; ++i, ++it) {
+                    const int s = it % STAGES;
+                    const uint32_t ph = (it / STAGES) & 1;
+                    ptx::mbar_wait(&full[s], ph);
+                    ptx::mbar_arrive_remote(ptx::mapa(ptx::smem_u32(&full[s]), 0));
+                }
+            }
+        } else if (lane == 0 && leader) {
             // ===== MMA issuer =====
-            constexpr uint32_t idesc = ptx::idesc_i8(kBM, Geo::NMMA);
+            constexpr uint32_t idesc = ptx::idesc_i8(kPair ? 2 * kBM : kBM, Geo::NMMA);
             constexpr uint32_t SBO = 8 * KB, LBO = 128;
             const uint64_t zdesc = ptx::smem_desc_kmajor(ptx::smem_u32(zero_tile), LBO, 8 * 32);
             uint32_t it = 0, j = 0;
-            for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++j) {
-                int64_t split, mt, nt;
-                tile_coords(t, mtiles, ntiles, split, mt, nt);
+            for (int64_t t = unit0; t < tiles; t += ustride, ++j) {
+                int64_t split, um, nt;
+                tile_coords(t, unit_m, ntiles, split, um, nt);
                 const int64_t kb0 = split * kb_per_split;
                 const int nkb = int(min(kbt, kb0 + kb_per_split) - kb0);
-                ptx::mbar_wait(tmem_empty, (j & 1) ^ 1);  // epilogue drained the previous tile
+                ptx::mbar_wait(tmem_empty, (j & 1) ^ 1);  // epilogue(s) drained the previous tile
                 ptx::tc_fence_after();
                 for (int i = 0; i < nkb; ++i, ++it) {
                     const int s = it % STAGES;
@@ -384,19 +463,27 @@ __global__ void __launch_bounds__(kThreads, 1)
                     for (int ks = 0; ks < KB / 32; ++ks) {
                         const uint64_t bdesc = ptx::smem_desc_kmajor(b_base + ks * 256, LBO, SBO);
                         const bool first = (i == 0 && ks == 0);
-                        if (first)  // zero groups D-1 .. 2D-2 (plane 0 initialises 0 .. D-1)
-                            ptx::mma_i8(tmem + (D - 1) * NT, zdesc, bdesc, idesc, 0);
+                        if (first) {  // zero groups D-1 .. 2D-2 (plane 0 initialises 0 .. D-1)
+                            if constexpr (kPair) ptx::mma_i8_pair(tmem + (D - 1) * NT, zdesc, bdesc, idesc, 0);
+                            else ptx::mma_i8(tmem + (D - 1) * NT, zdesc, bdesc, idesc, 0);
+                        }
 #pragma unroll
                         for (int p = 0; p < D; ++p) {
                             const uint64_t adesc = ptx::smem_desc_kmajor(
                                 a_base + p * (kBM * KB) + ks * 256, LBO, SBO);
-                            ptx::mma_i8(tmem + p * NT, adesc, bdesc, idesc,
-                                        (first && p == 0) ? 0u : 1u);
+                            if constexpr (kPair)
+                                ptx::mma_i8_pair(tmem + p * NT, adesc, bdesc, idesc,
+                                                 (first && p == 0) ? 0u : 1u);
+                            else
+                                ptx::mma_i8(tmem + p * NT, adesc, bdesc, idesc,
+                                            (first && p == 0) ? 0u : 1u);
                         }
                     }
-                    ptx::mma_commit(&empty[s]);
+                    if constexpr (kPair) ptx::mma_commit_pair(&empty[s]);
+                    else ptx::mma_commit(&empty[s]);
                 }
-                ptx::mma_commit(tmem_full);
+                if constexpr (kPair) ptx::mma_commit_pair(tmem_full);
+                else ptx::mma_commit(tmem_full);
             }
         }
     } else {
@@ -406,9 +493,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t trow = tmem + (uint32_t(quarter * 32) << 16) + half * COLS;
         const bool vec_ok = out.mode == 0 && (out.ldc % 8) == 0;
         uint32_t j = 0;
-        for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++j) {
-            int64_t split, mt, nt;
-            tile_coords(t, mtiles, ntiles, split, mt, nt);
+        const uint32_t tmem_empty_leader = kPair ? ptx::mapa(ptx::smem_u32(tmem_empty), 0) : 0u;
+        for (int64_t t = unit0; t < tiles; t += ustride, ++j) {
+            int64_t split, um, nt;
+            tile_coords(t, unit_m, ntiles, split, um, nt);
+            const int64_t mt = kPair ? 2 * um + rank : um;
             ptx::mbar_wait(tmem_full, j & 1);
             ptx::tc_fence_after();
             QT q[COLS];
@@ -432,7 +521,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             ptx::tc_fence_before();
             __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(tmem_empty);
+            if (lane == 0) {
+                if (kPair && !leader) ptx::mbar_arrive_remote(tmem_empty_leader);
+                else ptx::mbar_arrive(tmem_empty);
+            }
 
             const int64_t row = mt * kBM + quarter * 32 + lane;
             if (row >= M) continue;
@@ -468,10 +560,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     __syncwarp();
     ptx::tc_fence_before();
-    __syncthreads();
+    if constexpr (kPair) ptx::cluster_sync();
+    else __syncthreads();
     if (warp == 1) {
         ptx::tc_fence_after();
-        ptx::tmem_dealloc<Geo::TMEM_COLS>(tmem);
+        if constexpr (kPair) ptx::tmem_dealloc2<Geo::TMEM_COLS>(tmem);
+        else ptx::tmem_dealloc<Geo::TMEM_COLS>(tmem);
     }
 }
 
@@ -575,9 +669,14 @@ inline QuireGemmPlan plan_for(const PositFmt& f, int64_t M, int64_t N, int64_t K
     if (kbps < 1) kbps = 1;
     p.kb_per_split = p.kbt < kbps ? p.kbt : kbps;
     p.splits = (p.kbt + p.kb_per_split - 1) / p.kb_per_split;
-    p.a_img_bytes = size_t(p.mtiles) * p.kbt * Geo::A_BYTES;
+    // CTA pairs (cta_group::2) whenever there are two m-tiles to pair up;
+    // PNN_B200_NO_PAIR=1 forces the single-CTA kernel (A/B measurements).
+    static const bool no_pair = getenv("PNN_B200_NO_PAIR") != nullptr;
+    p.pair = (p.mtiles >= 2 && !no_pair) ? 1 : 0;
+    p.mtiles_alloc = p.pair ? (p.mtiles + 1) / 2 * 2 : p.mtiles;
+    p.a_img_bytes = size_t(p.mtiles_alloc) * p.kbt * Geo::A_BYTES;
     p.b_img_bytes = size_t(p.ntiles) * p.kbt * Geo::B_BYTES;
-    p.row_nar_bytes = size_t(p.mtiles) * kBM;
+    p.row_nar_bytes = size_t(p.mtiles_alloc) * kBM;
     p.col_nar_bytes = size_t(p.ntiles) * Geo::NT;
     p.partial_bytes = (p.splits > 1 || raw) ? size_t(p.splits) * M * N * 16 : 0;
     p.smem_bytes = Geo::SMEM;
@@ -629,28 +728,62 @@ cudaError_t launch_generic(const QuireGemmPlan& p, const GemmArgs& g, FA fa, FB 
     cudaError_t e;
     if ((e = cudaMemsetAsync(rnar, 0, p.off_flags + 16 - p.off_row_nar, st)) != cudaSuccess) return e;
     if (stats) cudaEventRecord(stats->ev[0], st);
-    const int64_t a_work = p.mtiles * p.kbt, b_work = p.ntiles * p.kbt;  // upper bounds
+    const int64_t a_work = p.mtiles_alloc * p.kbt, b_work = p.ntiles * p.kbt;  // upper bounds
     pack_kernel<D, kBM, CodeT, FA><<<int(a_work < 148 * 8 ? a_work : 148 * 8), 256, 0, st>>>(
-        fa, g.M, g.K, f, a_img, rnar, flags, p.mtiles, p.kbt);
+        fa, g.M, g.K, f, a_img, rnar, flags, p.mtiles_alloc, p.kbt);
     pack_kernel<D, Geo::NT, CodeT, FB><<<int(b_work < 148 * 8 ? b_work : 148 * 8), 256, 0, st>>>(
         fb, g.N, g.K, f, b_img, cnar, flags + 1, p.ntiles, p.kbt);
     if (stats) cudaEventRecord(stats->ev[1], st);
     // D <= 3 implies R <= 11, hence W <= 64: no 128-bit instantiation needed.
-    void (*kern)(const int8_t*, const int8_t*, int64_t, int64_t, const uint8_t*, const uint8_t*,
-                 OutMap<CodeT>, int64_t, int64_t, PositFmt, unsigned __int128*, int64_t, int64_t,
-                 int64_t);
-    if constexpr (D <= 3)
-        kern = f.W <= 32 ? quire_gemm_tc_kernel<D, 1, CodeT> : quire_gemm_tc_kernel<D, 2, CodeT>;
-    else
-        kern = f.W <= 64 ? quire_gemm_tc_kernel<D, 2, CodeT> : quire_gemm_tc_kernel<D, 4, CodeT>;
+    using KernFn = void (*)(const int8_t*, const int8_t*, int64_t, int64_t, const uint8_t*,
+                            const uint8_t*, OutMap<CodeT>, int64_t, int64_t, PositFmt,
+                            unsigned __int128*, int64_t, int64_t, int64_t);
+    KernFn kern;
+    if (p.pair) {
+        if constexpr (D <= 3)
+            kern = f.W <= 32 ? quire_gemm_tc_kernel<D, 1, CodeT, true>
+                             : quire_gemm_tc_kernel<D, 2, CodeT, true>;
+        else
+            kern = f.W <= 64 ? quire_gemm_tc_kernel<D, 2, CodeT, true>
+                             : quire_gemm_tc_kernel<D, 4, CodeT, true>;
+    } else {
+        if constexpr (D <= 3)
+            kern = f.W <= 32 ? quire_gemm_tc_kernel<D, 1, CodeT, false>
+                             : quire_gemm_tc_kernel<D, 2, CodeT, false>;
+        else
+            kern = f.W <= 64 ? quire_gemm_tc_kernel<D, 2, CodeT, false>
+                             : quire_gemm_tc_kernel<D, 4, CodeT, false>;
+    }
     if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Geo::SMEM)) !=
         cudaSuccess)
         return e;
-    const int64_t tiles = p.mtiles * p.ntiles * p.splits;
-    const int grid = int(tiles < num_sms() ? tiles : num_sms());
-    kern<<<grid, kThreads, Geo::SMEM, st>>>(a_img, b_img, p.kbt, p.kb_per_split,
-                                            g.row_nar ? rnar : nullptr, g.col_nar ? cnar : nullptr,
-                                            out, g.M, g.N, f, partial, p.mtiles, p.ntiles, p.splits);
+    const uint8_t* rn = g.row_nar ? rnar : nullptr;
+    const uint8_t* cn = g.col_nar ? cnar : nullptr;
+    if (p.pair) {
+        const int64_t units = (p.mtiles + 1) / 2 * p.ntiles * p.splits;
+        const int64_t pairs = units < num_sms() / 2 ? units : num_sms() / 2;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(unsigned(2 * pairs), 1, 1);
+        cfg.blockDim = dim3(kThreads, 1, 1);
+        cfg.dynamicSmemBytes = Geo::SMEM;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        if ((e = cudaLaunchKernelEx(&cfg, kern, (const int8_t*)a_img, (const int8_t*)b_img, p.kbt,
+                                    p.kb_per_split, rn, cn, out, g.M, g.N, f, partial, p.mtiles,
+                                    p.ntiles, p.splits)) != cudaSuccess)
+            return e;
+    } else {
+        const int64_t tiles = p.mtiles * p.ntiles * p.splits;
+        const int grid = int(tiles < num_sms() ? tiles : num_sms());
+        kern<<<grid, kThreads, Geo::SMEM, st>>>(a_img, b_img, p.kbt, p.kb_per_split, rn, cn, out,
+                                                g.M, g.N, f, partial, p.mtiles, p.ntiles, p.splits);
+    }
     if (stats) cudaEventRecord(stats->ev[2], st);
     if (use_partial) {
         quire_finalize_kernel<CodeT><<<grid_for(g.M * g.N, 256), 256, 0, st>>>(
