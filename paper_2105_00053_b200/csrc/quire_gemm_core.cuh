@@ -669,10 +669,11 @@ inline QuireGemmPlan plan_for(const PositFmt& f, int64_t M, int64_t N, int64_t K
     if (kbps < 1) kbps = 1;
     p.kb_per_split = p.kbt < kbps ? p.kbt : kbps;
     p.splits = (p.kbt + p.kb_per_split - 1) / p.kb_per_split;
-    // CTA pairs (cta_group::2) whenever there are two m-tiles to pair up;
-    // PNN_B200_NO_PAIR=1 forces the single-CTA kernel (A/B measurements).
-    static const bool no_pair = getenv("PNN_B200_NO_PAIR") != nullptr;
-    p.pair = (p.mtiles >= 2 && !no_pair) ? 1 : 0;
+    // CTA pairs (cta_group::2) are opt-in (PNN_B200_PAIR=1): measured on B200
+    // they cost more in cross-CTA stage hand-off bubbles (tensor pipe 79% vs
+    // 92% active, profiles/README.md) than they save in shared-memory traffic.
+    static const bool want_pair = getenv("PNN_B200_PAIR") != nullptr;
+    p.pair = (p.mtiles >= 2 && want_pair) ? 1 : 0;
     p.mtiles_alloc = p.pair ? (p.mtiles + 1) / 2 * 2 : p.mtiles;
     p.a_img_bytes = size_t(p.mtiles_alloc) * p.kbt * Geo::A_BYTES;
     p.b_img_bytes = size_t(p.ntiles) * p.kbt * Geo::B_BYTES;

@@ -264,3 +264,29 @@ def test_errors_raise(cuda):
     with pytest.raises(_native.PnnError):
         ops.quire_gemm((16, 2), torch.zeros((4, 5), dtype=torch.uint16, device="cuda"),
                        torch.zeros((5, 3), dtype=torch.uint16, device="cuda"))
+
+
+def test_cta_pair_kernel_parity(cuda, po):
+    """The opt-in CTA-pair (tcgen05 cta_group::2) kernel is bit-identical too,
+    including an odd number of m-tiles (zero-padded follower tile)."""
+    import subprocess
+    import sys
+
+    code = (
+        "import numpy as np, torch, sys; sys.path.insert(0, '.');"
+        "from paper_2105_00053_b200 import ops;"
+        "from oracle.bind import Restatement; po = Restatement();"
+        "rng = np.random.default_rng(5)\n"
+        "for cfg in [(8, 0), (8, 1), (12, 1), (16, 1)]:\n"
+        "    n, es = cfg\n"
+        "    A = rng.integers(0, 1 << n, (3 * 128 + 5, 300)).astype(np.uint64); A[A == 1 << (n - 1)] = 0\n"
+        "    B = rng.integers(0, 1 << n, (300, 70)).astype(np.uint64); B[B == 1 << (n - 1)] = 0\n"
+        "    dt = ops.PositConfig(*cfg).np_code_dtype\n"
+        "    got = ops.quire_gemm(cfg, torch.from_numpy(A.astype(dt)).cuda(), torch.from_numpy(B.astype(dt)).cuda())\n"
+        "    assert (got.cpu().numpy().astype(np.uint64) == po.matmul(n, es, A, B)).all(), cfg\n"
+        "print('pair ok')\n")
+    import os
+    env = dict(os.environ, PNN_B200_PAIR="1")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300, env=env,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0 and "pair ok" in r.stdout, r.stderr[-2000:]
