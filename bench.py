@@ -322,8 +322,10 @@ def main():
         e2e = {"value": world * e_steps * macs_per_step / te, "unit": UNIT,
                "h2d_bytes_per_step": sum(2 * M * K * 8 for _ in FORMATS),
                "d2h_bytes_per_step": sum(M * N * 8 for _ in FORMATS),
-               "path": "pnn_matmul_host: uint64 code arrays (reference Tensor storage) in pinned "
-                       "host memory -> H2D -> narrow -> quire GEMM -> widen -> D2H, wall clock"}
+               "path": "pnn_matmul_host: uint64 code arrays (reference Tensor storage, pinned) -> "
+                       "host-thread narrow to packed codes, chunked H2D overlapped -> quire GEMM -> "
+                       "chunked D2H overlapped with host-thread widen; wall clock (bound by host "
+                       "memory traffic of the 8-byte-per-code storage)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

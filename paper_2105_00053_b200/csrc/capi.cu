@@ -4,10 +4,15 @@
 // or a kernel fails, the call fails.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <condition_variable>
 #include <cstdint>
 #include <cstring>
+#include <functional>
 #include <mutex>
 #include <string>
+#include <thread>
+#include <vector>
 
 #include "../../include/pnn_b200.h"
 #include "posit_device.cuh"
@@ -57,11 +62,99 @@ int check_fmt(int nbits, int es) {
 cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
 
 // Grow-only device scratch for the synchronous host entry points.
+constexpr int64_t kHostChunk = int64_t(1) << 22;  // codes per host narrow/widen chunk
+constexpr int kEvents = 16;
+
+// Persistent host worker pool for the synchronous host entry points (the
+// reference's ThreadPool::parallel_for role, thread_pool.hpp:21-48: contiguous
+// chunks, caller participates).
+class HostPool {
+public:
+    HostPool() {
+        unsigned n = std::thread::hardware_concurrency();
+        nworkers_ = int(n < 2 ? 1 : (n > 32 ? 32 : n));
+        for (int i = 1; i < nworkers_; ++i) threads_.emplace_back([this, i] { loop(i); });
+    }
+    ~HostPool() {
+        {
+            std::lock_guard<std::mutex> l(mu_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        for (auto& t : threads_) t.join();
+    }
+    void parallel_for(int64_t n, const std::function<void(int64_t, int64_t)>& fn) {
+        if (n <= 0) return;
+        if (nworkers_ == 1 || n < 65536) {
+            fn(0, n);
+            return;
+        }
+        {
+            std::lock_guard<std::mutex> l(mu_);
+            fn_ = &fn;
+            n_ = n;
+            pending_ = nworkers_ - 1;
+            ++gen_;
+        }
+        cv_.notify_all();
+        fn(0, n / nworkers_);
+        std::unique_lock<std::mutex> l(mu_);
+        done_cv_.wait(l, [this] { return pending_ == 0; });
+        fn_ = nullptr;
+    }
+
+private:
+    void loop(int idx) {
+        uint64_t seen = 0;
+        for (;;) {
+            const std::function<void(int64_t, int64_t)>* fn;
+            int64_t n;
+            {
+                std::unique_lock<std::mutex> l(mu_);
+                cv_.wait(l, [&] { return stop_ || gen_ != seen; });
+                if (stop_) return;
+                seen = gen_;
+                fn = fn_;
+                n = n_;
+            }
+            (*fn)(n * idx / nworkers_, n * (idx + 1) / nworkers_);
+            std::lock_guard<std::mutex> l(mu_);
+            if (--pending_ == 0) done_cv_.notify_one();
+        }
+    }
+    int nworkers_ = 1;
+    std::vector<std::thread> threads_;
+    std::mutex mu_;
+    std::condition_variable cv_, done_cv_;
+    const std::function<void(int64_t, int64_t)>* fn_ = nullptr;
+    int64_t n_ = 0;
+    int pending_ = 0;
+    uint64_t gen_ = 0;
+    bool stop_ = false;
+};
+
+HostPool& host_pool() {
+    static HostPool pool;
+    return pool;
+}
+
 struct Scratch {
     std::mutex mu;
     void* ptr = nullptr;
     size_t bytes = 0;
+    void* hptr = nullptr;
+    size_t hbytes = 0;
     cudaStream_t stream = nullptr;
+    cudaEvent_t ev[kEvents] = {};
+    void* reserve_host(size_t n) {
+        if (n <= hbytes) return hptr;
+        if (hptr) cudaFreeHost(hptr);
+        hptr = nullptr;
+        hbytes = 0;
+        if (cudaHostAlloc(&hptr, n, cudaHostAllocDefault) != cudaSuccess) return nullptr;
+        hbytes = n;
+        return hptr;
+    }
     void* reserve(size_t n) {
         if (n <= bytes) return ptr;
         if (ptr) cudaFree(ptr);
@@ -222,39 +315,71 @@ int pnn_matmul_host(int nbits, int es, const uint64_t* A, const uint64_t* B, uin
     if (!g_scratch.stream) {
         if (cudaError_t e = cudaStreamCreateWithFlags(&g_scratch.stream, cudaStreamNonBlocking))
             return cuda_fail(e, "stream");
+        for (auto& ev : g_scratch.ev)
+            if (cudaError_t e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming))
+                return cuda_fail(e, "event");
     }
     cudaStream_t st = g_scratch.stream;
     QuireGemmPlan p;
     if (quire_gemm_plan(nbits, es, M, N, K, 0, &p)) return fail(PNN_EUNSUPPORTED, "format");
     const int cb = nbits <= 8 ? 1 : 2;
     auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
-    const size_t wide_a = al(size_t(M * K) * 8), wide_b = al(size_t(K * N) * 8),
-                 wide_c = al(size_t(M * N) * 8);
     const size_t pa = al(size_t(M * K) * cb), pb = al(size_t(K * N) * cb), pc = al(size_t(M * N) * cb);
-    uint8_t* base = static_cast<uint8_t*>(
-        g_scratch.reserve(wide_a + wide_b + wide_c + pa + pb + pc + p.workspace_bytes));
-    if (!base) return fail(PNN_ECUDA, "matmul_host: device allocation failed");
-    uint64_t* dA64 = reinterpret_cast<uint64_t*>(base);
-    uint64_t* dB64 = reinterpret_cast<uint64_t*>(base + wide_a);
-    uint64_t* dC64 = reinterpret_cast<uint64_t*>(base + wide_a + wide_b);
-    uint8_t* dA = base + wide_a + wide_b + wide_c;
-    uint8_t* dB = dA + pa;
-    uint8_t* dC = dB + pb;
-    uint8_t* ws = dC + pc;
+    uint8_t* base = static_cast<uint8_t*>(g_scratch.reserve(pa + pb + pc + p.workspace_bytes));
+    uint8_t* hbase = static_cast<uint8_t*>(g_scratch.reserve_host(pa + pb + pc));
+    if (!base || !hbase) return fail(PNN_ECUDA, "matmul_host: allocation failed");
+    uint8_t *dA = base, *dB = base + pa, *dC = base + pa + pb, *ws = base + pa + pb + pc;
+    uint8_t *hA = hbase, *hB = hbase + pa, *hC = hbase + pa + pb;
     const uint64_t mask = (uint64_t(1) << nbits) - 1;
+    HostPool& pool = host_pool();
     cudaError_t e;
-    if ((e = cudaMemcpyAsync(dA64, A, size_t(M * K) * 8, cudaMemcpyHostToDevice, st)))
-        return cuda_fail(e, "H2D A");
-    if ((e = cudaMemcpyAsync(dB64, B, size_t(K * N) * 8, cudaMemcpyHostToDevice, st)))
-        return cuda_fail(e, "H2D B");
-    narrow_codes_kernel<<<blocks_for(M * K), 256, 0, st>>>(dA64, dA, M * K, cb, mask);
-    narrow_codes_kernel<<<blocks_for(K * N), 256, 0, st>>>(dB64, dB, K * N, cb, mask);
+    // Host threads narrow the uint64 Tensor storage (tensor.hpp:10-14) to packed
+    // codes chunk by chunk; each chunk's H2D copy overlaps the next chunk's narrowing.
+    auto upload = [&](const uint64_t* src, uint8_t* hdst, uint8_t* ddst, int64_t n) -> cudaError_t {
+        for (int64_t c0 = 0; c0 < n; c0 += kHostChunk) {
+            const int64_t c1 = std::min(n, c0 + kHostChunk);
+            pool.parallel_for(c1 - c0, [&](int64_t lo, int64_t hi) {
+                if (cb == 1)
+                    for (int64_t i = c0 + lo; i < c0 + hi; ++i) hdst[i] = uint8_t(src[i] & mask);
+                else
+                    for (int64_t i = c0 + lo; i < c0 + hi; ++i)
+                        reinterpret_cast<uint16_t*>(hdst)[i] = uint16_t(src[i] & mask);
+            });
+            if (cudaError_t err = cudaMemcpyAsync(ddst + c0 * cb, hdst + c0 * cb, size_t(c1 - c0) * cb,
+                                                  cudaMemcpyHostToDevice, st))
+                return err;
+        }
+        return cudaSuccess;
+    };
+    if ((e = upload(A, hA, dA, M * K))) return cuda_fail(e, "H2D A");
+    if ((e = upload(B, hB, dB, K * N))) return cuda_fail(e, "H2D B");
     int rc = quire_gemm_launch(nbits, es, dA, dB, dC, M, N, K, K, N, N, ws, p.workspace_bytes, 0,
                                st, nullptr);
     if (rc) return rc == 4 ? cuda_fail(cudaGetLastError(), "matmul launch") : fail(rc, "matmul");
-    widen_codes_kernel<<<blocks_for(M * N), 256, 0, st>>>(dC, dC64, M * N, cb);
-    if ((e = cudaMemcpyAsync(C, dC64, size_t(M * N) * 8, cudaMemcpyDeviceToHost, st)))
-        return cuda_fail(e, "D2H C");
+    // D2H in chunks; widen chunk i on the host while chunk i+1 is in flight.
+    const int64_t n = M * N;
+    const int64_t nch = (n + kHostChunk - 1) / kHostChunk;
+    for (int64_t c = 0; c < nch; c += kEvents) {
+        const int64_t cend = std::min(nch, c + kEvents);
+        for (int64_t k = c; k < cend; ++k) {
+            const int64_t c0 = k * kHostChunk, c1 = std::min(n, c0 + kHostChunk);
+            if ((e = cudaMemcpyAsync(hC + c0 * cb, dC + c0 * cb, size_t(c1 - c0) * cb,
+                                     cudaMemcpyDeviceToHost, st)))
+                return cuda_fail(e, "D2H C");
+            cudaEventRecord(g_scratch.ev[k - c], st);
+        }
+        for (int64_t k = c; k < cend; ++k) {
+            if ((e = cudaEventSynchronize(g_scratch.ev[k - c]))) return cuda_fail(e, "D2H sync");
+            const int64_t c0 = k * kHostChunk, c1 = std::min(n, c0 + kHostChunk);
+            pool.parallel_for(c1 - c0, [&](int64_t lo, int64_t hi) {
+                if (cb == 1)
+                    for (int64_t i = c0 + lo; i < c0 + hi; ++i) C[i] = hC[i];
+                else
+                    for (int64_t i = c0 + lo; i < c0 + hi; ++i)
+                        C[i] = reinterpret_cast<const uint16_t*>(hC)[i];
+            });
+        }
+    }
     if ((e = cudaStreamSynchronize(st))) return cuda_fail(e, "matmul_host sync");
     return PNN_OK;
 }
