@@ -134,7 +134,7 @@ def int8_peak(L=None):
         if L.pnn_probe_int8_peak(20000, C.byref(tops), C.byref(ms)) == 0:
             return tops.value, (f"measured tensor-pipe ceiling: tcgen05 kind::i8 probe, 148 SMs x "
                                 f"20000 MMAs 128x256x32, {ms.value:.2f} ms")
-    p = os.path.join(REPO, "profiles", "int8_peak.json")
+    p = os.path.join(REPO, "profiles", "int8_peak_cublaslt.json")
     if os.path.exists(p):
         d = json.load(open(p))
         return d["int8_tops"], f"measured cuBLASLt int8 GEMM (torch._int_mm 8192^3, {d.get('when', '')})"
@@ -145,6 +145,19 @@ def int8_peak(L=None):
 
 
 _REF_CACHE = {}
+
+
+def ncu_traffic(kernel_prefix: str):
+    """DRAM bytes (read + write) per launch of the kernel from the committed
+    `ncu --set full` capture summary (profiles/ncu_full_r01.json)."""
+    p = os.path.join(REPO, "profiles", "ncu_full_r01.json")
+    if not os.path.exists(p):
+        return None
+    for rep, ks in json.load(open(p)).items():
+        for k in ks:
+            if k["kernel"].startswith(kernel_prefix) and "dram_traffic_bytes" in k:
+                return {"bytes_per_launch": k["dram_traffic_bytes"], "source": f"profiles/ncu_full_r01.json:{rep}"}
+    return None
 
 
 def run_cpu_reference_sample(rows: int, threads: int, cols: int = N):
@@ -284,6 +297,8 @@ def main():
     int8_ops = 2.0 * M * N * K * D * D  # algorithmic int8 ops per launch (D^2 digit MMAs / MAC)
     achieved = int8_ops / (per_fmt[dom]["mma_ms"] / 1000.0) / 1e12
     peak, peak_src = int8_peak(L)
+    traffic = ncu_traffic(f"quire_gemm_tc_kernel<{D}, {4 if ncfg.nbits > 8 else 1}, "
+                          f"{'unsigned short' if ncfg.nbits > 8 else 'unsigned char'}")
 
     # ---- e2e through the reference-facing host API (uint64 Tensor storage) ----
     e2e = None
@@ -354,7 +369,9 @@ def main():
             "per_format": {f"posit({f[0]},{f[1]})": per_fmt[f] for f in FORMATS},
             "roofline": {"bound": "tensor", "kernel": f"quire_gemm_tc_kernel posit({dom[0]},{dom[1]})",
                          "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": achieved / peak, "traffic": None,
+                         "frac": achieved / peak,
+                         "traffic": traffic["bytes_per_launch"] if traffic else None,
+                         "traffic_unit": "bytes/launch (dram read+write, ncu --set full)",
                          "note": f"int8 tensor ops (2/MAC) on tcgen05 kind::i8, {D}x{D} digit "
                                  f"MMAs per posit MAC; peak = {peak_src}"},
             "gpu_launches": args.steps * len(FORMATS) * 3,

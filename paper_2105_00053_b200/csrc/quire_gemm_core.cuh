@@ -45,11 +45,12 @@ namespace pnn_b200 {
 
 template <int D>
 struct TileCfg;
-// Stage sizes keep every stage's refill (L2 latency + transfer) shorter than
-// the MMA time of the stages still queued: many small stages, ~190 KB total.
-template <> struct TileCfg<2> { static constexpr int NT = 128, KB = 64, STAGES = 6; };
-template <> struct TileCfg<3> { static constexpr int NT = 64, KB = 32, STAGES = 10; };
-template <> struct TileCfg<4> { static constexpr int NT = 64, KB = 32, STAGES = 8; };
+// ~190 KB of stages per CTA.  (D=2 measured: 3 x 64 KB stages beat 6 x 32 KB,
+// 182 vs 193 us on the 4096^3 GEMM -- the kernel is shared-memory-bandwidth
+// bound, not refill-latency bound; profiles/README.md.)
+template <> struct TileCfg<2> { static constexpr int NT = 128, KB = 128, STAGES = 3; };
+template <> struct TileCfg<3> { static constexpr int NT = 64, KB = 64, STAGES = 5; };
+template <> struct TileCfg<4> { static constexpr int NT = 64, KB = 64, STAGES = 4; };
 template <> struct TileCfg<5> { static constexpr int NT = 32, KB = 32, STAGES = 6; };
 template <> struct TileCfg<6> { static constexpr int NT = 32, KB = 32, STAGES = 6; };
 template <> struct TileCfg<7> { static constexpr int NT = 32, KB = 32, STAGES = 5; };
