@@ -40,8 +40,29 @@ struct FetchIm2colFwd {  // X[r = (n,oy,ox)][k = (c,ky,kx) | bias col]
     int64_t kconv;
     uint32_t one_code;
     static constexpr bool kRowFastest = true;
-    static constexpr bool kVecK = false, kVecR = false;
+    static constexpr bool kVecK = false, kVecR = false, kSep = true;
     __device__ const CodeT* ptr(int64_t, int64_t) const { return nullptr; }
+    // separable form: row -> (image base + window origin), k -> (tap offset, tap)
+    struct RI { int64_t base; int iy0, ix0; };
+    struct KI { int64_t off; int ky, kx; };
+    __device__ __forceinline__ RI row(int64_t r) const {
+        const int64_t ohw = g.OH * g.OW;
+        const int64_t n = r / ohw, p = r - n * ohw, oy = p / g.OW, ox = p - oy * g.OW;
+        const int iy0 = int(oy * g.stride - g.pad), ix0 = int(ox * g.stride - g.pad);
+        return RI{n * g.C * g.H * g.W + int64_t(iy0) * g.W + ix0, iy0, ix0};
+    }
+    __device__ __forceinline__ KI kin(int64_t k) const {
+        if (k >= kconv) return KI{0, 1 << 30, 0};  // bias column
+        const int64_t khw = g.KH * g.KW;
+        const int64_t c = k / khw, t = k - c * khw, ky = t / g.KW, kx = t - ky * g.KW;
+        return KI{c * g.H * g.W + ky * g.W + kx, int(ky), int(kx)};
+    }
+    __device__ __forceinline__ uint32_t at(const RI& ri, const KI& ki) const {
+        if (ki.ky == (1 << 30)) return one_code;
+        const int iy = ri.iy0 + ki.ky, ix = ri.ix0 + ki.kx;
+        if (unsigned(iy) >= unsigned(g.H) || unsigned(ix) >= unsigned(g.W)) return 0;
+        return uint32_t(x[ri.base + ki.off]);
+    }
     __device__ __forceinline__ uint32_t operator()(int64_t r, int64_t k) const {
         if (k >= kconv) return one_code;
         const int64_t ohw = g.OH * g.OW;
@@ -60,8 +81,15 @@ struct FetchWeightFwd {  // X[r = f][k = (c,ky,kx) | bias col]
     const CodeT* bias;
     int64_t kconv;
     static constexpr bool kRowFastest = false;
-    static constexpr bool kVecK = false, kVecR = false;
+    static constexpr bool kVecK = false, kVecR = false, kSep = true;
     __device__ const CodeT* ptr(int64_t, int64_t) const { return nullptr; }
+    struct RI { int64_t base; int f, pad_; };
+    struct KI { int64_t off; int is_bias, pad_; };
+    __device__ __forceinline__ RI row(int64_t r) const { return RI{r * kconv, int(r), 0}; }
+    __device__ __forceinline__ KI kin(int64_t k) const { return KI{k, k >= kconv ? 1 : 0, 0}; }
+    __device__ __forceinline__ uint32_t at(const RI& ri, const KI& ki) const {
+        return ki.is_bias ? uint32_t(bias[ri.f]) : uint32_t(w[ri.base + ki.off]);
+    }
     __device__ __forceinline__ uint32_t operator()(int64_t r, int64_t k) const {
         return k < kconv ? uint32_t(w[r * kconv + k]) : uint32_t(bias[r]);
     }
@@ -74,8 +102,31 @@ struct FetchDgradDy {  // X[r = (n,iy,ix)][k = (f,ky,kx)]
     const CodeT* dy;
     ConvGeom g;
     static constexpr bool kRowFastest = true;
-    static constexpr bool kVecK = false, kVecR = false;
+    static constexpr bool kVecK = false, kVecR = false, kSep = true;
     __device__ const CodeT* ptr(int64_t, int64_t) const { return nullptr; }
+    struct RI { int64_t base; int ty0, tx0; };  // dy image base, padded input position
+    struct KI { int64_t off; int ky, kx; };     // channel-f plane offset, tap
+    __device__ __forceinline__ RI row(int64_t r) const {
+        const int64_t hw = g.H * g.W;
+        const int64_t n = r / hw, p = r - n * hw, iy = p / g.W, ix = p - iy * g.W;
+        return RI{n * g.F * g.OH * g.OW, int(iy + g.pad), int(ix + g.pad)};
+    }
+    __device__ __forceinline__ KI kin(int64_t k) const {
+        const int64_t khw = g.KH * g.KW;
+        const int64_t f = k / khw, t = k - f * khw, ky = t / g.KW, kx = t - ky * g.KW;
+        return KI{f * g.OH * g.OW, int(ky), int(kx)};
+    }
+    __device__ __forceinline__ uint32_t at(const RI& ri, const KI& ki) const {
+        int oy = ri.ty0 - ki.ky, ox = ri.tx0 - ki.kx;  // taps of tensor_ops.cpp:546-554
+        if (oy < 0 || ox < 0) return 0;
+        if (g.stride != 1) {
+            if (oy % g.stride || ox % g.stride) return 0;
+            oy /= g.stride;
+            ox /= g.stride;
+        }
+        if (oy >= g.OH || ox >= g.OW) return 0;
+        return uint32_t(dy[ri.base + ki.off + int64_t(oy) * g.OW + ox]);
+    }
     __device__ __forceinline__ uint32_t operator()(int64_t r, int64_t k) const {
         const int64_t hw = g.H * g.W;
         const int64_t n = r / hw, p = r - n * hw, iy = p / g.W, ix = p - iy * g.W;
@@ -94,8 +145,19 @@ struct FetchDgradW {  // X[r = c][k = (f,ky,kx)] = w[f][c][ky][kx]
     const CodeT* w;
     ConvGeom g;
     static constexpr bool kRowFastest = false;
-    static constexpr bool kVecK = false, kVecR = false;
+    static constexpr bool kVecK = false, kVecR = false, kSep = true;
     __device__ const CodeT* ptr(int64_t, int64_t) const { return nullptr; }
+    struct RI { int64_t base; int pad0, pad1; };
+    struct KI { int64_t off; int pad0, pad1; };
+    __device__ __forceinline__ RI row(int64_t r) const { return RI{r * g.KH * g.KW, 0, 0}; }
+    __device__ __forceinline__ KI kin(int64_t k) const {
+        const int64_t khw = g.KH * g.KW;
+        const int64_t f = k / khw, t = k - f * khw;
+        return KI{f * g.C * khw + t, 0, 0};
+    }
+    __device__ __forceinline__ uint32_t at(const RI& ri, const KI& ki) const {
+        return uint32_t(w[ri.base + ki.off]);
+    }
     __device__ __forceinline__ uint32_t operator()(int64_t r, int64_t k) const {
         const int64_t khw = g.KH * g.KW;
         const int64_t f = k / khw, t = k - f * khw;
@@ -139,8 +201,25 @@ struct FetchWgradX {  // X[r = (c,ky,kx)][k = (n,oy,ox)] = x_pad[n][c][oy*s+ky][
     const CodeT* x;
     ConvGeom g;
     static constexpr bool kRowFastest = false;
-    static constexpr bool kVecK = false, kVecR = false;
+    static constexpr bool kVecK = false, kVecR = false, kSep = true;
     __device__ const CodeT* ptr(int64_t, int64_t) const { return nullptr; }
+    struct RI { int64_t base; int ky_p, kx_p; };  // channel plane, tap - pad
+    struct KI { int64_t off; int oys, oxs; };     // image base, output position * stride
+    __device__ __forceinline__ RI row(int64_t r) const {
+        const int64_t khw = g.KH * g.KW;
+        const int64_t c = r / khw, t = r - c * khw, ky = t / g.KW, kx = t - ky * g.KW;
+        return RI{c * g.H * g.W, int(ky - g.pad), int(kx - g.pad)};
+    }
+    __device__ __forceinline__ KI kin(int64_t k) const {
+        const int64_t ohw = g.OH * g.OW;
+        const int64_t n = k / ohw, p = k - n * ohw, oy = p / g.OW, ox = p - oy * g.OW;
+        return KI{n * g.C * g.H * g.W, int(oy * g.stride), int(ox * g.stride)};
+    }
+    __device__ __forceinline__ uint32_t at(const RI& ri, const KI& ki) const {
+        const int iy = ki.oys + ri.ky_p, ix = ki.oxs + ri.kx_p;
+        if (unsigned(iy) >= unsigned(g.H) || unsigned(ix) >= unsigned(g.W)) return 0;
+        return uint32_t(x[ri.base + ki.off + int64_t(iy) * g.W + ix]);
+    }
     __device__ __forceinline__ uint32_t operator()(int64_t r, int64_t k) const {
         const int64_t khw = g.KH * g.KW;
         const int64_t c = r / khw, t = r - c * khw, ky = t / g.KW, kx = t - ky * g.KW;
@@ -157,8 +236,19 @@ struct FetchWgradDy {  // X[r = f][k = (n,o)] = dy[n][f][o]
     const CodeT* dy;
     ConvGeom g;
     static constexpr bool kRowFastest = false;
-    static constexpr bool kVecK = false, kVecR = false;
+    static constexpr bool kVecK = false, kVecR = false, kSep = true;
     __device__ const CodeT* ptr(int64_t, int64_t) const { return nullptr; }
+    struct RI { int64_t base; int pad0, pad1; };
+    struct KI { int64_t off; int pad0, pad1; };
+    __device__ __forceinline__ RI row(int64_t r) const { return RI{r * g.OH * g.OW, 0, 0}; }
+    __device__ __forceinline__ KI kin(int64_t k) const {
+        const int64_t ohw = g.OH * g.OW;
+        const int64_t n = k / ohw, p = k - n * ohw;
+        return KI{n * g.F * ohw + p, 0, 0};
+    }
+    __device__ __forceinline__ uint32_t at(const RI& ri, const KI& ki) const {
+        return uint32_t(dy[ri.base + ki.off]);
+    }
     __device__ __forceinline__ uint32_t operator()(int64_t r, int64_t k) const {
         const int64_t ohw = g.OH * g.OW;
         const int64_t n = k / ohw, p = k - n * ohw;

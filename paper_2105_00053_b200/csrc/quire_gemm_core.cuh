@@ -104,7 +104,7 @@ struct FetchRowMajor {  // X[r][k] = p[r*ld + k]
     const CodeT* p;
     int64_t ld;
     static constexpr bool kRowFastest = false;
-    static constexpr bool kVecK = true, kVecR = false;
+    static constexpr bool kVecK = true, kVecR = false, kSep = false;
     __device__ __forceinline__ const CodeT* ptr(int64_t r, int64_t k) const { return p + r * ld + k; }
     __device__ __forceinline__ uint32_t operator()(int64_t r, int64_t k) const {
         return uint32_t(p[r * ld + k]);
@@ -115,7 +115,7 @@ struct FetchColMajor {  // X[r][k] = p[k*ld + r]
     const CodeT* p;
     int64_t ld;
     static constexpr bool kRowFastest = true;
-    static constexpr bool kVecK = false, kVecR = true;
+    static constexpr bool kVecK = false, kVecR = true, kSep = false;
     __device__ __forceinline__ const CodeT* ptr(int64_t r, int64_t k) const { return p + k * ld + r; }
     __device__ __forceinline__ uint32_t operator()(int64_t r, int64_t k) const {
         return uint32_t(p[k * ld + r]);
@@ -199,6 +199,29 @@ __global__ void __launch_bounds__(256) pack_kernel(Fetch fetch, int64_t rows_tot
                 }
 #pragma unroll
                 for (int j = 0; j < VE; ++j) tile[(v * VE + j) * LD + k] = vals[j];
+            }
+        } else if constexpr (Fetch::kSep) {
+            // Separable gathers (im2col & co): the index decomposition of a row
+            // and of a k is computed once per pass into shared memory; each
+            // element is then a few adds, two range tests and one load.
+            __shared__ typename Fetch::RI rinfo[ROWS];
+            __shared__ typename Fetch::KI kinfo[KW];
+            for (int r = threadIdx.x; r < ROWS; r += blockDim.x)
+                rinfo[r] = fetch.row(r0 + r < rows_total ? r0 + r : 0);
+            for (int k = threadIdx.x; k < KW; k += blockDim.x)
+                kinfo[k] = fetch.kin(k0 + k < K ? k0 + k : 0);
+            __syncthreads();
+            for (int i = threadIdx.x; i < ROWS * KW; i += blockDim.x) {
+                int r, k;
+                if constexpr (Fetch::kRowFastest) {
+                    k = i / ROWS;
+                    r = i % ROWS;
+                } else {
+                    r = i / KW;
+                    k = i % KW;
+                }
+                const bool in = (r0 + r < rows_total) && (k0 + k < K);
+                tile[r * LD + k] = in ? CodeT(fetch.at(rinfo[r], kinfo[k])) : CodeT(0);
             }
         } else if constexpr (!Fetch::kRowFastest) {
             for (int i = threadIdx.x; i < ROWS * KW; i += blockDim.x) {
