@@ -147,6 +147,24 @@ int pnn_pack_round(int nbits, int es, const int32_t* neg, const int32_t* scale,
                    const uint64_t* sig, const int32_t* sticky, int64_t n, uint32_t* codes,
                    void* stream);
 
+/* ---- non-quire posit path (use_quire = false) -----------------------------
+ * One correctly rounded posit multiply and add per term in the reference's
+ * term order: matmul_seq / conv_seq / gather_seq(_sum), tensor_ops.cpp:145-164,
+ * 232-264, 302-335.  Device pointers to packed codes; one thread per output. */
+int pnn_matmul_seq(int nbits, int es, const void* A, const void* B, void* C, int64_t M, int64_t N,
+                   int64_t K, void* stream);
+int pnn_conv2d_fwd_seq(int nbits, int es, const void* x, int64_t N, int64_t C, int64_t H, int64_t W,
+                       const void* w, int64_t F, int64_t KH, int64_t KW, const void* bias,
+                       int stride, int pad, void* y, void* stream);
+int pnn_conv2d_dgrad_seq(int nbits, int es, const void* dy, int64_t N, int64_t F, int64_t OH,
+                         int64_t OW, const void* w, int64_t C, int64_t KH, int64_t KW, int64_t H,
+                         int64_t W, int stride, int pad, void* dx, void* stream);
+int pnn_conv2d_wgrad_seq(int nbits, int es, const void* dy, int64_t N, int64_t F, int64_t OH,
+                         int64_t OW, const void* x, int64_t C, int64_t H, int64_t W, int64_t KH,
+                         int64_t KW, int stride, int pad, void* dw, void* stream);
+int pnn_bias_grad_seq(int nbits, int es, const void* dy, int64_t N, int64_t F, int64_t P, void* db,
+                      void* stream);
+
 /* ---- data-parallel quire-word reduction --------------
  * Raw W-bit quire words (16 bytes each) + NaR bytes -> int64 lanes
  * [n][L+1] of 60-bit digits (L = pnn_quire_lanes) plus a NaR lane, ready for

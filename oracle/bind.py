@@ -253,6 +253,55 @@ class Restatement(_Base):
                                                  _p(dx)), "maxpool2d_backward")
         return dx.reshape(x_shape)
 
+    # -- non-quire sequential kernels (use_quire=false) --
+    def matmul_seq(self, n, es, A, B):
+        A, B = _codes(A), _codes(B)
+        m, k = A.shape
+        nn = B.shape[1]
+        Cm = np.zeros((m, nn), np.uint64)
+        self._chk(self.lib.po_matmul_seq(n, es, _p(A), _p(B), _p(Cm), i64(m), i64(k), i64(nn)), "matmul_seq")
+        return Cm
+
+    def conv2d_seq(self, n, es, x, w, bias, stride, pad):
+        x, w = _codes(x), _codes(w)
+        N, Cc, H, W = x.shape
+        F, _, KH, KW = w.shape
+        OH, OW = (H + 2 * pad - KH) // stride + 1, (W + 2 * pad - KW) // stride + 1
+        y = np.zeros((N, F, OH, OW), np.uint64)
+        b = _codes(bias) if bias is not None else None
+        self._chk(self.lib.po_conv2d_seq(n, es, _p(x), i64(N), i64(Cc), i64(H), i64(W), _p(w), i64(F),
+                                         i64(KH), i64(KW), _p(b), stride, pad, _p(y)), "conv2d_seq")
+        return y
+
+    def conv2d_input_grad_seq(self, n, es, dy, w, x_shape, stride, pad):
+        dy, w = _codes(dy), _codes(w)
+        N, F, OH, OW = dy.shape
+        _, Cc, KH, KW = w.shape
+        H, W = x_shape[2], x_shape[3]
+        dx = np.zeros((N, Cc, H, W), np.uint64)
+        self._chk(self.lib.po_conv2d_input_grad_seq(n, es, _p(dy), i64(N), i64(F), i64(OH), i64(OW), _p(w),
+                                                    i64(Cc), i64(KH), i64(KW), i64(H), i64(W), stride, pad,
+                                                    _p(dx)), "conv2d_input_grad_seq")
+        return dx
+
+    def conv2d_weight_grad_seq(self, n, es, dy, x, w_shape, stride, pad):
+        dy, x = _codes(dy), _codes(x)
+        N, F, OH, OW = dy.shape
+        _, Cc, H, W = x.shape
+        KH, KW = w_shape[2], w_shape[3]
+        dw = np.zeros((F, Cc, KH, KW), np.uint64)
+        self._chk(self.lib.po_conv2d_weight_grad_seq(n, es, _p(dy), i64(N), i64(F), i64(OH), i64(OW), _p(x),
+                                                     i64(Cc), i64(H), i64(W), i64(KH), i64(KW), stride, pad,
+                                                     _p(dw)), "conv2d_weight_grad_seq")
+        return dw
+
+    def bias_grad_seq(self, n, es, dy3):
+        dy3 = _codes(dy3)
+        N, F, P = dy3.shape
+        db = np.zeros((F,), np.uint64)
+        self._chk(self.lib.po_bias_grad_seq(n, es, _p(dy3), i64(N), i64(F), i64(P), _p(db)), "bias_grad_seq")
+        return db
+
     def quire_words(self, q) -> tuple[int, bool]:
         """(W-bit quire value as a Python int, NaR flag) of a restatement quire."""
         buf = (C.c_uint64 * 16)()
@@ -355,7 +404,7 @@ class Reference(_Base):
         t = self.lib.ref_time_matmul(n, es, _p(A), _p(B), _p(Cm), i64(m), i64(k), i64(nn), threads)
         return t, Cm
 
-    def conv2d(self, n, es, x, w, bias, stride, pad, threads: int = 1):
+    def conv2d(self, n, es, x, w, bias, stride, pad, threads: int = 1, use_quire: bool = True):
         x, w = _codes(x), _codes(w)
         N, Cc, H, W = x.shape
         F, _, KH, KW = w.shape
@@ -363,10 +412,10 @@ class Reference(_Base):
         y = np.zeros((N, F, OH, OW), np.uint64)
         b = _codes(bias) if bias is not None else None
         self._chk(self.lib.ref_conv2d(n, es, _p(x), i64(N), i64(Cc), i64(H), i64(W), _p(w), i64(F),
-                                      i64(KH), i64(KW), _p(b), stride, pad, 1, threads, _p(y)))
+                                      i64(KH), i64(KW), _p(b), stride, pad, int(use_quire), threads, _p(y)))
         return y
 
-    def conv2d_input_grad(self, n, es, dy, w, x_shape, stride, pad, threads: int = 1):
+    def conv2d_input_grad(self, n, es, dy, w, x_shape, stride, pad, threads: int = 1, use_quire: bool = True):
         dy, w = _codes(dy), _codes(w)
         N, F, OH, OW = dy.shape
         _, Cc, KH, KW = w.shape
@@ -374,10 +423,10 @@ class Reference(_Base):
         dx = np.zeros((N, Cc, H, W), np.uint64)
         self._chk(self.lib.ref_conv2d_input_grad(n, es, _p(dy), i64(N), i64(F), i64(OH), i64(OW),
                                                  _p(w), i64(Cc), i64(KH), i64(KW), i64(H), i64(W),
-                                                 stride, pad, 1, threads, _p(dx)))
+                                                 stride, pad, int(use_quire), threads, _p(dx)))
         return dx
 
-    def conv2d_weight_grad(self, n, es, dy, x, w_shape, stride, pad, threads: int = 1):
+    def conv2d_weight_grad(self, n, es, dy, x, w_shape, stride, pad, threads: int = 1, use_quire: bool = True):
         dy, x = _codes(dy), _codes(x)
         N, F, OH, OW = dy.shape
         _, Cc, H, W = x.shape
@@ -385,22 +434,22 @@ class Reference(_Base):
         dw = np.zeros((F, Cc, KH, KW), np.uint64)
         self._chk(self.lib.ref_conv2d_weight_grad(n, es, _p(dy), i64(N), i64(F), i64(OH), i64(OW),
                                                   _p(x), i64(Cc), i64(H), i64(W), i64(KH), i64(KW),
-                                                  stride, pad, 1, threads, _p(dw)))
+                                                  stride, pad, int(use_quire), threads, _p(dw)))
         return dw
 
-    def conv2d_bias_grad(self, n, es, dy):
+    def conv2d_bias_grad(self, n, es, dy, use_quire: bool = True):
         dy = _codes(dy)
         N, F, OH, OW = dy.shape
         db = np.zeros((F,), np.uint64)
-        self._chk(self.lib.ref_conv2d_bias_grad(n, es, _p(dy), i64(N), i64(F), i64(OH), i64(OW), 1,
+        self._chk(self.lib.ref_conv2d_bias_grad(n, es, _p(dy), i64(N), i64(F), i64(OH), i64(OW), int(use_quire),
                                                 _p(db)))
         return db
 
-    def column_sum(self, n, es, x):
+    def column_sum(self, n, es, x, use_quire: bool = True):
         x = _codes(x)
         B, N = x.shape
         out = np.zeros((N,), np.uint64)
-        self._chk(self.lib.ref_column_sum(n, es, _p(x), i64(B), i64(N), 1, _p(out)))
+        self._chk(self.lib.ref_column_sum(n, es, _p(x), i64(B), i64(N), int(use_quire), _p(out)))
         return out
 
     def maxpool2d(self, n, es, x, k, stride):

@@ -795,3 +795,117 @@ uint64_t po_round_words(int nbits, int es, const uint64_t* words, int nwords) {
     for (int i = 0; i < nwords && i < WL; ++i) w.w[i] = words[i];
     return wide_round(nbits, es, &w, po_quire_bits(nbits, es), -2 * po_max_scale(nbits, es));
 }
+
+/* ------------------------------------------- non-quire sequential kernels */
+/* matmul_seq / conv_seq / gather_seq(_sum), tensor_ops.cpp:145-164, 232-264,
+ * 302-335: one correctly rounded multiply and add per term, in order. */
+
+#define SEQ_ACC(acc, first, p) do { acc = first ? (p) : OP_ADD(acc, (p)); first = 0; } while (0)
+
+int po_matmul_seq(int nbits, int es, const uint64_t* A, const uint64_t* B, uint64_t* C,
+                  int64_t m, int64_t k, int64_t n) {
+    if (!fmt_ok(nbits, es)) return 1;
+    for (int64_t i = 0; i < m; ++i)
+        for (int64_t j = 0; j < n; ++j) {
+            if (k == 0) { C[i * n + j] = 0; continue; }
+            uint64_t acc = OP_MUL(A[i * k], B[j]);
+            for (int64_t t = 1; t < k; ++t) acc = OP_ADD(acc, OP_MUL(A[i * k + t], B[t * n + j]));
+            C[i * n + j] = acc;
+        }
+    return 0;
+}
+
+int po_conv2d_seq(int nbits, int es, const uint64_t* x, int64_t N, int64_t C, int64_t H, int64_t W,
+                  const uint64_t* w, int64_t F, int64_t KH, int64_t KW, const uint64_t* bias,
+                  int stride, int pad, uint64_t* y) {
+    if (!fmt_ok(nbits, es) || stride < 1 || pad < 0) return 1;
+    int64_t OH = (H + 2 * pad - KH) / stride + 1, OW = (W + 2 * pad - KW) / stride + 1;
+    for (int64_t nn = 0; nn < N; ++nn)
+        for (int64_t ff = 0; ff < F; ++ff)
+            for (int64_t oy = 0; oy < OH; ++oy)
+                for (int64_t ox = 0; ox < OW; ++ox) {
+                    uint64_t acc = 0;
+                    int first = 1;
+                    for (int64_t c = 0; c < C; ++c)
+                        for (int64_t ky = 0; ky < KH; ++ky)
+                            for (int64_t kx = 0; kx < KW; ++kx) {
+                                int64_t iy = oy * stride + ky - pad, ix = ox * stride + kx - pad;
+                                uint64_t xv = (iy < 0 || iy >= H || ix < 0 || ix >= W)
+                                                  ? 0 : x[((nn * C + c) * H + iy) * W + ix];
+                                uint64_t p = OP_MUL(xv, w[((ff * C + c) * KH + ky) * KW + kx]);
+                                SEQ_ACC(acc, first, p);
+                            }
+                    if (bias) acc = OP_ADD(acc, bias[ff]);
+                    y[((nn * F + ff) * OH + oy) * OW + ox] = acc;
+                }
+    return 0;
+}
+
+int po_conv2d_input_grad_seq(int nbits, int es, const uint64_t* dy, int64_t N, int64_t F,
+                             int64_t OH, int64_t OW, const uint64_t* w, int64_t C, int64_t KH,
+                             int64_t KW, int64_t H, int64_t W, int stride, int pad, uint64_t* dx) {
+    if (!fmt_ok(nbits, es) || stride < 1 || pad < 0) return 1;
+    for (int64_t nn = 0; nn < N; ++nn)
+        for (int64_t c = 0; c < C; ++c)
+            for (int64_t y0 = 0; y0 < H; ++y0)
+                for (int64_t x0 = 0; x0 < W; ++x0) {
+                    int64_t iy = y0 + pad, ix = x0 + pad;
+                    uint64_t acc = 0;
+                    int first = 1;
+                    for (int64_t ff = 0; ff < F; ++ff)
+                        for (int64_t ky = 0; ky < KH; ++ky) {
+                            int64_t ty = iy - ky;
+                            if (ty < 0 || ty % stride) continue;
+                            int64_t oy = ty / stride;
+                            if (oy >= OH) continue;
+                            for (int64_t kx = 0; kx < KW; ++kx) {
+                                int64_t tx = ix - kx;
+                                if (tx < 0 || tx % stride) continue;
+                                int64_t ox = tx / stride;
+                                if (ox >= OW) continue;
+                                uint64_t p = OP_MUL(dy[((nn * F + ff) * OH + oy) * OW + ox],
+                                                    w[((ff * C + c) * KH + ky) * KW + kx]);
+                                SEQ_ACC(acc, first, p);
+                            }
+                        }
+                    dx[((nn * C + c) * H + y0) * W + x0] = acc;
+                }
+    return 0;
+}
+
+int po_conv2d_weight_grad_seq(int nbits, int es, const uint64_t* dy, int64_t N, int64_t F,
+                              int64_t OH, int64_t OW, const uint64_t* x, int64_t C, int64_t H,
+                              int64_t W, int64_t KH, int64_t KW, int stride, int pad, uint64_t* dw) {
+    if (!fmt_ok(nbits, es) || stride < 1 || pad < 0) return 1;
+    for (int64_t ff = 0; ff < F; ++ff)
+        for (int64_t c = 0; c < C; ++c)
+            for (int64_t ky = 0; ky < KH; ++ky)
+                for (int64_t kx = 0; kx < KW; ++kx) {
+                    uint64_t acc = 0;
+                    int first = 1;
+                    for (int64_t nn = 0; nn < N; ++nn)
+                        for (int64_t oy = 0; oy < OH; ++oy)
+                            for (int64_t ox = 0; ox < OW; ++ox) {
+                                int64_t iy = oy * stride + ky - pad, ix = ox * stride + kx - pad;
+                                uint64_t xv = (iy < 0 || iy >= H || ix < 0 || ix >= W)
+                                                  ? 0 : x[((nn * C + c) * H + iy) * W + ix];
+                                uint64_t p = OP_MUL(dy[((nn * F + ff) * OH + oy) * OW + ox], xv);
+                                SEQ_ACC(acc, first, p);
+                            }
+                    dw[((ff * C + c) * KH + ky) * KW + kx] = acc;
+                }
+    return 0;
+}
+
+int po_bias_grad_seq(int nbits, int es, const uint64_t* dy, int64_t N, int64_t F, int64_t P,
+                     uint64_t* db) {
+    if (!fmt_ok(nbits, es)) return 1;
+    for (int64_t ff = 0; ff < F; ++ff) {
+        uint64_t acc = 0;
+        int first = 1;
+        for (int64_t nn = 0; nn < N; ++nn)
+            for (int64_t p = 0; p < P; ++p) SEQ_ACC(acc, first, dy[(nn * F + ff) * P + p]);
+        db[ff] = acc;
+    }
+    return 0;
+}

@@ -69,6 +69,22 @@ uint64_t po_quire_to_posit(const po_quire* q);
 /* Raw quire words (little-endian uint64 limbs, W bits, two's complement). */
 int po_quire_words(const po_quire* q, uint64_t* out, int max_words, int* nar);
 
+/* Non-quire sequential kernels (use_quire=false): tensor_ops.cpp:145-164,
+ * 232-264, 302-335 -- one rounding per multiply and per add, in order. */
+int po_matmul_seq(int nbits, int es, const uint64_t* A, const uint64_t* B, uint64_t* C,
+                  int64_t m, int64_t k, int64_t n);
+int po_conv2d_seq(int nbits, int es, const uint64_t* x, int64_t N, int64_t C, int64_t H, int64_t W,
+                  const uint64_t* w, int64_t F, int64_t KH, int64_t KW, const uint64_t* bias,
+                  int stride, int pad, uint64_t* y);
+int po_conv2d_input_grad_seq(int nbits, int es, const uint64_t* dy, int64_t N, int64_t F,
+                             int64_t OH, int64_t OW, const uint64_t* w, int64_t C, int64_t KH,
+                             int64_t KW, int64_t H, int64_t W, int stride, int pad, uint64_t* dx);
+int po_conv2d_weight_grad_seq(int nbits, int es, const uint64_t* dy, int64_t N, int64_t F,
+                              int64_t OH, int64_t OW, const uint64_t* x, int64_t C, int64_t H,
+                              int64_t W, int64_t KH, int64_t KW, int stride, int pad, uint64_t* dw);
+int po_bias_grad_seq(int nbits, int es, const uint64_t* dy, int64_t N, int64_t F, int64_t P,
+                     uint64_t* db);
+
 /* Round externally summed W-bit quire words once (data-parallel reduction). */
 uint64_t po_round_words(int nbits, int es, const uint64_t* words, int nwords);
 

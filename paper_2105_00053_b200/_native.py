@@ -60,6 +60,14 @@ _SIGS = {
     "pnn_quire_lanes": (C.c_int, [C.c_int, C.c_int]),
     "pnn_quire_to_lanes": (C.c_int, [C.c_int, C.c_int, _vp, _vp, _i64, _vp, _vp]),
     "pnn_lanes_to_posit": (C.c_int, [C.c_int, C.c_int, _vp, _i64, _vp, _vp, _vp]),
+    "pnn_matmul_seq": (C.c_int, [C.c_int, C.c_int, _vp, _vp, _vp, _i64, _i64, _i64, _vp]),
+    "pnn_conv2d_fwd_seq": (C.c_int, [C.c_int, C.c_int, _vp] + [_i64] * 4 + [_vp] + [_i64] * 3 +
+                           [_vp, C.c_int, C.c_int, _vp, _vp]),
+    "pnn_conv2d_dgrad_seq": (C.c_int, [C.c_int, C.c_int, _vp] + [_i64] * 4 + [_vp] + [_i64] * 5 +
+                             [C.c_int, C.c_int, _vp, _vp]),
+    "pnn_conv2d_wgrad_seq": (C.c_int, [C.c_int, C.c_int, _vp] + [_i64] * 4 + [_vp] + [_i64] * 5 +
+                             [C.c_int, C.c_int, _vp, _vp]),
+    "pnn_bias_grad_seq": (C.c_int, [C.c_int, C.c_int, _vp, _i64, _i64, _i64, _vp, _vp]),
     "pnn_probe_int8_peak": (C.c_int, [C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
 }
 

@@ -216,7 +216,7 @@ __device__ __forceinline__ uint32_t p_from_int64(const PositFmt& f, int64_t v) {
 
 // exp_posit: k = round(x * log2e); r = x - k*ln2; degree-10 Horner in posit
 // ops with 1/k! quantized by from_float64; ldexp by k.
-__device__ __noinline__ uint32_t p_exp(const PositFmt& f, uint32_t x) {
+static __device__ __noinline__ uint32_t p_exp(const PositFmt& f, uint32_t x) {
     x &= code_mask(f);
     if (x == nar_of(f)) return x;
     if (x == 0) return p_from_int64(f, 1);
@@ -239,7 +239,7 @@ __device__ __noinline__ uint32_t p_exp(const PositFmt& f, uint32_t x) {
 
 // log_posit: x = m * 2^s, m in [1, 1.5) after one halving, 2*atanh series
 // in t = (m-1)/(m+1), 8 terms with 1/(2k+1) quantized by from_float64.
-__device__ __noinline__ uint32_t p_log(const PositFmt& f, uint32_t x) {
+static __device__ __noinline__ uint32_t p_log(const PositFmt& f, uint32_t x) {
     x &= code_mask(f);
     const uint32_t nar = nar_of(f);
     if (x == nar || x == 0 || (x & nar)) return nar;

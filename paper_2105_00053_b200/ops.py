@@ -129,12 +129,15 @@ def quire_gemm(cfg, A, B, out=None, max_kblocks: int | None = None):
 def matmul(a, b, use_quire: bool = True, pool=None, cfg=None):
     """tensor_ops.hpp:28-29.  ``pool`` is accepted and ignored (results are
     worker-count invariant in the reference, tensor_ops.hpp:12-13)."""
-    if not use_quire:
-        raise NotImplementedError("non-quire sequential-rounding matmul is outside this path "
-                                  "(SURVEY.md §8f item 1)")
     if cfg is None:
         raise _native.PnnInvalidArgument(1, "matmul: posit config required")
     cfg = _cfg(cfg)
+    if not use_quire:  # sequential rounding per term (tensor_ops.cpp:145-164)
+        if isinstance(a, np.ndarray):
+            d = matmul_seq(cfg, torch.from_numpy(np.ascontiguousarray(a).astype(cfg.np_code_dtype)).cuda(),
+                           torch.from_numpy(np.ascontiguousarray(b).astype(cfg.np_code_dtype)).cuda())
+            return d.cpu().numpy().astype(np.int64).astype(np.uint64)
+        return matmul_seq(cfg, a, b)
     if isinstance(a, np.ndarray):
         a = np.ascontiguousarray(a, dtype=np.uint64)
         b = np.ascontiguousarray(b, dtype=np.uint64)
@@ -149,6 +152,21 @@ def matmul(a, b, use_quire: bool = True, pool=None, cfg=None):
                                                     c.ctypes.data, M, K, N))
         return c
     return quire_gemm(cfg, a, b)
+
+
+def matmul_seq(cfg, A, B):
+    """Non-quire posit matmul (matmul_seq, tensor_ops.cpp:145-164) on device codes."""
+    cfg = _cfg(cfg)
+    if A.dim() != 2 or B.dim() != 2 or A.shape[1] != B.shape[0]:
+        raise _native.PnnInvalidArgument(1, "matmul: bad shapes")
+    _check_codes(cfg, A, B)
+    A, B = A.contiguous(), B.contiguous()
+    M, K = A.shape
+    N = B.shape[1]
+    out = torch.empty((M, N), dtype=cfg.code_dtype, device=A.device)
+    _native.check(_native.lib().pnn_matmul_seq(cfg.nbits, cfg.es, A.data_ptr(), B.data_ptr(), out.data_ptr(),
+                                               M, N, K, _stream_ptr(A.device)))
+    return out
 
 
 def par_matmul(a, b, use_quire: bool, workers: int, cfg=None):
@@ -210,8 +228,6 @@ def _check_codes(cfg, *ts):
 
 def conv2d(cfg, x, w, bias, stride: int, pad: int, use_quire: bool = True, pool=None):
     """tensor_ops.hpp:34-35: y = round(conv(x_pad, w) + bias), bias inside the quire."""
-    if not use_quire:
-        raise NotImplementedError("non-quire conv is outside this path (SURVEY.md §8f)")
     cfg = _cfg(cfg)
     if x.dim() != 4 or w.dim() != 4:
         raise _native.PnnInvalidArgument(1, "conv2d: NCHW/FCKK tensors required")
@@ -224,6 +240,11 @@ def conv2d(cfg, x, w, bias, stride: int, pad: int, use_quire: bool = True, pool=
     F, _, KH, KW = w.shape
     OH, OW = (H + 2 * pad - KH) // stride + 1, (W + 2 * pad - KW) // stride + 1
     y = torch.empty((N, F, OH, OW), dtype=cfg.code_dtype, device=x.device)
+    if not use_quire:  # conv_seq, tensor_ops.cpp:232-264
+        _native.check(_native.lib().pnn_conv2d_fwd_seq(
+            cfg.nbits, cfg.es, x.data_ptr(), N, Cc, H, W, w.data_ptr(), F, KH, KW,
+            bias.data_ptr() if bias is not None else None, stride, pad, y.data_ptr(), _stream_ptr(x.device)))
+        return y
     ws = _ws.get(x.device, _conv_ws(0, cfg, N, Cc, H, W, F, KH, KW, stride, pad, bias is not None))
     _native.check(_native.lib().pnn_conv2d_fwd(
         cfg.nbits, cfg.es, x.data_ptr(), N, Cc, H, W, w.data_ptr(), F, KH, KW,
@@ -241,6 +262,11 @@ def conv2d_input_grad(cfg, dy, w, x_shape, stride: int, pad: int, use_quire: boo
     _, F, OH, OW = dy.shape
     _, _, KH, KW = w.shape
     dx = torch.empty((N, Cc, H, W), dtype=cfg.code_dtype, device=dy.device)
+    if not use_quire:  # gather_seq over the valid taps, tensor_ops.cpp:302-318, 539-560
+        _native.check(_native.lib().pnn_conv2d_dgrad_seq(
+            cfg.nbits, cfg.es, dy.data_ptr(), N, F, OH, OW, w.data_ptr(), Cc, KH, KW, H, W, stride, pad,
+            dx.data_ptr(), _stream_ptr(dy.device)))
+        return dx
     ws = _ws.get(dy.device, _conv_ws(1, cfg, N, Cc, H, W, F, KH, KW, stride, pad, False))
     _native.check(_native.lib().pnn_conv2d_dgrad(
         cfg.nbits, cfg.es, dy.data_ptr(), N, F, OH, OW, w.data_ptr(), Cc, KH, KW, H, W, stride, pad,
@@ -259,6 +285,13 @@ def conv2d_weight_grad(cfg, dy, x, w_shape, stride: int, pad: int, use_quire: bo
     _, Cc, H, W = x.shape
     KH, KW = int(w_shape[2]), int(w_shape[3])
     dw = torch.empty((F, Cc, KH, KW), dtype=cfg.code_dtype, device=dy.device)
+    if not use_quire:  # gather_seq over (n, oy, ox), tensor_ops.cpp:302-318, 586-600
+        if raw:
+            raise _native.PnnInvalidArgument(1, "raw quire words need use_quire=True")
+        _native.check(_native.lib().pnn_conv2d_wgrad_seq(
+            cfg.nbits, cfg.es, dy.data_ptr(), N, F, OH, OW, x.data_ptr(), Cc, H, W, KH, KW, stride, pad,
+            dw.data_ptr(), _stream_ptr(dy.device)))
+        return dw
     words = nar = None
     if raw:
         words = torch.empty((F, Cc, KH, KW, 2), dtype=torch.int64, device=dy.device)
@@ -271,9 +304,13 @@ def conv2d_weight_grad(cfg, dy, x, w_shape, stride: int, pad: int, use_quire: bo
     return (dw, words, nar) if raw else dw
 
 
-def _bias_grad(cfg, dy3, raw=False):
+def _bias_grad(cfg, dy3, raw=False, use_quire=True):
     N, F, P = dy3.shape
     db = torch.empty((F,), dtype=cfg.code_dtype, device=dy3.device)
+    if not use_quire:  # gather_seq_sum, tensor_ops.cpp:320-335
+        _native.check(_native.lib().pnn_bias_grad_seq(cfg.nbits, cfg.es, dy3.data_ptr(), N, F, P, db.data_ptr(),
+                                                      _stream_ptr(dy3.device)))
+        return db
     words = nar = None
     if raw:
         words = torch.empty((F, 2), dtype=torch.int64, device=dy3.device)
@@ -295,7 +332,7 @@ def conv2d_bias_grad(cfg, dy, use_quire: bool = True, raw: bool = False):
     if dy.dim() != 4:
         raise _native.PnnInvalidArgument(1, "conv2d_bias_grad: bad rank")
     N, F, OH, OW = dy.shape
-    return _bias_grad(cfg, dy.contiguous().view(N, F, OH * OW), raw)
+    return _bias_grad(cfg, dy.contiguous().view(N, F, OH * OW), raw, use_quire)
 
 
 def column_sum(cfg, x, use_quire: bool = True, raw: bool = False):
@@ -305,7 +342,7 @@ def column_sum(cfg, x, use_quire: bool = True, raw: bool = False):
     if x.dim() != 2:
         raise _native.PnnInvalidArgument(1, "column_sum: rank-2 tensor required")
     B, N = x.shape
-    return _bias_grad(cfg, x.contiguous().view(B, N, 1), raw)
+    return _bias_grad(cfg, x.contiguous().view(B, N, 1), raw, use_quire)
 
 
 # ---- elementwise kernels of the training step -------------------------------

