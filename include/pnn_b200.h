@@ -124,11 +124,19 @@ int pnn_softmax_xent(int nbits, int es, const void* logits, const int32_t* label
 int pnn_sgd_step(int opt_nbits, int opt_es, void* master, int g_nbits, int g_es, const void* grad,
                  int64_t n, uint32_t lr_code, int c1_nbits, int c1_es, void* copy1, int c2_nbits,
                  int c2_es, void* copy2, void* stream);
+/* avgpool2d / avgpool2d_backward (tensor_ops.cpp:672-720): window sum (quire
+ * when use_quire, else an add chain) times the caller-quantized reciprocal. */
+int pnn_avgpool2d_fwd(int nbits, int es, const void* x, int64_t N, int64_t C, int64_t H,
+                      int64_t W, int k, int stride, int use_quire, uint32_t recip_code, void* y,
+                      void* stream);
+int pnn_avgpool2d_bwd(int nbits, int es, const void* dy, int64_t N, int64_t C, int64_t H,
+                      int64_t W, int k, int stride, uint32_t recip_code, void* dx, void* stream);
 /* Data ingestion: from_float64 (posit.cpp:502-508) of device doubles into
  * packed codes -- inputs, labels-free data and initial weights. */
 int pnn_from_float64(int nbits, int es, const double* x, void* codes, int64_t n, void* stream);
 /* Scalar ALU on device (parity): op 0 add 1 sub 2 mul 3 div 4 exp 5 log
- * 6 round_to_int 7 ldexp(a, (int)b) 8 compare 9 to_int64 (low 32 bits). */
+ * 6 round_to_int 7 ldexp(a, (int)b) 8 compare 9 to_int64 (low 32 bits) 10 tanh
+ * 11 sigmoid (posit_math.cpp:109-130). */
 int pnn_scalar_eval(int nbits, int es, int op, const uint32_t* a, const uint32_t* b,
                     uint32_t* out, int64_t n, void* stream);
 

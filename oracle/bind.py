@@ -74,6 +74,8 @@ class _Base:
             ("from_int64", C.c_uint64, [C.c_int, C.c_int, C.c_int64]),
             ("exp", C.c_uint64, [C.c_int, C.c_int, C.c_uint64]),
             ("log", C.c_uint64, [C.c_int, C.c_int, C.c_uint64]),
+            ("tanh", C.c_uint64, [C.c_int, C.c_int, C.c_uint64]),
+            ("sigmoid", C.c_uint64, [C.c_int, C.c_int, C.c_uint64]),
             ("quire_new", C.c_void_p, [C.c_int, C.c_int]),
             ("quire_free", None, [C.c_void_p]),
             ("quire_clear", None, [C.c_void_p]),
@@ -122,6 +124,33 @@ class _Base:
 
     def log(self, n, es, code):
         return self._f("log")(n, es, int(code))
+
+    def tanh(self, n, es, code):
+        return self._f("tanh")(n, es, int(code))
+
+    def sigmoid(self, n, es, code):
+        return self._f("sigmoid")(n, es, int(code))
+
+    def avgpool2d(self, n, es, x, k, stride, use_quire, recip):
+        x = _codes(x)
+        N, Cc, H, W = x.shape
+        OH, OW = (H - k) // stride + 1, (W - k) // stride + 1
+        y = np.zeros((N, Cc, OH, OW), np.uint64)
+        rc = self._f("avgpool2d")(n, es, _p(x), i64(N), i64(Cc), i64(H), i64(W), k, stride, int(use_quire),
+                                  C.c_uint64(int(recip)), _p(y))
+        if rc:
+            raise ValueError("avgpool2d rejected its arguments")
+        return y
+
+    def avgpool2d_backward(self, n, es, dy, k, stride, x_shape, recip):
+        dy = _codes(dy)
+        N, Cc, H, W = x_shape
+        dx = np.zeros(tuple(x_shape), np.uint64)
+        rc = self._f("avgpool2d_backward")(n, es, _p(dy), i64(N), i64(Cc), i64(H), i64(W), k, stride,
+                                           C.c_uint64(int(recip)), _p(dx))
+        if rc:
+            raise ValueError("avgpool2d_backward rejected its arguments")
+        return dx
 
     def quire(self, n, es):
         return _Quire(self, n, es)

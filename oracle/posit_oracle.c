@@ -909,3 +909,76 @@ int po_bias_grad_seq(int nbits, int es, const uint64_t* dy, int64_t N, int64_t F
     }
     return 0;
 }
+
+/* tanh_posit / sigmoid_posit, posit_math.cpp:109-130 (posit-op sequences). */
+uint64_t po_tanh(int nbits, int es, uint64_t x) {
+    uint64_t m = pmask(nbits), nar = nar_of(nbits);
+    x &= m;
+    if (x == nar || x == 0) return x;
+    int neg = (int)((x >> (nbits - 1)) & 1);
+    uint64_t ax = neg ? ((~x + 1) & m) : x;
+    uint64_t one = po_from_int64(nbits, es, 1);
+    uint64_t t2 = po_ldexp(nbits, es, ax, 1);
+    uint64_t t = po_exp(nbits, es, (~t2 + 1) & m);
+    uint64_t r = OP_DIV(OP_SUB(one, t), OP_ADD(one, t));
+    return neg ? ((~r + 1) & m) : r;
+}
+
+uint64_t po_sigmoid(int nbits, int es, uint64_t x) {
+    uint64_t m = pmask(nbits), nar = nar_of(nbits);
+    x &= m;
+    if (x == nar) return x;
+    uint64_t one = po_from_int64(nbits, es, 1);
+    if (!((x >> (nbits - 1)) & 1)) {
+        uint64_t t = po_exp(nbits, es, (~x + 1) & m);
+        return OP_DIV(one, OP_ADD(one, t));
+    }
+    uint64_t t = po_exp(nbits, es, x);
+    return OP_DIV(t, OP_ADD(one, t));
+}
+
+/* avgpool2d / avgpool2d_backward, tensor_ops.cpp:672-720. */
+int po_avgpool2d(int nbits, int es, const uint64_t* x, int64_t N, int64_t C, int64_t H, int64_t W,
+                 int k, int stride, int use_quire, uint64_t recip, uint64_t* y) {
+    if (H < k || W < k) return 1;
+    int64_t OH = (H - k) / stride + 1, OW = (W - k) / stride + 1;
+    for (int64_t nc = 0; nc < N * C; ++nc)
+        for (int64_t oy = 0; oy < OH; ++oy)
+            for (int64_t ox = 0; ox < OW; ++ox) {
+                uint64_t sum = 0;
+                if (use_quire) {
+                    po_quire* q = po_quire_new(nbits, es);
+                    for (int ky = 0; ky < k; ++ky)
+                        for (int kx = 0; kx < k; ++kx)
+                            po_quire_add_posit(q, x[nc * H * W + (oy * stride + ky) * W + ox * stride + kx]);
+                    sum = po_quire_to_posit(q);
+                    po_quire_free(q);
+                } else {
+                    int first = 1;
+                    for (int ky = 0; ky < k; ++ky)
+                        for (int kx = 0; kx < k; ++kx) {
+                            uint64_t v = x[nc * H * W + (oy * stride + ky) * W + ox * stride + kx];
+                            SEQ_ACC(sum, first, v);
+                        }
+                }
+                y[(nc * OH + oy) * OW + ox] = OP_MUL(sum, recip);
+            }
+    return 0;
+}
+
+int po_avgpool2d_backward(int nbits, int es, const uint64_t* dy, int64_t N, int64_t C, int64_t H,
+                          int64_t W, int k, int stride, uint64_t recip, uint64_t* dx) {
+    int64_t OH = (H - k) / stride + 1, OW = (W - k) / stride + 1;
+    memset(dx, 0, sizeof(uint64_t) * (size_t)(N * C * H * W));
+    for (int64_t nc = 0; nc < N * C; ++nc)
+        for (int64_t oy = 0; oy < OH; ++oy)
+            for (int64_t ox = 0; ox < OW; ++ox) {
+                uint64_t g = OP_MUL(dy[(nc * OH + oy) * OW + ox], recip);
+                for (int ky = 0; ky < k; ++ky)
+                    for (int kx = 0; kx < k; ++kx) {
+                        int64_t t = nc * H * W + (oy * stride + ky) * W + ox * stride + kx;
+                        dx[t] = OP_ADD(dx[t], g);
+                    }
+            }
+    return 0;
+}

@@ -85,6 +85,15 @@ int po_conv2d_weight_grad_seq(int nbits, int es, const uint64_t* dy, int64_t N, 
 int po_bias_grad_seq(int nbits, int es, const uint64_t* dy, int64_t N, int64_t F, int64_t P,
                      uint64_t* db);
 
+/* tanh_posit / sigmoid_posit (posit_math.cpp:109-130) and avg-pool
+ * (tensor_ops.cpp:672-720) -- SURVEY.md §8f item 2. */
+uint64_t po_tanh(int nbits, int es, uint64_t x);
+uint64_t po_sigmoid(int nbits, int es, uint64_t x);
+int po_avgpool2d(int nbits, int es, const uint64_t* x, int64_t N, int64_t C, int64_t H, int64_t W,
+                 int k, int stride, int use_quire, uint64_t recip, uint64_t* y);
+int po_avgpool2d_backward(int nbits, int es, const uint64_t* dy, int64_t N, int64_t C, int64_t H,
+                          int64_t W, int k, int stride, uint64_t recip, uint64_t* dx);
+
 /* Round externally summed W-bit quire words once (data-parallel reduction). */
 uint64_t po_round_words(int nbits, int es, const uint64_t* words, int nwords);
 

@@ -141,6 +141,14 @@ uint64_t ref_log(int nbits, int es, uint64_t code) {
     return log_posit(PositValue{cfg_of(nbits, es), code}).bits;
 }
 
+uint64_t ref_tanh(int nbits, int es, uint64_t code) {
+    return tanh_posit(PositValue{cfg_of(nbits, es), code}).bits;
+}
+
+uint64_t ref_sigmoid(int nbits, int es, uint64_t code) {
+    return sigmoid_posit(PositValue{cfg_of(nbits, es), code}).bits;
+}
+
 uint64_t ref_from_int64(int nbits, int es, int64_t v) {
     return from_int64(v, cfg_of(nbits, es)).bits;
 }
@@ -265,6 +273,23 @@ int ref_maxpool2d_backward(int nbits, int es, const uint64_t* dy, int64_t ny,
         Tensor dyt = make_tensor(nbits, es, {ny}, dy);
         std::vector<int64_t> am(argmax, argmax + ny);
         copy_out(maxpool2d_backward(dyt, am, {N, C, H, W}), dx);
+    });
+}
+
+int ref_avgpool2d(int nbits, int es, const uint64_t* x, int64_t N, int64_t C, int64_t H,
+                  int64_t W, int k, int stride, int use_quire, uint64_t recip, uint64_t* y) {
+    return guarded([&] {
+        Tensor xt = make_tensor(nbits, es, {N, C, H, W}, x);
+        copy_out(avgpool2d(xt, k, stride, use_quire != 0, recip, nullptr), y);
+    });
+}
+
+int ref_avgpool2d_backward(int nbits, int es, const uint64_t* dy, int64_t N, int64_t C, int64_t H,
+                           int64_t W, int k, int stride, uint64_t recip, uint64_t* dx) {
+    return guarded([&] {
+        const int64_t OH = (H - k) / stride + 1, OW = (W - k) / stride + 1;
+        Tensor dyt = make_tensor(nbits, es, {N, C, OH, OW}, dy);
+        copy_out(avgpool2d_backward(dyt, k, stride, {N, C, H, W}, recip, nullptr), dx);
     });
 }
 

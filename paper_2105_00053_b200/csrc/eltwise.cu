@@ -192,6 +192,59 @@ __global__ void sgd_kernel(PositFmt fo, int bo, void* master, PositFmt fg, int b
     }
 }
 
+// avgpool2d, tensor_ops.cpp:672-691: window sum (quire: exact, one rounding;
+// sequential: add chain in (ky,kx) order) then mul by the caller-quantized
+// reciprocal (scale, :763-769).
+__global__ void avgpool_fwd_kernel(PositFmt f, int b, const void* x, int64_t NC, int64_t H,
+                                   int64_t W, int k, int s, int64_t OH, int64_t OW, int use_quire,
+                                   uint32_t recip, void* y) {
+    GRID_STRIDE(o, NC * OH * OW) {
+        const int64_t ox = o % OW, oy = (o / OW) % OH, nc = o / (OW * OH);
+        const int64_t base = nc * H * W + (oy * s) * W + ox * s;
+        uint32_t sum = 0;
+        if (use_quire) {
+            __int128 acc = 0;
+            bool nar = false;
+            for (int ky = 0; ky < k; ++ky)
+                for (int kx = 0; kx < k; ++kx) {
+                    int64_t X;
+                    nar |= decode_x(load_any(x, base + ky * W + kx, b), f, X);
+                    acc += X;
+                }
+            const bool neg = acc < 0;
+            sum = nar ? nar_of(f)
+                      : round_mag128(f, neg, (unsigned __int128)(neg ? -acc : acc), -f.R);
+        } else {
+            bool first = true;
+            for (int ky = 0; ky < k; ++ky)
+                for (int kx = 0; kx < k; ++kx) {
+                    const uint32_t v = load_any(x, base + ky * W + kx, b);
+                    sum = first ? v : p_add(f, sum, v);
+                    first = false;
+                }
+        }
+        store_any(y, o, b, p_mul(f, sum, recip));
+    }
+}
+
+// avgpool2d_backward, tensor_ops.cpp:693-720: g = mul(dy, recip); each input
+// accumulates add(dx, g) over the windows containing it in output order.
+__global__ void avgpool_bwd_kernel(PositFmt f, int b, const void* dy, int64_t NC, int64_t H,
+                                   int64_t W, int k, int s, int64_t OH, int64_t OW, uint32_t recip,
+                                   void* dx) {
+    GRID_STRIDE(t, NC * H * W) {
+        const int64_t ix = t % W, iy = (t / W) % H, nc = t / (W * H);
+        const int64_t oy0 = iy - k + 1 > 0 ? (iy - k + 1 + s - 1) / s : 0;
+        const int64_t ox0 = ix - k + 1 > 0 ? (ix - k + 1 + s - 1) / s : 0;
+        const int64_t oy1 = min(OH - 1, iy / s), ox1 = min(OW - 1, ix / s);
+        uint32_t acc = 0;
+        for (int64_t oy = oy0; oy <= oy1; ++oy)
+            for (int64_t ox = ox0; ox <= ox1; ++ox)
+                acc = p_add(f, acc, p_mul(f, load_any(dy, (nc * OH + oy) * OW + ox, b), recip));
+        store_any(dx, t, b, acc);
+    }
+}
+
 __global__ void from_float64_kernel(PositFmt f, int b, const double* x, void* out, int64_t n) {
     GRID_STRIDE(i, n) { store_any(out, i, b, p_from_float64(f, x[i])); }
 }
@@ -208,6 +261,8 @@ __global__ void scalar_eval_kernel(PositFmt f, int op, const uint32_t* a, const 
             case 6: r = p_round_to_int(f, x); break;
             case 7: r = p_ldexp(f, x, int32_t(y)); break;
             case 8: r = uint32_t(p_compare(f, x, y)); break;
+            case 10: r = p_tanh(f, x); break;
+            case 11: r = p_sigmoid(f, x); break;
             default: r = uint32_t(p_to_int64(f, x)); break;
         }
         out[i] = r;
@@ -339,6 +394,32 @@ int pnn_sgd_step(int opt_nbits, int opt_es, void* master, int g_nbits, int g_es,
         bytes_of(g_nbits), grad, n, lr_code, f1, bytes_of(f1.nbits), copy1, f2,
         bytes_of(f2.nbits), copy2);
     return launched("sgd_step");
+}
+
+int pnn_avgpool2d_fwd(int nbits, int es, const void* x, int64_t N, int64_t C, int64_t H,
+                      int64_t W, int k, int stride, int use_quire, uint32_t recip_code, void* y,
+                      void* stream) {
+    CHECK_FMT(nbits, es);
+    if (N < 0 || C < 1 || k < 1 || stride < 1 || H < k || W < k)
+        return set_status(PNN_EINVAL, "avgpool2d: window larger than input");
+    const int64_t OH = (H - k) / stride + 1, OW = (W - k) / stride + 1;
+    if (N == 0) return PNN_OK;
+    avgpool_fwd_kernel<<<grid1(N * C * OH * OW), 256, 0, (cudaStream_t)stream>>>(
+        make_fmt(nbits, es), bytes_of(nbits), x, N * C, H, W, k, stride, OH, OW, use_quire,
+        recip_code, y);
+    return launched("avgpool2d_fwd");
+}
+
+int pnn_avgpool2d_bwd(int nbits, int es, const void* dy, int64_t N, int64_t C, int64_t H,
+                      int64_t W, int k, int stride, uint32_t recip_code, void* dx, void* stream) {
+    CHECK_FMT(nbits, es);
+    if (N < 0 || C < 1 || k < 1 || stride < 1 || H < k || W < k)
+        return set_status(PNN_EINVAL, "avgpool2d_backward: bad shape");
+    const int64_t OH = (H - k) / stride + 1, OW = (W - k) / stride + 1;
+    if (N == 0) return PNN_OK;
+    avgpool_bwd_kernel<<<grid1(N * C * H * W), 256, 0, (cudaStream_t)stream>>>(
+        make_fmt(nbits, es), bytes_of(nbits), dy, N * C, H, W, k, stride, OH, OW, recip_code, dx);
+    return launched("avgpool2d_bwd");
 }
 
 int pnn_from_float64(int nbits, int es, const double* x, void* codes, int64_t n, void* stream) {

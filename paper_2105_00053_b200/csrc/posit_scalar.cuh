@@ -261,4 +261,29 @@ static __device__ __noinline__ uint32_t p_log(const PositFmt& f, uint32_t x) {
     return p_add(f, p_mul(f, p_from_int64(f, s), ln2), logm);
 }
 
+// tanh_posit, posit_math.cpp:109-118: r = (1 - e^(-2|x|)) / (1 + e^(-2|x|)), odd.
+static __device__ __noinline__ uint32_t p_tanh(const PositFmt& f, uint32_t x) {
+    x &= code_mask(f);
+    if (x == nar_of(f) || x == 0) return x;
+    const bool neg = (x & nar_of(f)) != 0;
+    const uint32_t ax = neg ? p_negate(f, x) : x;
+    const uint32_t one = p_from_int64(f, 1);
+    const uint32_t t = p_exp(f, p_negate(f, p_ldexp(f, ax, 1)));
+    const uint32_t r = p_div(f, p_sub(f, one, t), p_add(f, one, t));
+    return neg ? p_negate(f, r) : r;
+}
+
+// sigmoid_posit, posit_math.cpp:120-130.
+static __device__ __noinline__ uint32_t p_sigmoid(const PositFmt& f, uint32_t x) {
+    x &= code_mask(f);
+    if (x == nar_of(f)) return x;
+    const uint32_t one = p_from_int64(f, 1);
+    if (!(x & nar_of(f))) {
+        const uint32_t t = p_exp(f, p_negate(f, x));
+        return p_div(f, one, p_add(f, one, t));
+    }
+    const uint32_t t = p_exp(f, x);
+    return p_div(f, t, p_add(f, one, t));
+}
+
 }  // namespace pnn_b200

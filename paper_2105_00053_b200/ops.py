@@ -469,3 +469,29 @@ def lanes_to_posit(cfg, lanes):
     _native.check(_native.lib().pnn_lanes_to_posit(cfg.nbits, cfg.es, lanes.contiguous().data_ptr(), n,
                                                    out.data_ptr(), None, _stream_ptr(lanes.device)))
     return out
+
+
+# ---- avg-pool (tensor_ops.hpp:53-58) ------------------------------------------
+
+def avgpool2d(cfg, x, k: int, stride: int, use_quire: bool, recip_bits: int, pool=None):
+    """Window sum (quire or add chain) times the caller-quantized 1/count."""
+    cfg = _cfg(cfg)
+    x = x.contiguous()
+    N, Cc, H, W = x.shape
+    if H < k or W < k:
+        raise _native.PnnInvalidArgument(1, "avgpool2d: window larger than input")
+    OH, OW = (H - k) // stride + 1, (W - k) // stride + 1
+    y = torch.empty((N, Cc, OH, OW), dtype=x.dtype, device=x.device)
+    _native.check(_native.lib().pnn_avgpool2d_fwd(cfg.nbits, cfg.es, x.data_ptr(), N, Cc, H, W, k, stride,
+                                                  int(use_quire), int(recip_bits), y.data_ptr(),
+                                                  _stream_ptr(x.device)))
+    return y
+
+
+def avgpool2d_backward(cfg, dy, k: int, stride: int, x_shape, recip_bits: int, pool=None):
+    cfg = _cfg(cfg)
+    N, Cc, H, W = (int(v) for v in x_shape)
+    dx = torch.empty((N, Cc, H, W), dtype=cfg.code_dtype, device=dy.device)
+    _native.check(_native.lib().pnn_avgpool2d_bwd(cfg.nbits, cfg.es, dy.contiguous().data_ptr(), N, Cc, H, W, k,
+                                                  stride, int(recip_bits), dx.data_ptr(), _stream_ptr(dy.device)))
+    return dx
