@@ -300,6 +300,36 @@ def train_step(model: Sequential, loss_fn: CrossEntropyLoss, opt: SGD, x_fwd, la
     return loss
 
 
+class GraphedTrainStep:
+    """One training step captured as a CUDA graph (every kernel of forward,
+    loss, backward and SGD on one stream; no host round trips), replayed per
+    step.  Feed new data by copying into ``x`` / ``labels`` before ``step()``.
+    The first call runs ``warmup`` eager steps (sizing workspaces), then
+    captures; each capture/replay is a real, bit-identical training step."""
+
+    def __init__(self, model: Sequential, loss_fn: CrossEntropyLoss, opt: SGD, x_static, labels_static,
+                 global_batch: int, warmup: int = 1):
+        self.model, self.loss_fn, self.opt = model, loss_fn, opt
+        self.x, self.labels, self.B = x_static, labels_static, global_batch
+        self.warmup = warmup
+        self.graph = None
+        self.loss = None
+
+    def step(self):
+        if self.graph is None:
+            if self.warmup > 0:
+                self.warmup -= 1
+                return train_step(self.model, self.loss_fn, self.opt, self.x, self.labels, self.B)
+            s = torch.cuda.Stream()
+            s.wait_stream(torch.cuda.current_stream())
+            self.graph = torch.cuda.CUDAGraph()
+            with torch.cuda.stream(s), torch.cuda.graph(self.graph, stream=s):
+                self.loss = train_step(self.model, self.loss_fn, self.opt, self.x, self.labels, self.B)
+            torch.cuda.current_stream().wait_stream(s)
+        self.graph.replay()
+        return self.loss
+
+
 def layer_description(model: Sequential):
     """The oracle-step layer list (oracle/step.py) of a model."""
     out = []

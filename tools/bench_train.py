@@ -109,7 +109,7 @@ CONFIGS = {
 }
 
 
-def run(cfg_key, steps, warmup, cpu):
+def run(cfg_key, steps, warmup, cpu, graph=False):
     c = CONFIGS[cfg_key]
     st = nn.StagePrecisions(*c["st"])
     B = c["batch"]
@@ -129,20 +129,25 @@ def run(cfg_key, steps, warmup, cpu):
     opt = nn.SGD(model.params(), 1.0 / 16, st)
     params0 = [(codec.to_host(l.w.master), codec.to_host(l.b.master))
                for l in model.layers if isinstance(l, nn.Conv2d)]
-    for _ in range(warmup):
-        nn.train_step(model, loss_fn, opt, xd, lab, B)
+    g = nn.GraphedTrainStep(model, loss_fn, opt, xd, lab, B, warmup=1) if graph else None
+
+    def one():
+        return g.step() if g else nn.train_step(model, loss_fn, opt, xd, lab, B)
+
+    for _ in range(max(warmup, 2 if graph else 0)):
+        one()
     torch.cuda.synchronize()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0 = time.perf_counter()
     s.record()
     for _ in range(steps):
-        nn.train_step(model, loss_fn, opt, xd, lab, B)
+        one()
     e.record()
     torch.cuda.synchronize()
     wall = (time.perf_counter() - t0) / steps
     dev_ms = s.elapsed_time(e) / steps
     macs = step_macs(layers, 32, cin) * B
-    out = {"config": c["name"], "batch": B, "steps": steps, "gpu_ms_per_step": dev_ms,
+    out = {"config": c["name"], "batch": B, "steps": steps, "cuda_graph": graph, "gpu_ms_per_step": dev_ms,
            "gpu_wall_ms_per_step": wall * 1e3, "images_per_s": B / (dev_ms / 1e3),
            "posit_mac_per_s": macs / (dev_ms / 1e3), "macs_per_step": macs}
     if cpu:
@@ -169,9 +174,10 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--cpu", action="store_true")
+    ap.add_argument("--graph", action="store_true", help="replay a CUDA-graph-captured step")
     a = ap.parse_args()
     for k in a.configs.split(","):
-        print(json.dumps(run(k, a.steps, a.warmup, a.cpu and k in ("0", "2"))), flush=True)
+        print(json.dumps(run(k, a.steps, a.warmup, a.cpu and k in ("0", "2"), a.graph)), flush=True)
 
 
 if __name__ == "__main__":
