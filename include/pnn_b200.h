@@ -71,7 +71,15 @@ int pnn_matmul_host(int nbits, int es, const uint64_t* A, const uint64_t* B, uin
  * 1x1 convolution of x [B,in,1,1] with w [out,in,1,1].
  * pass: 0 forward (conv2d, tensor_ops.cpp:494-525 -- bias inside the quire),
  *       1 input grad (conv2d_input_grad, :527-574),
- *       2 weight grad (conv2d_weight_grad, :576-603). */
+ *       2 weight grad (conv2d_weight_grad, :576-603).
+ * Two implementations, same results bit for bit: the explicit path packs the
+ * im2col digit image in HBM; the implicit path (stride 1, contracted channels
+ * a multiple of 32, pixel rows tiling 128-row tiles) digitises each operand
+ * once and lets TMA tile loads do the gather.  pnn_conv_algo selects:
+ * 0 auto (implicit where eligible; default), 1 explicit only, 2 implicit only
+ * (ineligible shapes fail with PNN_EUNSUPPORTED).  Returns the previous
+ * setting, or -1 for an invalid value.  Query the workspace after setting. */
+int pnn_conv_algo(int algo);
 int pnn_conv2d_workspace(int pass, int nbits, int es, int64_t N, int64_t C, int64_t H, int64_t W,
                          int64_t F, int64_t KH, int64_t KW, int stride, int pad, int has_bias,
                          size_t* bytes);

@@ -35,6 +35,7 @@ _SIGS = {
     "pnn_decode_x": (C.c_int, [C.c_int, C.c_int, _vp, _i64, _vp, _vp, _vp]),
     "pnn_quire_round": (C.c_int, [C.c_int, C.c_int, _vp, _i64, _vp, _vp]),
     "pnn_pack_round": (C.c_int, [C.c_int, C.c_int, _vp, _vp, _vp, _vp, _i64, _vp, _vp]),
+    "pnn_conv_algo": (C.c_int, [C.c_int]),
     "pnn_conv2d_workspace": (C.c_int, [C.c_int, C.c_int, C.c_int] + [_i64] * 7 + [C.c_int, C.c_int, C.c_int,
                                                                            C.POINTER(C.c_size_t)]),
     "pnn_conv2d_fwd": (C.c_int, [C.c_int, C.c_int, _vp] + [_i64] * 4 + [_vp] + [_i64] * 3 +

@@ -21,15 +21,11 @@
 #include <string>
 
 #include "../../include/pnn_b200.h"
-#include "quire_gemm_core.cuh"
+#include "igemm.h"
+#include "igemm_core.cuh"
 #include "status.h"
 
 namespace pnn_b200 {
-
-struct ConvGeom {
-    int64_t N, C, H, W, F, KH, KW, OH, OW;
-    int stride, pad;
-};
 
 // ---- forward ---------------------------------------------------------------
 
@@ -164,35 +160,6 @@ struct FetchDgradW {  // X[r = c][k = (f,ky,kx)] = w[f][c][ky][kx]
         return uint32_t(w[(f * g.C + r) * khw + t]);
     }
 };
-
-// Weight-side NaR of the input gradient, exact per output over its valid taps.
-// Runs only when the pack pass saw a NaR weight (flag set on device).
-template <typename CodeT>
-__global__ void dgrad_weight_nar_kernel(CodeT* __restrict__ dx, const CodeT* __restrict__ w,
-                                        ConvGeom g, const uint8_t* __restrict__ any_nar_w,
-                                        uint32_t nar) {
-    if (*any_nar_w == 0) return;
-    const int64_t total = g.N * g.C * g.H * g.W;
-    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total;
-         i += int64_t(gridDim.x) * blockDim.x) {
-        const int64_t ix = i % g.W, iy = (i / g.W) % g.H, c = (i / (g.W * g.H)) % g.C;
-        bool hit = false;
-        for (int64_t f = 0; f < g.F && !hit; ++f)
-            for (int64_t ky = 0; ky < g.KH && !hit; ++ky) {
-                const int64_t ty = iy + g.pad - ky;
-                if (ty < 0 || ty % g.stride || ty / g.stride >= g.OH) continue;
-                for (int64_t kx = 0; kx < g.KW; ++kx) {
-                    const int64_t tx = ix + g.pad - kx;
-                    if (tx < 0 || tx % g.stride || tx / g.stride >= g.OW) continue;
-                    if (uint32_t(w[((f * g.C + c) * g.KH + ky) * g.KW + kx]) == nar) {
-                        hit = true;
-                        break;
-                    }
-                }
-            }
-        if (hit) dx[i] = CodeT(nar);
-    }
-}
 
 // ---- weight grad -------------------------------------------------------------
 
@@ -382,6 +349,8 @@ int pnn_conv2d_workspace(int pass, int nbits, int es, int64_t N, int64_t C, int6
         *bytes = 0;
         return PNN_OK;
     }
+    if (igemm_eligible(pass, make_fmt(nbits, es), g, pass == 2, bytes)) return PNN_OK;
+    if (conv_algo() == 2) return set_status(PNN_EUNSUPPORTED, "conv: implicit path not eligible");
     QuireGemmPlan p;
     if (plan_quire_gemm(make_fmt(nbits, es), M, Nn, K, 0, pass == 2, &p)) return PNN_EUNSUPPORTED;
     *bytes = p.workspace_bytes;
@@ -403,6 +372,10 @@ int pnn_conv2d_fwd(int nbits, int es, const void* x, int64_t N, int64_t C, int64
     const int64_t kconv = C * KH * KW;
     auto st = static_cast<cudaStream_t>(stream);
     int rc;
+    if (igemm_eligible(0, a.f, g, false, nullptr))
+        return status_of(igemm_conv_fwd(a.f, g, x, w, bias, y, workspace, workspace_bytes, st),
+                         "conv2d_fwd");
+    if (conv_algo() == 2) return set_status(PNN_EUNSUPPORTED, "conv2d_fwd: implicit path not eligible");
     if (nbits <= 8) {
         using T = uint8_t;
         rc = run_quire_gemm<T>(a, FetchIm2colFwd<T>{(const T*)x, g, kconv, one_code(a.f)},
@@ -434,9 +407,13 @@ int pnn_conv2d_dgrad(int nbits, int es, const void* dy, int64_t N, int64_t F, in
     a.max_kb_per_split = 0;
     a.row_nar = true;
     a.col_nar = false;  // weight NaR applied per valid tap below
+    auto st = static_cast<cudaStream_t>(stream);
+    if (igemm_eligible(1, a.f, g, false, nullptr))
+        return status_of(igemm_conv_dgrad(a.f, g, dy, w, dx, workspace, workspace_bytes, st),
+                         "conv2d_dgrad");
+    if (conv_algo() == 2) return set_status(PNN_EUNSUPPORTED, "conv2d_dgrad: implicit path not eligible");
     QuireGemmPlan p;
     if (plan_quire_gemm(a.f, a.M, a.N, a.K, 0, false, &p)) return PNN_EUNSUPPORTED;
-    auto st = static_cast<cudaStream_t>(stream);
     const uint8_t* flag_w = static_cast<const uint8_t*>(workspace) + p.off_flags + 1;
     int rc;
     const uint32_t nar = 1u << (nbits - 1);
@@ -486,6 +463,11 @@ int pnn_conv2d_wgrad(int nbits, int es, const void* dy, int64_t N, int64_t F, in
     a.row_nar = a.col_nar = true;
     a.raw_words = static_cast<unsigned __int128*>(raw_words);
     a.raw_nar = static_cast<uint8_t*>(raw_nar);
+    if (igemm_eligible(2, a.f, g, raw_words != nullptr, nullptr))
+        return status_of(igemm_conv_wgrad(a.f, g, dy, x, dw, a.raw_words, a.raw_nar, workspace,
+                                          workspace_bytes, st),
+                         "conv2d_wgrad");
+    if (conv_algo() == 2) return set_status(PNN_EUNSUPPORTED, "conv2d_wgrad: implicit path not eligible");
     // dw[f][(c,ky,kx)]: output (m=(c,ky,kx), n=f) -> f*M + m  (NCHW map with one "image")
     int rc;
     if (nbits <= 8) {

@@ -1,0 +1,483 @@
+// Host side of the implicit-GEMM convolution path: eligibility, workspace
+// plan, digitising launches, TMA tensor maps, kernel dispatch, NaR fix-ups.
+// See igemm_core.cuh for the kernel; conv.cu routes the C-ABI calls here.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "igemm.h"
+#include "igemm_core.cuh"
+
+namespace pnn_b200 {
+
+static int g_conv_algo = 0;
+int conv_algo() { return g_conv_algo; }
+int set_conv_algo(int a) {
+    const int prev = g_conv_algo;
+    g_conv_algo = a;
+    return prev;
+}
+
+namespace {
+
+int nt_for(int D) { return D == 2 ? TileCfg<2>::NT : D <= 4 ? TileCfg<4>::NT : TileCfg<8>::NT; }
+
+int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// Output-pixel raster tiles of 128 rows: whole rows of width Wt; either an
+// image spans tiles of Hb rows or a tile holds 128 / (Ht*Wt) whole images.
+bool tile_geom(int64_t Ht, int64_t Wt, int* tpi, int* ipt, int* Hb) {
+    if (Wt < 1 || Wt > 128 || Ht < 1) return false;
+    const int64_t P = Ht * Wt;
+    if (P >= 128) {
+        if (128 % Wt || Ht % (128 / Wt)) return false;
+        *Hb = int(128 / Wt);
+        *tpi = int(P / 128);
+        *ipt = 0;
+    } else {
+        if (128 % P) return false;
+        *Hb = int(Ht);
+        *tpi = 0;
+        *ipt = int(128 / P);
+    }
+    return true;
+}
+
+struct ImplPlan {
+    int mode, D, NT;
+    IgemmArgs a;
+    int64_t Ca, Wa, Ha;     // A digit tensor [D][N][Ha][Wa][Ca]
+    uint32_t boxA[4];       // {channels, w, h, n} (x D planes)
+    int64_t Kp, brows;      // modes 0/1: B digits [D][brows][taps * Kp]
+    int64_t Fpw;            // mode 2: B digits [D][N][OH][OW][Fpw]
+    size_t adig, bdig;      // bytes
+    size_t off_adig, off_bdig, off_col_add, off_maps, maps_bytes, off_pos_nar, off_chw_nar,
+        off_col_nar, off_flags, off_partial, total;
+};
+
+bool make_plan(int pass, const PositFmt& f, const ConvGeom& g, bool raw, ImplPlan* p) {
+    if (conv_algo() == 1 || g.stride != 1) return false;
+    if (g.N < 1 || g.N > (1 << 30)) return false;
+    const int D = digits_for(f);
+    if (D < 2 || D > 8) return false;
+    *p = ImplPlan{};
+    p->mode = pass;
+    p->D = D;
+    p->NT = nt_for(D);
+    IgemmArgs& a = p->a;
+    a.f = f;
+    a.KW = int(g.KW);
+    a.pad = g.pad;
+    const int64_t taps = g.KH * g.KW;
+    a.taps = int(taps);
+    size_t pos_nar = 0, chw_nar = 0, col_nar = 0, col_add = 0;
+    if (pass == 0 || pass == 1) {
+        const int64_t Cin = pass == 0 ? g.C : g.F;         // contracted channels
+        const int64_t Cout = pass == 0 ? g.F : g.C;
+        const int64_t Ht = pass == 0 ? g.OH : g.H, Wt = pass == 0 ? g.OW : g.W;
+        const int64_t Hs = pass == 0 ? g.H : g.OH, Ws = pass == 0 ? g.W : g.OW;
+        if (Cin % 32 || Ws > 256) return false;
+        int tpi, ipt, Hb;
+        if (!tile_geom(Ht, Wt, &tpi, &ipt, &Hb)) return false;
+        a.tiles_per_img = tpi;
+        a.imgs_per_tile = ipt;
+        a.Hb = Hb;
+        a.cch = int(Cin / 32);
+        a.M = g.N * Ht * Wt;
+        a.N = Cout;
+        a.mtiles = tpi > 0 ? g.N * tpi : cdiv(g.N, ipt);
+        a.ntiles = cdiv(Cout, p->NT);
+        a.kbt = taps * Cin / 32;
+        a.a_sw = 32;
+        a.b_sw = 32;
+        p->Ca = Cin;
+        p->Wa = Ws;
+        p->Ha = Hs;
+        p->boxA[0] = 32;
+        p->boxA[1] = uint32_t(Wt);
+        p->boxA[2] = uint32_t(Hb);
+        p->boxA[3] = uint32_t(tpi > 0 ? 1 : ipt);
+        p->Kp = Cin;
+        p->brows = Cout;
+        p->adig = size_t(D) * g.N * Hs * Ws * Cin;
+        p->bdig = size_t(D) * Cout * taps * Cin;
+        pos_nar = size_t(g.N) * Hs * Ws;
+        if (pass == 0) {
+            col_nar = size_t(Cout);
+            col_add = size_t(Cout) * 8;
+        }
+    } else {
+        if (!(g.C == 32 || g.C == 64 || g.C == 128) || g.W > 256 || g.OW > 256) return false;
+        int OWb, OHb;
+        if (g.OW >= 32) {
+            if (g.OW % 32) return false;
+            OWb = 32;
+            OHb = 1;
+        } else {
+            if (32 % g.OW || g.OH % (32 / g.OW)) return false;
+            OWb = int(g.OW);
+            OHb = int(32 / g.OW);
+        }
+        a.OWb = OWb;
+        a.OHb = OHb;
+        a.C = int(g.C);
+        a.slots = int(128 / g.C);
+        a.kpr = int(g.OW / OWb);
+        a.kpi = int((g.OH / OHb) * a.kpr);
+        a.M = taps * g.C;
+        a.N = g.F;
+        a.mtiles = cdiv(taps, a.slots);
+        p->Fpw = cdiv(g.F, p->NT) * p->NT;
+        a.ntiles = p->Fpw / p->NT;
+        a.kbt = g.N * a.kpi;
+        a.a_sw = int(g.C);
+        a.b_sw = p->NT;
+        p->Ca = g.C;
+        p->Wa = g.W;
+        p->Ha = g.H;
+        p->boxA[0] = uint32_t(g.C);
+        p->boxA[1] = uint32_t(OWb);
+        p->boxA[2] = uint32_t(OHb);
+        p->boxA[3] = 1;
+        p->adig = size_t(D) * g.N * g.H * g.W * g.C;
+        p->bdig = size_t(D) * g.N * g.OH * g.OW * p->Fpw;
+        chw_nar = size_t(g.C) * g.H * g.W;
+        col_nar = size_t(p->Fpw);
+    }
+    // split-K: int32 group sums exact for <= 131071 / D terms (W > 32), SM fill
+    int64_t kbps = f.W <= 32 ? a.kbt : (131071 / D) / kIKB;
+    const int64_t tiles = a.mtiles * a.ntiles;
+    const int sms = num_sms();
+    if (tiles < sms && a.kbt >= 8) {
+        int64_t want = cdiv(sms, tiles);
+        if (want > a.kbt / 4) want = a.kbt / 4;
+        if (want > 1) kbps = kbps < cdiv(a.kbt, want) ? kbps : cdiv(a.kbt, want);
+    }
+    if (kbps < 1) kbps = 1;
+    a.kb_per_split = a.kbt < kbps ? a.kbt : kbps;
+    a.splits = cdiv(a.kbt, a.kb_per_split);
+    const size_t partial = (a.splits > 1 || raw) ? size_t(a.splits) * a.M * a.N * 16 : 0;
+
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        const size_t o = off;
+        off += (bytes + 255) & ~size_t(255);
+        return o;
+    };
+    p->off_adig = take(p->adig);
+    p->off_bdig = take(p->bdig);
+    p->off_col_add = take(col_add);
+    p->off_maps = off;  // NaR maps and flags: zeroed by one memset
+    p->off_pos_nar = take(pos_nar);
+    p->off_chw_nar = take(chw_nar);
+    p->off_col_nar = take(col_nar);
+    p->off_flags = take(16);
+    p->maps_bytes = off - p->off_maps;
+    p->off_partial = take(partial);
+    p->total = off;
+    return true;
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (fn == nullptr) {
+        void* ptr = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &ptr, 12000, cudaEnableDefault,
+                                             &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+    }
+    return fn;
+}
+
+CUtensorMapSwizzle swz(int bytes) {
+    return bytes == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
+                       : bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B;
+}
+
+// dig[D][N][H][W][C] (int8) as a 5-D map {C, W, H, N, D}
+bool map_act(CUtensorMap* m, void* base, int D, int64_t N, int64_t H, int64_t W, int64_t C,
+             const uint32_t box[4], int sw) {
+    auto enc = encoder();
+    if (!enc) return false;
+    const cuuint64_t dims[5] = {cuuint64_t(C), cuuint64_t(W), cuuint64_t(H), cuuint64_t(N),
+                                cuuint64_t(D)};
+    const cuuint64_t strides[4] = {cuuint64_t(C), cuuint64_t(W * C), cuuint64_t(H * W * C),
+                                   cuuint64_t(N * H * W * C)};
+    const cuuint32_t boxd[5] = {box[0], box[1], box[2], box[3], cuuint32_t(D)};
+    const cuuint32_t es[5] = {1, 1, 1, 1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 5, base, dims, strides, boxd, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, swz(sw), CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// dig[D][rows][K] (int8) as a 3-D map {K, rows, D}, box {32, NT, D}
+bool map_weights(CUtensorMap* m, void* base, int D, int64_t rows, int64_t K, int NT) {
+    auto enc = encoder();
+    if (!enc) return false;
+    const cuuint64_t dims[3] = {cuuint64_t(K), cuuint64_t(rows), cuuint64_t(D)};
+    const cuuint64_t strides[2] = {cuuint64_t(K), cuuint64_t(rows * K)};
+    const cuuint32_t boxd[3] = {32, cuuint32_t(NT), cuuint32_t(D)};
+    const cuuint32_t es[3] = {1, 1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, base, dims, strides, boxd, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int D, typename CodeT, int MODE>
+cudaError_t launch_kernel(const CUtensorMap& tA, const CUtensorMap& tB, const IgemmArgs& a,
+                          OutMap<CodeT> out, cudaStream_t st) {
+    using Geo = ImplGeo<D>;
+    void (*k)(CUtensorMap, CUtensorMap, IgemmArgs, OutMap<CodeT>);
+    if constexpr (D <= 3)
+        k = a.f.W <= 32 ? igemm_kernel<D, 1, CodeT, MODE> : igemm_kernel<D, 2, CodeT, MODE>;
+    else
+        k = a.f.W <= 64 ? igemm_kernel<D, 2, CodeT, MODE> : igemm_kernel<D, 4, CodeT, MODE>;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Geo::SMEM);
+    if (e != cudaSuccess) return e;
+    const int64_t tiles = a.mtiles * a.ntiles * a.splits;
+    const int grid = int(tiles < num_sms() ? tiles : num_sms());
+    k<<<grid, kThreads, Geo::SMEM, st>>>(tA, tB, a, out);
+    return cudaGetLastError();
+}
+
+template <typename CodeT, int MODE>
+cudaError_t dispatch(int D, const CUtensorMap& tA, const CUtensorMap& tB, const IgemmArgs& a,
+                     OutMap<CodeT> out, cudaStream_t st) {
+    switch (D) {
+        case 2: return launch_kernel<2, CodeT, MODE>(tA, tB, a, out, st);
+        case 3: return launch_kernel<3, CodeT, MODE>(tA, tB, a, out, st);
+        case 4: return launch_kernel<4, CodeT, MODE>(tA, tB, a, out, st);
+        case 5: return launch_kernel<5, CodeT, MODE>(tA, tB, a, out, st);
+        case 6: return launch_kernel<6, CodeT, MODE>(tA, tB, a, out, st);
+        case 7: return launch_kernel<7, CodeT, MODE>(tA, tB, a, out, st);
+        case 8: return launch_kernel<8, CodeT, MODE>(tA, tB, a, out, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+template <typename CodeT>
+cudaError_t act_digits(int D, const CodeT* x, int64_t N, int64_t C, int64_t H, int64_t W,
+                       int64_t Cp, const PositFmt& f, int8_t* dig, uint8_t* pos_nar,
+                       uint8_t* chw_nar, uint8_t* chan_nar, uint8_t* any, cudaStream_t st) {
+    const int64_t rows = N * H;
+    const int grid = int(rows < 148 * 16 ? rows : 148 * 16);
+#define PNN_ACT(DD)                                                                              \
+    act_digits_kernel<DD, CodeT><<<grid, 256, 0, st>>>(x, N, int(C), int(H), int(W), int(Cp), f, \
+                                                       dig, pos_nar, chw_nar, chan_nar, any)
+    switch (D) {
+        case 2: PNN_ACT(2); break;
+        case 3: PNN_ACT(3); break;
+        case 4: PNN_ACT(4); break;
+        case 5: PNN_ACT(5); break;
+        case 6: PNN_ACT(6); break;
+        case 7: PNN_ACT(7); break;
+        case 8: PNN_ACT(8); break;
+        default: return cudaErrorInvalidValue;
+    }
+#undef PNN_ACT
+    return cudaGetLastError();
+}
+
+template <typename CodeT>
+cudaError_t weight_digits(int D, const CodeT* w, const CodeT* bias, int64_t F, int64_t C,
+                          int64_t taps, int64_t Kp, int transpose, const PositFmt& f, int8_t* dig,
+                          int64_t* col_add, uint8_t* col_nar, uint8_t* any, cudaStream_t st) {
+    const int64_t total = (transpose ? C : F) * taps * Kp;
+    const int grid = grid_for(total > F ? total : F, 256);
+#define PNN_WD(DD)                                                                              \
+    weight_digits_kernel<DD, CodeT><<<grid, 256, 0, st>>>(w, bias, int(F), int(C), int(taps),  \
+                                                          int(Kp), transpose, f, dig, col_add, \
+                                                          col_nar, any)
+    switch (D) {
+        case 2: PNN_WD(2); break;
+        case 3: PNN_WD(3); break;
+        case 4: PNN_WD(4); break;
+        case 5: PNN_WD(5); break;
+        case 6: PNN_WD(6); break;
+        case 7: PNN_WD(7); break;
+        case 8: PNN_WD(8); break;
+        default: return cudaErrorInvalidValue;
+    }
+#undef PNN_WD
+    return cudaGetLastError();
+}
+
+int rc_of(cudaError_t e) { return e == cudaSuccess ? 0 : 4; }
+
+template <typename CodeT>
+int run_fwd(const ImplPlan& p, const ConvGeom& g, const CodeT* x, const CodeT* w,
+            const CodeT* bias, CodeT* y, uint8_t* ws, cudaStream_t st) {
+    const PositFmt& f = p.a.f;
+    auto* adig = reinterpret_cast<int8_t*>(ws + p.off_adig);
+    auto* bdig = reinterpret_cast<int8_t*>(ws + p.off_bdig);
+    auto* col_add = reinterpret_cast<int64_t*>(ws + p.off_col_add);
+    uint8_t* pos_nar = ws + p.off_pos_nar;
+    uint8_t* col_nar = ws + p.off_col_nar;
+    uint8_t* flags = ws + p.off_flags;
+    cudaError_t e;
+    if ((e = cudaMemsetAsync(ws + p.off_maps, 0, p.maps_bytes, st)) != cudaSuccess) return 4;
+    if ((e = act_digits<CodeT>(p.D, x, g.N, g.C, g.H, g.W, p.Ca, f, adig, pos_nar, nullptr,
+                               nullptr, flags, st)) != cudaSuccess)
+        return 4;
+    const int64_t taps = g.KH * g.KW;
+    if ((e = weight_digits<CodeT>(p.D, w, bias, g.F, g.C, taps, p.Kp, 0, f, bdig, col_add, col_nar,
+                                  flags + 1, st)) != cudaSuccess)
+        return 4;
+    CUtensorMap tA, tB;
+    if (!map_act(&tA, adig, p.D, g.N, g.H, g.W, p.Ca, p.boxA, 32) ||
+        !map_weights(&tB, bdig, p.D, p.brows, taps * p.Kp, p.NT))
+        return 5;
+    IgemmArgs a = p.a;
+    a.col_add = bias ? col_add : nullptr;
+    a.col_nar = col_nar;
+    const bool use_partial = a.splits > 1;
+    a.partial = use_partial ? reinterpret_cast<unsigned __int128*>(ws + p.off_partial) : nullptr;
+    const OutMap<CodeT> out = out_nchw<CodeT>(y, g.OH * g.OW, g.F);
+    if ((e = dispatch<CodeT, 0>(p.D, tA, tB, a, out, st)) != cudaSuccess) return 4;
+    if (use_partial)
+        quire_finalize_kernel<CodeT><<<grid_for(a.M * a.N, 256), 256, 0, st>>>(
+            a.partial, int(a.splits), nullptr, col_nar, out, a.M, a.N, f, nullptr, nullptr);
+    fwd_nar_fixup_kernel<CodeT><<<grid_for(a.M, 256), 256, 0, st>>>(
+        y, pos_nar, flags, g.N, int(g.F), int(g.H), int(g.W), int(g.OH), int(g.OW), int(g.KH),
+        int(g.KW), g.pad, 1u << (f.nbits - 1));
+    return rc_of(cudaGetLastError());
+}
+
+template <typename CodeT>
+int run_dgrad(const ImplPlan& p, const ConvGeom& g, const CodeT* dy, const CodeT* w, CodeT* dx,
+              uint8_t* ws, cudaStream_t st) {
+    const PositFmt& f = p.a.f;
+    auto* adig = reinterpret_cast<int8_t*>(ws + p.off_adig);
+    auto* bdig = reinterpret_cast<int8_t*>(ws + p.off_bdig);
+    uint8_t* pos_nar = ws + p.off_pos_nar;
+    uint8_t* flags = ws + p.off_flags;
+    if (cudaMemsetAsync(ws + p.off_maps, 0, p.maps_bytes, st) != cudaSuccess) return 4;
+    if (act_digits<CodeT>(p.D, dy, g.N, g.F, g.OH, g.OW, p.Ca, f, adig, pos_nar, nullptr, nullptr,
+                          flags, st) != cudaSuccess)
+        return 4;
+    const int64_t taps = g.KH * g.KW;
+    if (weight_digits<CodeT>(p.D, w, nullptr, g.F, g.C, taps, p.Kp, 1, f, bdig, nullptr, nullptr,
+                             flags + 1, st) != cudaSuccess)
+        return 4;
+    CUtensorMap tA, tB;
+    if (!map_act(&tA, adig, p.D, g.N, g.OH, g.OW, p.Ca, p.boxA, 32) ||
+        !map_weights(&tB, bdig, p.D, p.brows, taps * p.Kp, p.NT))
+        return 5;
+    IgemmArgs a = p.a;
+    a.col_add = nullptr;
+    a.col_nar = nullptr;
+    const bool use_partial = a.splits > 1;
+    a.partial = use_partial ? reinterpret_cast<unsigned __int128*>(ws + p.off_partial) : nullptr;
+    const OutMap<CodeT> out = out_nchw<CodeT>(dx, g.H * g.W, g.C);
+    if (dispatch<CodeT, 1>(p.D, tA, tB, a, out, st) != cudaSuccess) return 4;
+    if (use_partial)
+        quire_finalize_kernel<CodeT><<<grid_for(a.M * a.N, 256), 256, 0, st>>>(
+            a.partial, int(a.splits), nullptr, nullptr, out, a.M, a.N, f, nullptr, nullptr);
+    const uint32_t nar = 1u << (f.nbits - 1);
+    dgrad_nar_fixup_kernel<CodeT><<<grid_for(a.M, 256), 256, 0, st>>>(
+        dx, pos_nar, flags, g.N, int(g.C), int(g.H), int(g.W), int(g.OH), int(g.OW), int(g.KH),
+        int(g.KW), g.pad, nar);
+    dgrad_weight_nar_kernel<CodeT><<<grid_for(a.M * a.N, 256), 256, 0, st>>>(dx, w, g, flags + 1,
+                                                                             nar);
+    return rc_of(cudaGetLastError());
+}
+
+template <typename CodeT>
+int run_wgrad(const ImplPlan& p, const ConvGeom& g, const CodeT* dy, const CodeT* x, CodeT* dw,
+              unsigned __int128* raw_words, uint8_t* raw_nar, uint8_t* ws, cudaStream_t st) {
+    const PositFmt& f = p.a.f;
+    auto* adig = reinterpret_cast<int8_t*>(ws + p.off_adig);
+    auto* bdig = reinterpret_cast<int8_t*>(ws + p.off_bdig);
+    uint8_t* chw_nar = ws + p.off_chw_nar;
+    uint8_t* col_nar = ws + p.off_col_nar;
+    uint8_t* flags = ws + p.off_flags;
+    if (cudaMemsetAsync(ws + p.off_maps, 0, p.maps_bytes, st) != cudaSuccess) return 4;
+    if (act_digits<CodeT>(p.D, x, g.N, g.C, g.H, g.W, p.Ca, f, adig, nullptr, chw_nar, nullptr,
+                          flags, st) != cudaSuccess)
+        return 4;
+    if (act_digits<CodeT>(p.D, dy, g.N, g.F, g.OH, g.OW, p.Fpw, f, bdig, nullptr, nullptr, col_nar,
+                          flags + 1, st) != cudaSuccess)
+        return 4;
+    CUtensorMap tA, tB;
+    const uint32_t boxB[4] = {uint32_t(p.NT), uint32_t(p.a.OWb), uint32_t(p.a.OHb), 1};
+    if (!map_act(&tA, adig, p.D, g.N, g.H, g.W, p.Ca, p.boxA, p.a.a_sw) ||
+        !map_act(&tB, bdig, p.D, g.N, g.OH, g.OW, p.Fpw, boxB, p.a.b_sw))
+        return 5;
+    IgemmArgs a = p.a;
+    a.col_add = nullptr;
+    a.col_nar = col_nar;
+    const bool use_partial = a.splits > 1 || raw_words != nullptr;
+    a.partial = use_partial ? reinterpret_cast<unsigned __int128*>(ws + p.off_partial) : nullptr;
+    OutMap<CodeT> out;
+    out.base = dw;
+    out.ldc = g.C * g.KH * g.KW;
+    out.inner = g.C;
+    out.ncols = g.KH * g.KW;
+    out.mode = 2;
+    if (dispatch<CodeT, 2>(p.D, tA, tB, a, out, st) != cudaSuccess) return 4;
+    if (use_partial)
+        quire_finalize_kernel<CodeT><<<grid_for(a.M * a.N, 256), 256, 0, st>>>(
+            a.partial, int(a.splits), nullptr, col_nar, out, a.M, a.N, f, raw_words, raw_nar);
+    wgrad_nar_fixup_kernel<CodeT><<<grid_for(g.C * g.KH * g.KW, 128), 128, 0, st>>>(
+        dw, raw_nar, chw_nar, flags, int(g.F), int(g.C), int(g.H), int(g.W), int(g.OH), int(g.OW),
+        int(g.KH), int(g.KW), g.pad, 1u << (f.nbits - 1));
+    return rc_of(cudaGetLastError());
+}
+
+}  // namespace
+
+bool igemm_eligible(int pass, const PositFmt& f, const ConvGeom& g, bool raw, size_t* bytes) {
+    ImplPlan p;
+    if (!make_plan(pass, f, g, raw, &p)) return false;
+    if (bytes) *bytes = p.total;
+    return true;
+}
+
+int igemm_conv_fwd(const PositFmt& f, const ConvGeom& g, const void* x, const void* w,
+                   const void* bias, void* y, void* ws, size_t ws_bytes, cudaStream_t st) {
+    ImplPlan p;
+    if (!make_plan(0, f, g, false, &p)) return 2;
+    if (ws_bytes < p.total) return 3;
+    auto* b = static_cast<uint8_t*>(ws);
+    if (f.nbits <= 8)
+        return run_fwd<uint8_t>(p, g, (const uint8_t*)x, (const uint8_t*)w, (const uint8_t*)bias,
+                                (uint8_t*)y, b, st);
+    return run_fwd<uint16_t>(p, g, (const uint16_t*)x, (const uint16_t*)w, (const uint16_t*)bias,
+                             (uint16_t*)y, b, st);
+}
+
+int igemm_conv_dgrad(const PositFmt& f, const ConvGeom& g, const void* dy, const void* w, void* dx,
+                     void* ws, size_t ws_bytes, cudaStream_t st) {
+    ImplPlan p;
+    if (!make_plan(1, f, g, false, &p)) return 2;
+    if (ws_bytes < p.total) return 3;
+    auto* b = static_cast<uint8_t*>(ws);
+    if (f.nbits <= 8)
+        return run_dgrad<uint8_t>(p, g, (const uint8_t*)dy, (const uint8_t*)w, (uint8_t*)dx, b, st);
+    return run_dgrad<uint16_t>(p, g, (const uint16_t*)dy, (const uint16_t*)w, (uint16_t*)dx, b, st);
+}
+
+int igemm_conv_wgrad(const PositFmt& f, const ConvGeom& g, const void* dy, const void* x, void* dw,
+                     unsigned __int128* raw_words, uint8_t* raw_nar, void* ws, size_t ws_bytes,
+                     cudaStream_t st) {
+    ImplPlan p;
+    if (!make_plan(2, f, g, raw_words != nullptr, &p)) return 2;
+    if (ws_bytes < p.total) return 3;
+    auto* b = static_cast<uint8_t*>(ws);
+    if (f.nbits <= 8)
+        return run_wgrad<uint8_t>(p, g, (const uint8_t*)dy, (const uint8_t*)x, (uint8_t*)dw,
+                                  raw_words, raw_nar, b, st);
+    return run_wgrad<uint16_t>(p, g, (const uint16_t*)dy, (const uint16_t*)x, (uint16_t*)dw,
+                               raw_words, raw_nar, b, st);
+}
+
+}  // namespace pnn_b200
+
+extern "C" int pnn_conv_algo(int algo) {
+    if (algo < 0 || algo > 2) return -1;
+    return pnn_b200::set_conv_algo(algo);
+}

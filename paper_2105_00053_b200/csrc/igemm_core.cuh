@@ -1,0 +1,515 @@
+// Implicit-GEMM convolution on the tcgen05 quire core: the im2col gather is
+// done by the TMA engine, not by a pack pass.
+//
+// Activations (and output gradients) are digitised ONCE per call into a
+// position-major digit tensor  dig[D][N][H][W][Cp]  (Cp = channels rounded up
+// to 32; one byte per balanced int8 digit, same digits as the pack path).  A
+// convolution tap is then a shifted box of that tensor: a 5-D TMA tile load
+// {32 channels, W, Hb, Nb, D planes} at signed coordinates, whose out-of-range
+// elements the TMA unit zero-fills -- exactly the convolution's zero padding
+// (tensor_ops.cpp:274-279, 546-554, 590-596).  HBM traffic per stage is the
+// digit bytes of the box, not KH*KW copies of every element.
+//
+//   mode 0  forward      M = output pixels (n,oy,ox)   N = F   K = (tap, c)   both K-major
+//   mode 1  input grad   M = input pixels (n,iy,ix)    N = C   K = (tap, f)   both K-major
+//   mode 2  weight grad  M = (tap, c)                  N = F   K = (n,oy,ox)  both MN-major
+//
+// K-major modes use the 32-byte-swizzled UMMA layout (one 32-channel chunk of
+// one tap per pipeline stage = one i8 MMA K-step); mode 2 reads the same
+// position-major tensors as MN-major operands (swizzle = channel bytes).
+// Accumulation, TMEM grouping, split-K and the quire epilogue are those of
+// quire_gemm_core.cuh.  The forward bias enters the quire in the epilogue as
+// X_bias * 2^R (= bias * 1.0, tensor_ops.cpp:292).
+#pragma once
+
+#include <cuda.h>
+
+#include "igemm.h"
+#include "quire_gemm_core.cuh"
+
+namespace pnn_b200 {
+
+constexpr int kIKB = 32;  // K bytes (channels or pixels) per pipeline stage
+
+template <int D>
+struct ImplGeo {
+    static constexpr int NT = TileCfg<D>::NT;
+    static constexpr int G = 2 * D - 1;
+    static constexpr int NMMA = D * NT;
+    static constexpr int A_BYTES = D * kBM * kIKB;
+    static constexpr int B_BYTES = D * NT * kIKB;
+    static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+    static constexpr int STAGES_FIT = (200 * 1024) / STAGE_BYTES;
+    static constexpr int STAGES = STAGES_FIT > 12 ? 12 : STAGES_FIT;
+    static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + kZeroBytes + 256;
+    static_assert(A_BYTES % 1024 == 0 && B_BYTES % 1024 == 0, "stage alignment");
+};
+
+struct IgemmArgs {
+    int64_t M, N;
+    int64_t mtiles, ntiles, kbt, kb_per_split, splits;
+    // modes 0/1: m-tile -> (n0, y0) of the output-pixel raster
+    int tiles_per_img;  // > 0: an image spans tiles_per_img tiles of Hb rows
+    int imgs_per_tile;  // tiles_per_img == 0: a tile holds imgs_per_tile images
+    int Hb;
+    int KW, pad, cch;   // taps' width, padding, 32-wide chunks per tap
+    // mode 2: K blocks of OWb x OHb output pixels, m-tile = `slots` taps of C channels
+    int slots, taps, C, OWb, OHb, kpr, kpi;  // k-blocks per row-block set / per image
+    int a_sw, b_sw;     // swizzle bytes of the A / B smem tiles
+    const int64_t* col_add;  // mode 0: X(bias) per column (added as X * 2^R)
+    const uint8_t* col_nar;
+    PositFmt f;
+    unsigned __int128* partial;
+};
+
+template <int D, int QW, typename CodeT, int MODE>
+__global__ void __launch_bounds__(kThreads, 1)
+    igemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                 const IgemmArgs a, const OutMap<CodeT> out) {
+    using Geo = ImplGeo<D>;
+    using QT = typename QuireWord<QW>::T;
+    constexpr int NT = Geo::NT, STAGES = Geo::STAGES, G = Geo::G;
+    constexpr int COLS = NT / 2;
+    constexpr int GB = G < 8 ? G : 8;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((1024 - (ptx::smem_u32(smem_raw) & 1023)) & 1023);
+    uint8_t* zero_tile = smem + STAGES * Geo::STAGE_BYTES;
+    uint64_t* full = reinterpret_cast<uint64_t*>(zero_tile + kZeroBytes);
+    uint64_t* empty = full + STAGES;
+    uint64_t* tmem_full = empty + STAGES;
+    uint64_t* tmem_empty = tmem_full + 1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 1);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int64_t tiles = a.mtiles * a.ntiles * a.splits;
+
+    for (int i = threadIdx.x; i < kZeroBytes / 16; i += kThreads)
+        reinterpret_cast<int4*>(zero_tile)[i] = make_int4(0, 0, 0, 0);
+    if (warp == 0 && lane == 0) {
+        ptx::tma_prefetch_desc(&tmA);
+        ptx::tma_prefetch_desc(&tmB);
+        for (int s = 0; s < STAGES; ++s) {
+            ptx::mbar_init(&full[s], 1);
+            ptx::mbar_init(&empty[s], 1);
+        }
+        ptx::mbar_init(tmem_full, 1);
+        ptx::mbar_init(tmem_empty, kEpiWarps);
+        ptx::fence_barrier_init();
+    }
+    if (warp == 1) ptx::tmem_alloc<512>(tmem_slot);
+    ptx::fence_proxy_async_smem();
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ===== producer: TMA tile boxes (the im2col gather) =====
+            uint32_t it = 0;
+            for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+                int64_t split, mt, nt;
+                tile_coords(t, a.mtiles, a.ntiles, split, mt, nt);
+                const int64_t kb0 = split * a.kb_per_split;
+                const int nkb = int(min(a.kbt, kb0 + a.kb_per_split) - kb0);
+                int n0 = 0, y0 = 0;
+                if (MODE != 2) {
+                    if (a.tiles_per_img > 0) {
+                        n0 = int(mt / a.tiles_per_img);
+                        y0 = int(mt % a.tiles_per_img) * a.Hb;
+                    } else {
+                        n0 = int(mt) * a.imgs_per_tile;
+                    }
+                }
+                for (int i = 0; i < nkb; ++i, ++it) {
+                    const int s = it % STAGES;
+                    const uint32_t ph = (it / STAGES) & 1;
+                    ptx::mbar_wait(&empty[s], ph ^ 1);
+                    uint8_t* sa = smem + s * Geo::STAGE_BYTES;
+                    uint8_t* sb = sa + Geo::A_BYTES;
+                    ptx::mbar_arrive_expect_tx(&full[s], Geo::STAGE_BYTES);
+                    const int kb = int(kb0 + i);
+                    if constexpr (MODE != 2) {
+                        const int tap = kb / a.cch, cc = kb - tap * a.cch;
+                        const int ky = tap / a.KW, kx = tap - ky * a.KW;
+                        if constexpr (MODE == 0)
+                            ptx::tma_load_5d(sa, &tmA, cc * 32, kx - a.pad, y0 + ky - a.pad, n0, 0,
+                                             &full[s]);
+                        else
+                            ptx::tma_load_5d(sa, &tmA, cc * 32, a.pad - kx, y0 + a.pad - ky, n0, 0,
+                                             &full[s]);
+                        ptx::tma_load_3d(sb, &tmB, kb * 32, int(nt) * NT, 0, &full[s]);
+                    } else {
+                        const int n = kb / a.kpi, r = kb - n * a.kpi;
+                        const int yb = (r / a.kpr) * a.OHb, xb = (r % a.kpr) * a.OWb;
+                        for (int sl = 0; sl < a.slots; ++sl) {
+                            int tap = int(mt) * a.slots + sl;
+                            if (tap >= a.taps) tap = a.taps - 1;  // rows >= M: discarded
+                            const int ky = tap / a.KW, kx = tap - ky * a.KW;
+                            ptx::tma_load_5d(sa + sl * (D * kIKB * a.C), &tmA, 0, xb + kx - a.pad,
+                                             yb + ky - a.pad, n, 0, &full[s]);
+                        }
+                        ptx::tma_load_5d(sb, &tmB, int(nt) * NT, xb, yb, n, 0, &full[s]);
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            // ===== MMA issuer =====
+            constexpr uint32_t idesc = ptx::idesc_i8(kBM, Geo::NMMA, MODE == 2, MODE == 2);
+            // all-zero A operand for initialising groups D-1 .. 2D-2 (layout-agnostic:
+            // the footprint of either major's no-swizzle layout stays inside the tile)
+            const uint64_t zdesc = MODE == 2
+                                       ? ptx::smem_desc_sw(ptx::smem_u32(zero_tile), 1024, 128, 0)
+                                       : ptx::smem_desc_kmajor(ptx::smem_u32(zero_tile), 128, 8 * 32);
+            const uint32_t a_lt = ptx::swizzle_layout_type(a.a_sw);
+            const uint32_t b_lt = ptx::swizzle_layout_type(a.b_sw);
+            uint32_t it = 0, j = 0;
+            for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++j) {
+                int64_t split, mt, nt;
+                tile_coords(t, a.mtiles, a.ntiles, split, mt, nt);
+                const int64_t kb0 = split * a.kb_per_split;
+                const int nkb = int(min(a.kbt, kb0 + a.kb_per_split) - kb0);
+                ptx::mbar_wait(tmem_empty, (j & 1) ^ 1);
+                ptx::tc_fence_after();
+                for (int i = 0; i < nkb; ++i, ++it) {
+                    const int s = it % STAGES;
+                    const uint32_t ph = (it / STAGES) & 1;
+                    ptx::mbar_wait(&full[s], ph);
+                    ptx::tc_fence_after();
+                    const uint32_t a_base = ptx::smem_u32(smem + s * Geo::STAGE_BYTES);
+                    const uint32_t b_base = a_base + Geo::A_BYTES;
+                    uint64_t bdesc;
+                    if constexpr (MODE == 2)  // D planes of NT columns, one MN atom each
+                        bdesc = ptx::smem_desc_sw(b_base, kIKB * a.b_sw, 8 * a.b_sw, b_lt);
+                    else
+                        bdesc = ptx::smem_desc_sw(b_base, 16, 8 * kIKB, b_lt);
+                    const bool first = i == 0;
+                    if (first) ptx::mma_i8(tmem + (D - 1) * NT, zdesc, bdesc, idesc, 0);
+#pragma unroll
+                    for (int p = 0; p < D; ++p) {
+                        uint64_t adesc;
+                        if constexpr (MODE == 2)  // slots of C channels, each an MN atom
+                            adesc = ptx::smem_desc_sw(a_base + p * (kIKB * a.a_sw),
+                                                      D * kIKB * a.a_sw, 8 * a.a_sw, a_lt);
+                        else
+                            adesc = ptx::smem_desc_sw(a_base + p * (kBM * kIKB), 16, 8 * kIKB, a_lt);
+                        ptx::mma_i8(tmem + p * NT, adesc, bdesc, idesc, (first && p == 0) ? 0u : 1u);
+                    }
+                    ptx::mma_commit(&empty[s]);
+                }
+                ptx::mma_commit(tmem_full);
+            }
+        }
+    } else {
+        // ===== epilogue: TMEM -> quire words -> posit codes / split-K partials =====
+        const int quarter = warp & 3;
+        const int half = (warp - 2) >> 2;
+        const uint32_t trow = tmem + (uint32_t(quarter * 32) << 16) + half * COLS;
+        uint32_t j = 0;
+        for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++j) {
+            int64_t split, mt, nt;
+            tile_coords(t, a.mtiles, a.ntiles, split, mt, nt);
+            ptx::mbar_wait(tmem_full, j & 1);
+            ptx::tc_fence_after();
+            QT q[COLS];
+#pragma unroll
+            for (int c = 0; c < COLS; ++c) q[c] = 0;
+#pragma unroll
+            for (int c0 = 0; c0 < COLS; c0 += 8) {
+#pragma unroll
+                for (int g0 = 0; g0 < G; g0 += GB) {
+                    uint32_t r[GB][8];
+#pragma unroll
+                    for (int g = 0; g < GB; ++g)
+                        if (g0 + g < G) ptx::tmem_ld8(trow + (g0 + g) * NT + c0, r[g]);
+                    ptx::tmem_wait_ld();
+#pragma unroll
+                    for (int g = 0; g < GB; ++g)
+                        if (g0 + g < G)
+#pragma unroll
+                            for (int x = 0; x < 8; ++x) q[c0 + x] += group_term<QT>(r[g][x], 8 * (g0 + g));
+                }
+            }
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(tmem_empty);
+
+            const int64_t row = mt * kBM + quarter * 32 + lane;
+            if (row >= a.M) continue;
+            const int64_t colbase = nt * NT + half * COLS;
+            if constexpr (MODE == 0) if (a.col_add != nullptr && split == 0) {
+#pragma unroll
+                for (int c = 0; c < COLS; ++c)
+                    if (colbase + c < a.N) {
+                        const int64_t xb = a.col_add[colbase + c];
+                        if constexpr (QW == 4) q[c] += QT(__int128(xb)) << a.f.R;
+                        else q[c] += QT(xb) << a.f.R;
+                    }
+            }
+#pragma unroll
+            for (int c0 = 0; c0 < COLS; c0 += 8) {
+                const int64_t col0 = colbase + c0;
+                if (col0 >= a.N) break;
+                const int valid = int(a.N - col0 < 8 ? a.N - col0 : 8);
+                if (a.partial != nullptr) {
+                    unsigned __int128* dst = a.partial + (split * a.M + row) * a.N + col0;
+#pragma unroll
+                    for (int x = 0; x < 8; ++x)
+                        if (x < valid) dst[x] = (unsigned __int128)q[c0 + x];
+                    continue;
+                }
+#pragma unroll
+                for (int x = 0; x < 8; ++x)
+                    if (x < valid) {
+                        const bool nar = a.col_nar != nullptr && a.col_nar[col0 + x];
+                        out.base[out.index(row, col0 + x)] =
+                            CodeT(nar ? (1u << (a.f.nbits - 1)) : quire_word_to_posit(a.f, q[c0 + x]));
+                    }
+            }
+        }
+    }
+    __syncwarp();
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc<512>(tmem);
+    }
+}
+
+// ------------------------------------------------------------- digitising
+
+// codes [N][C][H][W] -> dig[D][N][H][W][Cp] (balanced int8 digits; channels
+// >= C are zero), plus NaR summaries written only where a NaR is found:
+// pos_nar[n][h][w] (any channel), chw_nar[c][h][w] (any image), chan_nar[c],
+// *any.  One block per (n, h) image row; coalesced 32-channel x W tiles.
+template <int D, typename CodeT>
+__global__ void __launch_bounds__(256) act_digits_kernel(
+    const CodeT* __restrict__ x, int64_t N, int C, int H, int W, int Cp, PositFmt f,
+    int8_t* __restrict__ dig, uint8_t* __restrict__ pos_nar, uint8_t* __restrict__ chw_nar,
+    uint8_t* __restrict__ chan_nar, uint8_t* __restrict__ any) {
+    __shared__ CodeT tile[32 * 257];
+    __shared__ uint32_t lut[2 << kLutMaxBits];
+    const bool use_lut = f.nbits <= kLutMaxBits;
+    if (use_lut) {
+        for (int c = threadIdx.x; c < (1 << f.nbits); c += blockDim.x) {
+            uint32_t lo, hi;
+            bool nar;
+            digit_words<D>(uint32_t(c), f, lo, hi, nar);
+            lut[2 * c] = lo;
+            lut[2 * c + 1] = hi;
+        }
+    }
+    const uint32_t nar_code = 1u << (f.nbits - 1);
+    const int64_t HW = int64_t(H) * W;
+    const int64_t plane = N * HW * Cp;
+    const int LDT = W + 1;
+    for (int64_t rowi = blockIdx.x; rowi < N * H; rowi += gridDim.x) {
+        const int64_t n = rowi / H;
+        const int h = int(rowi - n * H);
+        for (int c0 = 0; c0 < Cp; c0 += 32) {
+            __syncthreads();
+            for (int i = threadIdx.x; i < 32 * W; i += blockDim.x) {
+                const int cl = i / W, w = i - cl * W;
+                const int c = c0 + cl;
+                tile[cl * LDT + w] = c < C ? x[((n * C + c) * H + h) * W + w] : CodeT(0);
+            }
+            __syncthreads();
+            for (int i = threadIdx.x; i < W * 8; i += blockDim.x) {
+                const int w = i >> 3, q = i & 7;
+                uint32_t lo[4], hi[4];
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj) {
+                    const int cl = 4 * q + jj;
+                    const uint32_t code = uint32_t(tile[cl * LDT + w]);
+                    bool nar;
+                    if (use_lut) {
+                        lo[jj] = lut[2 * code];
+                        hi[jj] = lut[2 * code + 1];
+                        nar = code == nar_code;
+                    } else {
+                        digit_words<D>(code, f, lo[jj], hi[jj], nar);
+                    }
+                    if (nar && c0 + cl < C) {
+                        const int c = c0 + cl;
+                        if (pos_nar) pos_nar[n * HW + int64_t(h) * W + w] = 1;
+                        if (chw_nar) chw_nar[int64_t(c) * HW + int64_t(h) * W + w] = 1;
+                        if (chan_nar) chan_nar[c] = 1;
+                        *any = 1;
+                    }
+                }
+                int8_t* dst = dig + ((n * H + h) * W + w) * Cp + c0 + 4 * q;
+#pragma unroll
+                for (int p = 0; p < D; ++p) {
+                    const int sh = 8 * (p & 3);
+                    uint32_t v = 0;
+#pragma unroll
+                    for (int jj = 0; jj < 4; ++jj)
+                        v |= (((p < 4 ? lo[jj] : hi[jj]) >> sh) & 0xFFu) << (8 * jj);
+                    *reinterpret_cast<uint32_t*>(dst + p * plane) = v;
+                }
+            }
+        }
+    }
+}
+
+// w [F][C][KH][KW] -> K-major weight digits dig[D][rows][taps * Kp]:
+//   transpose = 0 (forward):    rows = F, element (f, tap, c) = w[f][c][tap]
+//   transpose = 1 (input grad): rows = C, element (c, tap, f) = w[f][c][tap]
+// Forward: col_add[f] = X(bias[f]), col_nar[f] = NaR in weight row f or bias f.
+template <int D, typename CodeT>
+__global__ void weight_digits_kernel(const CodeT* __restrict__ w, const CodeT* __restrict__ bias,
+                                     int F, int C, int taps, int Kp, int transpose, PositFmt f,
+                                     int8_t* __restrict__ dig, int64_t* __restrict__ col_add,
+                                     uint8_t* __restrict__ col_nar, uint8_t* __restrict__ any) {
+    const int rows = transpose ? C : F;
+    const int inner = transpose ? F : C;
+    const int64_t total = int64_t(rows) * taps * Kp;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        const int k = int(i % Kp);
+        const int tap = int((i / Kp) % taps);
+        const int r = int(i / (int64_t(Kp) * taps));
+        uint32_t code = 0;
+        if (k < inner) {
+            const int fo = transpose ? k : r, ci = transpose ? r : k;
+            code = uint32_t(w[(int64_t(fo) * C + ci) * taps + tap]);
+        }
+        uint32_t lo, hi;
+        bool nar;
+        digit_words<D>(code, f, lo, hi, nar);
+        if (nar) {
+            if (col_nar && !transpose) col_nar[r] = 1;
+            *any = 1;
+        }
+#pragma unroll
+        for (int p = 0; p < D; ++p)
+            dig[int64_t(p) * total + i] = int8_t(((p < 4 ? lo : hi) >> (8 * (p & 3))) & 0xFFu);
+    }
+    if (!transpose && col_add != nullptr) {
+        for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r < F;
+             r += int64_t(gridDim.x) * blockDim.x) {
+            int64_t X = 0;
+            const bool nar = bias != nullptr && decode_x(uint32_t(bias[r]), f, X);
+            col_add[r] = X;
+            if (nar) col_nar[r] = 1;
+        }
+    }
+}
+
+// ------------------------------------------------------------- NaR fix-ups
+
+// Weight-side NaR of the input gradient, exact per output over its valid taps.
+// Runs only when the pack pass saw a NaR weight (flag set on device).
+template <typename CodeT>
+__global__ void dgrad_weight_nar_kernel(CodeT* __restrict__ dx, const CodeT* __restrict__ w,
+                                        ConvGeom g, const uint8_t* __restrict__ any_nar_w,
+                                        uint32_t nar) {
+    if (*any_nar_w == 0) return;
+    const int64_t total = g.N * g.C * g.H * g.W;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t ix = i % g.W, iy = (i / g.W) % g.H, c = (i / (g.W * g.H)) % g.C;
+        bool hit = false;
+        for (int64_t f = 0; f < g.F && !hit; ++f)
+            for (int64_t ky = 0; ky < g.KH && !hit; ++ky) {
+                const int64_t ty = iy + g.pad - ky;
+                if (ty < 0 || ty % g.stride || ty / g.stride >= g.OH) continue;
+                for (int64_t kx = 0; kx < g.KW; ++kx) {
+                    const int64_t tx = ix + g.pad - kx;
+                    if (tx < 0 || tx % g.stride || tx / g.stride >= g.OW) continue;
+                    if (uint32_t(w[((f * g.C + c) * g.KH + ky) * g.KW + kx]) == nar) {
+                        hit = true;
+                        break;
+                    }
+                }
+            }
+        if (hit) dx[i] = CodeT(nar);
+    }
+}
+
+// Row NaR of the implicit passes (an output is NaR iff one of its terms has a
+// NaR operand, quire.hpp:55); launched always, exit at once unless the
+// digitiser saw a NaR.
+
+// forward: y[n][:][oy][ox] = NaR if a tap in range reads a NaR pixel
+template <typename CodeT>
+__global__ void fwd_nar_fixup_kernel(CodeT* __restrict__ y, const uint8_t* __restrict__ pos_nar,
+                                     const uint8_t* __restrict__ any, int64_t N, int F, int H,
+                                     int W, int OH, int OW, int KH, int KW, int pad, uint32_t nar) {
+    if (*any == 0) return;
+    const int64_t total = N * OH * OW;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        const int ox = int(i % OW), oy = int((i / OW) % OH);
+        const int64_t n = i / (int64_t(OH) * OW);
+        bool hit = false;
+        for (int ky = 0; ky < KH && !hit; ++ky)
+            for (int kx = 0; kx < KW && !hit; ++kx) {
+                const int iy = oy + ky - pad, ix = ox + kx - pad;
+                if (unsigned(iy) < unsigned(H) && unsigned(ix) < unsigned(W))
+                    hit = pos_nar[(n * H + iy) * W + ix] != 0;
+            }
+        if (hit)
+            for (int fo = 0; fo < F; ++fo) y[((n * F + fo) * OH + oy) * OW + ox] = CodeT(nar);
+    }
+}
+
+// input grad: dx[n][:][iy][ix] = NaR if a valid tap reads a NaR output gradient
+template <typename CodeT>
+__global__ void dgrad_nar_fixup_kernel(CodeT* __restrict__ dx, const uint8_t* __restrict__ pos_nar,
+                                       const uint8_t* __restrict__ any, int64_t N, int C, int H,
+                                       int W, int OH, int OW, int KH, int KW, int pad, uint32_t nar) {
+    if (*any == 0) return;
+    const int64_t total = N * H * W;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        const int ix = int(i % W), iy = int((i / W) % H);
+        const int64_t n = i / (int64_t(H) * W);
+        bool hit = false;
+        for (int ky = 0; ky < KH && !hit; ++ky)
+            for (int kx = 0; kx < KW && !hit; ++kx) {
+                const int oy = iy + pad - ky, ox = ix + pad - kx;
+                if (unsigned(oy) < unsigned(OH) && unsigned(ox) < unsigned(OW))
+                    hit = pos_nar[(n * OH + oy) * OW + ox] != 0;
+            }
+        if (hit)
+            for (int c = 0; c < C; ++c) dx[((n * C + c) * H + iy) * W + ix] = CodeT(nar);
+    }
+}
+
+// weight grad: dw[:][c][tap] = NaR if the tap's window over channel c holds a NaR
+template <typename CodeT>
+__global__ void wgrad_nar_fixup_kernel(CodeT* __restrict__ dw, uint8_t* __restrict__ raw_nar,
+                                       const uint8_t* __restrict__ chw_nar,
+                                       const uint8_t* __restrict__ any, int F, int C, int H, int W,
+                                       int OH, int OW, int KH, int KW, int pad, uint32_t nar) {
+    if (*any == 0) return;
+    const int taps = KH * KW;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < C * taps; i += gridDim.x * blockDim.x) {
+        const int c = i / taps, tap = i % taps, ky = tap / KW, kx = tap % KW;
+        bool hit = false;
+        for (int oy = 0; oy < OH && !hit; ++oy) {
+            const int iy = oy + ky - pad;
+            if (unsigned(iy) >= unsigned(H)) continue;
+            for (int ox = 0; ox < OW; ++ox) {
+                const int ix = ox + kx - pad;
+                if (unsigned(ix) < unsigned(W) && chw_nar[(int64_t(c) * H + iy) * W + ix]) {
+                    hit = true;
+                    break;
+                }
+            }
+        }
+        if (hit)
+            for (int fo = 0; fo < F; ++fo) {
+                const int64_t o = (int64_t(fo) * C + c) * taps + tap;
+                if (dw) dw[o] = CodeT(nar);
+                if (raw_nar) raw_nar[o] = 1;
+            }
+    }
+}
+
+}  // namespace pnn_b200

@@ -293,7 +293,8 @@ __global__ void __launch_bounds__(256) pack_kernel(Fetch fetch, int64_t rows_tot
 // ------------------------------------------------------------- main kernel
 
 // Where output element (m, n) lives: mode 0 row-major (m*ldc + n); mode 1
-// NCHW scatter for convolutions (m = img*inner + pixel, n = channel).
+// NCHW scatter for convolutions (m = img*inner + pixel, n = channel); mode 2
+// tap-major weight-gradient rows (m = tap*inner + c -> n*ldc + c*ncols + tap).
 template <typename CodeT>
 struct OutMap {
     CodeT* base;
@@ -303,8 +304,9 @@ struct OutMap {
     int mode;
     __device__ __forceinline__ int64_t index(int64_t m, int64_t n) const {
         if (mode == 0) return m * ldc + n;
-        const int64_t img = m / inner, pix = m - img * inner;
-        return (img * ncols + n) * inner + pix;
+        const int64_t hi = m / inner, lo = m - hi * inner;
+        if (mode == 2) return n * ldc + lo * ncols + hi;
+        return (hi * ncols + n) * inner + lo;
     }
 };
 

@@ -191,13 +191,59 @@ __device__ __forceinline__ uint64_t smem_desc_kmajor(uint32_t saddr, uint32_t lb
     return d;
 }
 
-// Instruction descriptor: kind::i8, s8 x s8 -> s32, both K-major, M x N.
-__host__ __device__ constexpr uint32_t idesc_i8(int M, int N) {
+// Swizzled descriptor (layout type: 6 = 32B, 4 = 64B, 2 = 128B swizzle).
+// K-major: SBO = 8-row-group stride, LBO unused (one atom spans the MMA's K).
+// MN-major: LBO = stride between MN atoms, SBO = stride between 8-deep K groups.
+__device__ __forceinline__ uint64_t smem_desc_sw(uint32_t saddr, uint32_t lbo, uint32_t sbo,
+                                                 uint32_t layout) {
+    uint64_t d = 0;
+    d |= uint64_t((saddr >> 4) & 0x3FFF);
+    d |= uint64_t((lbo >> 4) & 0x3FFF) << 16;
+    d |= uint64_t((sbo >> 4) & 0x3FFF) << 32;
+    d |= uint64_t(1) << 46;
+    d |= uint64_t(layout & 7) << 61;
+    return d;
+}
+
+__host__ __device__ constexpr uint32_t swizzle_layout_type(int bytes) {
+    return bytes == 32 ? 6u : bytes == 64 ? 4u : bytes == 128 ? 2u : 0u;
+}
+
+// Instruction descriptor: kind::i8, s8 x s8 -> s32, M x N; operands K-major
+// unless a_mn / b_mn (MN-major, bits 15 / 16).
+__host__ __device__ constexpr uint32_t idesc_i8(int M, int N, bool a_mn = false, bool b_mn = false) {
     return (2u << 4)                      // c_format = S32
            | (1u << 7)                    // a_format = signed int8
            | (1u << 10)                   // b_format = signed int8
+           | (a_mn ? 1u << 15 : 0u)       // a_major
+           | (b_mn ? 1u << 16 : 0u)       // b_major
            | (uint32_t(N >> 3) << 17)     // N / 8
            | (uint32_t(M >> 4) << 24);    // M / 16
+}
+
+// ---- TMA tensor (tiled) loads: box at signed element coordinates, out-of-
+// range elements zero-filled (this is the convolution's zero padding) -------
+
+__device__ __forceinline__ void tma_load_5d(void* smem_dst, const void* tmap, int c0, int c1, int c2,
+                                            int c3, int c4, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_u32(smem_dst)),
+        "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_load_3d(void* smem_dst, const void* tmap, int c0, int c1, int c2,
+                                            uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(smem_dst)),
+        "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_prefetch_desc(const void* tmap) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(tmap) : "memory");
 }
 
 }  // namespace ptx

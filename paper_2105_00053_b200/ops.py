@@ -213,6 +213,16 @@ def pack_round(cfg, neg, scale, sig, sticky):
 
 # ---- Conv2d / Linear passes (tensor_ops.hpp:34-42, 61) ----------------------
 
+def conv_algo(algo: int) -> int:
+    """Select the conv implementation (pnn_conv_algo): 0 auto (implicit GEMM
+    where eligible), 1 explicit im2col pack, 2 implicit only.  Returns the
+    previous setting.  Results are bit-identical either way."""
+    prev = _native.lib().pnn_conv_algo(int(algo))
+    if prev < 0:
+        raise _native.PnnInvalidArgument(1, "conv_algo: 0, 1 or 2")
+    return prev
+
+
 def _conv_ws(pass_, cfg, N, Cc, H, W, F, KH, KW, stride, pad, has_bias):
     n = C.c_size_t()
     _native.check(_native.lib().pnn_conv2d_workspace(pass_, cfg.nbits, cfg.es, N, Cc, H, W, F, KH, KW,
