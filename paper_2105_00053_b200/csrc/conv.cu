@@ -245,20 +245,23 @@ __global__ void __launch_bounds__(256) bias_grad_partial_kernel(
             acc += X;
         }
     }
-    __shared__ unsigned long long lo_s[256], hi_s[256];
-    __shared__ int nar_s;
-    if (threadIdx.x == 0) nar_s = 0;
-    __syncthreads();
-    if (nar) nar_s = 1;
-    lo_s[threadIdx.x] = (unsigned long long)(uint64_t(acc));
-    hi_s[threadIdx.x] = (unsigned long long)(uint64_t((unsigned __int128)acc >> 64));
+    // block reduction: 128-bit butterfly per warp, then one word per warp
+    __shared__ unsigned __int128 warp_s[8];
+    unsigned __int128 s = (unsigned __int128)acc;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const uint64_t l2 = __shfl_xor_sync(0xFFFFFFFFu, uint64_t(s), o);
+        const uint64_t h2 = __shfl_xor_sync(0xFFFFFFFFu, uint64_t(s >> 64), o);
+        s += (unsigned __int128)l2 | ((unsigned __int128)h2 << 64);
+    }
+    nar = __syncthreads_or(nar) != 0;
+    if ((threadIdx.x & 31) == 0) warp_s[threadIdx.x >> 5] = s;
     __syncthreads();
     if (threadIdx.x == 0) {
-        unsigned __int128 s = 0;
-        for (int i = 0; i < blockDim.x; ++i)
-            s += (unsigned __int128)lo_s[i] | ((unsigned __int128)hi_s[i] << 64);
-        partial[ch * slices + slice] = s;
-        if (nar_s) nar_out[ch] = 1;
+        unsigned __int128 t = 0;
+        for (int i = 0; i < int(blockDim.x >> 5); ++i) t += warp_s[i];
+        partial[ch * slices + slice] = t;
+        if (nar) nar_out[ch] = 1;
     }
 }
 

@@ -93,35 +93,106 @@ __global__ void maxpool_bwd_kernel(PositFmt f, int b, const void* dy, const int6
         for (int64_t oy = oy0; oy <= oy1; ++oy)
             for (int64_t ox = ox0; ox <= ox1; ++ox) {
                 const int64_t o = (nc * OH + oy) * OW + ox;
-                if (argmax[o] == t) acc = p_add(f, acc, load_any(dy, o, b));
+                if (argmax[o] == t) {  // add(0, v) == v exactly (NaR included)
+                    const uint32_t v = load_any(dy, o, b);
+                    acc = acc == 0 ? v : p_add(f, acc, v);
+                }
             }
         store_any(dx, t, b, acc);
     }
 }
 
-// Softmax cross-entropy in the loss format, one row
-// per thread:  m = max z;  e_j = exp(z_j - m);  S = round(quire sum e_j);
+// Exactly tiled pooling (k == stride, H = OH*k, W = OW*k): each input lies in
+// exactly one window, so a thread per window writes its k x k inputs (argmax
+// position gets dy, the rest 0 -- the same values as the general kernel).
+// 32-bit index math (the callers check the sizes).
+__global__ void maxpool_bwd_tiled_kernel(int b, const void* dy, const int64_t* argmax, int NC,
+                                         int OH, int OW, int k, void* dx) {
+    const int W = OW * k, H = OH * k;
+    const int total = NC * OH * OW;
+    for (int o = blockIdx.x * blockDim.x + threadIdx.x; o < total; o += gridDim.x * blockDim.x) {
+        const int ox = o % OW, t = o / OW, oy = t % OH, nc = t / OH;
+        const int64_t base = (int64_t(nc) * H + oy * k) * W + ox * k;
+        const int64_t am = argmax[o];
+        const uint32_t v = load_any(dy, o, b);
+        for (int ky = 0; ky < k; ++ky)
+            for (int kx = 0; kx < k; ++kx) {
+                const int64_t idx = base + int64_t(ky) * W + kx;
+                store_any(dx, idx, b, idx == am ? v : 0u);
+            }
+    }
+}
+
+__global__ void maxpool_fwd_tiled_kernel(PositFmt f, int b, const void* x, int NC, int OH, int OW,
+                                         int k, void* y, int64_t* argmax) {
+    const int W = OW * k, H = OH * k;
+    const int total = NC * OH * OW;
+    for (int o = blockIdx.x * blockDim.x + threadIdx.x; o < total; o += gridDim.x * blockDim.x) {
+        const int ox = o % OW, t = o / OW, oy = t % OH, nc = t / OH;
+        const int64_t base = (int64_t(nc) * H + oy * k) * W + ox * k;
+        int64_t best = base;
+        uint32_t bv = load_any(x, best, b);
+        for (int ky = 0; ky < k; ++ky)
+            for (int kx = 0; kx < k; ++kx) {
+                const int64_t idx = base + int64_t(ky) * W + kx;
+                const uint32_t v = load_any(x, idx, b);
+                if (p_compare(f, v, bv) > 0) {
+                    best = idx;
+                    bv = v;
+                }
+            }
+        store_any(y, o, b, bv);
+        argmax[o] = best;
+    }
+}
+
+// Softmax cross-entropy in the loss format:
+//   m = max z;  e_j = exp(z_j - m);  S = round(quire sum e_j);
 // p_j = e_j / S;  loss_i = log(S) - (z_y - m);
 // dlogits_j = ldexp(p_j - [j==y], -log2_batch).
+// One warp per row, lanes over classes: the max (a total order on codes, so
+// any reduction order gives the same value), the exact integer sum of e_j
+// (butterfly over 128-bit lanes), one rounding, then p_j per lane.
 __global__ void softmax_xent_kernel(PositFmt f, int b, const void* logits, const int32_t* labels,
                                     int64_t B, int64_t Cn, int log2_batch, void* dlogits,
                                     void* loss_rows) {
-    GRID_STRIDE(i, B) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t i = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5; i < B; i += nwarps) {
         const int64_t row = i * Cn;
         uint32_t m = load_any(logits, row, b);
-        for (int64_t j = 1; j < Cn; ++j) {
+        for (int64_t j = lane; j < Cn; j += 32) {
             const uint32_t v = load_any(logits, row + j, b);
             if (p_compare(f, v, m) > 0) m = v;
         }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const uint32_t v = __shfl_xor_sync(0xFFFFFFFFu, m, o);
+            if (p_compare(f, v, m) > 0) m = v;
+        }
         // S = quire sum of e_j: exact in the integer image, one rounding
-        __int128 sx = 0;
+        uint64_t lo = 0, hi = 0;
         bool nar = false;
-        for (int64_t j = 0; j < Cn; ++j) {
+        uint32_t e0 = 0;  // this lane's first e_j, reused below
+        for (int64_t j = lane; j < Cn; j += 32) {
             const uint32_t e = p_exp(f, p_sub(f, load_any(logits, row + j, b), m));
+            if (j == lane) e0 = e;
             int64_t X;
             nar |= decode_x(e, f, X);
-            sx += X;
+            const unsigned __int128 s = ((unsigned __int128)hi << 64 | lo) + (unsigned __int128)(__int128)X;
+            lo = uint64_t(s);
+            hi = uint64_t(s >> 64);
         }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const uint64_t l2 = __shfl_xor_sync(0xFFFFFFFFu, lo, o);
+            const uint64_t h2 = __shfl_xor_sync(0xFFFFFFFFu, hi, o);
+            const unsigned __int128 s = ((unsigned __int128)hi << 64 | lo) + ((unsigned __int128)h2 << 64 | l2);
+            lo = uint64_t(s);
+            hi = uint64_t(s >> 64);
+        }
+        nar = __any_sync(0xFFFFFFFFu, nar);
+        const __int128 sx = (__int128)((unsigned __int128)hi << 64 | lo);
         uint32_t S;
         if (nar) {
             S = nar_of(f);
@@ -131,14 +202,16 @@ __global__ void softmax_xent_kernel(PositFmt f, int b, const void* logits, const
         }
         const int32_t y = labels[i];
         const uint32_t one = p_from_int64(f, 1);
-        for (int64_t j = 0; j < Cn; ++j) {
-            const uint32_t e = p_exp(f, p_sub(f, load_any(logits, row + j, b), m));
+        for (int64_t j = lane; j < Cn; j += 32) {
+            const uint32_t e = j == lane ? e0 : p_exp(f, p_sub(f, load_any(logits, row + j, b), m));
             const uint32_t pj = p_div(f, e, S);
             const uint32_t g = p_sub(f, pj, j == y ? one : 0u);
             store_any(dlogits, row + j, b, p_ldexp(f, g, -log2_batch));
         }
-        const uint32_t zy = load_any(logits, row + y, b);
-        store_any(loss_rows, i, b, p_sub(f, p_log(f, S), p_sub(f, zy, m)));
+        if (lane == 0) {
+            const uint32_t zy = load_any(logits, row + y, b);
+            store_any(loss_rows, i, b, p_sub(f, p_log(f, S), p_sub(f, zy, m)));
+        }
     }
 }
 
@@ -344,8 +417,12 @@ int pnn_maxpool2d_fwd(int nbits, int es, const void* x, int64_t N, int64_t C, in
         return set_status(PNN_EINVAL, "maxpool2d: window larger than input");
     const int64_t OH = (H - k) / stride + 1, OW = (W - k) / stride + 1;
     if (N == 0) return PNN_OK;
-    maxpool_fwd_kernel<<<grid1(N * C * OH * OW), 256, 0, (cudaStream_t)stream>>>(
-        make_fmt(nbits, es), bytes_of(nbits), x, N * C, H, W, k, stride, OH, OW, y, argmax);
+    if (k == stride && H == OH * k && W == OW * k && N * C * H * W < (int64_t(1) << 31))
+        maxpool_fwd_tiled_kernel<<<grid1(N * C * OH * OW), 256, 0, (cudaStream_t)stream>>>(
+            make_fmt(nbits, es), bytes_of(nbits), x, int(N * C), int(OH), int(OW), k, y, argmax);
+    else
+        maxpool_fwd_kernel<<<grid1(N * C * OH * OW), 256, 0, (cudaStream_t)stream>>>(
+            make_fmt(nbits, es), bytes_of(nbits), x, N * C, H, W, k, stride, OH, OW, y, argmax);
     return launched("maxpool2d_fwd");
 }
 
@@ -356,8 +433,12 @@ int pnn_maxpool2d_bwd(int nbits, int es, const void* dy, const int64_t* argmax, 
         return set_status(PNN_EINVAL, "maxpool2d_backward: bad shape");
     const int64_t OH = (H - k) / stride + 1, OW = (W - k) / stride + 1;
     if (N == 0) return PNN_OK;
-    maxpool_bwd_kernel<<<grid1(N * C * H * W), 256, 0, (cudaStream_t)stream>>>(
-        make_fmt(nbits, es), bytes_of(nbits), dy, argmax, N * C, H, W, k, stride, OH, OW, dx);
+    if (k == stride && H == OH * k && W == OW * k && N * C * H * W < (int64_t(1) << 31))
+        maxpool_bwd_tiled_kernel<<<grid1(N * C * OH * OW), 256, 0, (cudaStream_t)stream>>>(
+            bytes_of(nbits), dy, argmax, int(N * C), int(OH), int(OW), k, dx);
+    else
+        maxpool_bwd_kernel<<<grid1(N * C * H * W), 256, 0, (cudaStream_t)stream>>>(
+            make_fmt(nbits, es), bytes_of(nbits), dy, argmax, N * C, H, W, k, stride, OH, OW, dx);
     return launched("maxpool2d_bwd");
 }
 
@@ -369,7 +450,7 @@ int pnn_softmax_xent(int nbits, int es, const void* logits, const int32_t* label
         return set_status(PNN_EINVAL, "softmax_xent: bad arguments");
     const PositFmt f = make_fmt(nbits, es);
     auto st = (cudaStream_t)stream;
-    softmax_xent_kernel<<<grid1(B), 256, 0, st>>>(f, bytes_of(nbits), logits, labels, B, classes,
+    softmax_xent_kernel<<<grid1(B * 32), 256, 0, st>>>(f, bytes_of(nbits), logits, labels, B, classes,
                                                   log2_batch, dlogits, loss_rows);
     if (loss_out || raw_word)
         loss_reduce_kernel<<<1, 256, 0, st>>>(f, bytes_of(nbits), loss_rows, B, log2_batch,

@@ -53,7 +53,7 @@ struct ImplPlan {
     int64_t Kp, brows;      // modes 0/1: B digits [D][brows][taps * Kp]
     int64_t Fpw;            // mode 2: B digits [D][N][OH][OW][Fpw]
     size_t adig, bdig;      // bytes
-    size_t off_adig, off_bdig, off_col_add, off_maps, maps_bytes, off_pos_nar, off_chw_nar,
+    size_t off_adig, off_bdig, off_col_add, off_lut, off_maps, maps_bytes, off_pos_nar, off_chw_nar,
         off_col_nar, off_flags, off_partial, total;
 };
 
@@ -169,6 +169,7 @@ bool make_plan(int pass, const PositFmt& f, const ConvGeom& g, bool raw, ImplPla
     p->off_adig = take(p->adig);
     p->off_bdig = take(p->bdig);
     p->off_col_add = take(col_add);
+    p->off_lut = take(f.nbits <= kActLutBits ? size_t(8) << f.nbits : 0);
     p->off_maps = off;  // NaR maps and flags: zeroed by one memset
     p->off_pos_nar = take(pos_nar);
     p->off_chw_nar = take(chw_nar);
@@ -178,6 +179,10 @@ bool make_plan(int pass, const PositFmt& f, const ConvGeom& g, bool raw, ImplPla
     p->off_partial = take(partial);
     p->total = off;
     return true;
+}
+
+uint32_t* lut_of(const ImplPlan& p, uint8_t* ws) {
+    return p.a.f.nbits <= kActLutBits ? reinterpret_cast<uint32_t*>(ws + p.off_lut) : nullptr;
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encoder() {
@@ -261,13 +266,17 @@ cudaError_t dispatch(int D, const CUtensorMap& tA, const CUtensorMap& tB, const 
 
 template <typename CodeT>
 cudaError_t act_digits(int D, const CodeT* x, int64_t N, int64_t C, int64_t H, int64_t W,
-                       int64_t Cp, const PositFmt& f, int8_t* dig, uint8_t* pos_nar,
-                       uint8_t* chw_nar, uint8_t* chan_nar, uint8_t* any, cudaStream_t st) {
-    const int64_t rows = N * H;
-    const int grid = int(rows < 148 * 16 ? rows : 148 * 16);
+                       int64_t Cp, const PositFmt& f, uint32_t* lut, bool build_lut, int8_t* dig,
+                       uint8_t* pos_nar, uint8_t* chw_nar, uint8_t* chan_nar, uint8_t* any,
+                       cudaStream_t st) {
+    const int64_t RH = W >= kSlab ? 1 : (kSlab / W < H ? kSlab / W : H);
+    const int64_t items = N * ((H + RH - 1) / RH) * ((W + kSlab - 1) / kSlab);
+    const int grid = int(items < 148 * 16 ? items : 148 * 16);
+    if (lut == nullptr) build_lut = false;
 #define PNN_ACT(DD)                                                                              \
+    if (build_lut) digit_lut_kernel<DD><<<16, 256, 0, st>>>(f, lut);                             \
     act_digits_kernel<DD, CodeT><<<grid, 256, 0, st>>>(x, N, int(C), int(H), int(W), int(Cp), f, \
-                                                       dig, pos_nar, chw_nar, chan_nar, any)
+                                                       lut, dig, pos_nar, chw_nar, chan_nar, any)
     switch (D) {
         case 2: PNN_ACT(2); break;
         case 3: PNN_ACT(3); break;
@@ -320,7 +329,7 @@ int run_fwd(const ImplPlan& p, const ConvGeom& g, const CodeT* x, const CodeT* w
     uint8_t* flags = ws + p.off_flags;
     cudaError_t e;
     if ((e = cudaMemsetAsync(ws + p.off_maps, 0, p.maps_bytes, st)) != cudaSuccess) return 4;
-    if ((e = act_digits<CodeT>(p.D, x, g.N, g.C, g.H, g.W, p.Ca, f, adig, pos_nar, nullptr,
+    if ((e = act_digits<CodeT>(p.D, x, g.N, g.C, g.H, g.W, p.Ca, f, lut_of(p, ws), true, adig, pos_nar, nullptr,
                                nullptr, flags, st)) != cudaSuccess)
         return 4;
     const int64_t taps = g.KH * g.KW;
@@ -356,7 +365,7 @@ int run_dgrad(const ImplPlan& p, const ConvGeom& g, const CodeT* dy, const CodeT
     uint8_t* pos_nar = ws + p.off_pos_nar;
     uint8_t* flags = ws + p.off_flags;
     if (cudaMemsetAsync(ws + p.off_maps, 0, p.maps_bytes, st) != cudaSuccess) return 4;
-    if (act_digits<CodeT>(p.D, dy, g.N, g.F, g.OH, g.OW, p.Ca, f, adig, pos_nar, nullptr, nullptr,
+    if (act_digits<CodeT>(p.D, dy, g.N, g.F, g.OH, g.OW, p.Ca, f, lut_of(p, ws), true, adig, pos_nar, nullptr, nullptr,
                           flags, st) != cudaSuccess)
         return 4;
     const int64_t taps = g.KH * g.KW;
@@ -396,10 +405,10 @@ int run_wgrad(const ImplPlan& p, const ConvGeom& g, const CodeT* dy, const CodeT
     uint8_t* col_nar = ws + p.off_col_nar;
     uint8_t* flags = ws + p.off_flags;
     if (cudaMemsetAsync(ws + p.off_maps, 0, p.maps_bytes, st) != cudaSuccess) return 4;
-    if (act_digits<CodeT>(p.D, x, g.N, g.C, g.H, g.W, p.Ca, f, adig, nullptr, chw_nar, nullptr,
+    if (act_digits<CodeT>(p.D, x, g.N, g.C, g.H, g.W, p.Ca, f, lut_of(p, ws), true, adig, nullptr, chw_nar, nullptr,
                           flags, st) != cudaSuccess)
         return 4;
-    if (act_digits<CodeT>(p.D, dy, g.N, g.F, g.OH, g.OW, p.Fpw, f, bdig, nullptr, nullptr, col_nar,
+    if (act_digits<CodeT>(p.D, dy, g.N, g.F, g.OH, g.OW, p.Fpw, f, lut_of(p, ws), false, bdig, nullptr, nullptr, col_nar,
                           flags + 1, st) != cudaSuccess)
         return 4;
     CUtensorMap tA, tB;

@@ -29,7 +29,8 @@
 
 namespace pnn_b200 {
 
-constexpr int kIKB = 32;  // K bytes (channels or pixels) per pipeline stage
+constexpr int kIKB = 32;         // K bytes (channels or pixels) per pipeline stage
+constexpr int kActLutBits = 12;  // digitiser LUT up to 4096 codes (32 KB, L1-resident)
 
 template <int D>
 struct ImplGeo {
@@ -207,7 +208,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ===== epilogue: TMEM -> quire words -> posit codes / split-K partials =====
         const int quarter = warp & 3;
         const int half = (warp - 2) >> 2;
-        const uint32_t trow = tmem + (uint32_t(quarter * 32) << 16) + half * COLS;
+        // alternate 8-column chunks per warp of a lane quarter (balanced when N < NT)
+        const uint32_t trow = tmem + (uint32_t(quarter * 32) << 16) + half * 8;
         uint32_t j = 0;
         for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++j) {
             int64_t split, mt, nt;
@@ -224,7 +226,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     uint32_t r[GB][8];
 #pragma unroll
                     for (int g = 0; g < GB; ++g)
-                        if (g0 + g < G) ptx::tmem_ld8(trow + (g0 + g) * NT + c0, r[g]);
+                        if (g0 + g < G) ptx::tmem_ld8(trow + (g0 + g) * NT + 2 * c0, r[g]);
                     ptx::tmem_wait_ld();
 #pragma unroll
                     for (int g = 0; g < GB; ++g)
@@ -239,19 +241,19 @@ __global__ void __launch_bounds__(kThreads, 1)
 
             const int64_t row = mt * kBM + quarter * 32 + lane;
             if (row >= a.M) continue;
-            const int64_t colbase = nt * NT + half * COLS;
+            const int64_t colbase = nt * NT + half * 8;  // chunk c0 / 8 at colbase + 2 * c0
             if constexpr (MODE == 0) if (a.col_add != nullptr && split == 0) {
 #pragma unroll
                 for (int c = 0; c < COLS; ++c)
-                    if (colbase + c < a.N) {
-                        const int64_t xb = a.col_add[colbase + c];
+                    if (colbase + 2 * (c & ~7) + (c & 7) < a.N) {
+                        const int64_t xb = a.col_add[colbase + 2 * (c & ~7) + (c & 7)];
                         if constexpr (QW == 4) q[c] += QT(__int128(xb)) << a.f.R;
                         else q[c] += QT(xb) << a.f.R;
                     }
             }
 #pragma unroll
             for (int c0 = 0; c0 < COLS; c0 += 8) {
-                const int64_t col0 = colbase + c0;
+                const int64_t col0 = colbase + 2 * c0;
                 if (col0 >= a.N) break;
                 const int valid = int(a.N - col0 < 8 ? a.N - col0 : 8);
                 if (a.partial != nullptr) {
@@ -282,66 +284,86 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 // ------------------------------------------------------------- digitising
 
+// Digit words of every code of a format (formats up to kActLutBits bits),
+// built once per call into the workspace and read through L1 by the digitiser.
+template <int D>
+__global__ void digit_lut_kernel(PositFmt f, uint32_t* __restrict__ lut) {
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < (1 << f.nbits);
+         c += gridDim.x * blockDim.x) {
+        uint32_t lo, hi;
+        bool nar;
+        digit_words<D>(uint32_t(c), f, lo, hi, nar);
+        lut[2 * c] = lo;
+        lut[2 * c + 1] = hi;
+    }
+}
+
 // codes [N][C][H][W] -> dig[D][N][H][W][Cp] (balanced int8 digits; channels
 // >= C are zero), plus NaR summaries written only where a NaR is found:
 // pos_nar[n][h][w] (any channel), chw_nar[c][h][w] (any image), chan_nar[c],
-// *any.  One block per (n, h) image row; coalesced 32-channel x W tiles.
+// *any.  A work item is a slab of RH = 128 / W image rows (one image): 32
+// channels x RH*W pixels are loaded coalesced (rows of one channel are
+// contiguous in NCHW), transposed through shared memory and written as
+// 4-channel words per plane.  lut: digit_lut_kernel output, or null (decode).
+constexpr int kSlab = 128;  // pixels per work item (upper bound)
+
 template <int D, typename CodeT>
 __global__ void __launch_bounds__(256) act_digits_kernel(
     const CodeT* __restrict__ x, int64_t N, int C, int H, int W, int Cp, PositFmt f,
-    int8_t* __restrict__ dig, uint8_t* __restrict__ pos_nar, uint8_t* __restrict__ chw_nar,
-    uint8_t* __restrict__ chan_nar, uint8_t* __restrict__ any) {
-    __shared__ CodeT tile[32 * 257];
-    __shared__ uint32_t lut[2 << kLutMaxBits];
-    const bool use_lut = f.nbits <= kLutMaxBits;
-    if (use_lut) {
-        for (int c = threadIdx.x; c < (1 << f.nbits); c += blockDim.x) {
-            uint32_t lo, hi;
-            bool nar;
-            digit_words<D>(uint32_t(c), f, lo, hi, nar);
-            lut[2 * c] = lo;
-            lut[2 * c + 1] = hi;
-        }
-    }
+    const uint32_t* __restrict__ lut, int8_t* __restrict__ dig, uint8_t* __restrict__ pos_nar,
+    uint8_t* __restrict__ chw_nar, uint8_t* __restrict__ chan_nar, uint8_t* __restrict__ any) {
+    __shared__ CodeT tile[32 * (kSlab + 1)];
+    const int RH = W >= kSlab ? 1 : (kSlab / W < H ? kSlab / W : H);
+    const int slabs = (H + RH - 1) / RH;
     const uint32_t nar_code = 1u << (f.nbits - 1);
     const int64_t HW = int64_t(H) * W;
     const int64_t plane = N * HW * Cp;
-    const int LDT = W + 1;
-    for (int64_t rowi = blockIdx.x; rowi < N * H; rowi += gridDim.x) {
-        const int64_t n = rowi / H;
-        const int h = int(rowi - n * H);
+    const int wchunks = (W + kSlab - 1) / kSlab;  // W > 128: slabs of one row split in w
+    const int64_t items = N * slabs * wchunks;
+    for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+        const int64_t n = it / (int64_t(slabs) * wchunks);
+        const int rem = int(it - n * slabs * wchunks);
+        const int h0 = (rem / wchunks) * RH, w0 = (rem % wchunks) * kSlab;
+        const int rows = H - h0 < RH ? H - h0 : RH;
+        const int wl = W - w0 < kSlab ? W - w0 : kSlab;
+        const int P = rows * wl;  // pixels of this item (contiguous when wl == W)
+        const int LDT = P + 1;
         for (int c0 = 0; c0 < Cp; c0 += 32) {
             __syncthreads();
-            for (int i = threadIdx.x; i < 32 * W; i += blockDim.x) {
-                const int cl = i / W, w = i - cl * W;
+            for (int i = threadIdx.x; i < 32 * P; i += blockDim.x) {
+                const int cl = i / P, pix = i - cl * P;
                 const int c = c0 + cl;
-                tile[cl * LDT + w] = c < C ? x[((n * C + c) * H + h) * W + w] : CodeT(0);
+                const int hh = h0 + pix / wl, ww = w0 + pix % wl;
+                tile[cl * LDT + pix] =
+                    c < C ? x[((n * C + c) * H + hh) * W + ww] : CodeT(0);
             }
             __syncthreads();
-            for (int i = threadIdx.x; i < W * 8; i += blockDim.x) {
-                const int w = i >> 3, q = i & 7;
+            for (int i = threadIdx.x; i < P * 8; i += blockDim.x) {
+                const int pix = i >> 3, q = i & 7;
+                const int hh = h0 + pix / wl, ww = w0 + pix % wl;
                 uint32_t lo[4], hi[4];
 #pragma unroll
                 for (int jj = 0; jj < 4; ++jj) {
                     const int cl = 4 * q + jj;
-                    const uint32_t code = uint32_t(tile[cl * LDT + w]);
+                    const uint32_t code = uint32_t(tile[cl * LDT + pix]);
                     bool nar;
-                    if (use_lut) {
-                        lo[jj] = lut[2 * code];
-                        hi[jj] = lut[2 * code + 1];
+                    if (lut != nullptr) {
+                        const uint2 v = __ldg(reinterpret_cast<const uint2*>(lut) + code);
+                        lo[jj] = v.x;
+                        hi[jj] = v.y;
                         nar = code == nar_code;
                     } else {
                         digit_words<D>(code, f, lo[jj], hi[jj], nar);
                     }
                     if (nar && c0 + cl < C) {
                         const int c = c0 + cl;
-                        if (pos_nar) pos_nar[n * HW + int64_t(h) * W + w] = 1;
-                        if (chw_nar) chw_nar[int64_t(c) * HW + int64_t(h) * W + w] = 1;
+                        if (pos_nar) pos_nar[n * HW + int64_t(hh) * W + ww] = 1;
+                        if (chw_nar) chw_nar[int64_t(c) * HW + int64_t(hh) * W + ww] = 1;
                         if (chan_nar) chan_nar[c] = 1;
                         *any = 1;
                     }
                 }
-                int8_t* dst = dig + ((n * H + h) * W + w) * Cp + c0 + 4 * q;
+                int8_t* dst = dig + ((n * H + hh) * W + ww) * Cp + c0 + 4 * q;
 #pragma unroll
                 for (int p = 0; p < D; ++p) {
                     const int sh = 8 * (p & 3);

@@ -518,7 +518,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ===== epilogue: TMEM -> quire words (registers) -> posit codes =====
         const int quarter = warp & 3;
         const int half = (warp - 2) >> 2;
-        const uint32_t trow = tmem + (uint32_t(quarter * 32) << 16) + half * COLS;
+        // the two warps of a lane quarter take alternate 8-column chunks, so both
+        // stay busy when the valid columns (N) fill only part of the tile
+        const uint32_t trow = tmem + (uint32_t(quarter * 32) << 16) + half * 8;
         const bool vec_ok = out.mode == 0 && (out.ldc % 8) == 0;
         uint32_t j = 0;
         const uint32_t tmem_empty_leader = kPair ? ptx::mapa(ptx::smem_u32(tmem_empty), 0) : 0u;
@@ -538,7 +540,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     uint32_t r[GB][8];
 #pragma unroll
                     for (int g = 0; g < GB; ++g)
-                        if (g0 + g < G) ptx::tmem_ld8(trow + (g0 + g) * NT + c0, r[g]);
+                        if (g0 + g < G) ptx::tmem_ld8(trow + (g0 + g) * NT + 2 * c0, r[g]);
                     ptx::tmem_wait_ld();
 #pragma unroll
                     for (int g = 0; g < GB; ++g)
@@ -557,10 +559,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int64_t row = mt * kBM + quarter * 32 + lane;
             if (row >= M) continue;
             const bool rnar = row_nar != nullptr && row_nar[row] != 0;
-            const int64_t colbase = nt * NT + half * COLS;
+            const int64_t colbase = nt * NT + half * 8;  // + 2 * c0 for chunk c0 / 8
 #pragma unroll
             for (int c0 = 0; c0 < COLS; c0 += 8) {
-                const int64_t col0 = colbase + c0;
+                const int64_t col0 = colbase + 2 * c0;
                 if (col0 >= N) break;
                 const int valid = int(N - col0 < 8 ? N - col0 : 8);
                 if (partial != nullptr) {
