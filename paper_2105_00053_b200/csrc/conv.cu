@@ -231,17 +231,25 @@ struct FetchWgradDy {  // X[r = f][k = (n,o)] = dy[n][f][o]
 template <typename CodeT>
 __global__ void __launch_bounds__(256) bias_grad_partial_kernel(
     const CodeT* __restrict__ dy, int64_t N, int64_t F, int64_t P, PositFmt f, int slices,
-    unsigned __int128* __restrict__ partial, uint8_t* __restrict__ nar_out) {
+    const int64_t* __restrict__ xlut, unsigned __int128* __restrict__ partial,
+    uint8_t* __restrict__ nar_out) {
     const int64_t ch = blockIdx.x, slice = blockIdx.y;
     const int64_t per = (N + slices - 1) / slices;
     const int64_t n0 = slice * per, n1 = min(N, n0 + per);
+    const uint32_t nar_code = 1u << (f.nbits - 1);
     __int128 acc = 0;
     bool nar = false;
     for (int64_t n = n0; n < n1; ++n) {
         const CodeT* row = dy + (n * F + ch) * P;
-        for (int64_t o = threadIdx.x; o < P; o += blockDim.x) {
+        for (int o = threadIdx.x; o < int(P); o += blockDim.x) {
+            const uint32_t code = uint32_t(row[o]);
             int64_t X;
-            nar |= decode_x(uint32_t(row[o]), f, X);
+            if (xlut != nullptr) {  // exact integer image from the per-call table
+                X = __ldg(xlut + code);
+                nar |= code == nar_code;
+            } else {
+                nar |= decode_x(code, f, X);
+            }
             acc += X;
         }
     }
@@ -262,6 +270,16 @@ __global__ void __launch_bounds__(256) bias_grad_partial_kernel(
         for (int i = 0; i < int(blockDim.x >> 5); ++i) t += warp_s[i];
         partial[ch * slices + slice] = t;
         if (nar) nar_out[ch] = 1;
+    }
+}
+
+// X (the exact integer image) of every code of a format, for table decode.
+__global__ void x_lut_kernel(PositFmt f, int64_t* __restrict__ lut) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c < (1 << f.nbits)) {
+        int64_t X;
+        decode_x(uint32_t(c), f, X);
+        lut[c] = X;
     }
 }
 
@@ -485,9 +503,15 @@ int pnn_conv2d_wgrad(int nbits, int es, const void* dy, int64_t N, int64_t F, in
     return status_of(rc, "conv2d_wgrad");
 }
 
+// workspace: [split partials F x 64 x 16 B][NaR flags F][X table of the format]
+constexpr int kBiasLutBits = 12;
+static size_t bias_lut_offset(int64_t F) {
+    return (size_t(F) * 16 * 64 + size_t(F) + 255) & ~size_t(255);
+}
+
 int pnn_bias_grad_workspace(int64_t F, size_t* bytes) {
     if (F < 0 || !bytes) return set_status(PNN_EINVAL, "conv: invalid shape or argument");
-    *bytes = size_t(F) * 16 * 64 + size_t(F) + 256;
+    *bytes = bias_lut_offset(F) + (size_t(8) << kBiasLutBits);
     return PNN_OK;
 }
 
@@ -508,15 +532,20 @@ int pnn_bias_grad(int nbits, int es, const void* dy, int64_t N, int64_t F, int64
     cudaMemsetAsync(nar, 0, size_t(F), st);
     cudaMemsetAsync(partial, 0, size_t(F) * 16 * slices, st);
     const dim3 grid{unsigned(F), unsigned(slices), 1u};
+    int64_t* xlut = nullptr;
+    if (nbits <= kBiasLutBits && N * P >= 4096) {  // table pays for itself
+        xlut = reinterpret_cast<int64_t*>(static_cast<uint8_t*>(workspace) + bias_lut_offset(F));
+        x_lut_kernel<<<(1 << nbits) / 256 + 1, 256, 0, st>>>(f, xlut);
+    }
     if (nbits <= 8) {
         bias_grad_partial_kernel<uint8_t><<<grid, 256, 0, st>>>((const uint8_t*)dy, N, F, P, f,
-                                                                 slices, partial, nar);
+                                                                 slices, xlut, partial, nar);
         bias_grad_final_kernel<uint8_t><<<grid_for(F, 128), 128, 0, st>>>(
             partial, slices, nar, F, f, (uint8_t*)db, (unsigned __int128*)raw_words,
             (uint8_t*)raw_nar);
     } else {
         bias_grad_partial_kernel<uint16_t><<<grid, 256, 0, st>>>((const uint16_t*)dy, N, F, P, f,
-                                                                  slices, partial, nar);
+                                                                  slices, xlut, partial, nar);
         bias_grad_final_kernel<uint16_t><<<grid_for(F, 128), 128, 0, st>>>(
             partial, slices, nar, F, f, (uint16_t*)db, (unsigned __int128*)raw_words,
             (uint8_t*)raw_nar);

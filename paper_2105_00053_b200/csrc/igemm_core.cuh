@@ -242,6 +242,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int64_t row = mt * kBM + quarter * 32 + lane;
             if (row >= a.M) continue;
             const int64_t colbase = nt * NT + half * 8;  // chunk c0 / 8 at colbase + 2 * c0
+            const int64_t obase = out.row_base(row), ostride = out.col_stride();
             if constexpr (MODE == 0) if (a.col_add != nullptr && split == 0) {
 #pragma unroll
                 for (int c = 0; c < COLS; ++c)
@@ -267,7 +268,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int x = 0; x < 8; ++x)
                     if (x < valid) {
                         const bool nar = a.col_nar != nullptr && a.col_nar[col0 + x];
-                        out.base[out.index(row, col0 + x)] =
+                        out.base[obase + (col0 + x) * ostride] =
                             CodeT(nar ? (1u << (a.f.nbits - 1)) : quire_word_to_posit(a.f, q[c0 + x]));
                     }
             }
@@ -328,19 +329,27 @@ __global__ void __launch_bounds__(256) act_digits_kernel(
         const int wl = W - w0 < kSlab ? W - w0 : kSlab;
         const int P = rows * wl;  // pixels of this item (contiguous when wl == W)
         const int LDT = P + 1;
+        const bool whole_rows = wl == W;
+        // first pixel of the item in the [N][H][W] raster (pixel pix = raster0 + pix
+        // when whole_rows)
+        const int64_t raster0 = (n * H + h0) * int64_t(W) + w0;
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
         for (int c0 = 0; c0 < Cp; c0 += 32) {
             __syncthreads();
-            for (int i = threadIdx.x; i < 32 * P; i += blockDim.x) {
-                const int cl = i / P, pix = i - cl * P;
+            // load: a warp per channel row, lanes along the (contiguous) pixels
+            for (int cl = warp; cl < 32; cl += 8) {
                 const int c = c0 + cl;
-                const int hh = h0 + pix / wl, ww = w0 + pix % wl;
-                tile[cl * LDT + pix] =
-                    c < C ? x[((n * C + c) * H + hh) * W + ww] : CodeT(0);
+                const CodeT* src = x + ((n * C + c) * H + h0) * int64_t(W) + w0;
+                for (int pix = lane; pix < P; pix += 32) {
+                    const int off = whole_rows ? pix : (pix / wl) * W + pix % wl;
+                    tile[cl * LDT + pix] = c < C ? src[off] : CodeT(0);
+                }
             }
             __syncthreads();
             for (int i = threadIdx.x; i < P * 8; i += blockDim.x) {
                 const int pix = i >> 3, q = i & 7;
-                const int hh = h0 + pix / wl, ww = w0 + pix % wl;
+                const int64_t r = whole_rows ? raster0 + pix
+                                             : raster0 + int64_t(pix / wl) * W + pix % wl;
                 uint32_t lo[4], hi[4];
 #pragma unroll
                 for (int jj = 0; jj < 4; ++jj) {
@@ -357,21 +366,21 @@ __global__ void __launch_bounds__(256) act_digits_kernel(
                     }
                     if (nar && c0 + cl < C) {
                         const int c = c0 + cl;
-                        if (pos_nar) pos_nar[n * HW + int64_t(hh) * W + ww] = 1;
-                        if (chw_nar) chw_nar[int64_t(c) * HW + int64_t(hh) * W + ww] = 1;
+                        if (pos_nar) pos_nar[r] = 1;
+                        if (chw_nar) chw_nar[int64_t(c) * HW + (r - n * HW)] = 1;
                         if (chan_nar) chan_nar[c] = 1;
                         *any = 1;
                     }
                 }
-                int8_t* dst = dig + ((n * H + hh) * W + ww) * Cp + c0 + 4 * q;
+                int8_t* dst = dig + r * Cp + c0 + 4 * q;
+                // 4 codes x D digit bytes -> one 4-byte word per plane (byte transpose)
 #pragma unroll
                 for (int p = 0; p < D; ++p) {
-                    const int sh = 8 * (p & 3);
-                    uint32_t v = 0;
-#pragma unroll
-                    for (int jj = 0; jj < 4; ++jj)
-                        v |= (((p < 4 ? lo[jj] : hi[jj]) >> sh) & 0xFFu) << (8 * jj);
-                    *reinterpret_cast<uint32_t*>(dst + p * plane) = v;
+                    const uint32_t* w = p < 4 ? lo : hi;
+                    const uint32_t sel = (p & 3) | (((p & 3) + 4) << 4);
+                    const uint32_t a = __byte_perm(w[0], w[1], sel);
+                    const uint32_t b = __byte_perm(w[2], w[3], sel);
+                    *reinterpret_cast<uint32_t*>(dst + p * plane) = __byte_perm(a, b, 0x5410);
                 }
             }
         }

@@ -308,6 +308,16 @@ struct OutMap {
         if (mode == 2) return n * ldc + lo * ncols + hi;
         return (hi * ncols + n) * inner + lo;
     }
+    // index(m, n) == row_base(m) + n * col_stride(): one division per row
+    __device__ __forceinline__ int64_t row_base(int64_t m) const {
+        if (mode == 0) return m * ldc;
+        const int64_t hi = m / inner, lo = m - hi * inner;
+        if (mode == 2) return lo * ncols + hi;
+        return hi * ncols * inner + lo;
+    }
+    __device__ __forceinline__ int64_t col_stride() const {
+        return mode == 0 ? 1 : mode == 2 ? ldc : inner;
+    }
 };
 
 template <typename CodeT>
@@ -581,9 +591,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (vec_ok) {
                     store_codes8(out.base + row * out.ldc + col0, codes, valid, true);
                 } else {
+                    const int64_t cs = out.col_stride();
+                    CodeT* dst = out.base + out.row_base(row) + col0 * cs;
 #pragma unroll
                     for (int x = 0; x < 8; ++x)
-                        if (x < valid) out.base[out.index(row, col0 + x)] = CodeT(codes[x]);
+                        if (x < valid) dst[x * cs] = CodeT(codes[x]);
                 }
             }
         }
