@@ -218,9 +218,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::tc_fence_after();
             QT q[COLS];
 #pragma unroll
-            for (int c = 0; c < COLS; ++c) q[c] = 0;
-#pragma unroll
             for (int c0 = 0; c0 < COLS; c0 += 8) {
+                QAcc<QT> acc[8];
 #pragma unroll
                 for (int g0 = 0; g0 < G; g0 += GB) {
                     uint32_t r[GB][8];
@@ -232,8 +231,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                     for (int g = 0; g < GB; ++g)
                         if (g0 + g < G)
 #pragma unroll
-                            for (int x = 0; x < 8; ++x) q[c0 + x] += group_term<QT>(r[g][x], 8 * (g0 + g));
+                            for (int x = 0; x < 8; ++x) acc[x].add(g0 + g, r[g][x]);
                 }
+#pragma unroll
+                for (int x = 0; x < 8; ++x) q[c0 + x] = acc[x].get();
             }
             ptx::tc_fence_before();
             __syncwarp();
@@ -299,13 +300,47 @@ __global__ void digit_lut_kernel(PositFmt f, uint32_t* __restrict__ lut) {
     }
 }
 
+// Digits of 4 consecutive channels (codes c[0..3]) written as one 4-byte word
+// per plane at dst + p * plane; returns a mask of NaR codes.
+template <int D>
+__device__ __forceinline__ uint32_t digits4(const uint32_t (&c)[4], const PositFmt& f,
+                                            const uint32_t* __restrict__ lut, int8_t* dst,
+                                            int64_t plane) {
+    const uint32_t nar_code = 1u << (f.nbits - 1);
+    uint32_t lo[4], hi[4], nm = 0;
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj) {
+        bool nar;
+        if (lut != nullptr) {
+            const uint2 v = __ldg(reinterpret_cast<const uint2*>(lut) + c[jj]);
+            lo[jj] = v.x;
+            hi[jj] = v.y;
+            nar = c[jj] == nar_code;
+        } else {
+            digit_words<D>(c[jj], f, lo[jj], hi[jj], nar);
+        }
+        nm |= nar ? 1u << jj : 0u;
+    }
+    // 4 codes x D digit bytes -> one word per plane (byte transpose)
+#pragma unroll
+    for (int p = 0; p < D; ++p) {
+        const uint32_t* w = p < 4 ? lo : hi;
+        const uint32_t sel = (p & 3) | (((p & 3) + 4) << 4);
+        const uint32_t a = __byte_perm(w[0], w[1], sel);
+        const uint32_t b = __byte_perm(w[2], w[3], sel);
+        *reinterpret_cast<uint32_t*>(dst + p * plane) = __byte_perm(a, b, 0x5410);
+    }
+    return nm;
+}
+
 // codes [N][C][H][W] -> dig[D][N][H][W][Cp] (balanced int8 digits; channels
 // >= C are zero), plus NaR summaries written only where a NaR is found:
 // pos_nar[n][h][w] (any channel), chw_nar[c][h][w] (any image), chan_nar[c],
 // *any.  A work item is a slab of RH = 128 / W image rows (one image): 32
 // channels x RH*W pixels are loaded coalesced (rows of one channel are
 // contiguous in NCHW), transposed through shared memory and written as
-// 4-channel words per plane.  lut: digit_lut_kernel output, or null (decode).
+// 4-channel words per plane.  1x1 images (Linear layers) need no transpose
+// and take an elementwise path.  lut: digit_lut_kernel output, or null.
 constexpr int kSlab = 128;  // pixels per work item (upper bound)
 
 template <int D, typename CodeT>
@@ -314,11 +349,31 @@ __global__ void __launch_bounds__(256) act_digits_kernel(
     const uint32_t* __restrict__ lut, int8_t* __restrict__ dig, uint8_t* __restrict__ pos_nar,
     uint8_t* __restrict__ chw_nar, uint8_t* __restrict__ chan_nar, uint8_t* __restrict__ any) {
     __shared__ CodeT tile[32 * (kSlab + 1)];
-    const int RH = W >= kSlab ? 1 : (kSlab / W < H ? kSlab / W : H);
-    const int slabs = (H + RH - 1) / RH;
-    const uint32_t nar_code = 1u << (f.nbits - 1);
     const int64_t HW = int64_t(H) * W;
     const int64_t plane = N * HW * Cp;
+    if (HW == 1) {
+        const int groups = Cp / 4;
+        for (int64_t g = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; g < N * groups;
+             g += int64_t(gridDim.x) * blockDim.x) {
+            const int64_t n = g / groups;
+            const int c0 = int(g - n * groups) * 4;
+            uint32_t c[4];
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) c[jj] = c0 + jj < C ? uint32_t(x[n * C + c0 + jj]) : 0u;
+            const uint32_t nm = digits4<D>(c, f, lut, dig + n * Cp + c0, plane);
+            if (nm)
+                for (int jj = 0; jj < 4; ++jj)
+                    if (((nm >> jj) & 1) && c0 + jj < C) {
+                        if (pos_nar) pos_nar[n] = 1;
+                        if (chw_nar) chw_nar[c0 + jj] = 1;
+                        if (chan_nar) chan_nar[c0 + jj] = 1;
+                        *any = 1;
+                    }
+        }
+        return;
+    }
+    const int RH = W >= kSlab ? 1 : (kSlab / W < H ? kSlab / W : H);
+    const int slabs = (H + RH - 1) / RH;
     const int wchunks = (W + kSlab - 1) / kSlab;  // W > 128: slabs of one row split in w
     const int64_t items = N * slabs * wchunks;
     for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
@@ -330,8 +385,7 @@ __global__ void __launch_bounds__(256) act_digits_kernel(
         const int P = rows * wl;  // pixels of this item (contiguous when wl == W)
         const int LDT = P + 1;
         const bool whole_rows = wl == W;
-        // first pixel of the item in the [N][H][W] raster (pixel pix = raster0 + pix
-        // when whole_rows)
+        // first pixel of the item in the [N][H][W] raster
         const int64_t raster0 = (n * H + h0) * int64_t(W) + w0;
         const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
         for (int c0 = 0; c0 < Cp; c0 += 32) {
@@ -350,38 +404,20 @@ __global__ void __launch_bounds__(256) act_digits_kernel(
                 const int pix = i >> 3, q = i & 7;
                 const int64_t r = whole_rows ? raster0 + pix
                                              : raster0 + int64_t(pix / wl) * W + pix % wl;
-                uint32_t lo[4], hi[4];
+                uint32_t c[4];
 #pragma unroll
-                for (int jj = 0; jj < 4; ++jj) {
-                    const int cl = 4 * q + jj;
-                    const uint32_t code = uint32_t(tile[cl * LDT + pix]);
-                    bool nar;
-                    if (lut != nullptr) {
-                        const uint2 v = __ldg(reinterpret_cast<const uint2*>(lut) + code);
-                        lo[jj] = v.x;
-                        hi[jj] = v.y;
-                        nar = code == nar_code;
-                    } else {
-                        digit_words<D>(code, f, lo[jj], hi[jj], nar);
+                for (int jj = 0; jj < 4; ++jj) c[jj] = uint32_t(tile[(4 * q + jj) * LDT + pix]);
+                const uint32_t nm = digits4<D>(c, f, lut, dig + r * Cp + c0 + 4 * q, plane);
+                if (nm)
+                    for (int jj = 0; jj < 4; ++jj) {
+                        const int ch = c0 + 4 * q + jj;
+                        if (((nm >> jj) & 1) && ch < C) {
+                            if (pos_nar) pos_nar[r] = 1;
+                            if (chw_nar) chw_nar[int64_t(ch) * HW + (r - n * HW)] = 1;
+                            if (chan_nar) chan_nar[ch] = 1;
+                            *any = 1;
+                        }
                     }
-                    if (nar && c0 + cl < C) {
-                        const int c = c0 + cl;
-                        if (pos_nar) pos_nar[r] = 1;
-                        if (chw_nar) chw_nar[int64_t(c) * HW + (r - n * HW)] = 1;
-                        if (chan_nar) chan_nar[c] = 1;
-                        *any = 1;
-                    }
-                }
-                int8_t* dst = dig + r * Cp + c0 + 4 * q;
-                // 4 codes x D digit bytes -> one 4-byte word per plane (byte transpose)
-#pragma unroll
-                for (int p = 0; p < D; ++p) {
-                    const uint32_t* w = p < 4 ? lo : hi;
-                    const uint32_t sel = (p & 3) | (((p & 3) + 4) << 4);
-                    const uint32_t a = __byte_perm(w[0], w[1], sel);
-                    const uint32_t b = __byte_perm(w[2], w[3], sel);
-                    *reinterpret_cast<uint32_t*>(dst + p * plane) = __byte_perm(a, b, 0x5410);
-                }
             }
         }
     }

@@ -357,6 +357,45 @@ __device__ __forceinline__ T group_term(uint32_t acc, int sh) {
     else return T(__int128(int32_t(acc))) << sh;
 }
 
+// Quire word of one output from its int32 group sums, Q = sum_g S_g 256^g
+// (mod the word size).  Groups are accumulated per 32-bit word position in
+// int64 (one IMAD.WIDE each: |S_g * 2^(8g mod 32)| < 2^55, <= 4 terms per
+// word) and the words are combined once -- instead of a wide shift-add per
+// group.  `gg` is a compile-time constant after unrolling.
+template <typename T>
+struct QAcc;
+template <>
+struct QAcc<uint32_t> {  // W <= 32
+    uint32_t v = 0;
+    __device__ __forceinline__ void add(int gg, uint32_t s) {
+        if (8 * gg < 32) v += s << (8 * gg);
+    }
+    __device__ __forceinline__ uint32_t get() const { return v; }
+};
+template <>
+struct QAcc<uint64_t> {  // W <= 64
+    int64_t w0 = 0, w1 = 0;
+    __device__ __forceinline__ void add(int gg, uint32_t s) {
+        const int64_t x = int64_t(int32_t(s));
+        if (8 * gg < 32) w0 += x * int64_t(1 << (8 * gg));
+        else if (8 * gg < 64) w1 += x * int64_t(1 << (8 * gg - 32));
+    }
+    __device__ __forceinline__ uint64_t get() const { return uint64_t(w0) + (uint64_t(w1) << 32); }
+};
+template <>
+struct QAcc<unsigned __int128> {  // W <= 128
+    int64_t w[4] = {0, 0, 0, 0};
+    __device__ __forceinline__ void add(int gg, uint32_t s) {
+        const int64_t x = int64_t(int32_t(s));
+        const int wi = (8 * gg) >> 5;
+        if (wi < 4) w[wi] += x * int64_t(1 << ((8 * gg) & 31));
+    }
+    __device__ __forceinline__ unsigned __int128 get() const {
+        return (unsigned __int128)(__int128(w[0]) + (__int128(w[1]) << 32) + (__int128(w[2]) << 64) +
+                                   (__int128(w[3]) << 96));
+    }
+};
+
 // Raster: tiles grouped by kGroupM m-tiles so the ~148 tiles in flight share
 // A and B digit planes in L2.
 constexpr int kGroupM = 8;
@@ -542,9 +581,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::tc_fence_after();
             QT q[COLS];
 #pragma unroll
-            for (int c = 0; c < COLS; ++c) q[c] = 0;
-#pragma unroll
             for (int c0 = 0; c0 < COLS; c0 += 8) {
+                QAcc<QT> acc[8];
 #pragma unroll
                 for (int g0 = 0; g0 < G; g0 += GB) {
                     uint32_t r[GB][8];
@@ -556,8 +594,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                     for (int g = 0; g < GB; ++g)
                         if (g0 + g < G)
 #pragma unroll
-                            for (int x = 0; x < 8; ++x) q[c0 + x] += group_term<QT>(r[g][x], 8 * (g0 + g));
+                            for (int x = 0; x < 8; ++x) acc[x].add(g0 + g, r[g][x]);
                 }
+#pragma unroll
+                for (int x = 0; x < 8; ++x) q[c0 + x] = acc[x].get();
             }
             ptx::tc_fence_before();
             __syncwarp();

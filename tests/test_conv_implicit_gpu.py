@@ -27,6 +27,8 @@ SHAPES = [
     (2, 32, 10, 10, 32, 3, 0, "fw"),     # valid conv: fwd 8x8 tiles, box reads inside 10x10
     (2, 32, 8, 8, 40, 3, 1, "fw"),       # F = 40: partial N tile / padded dy digits
     (2, 128, 8, 8, 32, 3, 1, "fdw"),     # 128-channel wgrad slot (128B swizzle)
+    (4, 64, 1, 1, 32, 1, 0, "fd"),       # Linear as 1x1 conv: elementwise digitiser
+    (130, 32, 1, 1, 64, 1, 0, "fd"),     # Linear, 128 rows per tile + a partial tile
 ]
 
 
@@ -108,6 +110,25 @@ def test_implicit_conv_nar(cuda, po, cfg, implicit_only):
     dw2 = host(ops.conv2d_weight_grad(cfg, dev(cfg, dy2), dev(cfg, x), w.shape, 1, p))
     want2 = po.conv2d_weight_grad(n, es, dy2, x, w.shape, 1, p)
     assert (dw2 == want2).all() and (want2 != nar).any()
+
+
+@pytest.mark.parametrize("cfg", FORMATS)
+def test_implicit_linear_nar(cuda, po, cfg, implicit_only):
+    n, es = cfg
+    nar = 1 << (n - 1)
+    rng = np.random.default_rng(11 + n + es)
+    x = rand_codes(rng, n, (6, 64, 1, 1))
+    w = rand_codes(rng, n, (32, 64, 1, 1))
+    b = rand_codes(rng, n, (32,))
+    x[2, 17, 0, 0] = nar
+    w[5, 3, 0, 0] = nar
+    y = host(ops.conv2d(cfg, dev(cfg, x), dev(cfg, w), dev(cfg, b), 1, 0))
+    want = po.conv2d(n, es, x, w, b, 1, 0)
+    assert (y == want).all() and (want != nar).any()
+    dy = rand_codes(rng, n, want.shape)
+    dy[4, 9, 0, 0] = nar
+    dx = host(ops.conv2d_input_grad(cfg, dev(cfg, dy), dev(cfg, w), x.shape, 1, 0))
+    assert (dx == po.conv2d_input_grad(n, es, dy, w, x.shape, 1, 0)).all()
 
 
 @pytest.mark.parametrize("cfg", [(8, 1), (12, 1), (16, 1)])
