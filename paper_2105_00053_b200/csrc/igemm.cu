@@ -147,15 +147,8 @@ bool make_plan(int pass, const PositFmt& f, const ConvGeom& g, bool raw, ImplPla
         col_nar = size_t(p->Fpw);
     }
     // split-K: int32 group sums exact for <= 131071 / D terms (W > 32), SM fill
-    int64_t kbps = f.W <= 32 ? a.kbt : (131071 / D) / kIKB;
-    const int64_t tiles = a.mtiles * a.ntiles;
-    const int sms = num_sms();
-    if (tiles < sms && a.kbt >= 8) {
-        int64_t want = cdiv(sms, tiles);
-        if (want > a.kbt / 4) want = a.kbt / 4;
-        if (want > 1) kbps = kbps < cdiv(a.kbt, want) ? kbps : cdiv(a.kbt, want);
-    }
-    if (kbps < 1) kbps = 1;
+    const int64_t cap = f.W <= 32 ? a.kbt : (131071 / D) / kIKB;
+    const int64_t kbps = split_kblocks(a.kbt, cap < 1 ? 1 : cap, a.mtiles * a.ntiles, num_sms());
     a.kb_per_split = a.kbt < kbps ? a.kbt : kbps;
     a.splits = cdiv(a.kbt, a.kb_per_split);
     const size_t partial = (a.splits > 1 || raw) ? size_t(a.splits) * a.M * a.N * 16 : 0;

@@ -703,6 +703,21 @@ inline int num_sms() {
     return n;
 }
 
+// K-blocks per split: at most `cap` (int32 exactness of the group sums), and,
+// when the output tiles alone cannot fill the SMs, a split count that makes
+// whole waves of sms / tiles units (a partial last wave doubles the time).
+inline int64_t split_kblocks(int64_t kbt, int64_t cap, int64_t tiles, int sms) {
+    int64_t splits = (kbt + cap - 1) / cap;  // minimum for exactness
+    if (tiles < sms && kbt >= 8) {
+        const int64_t per_wave = sms / tiles;
+        int64_t s = (splits + per_wave - 1) / per_wave * per_wave;
+        const int64_t most = kbt / 4 > splits ? kbt / 4 : splits;  // >= 4 k-blocks each
+        splits = s < most ? s : most;
+    }
+    const int64_t kbps = (kbt + splits - 1) / splits;
+    return kbps < 1 ? 1 : kbps;
+}
+
 inline int grid_for(int64_t items, int threads) {
     int64_t b = (items + threads - 1) / threads;
     if (b > 148 * 64) b = 148 * 64;
@@ -734,20 +749,10 @@ inline QuireGemmPlan plan_for(const PositFmt& f, int64_t M, int64_t N, int64_t K
     // int32 group sums stay exact for K <= 131071 / D (|digit| <= 128); a
     // quire of W <= 32 bits is itself mod 2^32, so wrapping is exact there.
     int64_t kbps = f.W <= 32 ? p.kbt : (131071 / D) / Geo::KB;
-    if (max_kb_per_split > 0) {
+    if (max_kb_per_split > 0)
         kbps = kbps < max_kb_per_split ? kbps : max_kb_per_split;
-    } else {
-        const int64_t tiles = p.mtiles * p.ntiles;
-        const int sms = num_sms();
-        if (tiles < sms && p.kbt >= 8) {  // few output tiles, long K: split for SM fill
-            int64_t want = (sms + tiles - 1) / tiles;
-            if (want > p.kbt / 4) want = p.kbt / 4;
-            if (want > 1) {
-                const int64_t per = (p.kbt + want - 1) / want;
-                kbps = kbps < per ? kbps : per;
-            }
-        }
-    }
+    else
+        kbps = split_kblocks(p.kbt, kbps < 1 ? 1 : kbps, p.mtiles * p.ntiles, num_sms());
     if (kbps < 1) kbps = 1;
     p.kb_per_split = p.kbt < kbps ? p.kbt : kbps;
     p.splits = (p.kbt + p.kb_per_split - 1) / p.kb_per_split;
