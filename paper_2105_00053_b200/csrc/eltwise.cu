@@ -146,6 +146,105 @@ __global__ void maxpool_fwd_tiled_kernel(PositFmt f, int b, const void* x, int N
     }
 }
 
+// ---- vectorised elementwise paths (16-byte accesses, 8 codes per thread-step)
+
+template <typename T>
+struct Vec8;  // 8 codes
+template <>
+struct Vec8<uint8_t> {
+    using V = uint2;
+};
+template <>
+struct Vec8<uint16_t> {
+    using V = uint4;
+};
+
+template <typename T>
+__device__ __forceinline__ void unpack8(const typename Vec8<T>::V& v, uint32_t (&c)[8]) {
+    const uint32_t* w = reinterpret_cast<const uint32_t*>(&v);
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+        c[j] = sizeof(T) == 1 ? (w[j >> 2] >> (8 * (j & 3))) & 0xFFu : (w[j >> 1] >> (16 * (j & 1))) & 0xFFFFu;
+}
+
+template <typename T>
+__device__ __forceinline__ typename Vec8<T>::V pack8(const uint32_t (&c)[8]) {
+    typename Vec8<T>::V v;
+    uint32_t* w = reinterpret_cast<uint32_t*>(&v);
+    if constexpr (sizeof(T) == 1) {
+        w[0] = (c[0] & 0xFF) | ((c[1] & 0xFF) << 8) | ((c[2] & 0xFF) << 16) | ((c[3] & 0xFF) << 24);
+        w[1] = (c[4] & 0xFF) | ((c[5] & 0xFF) << 8) | ((c[6] & 0xFF) << 16) | ((c[7] & 0xFF) << 24);
+    } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) w[j] = (c[2 * j] & 0xFFFF) | ((c[2 * j + 1] & 0xFFFF) << 16);
+    }
+    return v;
+}
+
+__device__ __forceinline__ bool positive_code(uint32_t c, int nbits) {
+    return c != 0 && ((c >> (nbits - 1)) & 1u) == 0;
+}
+
+// stage conversion; formats up to 12 bits convert through a per-block table
+// (persistent grid: building it costs 1 << nbits conversions per block)
+template <typename S, typename Dt>
+__global__ void __launch_bounds__(256) convert_vec_kernel(PositFmt s, const S* __restrict__ src,
+                                                          PositFmt d, Dt* __restrict__ dst,
+                                                          int64_t n) {
+    __shared__ uint16_t lut[1 << 12];
+    const bool use_lut = s.nbits <= 12;
+    if (use_lut) {
+        for (int c = threadIdx.x; c < (1 << s.nbits); c += blockDim.x) lut[c] = uint16_t(p_convert(s, d, uint32_t(c)));
+        __syncthreads();
+    }
+    const int64_t n8 = n / 8;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n8;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        uint32_t c[8];
+        unpack8<S>(reinterpret_cast<const typename Vec8<S>::V*>(src)[i], c);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) c[j] = use_lut ? uint32_t(lut[c[j]]) : p_convert(s, d, c[j]);
+        reinterpret_cast<typename Vec8<Dt>::V*>(dst)[i] = pack8<Dt>(c);
+    }
+    for (int64_t i = n8 * 8 + blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x)
+        dst[i] = Dt(use_lut ? uint32_t(lut[uint32_t(src[i])]) : p_convert(s, d, uint32_t(src[i])));
+}
+
+template <typename T>
+__global__ void relu_fwd_vec_kernel(int nbits, const T* __restrict__ x, T* __restrict__ y, int64_t n) {
+    const int64_t n8 = n / 8;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n8;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        uint32_t c[8];
+        unpack8<T>(reinterpret_cast<const typename Vec8<T>::V*>(x)[i], c);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) c[j] = positive_code(c[j], nbits) ? c[j] : 0u;
+        reinterpret_cast<typename Vec8<T>::V*>(y)[i] = pack8<T>(c);
+    }
+    for (int64_t i = n8 * 8 + blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x)
+        y[i] = positive_code(uint32_t(x[i]), nbits) ? x[i] : T(0);
+}
+
+template <typename TX, typename TG>
+__global__ void relu_bwd_vec_kernel(int x_nbits, const TX* __restrict__ x,
+                                    const TG* __restrict__ dy, TG* __restrict__ dx, int64_t n) {
+    const int64_t n8 = n / 8;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n8;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        uint32_t cx[8], g[8];
+        unpack8<TX>(reinterpret_cast<const typename Vec8<TX>::V*>(x)[i], cx);
+        unpack8<TG>(reinterpret_cast<const typename Vec8<TG>::V*>(dy)[i], g);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) g[j] = positive_code(cx[j], x_nbits) ? g[j] : 0u;
+        reinterpret_cast<typename Vec8<TG>::V*>(dx)[i] = pack8<TG>(g);
+    }
+    for (int64_t i = n8 * 8 + blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x)
+        dx[i] = positive_code(uint32_t(x[i]), x_nbits) ? dy[i] : TG(0);
+}
+
 // Softmax cross-entropy in the loss format:
 //   m = max z;  e_j = exp(z_j - m);  S = round(quire sum e_j);
 // p_j = e_j / S;  loss_i = log(S) - (z_y - m);
@@ -365,6 +464,8 @@ int grid1(int64_t n) {
     return int(b < 1 ? 1 : b);
 }
 
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
 int launched(const char* what) {
     const cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess) return PNN_OK;
@@ -384,9 +485,23 @@ int pnn_convert(int src_nbits, int src_es, int dst_nbits, int dst_es, const void
     CHECK_FMT(dst_nbits, dst_es);
     if (n < 0 || (n > 0 && (!src || !dst))) return set_status(PNN_EINVAL, "convert: bad arguments");
     if (n == 0) return PNN_OK;
-    convert_kernel<<<grid1(n), 256, 0, (cudaStream_t)stream>>>(
-        make_fmt(src_nbits, src_es), bytes_of(src_nbits), src, make_fmt(dst_nbits, dst_es),
-        bytes_of(dst_nbits), dst, n);
+    const PositFmt s = make_fmt(src_nbits, src_es), d = make_fmt(dst_nbits, dst_es);
+    auto st = (cudaStream_t)stream;
+    if (aligned16(src) && aligned16(dst)) {
+        const int grid = grid1(n / 8 + 1) < 148 * 4 ? grid1(n / 8 + 1) : 148 * 4;
+        const int sb = bytes_of(src_nbits), db = bytes_of(dst_nbits);
+        if (sb == 1 && db == 1)
+            convert_vec_kernel<uint8_t, uint8_t><<<grid, 256, 0, st>>>(s, (const uint8_t*)src, d, (uint8_t*)dst, n);
+        else if (sb == 1)
+            convert_vec_kernel<uint8_t, uint16_t><<<grid, 256, 0, st>>>(s, (const uint8_t*)src, d, (uint16_t*)dst, n);
+        else if (db == 1)
+            convert_vec_kernel<uint16_t, uint8_t><<<grid, 256, 0, st>>>(s, (const uint16_t*)src, d, (uint8_t*)dst, n);
+        else
+            convert_vec_kernel<uint16_t, uint16_t><<<grid, 256, 0, st>>>(s, (const uint16_t*)src, d, (uint16_t*)dst, n);
+    } else {
+        convert_kernel<<<grid1(n), 256, 0, st>>>(s, bytes_of(src_nbits), src, d, bytes_of(dst_nbits),
+                                                 dst, n);
+    }
     return launched("convert");
 }
 
@@ -394,8 +509,15 @@ int pnn_relu_fwd(int nbits, int es, const void* x, void* y, int64_t n, void* str
     CHECK_FMT(nbits, es);
     if (n < 0) return set_status(PNN_EINVAL, "relu: bad size");
     if (n == 0) return PNN_OK;
-    relu_fwd_kernel<<<grid1(n), 256, 0, (cudaStream_t)stream>>>(make_fmt(nbits, es),
-                                                                bytes_of(nbits), x, y, n);
+    auto st = (cudaStream_t)stream;
+    if (aligned16(x) && aligned16(y)) {
+        if (bytes_of(nbits) == 1)
+            relu_fwd_vec_kernel<uint8_t><<<grid1(n / 8 + 1), 256, 0, st>>>(nbits, (const uint8_t*)x, (uint8_t*)y, n);
+        else
+            relu_fwd_vec_kernel<uint16_t><<<grid1(n / 8 + 1), 256, 0, st>>>(nbits, (const uint16_t*)x, (uint16_t*)y, n);
+    } else {
+        relu_fwd_kernel<<<grid1(n), 256, 0, st>>>(make_fmt(nbits, es), bytes_of(nbits), x, y, n);
+    }
     return launched("relu_fwd");
 }
 
@@ -405,8 +527,22 @@ int pnn_relu_bwd(int x_nbits, int x_es, const void* x, int g_nbits, int g_es, co
     CHECK_FMT(g_nbits, g_es);
     if (n < 0) return set_status(PNN_EINVAL, "relu: bad size");
     if (n == 0) return PNN_OK;
-    relu_bwd_kernel<<<grid1(n), 256, 0, (cudaStream_t)stream>>>(
-        make_fmt(x_nbits, x_es), bytes_of(x_nbits), x, bytes_of(g_nbits), dy, dx, n);
+    auto st = (cudaStream_t)stream;
+    if (aligned16(x) && aligned16(dy) && aligned16(dx)) {
+        const int grid = grid1(n / 8 + 1);
+        const int xb = bytes_of(x_nbits), gb = bytes_of(g_nbits);
+        if (xb == 1 && gb == 1)
+            relu_bwd_vec_kernel<uint8_t, uint8_t><<<grid, 256, 0, st>>>(x_nbits, (const uint8_t*)x, (const uint8_t*)dy, (uint8_t*)dx, n);
+        else if (xb == 1)
+            relu_bwd_vec_kernel<uint8_t, uint16_t><<<grid, 256, 0, st>>>(x_nbits, (const uint8_t*)x, (const uint16_t*)dy, (uint16_t*)dx, n);
+        else if (gb == 1)
+            relu_bwd_vec_kernel<uint16_t, uint8_t><<<grid, 256, 0, st>>>(x_nbits, (const uint16_t*)x, (const uint8_t*)dy, (uint8_t*)dx, n);
+        else
+            relu_bwd_vec_kernel<uint16_t, uint16_t><<<grid, 256, 0, st>>>(x_nbits, (const uint16_t*)x, (const uint16_t*)dy, (uint16_t*)dx, n);
+    } else {
+        relu_bwd_kernel<<<grid1(n), 256, 0, st>>>(make_fmt(x_nbits, x_es), bytes_of(x_nbits), x,
+                                                  bytes_of(g_nbits), dy, dx, n);
+    }
     return launched("relu_bwd");
 }
 

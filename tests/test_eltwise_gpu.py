@@ -85,6 +85,23 @@ def test_relu(cuda, po, cfg):
     assert (host(ops.relu_bwd(cfg, dev(cfg, x), g, dev(g, dy))) == po.relu_bwd(n, es, x, dy)).all()
 
 
+@pytest.mark.parametrize("pair", [((8, 1), (12, 1)), ((12, 1), (16, 1)), ((16, 1), (8, 0))])
+def test_vector_paths_tails_and_unaligned(cuda, po, pair):
+    """16-byte vector paths: lengths that are not multiples of 8 (scalar tail)
+    and unaligned views (scalar fallback) give the same codes."""
+    (sn, se), (dn, de) = pair
+    rng = np.random.default_rng(sn + dn)
+    x = rng.integers(0, 1 << sn, 5003).astype(np.uint64)
+    dy = rng.integers(0, 1 << dn, 5003).astype(np.uint64)
+    xt, dyt = dev((sn, se), x), dev((dn, de), dy)
+    for sl in (slice(0, 5003), slice(1, 5003), slice(3, 4000)):
+        got = host(ops.convert_tensor(xt[sl], (sn, se), (dn, de)))
+        assert (got == po.convert_tensor(sn, se, dn, de, x[sl])).all(), sl
+        assert (host(ops.relu_fwd((sn, se), xt[sl])) == po.relu_fwd(sn, se, x[sl])).all(), sl
+        got = host(ops.relu_bwd((sn, se), xt[sl], (dn, de), dyt[sl]))
+        assert (got == po.relu_bwd(sn, se, x[sl], dy[sl])).all(), sl
+
+
 @pytest.mark.parametrize("cfg", FORMATS)
 @pytest.mark.parametrize("geom", [(2, 2), (3, 2), (3, 1), (2, 1)])
 def test_maxpool(cuda, po, cfg, geom):
