@@ -234,6 +234,16 @@ cudaError_t launch_kernel(const CUtensorMap& tA, const CUtensorMap& tB, const Ig
         k = a.f.W <= 32 ? igemm_kernel<D, 1, CodeT, MODE> : igemm_kernel<D, 2, CodeT, MODE>;
     else
         k = a.f.W <= 64 ? igemm_kernel<D, 2, CodeT, MODE> : igemm_kernel<D, 4, CodeT, MODE>;
+    // BASELINE formats: epilogue specialised on the compile-time format
+    const int fid = fixed_fmt_id(a.f);
+    if constexpr (D == 2 && sizeof(CodeT) == 1)
+        if (fid == 1) k = igemm_kernel<2, 1, CodeT, MODE, 1>;
+    if constexpr (D == 4 && sizeof(CodeT) == 1)
+        if (fid == 2) k = igemm_kernel<4, 2, CodeT, MODE, 2>;
+    if constexpr (D == 6 && sizeof(CodeT) == 2)
+        if (fid == 3) k = igemm_kernel<6, 4, CodeT, MODE, 3>;
+    if constexpr (D == 8 && sizeof(CodeT) == 2)
+        if (fid == 4) k = igemm_kernel<8, 4, CodeT, MODE, 4>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Geo::SMEM);
     if (e != cudaSuccess) return e;
     const int64_t tiles = a.mtiles * a.ntiles * a.splits;

@@ -63,7 +63,7 @@ struct IgemmArgs {
     unsigned __int128* partial;
 };
 
-template <int D, int QW, typename CodeT, int MODE>
+template <int D, int QW, typename CodeT, int MODE, int FMT = 0>
 __global__ void __launch_bounds__(kThreads, 1)
     igemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  const IgemmArgs a, const OutMap<CodeT> out) {
@@ -207,6 +207,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else {
         // ===== epilogue: TMEM -> quire words -> posit codes / split-K partials =====
         const int quarter = warp & 3;
+        const PositFmt f = fixed_fmt<FMT>(a.f);  // compile-time for the BASELINE formats
         const int half = (warp - 2) >> 2;
         // alternate 8-column chunks per warp of a lane quarter (balanced when N < NT)
         const uint32_t trow = tmem + (uint32_t(quarter * 32) << 16) + half * 8;
@@ -249,8 +250,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int c = 0; c < COLS; ++c)
                     if (colbase + 2 * (c & ~7) + (c & 7) < a.N) {
                         const int64_t xb = a.col_add[colbase + 2 * (c & ~7) + (c & 7)];
-                        if constexpr (QW == 4) q[c] += QT(__int128(xb)) << a.f.R;
-                        else q[c] += QT(xb) << a.f.R;
+                        if constexpr (QW == 4) q[c] += QT(__int128(xb)) << f.R;
+                        else q[c] += QT(xb) << f.R;
                     }
             }
 #pragma unroll
@@ -270,7 +271,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (x < valid) {
                         const bool nar = a.col_nar != nullptr && a.col_nar[col0 + x];
                         out.base[obase + (col0 + x) * ostride] =
-                            CodeT(nar ? (1u << (a.f.nbits - 1)) : quire_word_to_posit(a.f, q[c0 + x]));
+                            CodeT(nar ? (1u << (f.nbits - 1)) : quire_word_to_posit(f, q[c0 + x]));
                     }
             }
         }

@@ -33,6 +33,25 @@ __host__ __device__ inline PositFmt make_fmt(int nbits, int es) {
     return f;
 }
 
+// Compile-time formats of the BASELINE configs, for kernel specialisations
+// whose epilogues then constant-fold every mask and shift; 0 = the runtime
+// format argument.
+template <int FMT>
+__device__ __forceinline__ PositFmt fixed_fmt(const PositFmt& rt) {
+    if constexpr (FMT == 1) return PositFmt{8, 0, 6, 32};
+    else if constexpr (FMT == 2) return PositFmt{8, 1, 12, 56};
+    else if constexpr (FMT == 3) return PositFmt{12, 1, 20, 92};
+    else if constexpr (FMT == 4) return PositFmt{16, 1, 28, 128};
+    else return rt;
+}
+inline int fixed_fmt_id(const PositFmt& f) {
+    if (f.es == 0 && f.nbits == 8) return 1;
+    if (f.es == 1 && f.nbits == 8) return 2;
+    if (f.es == 1 && f.nbits == 12) return 3;
+    if (f.es == 1 && f.nbits == 16) return 4;
+    return 0;
+}
+
 // Decode one code into X (two's complement int64).  Returns true for NaR.
 // Valid for 2 <= nbits <= 32 and 2R <= 62 (X fits int64).
 __device__ __forceinline__ bool decode_x(uint32_t code, const PositFmt& f, int64_t& X) {

@@ -416,17 +416,18 @@ __device__ __forceinline__ void tile_coords(int64_t t, int64_t mtiles, int64_t n
 // issuer, warps 2..9 = epilogue (2 warps per TMEM lane quarter, each owning
 // half of the tile's columns).  The epilogue drains TMEM into registers,
 // releases it (tmem_empty), and rounds/stores while the next tile's MMAs run.
-template <int D, int QW, typename CodeT, bool kPair>
+template <int D, int QW, typename CodeT, bool kPair, int FMT = 0>
 __global__ void __launch_bounds__(kThreads, 1)
     quire_gemm_tc_kernel(const int8_t* __restrict__ a_img, const int8_t* __restrict__ b_img,
                          int64_t kbt, int64_t kb_per_split, const uint8_t* __restrict__ row_nar,
                          const uint8_t* __restrict__ col_nar, OutMap<CodeT> out, int64_t M,
-                         int64_t N, PositFmt f,
+                         int64_t N, PositFmt f_arg,
                          unsigned __int128* __restrict__ partial, int64_t mtiles, int64_t ntiles,
                          int64_t splits) {
     // kPair: clusters of 2 CTAs run one M=256 tcgen05.mma.cta_group::2 per
     // digit plane; each CTA stages its own 128-row A tile and HALF of the
     // concatenated B rows, halving each SM's shared-memory operand traffic.
+    const PositFmt f = fixed_fmt<FMT>(f_arg);  // compile-time for the BASELINE formats
     using Geo = Geometry<D>;
     using QT = typename QuireWord<QW>::T;
     constexpr int NT = Geo::NT, KB = Geo::KB, STAGES = Geo::STAGES, G = Geo::G;
@@ -841,6 +842,16 @@ cudaError_t launch_generic(const QuireGemmPlan& p, const GemmArgs& g, FA fa, FB 
         else
             kern = f.W <= 64 ? quire_gemm_tc_kernel<D, 2, CodeT, false>
                              : quire_gemm_tc_kernel<D, 4, CodeT, false>;
+        // BASELINE formats: epilogue specialised on the compile-time format
+        const int fid = fixed_fmt_id(f);
+        if constexpr (D == 2 && sizeof(CodeT) == 1)
+            if (fid == 1) kern = quire_gemm_tc_kernel<2, 1, CodeT, false, 1>;
+        if constexpr (D == 4 && sizeof(CodeT) == 1)
+            if (fid == 2) kern = quire_gemm_tc_kernel<4, 2, CodeT, false, 2>;
+        if constexpr (D == 6 && sizeof(CodeT) == 2)
+            if (fid == 3) kern = quire_gemm_tc_kernel<6, 4, CodeT, false, 3>;
+        if constexpr (D == 8 && sizeof(CodeT) == 2)
+            if (fid == 4) kern = quire_gemm_tc_kernel<8, 4, CodeT, false, 4>;
     }
     if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Geo::SMEM)) !=
         cudaSuccess)
