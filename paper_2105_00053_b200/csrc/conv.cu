@@ -239,18 +239,31 @@ __global__ void __launch_bounds__(256) bias_grad_partial_kernel(
     const uint32_t nar_code = 1u << (f.nbits - 1);
     __int128 acc = 0;
     bool nar = false;
+    auto term = [&](uint32_t code) {
+        int64_t X;
+        if (xlut != nullptr) {  // exact integer image from the per-call table
+            X = __ldg(xlut + code);
+            nar |= code == nar_code;
+        } else {
+            nar |= decode_x(code, f, X);
+        }
+        acc += X;
+    };
+    constexpr int VE = 16 / int(sizeof(CodeT));  // codes per 16-byte load
     for (int64_t n = n0; n < n1; ++n) {
         const CodeT* row = dy + (n * F + ch) * P;
-        for (int o = threadIdx.x; o < int(P); o += blockDim.x) {
-            const uint32_t code = uint32_t(row[o]);
-            int64_t X;
-            if (xlut != nullptr) {  // exact integer image from the per-call table
-                X = __ldg(xlut + code);
-                nar |= code == nar_code;
-            } else {
-                nar |= decode_x(code, f, X);
+        if (P % VE == 0 && (reinterpret_cast<uintptr_t>(row) & 15) == 0) {
+            // 16-byte loads: VE independent table lookups in flight per thread
+            for (int v = threadIdx.x; v < int(P / VE); v += blockDim.x) {
+                const uint4 w = __ldg(reinterpret_cast<const uint4*>(row) + v);
+                const uint32_t* ww = reinterpret_cast<const uint32_t*>(&w);
+#pragma unroll
+                for (int j = 0; j < VE; ++j)
+                    term(sizeof(CodeT) == 1 ? (ww[j >> 2] >> (8 * (j & 3))) & 0xFFu
+                                            : (ww[j >> 1] >> (16 * (j & 1))) & 0xFFFFu);
             }
-            acc += X;
+        } else {
+            for (int o = threadIdx.x; o < int(P); o += blockDim.x) term(uint32_t(row[o]));
         }
     }
     // block reduction: 128-bit butterfly per warp, then one word per warp

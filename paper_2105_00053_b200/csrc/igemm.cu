@@ -55,14 +55,36 @@ struct ImplPlan {
     size_t adig, bdig;      // bytes
     size_t off_adig, off_bdig, off_col_add, off_lut, off_maps, maps_bytes, off_pos_nar, off_chw_nar,
         off_col_nar, off_flags, off_partial, total;
+    bool fold;    // first-layer tap folding: planned on the virtual 1x1 geometry gv
+    int ckk;      // C * KH * KW of the real layer
+    ConvGeom gv;  // geometry the plan runs on (== the real one unless folded)
 };
 
-bool make_plan(int pass, const PositFmt& f, const ConvGeom& g, bool raw, ImplPlan* p) {
-    if (conv_algo() == 1 || g.stride != 1) return false;
-    if (g.N < 1 || g.N > (1 << 30)) return false;
+// A first layer with few input channels (C*KH*KW <= 32, stride 1) runs as a
+// 1x1 convolution over the folded receptive fields (im2col_digits_kernel):
+// one 32-wide K block for the forward pass, one 32-row M tile for the weight
+// gradient.  (Its input gradient is never needed, so pass 1 does not fold.)
+bool fold_geom(int pass, const ConvGeom& g, ConvGeom* gv) {
+    if (pass == 1 || g.stride != 1 || g.C % 32 == 0 || g.C * g.KH * g.KW > 32) return false;
+    *gv = g;
+    gv->C = 32;
+    gv->H = g.OH;
+    gv->W = g.OW;
+    gv->KH = gv->KW = 1;
+    gv->pad = 0;
+    return true;
+}
+
+bool make_plan(int pass, const PositFmt& f, const ConvGeom& g_real, bool raw, ImplPlan* p) {
+    if (conv_algo() == 1 || g_real.stride != 1) return false;
+    if (g_real.N < 1 || g_real.N > (1 << 30)) return false;
     const int D = digits_for(f);
     if (D < 2 || D > 8) return false;
     *p = ImplPlan{};
+    p->ckk = int(g_real.C * g_real.KH * g_real.KW);
+    p->gv = g_real;
+    p->fold = fold_geom(pass, g_real, &p->gv);
+    const ConvGeom& g = p->gv;
     p->mode = pass;
     p->D = D;
     p->NT = nt_for(D);
@@ -126,7 +148,7 @@ bool make_plan(int pass, const PositFmt& f, const ConvGeom& g, bool raw, ImplPla
         a.slots = int(128 / g.C);
         a.kpr = int(g.OW / OWb);
         a.kpi = int((g.OH / OHb) * a.kpr);
-        a.M = taps * g.C;
+        a.M = p->fold ? p->ckk : taps * g.C;  // folded: rows (c,ky,kx) < C*KH*KW
         a.N = g.F;
         a.mtiles = cdiv(taps, a.slots);
         p->Fpw = cdiv(g.F, p->NT) * p->NT;
@@ -295,6 +317,30 @@ cudaError_t act_digits(int D, const CodeT* x, int64_t N, int64_t C, int64_t H, i
 }
 
 template <typename CodeT>
+cudaError_t im2col_digits(int D, const CodeT* x, const ConvGeom& g, const PositFmt& f, uint32_t* lut,
+                          int8_t* dig, uint8_t* pos_nar, uint8_t* chw_nar, uint8_t* any,
+                          cudaStream_t st) {
+    const int grid = grid_for(g.N * g.OH * g.OW * 8, 256);
+#define PNN_I2C(DD)                                                                          \
+    if (lut) digit_lut_kernel<DD><<<16, 256, 0, st>>>(f, lut);                               \
+    im2col_digits_kernel<DD, CodeT><<<grid, 256, 0, st>>>(                                   \
+        x, g.N, int(g.C), int(g.H), int(g.W), int(g.KH), int(g.KW), g.pad, int(g.OH), int(g.OW), \
+        f, lut, dig, pos_nar, chw_nar, any)
+    switch (D) {
+        case 2: PNN_I2C(2); break;
+        case 3: PNN_I2C(3); break;
+        case 4: PNN_I2C(4); break;
+        case 5: PNN_I2C(5); break;
+        case 6: PNN_I2C(6); break;
+        case 7: PNN_I2C(7); break;
+        case 8: PNN_I2C(8); break;
+        default: return cudaErrorInvalidValue;
+    }
+#undef PNN_I2C
+    return cudaGetLastError();
+}
+
+template <typename CodeT>
 cudaError_t weight_digits(int D, const CodeT* w, const CodeT* bias, int64_t F, int64_t C,
                           int64_t taps, int64_t Kp, int transpose, const PositFmt& f, int8_t* dig,
                           int64_t* col_add, uint8_t* col_nar, uint8_t* any, cudaStream_t st) {
@@ -332,15 +378,19 @@ int run_fwd(const ImplPlan& p, const ConvGeom& g, const CodeT* x, const CodeT* w
     uint8_t* flags = ws + p.off_flags;
     cudaError_t e;
     if ((e = cudaMemsetAsync(ws + p.off_maps, 0, p.maps_bytes, st)) != cudaSuccess) return 4;
-    if ((e = act_digits<CodeT>(p.D, x, g.N, g.C, g.H, g.W, p.Ca, f, lut_of(p, ws), true, adig, pos_nar, nullptr,
-                               nullptr, flags, st)) != cudaSuccess)
-        return 4;
-    const int64_t taps = g.KH * g.KW;
-    if ((e = weight_digits<CodeT>(p.D, w, bias, g.F, g.C, taps, p.Kp, 0, f, bdig, col_add, col_nar,
-                                  flags + 1, st)) != cudaSuccess)
+    const ConvGeom& gv = p.gv;  // virtual 1x1 geometry when the first layer is folded
+    if (p.fold)
+        e = im2col_digits<CodeT>(p.D, x, g, f, lut_of(p, ws), adig, pos_nar, nullptr, flags, st);
+    else
+        e = act_digits<CodeT>(p.D, x, g.N, g.C, g.H, g.W, p.Ca, f, lut_of(p, ws), true, adig,
+                              pos_nar, nullptr, nullptr, flags, st);
+    if (e != cudaSuccess) return 4;
+    const int64_t taps = gv.KH * gv.KW;  // weights: [F][C*KH*KW] read as [F][ckk][1][1] if folded
+    if ((e = weight_digits<CodeT>(p.D, w, bias, g.F, p.fold ? p.ckk : g.C, taps, p.Kp, 0, f, bdig,
+                                  col_add, col_nar, flags + 1, st)) != cudaSuccess)
         return 4;
     CUtensorMap tA, tB;
-    if (!map_act(&tA, adig, p.D, g.N, g.H, g.W, p.Ca, p.boxA, 32) ||
+    if (!map_act(&tA, adig, p.D, gv.N, gv.H, gv.W, p.Ca, p.boxA, 32) ||
         !map_weights(&tB, bdig, p.D, p.brows, taps * p.Kp, p.NT))
         return 5;
     IgemmArgs a = p.a;
@@ -354,8 +404,8 @@ int run_fwd(const ImplPlan& p, const ConvGeom& g, const CodeT* x, const CodeT* w
         quire_finalize_kernel<CodeT><<<grid_for(a.M * a.N, 256), 256, 0, st>>>(
             a.partial, int(a.splits), nullptr, col_nar, out, a.M, a.N, f, nullptr, nullptr);
     fwd_nar_fixup_kernel<CodeT><<<grid_for(a.M, 256), 256, 0, st>>>(
-        y, pos_nar, flags, g.N, int(g.F), int(g.H), int(g.W), int(g.OH), int(g.OW), int(g.KH),
-        int(g.KW), g.pad, 1u << (f.nbits - 1));
+        y, pos_nar, flags, g.N, int(g.F), int(gv.H), int(gv.W), int(g.OH), int(g.OW), int(gv.KH),
+        int(gv.KW), gv.pad, 1u << (f.nbits - 1));
     return rc_of(cudaGetLastError());
 }
 
@@ -408,15 +458,20 @@ int run_wgrad(const ImplPlan& p, const ConvGeom& g, const CodeT* dy, const CodeT
     uint8_t* col_nar = ws + p.off_col_nar;
     uint8_t* flags = ws + p.off_flags;
     if (cudaMemsetAsync(ws + p.off_maps, 0, p.maps_bytes, st) != cudaSuccess) return 4;
-    if (act_digits<CodeT>(p.D, x, g.N, g.C, g.H, g.W, p.Ca, f, lut_of(p, ws), true, adig, nullptr, chw_nar, nullptr,
-                          flags, st) != cudaSuccess)
-        return 4;
+    const ConvGeom& gv = p.gv;  // virtual 1x1 geometry when the first layer is folded
+    cudaError_t e;
+    if (p.fold)
+        e = im2col_digits<CodeT>(p.D, x, g, f, lut_of(p, ws), adig, nullptr, chw_nar, flags, st);
+    else
+        e = act_digits<CodeT>(p.D, x, g.N, g.C, g.H, g.W, p.Ca, f, lut_of(p, ws), true, adig,
+                              nullptr, chw_nar, nullptr, flags, st);
+    if (e != cudaSuccess) return 4;
     if (act_digits<CodeT>(p.D, dy, g.N, g.F, g.OH, g.OW, p.Fpw, f, lut_of(p, ws), false, bdig, nullptr, nullptr, col_nar,
                           flags + 1, st) != cudaSuccess)
         return 4;
     CUtensorMap tA, tB;
     const uint32_t boxB[4] = {uint32_t(p.NT), uint32_t(p.a.OWb), uint32_t(p.a.OHb), 1};
-    if (!map_act(&tA, adig, p.D, g.N, g.H, g.W, p.Ca, p.boxA, p.a.a_sw) ||
+    if (!map_act(&tA, adig, p.D, gv.N, gv.H, gv.W, p.Ca, p.boxA, p.a.a_sw) ||
         !map_act(&tB, bdig, p.D, g.N, g.OH, g.OW, p.Fpw, boxB, p.a.b_sw))
         return 5;
     IgemmArgs a = p.a;
@@ -426,17 +481,17 @@ int run_wgrad(const ImplPlan& p, const ConvGeom& g, const CodeT* dy, const CodeT
     a.partial = use_partial ? reinterpret_cast<unsigned __int128*>(ws + p.off_partial) : nullptr;
     OutMap<CodeT> out;
     out.base = dw;
-    out.ldc = g.C * g.KH * g.KW;
-    out.inner = g.C;
-    out.ncols = g.KH * g.KW;
+    out.ldc = p.ckk;    // dw[f][(c,ky,kx)]
+    out.inner = gv.C;   // rows m = tap * inner + channel (folded: m = (c,ky,kx), one tap)
+    out.ncols = gv.KH * gv.KW;
     out.mode = 2;
     if (dispatch<CodeT, 2>(p.D, tA, tB, a, out, st) != cudaSuccess) return 4;
     if (use_partial)
         quire_finalize_kernel<CodeT><<<grid_for(a.M * a.N, 256), 256, 0, st>>>(
             a.partial, int(a.splits), nullptr, col_nar, out, a.M, a.N, f, raw_words, raw_nar);
-    wgrad_nar_fixup_kernel<CodeT><<<grid_for(g.C * g.KH * g.KW, 128), 128, 0, st>>>(
-        dw, raw_nar, chw_nar, flags, int(g.F), int(g.C), int(g.H), int(g.W), int(g.OH), int(g.OW),
-        int(g.KH), int(g.KW), g.pad, 1u << (f.nbits - 1));
+    wgrad_nar_fixup_kernel<CodeT><<<grid_for(p.ckk, 128), 128, 0, st>>>(
+        dw, raw_nar, chw_nar, flags, int(g.F), p.fold ? p.ckk : int(g.C), int(gv.H), int(gv.W),
+        int(g.OH), int(g.OW), int(gv.KH), int(gv.KW), gv.pad, 1u << (f.nbits - 1));
     return rc_of(cudaGetLastError());
 }
 

@@ -424,6 +424,49 @@ __global__ void __launch_bounds__(256) act_digits_kernel(
     }
 }
 
+// First-layer tap folding (C*KH*KW <= 32, stride 1): the receptive field of
+// each output pixel becomes the 32 "channels" of a virtual 1x1 convolution,
+// dig[D][N][OH][OW][32] with channel k = (c, ky, kx) (zero past C*KH*KW and
+// outside the image).  NaR summaries in the virtual geometry: pos_nar[n][oy][ox]
+// (forward rows) and chw_nar[k][oy][ox] (weight-grad rows).
+template <int D, typename CodeT>
+__global__ void __launch_bounds__(256) im2col_digits_kernel(
+    const CodeT* __restrict__ x, int64_t N, int C, int H, int W, int KH, int KW, int pad, int OH,
+    int OW, PositFmt f, const uint32_t* __restrict__ lut, int8_t* __restrict__ dig,
+    uint8_t* __restrict__ pos_nar, uint8_t* __restrict__ chw_nar, uint8_t* __restrict__ any) {
+    const int ckk = C * KH * KW, khw = KH * KW;
+    const int64_t P = int64_t(OH) * OW;
+    const int64_t plane = N * P * 32;
+    for (int64_t g = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; g < N * P * 8;
+         g += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t pos = g >> 3;  // (n, oy, ox) raster
+        const int q = int(g & 7);
+        const int64_t n = pos / P;
+        const int pix = int(pos - n * P), oy = pix / OW, ox = pix - oy * OW;
+        uint32_t c4[4];
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+            const int k = 4 * q + jj;
+            uint32_t code = 0;
+            if (k < ckk) {
+                const int c = k / khw, t = k - c * khw, ky = t / KW, kx = t - ky * KW;
+                const int iy = oy + ky - pad, ix = ox + kx - pad;
+                if (unsigned(iy) < unsigned(H) && unsigned(ix) < unsigned(W))
+                    code = uint32_t(x[((n * C + c) * H + iy) * W + ix]);
+            }
+            c4[jj] = code;
+        }
+        const uint32_t nm = digits4<D>(c4, f, lut, dig + pos * 32 + 4 * q, plane);
+        if (nm)
+            for (int jj = 0; jj < 4; ++jj)
+                if (((nm >> jj) & 1) && 4 * q + jj < ckk) {
+                    if (pos_nar) pos_nar[pos] = 1;
+                    if (chw_nar) chw_nar[int64_t(4 * q + jj) * P + pix] = 1;
+                    *any = 1;
+                }
+    }
+}
+
 // w [F][C][KH][KW] -> K-major weight digits dig[D][rows][taps * Kp]:
 //   transpose = 0 (forward):    rows = F, element (f, tap, c) = w[f][c][tap]
 //   transpose = 1 (input grad): rows = C, element (c, tap, f) = w[f][c][tap]

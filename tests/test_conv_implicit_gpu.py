@@ -27,6 +27,9 @@ SHAPES = [
     (2, 32, 10, 10, 32, 3, 0, "fw"),     # valid conv: fwd 8x8 tiles, box reads inside 10x10
     (2, 32, 8, 8, 40, 3, 1, "fw"),       # F = 40: partial N tile / padded dy digits
     (2, 128, 8, 8, 32, 3, 1, "fdw"),     # 128-channel wgrad slot (128B swizzle)
+    (2, 3, 32, 32, 32, 3, 1, "fdw"),     # first layer: taps folded into 27 of 32 channels
+    (2, 1, 16, 16, 8, 5, 2, "fw"),       # folded 5x5, C = 1 (25 taps), pad 2
+    (4, 2, 10, 10, 32, 3, 0, "fw"),      # folded valid conv
     (4, 64, 1, 1, 32, 1, 0, "fd"),       # Linear as 1x1 conv: elementwise digitiser
     (130, 32, 1, 1, 64, 1, 0, "fd"),     # Linear, 128 rows per tile + a partial tile
 ]
@@ -113,6 +116,26 @@ def test_implicit_conv_nar(cuda, po, cfg, implicit_only):
 
 
 @pytest.mark.parametrize("cfg", FORMATS)
+def test_folded_first_layer_nar(cuda, po, cfg, implicit_only):
+    """Tap-folded first layer: NaR rows rebuilt from the folded receptive fields."""
+    n, es = cfg
+    nar = 1 << (n - 1)
+    rng = np.random.default_rng(21 + n + es)
+    x = rand_codes(rng, n, (2, 3, 16, 16))
+    w = rand_codes(rng, n, (32, 3, 3, 3))
+    b = rand_codes(rng, n, (32,))
+    x[1, 2, 15, 0] = nar  # corner: only taps reaching it see it
+    w[4, 1, 0, 2] = nar
+    y = host(ops.conv2d(cfg, dev(cfg, x), dev(cfg, w), dev(cfg, b), 1, 1))
+    want = po.conv2d(n, es, x, w, b, 1, 1)
+    assert (y == want).all() and (want != nar).any()
+    dy = rand_codes(rng, n, want.shape)
+    dw = host(ops.conv2d_weight_grad(cfg, dev(cfg, dy), dev(cfg, x), w.shape, 1, 1))
+    want = po.conv2d_weight_grad(n, es, dy, x, w.shape, 1, 1)
+    assert (dw == want).all() and (want != nar).any()
+
+
+@pytest.mark.parametrize("cfg", FORMATS)
 def test_implicit_linear_nar(cuda, po, cfg, implicit_only):
     n, es = cfg
     nar = 1 << (n - 1)
@@ -151,10 +174,10 @@ def test_implicit_wgrad_long_k_raw_words(cuda, po, cfg, implicit_only):
 
 def test_ineligible_shape_fails_loudly_when_forced(cuda, implicit_only):
     cfg = (8, 0)
-    x = torch.zeros((1, 3, 8, 8), dtype=torch.uint8, device="cuda")
-    w = torch.zeros((32, 3, 3, 3), dtype=torch.uint8, device="cuda")
+    x = torch.zeros((1, 32, 8, 8), dtype=torch.uint8, device="cuda")
+    w = torch.zeros((32, 32, 3, 3), dtype=torch.uint8, device="cuda")
     with pytest.raises(Exception):
-        ops.conv2d(cfg, x, w, None, 1, 1)
+        ops.conv2d(cfg, x, w, None, 2, 1)  # stride 2: no implicit tiling
 
 
 def test_auto_matches_explicit_on_cifar_layer(cuda):
