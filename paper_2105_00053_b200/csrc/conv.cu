@@ -228,6 +228,35 @@ struct FetchWgradDy {  // X[r = f][k = (n,o)] = dy[n][f][o]
 // Exact quire sum of dy over (n, pixel) per channel: Q_f = 2^R * sum X (mod
 // 2^W).  Stage 1: each block reduces a slice of (n) for one f into a 128-bit
 // partial (|sum X| < 2^56 * 2^31 fits); stage 2 sums partials and rounds.
+// P == 1 (Linear layers, column sums of dy [N][F]): a thread per channel,
+// coalesced along F, a slice of rows per blockIdx.y; same partial layout.
+template <typename CodeT>
+__global__ void __launch_bounds__(256) bias_grad_cols_kernel(
+    const CodeT* __restrict__ dy, int64_t N, int64_t F, PositFmt f, int slices,
+    const int64_t* __restrict__ xlut, unsigned __int128* __restrict__ partial,
+    uint8_t* __restrict__ nar_out) {
+    const int64_t ch = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+    if (ch >= F) return;
+    const int64_t slice = blockIdx.y, per = (N + slices - 1) / slices;
+    const int64_t n0 = slice * per, n1 = min(N, n0 + per);
+    const uint32_t nar_code = 1u << (f.nbits - 1);
+    __int128 acc = 0;
+    bool nar = false;
+    for (int64_t n = n0; n < n1; ++n) {
+        const uint32_t code = uint32_t(dy[n * F + ch]);
+        int64_t X;
+        if (xlut != nullptr) {
+            X = __ldg(xlut + code);
+            nar |= code == nar_code;
+        } else {
+            nar |= decode_x(code, f, X);
+        }
+        acc += X;
+    }
+    partial[ch * slices + slice] = (unsigned __int128)acc;
+    if (nar) nar_out[ch] = 1;
+}
+
 template <typename CodeT>
 __global__ void __launch_bounds__(256) bias_grad_partial_kernel(
     const CodeT* __restrict__ dy, int64_t N, int64_t F, int64_t P, PositFmt f, int slices,
@@ -550,7 +579,20 @@ int pnn_bias_grad(int nbits, int es, const void* dy, int64_t N, int64_t F, int64
         xlut = reinterpret_cast<int64_t*>(static_cast<uint8_t*>(workspace) + bias_lut_offset(F));
         x_lut_kernel<<<(1 << nbits) / 256 + 1, 256, 0, st>>>(f, xlut);
     }
-    if (nbits <= 8) {
+    const dim3 cgrid{unsigned((F + 255) / 256), unsigned(slices), 1u};
+    if (P == 1 && nbits <= 8) {
+        bias_grad_cols_kernel<uint8_t><<<cgrid, 256, 0, st>>>((const uint8_t*)dy, N, F, f, slices,
+                                                              xlut, partial, nar);
+        bias_grad_final_kernel<uint8_t><<<grid_for(F, 128), 128, 0, st>>>(
+            partial, slices, nar, F, f, (uint8_t*)db, (unsigned __int128*)raw_words,
+            (uint8_t*)raw_nar);
+    } else if (P == 1) {
+        bias_grad_cols_kernel<uint16_t><<<cgrid, 256, 0, st>>>((const uint16_t*)dy, N, F, f,
+                                                               slices, xlut, partial, nar);
+        bias_grad_final_kernel<uint16_t><<<grid_for(F, 128), 128, 0, st>>>(
+            partial, slices, nar, F, f, (uint16_t*)db, (unsigned __int128*)raw_words,
+            (uint8_t*)raw_nar);
+    } else if (nbits <= 8) {
         bias_grad_partial_kernel<uint8_t><<<grid, 256, 0, st>>>((const uint8_t*)dy, N, F, P, f,
                                                                  slices, xlut, partial, nar);
         bias_grad_final_kernel<uint8_t><<<grid_for(F, 128), 128, 0, st>>>(

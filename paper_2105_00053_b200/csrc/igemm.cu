@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "igemm.h"
 #include "igemm_core.cuh"
@@ -90,6 +91,8 @@ bool make_plan(int pass, const PositFmt& f, const ConvGeom& g_real, bool raw, Im
     p->NT = nt_for(D);
     IgemmArgs& a = p->a;
     a.f = f;
+    static const int debug = getenv("PNN_IGEMM_DEBUG") ? atoi(getenv("PNN_IGEMM_DEBUG")) : 0;
+    a.debug = debug;  // profiling experiments only: results are wrong when set
     a.KW = int(g.KW);
     a.pad = g.pad;
     const int64_t taps = g.KH * g.KW;
@@ -270,7 +273,7 @@ cudaError_t launch_kernel(const CUtensorMap& tA, const CUtensorMap& tB, const Ig
     if (e != cudaSuccess) return e;
     const int64_t tiles = a.mtiles * a.ntiles * a.splits;
     const int grid = int(tiles < num_sms() ? tiles : num_sms());
-    k<<<grid, kThreads, Geo::SMEM, st>>>(tA, tB, a, out);
+    k<<<grid, kIThreads, Geo::SMEM, st>>>(tA, tB, a, out);
     return cudaGetLastError();
 }
 
@@ -294,9 +297,7 @@ cudaError_t act_digits(int D, const CodeT* x, int64_t N, int64_t C, int64_t H, i
                        int64_t Cp, const PositFmt& f, uint32_t* lut, bool build_lut, int8_t* dig,
                        uint8_t* pos_nar, uint8_t* chw_nar, uint8_t* chan_nar, uint8_t* any,
                        cudaStream_t st) {
-    const int64_t RH = W >= kSlab ? 1 : (kSlab / W < H ? kSlab / W : H);
-    const int64_t items = N * ((H + RH - 1) / RH) * ((W + kSlab - 1) / kSlab);
-    const int grid = int(items < 148 * 16 ? items : 148 * 16);
+    const int grid = grid_for(N * H * W * (Cp / 32), 256);  // thread per (pixel, 32 channels)
     if (lut == nullptr) build_lut = false;
 #define PNN_ACT(DD)                                                                              \
     if (build_lut) digit_lut_kernel<DD><<<16, 256, 0, st>>>(f, lut);                             \
@@ -320,7 +321,7 @@ template <typename CodeT>
 cudaError_t im2col_digits(int D, const CodeT* x, const ConvGeom& g, const PositFmt& f, uint32_t* lut,
                           int8_t* dig, uint8_t* pos_nar, uint8_t* chw_nar, uint8_t* any,
                           cudaStream_t st) {
-    const int grid = grid_for(g.N * g.OH * g.OW * 8, 256);
+    const int grid = grid_for(g.N * g.OH * g.OW, 256);  // thread per output pixel
 #define PNN_I2C(DD)                                                                          \
     if (lut) digit_lut_kernel<DD><<<16, 256, 0, st>>>(f, lut);                               \
     im2col_digits_kernel<DD, CodeT><<<grid, 256, 0, st>>>(                                   \

@@ -61,17 +61,26 @@ struct IgemmArgs {
     const uint8_t* col_nar;
     PositFmt f;
     unsigned __int128* partial;
+    int debug;  // profiling only (PNN_IGEMM_DEBUG): 1 skip conversion, 2 skip MMA, 4 skip TMA waits
 };
 
+// 16 epilogue warps (4 per TMEM lane quarter): the epilogue (TMEM drain, quire
+// accumulation, quire -> posit) is the per-tile critical path for the narrow
+// convolution tiles, and it is latency-bound -- more warps, more overlap.
+constexpr int kIEpiWarps = 16;
+constexpr int kIThreads = 64 + 32 * kIEpiWarps;
+
 template <int D, int QW, typename CodeT, int MODE, int FMT = 0>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kIThreads, 1)
     igemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  const IgemmArgs a, const OutMap<CodeT> out) {
     using Geo = ImplGeo<D>;
     using QT = typename QuireWord<QW>::T;
     constexpr int NT = Geo::NT, STAGES = Geo::STAGES, G = Geo::G;
-    constexpr int COLS = NT / 2;
-    constexpr int GB = G < 8 ? G : 8;
+    constexpr int SUB = kIEpiWarps / 4;  // warps per lane quarter
+    constexpr int COLS = NT / SUB;       // columns per epilogue thread
+    static_assert(COLS % 8 == 0, "epilogue chunks");
+    constexpr int GB = G < 8 ? G : (QW == 4 ? 4 : 8);  // TMEM loads per wait (registers)
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024 - (ptx::smem_u32(smem_raw) & 1023)) & 1023);
     uint8_t* zero_tile = smem + STAGES * Geo::STAGE_BYTES;
@@ -85,7 +94,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int lane = threadIdx.x & 31;
     const int64_t tiles = a.mtiles * a.ntiles * a.splits;
 
-    for (int i = threadIdx.x; i < kZeroBytes / 16; i += kThreads)
+    for (int i = threadIdx.x; i < kZeroBytes / 16; i += kIThreads)
         reinterpret_cast<int4*>(zero_tile)[i] = make_int4(0, 0, 0, 0);
     if (warp == 0 && lane == 0) {
         ptx::tma_prefetch_desc(&tmA);
@@ -95,7 +104,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::mbar_init(&empty[s], 1);
         }
         ptx::mbar_init(tmem_full, 1);
-        ptx::mbar_init(tmem_empty, kEpiWarps);
+        ptx::mbar_init(tmem_empty, kIEpiWarps);
         ptx::fence_barrier_init();
     }
     if (warp == 1) ptx::tmem_alloc<512>(tmem_slot);
@@ -129,6 +138,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                     ptx::mbar_wait(&empty[s], ph ^ 1);
                     uint8_t* sa = smem + s * Geo::STAGE_BYTES;
                     uint8_t* sb = sa + Geo::A_BYTES;
+                    if (a.debug & 4) {  // profiling: no operand traffic
+                        ptx::mbar_arrive(&full[s]);
+                        continue;
+                    }
                     ptx::mbar_arrive_expect_tx(&full[s], Geo::STAGE_BYTES);
                     const int kb = int(kb0 + i);
                     if constexpr (MODE != 2) {
@@ -197,7 +210,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                                       D * kIKB * a.a_sw, 8 * a.a_sw, a_lt);
                         else
                             adesc = ptx::smem_desc_sw(a_base + p * (kBM * kIKB), 16, 8 * kIKB, a_lt);
-                        ptx::mma_i8(tmem + p * NT, adesc, bdesc, idesc, (first && p == 0) ? 0u : 1u);
+                        if (!(a.debug & 2)) ptx::mma_i8(tmem + p * NT, adesc, bdesc, idesc, (first && p == 0) ? 0u : 1u);
                     }
                     ptx::mma_commit(&empty[s]);
                 }
@@ -208,9 +221,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ===== epilogue: TMEM -> quire words -> posit codes / split-K partials =====
         const int quarter = warp & 3;
         const PositFmt f = fixed_fmt<FMT>(a.f);  // compile-time for the BASELINE formats
-        const int half = (warp - 2) >> 2;
-        // alternate 8-column chunks per warp of a lane quarter (balanced when N < NT)
-        const uint32_t trow = tmem + (uint32_t(quarter * 32) << 16) + half * 8;
+        const int sub = (warp - 2) >> 2;
+        // the SUB warps of a lane quarter take interleaved 8-column chunks
+        // (chunk i of warp sub = tile columns (sub + SUB * i) * 8: balanced when N < NT)
+        const uint32_t trow = tmem + (uint32_t(quarter * 32) << 16) + sub * 8;
         uint32_t j = 0;
         for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++j) {
             int64_t split, mt, nt;
@@ -226,7 +240,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     uint32_t r[GB][8];
 #pragma unroll
                     for (int g = 0; g < GB; ++g)
-                        if (g0 + g < G) ptx::tmem_ld8(trow + (g0 + g) * NT + 2 * c0, r[g]);
+                        if (g0 + g < G) ptx::tmem_ld8(trow + (g0 + g) * NT + SUB * c0, r[g]);
                     ptx::tmem_wait_ld();
 #pragma unroll
                     for (int g = 0; g < GB; ++g)
@@ -243,20 +257,20 @@ __global__ void __launch_bounds__(kThreads, 1)
 
             const int64_t row = mt * kBM + quarter * 32 + lane;
             if (row >= a.M) continue;
-            const int64_t colbase = nt * NT + half * 8;  // chunk c0 / 8 at colbase + 2 * c0
+            const int64_t colbase = nt * NT + sub * 8;  // chunk c0 / 8 at colbase + SUB * c0
             const int64_t obase = out.row_base(row), ostride = out.col_stride();
             if constexpr (MODE == 0) if (a.col_add != nullptr && split == 0) {
 #pragma unroll
                 for (int c = 0; c < COLS; ++c)
-                    if (colbase + 2 * (c & ~7) + (c & 7) < a.N) {
-                        const int64_t xb = a.col_add[colbase + 2 * (c & ~7) + (c & 7)];
+                    if (colbase + SUB * (c & ~7) + (c & 7) < a.N) {
+                        const int64_t xb = a.col_add[colbase + SUB * (c & ~7) + (c & 7)];
                         if constexpr (QW == 4) q[c] += QT(__int128(xb)) << f.R;
                         else q[c] += QT(xb) << f.R;
                     }
             }
 #pragma unroll
             for (int c0 = 0; c0 < COLS; c0 += 8) {
-                const int64_t col0 = colbase + 2 * c0;
+                const int64_t col0 = colbase + SUB * c0;
                 if (col0 >= a.N) break;
                 const int valid = int(a.N - col0 < 8 ? a.N - col0 : 8);
                 if (a.partial != nullptr) {
@@ -266,13 +280,21 @@ __global__ void __launch_bounds__(kThreads, 1)
                         if (x < valid) dst[x] = (unsigned __int128)q[c0 + x];
                     continue;
                 }
+                // 8 independent branch-free conversions, then predicated stores;
+                // column NaR flags as one 8-byte load (buffers are 256-byte padded)
+                const uint64_t cn = a.col_nar != nullptr
+                                        ? *reinterpret_cast<const uint64_t*>(a.col_nar + col0)
+                                        : 0ull;
+                uint32_t codes[8];
+#pragma unroll
+                for (int x = 0; x < 8; ++x) {
+                    const uint32_t c = (a.debug & 1) ? uint32_t(q[c0 + x]) : quire_word_to_posit_bf(f, q[c0 + x]);
+                    codes[x] = ((cn >> (8 * x)) & 0xFF) ? (1u << (f.nbits - 1)) : c;
+                }
+                CodeT* dst = out.base + obase + col0 * ostride;
 #pragma unroll
                 for (int x = 0; x < 8; ++x)
-                    if (x < valid) {
-                        const bool nar = a.col_nar != nullptr && a.col_nar[col0 + x];
-                        out.base[obase + (col0 + x) * ostride] =
-                            CodeT(nar ? (1u << (f.nbits - 1)) : quire_word_to_posit(f, q[c0 + x]));
-                    }
+                    if (x < valid) dst[x * ostride] = CodeT(codes[x]);
             }
         }
     }
@@ -334,92 +356,88 @@ __device__ __forceinline__ uint32_t digits4(const uint32_t (&c)[4], const PositF
     return nm;
 }
 
+// As digits4, but the plane words go to registers: words[p][q] for 4-channel
+// group q (the caller stores whole 32-byte rows per plane).
+template <int D>
+__device__ __forceinline__ uint32_t digits4_words(const uint32_t (&c)[4], const PositFmt& f,
+                                                  const uint32_t* __restrict__ lut,
+                                                  uint32_t (&words)[D][8], int q) {
+    const uint32_t nar_code = 1u << (f.nbits - 1);
+    uint32_t lo[4], hi[4], nm = 0;
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj) {
+        bool nar;
+        if (lut != nullptr) {
+            const uint2 v = __ldg(reinterpret_cast<const uint2*>(lut) + c[jj]);
+            lo[jj] = v.x;
+            hi[jj] = v.y;
+            nar = c[jj] == nar_code;
+        } else {
+            digit_words<D>(c[jj], f, lo[jj], hi[jj], nar);
+        }
+        nm |= nar ? 1u << jj : 0u;
+    }
+#pragma unroll
+    for (int p = 0; p < D; ++p) {
+        const uint32_t* w = p < 4 ? lo : hi;
+        const uint32_t sel = (p & 3) | (((p & 3) + 4) << 4);
+        const uint32_t a = __byte_perm(w[0], w[1], sel);
+        const uint32_t b = __byte_perm(w[2], w[3], sel);
+        words[p][q] = __byte_perm(a, b, 0x5410);
+    }
+    return nm;
+}
+
 // codes [N][C][H][W] -> dig[D][N][H][W][Cp] (balanced int8 digits; channels
 // >= C are zero), plus NaR summaries written only where a NaR is found:
 // pos_nar[n][h][w] (any channel), chw_nar[c][h][w] (any image), chan_nar[c],
-// *any.  A work item is a slab of RH = 128 / W image rows (one image): 32
-// channels x RH*W pixels are loaded coalesced (rows of one channel are
-// contiguous in NCHW), transposed through shared memory and written as
-// 4-channel words per plane.  1x1 images (Linear layers) need no transpose
-// and take an elementwise path.  lut: digit_lut_kernel output, or null.
-constexpr int kSlab = 128;  // pixels per work item (upper bound)
-
+// *any.  A thread owns one pixel x one 32-channel chunk: its 32 loads are
+// coalesced across the warp (consecutive pixels of one channel plane), and it
+// writes 32 contiguous digit bytes per plane (two 16-byte stores), so the
+// warp's stores are 1 KB contiguous per plane.  lut: digit_lut_kernel output
+// (formats up to 12 bits) or null (decode).
 template <int D, typename CodeT>
 __global__ void __launch_bounds__(256) act_digits_kernel(
     const CodeT* __restrict__ x, int64_t N, int C, int H, int W, int Cp, PositFmt f,
     const uint32_t* __restrict__ lut, int8_t* __restrict__ dig, uint8_t* __restrict__ pos_nar,
     uint8_t* __restrict__ chw_nar, uint8_t* __restrict__ chan_nar, uint8_t* __restrict__ any) {
-    __shared__ CodeT tile[32 * (kSlab + 1)];
     const int64_t HW = int64_t(H) * W;
-    const int64_t plane = N * HW * Cp;
-    if (HW == 1) {
-        const int groups = Cp / 4;
-        for (int64_t g = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; g < N * groups;
-             g += int64_t(gridDim.x) * blockDim.x) {
-            const int64_t n = g / groups;
-            const int c0 = int(g - n * groups) * 4;
-            uint32_t c[4];
+    const int64_t pixels = N * HW;
+    const int64_t plane = pixels * Cp;
+    const int chunks = Cp / 32;
+    for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < pixels * chunks;
+         t += int64_t(gridDim.x) * blockDim.x) {
+        const int cc = int(t / pixels);
+        const int64_t r = t - cc * pixels;  // pixel raster index (n, h, w)
+        const int64_t n = r / HW, pix = r - n * HW;
+        const int c0 = cc * 32;
+        const CodeT* src = x + (n * C + c0) * HW + pix;
+        uint32_t code[32];
 #pragma unroll
-            for (int jj = 0; jj < 4; ++jj) c[jj] = c0 + jj < C ? uint32_t(x[n * C + c0 + jj]) : 0u;
-            const uint32_t nm = digits4<D>(c, f, lut, dig + n * Cp + c0, plane);
-            if (nm)
-                for (int jj = 0; jj < 4; ++jj)
-                    if (((nm >> jj) & 1) && c0 + jj < C) {
-                        if (pos_nar) pos_nar[n] = 1;
-                        if (chw_nar) chw_nar[c0 + jj] = 1;
-                        if (chan_nar) chan_nar[c0 + jj] = 1;
-                        *any = 1;
-                    }
+        for (int j = 0; j < 32; ++j) code[j] = c0 + j < C ? uint32_t(src[j * HW]) : 0u;
+        uint32_t words[D][8];
+        uint32_t nm = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const uint32_t c4[4] = {code[4 * q], code[4 * q + 1], code[4 * q + 2], code[4 * q + 3]};
+            nm |= digits4_words<D>(c4, f, lut, words, q) << (4 * q);
         }
-        return;
-    }
-    const int RH = W >= kSlab ? 1 : (kSlab / W < H ? kSlab / W : H);
-    const int slabs = (H + RH - 1) / RH;
-    const int wchunks = (W + kSlab - 1) / kSlab;  // W > 128: slabs of one row split in w
-    const int64_t items = N * slabs * wchunks;
-    for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
-        const int64_t n = it / (int64_t(slabs) * wchunks);
-        const int rem = int(it - n * slabs * wchunks);
-        const int h0 = (rem / wchunks) * RH, w0 = (rem % wchunks) * kSlab;
-        const int rows = H - h0 < RH ? H - h0 : RH;
-        const int wl = W - w0 < kSlab ? W - w0 : kSlab;
-        const int P = rows * wl;  // pixels of this item (contiguous when wl == W)
-        const int LDT = P + 1;
-        const bool whole_rows = wl == W;
-        // first pixel of the item in the [N][H][W] raster
-        const int64_t raster0 = (n * H + h0) * int64_t(W) + w0;
-        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-        for (int c0 = 0; c0 < Cp; c0 += 32) {
-            __syncthreads();
-            // load: a warp per channel row, lanes along the (contiguous) pixels
-            for (int cl = warp; cl < 32; cl += 8) {
-                const int c = c0 + cl;
-                const CodeT* src = x + ((n * C + c) * H + h0) * int64_t(W) + w0;
-                for (int pix = lane; pix < P; pix += 32) {
-                    const int off = whole_rows ? pix : (pix / wl) * W + pix % wl;
-                    tile[cl * LDT + pix] = c < C ? src[off] : CodeT(0);
-                }
-            }
-            __syncthreads();
-            for (int i = threadIdx.x; i < P * 8; i += blockDim.x) {
-                const int pix = i >> 3, q = i & 7;
-                const int64_t r = whole_rows ? raster0 + pix
-                                             : raster0 + int64_t(pix / wl) * W + pix % wl;
-                uint32_t c[4];
+        int8_t* dst = dig + r * Cp + c0;
 #pragma unroll
-                for (int jj = 0; jj < 4; ++jj) c[jj] = uint32_t(tile[(4 * q + jj) * LDT + pix]);
-                const uint32_t nm = digits4<D>(c, f, lut, dig + r * Cp + c0 + 4 * q, plane);
-                if (nm)
-                    for (int jj = 0; jj < 4; ++jj) {
-                        const int ch = c0 + 4 * q + jj;
-                        if (((nm >> jj) & 1) && ch < C) {
-                            if (pos_nar) pos_nar[r] = 1;
-                            if (chw_nar) chw_nar[int64_t(ch) * HW + (r - n * HW)] = 1;
-                            if (chan_nar) chan_nar[ch] = 1;
-                            *any = 1;
-                        }
-                    }
-            }
+        for (int p = 0; p < D; ++p) {
+            reinterpret_cast<uint4*>(dst + p * plane)[0] =
+                make_uint4(words[p][0], words[p][1], words[p][2], words[p][3]);
+            reinterpret_cast<uint4*>(dst + p * plane)[1] =
+                make_uint4(words[p][4], words[p][5], words[p][6], words[p][7]);
+        }
+        if (nm) {
+            for (int j = 0; j < 32; ++j)
+                if (((nm >> j) & 1) && c0 + j < C) {
+                    if (pos_nar) pos_nar[r] = 1;
+                    if (chw_nar) chw_nar[int64_t(c0 + j) * HW + pix] = 1;
+                    if (chan_nar) chan_nar[c0 + j] = 1;
+                    *any = 1;
+                }
         }
     }
 }
@@ -427,7 +445,9 @@ __global__ void __launch_bounds__(256) act_digits_kernel(
 // First-layer tap folding (C*KH*KW <= 32, stride 1): the receptive field of
 // each output pixel becomes the 32 "channels" of a virtual 1x1 convolution,
 // dig[D][N][OH][OW][32] with channel k = (c, ky, kx) (zero past C*KH*KW and
-// outside the image).  NaR summaries in the virtual geometry: pos_nar[n][oy][ox]
+// outside the image).  A thread per output pixel: its gathers are coalesced
+// across the warp (consecutive pixels), its 32 digit bytes per plane go out as
+// two 16-byte stores.  NaR summaries in the virtual geometry: pos_nar[n][oy][ox]
 // (forward rows) and chw_nar[k][oy][ox] (weight-grad rows).
 template <int D, typename CodeT>
 __global__ void __launch_bounds__(256) im2col_digits_kernel(
@@ -437,31 +457,42 @@ __global__ void __launch_bounds__(256) im2col_digits_kernel(
     const int ckk = C * KH * KW, khw = KH * KW;
     const int64_t P = int64_t(OH) * OW;
     const int64_t plane = N * P * 32;
-    for (int64_t g = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; g < N * P * 8;
-         g += int64_t(gridDim.x) * blockDim.x) {
-        const int64_t pos = g >> 3;  // (n, oy, ox) raster
-        const int q = int(g & 7);
+    for (int64_t pos = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; pos < N * P;
+         pos += int64_t(gridDim.x) * blockDim.x) {
         const int64_t n = pos / P;
         const int pix = int(pos - n * P), oy = pix / OW, ox = pix - oy * OW;
-        uint32_t c4[4];
+        uint32_t words[D][8];
+        uint32_t nm = 0;
 #pragma unroll
-        for (int jj = 0; jj < 4; ++jj) {
-            const int k = 4 * q + jj;
-            uint32_t code = 0;
-            if (k < ckk) {
-                const int c = k / khw, t = k - c * khw, ky = t / KW, kx = t - ky * KW;
-                const int iy = oy + ky - pad, ix = ox + kx - pad;
-                if (unsigned(iy) < unsigned(H) && unsigned(ix) < unsigned(W))
-                    code = uint32_t(x[((n * C + c) * H + iy) * W + ix]);
+        for (int q = 0; q < 8; ++q) {
+            uint32_t c4[4];
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) {
+                const int k = 4 * q + jj;
+                uint32_t code = 0;
+                if (k < ckk) {
+                    const int c = k / khw, t = k - c * khw, ky = t / KW, kx = t - ky * KW;
+                    const int iy = oy + ky - pad, ix = ox + kx - pad;
+                    if (unsigned(iy) < unsigned(H) && unsigned(ix) < unsigned(W))
+                        code = uint32_t(x[((n * C + c) * H + iy) * W + ix]);
+                }
+                c4[jj] = code;
             }
-            c4[jj] = code;
+            nm |= digits4_words<D>(c4, f, lut, words, q) << (4 * q);
         }
-        const uint32_t nm = digits4<D>(c4, f, lut, dig + pos * 32 + 4 * q, plane);
+        int8_t* dst = dig + pos * 32;
+#pragma unroll
+        for (int p = 0; p < D; ++p) {
+            reinterpret_cast<uint4*>(dst + p * plane)[0] =
+                make_uint4(words[p][0], words[p][1], words[p][2], words[p][3]);
+            reinterpret_cast<uint4*>(dst + p * plane)[1] =
+                make_uint4(words[p][4], words[p][5], words[p][6], words[p][7]);
+        }
         if (nm)
-            for (int jj = 0; jj < 4; ++jj)
-                if (((nm >> jj) & 1) && 4 * q + jj < ckk) {
+            for (int k = 0; k < ckk; ++k)
+                if ((nm >> k) & 1) {
                     if (pos_nar) pos_nar[pos] = 1;
-                    if (chw_nar) chw_nar[int64_t(4 * q + jj) * P + pix] = 1;
+                    if (chw_nar) chw_nar[int64_t(k) * P + pix] = 1;
                     *any = 1;
                 }
     }

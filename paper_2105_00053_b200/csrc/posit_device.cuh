@@ -157,6 +157,72 @@ __device__ __forceinline__ uint32_t pack_round32(const PositFmt& f, bool neg, in
     return neg ? ((0u - pat) & mask) : pat;
 }
 
+// Branch-free pack_round32 (same result): saturation and the round-up are
+// selects, shifts are kept in range by clamping the scale, so the GEMM
+// epilogue can interleave the conversions of its 8 columns.
+__device__ __forceinline__ uint32_t pack_round32_bf(const PositFmt& f, bool neg, int scale,
+                                                    uint32_t sig32, bool sticky) {
+    const bool hi_sat = scale >= f.R, lo_sat = scale < -f.R;
+    const int sc = scale < -f.R ? -f.R : (scale > f.R - 1 ? f.R - 1 : scale);
+    const int k = sc >> f.es;
+    const int e = sc - (k << f.es);
+    const bool kpos = k >= 0;
+    const int rl = kpos ? k + 2 : 1 - k;
+    const uint32_t regime = kpos ? (((1u << (k + 1)) - 1u) << 1) : 1u;
+    const int head = rl + f.es;
+    uint32_t w = regime << (32 - rl);
+    if (f.es > 0) w |= uint32_t(e) << (32 - head);
+    const uint32_t frac = sig32 << 1;
+    w |= frac >> head;
+    const bool st = sticky || (frac << (32 - head)) != 0 || (w << f.nbits) != 0;
+    uint32_t pat = w >> (33 - f.nbits);
+    const uint32_t guard = (w >> (32 - f.nbits)) & 1u;
+    pat += guard & (uint32_t(st) | (pat & 1u));
+    pat = hi_sat ? (1u << (f.nbits - 1)) - 1u : (lo_sat ? 1u : pat);
+    const uint32_t mask = (1u << f.nbits) - 1u;
+    return neg ? ((0u - pat) & mask) : pat;
+}
+
+// Branch-free quire word -> posit (same results as quire_word_to_posit).
+__device__ __forceinline__ uint32_t quire_word_to_posit_bf(const PositFmt& f, uint32_t q) {
+    const uint32_t m = f.W >= 32 ? 0xFFFFFFFFu : ((1u << f.W) - 1u);
+    q &= m;
+    const bool neg = ((q >> (f.W - 1)) & 1u) != 0;
+    const uint32_t mag = neg ? ((0u - q) & m) : q;
+    const int lz = __clz(mag);
+    const uint32_t c = pack_round32_bf(f, neg, 31 - lz - 2 * f.R, mag << (lz & 31), false);
+    return mag == 0 ? 0u : c;
+}
+__device__ __forceinline__ uint32_t quire_word_to_posit_bf(const PositFmt& f, uint64_t q) {
+    const uint64_t m = f.W >= 64 ? ~uint64_t(0) : ((uint64_t(1) << f.W) - 1);
+    q &= m;
+    const bool neg = ((q >> (f.W - 1)) & 1) != 0;
+    const uint64_t mag = neg ? ((0 - q) & m) : q;
+    const int lz = __clzll(mag);
+    const uint64_t sig = mag << (lz & 63);
+    const uint32_t c =
+        pack_round32_bf(f, neg, 63 - lz - 2 * f.R, uint32_t(sig >> 32), uint32_t(sig) != 0);
+    return mag == 0 ? 0u : c;
+}
+__device__ __forceinline__ uint32_t quire_word_to_posit_bf(const PositFmt& f, unsigned __int128 q) {
+    uint64_t lo = uint64_t(q), hi = uint64_t(q >> 64);
+    const uint64_t hmask = f.W >= 128 ? ~uint64_t(0) : ((uint64_t(1) << (f.W - 64)) - 1);  // W > 64
+    hi &= hmask;
+    const bool neg = ((hi >> (f.W - 65)) & 1) != 0;
+    const uint64_t nlo = 0 - lo, nhi = (~hi + (lo == 0 ? 1 : 0)) & hmask;
+    lo = neg ? nlo : lo;
+    hi = neg ? nhi : hi;
+    const bool hz = hi == 0;
+    const int lzh = __clzll(hi), lzl = __clzll(lo);
+    const uint64_t sig_h = (hi << (lzh & 63)) | ((lo >> 1) >> ((63 - lzh) & 63));
+    const bool st_h = (lo << (lzh & 63)) != 0;
+    const uint64_t sig = hz ? (lo << (lzl & 63)) : sig_h;
+    const bool sticky = (!hz && st_h) || uint32_t(sig) != 0;
+    const int top = hz ? 63 - lzl : 127 - lzh;
+    const uint32_t c = pack_round32_bf(f, neg, top - 2 * f.R, uint32_t(sig >> 32), sticky);
+    return (hz && lo == 0) ? 0u : c;
+}
+
 // Quire word (W <= 32 / 64 / 128 bits held in uint32 / uint64 / u128) -> posit,
 // nbits <= 16.  Same result as quire_to_posit.
 __device__ __forceinline__ uint32_t quire_word_to_posit(const PositFmt& f, uint32_t q) {

@@ -623,11 +623,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                         if (x < valid) dst[x] = (unsigned __int128)q[c0 + x];
                     continue;
                 }
+                // column NaR flags as one 8-byte load (flag buffer padded to whole tiles)
+                const uint64_t cn =
+                    col_nar != nullptr ? *reinterpret_cast<const uint64_t*>(col_nar + col0) : 0ull;
                 uint32_t codes[8];
 #pragma unroll
                 for (int x = 0; x < 8; ++x) {
-                    const bool nar = rnar || (col_nar != nullptr && x < valid && col_nar[col0 + x]);
-                    codes[x] = nar ? (1u << (f.nbits - 1)) : quire_word_to_posit(f, q[c0 + x]);
+                    const bool nar = rnar || ((cn >> (8 * x)) & 0xFF) != 0;
+                    codes[x] = nar ? (1u << (f.nbits - 1)) : quire_word_to_posit_bf(f, q[c0 + x]);
                 }
                 if (vec_ok) {
                     store_codes8(out.base + row * out.ldc + col0, codes, valid, true);
@@ -669,8 +672,17 @@ __global__ void quire_finalize_kernel(const unsigned __int128* __restrict__ part
          idx += int64_t(gridDim.x) * blockDim.x) {
         const int64_t i = idx / N, j = idx % N;
         const bool nar = (row_nar != nullptr && row_nar[i]) || (col_nar != nullptr && col_nar[j]);
-        unsigned __int128 q = 0;
-        for (int s = 0; s < splits; ++s) q += partial[s * total + idx];
+        // four independent chains: the split partials' loads overlap
+        unsigned __int128 q = 0, q1 = 0, q2 = 0, q3 = 0;
+        int s = 0;
+        for (; s + 4 <= splits; s += 4) {
+            q += partial[s * total + idx];
+            q1 += partial[(s + 1) * total + idx];
+            q2 += partial[(s + 2) * total + idx];
+            q3 += partial[(s + 3) * total + idx];
+        }
+        for (; s < splits; ++s) q += partial[s * total + idx];
+        q += q1 + q2 + q3;
         if (raw_words != nullptr) {  // raw words/NaR mask land in the output's layout
             const int64_t o = out.index(i, j);
             raw_words[o] = q & wmask;
