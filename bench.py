@@ -47,6 +47,7 @@ def parse():
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-train", action="store_true", help="skip the CNN training images/s leg")
     return p.parse_args()
 
 
@@ -177,6 +178,90 @@ def run_cpu_reference_sample(rows: int, threads: int, cols: int = N):
         total_macs += rows * K * cols
         total_t += t
     return total_macs / total_t, total_t
+
+
+TRAIN_PER_GPU_BATCH = 1024
+
+
+def run_training(args, rank, world, dev, dist):
+    """Second half of the BASELINE metric: CIFAR-shape CNN training images/s
+    (configs 3/4: stages fwd posit(8,1), grads posit(12,1), loss/optimizer
+    posit(16,1), all with quires), weak scaling at 1024 images per GPU.  One
+    GPU replays a CUDA-graph-captured step; N > 1 runs the data-parallel step
+    (raw quire words -> 60-bit lanes -> one NCCL all-reduce -> round once).
+    Device time (CUDA events) of K steps after W warm-ups, max over ranks."""
+    import torch
+
+    from paper_2105_00053_b200 import codec, dp, nn, ops
+
+    st = nn.StagePrecisions(ops.P81, ops.P121, ops.P121, ops.P161, ops.P161)
+    B = TRAIN_PER_GPU_BATCH
+    rng = np.random.default_rng(3 + rank)  # this rank's shard of the synthetic global batch
+    x = codec.from_float64_device(rng.uniform(-1.0, 1.0, (B, 3, 32, 32)), st.forward)
+    lab = torch.from_numpy(rng.integers(0, 10, B).astype(np.int32)).to(dev)
+    model = nn.cifar_cnn(st, seed=7)
+    loss_fn = nn.CrossEntropyLoss(st)
+    opt = nn.SGD(model.params(), 1.0 / 16, st)
+    gb = B * world
+    if world == 1:
+        g = nn.GraphedTrainStep(model, loss_fn, opt, x, lab, B, warmup=1)
+        one = g.step
+    else:
+        reducer = dp.QuireAllReduce(model.params(), st.gradient)
+        one = lambda: dp.dp_train_step(model, loss_fn, opt, reducer, x, lab, gb)  # noqa: E731
+    steps = max(5, min(args.steps, 50))
+    for _ in range(max(args.warmup, 3)):
+        one()
+    torch.cuda.synchronize(dev)
+    if dist:
+        dist.barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(steps):
+        one()
+    b.record()
+    torch.cuda.synchronize(dev)
+    t = torch.tensor([a.elapsed_time(b)], dtype=torch.float64, device=dev)
+    if dist:
+        dist.barrier()
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item()) / steps
+    out = {"workload": "BASELINE config 3/4 CIFAR-shape CNN (conv 3-32-32-pool-64-64-pool, "
+                       "Linear 4096-512-10) full SGD step, fwd posit(8,1), grad posit(12,1), "
+                       "loss/optimizer posit(16,1), quires everywhere",
+           "metric": "CNN training images/s", "value": gb / (ms / 1000.0), "unit": "images/s",
+           "ms_per_step": ms, "global_batch": gb, "per_gpu_batch": B, "steps": steps,
+           "scaling": "weak", "cuda_graph": world == 1,
+           "parallelism": f"dp{world}" + (" (quire-lane NCCL all-reduce)" if world > 1 else ""),
+           "data": "synthetic uniform [-1,1) images, uniform labels (seeded per rank)"}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from oracle import bind
+
+        if bind.reference_available():
+            import importlib.util
+
+            spec = importlib.util.spec_from_file_location("bench_train", os.path.join(REPO, "tools", "bench_train.py"))
+            bt = importlib.util.module_from_spec(spec)
+            spec.loader.exec_module(bt)
+            from oracle.step import CIFAR_CNN, oracle_step
+
+            threads = os.cpu_count() or 1
+            Bc = 16
+            xc = codec.to_host(x[:Bc])
+            labc = lab[:Bc].cpu().numpy()
+            params0 = [(codec.to_host(l.w.master), codec.to_host(l.b.master))
+                       for l in nn.cifar_cnn(st, seed=7).layers if isinstance(l, nn.Conv2d)]
+            std = {k: (getattr(st, k).nbits, getattr(st, k).es)
+                   for k in ("forward", "backward", "gradient", "optimizer", "loss")}
+            t0 = time.perf_counter()
+            oracle_step(bt.HybridRef(threads), CIFAR_CNN, std, params0, xc, labc, 1.0 / 16, Bc)
+            tc = time.perf_counter() - t0
+            out["cpu_baseline"] = {"value": Bc / tc, "unit": "images/s", "cores": threads,
+                                   "kind": "reference",
+                                   "sample": f"one SGD step of the same CNN at batch {Bc}: reference "
+                                             f"tensor kernels (oracle/_ref) + restated elementwise, "
+                                             f"{tc:.1f} s"}
+    return out
 
 
 def run_reference_impl(args):
@@ -355,6 +440,10 @@ def main():
                              f"{2 * rows * K * N / 1e9:.2f} G exact MACs in {tcpu:.1f} s "
                              f"(oracle/_ref/libpnn_ref.so matmul, ThreadPool({threads}))"}
 
+    training = None
+    if not args.no_train:
+        training = run_training(args, rank, world, dev, dist)
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -381,6 +470,8 @@ def main():
             line["e2e"] = e2e
         if cpu:
             line["cpu_baseline"] = cpu
+        if training:
+            line["training"] = training
         print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
