@@ -5,7 +5,10 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <condition_variable>
+#include <cstdio>
+#include <cstdlib>
 #include <cstdint>
 #include <cstring>
 #include <functional>
@@ -351,8 +354,12 @@ int pnn_matmul_host(int nbits, int es, const uint64_t* A, const uint64_t* B, uin
         }
         return cudaSuccess;
     };
+    static const bool prof = getenv("PNN_HOST_PROFILE") != nullptr;  // phase times to stderr
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    const auto t0 = now();
     if ((e = upload(A, hA, dA, M * K))) return cuda_fail(e, "H2D A");
     if ((e = upload(B, hB, dB, K * N))) return cuda_fail(e, "H2D B");
+    const auto t1 = now();
     int rc = quire_gemm_launch(nbits, es, dA, dB, dC, M, N, K, K, N, N, ws, p.workspace_bytes, 0,
                                st, nullptr);
     if (rc) return rc == 4 ? cuda_fail(cudaGetLastError(), "matmul launch") : fail(rc, "matmul");
@@ -381,6 +388,12 @@ int pnn_matmul_host(int nbits, int es, const uint64_t* A, const uint64_t* B, uin
         }
     }
     if ((e = cudaStreamSynchronize(st))) return cuda_fail(e, "matmul_host sync");
+    if (prof) {
+        const auto t2 = now();
+        fprintf(stderr, "[pnn_matmul_host] narrow+H2D issue %.2f ms, GEMM+D2H+widen %.2f ms\n",
+                std::chrono::duration<double, std::milli>(t1 - t0).count(),
+                std::chrono::duration<double, std::milli>(t2 - t1).count());
+    }
     return PNN_OK;
 }
 
