@@ -50,7 +50,7 @@ struct ImplPlan {
     int mode, D, NT;
     IgemmArgs a;
     int64_t Ca, Wa, Ha;     // A digit tensor [D][N][Ha][Wa][Ca]
-    uint32_t boxA[4];       // {channels, w, h, n} (x D planes)
+    uint32_t boxA[5];       // slice-layout box {2 * w, h, n, slices, planes}
     int64_t Kp, brows;      // modes 0/1: B digits [D][brows][taps * Kp]
     int64_t Fpw;            // mode 2: B digits [D][N][OH][OW][Fpw]
     size_t adig, bdig;      // bytes
@@ -115,15 +115,14 @@ bool make_plan(int pass, const PositFmt& f, const ConvGeom& g_real, bool raw, Im
         a.mtiles = tpi > 0 ? g.N * tpi : cdiv(g.N, ipt);
         a.ntiles = cdiv(Cout, p->NT);
         a.kbt = taps * Cin / 32;
-        a.a_sw = 32;
-        a.b_sw = 32;
         p->Ca = Cin;
         p->Wa = Ws;
         p->Ha = Hs;
-        p->boxA[0] = 32;
-        p->boxA[1] = uint32_t(Wt);
-        p->boxA[2] = uint32_t(Hb);
-        p->boxA[3] = uint32_t(tpi > 0 ? 1 : ipt);
+        p->boxA[0] = uint32_t(2 * Wt);
+        p->boxA[1] = uint32_t(Hb);
+        p->boxA[2] = uint32_t(tpi > 0 ? 1 : ipt);
+        p->boxA[3] = 2;  // one 32-channel K step
+        p->boxA[4] = uint32_t(D);
         p->Kp = Cin;
         p->brows = Cout;
         p->adig = size_t(D) * g.N * Hs * Ws * Cin;
@@ -134,7 +133,7 @@ bool make_plan(int pass, const PositFmt& f, const ConvGeom& g_real, bool raw, Im
             col_add = size_t(Cout) * 8;
         }
     } else {
-        if (!(g.C == 32 || g.C == 64 || g.C == 128) || g.W > 256 || g.OW > 256) return false;
+        if (g.C % 32 || g.W > 256 || g.OW > 256) return false;
         int OWb, OHb;
         if (g.OW >= 32) {
             if (g.OW % 32) return false;
@@ -148,25 +147,28 @@ bool make_plan(int pass, const PositFmt& f, const ConvGeom& g_real, bool raw, Im
         a.OWb = OWb;
         a.OHb = OHb;
         a.C = int(g.C);
-        a.slots = int(128 / g.C);
         a.kpr = int(g.OW / OWb);
         a.kpi = int((g.OH / OHb) * a.kpr);
-        a.M = p->fold ? p->ckk : taps * g.C;  // folded: rows (c,ky,kx) < C*KH*KW
+        a.KH = int(g.KH);
+        a.kgroups = int((g.KW + 3) / 4);
+        a.cgroups = int(g.C / 32);
+        a.Hp = int(g.H + 2 * g.pad);
+        a.mtiles = int64_t(a.KH) * a.kgroups * a.cgroups;
+        a.M = a.mtiles * kBM;  // padding rows (kx >= KW, folded c >= C*KH*KW) not stored
         a.N = g.F;
-        a.mtiles = cdiv(taps, a.slots);
         p->Fpw = cdiv(g.F, p->NT) * p->NT;
         a.ntiles = p->Fpw / p->NT;
         a.kbt = g.N * a.kpi;
-        a.a_sw = int(g.C);
-        a.b_sw = p->NT;
         p->Ca = g.C;
-        p->Wa = g.W;
-        p->Ha = g.H;
-        p->boxA[0] = uint32_t(g.C);
-        p->boxA[1] = uint32_t(OWb);
-        p->boxA[2] = uint32_t(OHb);
-        p->boxA[3] = 1;
-        p->adig = size_t(D) * g.N * g.H * g.W * g.C;
+        p->Wa = g.W + 2 * g.pad;  // zero-padded x digits
+        p->Ha = g.H + 2 * g.pad;
+        p->boxA[0] = uint32_t(2 * OWb);
+        p->boxA[1] = uint32_t(OHb);
+        p->boxA[2] = 4;   // kx taps of one group
+        p->boxA[3] = 2;   // one 32-channel group
+        p->boxA[4] = uint32_t(D);
+        // + margin: the dummy kx taps of the last row read up to 3 pixels past it
+        p->adig = size_t(D) * g.N * p->Ha * p->Wa * g.C + 64;
         p->bdig = size_t(D) * g.N * g.OH * g.OW * p->Fpw;
         chw_nar = size_t(g.C) * g.H * g.W;
         col_nar = size_t(p->Fpw);
@@ -216,38 +218,60 @@ PFN_cuTensorMapEncodeTiled_v12000 encoder() {
     return fn;
 }
 
-CUtensorMapSwizzle swz(int bytes) {
-    return bytes == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
-                       : bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B;
-}
-
-// dig[D][N][H][W][C] (int8) as a 5-D map {C, W, H, N, D}
+// Slice layout dig[D][N][H][C/16][W][16] (int8 digits, 16 channels per 16-byte
+// cell) as a 5-D map of 8-byte elements {2W, H, N, C/16, D}: a box row is a run
+// of pixels of one 16-channel slice, contiguous in HBM.  No swizzle: the
+// canonical 8 x 16-byte core matrices of the UMMA layouts are exactly 8
+// consecutive pixels of a slice.  box = {2 * pixels, h, n, slices, planes}.
 bool map_act(CUtensorMap* m, void* base, int D, int64_t N, int64_t H, int64_t W, int64_t C,
-             const uint32_t box[4], int sw) {
+             const uint32_t box[5]) {
     auto enc = encoder();
     if (!enc) return false;
-    const cuuint64_t dims[5] = {cuuint64_t(C), cuuint64_t(W), cuuint64_t(H), cuuint64_t(N),
+    const int64_t CS = C / 16;
+    const cuuint64_t dims[5] = {cuuint64_t(2 * W), cuuint64_t(H), cuuint64_t(N), cuuint64_t(CS),
                                 cuuint64_t(D)};
-    const cuuint64_t strides[4] = {cuuint64_t(C), cuuint64_t(W * C), cuuint64_t(H * W * C),
-                                   cuuint64_t(N * H * W * C)};
-    const cuuint32_t boxd[5] = {box[0], box[1], box[2], box[3], cuuint32_t(D)};
+    const cuuint64_t strides[4] = {cuuint64_t(CS * W * 16), cuuint64_t(H * CS * W * 16),
+                                   cuuint64_t(W * 16), cuuint64_t(N * H * CS * W * 16)};
     const cuuint32_t es[5] = {1, 1, 1, 1, 1};
-    return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 5, base, dims, strides, boxd, es,
-               CU_TENSOR_MAP_INTERLEAVE_NONE, swz(sw), CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT64, 5, base, dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// dig[D][rows][K] (int8) as a 3-D map {K, rows, D}, box {32, NT, D}
+// Zero-padded x digits dig[D][N][Hp][C/16][Wp][16] for the weight gradient as
+// {2 * Wp, N * Hp, 4, C/16, D}: rows of all images stacked (the pad rows make
+// that safe), and a 4-wide kx dimension of stride one 16-byte pixel -- an
+// overlapping view, so ONE box {pixels, rows, 4 kx, 2 slices, D} holds the
+// operand of 4 taps x 32 channels x D planes.
+bool map_wgrad_x(CUtensorMap* m, void* base, int D, int64_t N, int64_t Hp, int64_t Wp, int64_t C,
+                 const uint32_t box[5]) {
+    auto enc = encoder();
+    if (!enc) return false;
+    const int64_t CS = C / 16;
+    const cuuint64_t dims[5] = {cuuint64_t(2 * Wp), cuuint64_t(N * Hp), 4, cuuint64_t(CS),
+                                cuuint64_t(D)};
+    const cuuint64_t strides[4] = {cuuint64_t(CS * Wp * 16), 16, cuuint64_t(Wp * 16),
+                                   cuuint64_t(N * Hp * CS * Wp * 16)};
+    const cuuint32_t es[5] = {1, 1, 1, 1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT64, 5, base, dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// Weight digits dig[D][K/16][rows][16] as a 3-D map {2 * rows, D, K/16} of
+// 8-byte elements; box {2 * NT, D, 2} -> smem [2 slices][D][NT][16 B], i.e. the
+// D planes concatenated along N with a uniform 128-byte 8-row stride.
 bool map_weights(CUtensorMap* m, void* base, int D, int64_t rows, int64_t K, int NT) {
     auto enc = encoder();
     if (!enc) return false;
-    const cuuint64_t dims[3] = {cuuint64_t(K), cuuint64_t(rows), cuuint64_t(D)};
-    const cuuint64_t strides[2] = {cuuint64_t(K), cuuint64_t(rows * K)};
-    const cuuint32_t boxd[3] = {32, cuuint32_t(NT), cuuint32_t(D)};
+    const int64_t KS = K / 16;
+    const cuuint64_t dims[3] = {cuuint64_t(2 * rows), cuuint64_t(D), cuuint64_t(KS)};
+    const cuuint64_t strides[2] = {cuuint64_t(KS * rows * 16), cuuint64_t(rows * 16)};
+    const cuuint32_t boxd[3] = {cuuint32_t(2 * NT), cuuint32_t(D), 2};
     const cuuint32_t es[3] = {1, 1, 1};
-    return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, base, dims, strides, boxd, es,
-               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B,
-               CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, base, dims, strides, boxd, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 template <int D, typename CodeT, int MODE>
@@ -294,14 +318,14 @@ cudaError_t dispatch(int D, const CUtensorMap& tA, const CUtensorMap& tB, const 
 
 template <typename CodeT>
 cudaError_t act_digits(int D, const CodeT* x, int64_t N, int64_t C, int64_t H, int64_t W,
-                       int64_t Cp, const PositFmt& f, uint32_t* lut, bool build_lut, int8_t* dig,
+                       int64_t Cp, int pad, const PositFmt& f, uint32_t* lut, bool build_lut, int8_t* dig,
                        uint8_t* pos_nar, uint8_t* chw_nar, uint8_t* chan_nar, uint8_t* any,
                        cudaStream_t st) {
     const int grid = grid_for(N * H * W * (Cp / 32), 256);  // thread per (pixel, 32 channels)
     if (lut == nullptr) build_lut = false;
 #define PNN_ACT(DD)                                                                              \
     if (build_lut) digit_lut_kernel<DD><<<16, 256, 0, st>>>(f, lut);                             \
-    act_digits_kernel<DD, CodeT><<<grid, 256, 0, st>>>(x, N, int(C), int(H), int(W), int(Cp), f, \
+    act_digits_kernel<DD, CodeT><<<grid, 256, 0, st>>>(x, N, int(C), int(H), int(W), int(Cp), pad, f, \
                                                        lut, dig, pos_nar, chw_nar, chan_nar, any)
     switch (D) {
         case 2: PNN_ACT(2); break;
@@ -383,7 +407,7 @@ int run_fwd(const ImplPlan& p, const ConvGeom& g, const CodeT* x, const CodeT* w
     if (p.fold)
         e = im2col_digits<CodeT>(p.D, x, g, f, lut_of(p, ws), adig, pos_nar, nullptr, flags, st);
     else
-        e = act_digits<CodeT>(p.D, x, g.N, g.C, g.H, g.W, p.Ca, f, lut_of(p, ws), true, adig,
+        e = act_digits<CodeT>(p.D, x, g.N, g.C, g.H, g.W, p.Ca, 0, f, lut_of(p, ws), true, adig,
                               pos_nar, nullptr, nullptr, flags, st);
     if (e != cudaSuccess) return 4;
     const int64_t taps = gv.KH * gv.KW;  // weights: [F][C*KH*KW] read as [F][ckk][1][1] if folded
@@ -391,7 +415,7 @@ int run_fwd(const ImplPlan& p, const ConvGeom& g, const CodeT* x, const CodeT* w
                                   col_add, col_nar, flags + 1, st)) != cudaSuccess)
         return 4;
     CUtensorMap tA, tB;
-    if (!map_act(&tA, adig, p.D, gv.N, gv.H, gv.W, p.Ca, p.boxA, 32) ||
+    if (!map_act(&tA, adig, p.D, gv.N, gv.H, gv.W, p.Ca, p.boxA) ||
         !map_weights(&tB, bdig, p.D, p.brows, taps * p.Kp, p.NT))
         return 5;
     IgemmArgs a = p.a;
@@ -419,7 +443,7 @@ int run_dgrad(const ImplPlan& p, const ConvGeom& g, const CodeT* dy, const CodeT
     uint8_t* pos_nar = ws + p.off_pos_nar;
     uint8_t* flags = ws + p.off_flags;
     if (cudaMemsetAsync(ws + p.off_maps, 0, p.maps_bytes, st) != cudaSuccess) return 4;
-    if (act_digits<CodeT>(p.D, dy, g.N, g.F, g.OH, g.OW, p.Ca, f, lut_of(p, ws), true, adig, pos_nar, nullptr, nullptr,
+    if (act_digits<CodeT>(p.D, dy, g.N, g.F, g.OH, g.OW, p.Ca, 0, f, lut_of(p, ws), true, adig, pos_nar, nullptr, nullptr,
                           flags, st) != cudaSuccess)
         return 4;
     const int64_t taps = g.KH * g.KW;
@@ -427,7 +451,7 @@ int run_dgrad(const ImplPlan& p, const ConvGeom& g, const CodeT* dy, const CodeT
                              flags + 1, st) != cudaSuccess)
         return 4;
     CUtensorMap tA, tB;
-    if (!map_act(&tA, adig, p.D, g.N, g.OH, g.OW, p.Ca, p.boxA, 32) ||
+    if (!map_act(&tA, adig, p.D, g.N, g.OH, g.OW, p.Ca, p.boxA) ||
         !map_weights(&tB, bdig, p.D, p.brows, taps * p.Kp, p.NT))
         return 5;
     IgemmArgs a = p.a;
@@ -464,28 +488,39 @@ int run_wgrad(const ImplPlan& p, const ConvGeom& g, const CodeT* dy, const CodeT
     if (p.fold)
         e = im2col_digits<CodeT>(p.D, x, g, f, lut_of(p, ws), adig, nullptr, chw_nar, flags, st);
     else
-        e = act_digits<CodeT>(p.D, x, g.N, g.C, g.H, g.W, p.Ca, f, lut_of(p, ws), true, adig,
-                              nullptr, chw_nar, nullptr, flags, st);
+        e = act_digits<CodeT>(p.D, x, g.N, g.C, g.H, g.W, p.Ca, g.pad, f, lut_of(p, ws), true,
+                              adig, nullptr, chw_nar, nullptr, flags, st);
     if (e != cudaSuccess) return 4;
-    if (act_digits<CodeT>(p.D, dy, g.N, g.F, g.OH, g.OW, p.Fpw, f, lut_of(p, ws), false, bdig, nullptr, nullptr, col_nar,
+    if (!p.fold && g.pad > 0) {  // zero the pad ring of the padded x digits
+        const int64_t cells = int64_t(p.D) * g.N * (p.Ca / 16) *
+                              (int64_t(2 * g.pad) * (g.W + 2 * g.pad) + g.H * 2 * g.pad);
+        pad_zero_kernel<<<grid_for(cells, 256), 256, 0, st>>>(reinterpret_cast<uint4*>(adig),
+                                                              int64_t(p.D) * g.N, int(g.H), int(g.W),
+                                                              int(p.Ca / 16), g.pad);
+    }
+    if (act_digits<CodeT>(p.D, dy, g.N, g.F, g.OH, g.OW, p.Fpw, 0, f, lut_of(p, ws), false, bdig, nullptr, nullptr, col_nar,
                           flags + 1, st) != cudaSuccess)
         return 4;
     CUtensorMap tA, tB;
-    const uint32_t boxB[4] = {uint32_t(p.NT), uint32_t(p.a.OWb), uint32_t(p.a.OHb), 1};
-    if (!map_act(&tA, adig, p.D, gv.N, gv.H, gv.W, p.Ca, p.boxA, p.a.a_sw) ||
-        !map_act(&tB, bdig, p.D, g.N, g.OH, g.OW, p.Fpw, boxB, p.a.b_sw))
+    const uint32_t boxB[5] = {uint32_t(2 * p.a.OWb), uint32_t(p.a.OHb), 1, uint32_t(p.NT / 16),
+                              uint32_t(p.D)};
+    if (!map_wgrad_x(&tA, adig, p.D, gv.N, p.Ha, p.Wa, p.Ca, p.boxA) ||
+        !map_act(&tB, bdig, p.D, g.N, g.OH, g.OW, p.Fpw, boxB))
         return 5;
     IgemmArgs a = p.a;
     a.col_add = nullptr;
     a.col_nar = col_nar;
     const bool use_partial = a.splits > 1 || raw_words != nullptr;
     a.partial = use_partial ? reinterpret_cast<unsigned __int128*>(ws + p.off_partial) : nullptr;
-    OutMap<CodeT> out;
+    OutMap<CodeT> out{};
     out.base = dw;
     out.ldc = p.ckk;    // dw[f][(c,ky,kx)]
-    out.inner = gv.C;   // rows m = tap * inner + channel (folded: m = (c,ky,kx), one tap)
-    out.ncols = gv.KH * gv.KW;
-    out.mode = 2;
+    out.mode = 3;       // rows: tiles (ky, kx group, 32-channel group) x (slice, kx, c16)
+    out.kh = int(gv.KH);
+    out.kw = int(gv.KW);
+    out.kgroups = p.a.kgroups;
+    out.cgroups = p.a.cgroups;
+    out.cvalid = p.fold ? p.ckk : int(g.C);
     if (dispatch<CodeT, 2>(p.D, tA, tB, a, out, st) != cudaSuccess) return 4;
     if (use_partial)
         quire_finalize_kernel<CodeT><<<grid_for(a.M * a.N, 256), 256, 0, st>>>(

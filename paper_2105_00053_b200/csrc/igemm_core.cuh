@@ -54,9 +54,9 @@ struct IgemmArgs {
     int imgs_per_tile;  // tiles_per_img == 0: a tile holds imgs_per_tile images
     int Hb;
     int KW, pad, cch;   // taps' width, padding, 32-wide chunks per tap
-    // mode 2: K blocks of OWb x OHb output pixels, m-tile = `slots` taps of C channels
-    int slots, taps, C, OWb, OHb, kpr, kpi;  // k-blocks per row-block set / per image
-    int a_sw, b_sw;     // swizzle bytes of the A / B smem tiles
+    // mode 2: K blocks of OWb x OHb output pixels; m-tile = one ky, 4 kx, 32 channels
+    int taps, C, OWb, OHb, kpr, kpi;  // k-blocks per row-block set / per image
+    int KH, kgroups, cgroups, Hp;     // kx groups of 4, 32-channel groups, padded height
     const int64_t* col_add;  // mode 0: X(bias) per column (added as X * 2^R)
     const uint8_t* col_nar;
     PositFmt f;
@@ -117,6 +117,8 @@ __global__ void __launch_bounds__(kIThreads, 1)
     if (warp == 0) {
         if (lane == 0) {
             // ===== producer: TMA tile boxes (the im2col gather) =====
+            // Slice layout: every box row is a run of pixels x 16 channel bytes,
+            // contiguous in HBM (up to 2 KB), so a stage is a few dozen requests.
             uint32_t it = 0;
             for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
                 int64_t split, mt, nt;
@@ -145,41 +147,41 @@ __global__ void __launch_bounds__(kIThreads, 1)
                     ptx::mbar_arrive_expect_tx(&full[s], Geo::STAGE_BYTES);
                     const int kb = int(kb0 + i);
                     if constexpr (MODE != 2) {
+                        // A box {w, h, n, 2 slices, D} -> [D][2][pixels][16 B]
                         const int tap = kb / a.cch, cc = kb - tap * a.cch;
                         const int ky = tap / a.KW, kx = tap - ky * a.KW;
                         if constexpr (MODE == 0)
-                            ptx::tma_load_5d(sa, &tmA, cc * 32, kx - a.pad, y0 + ky - a.pad, n0, 0,
+                            ptx::tma_load_5d(sa, &tmA, 2 * (kx - a.pad), y0 + ky - a.pad, n0, 2 * cc, 0,
                                              &full[s]);
                         else
-                            ptx::tma_load_5d(sa, &tmA, cc * 32, a.pad - kx, y0 + a.pad - ky, n0, 0,
+                            ptx::tma_load_5d(sa, &tmA, 2 * (a.pad - kx), y0 + a.pad - ky, n0, 2 * cc, 0,
                                              &full[s]);
-                        ptx::tma_load_3d(sb, &tmB, kb * 32, int(nt) * NT, 0, &full[s]);
+                        // B box {NT rows, D, 2 slices} -> [2][D][NT][16 B]
+                        ptx::tma_load_3d(sb, &tmB, 2 * int(nt) * NT, 0, 2 * kb, &full[s]);
                     } else {
                         const int n = kb / a.kpi, r = kb - n * a.kpi;
                         const int yb = (r / a.kpr) * a.OHb, xb = (r % a.kpr) * a.OWb;
-                        for (int sl = 0; sl < a.slots; ++sl) {
-                            int tap = int(mt) * a.slots + sl;
-                            if (tap >= a.taps) tap = a.taps - 1;  // rows >= M: discarded
-                            const int ky = tap / a.KW, kx = tap - ky * a.KW;
-                            ptx::tma_load_5d(sa + sl * (D * kIKB * a.C), &tmA, 0, xb + kx - a.pad,
-                                             yb + ky - a.pad, n, 0, &full[s]);
-                        }
-                        ptx::tma_load_5d(sb, &tmB, int(nt) * NT, xb, yb, n, 0, &full[s]);
+                        const int kc = a.kgroups * a.cgroups;
+                        const int ky = int(mt) / kc, kg = (int(mt) % kc) / a.cgroups,
+                                  cg = int(mt) % a.cgroups;
+                        // A: ONE box {pixels, rows, 4 kx taps, 2 slices, D} of the
+                        // zero-padded x digits; the kx dimension is an overlapping view
+                        // (stride = one 16-byte pixel) -> [D][2][4][OHb][OWb][16 B]
+                        ptx::tma_load_5d(sa, &tmA, 2 * (xb + 4 * kg), n * a.Hp + yb + ky, 0, 2 * cg, 0,
+                                         &full[s]);
+                        // B box {pixels, rows, 1, NT/16 slices, D} -> [D][NT/16][32][16 B]
+                        ptx::tma_load_5d(sb, &tmB, 2 * xb, yb, n, int(nt) * (NT / 16), 0, &full[s]);
                     }
                 }
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {
-            // ===== MMA issuer =====
+            // ===== MMA issuer (no-swizzle canonical layouts, 16-byte core rows) =====
             constexpr uint32_t idesc = ptx::idesc_i8(kBM, Geo::NMMA, MODE == 2, MODE == 2);
-            // all-zero A operand for initialising groups D-1 .. 2D-2 (layout-agnostic:
-            // the footprint of either major's no-swizzle layout stays inside the tile)
-            const uint64_t zdesc = MODE == 2
-                                       ? ptx::smem_desc_sw(ptx::smem_u32(zero_tile), 1024, 128, 0)
-                                       : ptx::smem_desc_kmajor(ptx::smem_u32(zero_tile), 128, 8 * 32);
-            const uint32_t a_lt = ptx::swizzle_layout_type(a.a_sw);
-            const uint32_t b_lt = ptx::swizzle_layout_type(a.b_sw);
+            // all-zero A operand for initialising groups D-1 .. 2D-2; footprint <= 4 KB
+            const uint64_t zdesc = MODE == 2 ? ptx::smem_desc_kmajor(ptx::smem_u32(zero_tile), 128, 512)
+                                             : ptx::smem_desc_kmajor(ptx::smem_u32(zero_tile), 128, 256);
             uint32_t it = 0, j = 0;
             for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++j) {
                 int64_t split, mt, nt;
@@ -195,22 +197,20 @@ __global__ void __launch_bounds__(kIThreads, 1)
                     ptx::tc_fence_after();
                     const uint32_t a_base = ptx::smem_u32(smem + s * Geo::STAGE_BYTES);
                     const uint32_t b_base = a_base + Geo::A_BYTES;
-                    uint64_t bdesc;
-                    if constexpr (MODE == 2)  // D planes of NT columns, one MN atom each
-                        bdesc = ptx::smem_desc_sw(b_base, kIKB * a.b_sw, 8 * a.b_sw, b_lt);
-                    else
-                        bdesc = ptx::smem_desc_sw(b_base, 16, 8 * kIKB, b_lt);
+                    // K-major: LBO = next 16 K bytes (next slice), SBO = next 8 rows (128 B).
+                    // MN-major: LBO = next 8 K rows (128 B), SBO = next 16-wide MN atom.
+                    const uint64_t bdesc = MODE == 2
+                                               ? ptx::smem_desc_kmajor(b_base, 128, kIKB * 16)
+                                               : ptx::smem_desc_kmajor(b_base, D * NT * 16, 128);
                     const bool first = i == 0;
                     if (first) ptx::mma_i8(tmem + (D - 1) * NT, zdesc, bdesc, idesc, 0);
 #pragma unroll
                     for (int p = 0; p < D; ++p) {
-                        uint64_t adesc;
-                        if constexpr (MODE == 2)  // slots of C channels, each an MN atom
-                            adesc = ptx::smem_desc_sw(a_base + p * (kIKB * a.a_sw),
-                                                      D * kIKB * a.a_sw, 8 * a.a_sw, a_lt);
-                        else
-                            adesc = ptx::smem_desc_sw(a_base + p * (kBM * kIKB), 16, 8 * kIKB, a_lt);
-                        if (!(a.debug & 2)) ptx::mma_i8(tmem + p * NT, adesc, bdesc, idesc, (first && p == 0) ? 0u : 1u);
+                        const uint32_t ap = a_base + p * (kBM * kIKB);
+                        const uint64_t adesc = MODE == 2 ? ptx::smem_desc_kmajor(ap, 128, kIKB * 16)
+                                                         : ptx::smem_desc_kmajor(ap, kBM * 16, 128);
+                        if (!(a.debug & 2))
+                            ptx::mma_i8(tmem + p * NT, adesc, bdesc, idesc, (first && p == 0) ? 0u : 1u);
                     }
                     ptx::mma_commit(&empty[s]);
                 }
@@ -259,6 +259,7 @@ __global__ void __launch_bounds__(kIThreads, 1)
             if (row >= a.M) continue;
             const int64_t colbase = nt * NT + sub * 8;  // chunk c0 / 8 at colbase + SUB * c0
             const int64_t obase = out.row_base(row), ostride = out.col_stride();
+            if (obase < 0 && a.partial == nullptr) continue;  // padding row (weight grad)
             if constexpr (MODE == 0) if (a.col_add != nullptr && split == 0) {
 #pragma unroll
                 for (int c = 0; c < COLS; ++c)
@@ -398,12 +399,13 @@ __device__ __forceinline__ uint32_t digits4_words(const uint32_t (&c)[4], const 
 // (formats up to 12 bits) or null (decode).
 template <int D, typename CodeT>
 __global__ void __launch_bounds__(256) act_digits_kernel(
-    const CodeT* __restrict__ x, int64_t N, int C, int H, int W, int Cp, PositFmt f,
+    const CodeT* __restrict__ x, int64_t N, int C, int H, int W, int Cp, int pad, PositFmt f,
     const uint32_t* __restrict__ lut, int8_t* __restrict__ dig, uint8_t* __restrict__ pos_nar,
     uint8_t* __restrict__ chw_nar, uint8_t* __restrict__ chan_nar, uint8_t* __restrict__ any) {
     const int64_t HW = int64_t(H) * W;
     const int64_t pixels = N * HW;
-    const int64_t plane = pixels * Cp;
+    const int Hp = H + 2 * pad, Wp = W + 2 * pad;  // zero-padded image (weight grad)
+    const int64_t plane = N * int64_t(Hp) * Wp * Cp;
     const int chunks = Cp / 32;
     for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < pixels * chunks;
          t += int64_t(gridDim.x) * blockDim.x) {
@@ -422,12 +424,14 @@ __global__ void __launch_bounds__(256) act_digits_kernel(
             const uint32_t c4[4] = {code[4 * q], code[4 * q + 1], code[4 * q + 2], code[4 * q + 3]};
             nm |= digits4_words<D>(c4, f, lut, words, q) << (4 * q);
         }
-        int8_t* dst = dig + r * Cp + c0;
+        // slice layout [D][N][Hp][Cp/16][Wp][16]: this chunk = slices 2cc, 2cc+1
+        const int h = int(pix / W), w = int(pix - int64_t(h) * W);
+        int8_t* dst = dig + (((n * Hp + h + pad) * (Cp / 16) + 2 * cc) * Wp + w + pad) * 16;
 #pragma unroll
         for (int p = 0; p < D; ++p) {
-            reinterpret_cast<uint4*>(dst + p * plane)[0] =
+            *reinterpret_cast<uint4*>(dst + p * plane) =
                 make_uint4(words[p][0], words[p][1], words[p][2], words[p][3]);
-            reinterpret_cast<uint4*>(dst + p * plane)[1] =
+            *reinterpret_cast<uint4*>(dst + p * plane + int64_t(Wp) * 16) =
                 make_uint4(words[p][4], words[p][5], words[p][6], words[p][7]);
         }
         if (nm) {
@@ -439,6 +443,34 @@ __global__ void __launch_bounds__(256) act_digits_kernel(
                     *any = 1;
                 }
         }
+    }
+}
+
+// Zero the pad cells of a padded slice-layout digit tensor
+// [D*N][Hp][CS][Wp] (16-byte cells): the top/bottom pad rows and the left/right
+// pad columns of every row.
+static __global__ void pad_zero_kernel(uint4* __restrict__ dig, int64_t DN, int H, int W, int CS,
+                                int pad) {
+    const int Hp = H + 2 * pad, Wp = W + 2 * pad;
+    const int64_t border = int64_t(2 * pad) * Wp + int64_t(H) * 2 * pad;
+    const int64_t total = DN * CS * border;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t b = i % border, rest = i / border;
+        const int cs = int(rest % CS);
+        const int64_t dn = rest / CS;
+        int hh, ww;
+        if (b < int64_t(2 * pad) * Wp) {
+            const int r = int(b / Wp);
+            hh = r < pad ? r : H + r;
+            ww = int(b % Wp);
+        } else {
+            const int64_t b2 = b - int64_t(2 * pad) * Wp;
+            hh = pad + int(b2 / (2 * pad));
+            const int c = int(b2 % (2 * pad));
+            ww = c < pad ? c : W + c;
+        }
+        dig[((dn * Hp + hh) * CS + cs) * Wp + ww] = make_uint4(0, 0, 0, 0);
     }
 }
 
@@ -480,12 +512,14 @@ __global__ void __launch_bounds__(256) im2col_digits_kernel(
             }
             nm |= digits4_words<D>(c4, f, lut, words, q) << (4 * q);
         }
-        int8_t* dst = dig + pos * 32;
+        // slice layout of the virtual [N][OH][2 slices][OW][16] image
+        const int64_t row = pos / OW;
+        int8_t* dst = dig + ((row * 2) * OW + ox) * 16;
 #pragma unroll
         for (int p = 0; p < D; ++p) {
-            reinterpret_cast<uint4*>(dst + p * plane)[0] =
+            *reinterpret_cast<uint4*>(dst + p * plane) =
                 make_uint4(words[p][0], words[p][1], words[p][2], words[p][3]);
-            reinterpret_cast<uint4*>(dst + p * plane)[1] =
+            *reinterpret_cast<uint4*>(dst + p * plane + int64_t(OW) * 16) =
                 make_uint4(words[p][4], words[p][5], words[p][6], words[p][7]);
         }
         if (nm)
@@ -498,7 +532,8 @@ __global__ void __launch_bounds__(256) im2col_digits_kernel(
     }
 }
 
-// w [F][C][KH][KW] -> K-major weight digits dig[D][rows][taps * Kp]:
+// w [F][C][KH][KW] -> K-major weight digits in the slice layout
+// dig[D][taps*Kp/16][rows][16] (16 K bytes of one row contiguous):
 //   transpose = 0 (forward):    rows = F, element (f, tap, c) = w[f][c][tap]
 //   transpose = 1 (input grad): rows = C, element (c, tap, f) = w[f][c][tap]
 // Forward: col_add[f] = X(bias[f]), col_nar[f] = NaR in weight row f or bias f.
@@ -515,6 +550,7 @@ __global__ void weight_digits_kernel(const CodeT* __restrict__ w, const CodeT* _
         const int k = int(i % Kp);
         const int tap = int((i / Kp) % taps);
         const int r = int(i / (int64_t(Kp) * taps));
+        const int64_t kg = int64_t(tap) * Kp + k;  // K index; slice layout [D][K/16][rows][16]
         uint32_t code = 0;
         if (k < inner) {
             const int fo = transpose ? k : r, ci = transpose ? r : k;
@@ -529,7 +565,8 @@ __global__ void weight_digits_kernel(const CodeT* __restrict__ w, const CodeT* _
         }
 #pragma unroll
         for (int p = 0; p < D; ++p)
-            dig[int64_t(p) * total + i] = int8_t(((p < 4 ? lo : hi) >> (8 * (p & 3))) & 0xFFu);
+            dig[int64_t(p) * total + ((kg >> 4) * rows + r) * 16 + (kg & 15)] =
+                int8_t(((p < 4 ? lo : hi) >> (8 * (p & 3))) & 0xFFu);
     }
     if (!transpose && col_add != nullptr) {
         for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r < F;

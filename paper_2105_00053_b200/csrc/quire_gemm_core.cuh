@@ -302,21 +302,30 @@ struct OutMap {
     int64_t inner;
     int64_t ncols;
     int mode;
-    __device__ __forceinline__ int64_t index(int64_t m, int64_t n) const {
-        if (mode == 0) return m * ldc + n;
-        const int64_t hi = m / inner, lo = m - hi * inner;
-        if (mode == 2) return n * ldc + lo * ncols + hi;
-        return (hi * ncols + n) * inner + lo;
-    }
-    // index(m, n) == row_base(m) + n * col_stride(): one division per row
+    // mode 3 (implicit weight grad): 128-row tiles (ky, kx group, 32-channel group),
+    // row within a tile = (slice j, kx k, channel c16) -> dw[n][c][ky][kx]
+    int kh, kw, kgroups, cgroups, cvalid;
     __device__ __forceinline__ int64_t row_base(int64_t m) const {
         if (mode == 0) return m * ldc;
+        if (mode == 3) {
+            const int mt = int(m >> 7), ml = int(m & 127);
+            const int kc = kgroups * cgroups;
+            const int ky = mt / kc, kx = ((mt % kc) / cgroups) * 4 + ((ml >> 4) & 3);
+            const int c = (mt % cgroups) * 32 + (ml >> 6) * 16 + (ml & 15);
+            if (ky >= kh || kx >= kw || c >= cvalid) return -1;  // padding rows
+            return int64_t(c) * (kh * kw) + ky * kw + kx;
+        }
         const int64_t hi = m / inner, lo = m - hi * inner;
         if (mode == 2) return lo * ncols + hi;
         return hi * ncols * inner + lo;
     }
+    // index(m, n) == row_base(m) + n * col_stride(); -1: no output for row m
+    __device__ __forceinline__ int64_t index(int64_t m, int64_t n) const {
+        const int64_t b = row_base(m);
+        return b < 0 ? -1 : b + n * col_stride();
+    }
     __device__ __forceinline__ int64_t col_stride() const {
-        return mode == 0 ? 1 : mode == 2 ? ldc : inner;
+        return mode == 0 ? 1 : (mode == 2 || mode == 3) ? ldc : inner;
     }
 };
 
@@ -683,13 +692,14 @@ __global__ void quire_finalize_kernel(const unsigned __int128* __restrict__ part
         }
         for (; s < splits; ++s) q += partial[s * total + idx];
         q += q1 + q2 + q3;
+        const int64_t o = out.index(i, j);
+        if (o < 0) continue;  // padding row of the implicit weight gradient
         if (raw_words != nullptr) {  // raw words/NaR mask land in the output's layout
-            const int64_t o = out.index(i, j);
             raw_words[o] = q & wmask;
             raw_nar[o] = nar ? 1 : 0;
         }
         if (out.base != nullptr)
-            out.base[out.index(i, j)] = CodeT(nar ? (1u << (f.nbits - 1)) : quire_word_to_posit(f, q));
+            out.base[o] = CodeT(nar ? (1u << (f.nbits - 1)) : quire_word_to_posit(f, q));
     }
 }
 
@@ -930,7 +940,7 @@ int run_quire_gemm(const GemmArgs& g, FA fa, FB fb, OutMap<CodeT> out, void* wor
 
 template <typename CodeT>
 inline OutMap<CodeT> out_rowmajor(void* base, int64_t ldc) {
-    OutMap<CodeT> o;
+    OutMap<CodeT> o{};
     o.base = static_cast<CodeT*>(base);
     o.ldc = ldc;
     o.inner = 1;
@@ -941,7 +951,7 @@ inline OutMap<CodeT> out_rowmajor(void* base, int64_t ldc) {
 
 template <typename CodeT>
 inline OutMap<CodeT> out_nchw(void* base, int64_t pixels, int64_t channels) {
-    OutMap<CodeT> o;
+    OutMap<CodeT> o{};
     o.base = static_cast<CodeT*>(base);
     o.ldc = 0;
     o.inner = pixels;
