@@ -23,7 +23,11 @@ int set_conv_algo(int a) {
 
 namespace {
 
-int nt_for(int D) { return D == 2 ? TileCfg<2>::NT : D <= 4 ? TileCfg<4>::NT : TileCfg<8>::NT; }
+// N tile: modes 0/1 two CTAs per SM (small_nt), mode 2 the one-CTA TileCfg tile
+int nt_for(int D, int mode) {
+    if (mode != 2 && D <= 4) return small_nt(D);
+    return D == 2 ? TileCfg<2>::NT : D <= 4 ? TileCfg<4>::NT : TileCfg<8>::NT;
+}
 
 int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
@@ -88,7 +92,7 @@ bool make_plan(int pass, const PositFmt& f, const ConvGeom& g_real, bool raw, Im
     const ConvGeom& g = p->gv;
     p->mode = pass;
     p->D = D;
-    p->NT = nt_for(D);
+    p->NT = nt_for(D, pass);
     IgemmArgs& a = p->a;
     a.f = f;
     static const int debug = getenv("PNN_IGEMM_DEBUG") ? atoi(getenv("PNN_IGEMM_DEBUG")) : 0;
@@ -175,9 +179,11 @@ bool make_plan(int pass, const PositFmt& f, const ConvGeom& g_real, bool raw, Im
     }
     // split-K: int32 group sums exact for <= 131071 / D terms (W > 32), SM fill
     const int64_t cap = f.W <= 32 ? a.kbt : (131071 / D) / kIKB;
-    const int64_t kbps = split_kblocks(a.kbt, cap < 1 ? 1 : cap, a.mtiles * a.ntiles, num_sms());
+    const int64_t kbps = split_kblocks(a.kbt, cap < 1 ? 1 : cap, a.mtiles * a.ntiles,
+                                       num_sms() * ((pass == 2 || D >= 5) ? 1 : 2));  // CTAs in flight
     a.kb_per_split = a.kbt < kbps ? a.kbt : kbps;
     a.splits = cdiv(a.kbt, a.kb_per_split);
+    if (a.mtiles * a.ntiles * a.splits >= (int64_t(1) << 31) || a.M >= (int64_t(1) << 31)) return false;
     const size_t partial = (a.splits > 1 || raw) ? size_t(a.splits) * a.M * a.N * 16 : 0;
 
     size_t off = 0;
@@ -274,30 +280,44 @@ bool map_weights(CUtensorMap* m, void* base, int D, int64_t rows, int64_t K, int
                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// Modes 0/1 with D <= 4 run two CTAs per SM with the small N tile (measured:
+// config 4 (8,0) 3.96 -> 3.52 ms, (8,1) 3.99 -> 3.79 ms per step); with D >= 5
+// the 104 KB stage budget of a half SM leaves too few stages to cover the TMA
+// latency (measured slower), so they and mode 2 (few output tiles, long K)
+// run one CTA per SM with the full-TMEM N tile.
+template <int MODE, int D>
+constexpr int cps_of() { return (MODE == 2 || D >= 5) ? 1 : 2; }
+template <int MODE, int D>
+constexpr int nt_of() { return cps_of<MODE, D>() == 2 ? small_nt(D) : TileCfg<D>::NT; }
+
 template <int D, typename CodeT, int MODE>
 cudaError_t launch_kernel(const CUtensorMap& tA, const CUtensorMap& tB, const IgemmArgs& a,
                           OutMap<CodeT> out, cudaStream_t st) {
-    using Geo = ImplGeo<D>;
+    constexpr int NTT = nt_of<MODE, D>(), CPS = cps_of<MODE, D>();
+    using Geo = ImplGeo<D, NTT, CPS>;
     void (*k)(CUtensorMap, CUtensorMap, IgemmArgs, OutMap<CodeT>);
     if constexpr (D <= 3)
-        k = a.f.W <= 32 ? igemm_kernel<D, 1, CodeT, MODE> : igemm_kernel<D, 2, CodeT, MODE>;
+        k = a.f.W <= 32 ? igemm_kernel<D, NTT, CPS, 1, CodeT, MODE>
+                        : igemm_kernel<D, NTT, CPS, 2, CodeT, MODE>;
     else
-        k = a.f.W <= 64 ? igemm_kernel<D, 2, CodeT, MODE> : igemm_kernel<D, 4, CodeT, MODE>;
+        k = a.f.W <= 64 ? igemm_kernel<D, NTT, CPS, 2, CodeT, MODE>
+                        : igemm_kernel<D, NTT, CPS, 4, CodeT, MODE>;
     // BASELINE formats: epilogue specialised on the compile-time format
     const int fid = fixed_fmt_id(a.f);
     if constexpr (D == 2 && sizeof(CodeT) == 1)
-        if (fid == 1) k = igemm_kernel<2, 1, CodeT, MODE, 1>;
+        if (fid == 1) k = igemm_kernel<2, NTT, CPS, 1, CodeT, MODE, 1>;
     if constexpr (D == 4 && sizeof(CodeT) == 1)
-        if (fid == 2) k = igemm_kernel<4, 2, CodeT, MODE, 2>;
+        if (fid == 2) k = igemm_kernel<4, NTT, CPS, 2, CodeT, MODE, 2>;
     if constexpr (D == 6 && sizeof(CodeT) == 2)
-        if (fid == 3) k = igemm_kernel<6, 4, CodeT, MODE, 3>;
+        if (fid == 3) k = igemm_kernel<6, NTT, CPS, 4, CodeT, MODE, 3>;
     if constexpr (D == 8 && sizeof(CodeT) == 2)
-        if (fid == 4) k = igemm_kernel<8, 4, CodeT, MODE, 4>;
+        if (fid == 4) k = igemm_kernel<8, NTT, CPS, 4, CodeT, MODE, 4>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Geo::SMEM);
     if (e != cudaSuccess) return e;
     const int64_t tiles = a.mtiles * a.ntiles * a.splits;
-    const int grid = int(tiles < num_sms() ? tiles : num_sms());
-    k<<<grid, kIThreads, Geo::SMEM, st>>>(tA, tB, a, out);
+    const int64_t slots = int64_t(CPS) * num_sms();
+    const int grid = int(tiles < slots ? tiles : slots);
+    k<<<grid, Geo::THREADS, Geo::SMEM, st>>>(tA, tB, a, out);
     return cudaGetLastError();
 }
 

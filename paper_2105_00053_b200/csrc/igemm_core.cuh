@@ -32,19 +32,34 @@ namespace pnn_b200 {
 constexpr int kIKB = 32;         // K bytes (channels or pixels) per pipeline stage
 constexpr int kActLutBits = 12;  // digitiser LUT up to 4096 codes (32 KB, L1-resident)
 
-template <int D>
+// Tile geometry.  CPS = CTAs per SM.  CPS 2 (the forward / input-grad passes):
+// each CTA owns 256 TMEM columns and ~100 KB of stages, so two tiles are in
+// flight per SM -- one CTA's TMEM drain and rounding overlap the other's MMAs
+// (a single CTA cannot double-buffer G*NT > 256 columns).  CPS 1 (weight grad,
+// whose few output tiles run long split-K loops): 512 columns, ~200 KB.
+template <int D, int NT_, int CPS>
 struct ImplGeo {
-    static constexpr int NT = TileCfg<D>::NT;
+    static constexpr int NT = NT_;
     static constexpr int G = 2 * D - 1;
     static constexpr int NMMA = D * NT;
     static constexpr int A_BYTES = D * kBM * kIKB;
     static constexpr int B_BYTES = D * NT * kIKB;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-    static constexpr int STAGES_FIT = (200 * 1024) / STAGE_BYTES;
+    static constexpr int BUDGET = CPS == 2 ? 104 * 1024 : 200 * 1024;
+    static constexpr int STAGES_FIT = BUDGET / STAGE_BYTES;
     static constexpr int STAGES = STAGES_FIT > 12 ? 12 : STAGES_FIT;
     static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + kZeroBytes + 256;
-    static_assert(A_BYTES % 1024 == 0 && B_BYTES % 1024 == 0, "stage alignment");
+    static constexpr uint32_t TMEM_COLS = CPS == 2 ? 256 : 512;
+    static constexpr int EPI = CPS == 2 ? 8 : 16;  // epilogue warps
+    static constexpr int THREADS = 64 + 32 * EPI;
+    static_assert(G * NT <= int(TMEM_COLS), "TMEM overflow");
+    static_assert(NMMA % 16 == 0 && NMMA <= 256, "bad UMMA N");
+    static_assert(STAGES >= 2, "pipeline depth");
+    static_assert(A_BYTES % 1024 == 0 && B_BYTES % 512 == 0, "stage alignment");
 };
+
+// N tile of the two-CTAs-per-SM passes: G * NT <= 256 TMEM columns
+__host__ __device__ constexpr int small_nt(int D) { return D == 2 ? 64 : D <= 4 ? 32 : 16; }
 
 struct IgemmArgs {
     int64_t M, N;
@@ -64,17 +79,15 @@ struct IgemmArgs {
     int debug;  // profiling only (PNN_IGEMM_DEBUG): 1 skip conversion, 2 skip MMA, 4 skip TMA waits
 };
 
-// 16 epilogue warps (4 per TMEM lane quarter): the epilogue (TMEM drain, quire
-// accumulation, quire -> posit) is the per-tile critical path for the narrow
-// convolution tiles, and it is latency-bound -- more warps, more overlap.
-constexpr int kIEpiWarps = 16;
-constexpr int kIThreads = 64 + 32 * kIEpiWarps;
-
-template <int D, int QW, typename CodeT, int MODE, int FMT = 0>
-__global__ void __launch_bounds__(kIThreads, 1)
+// Epilogue warps: 8 (two CTAs per SM) or 16 (one): the epilogue (TMEM drain,
+// quire accumulation, quire -> posit) is latency-bound, so it gets the warps.
+template <int D, int NT_, int CPS, int QW, typename CodeT, int MODE, int FMT = 0>
+__global__ void __launch_bounds__(ImplGeo<D, NT_, CPS>::THREADS, CPS)
     igemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  const IgemmArgs a, const OutMap<CodeT> out) {
-    using Geo = ImplGeo<D>;
+    using Geo = ImplGeo<D, NT_, CPS>;
+    constexpr int kIEpiWarps = Geo::EPI;
+    constexpr int kIThreads = Geo::THREADS;
     using QT = typename QuireWord<QW>::T;
     constexpr int NT = Geo::NT, STAGES = Geo::STAGES, G = Geo::G;
     constexpr int SUB = kIEpiWarps / 4;  // warps per lane quarter
@@ -107,7 +120,7 @@ __global__ void __launch_bounds__(kIThreads, 1)
         ptx::mbar_init(tmem_empty, kIEpiWarps);
         ptx::fence_barrier_init();
     }
-    if (warp == 1) ptx::tmem_alloc<512>(tmem_slot);
+    if (warp == 1) ptx::tmem_alloc<Geo::TMEM_COLS>(tmem_slot);
     ptx::fence_proxy_async_smem();
     ptx::tc_fence_before();
     __syncthreads();
@@ -128,8 +141,8 @@ __global__ void __launch_bounds__(kIThreads, 1)
                 int n0 = 0, y0 = 0;
                 if (MODE != 2) {
                     if (a.tiles_per_img > 0) {
-                        n0 = int(mt / a.tiles_per_img);
-                        y0 = int(mt % a.tiles_per_img) * a.Hb;
+                        n0 = int(mt) / a.tiles_per_img;
+                        y0 = (int(mt) % a.tiles_per_img) * a.Hb;
                     } else {
                         n0 = int(mt) * a.imgs_per_tile;
                     }
@@ -240,7 +253,7 @@ __global__ void __launch_bounds__(kIThreads, 1)
                     uint32_t r[GB][8];
 #pragma unroll
                     for (int g = 0; g < GB; ++g)
-                        if (g0 + g < G) ptx::tmem_ld8(trow + (g0 + g) * NT + SUB * c0, r[g]);
+                        if (g0 + g < G) { if (a.debug & 8) { for (int x = 0; x < 8; ++x) r[g][x] = 0; } else ptx::tmem_ld8(trow + (g0 + g) * NT + SUB * c0, r[g]); }
                     ptx::tmem_wait_ld();
 #pragma unroll
                     for (int g = 0; g < GB; ++g)
@@ -254,6 +267,7 @@ __global__ void __launch_bounds__(kIThreads, 1)
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(tmem_empty);
+            if (a.debug & 16) continue;  // profiling: no output
 
             const int64_t row = mt * kBM + quarter * 32 + lane;
             if (row >= a.M) continue;
@@ -304,7 +318,7 @@ __global__ void __launch_bounds__(kIThreads, 1)
     __syncthreads();
     if (warp == 1) {
         ptx::tc_fence_after();
-        ptx::tmem_dealloc<512>(tmem);
+        ptx::tmem_dealloc<Geo::TMEM_COLS>(tmem);
     }
 }
 

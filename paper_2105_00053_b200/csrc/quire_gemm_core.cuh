@@ -315,7 +315,15 @@ struct OutMap {
             if (ky >= kh || kx >= kw || c >= cvalid) return -1;  // padding rows
             return int64_t(c) * (kh * kw) + ky * kw + kx;
         }
-        const int64_t hi = m / inner, lo = m - hi * inner;
+        int64_t hi, lo;
+        if (m < (int64_t(1) << 31) && inner < (int64_t(1) << 31)) {  // 32-bit division
+            const uint32_t h32 = uint32_t(m) / uint32_t(inner);
+            hi = h32;
+            lo = m - int64_t(h32) * inner;
+        } else {
+            hi = m / inner;
+            lo = m - hi * inner;
+        }
         if (mode == 2) return lo * ncols + hi;
         return hi * ncols * inner + lo;
     }
@@ -409,14 +417,19 @@ struct QAcc<unsigned __int128> {  // W <= 128
 // A and B digit planes in L2.
 constexpr int kGroupM = 8;
 
-__device__ __forceinline__ void tile_coords(int64_t t, int64_t mtiles, int64_t ntiles,
+// 32-bit arithmetic (the planners keep tile counts below 2^31): 64-bit integer
+// division is a ~100-instruction call, and every role of every tile runs this.
+__device__ __forceinline__ void tile_coords(int64_t t64, int64_t mtiles64, int64_t ntiles64,
                                             int64_t& split, int64_t& mt, int64_t& nt) {
-    const int64_t per_split = mtiles * ntiles;
-    split = t / per_split;
-    const int64_t r = t - split * per_split;
-    const int64_t group = r / (kGroupM * ntiles);
-    const int64_t within = r - group * (kGroupM * ntiles);
-    const int64_t gm = min(int64_t(kGroupM), mtiles - group * kGroupM);
+    const uint32_t t = uint32_t(t64), mtiles = uint32_t(mtiles64), ntiles = uint32_t(ntiles64);
+    const uint32_t per_split = mtiles * ntiles;
+    const uint32_t sp = t / per_split;
+    const uint32_t r = t - sp * per_split;
+    const uint32_t group = r / (kGroupM * ntiles);
+    const uint32_t within = r - group * (kGroupM * ntiles);
+    const uint32_t left = mtiles - group * kGroupM;
+    const uint32_t gm = left < uint32_t(kGroupM) ? left : uint32_t(kGroupM);
+    split = sp;
     mt = group * kGroupM + within % gm;
     nt = within / gm;
 }
@@ -820,6 +833,8 @@ inline int plan_quire_gemm(const PositFmt& f, int64_t M, int64_t N, int64_t K,
         case 8: *plan = plan_for<8>(f, M, N, K, max_kb_per_split, raw); break;
         default: return 2;
     }
+    // the kernels index tiles in 32 bits
+    if (plan->mtiles_alloc * plan->ntiles * plan->splits >= (int64_t(1) << 31)) return 2;
     return 0;
 }
 
