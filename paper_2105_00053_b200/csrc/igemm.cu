@@ -280,38 +280,43 @@ bool map_weights(CUtensorMap* m, void* base, int D, int64_t rows, int64_t K, int
                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// Modes 0/1 with D <= 4 run two CTAs per SM with the small N tile (measured:
-// config 4 (8,0) 3.96 -> 3.52 ms, (8,1) 3.99 -> 3.79 ms per step); with D >= 5
-// the 104 KB stage budget of a half SM leaves too few stages to cover the TMA
-// latency (measured slower), so they and mode 2 (few output tiles, long K)
-// run one CTA per SM with the full-TMEM N tile.
+// Tile shape per pass (measured on B200, profiles/README.md):
+//  * modes 0/1, D <= 4: two CTAs per SM, 256 TMEM columns each, small N tile --
+//    one CTA's drain/rounding overlaps the other's MMAs;
+//  * modes 0/1, D >= 5 and mode 2: one CTA per SM, full-TMEM N tile, one
+//    accumulator buffer.  (Two CTAs per SM leave too few stages for D >= 5;
+//    two accumulator buffers in one CTA need the small N tile, which doubles
+//    the tiles and the per-tile TMEM drain -- TMEM reads run at 64 B/cycle/SM
+//    -- and measured 25% slower.)
 template <int MODE, int D>
 constexpr int cps_of() { return (MODE == 2 || D >= 5) ? 1 : 2; }
+template <int MODE, int D>
+constexpr int acc_of() { return 1; }
 template <int MODE, int D>
 constexpr int nt_of() { return cps_of<MODE, D>() == 2 ? small_nt(D) : TileCfg<D>::NT; }
 
 template <int D, typename CodeT, int MODE>
 cudaError_t launch_kernel(const CUtensorMap& tA, const CUtensorMap& tB, const IgemmArgs& a,
                           OutMap<CodeT> out, cudaStream_t st) {
-    constexpr int NTT = nt_of<MODE, D>(), CPS = cps_of<MODE, D>();
-    using Geo = ImplGeo<D, NTT, CPS>;
+    constexpr int NTT = nt_of<MODE, D>(), CPS = cps_of<MODE, D>(), ACC = acc_of<MODE, D>();
+    using Geo = ImplGeo<D, NTT, CPS, ACC>;
     void (*k)(CUtensorMap, CUtensorMap, IgemmArgs, OutMap<CodeT>);
     if constexpr (D <= 3)
-        k = a.f.W <= 32 ? igemm_kernel<D, NTT, CPS, 1, CodeT, MODE>
-                        : igemm_kernel<D, NTT, CPS, 2, CodeT, MODE>;
+        k = a.f.W <= 32 ? igemm_kernel<D, NTT, CPS, ACC, 1, CodeT, MODE>
+                        : igemm_kernel<D, NTT, CPS, ACC, 2, CodeT, MODE>;
     else
-        k = a.f.W <= 64 ? igemm_kernel<D, NTT, CPS, 2, CodeT, MODE>
-                        : igemm_kernel<D, NTT, CPS, 4, CodeT, MODE>;
+        k = a.f.W <= 64 ? igemm_kernel<D, NTT, CPS, ACC, 2, CodeT, MODE>
+                        : igemm_kernel<D, NTT, CPS, ACC, 4, CodeT, MODE>;
     // BASELINE formats: epilogue specialised on the compile-time format
     const int fid = fixed_fmt_id(a.f);
     if constexpr (D == 2 && sizeof(CodeT) == 1)
-        if (fid == 1) k = igemm_kernel<2, NTT, CPS, 1, CodeT, MODE, 1>;
+        if (fid == 1) k = igemm_kernel<2, NTT, CPS, ACC, 1, CodeT, MODE, 1>;
     if constexpr (D == 4 && sizeof(CodeT) == 1)
-        if (fid == 2) k = igemm_kernel<4, NTT, CPS, 2, CodeT, MODE, 2>;
+        if (fid == 2) k = igemm_kernel<4, NTT, CPS, ACC, 2, CodeT, MODE, 2>;
     if constexpr (D == 6 && sizeof(CodeT) == 2)
-        if (fid == 3) k = igemm_kernel<6, NTT, CPS, 4, CodeT, MODE, 3>;
+        if (fid == 3) k = igemm_kernel<6, NTT, CPS, ACC, 4, CodeT, MODE, 3>;
     if constexpr (D == 8 && sizeof(CodeT) == 2)
-        if (fid == 4) k = igemm_kernel<8, NTT, CPS, 4, CodeT, MODE, 4>;
+        if (fid == 4) k = igemm_kernel<8, NTT, CPS, ACC, 4, CodeT, MODE, 4>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Geo::SMEM);
     if (e != cudaSuccess) return e;
     const int64_t tiles = a.mtiles * a.ntiles * a.splits;

@@ -37,7 +37,7 @@ constexpr int kActLutBits = 12;  // digitiser LUT up to 4096 codes (32 KB, L1-re
 // flight per SM -- one CTA's TMEM drain and rounding overlap the other's MMAs
 // (a single CTA cannot double-buffer G*NT > 256 columns).  CPS 1 (weight grad,
 // whose few output tiles run long split-K loops): 512 columns, ~200 KB.
-template <int D, int NT_, int CPS>
+template <int D, int NT_, int CPS, int ACC = 1>
 struct ImplGeo {
     static constexpr int NT = NT_;
     static constexpr int G = 2 * D - 1;
@@ -50,9 +50,13 @@ struct ImplGeo {
     static constexpr int STAGES = STAGES_FIT > 12 ? 12 : STAGES_FIT;
     static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + kZeroBytes + 256;
     static constexpr uint32_t TMEM_COLS = CPS == 2 ? 256 : 512;
-    static constexpr int EPI = CPS == 2 ? 8 : 16;  // epilogue warps
+    // ACC = 2: two accumulator buffers (at columns 0 and 256): tile t+1's MMAs
+    // run while the epilogue drains and rounds tile t.
+    static constexpr int ACC_STRIDE = 256;
+    static constexpr int EPI = (CPS == 2 || ACC == 2) ? 8 : 16;  // epilogue warps
     static constexpr int THREADS = 64 + 32 * EPI;
-    static_assert(G * NT <= int(TMEM_COLS), "TMEM overflow");
+    static_assert(G * NT <= (ACC == 2 ? ACC_STRIDE : int(TMEM_COLS)), "TMEM overflow");
+    static_assert(ACC == 1 || CPS == 1, "double buffering needs the whole TMEM");
     static_assert(NMMA % 16 == 0 && NMMA <= 256, "bad UMMA N");
     static_assert(STAGES >= 2, "pipeline depth");
     static_assert(A_BYTES % 1024 == 0 && B_BYTES % 512 == 0, "stage alignment");
@@ -81,11 +85,11 @@ struct IgemmArgs {
 
 // Epilogue warps: 8 (two CTAs per SM) or 16 (one): the epilogue (TMEM drain,
 // quire accumulation, quire -> posit) is latency-bound, so it gets the warps.
-template <int D, int NT_, int CPS, int QW, typename CodeT, int MODE, int FMT = 0>
-__global__ void __launch_bounds__(ImplGeo<D, NT_, CPS>::THREADS, CPS)
+template <int D, int NT_, int CPS, int ACC, int QW, typename CodeT, int MODE, int FMT = 0>
+__global__ void __launch_bounds__(ImplGeo<D, NT_, CPS, ACC>::THREADS, CPS)
     igemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  const IgemmArgs a, const OutMap<CodeT> out) {
-    using Geo = ImplGeo<D, NT_, CPS>;
+    using Geo = ImplGeo<D, NT_, CPS, ACC>;
     constexpr int kIEpiWarps = Geo::EPI;
     constexpr int kIThreads = Geo::THREADS;
     using QT = typename QuireWord<QW>::T;
@@ -99,9 +103,9 @@ __global__ void __launch_bounds__(ImplGeo<D, NT_, CPS>::THREADS, CPS)
     uint8_t* zero_tile = smem + STAGES * Geo::STAGE_BYTES;
     uint64_t* full = reinterpret_cast<uint64_t*>(zero_tile + kZeroBytes);
     uint64_t* empty = full + STAGES;
-    uint64_t* tmem_full = empty + STAGES;
-    uint64_t* tmem_empty = tmem_full + 1;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 1);
+    uint64_t* tmem_full = empty + STAGES;      // [ACC]
+    uint64_t* tmem_empty = tmem_full + ACC;    // [ACC]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + ACC);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -116,8 +120,10 @@ __global__ void __launch_bounds__(ImplGeo<D, NT_, CPS>::THREADS, CPS)
             ptx::mbar_init(&full[s], 1);
             ptx::mbar_init(&empty[s], 1);
         }
-        ptx::mbar_init(tmem_full, 1);
-        ptx::mbar_init(tmem_empty, kIEpiWarps);
+        for (int b = 0; b < ACC; ++b) {
+            ptx::mbar_init(&tmem_full[b], 1);
+            ptx::mbar_init(&tmem_empty[b], kIEpiWarps);
+        }
         ptx::fence_barrier_init();
     }
     if (warp == 1) ptx::tmem_alloc<Geo::TMEM_COLS>(tmem_slot);
@@ -201,8 +207,11 @@ __global__ void __launch_bounds__(ImplGeo<D, NT_, CPS>::THREADS, CPS)
                 tile_coords(t, a.mtiles, a.ntiles, split, mt, nt);
                 const int64_t kb0 = split * a.kb_per_split;
                 const int nkb = int(min(a.kbt, kb0 + a.kb_per_split) - kb0);
-                ptx::mbar_wait(tmem_empty, (j & 1) ^ 1);
+                const int buf = ACC == 2 ? int(j & 1) : 0;
+                const uint32_t jb = ACC == 2 ? (j >> 1) : j;  // uses of this buffer so far
+                ptx::mbar_wait(&tmem_empty[buf], (jb & 1) ^ 1);
                 ptx::tc_fence_after();
+                const uint32_t tacc = tmem + buf * Geo::ACC_STRIDE;
                 for (int i = 0; i < nkb; ++i, ++it) {
                     const int s = it % STAGES;
                     const uint32_t ph = (it / STAGES) & 1;
@@ -216,18 +225,18 @@ __global__ void __launch_bounds__(ImplGeo<D, NT_, CPS>::THREADS, CPS)
                                                ? ptx::smem_desc_kmajor(b_base, 128, kIKB * 16)
                                                : ptx::smem_desc_kmajor(b_base, D * NT * 16, 128);
                     const bool first = i == 0;
-                    if (first) ptx::mma_i8(tmem + (D - 1) * NT, zdesc, bdesc, idesc, 0);
+                    if (first) ptx::mma_i8(tacc + (D - 1) * NT, zdesc, bdesc, idesc, 0);
 #pragma unroll
                     for (int p = 0; p < D; ++p) {
                         const uint32_t ap = a_base + p * (kBM * kIKB);
                         const uint64_t adesc = MODE == 2 ? ptx::smem_desc_kmajor(ap, 128, kIKB * 16)
                                                          : ptx::smem_desc_kmajor(ap, kBM * 16, 128);
                         if (!(a.debug & 2))
-                            ptx::mma_i8(tmem + p * NT, adesc, bdesc, idesc, (first && p == 0) ? 0u : 1u);
+                            ptx::mma_i8(tacc + p * NT, adesc, bdesc, idesc, (first && p == 0) ? 0u : 1u);
                     }
                     ptx::mma_commit(&empty[s]);
                 }
-                ptx::mma_commit(tmem_full);
+                ptx::mma_commit(&tmem_full[buf]);
             }
         }
     } else {
@@ -242,8 +251,10 @@ __global__ void __launch_bounds__(ImplGeo<D, NT_, CPS>::THREADS, CPS)
         for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++j) {
             int64_t split, mt, nt;
             tile_coords(t, a.mtiles, a.ntiles, split, mt, nt);
-            ptx::mbar_wait(tmem_full, j & 1);
+            const int buf = ACC == 2 ? int(j & 1) : 0;
+            ptx::mbar_wait(&tmem_full[buf], ((ACC == 2 ? (j >> 1) : j)) & 1);
             ptx::tc_fence_after();
+            const uint32_t trow_b = trow + buf * Geo::ACC_STRIDE;
             QT q[COLS];
 #pragma unroll
             for (int c0 = 0; c0 < COLS; c0 += 8) {
@@ -253,7 +264,7 @@ __global__ void __launch_bounds__(ImplGeo<D, NT_, CPS>::THREADS, CPS)
                     uint32_t r[GB][8];
 #pragma unroll
                     for (int g = 0; g < GB; ++g)
-                        if (g0 + g < G) { if (a.debug & 8) { for (int x = 0; x < 8; ++x) r[g][x] = 0; } else ptx::tmem_ld8(trow + (g0 + g) * NT + SUB * c0, r[g]); }
+                        if (g0 + g < G) { if (a.debug & 8) { for (int x = 0; x < 8; ++x) r[g][x] = 0; } else ptx::tmem_ld8(trow_b + (g0 + g) * NT + SUB * c0, r[g]); }
                     ptx::tmem_wait_ld();
 #pragma unroll
                     for (int g = 0; g < GB; ++g)
@@ -266,7 +277,7 @@ __global__ void __launch_bounds__(ImplGeo<D, NT_, CPS>::THREADS, CPS)
             }
             ptx::tc_fence_before();
             __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(tmem_empty);
+            if (lane == 0) ptx::mbar_arrive(&tmem_empty[buf]);
             if (a.debug & 16) continue;  // profiling: no output
 
             const int64_t row = mt * kBM + quarter * 32 + lane;
