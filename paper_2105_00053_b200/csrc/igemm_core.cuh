@@ -335,20 +335,6 @@ __global__ void __launch_bounds__(ImplGeo<D, NT_, CPS, ACC>::THREADS, CPS)
 
 // ------------------------------------------------------------- digitising
 
-// Digit words of every code of a format (formats up to kActLutBits bits),
-// built once per call into the workspace and read through L1 by the digitiser.
-template <int D>
-__global__ void digit_lut_kernel(PositFmt f, uint32_t* __restrict__ lut) {
-    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < (1 << f.nbits);
-         c += gridDim.x * blockDim.x) {
-        uint32_t lo, hi;
-        bool nar;
-        digit_words<D>(uint32_t(c), f, lo, hi, nar);
-        lut[2 * c] = lo;
-        lut[2 * c + 1] = hi;
-    }
-}
-
 // Digits of 4 consecutive channels (codes c[0..3]) written as one 4-byte word
 // per plane at dst + p * plane; returns a mask of NaR codes.
 template <int D>

@@ -12,7 +12,7 @@ struct QuireGemmPlan {
     int D, NT, KB;
     int64_t mtiles, ntiles, kbt, kb_per_split, splits;
     size_t a_img_bytes, b_img_bytes, row_nar_bytes, col_nar_bytes, partial_bytes;
-    size_t off_a, off_b, off_row_nar, off_col_nar, off_flags, off_partial, workspace_bytes;
+    size_t off_a, off_b, off_row_nar, off_col_nar, off_flags, off_glut, off_partial, workspace_bytes;
     int smem_bytes;
     int pair;               // 1: CTA-pair (cta_group::2) kernel
     int64_t mtiles_alloc;   // A image m-tiles (even in pair mode)

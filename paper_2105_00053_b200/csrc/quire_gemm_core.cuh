@@ -97,6 +97,22 @@ __device__ __forceinline__ void digit_words(uint32_t code, const PositFmt& f, ui
 
 constexpr int kLutMaxBits = 10;  // shared-memory decode LUT up to 1024 codes (8 KB)
 
+// Digit words of every code of a format (wider formats: a global table),
+// built once per call into the workspace and read through L1 by the digitiser.
+template <int D>
+__global__ void digit_lut_kernel(PositFmt f, uint32_t* __restrict__ lut) {
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < (1 << f.nbits);
+         c += gridDim.x * blockDim.x) {
+        uint32_t lo, hi;
+        bool nar;
+        digit_words<D>(uint32_t(c), f, lo, hi, nar);
+        lut[2 * c] = lo;
+        lut[2 * c + 1] = hi;
+    }
+}
+
+
+
 // Operand fetch functors: X[r][k] for r < rows, k < K (bounds checked by the
 // caller).  kRowFastest picks the coalesced load order of the pack kernel.
 template <typename CodeT>
@@ -133,7 +149,7 @@ __global__ void __launch_bounds__(256) pack_kernel(Fetch fetch, int64_t rows_tot
                                                    int8_t* __restrict__ img,
                                                    uint8_t* __restrict__ nar_flags,
                                                    uint8_t* __restrict__ any_nar_flag, int64_t tiles,
-                                                   int64_t kbt) {
+                                                   int64_t kbt, const uint2* __restrict__ glut) {
     constexpr int KB = Geometry<D>::KB;
     constexpr int KC = KB / 16;
     // k-blocks per pass, so that every thread owns at least one 16-code unit
@@ -258,6 +274,11 @@ __global__ void __launch_bounds__(256) pack_kernel(Fetch fetch, int64_t rows_tot
                 if (use_lut) {
                     lo[j] = lut[2 * code];
                     hi[j] = D > 4 ? lut[2 * code + 1] : 0u;
+                    any_nar |= code == nar_code;
+                } else if (glut != nullptr) {  // 11-16-bit formats: L2-resident table
+                    const uint2 v = __ldg(glut + code);
+                    lo[j] = v.x;
+                    hi[j] = v.y;
                     any_nar |= code == nar_code;
                 } else {
                     bool nar;
@@ -815,6 +836,7 @@ inline QuireGemmPlan plan_for(const PositFmt& f, int64_t M, int64_t N, int64_t K
     p.off_row_nar = take(p.row_nar_bytes);
     p.off_col_nar = take(p.col_nar_bytes);
     p.off_flags = take(16);
+    p.off_glut = take(0);
     p.off_partial = take(p.partial_bytes);
     p.workspace_bytes = off;
     return p;
@@ -855,10 +877,14 @@ cudaError_t launch_generic(const QuireGemmPlan& p, const GemmArgs& g, FA fa, FB 
     if ((e = cudaMemsetAsync(rnar, 0, p.off_flags + 16 - p.off_row_nar, st)) != cudaSuccess) return e;
     if (stats) cudaEventRecord(stats->ev[0], st);
     const int64_t a_work = p.mtiles_alloc * p.kbt, b_work = p.ntiles * p.kbt;  // upper bounds
+    // Formats wider than the shared-memory LUT decode arithmetically: a global
+    // 2^16-entry digit table (glut) measured slower for posit(16,1) (L2-latency
+    // bound lookups: 176 vs 133 us for the 4096^2 pair of packs).
+    const uint2* glut = nullptr;
     pack_kernel<D, kBM, CodeT, FA><<<int(a_work < 148 * 8 ? a_work : 148 * 8), 256, 0, st>>>(
-        fa, g.M, g.K, f, a_img, rnar, flags, p.mtiles_alloc, p.kbt);
+        fa, g.M, g.K, f, a_img, rnar, flags, p.mtiles_alloc, p.kbt, glut);
     pack_kernel<D, Geo::NT, CodeT, FB><<<int(b_work < 148 * 8 ? b_work : 148 * 8), 256, 0, st>>>(
-        fb, g.N, g.K, f, b_img, cnar, flags + 1, p.ntiles, p.kbt);
+        fb, g.N, g.K, f, b_img, cnar, flags + 1, p.ntiles, p.kbt, glut);
     if (stats) cudaEventRecord(stats->ev[1], st);
     // D <= 3 implies R <= 11, hence W <= 64: no 128-bit instantiation needed.
     using KernFn = void (*)(const int8_t*, const int8_t*, int64_t, int64_t, const uint8_t*,
