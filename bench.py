@@ -427,8 +427,8 @@ def main():
                "h2d_bytes_per_step": sum(2 * M * K * 8 for _ in FORMATS),
                "d2h_bytes_per_step": sum(M * N * 8 for _ in FORMATS),
                "path": "pnn_matmul_host: uint64 code arrays (reference Tensor storage, pinned) -> "
-                       "host-thread narrow to packed codes, chunked H2D overlapped -> quire GEMM -> "
-                       "chunked D2H overlapped with host-thread widen; wall clock (bound by host "
+                       "host-thread AVX-512 narrow to packed codes, chunked H2D overlapped -> quire GEMM -> "
+                       "chunked D2H overlapped with host-thread widen (streaming stores); wall clock (bound by host "
                        "memory traffic of the 8-byte-per-code storage)"}
 
     cpu = None

@@ -41,6 +41,9 @@ int set_status(int code, const std::string& msg) {
     g_err = msg;
     return code;
 }
+// host_copy.cpp (AVX-512 when the CPU has it)
+void host_narrow_codes(const uint64_t* src, void* dst, int64_t n, int code_bytes, uint64_t mask);
+void host_widen_codes(const void* src, uint64_t* dst, int64_t n, int code_bytes);
 }  // namespace pnn_b200
 
 namespace {
@@ -342,11 +345,7 @@ int pnn_matmul_host(int nbits, int es, const uint64_t* A, const uint64_t* B, uin
         for (int64_t c0 = 0; c0 < n; c0 += kHostChunk) {
             const int64_t c1 = std::min(n, c0 + kHostChunk);
             pool.parallel_for(c1 - c0, [&](int64_t lo, int64_t hi) {
-                if (cb == 1)
-                    for (int64_t i = c0 + lo; i < c0 + hi; ++i) hdst[i] = uint8_t(src[i] & mask);
-                else
-                    for (int64_t i = c0 + lo; i < c0 + hi; ++i)
-                        reinterpret_cast<uint16_t*>(hdst)[i] = uint16_t(src[i] & mask);
+                host_narrow_codes(src + c0 + lo, hdst + (c0 + lo) * cb, hi - lo, cb, mask);
             });
             if (cudaError_t err = cudaMemcpyAsync(ddst + c0 * cb, hdst + c0 * cb, size_t(c1 - c0) * cb,
                                                   cudaMemcpyHostToDevice, st))
@@ -379,11 +378,7 @@ int pnn_matmul_host(int nbits, int es, const uint64_t* A, const uint64_t* B, uin
             if ((e = cudaEventSynchronize(g_scratch.ev[k - c]))) return cuda_fail(e, "D2H sync");
             const int64_t c0 = k * kHostChunk, c1 = std::min(n, c0 + kHostChunk);
             pool.parallel_for(c1 - c0, [&](int64_t lo, int64_t hi) {
-                if (cb == 1)
-                    for (int64_t i = c0 + lo; i < c0 + hi; ++i) C[i] = hC[i];
-                else
-                    for (int64_t i = c0 + lo; i < c0 + hi; ++i)
-                        C[i] = reinterpret_cast<const uint16_t*>(hC)[i];
+                host_widen_codes(hC + (c0 + lo) * cb, C + c0 + lo, hi - lo, cb);
             });
         }
     }
