@@ -205,10 +205,19 @@ def run_training(args, rank, world, dev, dist):
     gb = B * world
     if world == 1:
         g = nn.GraphedTrainStep(model, loss_fn, opt, x, lab, B, warmup=1)
-        one = g.step
-    else:
+    else:  # the data-parallel step, NCCL all-reduce of quire lanes inside the graph
         reducer = dp.QuireAllReduce(model.params(), st.gradient)
-        one = lambda: dp.dp_train_step(model, loss_fn, opt, reducer, x, lab, gb)  # noqa: E731
+        g = nn.GraphedTrainStep(model, loss_fn, opt, x, lab, gb, warmup=1,
+                                step_fn=lambda: dp.dp_train_step(model, loss_fn, opt, reducer, x, lab, gb))
+    graphed = True
+    try:
+        g.step()  # eager warm-up
+        g.step()  # capture + first replay
+        one = g.step
+    except Exception:  # capture unsupported here: same step, eager
+        graphed = False
+        torch.cuda.synchronize(dev)
+        one = g.step_fn
     steps = max(5, min(args.steps, 50))
     for _ in range(max(args.warmup, 3)):
         one()
@@ -231,7 +240,7 @@ def run_training(args, rank, world, dev, dist):
                        "loss/optimizer posit(16,1), quires everywhere",
            "metric": "CNN training images/s", "value": gb / (ms / 1000.0), "unit": "images/s",
            "ms_per_step": ms, "global_batch": gb, "per_gpu_batch": B, "steps": steps,
-           "scaling": "weak", "cuda_graph": world == 1,
+           "scaling": "weak", "cuda_graph": graphed,
            "parallelism": f"dp{world}" + (" (quire-lane NCCL all-reduce)" if world > 1 else ""),
            "data": "synthetic uniform [-1,1) images, uniform labels (seeded per rank)"}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

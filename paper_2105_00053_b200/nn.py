@@ -308,23 +308,28 @@ class GraphedTrainStep:
     captures; each capture/replay is a real, bit-identical training step."""
 
     def __init__(self, model: Sequential, loss_fn: CrossEntropyLoss, opt: SGD, x_static, labels_static,
-                 global_batch: int, warmup: int = 1):
+                 global_batch: int, warmup: int = 1, step_fn=None):
         self.model, self.loss_fn, self.opt = model, loss_fn, opt
         self.x, self.labels, self.B = x_static, labels_static, global_batch
         self.warmup = warmup
         self.graph = None
         self.loss = None
+        # step_fn: the step to capture (default: train_step on this device; the
+        # data-parallel step passes dp.dp_train_step -- its NCCL all-reduce is
+        # captured into the same graph)
+        self.step_fn = step_fn or (lambda: train_step(self.model, self.loss_fn, self.opt, self.x,
+                                                      self.labels, self.B))
 
     def step(self):
         if self.graph is None:
             if self.warmup > 0:
                 self.warmup -= 1
-                return train_step(self.model, self.loss_fn, self.opt, self.x, self.labels, self.B)
+                return self.step_fn()
             s = torch.cuda.Stream()
             s.wait_stream(torch.cuda.current_stream())
             self.graph = torch.cuda.CUDAGraph()
             with torch.cuda.stream(s), torch.cuda.graph(self.graph, stream=s):
-                self.loss = train_step(self.model, self.loss_fn, self.opt, self.x, self.labels, self.B)
+                self.loss = self.step_fn()
             torch.cuda.current_stream().wait_stream(s)
         self.graph.replay()
         return self.loss
