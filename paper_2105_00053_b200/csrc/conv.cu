@@ -279,19 +279,23 @@ __global__ void __launch_bounds__(256) bias_grad_partial_kernel(
         acc += X;
     };
     constexpr int VE = 16 / int(sizeof(CodeT));  // codes per 16-byte load
-    for (int64_t n = n0; n < n1; ++n) {
-        const CodeT* row = dy + (n * F + ch) * P;
-        if (P % VE == 0 && (reinterpret_cast<uintptr_t>(row) & 15) == 0) {
-            // 16-byte loads: VE independent table lookups in flight per thread
-            for (int v = threadIdx.x; v < int(P / VE); v += blockDim.x) {
-                const uint4 w = __ldg(reinterpret_cast<const uint4*>(row) + v);
-                const uint32_t* ww = reinterpret_cast<const uint32_t*>(&w);
+    const bool vec = P % VE == 0 && (reinterpret_cast<uintptr_t>(dy) & 15) == 0;
+    if (vec) {
+        // 16-byte loads over the flattened (image, vector) range of the slice, so
+        // every thread works even when P / VE < blockDim (small feature maps)
+        const int64_t vpr = P / VE, nv = (n1 - n0) * vpr;
+        for (int64_t i = threadIdx.x; i < nv; i += blockDim.x) {
+            const int64_t n = n0 + i / vpr, v = i - (n - n0) * vpr;
+            const uint4 w = __ldg(reinterpret_cast<const uint4*>(dy + (n * F + ch) * P) + v);
+            const uint32_t* ww = reinterpret_cast<const uint32_t*>(&w);
 #pragma unroll
-                for (int j = 0; j < VE; ++j)
-                    term(sizeof(CodeT) == 1 ? (ww[j >> 2] >> (8 * (j & 3))) & 0xFFu
-                                            : (ww[j >> 1] >> (16 * (j & 1))) & 0xFFFFu);
-            }
-        } else {
+            for (int j = 0; j < VE; ++j)
+                term(sizeof(CodeT) == 1 ? (ww[j >> 2] >> (8 * (j & 3))) & 0xFFu
+                                        : (ww[j >> 1] >> (16 * (j & 1))) & 0xFFFFu);
+        }
+    } else {
+        for (int64_t n = n0; n < n1; ++n) {
+            const CodeT* row = dy + (n * F + ch) * P;
             for (int o = threadIdx.x; o < int(P); o += blockDim.x) term(uint32_t(row[o]));
         }
     }
