@@ -81,11 +81,6 @@ void same_cfg(const Tensor& a, const Tensor& b, const char* what) {
         throw std::invalid_argument(std::string(what) + ": dtype mismatch");
 }
 
-void no_quire_path(bool use_quire) {
-    if (!use_quire)
-        throw std::invalid_argument("non-quire sequential kernels are outside this path (SURVEY.md §8f)");
-}
-
 void sync() { cuda(cudaDeviceSynchronize(), "sync"); }
 
 }  // namespace
@@ -94,8 +89,17 @@ Tensor matmul(const Tensor& a, const Tensor& b, bool use_quire, const void*) {
     require(a.rank() == 2 && b.rank() == 2, "matmul: rank-2 tensors required");
     require(a.dim(1) == b.dim(0), "matmul: inner dimensions disagree");
     same_cfg(a, b, "matmul");
-    no_quire_path(use_quire);
     Tensor c(a.config(), {a.dim(0), b.dim(1)});
+    if (!use_quire) {  // matmul_seq: one rounding per term (tensor_ops.cpp:145-164)
+        const auto& f = a.config();
+        auto da = upload(a), dbb = upload(b);
+        Dev out(size_t(c.numel()) * cb(f));
+        check(pnn_matmul_seq(f.nbits, f.es, da->p, dbb->p, out.p, a.dim(0), b.dim(1), a.dim(1),
+                             nullptr));
+        sync();
+        download(out, c);
+        return c;
+    }
     check(pnn_matmul_host(a.config().nbits, a.config().es, a.data(), b.data(), c.data(), a.dim(0),
                           a.dim(1), b.dim(1)));
     return c;
@@ -115,7 +119,6 @@ Tensor conv2d(const Tensor& x, const Tensor& w, const Tensor* bias, int stride, 
         require(bias->numel() == w.dim(0), "conv2d: bias size mismatch");
     }
     require(w.dim(1) == x.dim(1), "conv2d: channel mismatch");
-    no_quire_path(use_quire);
     const auto& f = x.config();
     const int64_t N = x.dim(0), C = x.dim(1), H = x.dim(2), W = x.dim(3), F = w.dim(0),
                   KH = w.dim(2), KW = w.dim(3);
@@ -125,6 +128,13 @@ Tensor conv2d(const Tensor& x, const Tensor& w, const Tensor* bias, int stride, 
     auto dx = upload(x), dw = upload(w);
     std::unique_ptr<Dev> db = bias ? upload(*bias) : nullptr;
     Dev dy(size_t(y.numel()) * cb(f));
+    if (!use_quire) {  // conv_seq (tensor_ops.cpp:232-264)
+        check(pnn_conv2d_fwd_seq(f.nbits, f.es, dx->p, N, C, H, W, dw->p, F, KH, KW,
+                                 db ? db->p : nullptr, stride, pad, dy.p, nullptr));
+        sync();
+        download(dy, y);
+        return y;
+    }
     size_t ws = 0;
     check(pnn_conv2d_workspace(0, f.nbits, f.es, N, C, H, W, F, KH, KW, stride, pad, bias != nullptr,
                                &ws));
@@ -140,12 +150,18 @@ Tensor conv2d_input_grad(const Tensor& dy, const Tensor& w, const std::vector<in
                          int stride, int pad, bool use_quire, const void*) {
     require(dy.rank() == 4 && w.rank() == 4 && x_shape.size() == 4, "conv2d_input_grad: bad ranks");
     same_cfg(dy, w, "conv2d_input_grad");
-    no_quire_path(use_quire);
     const auto& f = dy.config();
     const int64_t N = x_shape[0], C = x_shape[1], H = x_shape[2], W = x_shape[3];
     Tensor dx(f, x_shape);
     auto ddy = upload(dy), dw = upload(w);
     Dev out(size_t(dx.numel()) * cb(f));
+    if (!use_quire) {  // gather_seq (tensor_ops.cpp:302-318)
+        check(pnn_conv2d_dgrad_seq(f.nbits, f.es, ddy->p, N, dy.dim(1), dy.dim(2), dy.dim(3), dw->p,
+                                   C, w.dim(2), w.dim(3), H, W, stride, pad, out.p, nullptr));
+        sync();
+        download(out, dx);
+        return dx;
+    }
     size_t ws = 0;
     check(pnn_conv2d_workspace(1, f.nbits, f.es, N, C, H, W, w.dim(0), w.dim(2), w.dim(3), stride,
                                pad, 0, &ws));
@@ -161,11 +177,18 @@ Tensor conv2d_weight_grad(const Tensor& dy, const Tensor& x, const std::vector<i
                           int stride, int pad, bool use_quire, const void*) {
     require(dy.rank() == 4 && x.rank() == 4 && w_shape.size() == 4, "conv2d_weight_grad: bad ranks");
     same_cfg(dy, x, "conv2d_weight_grad");
-    no_quire_path(use_quire);
     const auto& f = dy.config();
     Tensor dw(f, w_shape);
     auto ddy = upload(dy), dx = upload(x);
     Dev out(size_t(dw.numel()) * cb(f));
+    if (!use_quire) {  // gather_seq over (n, oy, ox) (tensor_ops.cpp:302-318, 586-600)
+        check(pnn_conv2d_wgrad_seq(f.nbits, f.es, ddy->p, dy.dim(0), dy.dim(1), dy.dim(2), dy.dim(3),
+                                   dx->p, x.dim(1), x.dim(2), x.dim(3), w_shape[2], w_shape[3], stride,
+                                   pad, out.p, nullptr));
+        sync();
+        download(out, dw);
+        return dw;
+    }
     size_t ws = 0;
     check(pnn_conv2d_workspace(2, f.nbits, f.es, x.dim(0), x.dim(1), x.dim(2), x.dim(3), w_shape[0],
                                w_shape[2], w_shape[3], stride, pad, 0, &ws));
@@ -178,11 +201,17 @@ Tensor conv2d_weight_grad(const Tensor& dy, const Tensor& x, const std::vector<i
     return dw;
 }
 
-static Tensor bias_sum(const Tensor& t, int64_t N, int64_t F, int64_t P) {
+static Tensor bias_sum(const Tensor& t, int64_t N, int64_t F, int64_t P, bool use_quire) {
     const auto& f = t.config();
     Tensor db(f, {F});
     auto d = upload(t);
     Dev out(size_t(F) * cb(f));
+    if (!use_quire) {  // gather_seq_sum (tensor_ops.cpp:320-335)
+        check(pnn_bias_grad_seq(f.nbits, f.es, d->p, N, F, P, out.p, nullptr));
+        sync();
+        download(out, db);
+        return db;
+    }
     size_t ws = 0;
     check(pnn_bias_grad_workspace(F, &ws));
     Dev work(ws);
@@ -194,14 +223,12 @@ static Tensor bias_sum(const Tensor& t, int64_t N, int64_t F, int64_t P) {
 
 Tensor conv2d_bias_grad(const Tensor& dy, bool use_quire) {
     require(dy.rank() == 4, "conv2d_bias_grad: bad rank");
-    no_quire_path(use_quire);
-    return bias_sum(dy, dy.dim(0), dy.dim(1), dy.dim(2) * dy.dim(3));
+    return bias_sum(dy, dy.dim(0), dy.dim(1), dy.dim(2) * dy.dim(3), use_quire);
 }
 
 Tensor column_sum(const Tensor& x, bool use_quire) {
     require(x.rank() == 2, "column_sum: rank-2 tensor required");
-    no_quire_path(use_quire);
-    return bias_sum(x, x.dim(0), x.dim(1), 1);
+    return bias_sum(x, x.dim(0), x.dim(1), 1, use_quire);
 }
 
 MaxPoolResult maxpool2d(const Tensor& x, int k, int stride, const void*) {

@@ -86,6 +86,22 @@ int main() {
         for (int64_t i = 0; i < mp.out.numel(); ++i) EXPECT(mp.out.bits_at(i) == mpw[size_t(i)] && mp.argmax[size_t(i)] == amw[size_t(i)]);
         Tensor conv = pnn_b200::convert_tensor(x, p80);
         for (int64_t i = 0; i < x.numel(); ++i) EXPECT(conv.bits_at(i) == po_convert(f.nbits, f.es, 8, 0, x.bits_at(i)));
+        // use_quire = false: the sequential-rounding kernels (tensor_ops.cpp:145-164, 232-335)
+        Tensor Cs = pnn_b200::matmul(A, B, false);
+        po_matmul_seq(f.nbits, f.es, A.data(), B.data(), Cw.data(), 37, 53, 29);
+        for (int i = 0; i < 37 * 29; ++i) EXPECT(Cs.bits_at(i) == Cw[size_t(i)]);
+        Tensor ys = pnn_b200::conv2d(x, w, &bias, 1, 1, false);
+        po_conv2d_seq(f.nbits, f.es, x.data(), 2, 3, 9, 8, w.data(), 4, 3, 3, bias.data(), 1, 1, yw.data());
+        for (int64_t i = 0; i < ys.numel(); ++i) EXPECT(ys.bits_at(i) == yw[size_t(i)]);
+        Tensor dxs = pnn_b200::conv2d_input_grad(dy, w, x.shape(), 1, 1, false);
+        po_conv2d_input_grad_seq(f.nbits, f.es, dy.data(), 2, 4, 9, 8, w.data(), 3, 3, 3, 9, 8, 1, 1, dxw.data());
+        for (int64_t i = 0; i < dxs.numel(); ++i) EXPECT(dxs.bits_at(i) == dxw[size_t(i)]);
+        Tensor dws = pnn_b200::conv2d_weight_grad(dy, x, w.shape(), 1, 1, false);
+        po_conv2d_weight_grad_seq(f.nbits, f.es, dy.data(), 2, 4, 9, 8, x.data(), 3, 9, 8, 3, 3, 1, 1, dww.data());
+        for (int64_t i = 0; i < dws.numel(); ++i) EXPECT(dws.bits_at(i) == dww[size_t(i)]);
+        Tensor dbs = pnn_b200::conv2d_bias_grad(dy, false);
+        po_bias_grad_seq(f.nbits, f.es, dy.data(), 2, 4, 9 * 8, dbw.data());
+        for (int i = 0; i < 4; ++i) EXPECT(dbs.bits_at(i) == dbw[size_t(i)]);
     }
     std::printf("host_ops_test: %s (%d failures)\n", failures ? "FAILED" : "ok", failures);
     return failures ? 1 : 0;
