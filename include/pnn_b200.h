@@ -132,6 +132,19 @@ int pnn_softmax_xent(int nbits, int es, const void* logits, const int32_t* label
 int pnn_sgd_step(int opt_nbits, int opt_es, void* master, int g_nbits, int g_es, const void* grad,
                  int64_t n, uint32_t lr_code, int c1_nbits, int c1_es, void* copy1, int c2_nbits,
                  int c2_es, void* copy2, void* stream);
+/* Loss scaling by 2^s (SPEC "scale_gradients"): the
+ * logit gradient leaves the loss as ldexp(p - onehot, s - log2_batch) (the
+ * loss value is not scaled); the SGD step unscales in the optimizer format,
+ * g = ldexp(convert(grad), -s), before master = sub(master, mul(lr, g)).
+ * s = 0 is the unscaled entry above. */
+int pnn_softmax_xent_scaled(int nbits, int es, const void* logits, const int32_t* labels,
+                            int64_t B, int64_t classes, int log2_batch, int grad_scale_log2,
+                            void* dlogits, void* loss_rows, void* loss_out, void* raw_word,
+                            void* raw_nar, void* stream);
+int pnn_sgd_step_scaled(int opt_nbits, int opt_es, void* master, int g_nbits, int g_es,
+                        const void* grad, int64_t n, uint32_t lr_code, int c1_nbits, int c1_es,
+                        void* copy1, int c2_nbits, int c2_es, void* copy2, int grad_scale_log2,
+                        void* stream);
 /* avgpool2d / avgpool2d_backward (tensor_ops.cpp:672-720): window sum (quire
  * when use_quire, else an add chain) times the caller-quantized reciprocal. */
 int pnn_avgpool2d_fwd(int nbits, int es, const void* x, int64_t N, int64_t C, int64_t H,

@@ -366,21 +366,23 @@ class Restatement(_Base):
         self.lib.po_relu_bwd(xn, xes, _p(x), _p(dy), _p(dx), i64(x.size))
         return dx
 
-    def softmax_xent(self, n, es, logits, labels, log2_batch):
+    def softmax_xent(self, n, es, logits, labels, log2_batch, grad_scale_log2=0):
         z = _codes(logits)
         B, Cn = z.shape
         lab = np.ascontiguousarray(np.asarray(labels, np.int32))
         d = np.zeros(z.shape, np.uint64)
         rows = np.zeros((B,), np.uint64)
-        self.lib.po_softmax_xent.restype = C.c_uint64
-        loss = self.lib.po_softmax_xent(n, es, _p(z), lab.ctypes.data_as(C.POINTER(C.c_int32)), i64(B),
-                                        i64(Cn), int(log2_batch), _p(d), _p(rows))
+        self.lib.po_softmax_xent_scaled.restype = C.c_uint64
+        loss = self.lib.po_softmax_xent_scaled(n, es, _p(z), lab.ctypes.data_as(C.POINTER(C.c_int32)),
+                                               i64(B), i64(Cn), int(log2_batch), int(grad_scale_log2),
+                                               _p(d), _p(rows))
         return int(loss), d, rows
 
-    def sgd(self, on, oes, w, gn, ges, g, lr):
+    def sgd(self, on, oes, w, gn, ges, g, lr, grad_scale_log2=0):
         w = _codes(w).copy()
         g = _codes(g)
-        self.lib.po_sgd(on, oes, _p(w), gn, ges, _p(g), i64(w.size), C.c_uint64(int(lr)))
+        self.lib.po_sgd_scaled(on, oes, _p(w), gn, ges, _p(g), i64(w.size), C.c_uint64(int(lr)),
+                               int(grad_scale_log2))
         return w
 
     def convert_tensor(self, sn, se, dn, de, x):

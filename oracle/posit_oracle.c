@@ -753,6 +753,16 @@ void po_relu_bwd(int x_nbits, int x_es, const uint64_t* x, const uint64_t* dy, u
 uint64_t po_softmax_xent(int nbits, int es, const uint64_t* logits, const int32_t* labels,
                          int64_t B, int64_t C, int log2_batch, uint64_t* dlogits,
                          uint64_t* loss_rows) {
+    return po_softmax_xent_scaled(nbits, es, logits, labels, B, C, log2_batch, 0, dlogits,
+                                  loss_rows);
+}
+
+/* Loss scaling (SPEC "scale_gradients"): the logit
+ * gradient carries an extra 2^s, dlogits = ldexp(p - [j==y], s - log2 B); the
+ * loss itself is not scaled. */
+uint64_t po_softmax_xent_scaled(int nbits, int es, const uint64_t* logits, const int32_t* labels,
+                                int64_t B, int64_t C, int log2_batch, int grad_scale_log2,
+                                uint64_t* dlogits, uint64_t* loss_rows) {
     const uint64_t one = po_from_int64(nbits, es, 1);
     po_quire* tot = po_quire_new(nbits, es);
     po_quire* q = po_quire_new(nbits, es);
@@ -767,7 +777,8 @@ uint64_t po_softmax_xent(int nbits, int es, const uint64_t* logits, const int32_
         const int32_t y = labels[i];
         for (int64_t j = 0; j < C; ++j) {
             const uint64_t p = OP_DIV(po_exp(nbits, es, OP_SUB(z[j], m)), S);
-            dlogits[i * C + j] = po_ldexp(nbits, es, OP_SUB(p, j == y ? one : 0), -log2_batch);
+            dlogits[i * C + j] =
+                po_ldexp(nbits, es, OP_SUB(p, j == y ? one : 0), grad_scale_log2 - log2_batch);
         }
         loss_rows[i] = OP_SUB(po_log(nbits, es, S), OP_SUB(z[y], m));
         po_quire_add_posit(tot, loss_rows[i]);
@@ -780,8 +791,16 @@ uint64_t po_softmax_xent(int nbits, int es, const uint64_t* logits, const int32_
 
 void po_sgd(int opt_nbits, int opt_es, uint64_t* w, int g_nbits, int g_es, const uint64_t* g,
             int64_t n, uint64_t lr) {
+    po_sgd_scaled(opt_nbits, opt_es, w, g_nbits, g_es, g, n, lr, 0);
+}
+
+/* Loss-scaled SGD: the gradient is unscaled in the optimizer format,
+ * g_opt = ldexp(convert(g), -s), then w = sub(w, mul(lr, g_opt)). */
+void po_sgd_scaled(int opt_nbits, int opt_es, uint64_t* w, int g_nbits, int g_es,
+                   const uint64_t* g, int64_t n, uint64_t lr, int grad_scale_log2) {
     for (int64_t i = 0; i < n; ++i) {
-        const uint64_t gg = po_convert(g_nbits, g_es, opt_nbits, opt_es, g[i]);
+        uint64_t gg = po_convert(g_nbits, g_es, opt_nbits, opt_es, g[i]);
+        if (grad_scale_log2 != 0) gg = po_ldexp(opt_nbits, opt_es, gg, -grad_scale_log2);
         w[i] = po_scalar_op(opt_nbits, opt_es, 1, w[i],
                             po_scalar_op(opt_nbits, opt_es, 2, lr, gg));
     }

@@ -139,6 +139,13 @@ uint64_t po_softmax_xent(int nbits, int es, const uint64_t* logits, const int32_
 /* A.7 SGD: w = sub(w, mul(lr, convert(g -> opt))) in the optimizer format. */
 void po_sgd(int opt_nbits, int opt_es, uint64_t* w, int g_nbits, int g_es, const uint64_t* g,
             int64_t n, uint64_t lr);
+/* Loss scaling by 2^s: dlogits carry 2^s; the SGD
+ * update unscales in the optimizer format, g = ldexp(convert(g), -s). */
+uint64_t po_softmax_xent_scaled(int nbits, int es, const uint64_t* logits, const int32_t* labels,
+                                int64_t B, int64_t C, int log2_batch, int grad_scale_log2,
+                                uint64_t* dlogits, uint64_t* loss_rows);
+void po_sgd_scaled(int opt_nbits, int opt_es, uint64_t* w, int g_nbits, int g_es,
+                   const uint64_t* g, int64_t n, uint64_t lr, int grad_scale_log2);
 
 #ifdef __cplusplus
 }

@@ -39,11 +39,12 @@ def _cv(po, src, dst, x):
     return po.convert_tensor(*src, *dst, x)
 
 
-def oracle_step(po, layers, st, params, x, labels, lr, global_batch, record=None):
+def oracle_step(po, layers, st, params, x, labels, lr, global_batch, record=None, grad_scale_log2=0):
     """One SGD step.  st = dict(forward, backward, gradient, optimizer, loss) of
     (nbits, es); x = input codes in the forward format; returns (loss_code,
     new_params, grads) and fills ``record`` (if given) with every activation
-    and gradient, keyed like the GPU model's recording."""
+    and gradient, keyed like the GPU model's recording.  grad_scale_log2 = s:
+    loss scaling by 2^s (dlogits carry 2^s, SGD unscales)."""
     f, b, g, o, lf = (tuple(st[k]) for k in ("forward", "backward", "gradient", "optimizer", "loss"))
     lb = int(round(math.log2(global_batch)))
     rec = record if record is not None else {}
@@ -78,7 +79,7 @@ def oracle_step(po, layers, st, params, x, labels, lr, global_batch, record=None
             h = h.reshape(h.shape[0], -1)
         rec[f"act{li}"] = h
     z = _cv(po, f, lf, h)
-    loss, d, rows = po.softmax_xent(*lf, z, labels, lb)
+    loss, d, rows = po.softmax_xent(*lf, z, labels, lb, grad_scale_log2)
     rec["loss_rows"] = rows
     dy = _cv(po, lf, b, d)
     rec["dlogits"] = dy
@@ -111,7 +112,8 @@ def oracle_step(po, layers, st, params, x, labels, lr, global_batch, record=None
     lr_code = po.from_float64(*o, lr)
     new_params = []
     for (w, bias), (dw, db) in zip(params, grads):
-        new_params.append((po.sgd(*o, w, *g, dw, lr_code), po.sgd(*o, bias, *g, db, lr_code)))
+        new_params.append((po.sgd(*o, w, *g, dw, lr_code, grad_scale_log2),
+                           po.sgd(*o, bias, *g, db, lr_code, grad_scale_log2)))
     return loss, new_params, grads
 
 

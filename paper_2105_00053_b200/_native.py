@@ -56,6 +56,10 @@ _SIGS = {
                                    _vp]),
     "pnn_sgd_step": (C.c_int, [C.c_int, C.c_int, _vp, C.c_int, C.c_int, _vp, _i64, C.c_uint32, C.c_int,
                                C.c_int, _vp, C.c_int, C.c_int, _vp, _vp]),
+    "pnn_softmax_xent_scaled": (C.c_int, [C.c_int, C.c_int, _vp, _vp, _i64, _i64, C.c_int, C.c_int, _vp,
+                                          _vp, _vp, _vp, _vp, _vp]),
+    "pnn_sgd_step_scaled": (C.c_int, [C.c_int, C.c_int, _vp, C.c_int, C.c_int, _vp, _i64, C.c_uint32,
+                                      C.c_int, C.c_int, _vp, C.c_int, C.c_int, _vp, C.c_int, _vp]),
     "pnn_avgpool2d_fwd": (C.c_int, [C.c_int, C.c_int, _vp] + [_i64] * 4 + [C.c_int, C.c_int, C.c_int,
                                                                          C.c_uint32, _vp, _vp]),
     "pnn_avgpool2d_bwd": (C.c_int, [C.c_int, C.c_int, _vp] + [_i64] * 4 + [C.c_int, C.c_int, C.c_uint32,

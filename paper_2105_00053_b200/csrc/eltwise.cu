@@ -253,8 +253,8 @@ __global__ void relu_bwd_vec_kernel(int x_nbits, const TX* __restrict__ x,
 // any reduction order gives the same value), the exact integer sum of e_j
 // (butterfly over 128-bit lanes), one rounding, then p_j per lane.
 __global__ void softmax_xent_kernel(PositFmt f, int b, const void* logits, const int32_t* labels,
-                                    int64_t B, int64_t Cn, int log2_batch, void* dlogits,
-                                    void* loss_rows) {
+                                    int64_t B, int64_t Cn, int log2_batch, int grad_scale_log2,
+                                    void* dlogits, void* loss_rows) {
     const int lane = threadIdx.x & 31;
     const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
     for (int64_t i = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5; i < B; i += nwarps) {
@@ -276,9 +276,9 @@ __global__ void softmax_xent_kernel(PositFmt f, int b, const void* logits, const
         for (int64_t j = lane; j < Cn; j += 32) {
             const uint32_t e = p_exp(f, p_sub(f, load_any(logits, row + j, b), m));
             if (j == lane) e0 = e;
-            int64_t X;
-            nar |= decode_x(e, f, X);
-            const unsigned __int128 s = ((unsigned __int128)hi << 64 | lo) + (unsigned __int128)(__int128)X;
+            __int128 X;
+            nar |= decode_x128(e, f, X);
+            const unsigned __int128 s = ((unsigned __int128)hi << 64 | lo) + (unsigned __int128)X;
             lo = uint64_t(s);
             hi = uint64_t(s >> 64);
         }
@@ -305,7 +305,7 @@ __global__ void softmax_xent_kernel(PositFmt f, int b, const void* logits, const
             const uint32_t e = j == lane ? e0 : p_exp(f, p_sub(f, load_any(logits, row + j, b), m));
             const uint32_t pj = p_div(f, e, S);
             const uint32_t g = p_sub(f, pj, j == y ? one : 0u);
-            store_any(dlogits, row + j, b, p_ldexp(f, g, -log2_batch));
+            store_any(dlogits, row + j, b, p_ldexp(f, g, grad_scale_log2 - log2_batch));
         }
         if (lane == 0) {
             const uint32_t zy = load_any(logits, row + y, b);
@@ -325,8 +325,8 @@ __global__ void loss_reduce_kernel(PositFmt f, int b, const void* loss_rows, int
     __syncthreads();
     __int128 acc = 0;
     for (int64_t i = threadIdx.x; i < B; i += blockDim.x) {
-        int64_t X;
-        if (decode_x(load_any(loss_rows, i, b), f, X)) nar_s = 1;
+        __int128 X;
+        if (decode_x128(load_any(loss_rows, i, b), f, X)) nar_s = 1;
         acc += X;
     }
     lo_s[threadIdx.x] = (unsigned long long)uint64_t(acc);
@@ -336,15 +336,20 @@ __global__ void loss_reduce_kernel(PositFmt f, int b, const void* loss_rows, int
         unsigned __int128 s = 0;
         for (int t = 0; t < blockDim.x; ++t)
             s += (unsigned __int128)lo_s[t] | ((unsigned __int128)hi_s[t] << 64);
-        const unsigned __int128 one = 1;
-        const unsigned __int128 wmask = f.W >= 128 ? ~(unsigned __int128)0 : ((one << f.W) - 1);
-        const unsigned __int128 q = (s << f.R) & wmask;
-        if (raw_word) {
-            *raw_word = q;
+        if (raw_word) {  // W <= 128 (host-checked)
+            const unsigned __int128 one = 1;
+            const unsigned __int128 wmask = f.W >= 128 ? ~(unsigned __int128)0 : ((one << f.W) - 1);
+            *raw_word = (s << f.R) & wmask;
             *raw_nar = nar_s ? 1 : 0;
         }
         if (loss_out) {
-            const uint32_t c = nar_s ? nar_of(f) : quire_to_posit(f, q);
+            // the same exact sum rounded once, from the image (LSB 2^-R)
+            const __int128 sx = (__int128)s;
+            const bool neg = sx < 0;
+            const uint32_t c =
+                nar_s ? nar_of(f)
+                      : (sx == 0 ? 0u
+                                 : round_mag128(f, neg, (unsigned __int128)(neg ? -sx : sx), -f.R));
             store_any(loss_out, 0, b, p_ldexp(f, c, -log2_batch));
         }
     }
@@ -354,9 +359,10 @@ __global__ void loss_reduce_kernel(PositFmt f, int b, const void* loss_rows, int
 // the optimizer format, then refresh the stage copies (convert, SPEC §3.3).
 __global__ void sgd_kernel(PositFmt fo, int bo, void* master, PositFmt fg, int bg, const void* grad,
                            int64_t n, uint32_t lr, PositFmt f1, int b1, void* copy1, PositFmt f2,
-                           int b2, void* copy2) {
+                           int b2, void* copy2, int grad_scale_log2) {
     GRID_STRIDE(i, n) {
-        const uint32_t g = p_convert(fg, fo, load_any(grad, i, bg));
+        uint32_t g = p_convert(fg, fo, load_any(grad, i, bg));
+        if (grad_scale_log2 != 0) g = p_ldexp(fo, g, -grad_scale_log2);  // loss-scale undo
         const uint32_t w = p_sub(fo, load_any(master, i, bo), p_mul(fo, lr, g));
         store_any(master, i, bo, w);
         if (copy1) store_any(copy1, i, b1, p_convert(fo, f1, w));
@@ -379,8 +385,8 @@ __global__ void avgpool_fwd_kernel(PositFmt f, int b, const void* x, int64_t NC,
             bool nar = false;
             for (int ky = 0; ky < k; ++ky)
                 for (int kx = 0; kx < k; ++kx) {
-                    int64_t X;
-                    nar |= decode_x(load_any(x, base + ky * W + kx, b), f, X);
+                    __int128 X;
+                    nar |= decode_x128(load_any(x, base + ky * W + kx, b), f, X);
                     acc += X;
                 }
             const bool neg = acc < 0;
@@ -453,7 +459,7 @@ namespace {
 
 bool elt_fmt_ok(int nbits, int es) {
     if (nbits < 2 || nbits > 16 || es < 0 || es > 4) return false;
-    return 2 * make_fmt(nbits, es).R <= 56;
+    return 2 * make_fmt(nbits, es).R <= 96;  // 128-bit images; up to posit(12,2)
 }
 
 int bytes_of(int nbits) { return nbits <= 8 ? 1 : 2; }
@@ -581,13 +587,24 @@ int pnn_maxpool2d_bwd(int nbits, int es, const void* dy, const int64_t* argmax, 
 int pnn_softmax_xent(int nbits, int es, const void* logits, const int32_t* labels, int64_t B,
                      int64_t classes, int log2_batch, void* dlogits, void* loss_rows,
                      void* loss_out, void* raw_word, void* raw_nar, void* stream) {
+    return pnn_softmax_xent_scaled(nbits, es, logits, labels, B, classes, log2_batch, 0, dlogits,
+                                   loss_rows, loss_out, raw_word, raw_nar, stream);
+}
+
+int pnn_softmax_xent_scaled(int nbits, int es, const void* logits, const int32_t* labels,
+                            int64_t B, int64_t classes, int log2_batch, int grad_scale_log2,
+                            void* dlogits, void* loss_rows, void* loss_out, void* raw_word,
+                            void* raw_nar, void* stream) {
     CHECK_FMT(nbits, es);
     if (B < 1 || classes < 1 || !logits || !labels || !dlogits || !loss_rows)
         return set_status(PNN_EINVAL, "softmax_xent: bad arguments");
     const PositFmt f = make_fmt(nbits, es);
+    if (raw_word && f.W > 128)
+        return set_status(PNN_EUNSUPPORTED, "softmax_xent: raw loss words need a quire of <= 128 bits");
     auto st = (cudaStream_t)stream;
     softmax_xent_kernel<<<grid1(B * 32), 256, 0, st>>>(f, bytes_of(nbits), logits, labels, B, classes,
-                                                  log2_batch, dlogits, loss_rows);
+                                                      log2_batch, grad_scale_log2, dlogits,
+                                                      loss_rows);
     if (loss_out || raw_word)
         loss_reduce_kernel<<<1, 256, 0, st>>>(f, bytes_of(nbits), loss_rows, B, log2_batch,
                                               loss_out, (unsigned __int128*)raw_word,
@@ -598,6 +615,14 @@ int pnn_softmax_xent(int nbits, int es, const void* logits, const int32_t* label
 int pnn_sgd_step(int opt_nbits, int opt_es, void* master, int g_nbits, int g_es, const void* grad,
                  int64_t n, uint32_t lr_code, int c1_nbits, int c1_es, void* copy1, int c2_nbits,
                  int c2_es, void* copy2, void* stream) {
+    return pnn_sgd_step_scaled(opt_nbits, opt_es, master, g_nbits, g_es, grad, n, lr_code, c1_nbits,
+                               c1_es, copy1, c2_nbits, c2_es, copy2, 0, stream);
+}
+
+int pnn_sgd_step_scaled(int opt_nbits, int opt_es, void* master, int g_nbits, int g_es,
+                        const void* grad, int64_t n, uint32_t lr_code, int c1_nbits, int c1_es,
+                        void* copy1, int c2_nbits, int c2_es, void* copy2, int grad_scale_log2,
+                        void* stream) {
     CHECK_FMT(opt_nbits, opt_es);
     CHECK_FMT(g_nbits, g_es);
     if (copy1) CHECK_FMT(c1_nbits, c1_es);
@@ -609,7 +634,7 @@ int pnn_sgd_step(int opt_nbits, int opt_es, void* master, int g_nbits, int g_es,
     sgd_kernel<<<grid1(n), 256, 0, (cudaStream_t)stream>>>(
         make_fmt(opt_nbits, opt_es), bytes_of(opt_nbits), master, make_fmt(g_nbits, g_es),
         bytes_of(g_nbits), grad, n, lr_code, f1, bytes_of(f1.nbits), copy1, f2,
-        bytes_of(f2.nbits), copy2);
+        bytes_of(f2.nbits), copy2, grad_scale_log2);
     return launched("sgd_step");
 }
 

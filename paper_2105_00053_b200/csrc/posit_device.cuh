@@ -86,6 +86,38 @@ __device__ __forceinline__ bool decode_x(uint32_t code, const PositFmt& f, int64
     return false;
 }
 
+// Same, into a 128-bit image: valid for 2R <= 124 (the elementwise formats up
+// to posit(12,2), R = 40, used by the posit(8,2)* optimizer and loss stages).
+__device__ __forceinline__ bool decode_x128(uint32_t code, const PositFmt& f, __int128& X) {
+    const uint32_t mask = f.nbits == 32 ? 0xFFFFFFFFu : ((1u << f.nbits) - 1u);
+    code &= mask;
+    X = 0;
+    if (code == 0) return false;
+    const uint32_t nar = 1u << (f.nbits - 1);
+    if (code == nar) return true;
+    const bool neg = (code & nar) != 0;
+    const uint32_t mag = neg ? ((0u - code) & mask) : code;
+    const uint32_t p = mag << (33 - f.nbits);
+    const bool first = (p >> 31) != 0;
+    int run = first ? __clz(~p) : __clz(p);
+    if (run > f.nbits - 1) run = f.nbits - 1;
+    const int k = first ? run - 1 : -run;
+    const int used = run + 1;
+    int rem = f.nbits - 1 - used;
+    if (rem < 0) rem = 0;
+    const uint32_t tail = used < 32 ? (p << used) : 0u;
+    const int ebits = f.es < rem ? f.es : rem;
+    uint32_t e = ebits > 0 ? (tail >> (32 - ebits)) : 0u;
+    e <<= (f.es - ebits);
+    const int fb = rem - ebits;
+    const uint32_t frac = fb > 0 ? ((tail << ebits) >> (32 - fb)) : 0u;
+    const int scale = k * (1 << f.es) + int(e);
+    const unsigned __int128 sig = (unsigned __int128)((uint64_t(1) << fb) | frac);
+    const __int128 mx = (__int128)(sig << (scale - fb + f.R));
+    X = neg ? -mx : mx;
+    return false;
+}
+
 // Balanced base-256 digits: X = sum_d digit[d] * 256^d, digit in [-128, 127].
 template <int D>
 __device__ __forceinline__ void balanced_digits(int64_t X, int8_t (&dig)[D]) {

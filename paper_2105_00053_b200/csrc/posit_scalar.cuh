@@ -87,6 +87,31 @@ __device__ __forceinline__ uint32_t p_negate(const PositFmt& f, uint32_t a) {
     return (0u - a) & code_mask(f);
 }
 
+// add/sub/mul for the wide elementwise formats (56 < 2R <= 124, e.g. the
+// posit(12,2) optimizer and posit(10,2) loss of the posit(8,2)* preset):
+// add/sub on 128-bit integer images (|X| <= 2^(2R) < 2^125, exact); mul on
+// the significands (two <= 16-bit significands, exact 128-bit product).
+// Either way the exact result is rounded once, as in the narrow path.
+static __device__ __noinline__ uint32_t p_op_wide(const PositFmt& f, int op, uint32_t a,
+                                                  uint32_t b) {
+    if (op == 2) {
+        const Unp ua = unpack(f, a), ub = unpack(f, b);
+        if (ua.cls == 0 || ub.cls == 0) return 0;
+        const unsigned __int128 pr = (unsigned __int128)ua.sig * ub.sig;  // value * 2^(126-sa-sb)
+        return round_mag128(f, ua.neg != ub.neg, pr, ua.scale + ub.scale - 126);
+    }
+    __int128 xa, xb;
+    decode_x128(a, f, xa);
+    decode_x128(b, f, xb);
+    if (op == 1) xb = -xb;
+    if (xb == 0) return a;                          // x + 0 == x (posit.cpp:400)
+    if (xa == 0) return op == 1 ? p_negate(f, b) : b;
+    const __int128 s = xa + xb;
+    if (s == 0) return 0;
+    const bool neg = s < 0;
+    return round_mag128(f, neg, (unsigned __int128)(neg ? -s : s), -f.R);
+}
+
 // op: 0 add, 1 sub, 2 mul, 3 div
 __device__ __forceinline__ uint32_t p_op(const PositFmt& f, int op, uint32_t a, uint32_t b) {
     const uint32_t m = code_mask(f), nar = nar_of(f);
@@ -113,6 +138,7 @@ __device__ __forceinline__ uint32_t p_op(const PositFmt& f, int op, uint32_t a, 
         }
         return pack_round(f, ua.neg != ub.neg, scale, sig, sticky);
     }
+    if (2 * f.R > 56) return p_op_wide(f, op, a, b);
     int64_t xa, xb;
     decode_x(a, f, xa);
     decode_x(b, f, xb);

@@ -46,6 +46,12 @@ class StagePrecisions:
         c = ops._cfg(cfg)
         return StagePrecisions(c, c, c, c, c)
 
+    @staticmethod
+    def posit82_star() -> "StagePrecisions":
+        """posit(8,2)* = O12L10 (Table 4): optimizer
+        posit(12,2), loss posit(10,2), everything else posit(8,2)."""
+        return StagePrecisions(ops.P82, ops.P82, ops.P82, ops.P122, ops.P102)
+
 
 class MixedParam:
     """Master copy in p_optimizer plus converted copies per stage format."""
@@ -196,17 +202,21 @@ class Flatten(Module):
 
 class CrossEntropyLoss(Module):
     """Softmax cross-entropy in p_loss (Appendix A.5); the gradient is already
-    divided by the GLOBAL batch (2^-log2_batch)."""
+    divided by the GLOBAL batch (2^-log2_batch).  grad_scale_log2 = s scales
+    the logit gradient by 2^s (loss scaling, SPEC scale_gradients); pair it
+    with SGD(..., grad_scale_log2=s), which unscales in p_optimizer."""
 
-    def __init__(self, st: StagePrecisions):
+    def __init__(self, st: StagePrecisions, grad_scale_log2: int = 0):
         self.st = st
+        self.grad_scale_log2 = int(grad_scale_log2)
 
     def __call__(self, logits_fwd, labels, global_batch: int, raw=False):
         lb = int(round(math.log2(global_batch)))
         if 1 << lb != global_batch:
             raise ValueError("global batch must be a power of two (Appendix A.5)")
         z = ops.convert_tensor(logits_fwd, self.st.forward, self.st.loss)
-        out = ops.softmax_xent(self.st.loss, z, labels, lb, raw=raw)
+        out = ops.softmax_xent(self.st.loss, z, labels, lb, raw=raw,
+                               grad_scale_log2=self.grad_scale_log2)
         dz = ops.convert_tensor(out[1], self.st.loss, self.st.backward)
         if raw:
             loss, _, rows, word, nar = out
@@ -242,11 +252,12 @@ class SGD:
     """master = sub(master, mul(lr, convert(grad -> p_opt))), copies refreshed
     (Appendix A.7; momentum 0)."""
 
-    def __init__(self, params, lr: float, st: StagePrecisions):
+    def __init__(self, params, lr: float, st: StagePrecisions, grad_scale_log2: int = 0):
         from .codec import from_float64_array
 
         self.params = params
         self.st = st
+        self.grad_scale_log2 = int(grad_scale_log2)
         self.lr_code = int(from_float64_array(np.array([lr]), st.optimizer)[0])
 
     def step(self):
@@ -254,7 +265,8 @@ class SGD:
         for p in self.params:
             fmts = p.stage_formats()
             fused = [(c, p.copies[c]) for c in fmts[:2]]  # refreshed inside the SGD kernel
-            ops.sgd_step(st.optimizer, p.master, st.gradient, p.grad, self.lr_code, fused)
+            ops.sgd_step(st.optimizer, p.master, st.gradient, p.grad, self.lr_code, fused,
+                         grad_scale_log2=self.grad_scale_log2)
             for c in fmts[2:]:
                 p.copies[c] = ops.convert_tensor(p.master, st.optimizer, c)
 

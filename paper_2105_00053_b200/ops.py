@@ -61,6 +61,9 @@ class PositConfig:
 
 P80, P81, P82 = PositConfig(8, 0), PositConfig(8, 1), PositConfig(8, 2)
 P121, P161 = PositConfig(12, 1), PositConfig(16, 1)
+# optimizer / loss formats of the posit(8,2)* preset (O12L10);
+# elementwise-only (convert, softmax cross-entropy, SGD), no quire GEMMs
+P102, P122 = PositConfig(10, 2), PositConfig(12, 2)
 
 
 def _cfg(cfg) -> PositConfig:
@@ -415,8 +418,9 @@ def maxpool2d_backward(cfg, dy, argmax, x_shape, k: int = 2, stride: int = 2):
     return dx
 
 
-def softmax_xent(cfg, logits, labels, log2_batch: int, raw: bool = False):
-    """SURVEY.md Appendix A.5 -> (loss code tensor [1], dlogits, loss_rows[, raw word, raw nar])."""
+def softmax_xent(cfg, logits, labels, log2_batch: int, raw: bool = False, grad_scale_log2: int = 0):
+    """SURVEY.md Appendix A.5 -> (loss code tensor [1], dlogits, loss_rows[, raw word, raw nar]).
+    grad_scale_log2 = s multiplies dlogits by 2^s (loss scaling)."""
     cfg = _cfg(cfg)
     logits = logits.contiguous()
     B, Cn = logits.shape
@@ -426,23 +430,26 @@ def softmax_xent(cfg, logits, labels, log2_batch: int, raw: bool = False):
     loss = torch.empty((1,), dtype=logits.dtype, device=logits.device)
     word = torch.empty((2,), dtype=torch.int64, device=logits.device) if raw else None
     nar = torch.empty((1,), dtype=torch.uint8, device=logits.device) if raw else None
-    _native.check(_native.lib().pnn_softmax_xent(cfg.nbits, cfg.es, logits.data_ptr(), labels.data_ptr(), B, Cn,
-                                                 int(log2_batch), d.data_ptr(), rows.data_ptr(),
+    _native.check(_native.lib().pnn_softmax_xent_scaled(cfg.nbits, cfg.es, logits.data_ptr(), labels.data_ptr(),
+                                                 B, Cn, int(log2_batch), int(grad_scale_log2),
+                                                 d.data_ptr(), rows.data_ptr(),
                                                  loss.data_ptr(), word.data_ptr() if raw else None,
                                                  nar.data_ptr() if raw else None, _stream_ptr(logits.device)))
     return (loss, d, rows, word, nar) if raw else (loss, d, rows)
 
 
-def sgd_step(opt_cfg, master, g_cfg, grad, lr_code: int, copies=()):
-    """SURVEY.md Appendix A.7, in place on master; copies = [(cfg, tensor), ...] (<= 2)."""
+def sgd_step(opt_cfg, master, g_cfg, grad, lr_code: int, copies=(), grad_scale_log2: int = 0):
+    """SURVEY.md Appendix A.7, in place on master; copies = [(cfg, tensor), ...] (<= 2).
+    grad_scale_log2 = s unscales the gradient by 2^-s in the optimizer format."""
     oc, gc = _cfg(opt_cfg), _cfg(g_cfg)
     cps = [(_cfg(c), t) for c, t in copies] + [(oc, None)] * (2 - len(copies))
     (c1, t1), (c2, t2) = cps[0], cps[1]
-    _native.check(_native.lib().pnn_sgd_step(oc.nbits, oc.es, master.data_ptr(), gc.nbits, gc.es,
-                                             grad.contiguous().data_ptr(), master.numel(), int(lr_code),
-                                             c1.nbits, c1.es, t1.data_ptr() if t1 is not None else None,
-                                             c2.nbits, c2.es, t2.data_ptr() if t2 is not None else None,
-                                             _stream_ptr(master.device)))
+    _native.check(_native.lib().pnn_sgd_step_scaled(oc.nbits, oc.es, master.data_ptr(), gc.nbits, gc.es,
+                                                    grad.contiguous().data_ptr(), master.numel(),
+                                                    int(lr_code), c1.nbits, c1.es,
+                                                    t1.data_ptr() if t1 is not None else None,
+                                                    c2.nbits, c2.es, t2.data_ptr() if t2 is not None else None,
+                                                    int(grad_scale_log2), _stream_ptr(master.device)))
     return master
 
 

@@ -49,7 +49,25 @@ def test_scalar_ops_random(cuda, po, cfg):
         assert (got == want).all(), op
 
 
-@pytest.mark.parametrize("cfg", [(8, 0), (8, 1), (12, 1), (16, 1)])
+@pytest.mark.parametrize("cfg", [(10, 2), (12, 2)])
+def test_scalar_ops_wide_formats(cuda, po, cfg):
+    """The posit(8,2)* optimizer / loss formats (2R > 56: 128-bit images and
+    significand products): every op on random pairs plus the corner codes."""
+    n, es = cfg
+    rng = np.random.default_rng(n * 7 + es)
+    corners = np.array([0, 1, 2, 3, (1 << (n - 1)) - 1, (1 << (n - 1)) - 2, 1 << (n - 1),
+                        (1 << (n - 1)) + 1, (1 << n) - 1, (1 << n) - 2, 1 << (n - 2)], np.int64)
+    a = np.concatenate([rng.integers(0, 1 << n, 300000), np.repeat(corners, corners.size)])
+    b = np.concatenate([rng.integers(0, 1 << n, 300000), np.tile(corners, corners.size)])
+    a, b = a.astype(np.int64), b.astype(np.int64)
+    for op in range(4):
+        got = host(ops.scalar_eval(cfg, op, torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda())) & mask(n)
+        want = po.ew(n, es, op, a.astype(np.uint64), b.astype(np.uint64))
+        bad = np.nonzero(got != want)[0]
+        assert bad.size == 0, (op, a[bad[:3]], b[bad[:3]], got[bad[:3]], want[bad[:3]])
+
+
+@pytest.mark.parametrize("cfg", [(8, 0), (8, 1), (12, 1), (16, 1), (10, 2), (12, 2)])
 def test_exp_log_all_codes(cuda, po, cfg):
     n, es = cfg
     codes = np.arange(1 << n, dtype=np.int64)
@@ -120,7 +138,7 @@ def test_maxpool(cuda, po, cfg, geom):
     assert (host(dx) == po.maxpool2d_backward(n, es, dy, amw, x.shape)).all()
 
 
-@pytest.mark.parametrize("cfg", [(16, 1), (12, 1), (8, 0)])
+@pytest.mark.parametrize("cfg", [(16, 1), (12, 1), (8, 0), (10, 2), (12, 2)])
 def test_softmax_xent(cuda, po, cfg):
     n, es = cfg
     rng = np.random.default_rng(n + 3)
@@ -149,3 +167,43 @@ def test_sgd_step(cuda, po, fmts):
     assert (host(m) == want).all()
     assert (host(c1) == po.convert_tensor(on, oe, 8, 0, want)).all()
     assert (host(c2) == po.convert_tensor(on, oe, 12, 1, want)).all()
+
+
+@pytest.mark.parametrize("cfg", [(16, 1), (10, 2), (8, 2)])
+@pytest.mark.parametrize("scale", [0, 3, 10, -2])
+def test_softmax_xent_loss_scaled(cuda, po, cfg, scale):
+    """Loss scaling (SPEC scale_gradients): dlogits carry 2^s, the loss does not."""
+    n, es = cfg
+    rng = np.random.default_rng(n + 11 + scale)
+    B, Cn = 32, 10
+    z = np.array([[po.from_float64(n, es, v) for v in row] for row in rng.normal(0, 3, (B, Cn))], np.uint64)
+    labels = rng.integers(0, Cn, B).astype(np.int32)
+    loss, d, rows = ops.softmax_xent(cfg, dev(cfg, z), torch.from_numpy(labels).cuda(), 5,
+                                     grad_scale_log2=scale)
+    lw, dw, rw = po.softmax_xent(n, es, z, labels, 5, scale)
+    assert (host(d) == dw).all() and (host(rows) == rw).all() and int(host(loss)[0]) == lw
+    l0, _, r0 = po.softmax_xent(n, es, z, labels, 5, 0)
+    assert lw == l0 and (rw == r0).all()  # the loss itself is not scaled
+
+
+@pytest.mark.parametrize("fmts", [((12, 2), (8, 2)), ((16, 1), (12, 1))])
+@pytest.mark.parametrize("scale", [0, 4, -3])
+def test_sgd_step_scaled(cuda, po, fmts, scale):
+    (on, oe), (gn, ge) = fmts
+    rng = np.random.default_rng(17 + scale)
+    w = rand_codes(rng, on, (5000,))
+    g = rand_codes(rng, gn, (5000,))
+    lr = po.from_float64(on, oe, 1.0 / 16)
+    m = dev((on, oe), w)
+    c1 = torch.empty(5000, dtype=torch.uint8, device="cuda")
+    ops.sgd_step((on, oe), m, (gn, ge), dev((gn, ge), g), lr, copies=[((8, 2), c1)], grad_scale_log2=scale)
+    want = po.sgd(on, oe, w, gn, ge, g, lr, scale)
+    assert (host(m) == want).all()
+    assert (host(c1) == po.convert_tensor(on, oe, 8, 2, want)).all()
+
+
+def test_softmax_raw_word_needs_narrow_quire(cuda):
+    z = torch.zeros((4, 10), dtype=torch.uint16, device="cuda")
+    lab = torch.zeros(4, dtype=torch.int32, device="cuda")
+    with pytest.raises(Exception, match="128 bits"):
+        ops.softmax_xent((10, 2), z, lab, 2, raw=True)

@@ -18,7 +18,7 @@ def st_dict(st):
             for k in ("forward", "backward", "gradient", "optimizer", "loss")}
 
 
-def run_and_compare(po, model, st, x64, labels, lr, steps=1):
+def run_and_compare(po, model, st, x64, labels, lr, steps=1, grad_scale_log2=0):
     B = x64.shape[0]
     f = (st.forward.nbits, st.forward.es)
     xq = np.array([po.from_float64(*f, v) for v in x64.ravel()], np.uint64).reshape(x64.shape)
@@ -27,14 +27,15 @@ def run_and_compare(po, model, st, x64, labels, lr, steps=1):
     layers = nn.layer_description(model)
     params = [(codec.to_host(l.w.master), codec.to_host(l.b.master))
               for l in model.layers if isinstance(l, nn.Conv2d)]
-    loss_fn = nn.CrossEntropyLoss(st)
-    opt = nn.SGD(model.params(), lr, st)
+    loss_fn = nn.CrossEntropyLoss(st, grad_scale_log2=grad_scale_log2)
+    opt = nn.SGD(model.params(), lr, st, grad_scale_log2=grad_scale_log2)
     lab = torch.from_numpy(labels.astype(np.int32)).cuda()
     for step in range(steps):
         rec_gpu, rec_cpu = {}, {}
         loss = nn.train_step(model, loss_fn, opt, xd, lab, B, record=rec_gpu)
         torch.cuda.synchronize()
-        lw, params, _ = oracle_step(po, layers, st_dict(st), params, xq, labels, lr, B, rec_cpu)
+        lw, params, _ = oracle_step(po, layers, st_dict(st), params, xq, labels, lr, B, rec_cpu,
+                                    grad_scale_log2=grad_scale_log2)
         for k, v in rec_cpu.items():
             if k == "loss_rows":
                 continue
@@ -95,3 +96,28 @@ def test_config3_cifar_cnn_formats_small_batch(cuda, po):
     labels = rng.integers(0, 10, 4)
     model = nn.cifar_cnn(st, seed=5)
     run_and_compare(po, model, st, x, labels, 1.0 / 16, steps=1)
+
+
+@pytest.mark.parametrize("scale", [0, 6])
+def test_posit82_star_lenet5_loss_scaled(cuda, po, scale):
+    """The posit(8,2)* preset (O12L10: optimizer (12,2), loss (10,2), the rest
+    (8,2)) with and without loss scaling by 2^6, two steps."""
+    st = nn.StagePrecisions.posit82_star()
+    x, labels = blob_images(seed=41, n=64)
+    model = nn.lenet5(st, seed=13)
+    run_and_compare(po, model, st, x, labels, 1.0 / 16, steps=2, grad_scale_log2=scale)
+
+
+def test_loss_scaling_changes_small_gradients(cuda, po):
+    """With posit(8,2) gradients, scaling by 2^6 changes the update (small
+    gradients escape the low-precision tail) -- the point of the feature."""
+    st = nn.StagePrecisions.posit82_star()
+    x, labels = blob_images(seed=41, n=64)
+    a, b = nn.lenet5(st, seed=13), nn.lenet5(st, seed=13)
+    xd = codec.from_float64_device(x, st.forward)
+    lab = torch.from_numpy(labels.astype(np.int32)).cuda()
+    for m, s in ((a, 0), (b, 6)):
+        nn.train_step(m, nn.CrossEntropyLoss(st, s), nn.SGD(m.params(), 1 / 16, st, s), xd, lab, 64)
+    diff = sum(int((codec.to_host(p.master) != codec.to_host(q.master)).sum())
+               for p, q in zip(a.params(), b.params()))
+    assert diff > 0
