@@ -141,6 +141,12 @@ int pnn_softmax_xent_scaled(int nbits, int es, const void* logits, const int32_t
                             int64_t B, int64_t classes, int log2_batch, int grad_scale_log2,
                             void* dlogits, void* loss_rows, void* loss_out, void* raw_word,
                             void* raw_nar, void* stream);
+/* The batch-loss half of pnn_softmax_xent on its own: loss_out[0] =
+ * ldexp(round(quire sum of loss_rows[0..B)), -log2_batch).  Data-parallel
+ * training gathers the ranks' loss rows through it when the loss format's
+ * quire is wider than the 128-bit raw word (posit(10,2): W = 138). */
+int pnn_loss_reduce(int nbits, int es, const void* loss_rows, int64_t B, int log2_batch,
+                    void* loss_out, void* stream);
 int pnn_sgd_step_scaled(int opt_nbits, int opt_es, void* master, int g_nbits, int g_es,
                         const void* grad, int64_t n, uint32_t lr_code, int c1_nbits, int c1_es,
                         void* copy1, int c2_nbits, int c2_es, void* copy2, int grad_scale_log2,

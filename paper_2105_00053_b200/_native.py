@@ -60,6 +60,7 @@ _SIGS = {
                                           _vp, _vp, _vp, _vp, _vp]),
     "pnn_sgd_step_scaled": (C.c_int, [C.c_int, C.c_int, _vp, C.c_int, C.c_int, _vp, _i64, C.c_uint32,
                                       C.c_int, C.c_int, _vp, C.c_int, C.c_int, _vp, C.c_int, _vp]),
+    "pnn_loss_reduce": (C.c_int, [C.c_int, C.c_int, _vp, _i64, C.c_int, _vp, _vp]),
     "pnn_avgpool2d_fwd": (C.c_int, [C.c_int, C.c_int, _vp] + [_i64] * 4 + [C.c_int, C.c_int, C.c_int,
                                                                          C.c_uint32, _vp, _vp]),
     "pnn_avgpool2d_bwd": (C.c_int, [C.c_int, C.c_int, _vp] + [_i64] * 4 + [C.c_int, C.c_int, C.c_uint32,

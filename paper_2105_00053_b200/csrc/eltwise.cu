@@ -612,6 +612,16 @@ int pnn_softmax_xent_scaled(int nbits, int es, const void* logits, const int32_t
     return launched("softmax_xent");
 }
 
+int pnn_loss_reduce(int nbits, int es, const void* loss_rows, int64_t B, int log2_batch,
+                    void* loss_out, void* stream) {
+    CHECK_FMT(nbits, es);
+    if (B < 1 || !loss_rows || !loss_out) return set_status(PNN_EINVAL, "loss_reduce: bad arguments");
+    loss_reduce_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(make_fmt(nbits, es), bytes_of(nbits),
+                                                            loss_rows, B, log2_batch, loss_out,
+                                                            nullptr, nullptr);
+    return launched("loss_reduce");
+}
+
 int pnn_sgd_step(int opt_nbits, int opt_es, void* master, int g_nbits, int g_es, const void* grad,
                  int64_t n, uint32_t lr_code, int c1_nbits, int c1_es, void* copy1, int c2_nbits,
                  int c2_es, void* copy2, void* stream) {

@@ -101,6 +101,18 @@ def reduce_loss(loss_cfg, word, nar, global_batch: int, group=None):
                            torch.full((1,), -lb, dtype=torch.int32, device=word.device)).to(cfg.code_dtype)
 
 
+def gather_loss(loss_cfg, rows, global_batch: int, group=None):
+    """All-gather every rank's per-sample loss rows (rank order = batch
+    order) and reduce them once: the exact quire sum is order-independent, so
+    this equals the single-process loss for any rank count."""
+    full = rows
+    if group is not False and torch.distributed.is_available() and torch.distributed.is_initialized():
+        world = torch.distributed.get_world_size(group)
+        full = torch.empty((rows.numel() * world,), dtype=rows.dtype, device=rows.device)
+        torch.distributed.all_gather_into_tensor(full, rows.contiguous(), group=group)
+    return ops.loss_reduce(loss_cfg, full, int(round(math.log2(global_batch))))
+
+
 def dp_train_step(model: nn.Sequential, loss_fn: nn.CrossEntropyLoss, opt: nn.SGD, reducer: QuireAllReduce,
                   x_shard, labels_shard, global_batch: int, group=None):
     """One data-parallel SGD step on this rank's shard; returns the global loss."""
@@ -108,6 +120,9 @@ def dp_train_step(model: nn.Sequential, loss_fn: nn.CrossEntropyLoss, opt: nn.SG
     _, dz, word, nar = loss_fn(logits, labels_shard, global_batch, raw=True)
     model.backward(dz, raw=True)
     reducer.reduce()
-    loss = reduce_loss(loss_fn.st.loss, word, nar, global_batch, group)
+    if word is None:  # loss quire wider than the 128-bit raw word
+        loss = gather_loss(loss_fn.st.loss, loss_fn.rows, global_batch, group)
+    else:
+        loss = reduce_loss(loss_fn.st.loss, word, nar, global_batch, group)
     opt.step()
     return loss

@@ -215,12 +215,18 @@ class CrossEntropyLoss(Module):
         if 1 << lb != global_batch:
             raise ValueError("global batch must be a power of two (Appendix A.5)")
         z = ops.convert_tensor(logits_fwd, self.st.forward, self.st.loss)
-        out = ops.softmax_xent(self.st.loss, z, labels, lb, raw=raw,
+        # raw quire words need W <= 128; wider loss quires (posit(10,2)) hand
+        # the data-parallel path the loss rows instead (word = nar = None)
+        raw_words = raw and ops.quire_bits(self.st.loss) <= 128
+        out = ops.softmax_xent(self.st.loss, z, labels, lb, raw=raw_words,
                                grad_scale_log2=self.grad_scale_log2)
+        self.rows = out[2]
         dz = ops.convert_tensor(out[1], self.st.loss, self.st.backward)
-        if raw:
+        if raw_words:
             loss, _, rows, word, nar = out
             return loss, dz, word, nar
+        if raw:
+            return out[0], dz, None, None
         return out[0], dz
 
 

@@ -438,6 +438,22 @@ def softmax_xent(cfg, logits, labels, log2_batch: int, raw: bool = False, grad_s
     return (loss, d, rows, word, nar) if raw else (loss, d, rows)
 
 
+def loss_reduce(cfg, loss_rows, log2_batch: int):
+    """Batch loss from per-sample loss rows: ldexp(round(quire sum), -log2_batch)."""
+    cfg = _cfg(cfg)
+    rows = loss_rows.contiguous()
+    out = torch.empty((1,), dtype=rows.dtype, device=rows.device)
+    _native.check(_native.lib().pnn_loss_reduce(cfg.nbits, cfg.es, rows.data_ptr(), rows.numel(),
+                                                int(log2_batch), out.data_ptr(), _stream_ptr(rows.device)))
+    return out
+
+
+def quire_bits(cfg) -> int:
+    """W = 4R + nbits, R = (nbits - 2) << es."""
+    cfg = _cfg(cfg)
+    return 4 * ((cfg.nbits - 2) << cfg.es) + cfg.nbits
+
+
 def sgd_step(opt_cfg, master, g_cfg, grad, lr_code: int, copies=(), grad_scale_log2: int = 0):
     """SURVEY.md Appendix A.7, in place on master; copies = [(cfg, tensor), ...] (<= 2).
     grad_scale_log2 = s unscales the gradient by 2^-s in the optimizer format."""

@@ -61,3 +61,39 @@ def test_dp_train_step_world1_equals_train_step(cuda):
     assert int(codec.to_host(la)[0]) == int(codec.to_host(lb)[0])
     for p, q in zip(a.params(), b.params()):
         assert (codec.to_host(p.master) == codec.to_host(q.master)).all()
+
+
+@pytest.mark.parametrize("world", [1, 4])
+def test_posit82_star_sharded_with_loss_scaling(cuda, world):
+    """The posit(8,2)* preset: gradients go through (8,2) quire lanes; the
+    posit(10,2) loss quire (W = 138) is wider than a raw word, so the loss
+    rows are gathered and reduced once -- both equal the full-batch step."""
+    st = nn.StagePrecisions.posit82_star()
+    B, s = 64, 5
+    rng = np.random.default_rng(world + 40)
+    x = codec.from_float64_device(rng.random((B, 1, 32, 32)), st.forward)
+    labels = torch.from_numpy(rng.integers(0, 10, B).astype(np.int32)).cuda()
+    ref = nn.lenet5(st, seed=4)
+    ref_loss = nn.train_step(ref, nn.CrossEntropyLoss(st, s), nn.SGD(ref.params(), 1 / 16, st, s), x, labels, B)
+
+    reps, rows = [], []
+    lanes_sum = None
+    for r in range(world):
+        lo, hi = dp.shard_bounds(B, r, world)
+        rep = nn.lenet5(st, seed=4)
+        lf = nn.CrossEntropyLoss(st, s)
+        _, dzr, word, nar = lf(rep.forward(x[lo:hi]), labels[lo:hi], B, raw=True)
+        assert word is None and nar is None
+        rows.append(lf.rows)
+        rep.backward(dzr, raw=True)
+        lanes = [ops.quire_to_lanes(st.gradient, p.grad_words, p.grad_nar) for p in rep.params()]
+        lanes_sum = lanes if lanes_sum is None else [a + b for a, b in zip(lanes_sum, lanes)]
+        reps.append(rep)
+    rep = reps[0]
+    for p, ls in zip(rep.params(), lanes_sum):
+        p.grad = ops.lanes_to_posit(st.gradient, ls).reshape(p.master.shape)
+    nn.SGD(rep.params(), 1 / 16, st, s).step()
+    loss = dp.gather_loss(st.loss, torch.cat(rows), B, group=False)
+    assert int(codec.to_host(loss)[0]) == int(codec.to_host(ref_loss)[0])
+    for p, q in zip(ref.params(), rep.params()):
+        assert (codec.to_host(p.master) == codec.to_host(q.master)).all()
