@@ -158,12 +158,60 @@ int pnn_avgpool2d_fwd(int nbits, int es, const void* x, int64_t N, int64_t C, in
                       void* stream);
 int pnn_avgpool2d_bwd(int nbits, int es, const void* dy, int64_t N, int64_t C, int64_t H,
                       int64_t W, int k, int stride, uint32_t recip_code, void* dx, void* stream);
+
+/* ---- remaining SPEC layers ---------
+ * No reference code exists for these (placeholders); the rounding sequence of
+ * each is fixed in oracle/layers_oracle.c and reproduced bit for bit.
+ * Reductions are exact quires, so the formats they run in need W <= 128
+ * (PNN_EUNSUPPORTED otherwise); elementwise steps take formats up to 2R <= 96.
+ *
+ * Activation layers, kind 1 tanh / 2 sigmoid (posit_math.cpp:109-130):
+ * y = act(x); backward from the forward OUTPUT y (converted to dy's format b):
+ * tanh dx = dy*(1 - y*y), sigmoid dx = dy*(y*(1 - y)), each op rounded in b. */
+int pnn_act_fwd(int kind, int nbits, int es, const void* x, void* y, int64_t n, void* stream);
+int pnn_act_bwd(int kind, int f_nbits, int f_es, const void* y, int b_nbits, int b_es,
+                const void* dy, void* dx, int64_t n, void* stream);
+/* Dropout (seeded mask, scale 1/(1-p)): with s = seed + (*seed_offset if
+ * seed_offset, a DEVICE uint64, is not NULL -- a per-step counter that a
+ * captured CUDA graph advances on replay), keep element i iff
+ * (splitmix64(s ^ i*0xD1B54A32D192ED03) >> 32) >= thresh (thresh =
+ * floor(p*2^32)); y = keep ? x*scale : 0.  The backward is the same call on
+ * dy with the backward format's scale code and the same seed. */
+int pnn_dropout(int nbits, int es, const void* x, void* y, int64_t n, uint64_t seed,
+                const void* seed_offset, uint32_t thresh, uint32_t scale_code, void* stream);
+/* MSE: d = y - t; loss = round(quire sum d*d) / G;
+ * grad = ldexp(d * (2 / G), grad_scale_log2); G = global element count. */
+int pnn_mse(int nbits, int es, const void* y, const void* t, int64_t n, int64_t global_count,
+            int grad_scale_log2, void* grad, void* loss_out, void* stream);
+/* Batch normalisation over [N, C, HW] per channel (training: batch mean /
+ * biased variance by quire sums, running stats updated in the optimizer
+ * format with momentum code mom; eval: the running stats).  y = gamma*xhat +
+ * beta, xhat and inv = 1/sqrt(var + eps) saved for the backward. */
+int pnn_batchnorm_workspace(int64_t C, size_t* bytes);
+int pnn_batchnorm_fwd(int f_nbits, int f_es, const void* x, int64_t N, int64_t C, int64_t HW,
+                      const void* gamma, const void* beta, uint32_t eps_code, int training,
+                      int o_nbits, int o_es, void* run_mean, void* run_var, uint32_t mom_code,
+                      void* y, void* xhat, void* inv, void* workspace, size_t workspace_bytes,
+                      void* stream);
+/* dgamma / dbeta (gradient format, may be NULL) and/or their raw quire words
+ * (16 bytes + NaR byte per channel) for the data-parallel reduction. */
+int pnn_batchnorm_bwd(int f_nbits, int f_es, const void* xhat, const void* inv, int b_nbits,
+                      int b_es, const void* dy, int64_t N, int64_t C, int64_t HW,
+                      const void* gamma_b, int g_nbits, int g_es, void* dx, void* dgamma,
+                      void* dbeta, void* dgamma_raw, void* dgamma_nar, void* dbeta_raw,
+                      void* dbeta_nar, void* workspace, size_t workspace_bytes, void* stream);
+/* SGD with momentum in the optimizer format:
+ * g = ldexp(convert(grad), -s); v = mu*v + g; master = master - lr*v. */
+int pnn_sgd_step_momentum(int opt_nbits, int opt_es, void* master, void* velocity, int g_nbits,
+                          int g_es, const void* grad, int64_t n, uint32_t lr_code,
+                          uint32_t mu_code, int c1_nbits, int c1_es, void* copy1, int c2_nbits,
+                          int c2_es, void* copy2, int grad_scale_log2, void* stream);
 /* Data ingestion: from_float64 (posit.cpp:502-508) of device doubles into
  * packed codes -- inputs, labels-free data and initial weights. */
 int pnn_from_float64(int nbits, int es, const double* x, void* codes, int64_t n, void* stream);
 /* Scalar ALU on device (parity): op 0 add 1 sub 2 mul 3 div 4 exp 5 log
  * 6 round_to_int 7 ldexp(a, (int)b) 8 compare 9 to_int64 (low 32 bits) 10 tanh
- * 11 sigmoid (posit_math.cpp:109-130). */
+ * 11 sigmoid (posit_math.cpp:109-130) 12 sqrt (posit_math.cpp:132-160). */
 int pnn_scalar_eval(int nbits, int es, int op, const uint32_t* a, const uint32_t* b,
                     uint32_t* out, int64_t n, void* stream);
 

@@ -76,6 +76,7 @@ class _Base:
             ("log", C.c_uint64, [C.c_int, C.c_int, C.c_uint64]),
             ("tanh", C.c_uint64, [C.c_int, C.c_int, C.c_uint64]),
             ("sigmoid", C.c_uint64, [C.c_int, C.c_int, C.c_uint64]),
+            ("sqrt", C.c_uint64, [C.c_int, C.c_int, C.c_uint64]),
             ("quire_new", C.c_void_p, [C.c_int, C.c_int]),
             ("quire_free", None, [C.c_void_p]),
             ("quire_clear", None, [C.c_void_p]),
@@ -130,6 +131,9 @@ class _Base:
 
     def sigmoid(self, n, es, code):
         return self._f("sigmoid")(n, es, int(code))
+
+    def sqrt(self, n, es, code):
+        return self._f("sqrt")(n, es, int(code))
 
     def avgpool2d(self, n, es, x, k, stride, use_quire, recip):
         x = _codes(x)
@@ -394,6 +398,67 @@ class Restatement(_Base):
                   "convert_tensor")
         y[...] = yf.reshape(x.shape)
         return y
+
+
+    # ---- remaining SPEC layers (layers_oracle.c) ----
+    def act_fwd(self, kind, n, es, x):
+        x = _codes(x)
+        y = np.zeros(x.shape, np.uint64)
+        self.lib.po_act_fwd(int(kind), n, es, _p(x), _p(y), i64(x.size))
+        return y
+
+    def act_bwd(self, kind, f, y, b, dy):
+        y, dy = _codes(y), _codes(dy)
+        dx = np.zeros(dy.shape, np.uint64)
+        self.lib.po_act_bwd(int(kind), *f, _p(y), *b, _p(dy), _p(dx), i64(dy.size))
+        return dx
+
+    def dropout_bits(self, seed, i):
+        self.lib.po_dropout_bits.restype = C.c_uint64
+        return self.lib.po_dropout_bits(C.c_uint64(int(seed)), i64(int(i)))
+
+    def dropout(self, n, es, x, seed, thresh, scale):
+        x = _codes(x)
+        y = np.zeros(x.shape, np.uint64)
+        self.lib.po_dropout(n, es, _p(x), _p(y), i64(x.size), C.c_uint64(int(seed)),
+                            C.c_uint32(int(thresh)), C.c_uint64(int(scale)))
+        return y
+
+    def mse(self, n, es, y, t, global_count, grad_scale_log2=0):
+        y, t = _codes(y), _codes(t)
+        g = np.zeros(y.shape, np.uint64)
+        self.lib.po_mse.restype = C.c_uint64
+        loss = self.lib.po_mse(n, es, _p(y), _p(t), i64(y.size), i64(int(global_count)),
+                               int(grad_scale_log2), _p(g))
+        return int(loss), g
+
+    def batchnorm_fwd(self, f, x, gamma, beta, eps, training, o, run_mean, run_var, mom):
+        x = _codes(x)
+        N, Cc = x.shape[:2]
+        HW = int(np.prod(x.shape[2:], dtype=np.int64)) if x.ndim > 2 else 1
+        rm, rv = _codes(run_mean).copy(), _codes(run_var).copy()
+        y, xh = np.zeros(x.shape, np.uint64), np.zeros(x.shape, np.uint64)
+        inv = np.zeros(Cc, np.uint64)
+        self.lib.po_batchnorm_fwd(*f, _p(x), i64(N), i64(Cc), i64(HW), _p(_codes(gamma)), _p(_codes(beta)),
+                                  C.c_uint64(int(eps)), int(training), *o, _p(rm), _p(rv),
+                                  C.c_uint64(int(mom)), _p(y), _p(xh), _p(inv))
+        return y, xh, inv, rm, rv
+
+    def batchnorm_bwd(self, f, xhat, inv, b, dy, gamma_b, g):
+        xhat, dy = _codes(xhat), _codes(dy)
+        N, Cc = dy.shape[:2]
+        HW = int(np.prod(dy.shape[2:], dtype=np.int64)) if dy.ndim > 2 else 1
+        dx = np.zeros(dy.shape, np.uint64)
+        dgm, dbt = np.zeros(Cc, np.uint64), np.zeros(Cc, np.uint64)
+        self.lib.po_batchnorm_bwd(*f, _p(xhat), _p(_codes(inv)), *b, _p(dy), i64(N), i64(Cc), i64(HW),
+                                  _p(_codes(gamma_b)), *g, _p(dx), _p(dgm), _p(dbt))
+        return dx, dgm, dbt
+
+    def sgd_momentum(self, o, w, v, g_fmt, g, lr, mu, grad_scale_log2=0):
+        w, v, g = _codes(w).copy(), _codes(v).copy(), _codes(g)
+        self.lib.po_sgd_momentum(*o, _p(w), _p(v), *g_fmt, _p(g), i64(w.size), C.c_uint64(int(lr)),
+                                 C.c_uint64(int(mu)), int(grad_scale_log2))
+        return w, v
 
 
 class Reference(_Base):

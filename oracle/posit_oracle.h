@@ -147,6 +147,27 @@ uint64_t po_softmax_xent_scaled(int nbits, int es, const uint64_t* logits, const
 void po_sgd_scaled(int opt_nbits, int opt_es, uint64_t* w, int g_nbits, int g_es,
                    const uint64_t* g, int64_t n, uint64_t lr, int grad_scale_log2);
 
+/* ---- remaining SPEC layers (layers_oracle.c; semantics written there) ---- */
+uint64_t po_sqrt(int nbits, int es, uint64_t x); /* posit_math.cpp:132-160 */
+void po_act_fwd(int kind, int nbits, int es, const uint64_t* x, uint64_t* y, int64_t n);
+void po_act_bwd(int kind, int fn, int fe, const uint64_t* y, int bn, int be, const uint64_t* dy,
+                uint64_t* dx, int64_t n);
+uint64_t po_dropout_bits(uint64_t seed, int64_t i);
+void po_dropout(int nbits, int es, const uint64_t* x, uint64_t* y, int64_t n, uint64_t seed,
+                uint32_t thresh, uint64_t scale);
+uint64_t po_mse(int nbits, int es, const uint64_t* y, const uint64_t* t, int64_t n, int64_t G,
+                int grad_scale_log2, uint64_t* grad);
+void po_batchnorm_fwd(int fn, int fe, const uint64_t* x, int64_t N, int64_t C, int64_t HW,
+                      const uint64_t* gamma, const uint64_t* beta, uint64_t eps, int training,
+                      int on, int oe, uint64_t* run_mean, uint64_t* run_var, uint64_t mom,
+                      uint64_t* y, uint64_t* xhat, uint64_t* inv_out);
+void po_batchnorm_bwd(int fn, int fe, const uint64_t* xhat, const uint64_t* inv, int bn, int be,
+                      const uint64_t* dy, int64_t N, int64_t C, int64_t HW,
+                      const uint64_t* gamma_b, int gn, int ge, uint64_t* dx, uint64_t* dgamma,
+                      uint64_t* dbeta);
+void po_sgd_momentum(int on, int oe, uint64_t* w, uint64_t* v, int gn, int ge, const uint64_t* grad,
+                     int64_t n, uint64_t lr, uint64_t mu, int grad_scale_log2);
+
 #ifdef __cplusplus
 }
 #endif

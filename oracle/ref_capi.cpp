@@ -149,6 +149,10 @@ uint64_t ref_sigmoid(int nbits, int es, uint64_t code) {
     return sigmoid_posit(PositValue{cfg_of(nbits, es), code}).bits;
 }
 
+uint64_t ref_sqrt(int nbits, int es, uint64_t code) {
+    return sqrt_posit(PositValue{cfg_of(nbits, es), code}).bits;
+}
+
 uint64_t ref_from_int64(int nbits, int es, int64_t v) {
     return from_int64(v, cfg_of(nbits, es)).bits;
 }

@@ -12,8 +12,9 @@ softmax cross-entropy, SGD) restated in the same C file.
 A layer description is a list of tuples:
     ("conv", cin, cout, k, stride, pad, first_layer)   ("linear", fin, fout, first_layer)
     ("relu",)   ("pool", k, stride)   ("flatten",)
+    ("tanh",)  ("sigmoid",)  ("avgpool", k, stride)  ("dropout", p, seed)  ("bn", training)
 Params are host uint64 code arrays in the optimizer format, one (w, b) pair
-per conv / linear, in order.
+per conv / linear (and one (gamma, beta) pair per bn), in order.
 """
 from __future__ import annotations
 
@@ -39,12 +40,28 @@ def _cv(po, src, dst, x):
     return po.convert_tensor(*src, *dst, x)
 
 
-def oracle_step(po, layers, st, params, x, labels, lr, global_batch, record=None, grad_scale_log2=0):
+def _onehot(po, lf, labels, classes):
+    one = po.from_float64(*lf, 1.0)
+    t = np.zeros((len(labels), classes), np.uint64)
+    t[np.arange(len(labels)), labels] = one
+    return t
+
+
+def oracle_step(po, layers, st, params, x, labels, lr, global_batch, record=None, grad_scale_log2=0,
+                state=None, loss="xent", momentum=0.0, velocity=None):
     """One SGD step.  st = dict(forward, backward, gradient, optimizer, loss) of
     (nbits, es); x = input codes in the forward format; returns (loss_code,
     new_params, grads) and fills ``record`` (if given) with every activation
     and gradient, keyed like the GPU model's recording.  grad_scale_log2 = s:
-    loss scaling by 2^s (dlogits carry 2^s, SGD unscales)."""
+    loss scaling by 2^s (dlogits carry 2^s, SGD unscales).
+
+    §8f.2 layers (rounding sequences in oracle/layers_oracle.c):
+    ("tanh",) ("sigmoid",) ("avgpool", k, stride) ("dropout", p, seed or None
+    in eval) ("bn", training) -- a bn layer owns a (gamma, beta) params pair
+    and ``state[layer index] = [running_mean, running_var]`` (updated in
+    place).  loss: "xent" (softmax cross-entropy) or "mse" (one-hot targets).
+    momentum != 0: ``velocity`` = one [vw, vb] list per params pair, updated
+    in place (SGD with momentum)."""
     f, b, g, o, lf = (tuple(st[k]) for k in ("forward", "backward", "gradient", "optimizer", "loss"))
     lb = int(round(math.log2(global_batch)))
     rec = record if record is not None else {}
@@ -77,14 +94,42 @@ def oracle_step(po, layers, st, params, x, labels, lr, global_batch, record=None
         elif kind == "flatten":
             caches.append(("flatten", h.shape))
             h = h.reshape(h.shape[0], -1)
+        elif kind in ("tanh", "sigmoid"):
+            h = po.act_fwd(1 if kind == "tanh" else 2, *f, h)
+            caches.append((kind, h))
+        elif kind == "avgpool":
+            _, k, s = L
+            caches.append(("avgpool", h.shape, k, s))
+            h = po.avgpool2d(*f, h, k, s, True, po.from_float64(*f, 1.0 / (k * k)))
+        elif kind == "dropout":
+            _, p, seed = L
+            if seed is None:
+                caches.append(("dropout", None, None))
+            else:
+                thresh = int(p * 4294967296.0)
+                caches.append(("dropout", seed, thresh, p))
+                h = po.dropout(*f, h, seed, thresh, po.from_float64(*f, 1.0 / (1.0 - p)))
+        elif kind == "bn":
+            gamma, beta = params[pi]
+            rs = state[li]
+            y, xh, inv, rm, rv = po.batchnorm_fwd(
+                f, h, _cv(po, o, f, gamma), _cv(po, o, f, beta), po.from_float64(*f, 1e-5), L[1], o,
+                rs[0], rs[1], po.from_float64(*o, 0.1))
+            rs[0], rs[1] = rm, rv
+            caches.append(("bn", pi, gamma, xh, inv))
+            pi += 1
+            h = y
         rec[f"act{li}"] = h
     z = _cv(po, f, lf, h)
-    loss, d, rows = po.softmax_xent(*lf, z, labels, lb, grad_scale_log2)
-    rec["loss_rows"] = rows
+    if loss == "mse":
+        Bn, classes = z.shape
+        lw, d = po.mse(*lf, z, _onehot(po, lf, labels, classes), global_batch * classes, grad_scale_log2)
+    else:
+        lw, d, rows = po.softmax_xent(*lf, z, labels, lb, grad_scale_log2)
+        rec["loss_rows"] = rows
     dy = _cv(po, lf, b, d)
     rec["dlogits"] = dy
     grads = [None] * len(params)
-    pi = len(params)
     for li in range(len(layers) - 1, -1, -1):
         c = caches[li]
         kind = c[0]
@@ -108,13 +153,34 @@ def oracle_step(po, layers, st, params, x, labels, lr, global_batch, record=None
             dy = po.maxpool2d_backward(*b, dy, c[2], c[1])
         elif kind == "flatten":
             dy = dy.reshape(c[1])
+        elif kind in ("tanh", "sigmoid"):
+            dy = po.act_bwd(1 if kind == "tanh" else 2, f, c[1], b, dy)
+        elif kind == "avgpool":
+            _, shape, k, s = c
+            dy = po.avgpool2d_backward(*b, dy, k, s, shape, po.from_float64(*b, 1.0 / (k * k)))
+        elif kind == "dropout":
+            if c[1] is not None:
+                dy = po.dropout(*b, dy, c[1], c[2], po.from_float64(*b, 1.0 / (1.0 - c[3])))
+        elif kind == "bn":
+            _, bpi, gamma, xh, inv = c
+            pi = bpi
+            dy, dgm, dbt = po.batchnorm_bwd(f, xh, inv, b, dy, _cv(po, o, b, gamma), g)
+            grads[bpi] = (dgm, dbt)
+            rec[f"grad_w{bpi}"], rec[f"grad_b{bpi}"] = dgm, dbt
         rec[f"dact{li}"] = dy
     lr_code = po.from_float64(*o, lr)
     new_params = []
-    for (w, bias), (dw, db) in zip(params, grads):
-        new_params.append((po.sgd(*o, w, *g, dw, lr_code, grad_scale_log2),
-                           po.sgd(*o, bias, *g, db, lr_code, grad_scale_log2)))
-    return loss, new_params, grads
+    if momentum:
+        mu = po.from_float64(*o, momentum)
+        for i, ((w, bias), (dw, db)) in enumerate(zip(params, grads)):
+            w2, velocity[i][0] = po.sgd_momentum(o, w, velocity[i][0], g, dw, lr_code, mu, grad_scale_log2)
+            b2, velocity[i][1] = po.sgd_momentum(o, bias, velocity[i][1], g, db, lr_code, mu, grad_scale_log2)
+            new_params.append((w2, b2))
+    else:
+        for (w, bias), (dw, db) in zip(params, grads):
+            new_params.append((po.sgd(*o, w, *g, dw, lr_code, grad_scale_log2),
+                               po.sgd(*o, bias, *g, db, lr_code, grad_scale_log2)))
+    return lw, new_params, grads
 
 
 def blob_images(seed: int, n: int, classes: int = 10, shape=(1, 32, 32), sigma: float = 0.3):

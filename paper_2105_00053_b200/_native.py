@@ -61,6 +61,21 @@ _SIGS = {
     "pnn_sgd_step_scaled": (C.c_int, [C.c_int, C.c_int, _vp, C.c_int, C.c_int, _vp, _i64, C.c_uint32,
                                       C.c_int, C.c_int, _vp, C.c_int, C.c_int, _vp, C.c_int, _vp]),
     "pnn_loss_reduce": (C.c_int, [C.c_int, C.c_int, _vp, _i64, C.c_int, _vp, _vp]),
+    "pnn_act_fwd": (C.c_int, [C.c_int, C.c_int, C.c_int, _vp, _vp, _i64, _vp]),
+    "pnn_act_bwd": (C.c_int, [C.c_int, C.c_int, C.c_int, _vp, C.c_int, C.c_int, _vp, _vp, _i64, _vp]),
+    "pnn_dropout": (C.c_int, [C.c_int, C.c_int, _vp, _vp, _i64, C.c_uint64, _vp, C.c_uint32, C.c_uint32,
+                              _vp]),
+    "pnn_mse": (C.c_int, [C.c_int, C.c_int, _vp, _vp, _i64, _i64, C.c_int, _vp, _vp, _vp]),
+    "pnn_batchnorm_workspace": (C.c_int, [_i64, C.POINTER(C.c_size_t)]),
+    "pnn_batchnorm_fwd": (C.c_int, [C.c_int, C.c_int, _vp, _i64, _i64, _i64, _vp, _vp, C.c_uint32, C.c_int,
+                                    C.c_int, C.c_int, _vp, _vp, C.c_uint32, _vp, _vp, _vp, _vp, C.c_size_t,
+                                    _vp]),
+    "pnn_batchnorm_bwd": (C.c_int, [C.c_int, C.c_int, _vp, _vp, C.c_int, C.c_int, _vp, _i64, _i64, _i64, _vp,
+                                    C.c_int, C.c_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, C.c_size_t,
+                                    _vp]),
+    "pnn_sgd_step_momentum": (C.c_int, [C.c_int, C.c_int, _vp, _vp, C.c_int, C.c_int, _vp, _i64, C.c_uint32,
+                                        C.c_uint32, C.c_int, C.c_int, _vp, C.c_int, C.c_int, _vp, C.c_int,
+                                        _vp]),
     "pnn_avgpool2d_fwd": (C.c_int, [C.c_int, C.c_int, _vp] + [_i64] * 4 + [C.c_int, C.c_int, C.c_int,
                                                                          C.c_uint32, _vp, _vp]),
     "pnn_avgpool2d_bwd": (C.c_int, [C.c_int, C.c_int, _vp] + [_i64] * 4 + [C.c_int, C.c_int, C.c_uint32,

@@ -12,28 +12,11 @@
 #include <cstdint>
 
 #include "../../include/pnn_b200.h"
+#include "eltwise_common.cuh"
 #include "posit_scalar.cuh"
 #include "status.h"
 
 namespace pnn_b200 {
-
-template <typename T>
-__device__ __forceinline__ uint32_t ld_code(const void* p, int64_t i) {
-    return uint32_t(static_cast<const T*>(p)[i]);
-}
-
-__device__ __forceinline__ uint32_t load_any(const void* p, int64_t i, int bytes) {
-    return bytes == 1 ? uint32_t(static_cast<const uint8_t*>(p)[i])
-                      : uint32_t(static_cast<const uint16_t*>(p)[i]);
-}
-__device__ __forceinline__ void store_any(void* p, int64_t i, int bytes, uint32_t c) {
-    if (bytes == 1) static_cast<uint8_t*>(p)[i] = uint8_t(c);
-    else static_cast<uint16_t*>(p)[i] = uint16_t(c);
-}
-
-#define GRID_STRIDE(i, n)                                                        \
-    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < (n); \
-         i += int64_t(gridDim.x) * blockDim.x)
 
 __global__ void convert_kernel(PositFmt s, int sb, const void* src, PositFmt d, int db, void* dst,
                                int64_t n) {
@@ -441,6 +424,7 @@ __global__ void scalar_eval_kernel(PositFmt f, int op, const uint32_t* a, const 
             case 8: r = uint32_t(p_compare(f, x, y)); break;
             case 10: r = p_tanh(f, x); break;
             case 11: r = p_sigmoid(f, x); break;
+            case 12: r = p_sqrt(f, x); break;
             default: r = uint32_t(p_to_int64(f, x)); break;
         }
         out[i] = r;

@@ -312,4 +312,29 @@ static __device__ __noinline__ uint32_t p_sigmoid(const PositFmt& f, uint32_t x)
     return p_div(f, t, p_add(f, one, t));
 }
 
+// sqrt_posit, posit_math.cpp:132-160: correctly rounded.  value = M * 2^(2q)
+// with M = sig << j in [2^126, 2^128); the floor root r in [2^63, 2^64) and
+// its remainder are unique, found here by the restoring (digit-by-digit)
+// method; sticky = remainder != 0.
+static __device__ __noinline__ uint32_t p_sqrt(const PositFmt& f, uint32_t x) {
+    x &= code_mask(f);
+    if (x == 0 || x == nar_of(f)) return x;
+    if (x & nar_of(f)) return nar_of(f);
+    const Unp u = unpack(f, x);
+    const int j = (u.scale & 1) == 0 ? 63 : 64;
+    const unsigned __int128 M = (unsigned __int128)u.sig << j;
+    const int q = (u.scale - 63 - j) / 2;
+    unsigned __int128 rem = 0, root = 0;
+    for (int i = 63; i >= 0; --i) {
+        rem = (rem << 2) | ((M >> (2 * i)) & 3);
+        const unsigned __int128 t = (root << 2) | 1;
+        root <<= 1;
+        if (rem >= t) {
+            rem -= t;
+            root |= 1;
+        }
+    }
+    return pack_round(f, false, q + 63, uint64_t(root), rem != 0);
+}
+
 }  // namespace pnn_b200

@@ -188,6 +188,126 @@ class MaxPool2d(Module):
                                       self.stride)
 
 
+class _Act(Module):
+    kind = 0
+
+    def __init__(self, st: StagePrecisions):
+        self.st = st
+        self.y = None
+
+    def forward(self, x):
+        self.y = ops.act_fwd(self.kind, self.st.forward, x)
+        return self.y
+
+    def backward(self, dy, raw=False):
+        return ops.act_bwd(self.kind, self.st.forward, self.y, self.st.backward, dy)
+
+
+class Tanh(_Act):
+    """tanh_posit layer (posit_math.cpp:109-118); backward dy*(1 - y*y) in p_backward."""
+    kind = ops.ACT_TANH
+
+
+class Sigmoid(_Act):
+    """sigmoid_posit layer (posit_math.cpp:120-130); backward dy*(y*(1 - y))."""
+    kind = ops.ACT_SIGMOID
+
+
+class AvgPool2d(Module):
+    """avgpool2d / avgpool2d_backward (tensor_ops.cpp:672-720), quire window
+    sum times 1/k^2 quantised in the forward / backward format."""
+
+    def __init__(self, k, st: StagePrecisions, stride=None):
+        from .codec import from_float64_array
+
+        self.k, self.stride, self.st = k, stride or k, st
+        r = np.array([1.0 / (k * k)])
+        self.recip_f = int(from_float64_array(r, st.forward)[0])
+        self.recip_b = int(from_float64_array(r, st.backward)[0])
+        self.x_shape = None
+
+    def forward(self, x):
+        self.x_shape = x.shape
+        return ops.avgpool2d(self.st.forward, x, self.k, self.stride, True, self.recip_f)
+
+    def backward(self, dy, raw=False):
+        return ops.avgpool2d_backward(self.st.backward, dy, self.k, self.stride, self.x_shape,
+                                      self.recip_b)
+
+
+class Dropout(Module):
+    """Seeded dropout: the mask of step t uses seed + t, t a
+    device counter advanced after every training forward (so a captured CUDA
+    graph draws a fresh mask per replay); identity in eval mode."""
+
+    def __init__(self, p, st: StagePrecisions, seed=0, device="cuda"):
+        from .codec import from_float64_array
+
+        self.p, self.st, self.seed = p, st, int(seed)
+        self.thresh = ops.dropout_threshold(p)
+        s = np.array([1.0 / (1.0 - p)])
+        self.scale_f = int(from_float64_array(s, st.forward)[0])
+        self.scale_b = int(from_float64_array(s, st.backward)[0])
+        self.counter = torch.zeros((1,), dtype=torch.int64, device=device)
+        self.cur = None
+        self.used = False
+
+    def forward(self, x):
+        if not self.training:
+            self.used = False
+            return x
+        self.cur = self.counter.clone()
+        self.counter.add_(1)
+        self.used = True
+        return ops.dropout(self.st.forward, x, self.seed, self.thresh, self.scale_f, self.cur)
+
+    def backward(self, dy, raw=False):
+        if not self.used:
+            return dy
+        return ops.dropout(self.st.backward, dy, self.seed, self.thresh, self.scale_b, self.cur)
+
+
+class BatchNorm2d(Module):
+    """Per-channel batch normalisation (rounding sequence in
+    oracle/layers_oracle.c): gamma / beta are MixedParams (master in
+    p_optimizer), running mean / variance live in p_optimizer.  Works on
+    [N, C, H, W] and on [N, C] (BatchNorm1d after a Linear)."""
+
+    def __init__(self, C, st: StagePrecisions, eps=1e-5, momentum=0.1, device="cuda"):
+        from .codec import from_float64_array
+
+        self.C, self.st = C, st
+        dt = st.optimizer.np_code_dtype
+        one = from_float64_array(np.ones(C), st.optimizer).astype(dt)
+        self.gamma = MixedParam(torch.from_numpy(one).to(device), st)
+        self.beta = MixedParam(torch.zeros((C,), dtype=st.optimizer.code_dtype, device=device), st)
+        self.running_mean = torch.zeros((C,), dtype=st.optimizer.code_dtype, device=device)
+        self.running_var = torch.from_numpy(one.copy()).to(device)
+        self.eps_code = int(from_float64_array(np.array([eps]), st.forward)[0])
+        self.mom_code = int(from_float64_array(np.array([momentum]), st.optimizer)[0])
+        self.xhat = self.inv = None
+
+    def params(self):
+        return [self.gamma, self.beta]
+
+    def forward(self, x):
+        f = self.st.forward
+        y, self.xhat, self.inv = ops.batchnorm_fwd(f, x, self.gamma.as_(f), self.beta.as_(f), self.eps_code,
+                                                   self.training, self.st.optimizer, self.running_mean,
+                                                   self.running_var, self.mom_code)
+        return y
+
+    def backward(self, dy, raw=False):
+        st = self.st
+        out = ops.batchnorm_bwd(st.forward, self.xhat, self.inv, st.backward, dy,
+                                self.gamma.as_(st.backward), st.gradient, raw=raw)
+        if raw:
+            dx, (self.gamma.grad_words, self.gamma.grad_nar), (self.beta.grad_words, self.beta.grad_nar) = out
+        else:
+            dx, self.gamma.grad, self.beta.grad = out
+        return dx
+
+
 class Flatten(Module):
     def __init__(self):
         self.shape = None
@@ -230,9 +350,47 @@ class CrossEntropyLoss(Module):
         return out[0], dz
 
 
+class MSELoss(Module):
+    """Mean squared error against one-hot targets in p_loss (SPEC.md:342-344;
+    rounding sequence in oracle/layers_oracle.c): loss = sum (z - t)^2 / G,
+    dlogits = (z - t) * (2 / G) with G = global batch x classes."""
+
+    def __init__(self, st: StagePrecisions, grad_scale_log2: int = 0):
+        self.st = st
+        self.grad_scale_log2 = int(grad_scale_log2)
+        self._onehot = {}
+
+    def targets(self, labels, classes: int):
+        from .codec import from_float64_array
+
+        key = (classes, labels.device)
+        if key not in self._onehot:
+            one = int(from_float64_array(np.array([1.0]), self.st.loss)[0])
+            self._onehot[key] = torch.tensor([0, one], dtype=torch.int64, device=labels.device)
+        return self._onehot[key][torch.nn.functional.one_hot(labels.long(), classes)].to(
+            self.st.loss.code_dtype)
+
+    def __call__(self, logits_fwd, labels, global_batch: int, raw=False):
+        if raw:
+            raise NotImplementedError("MSELoss has no data-parallel (raw) mode")
+        B, classes = logits_fwd.shape
+        z = ops.convert_tensor(logits_fwd, self.st.forward, self.st.loss)
+        loss, g = ops.mse(self.st.loss, z, self.targets(labels, classes), global_batch * classes,
+                          self.grad_scale_log2)
+        return loss, ops.convert_tensor(g, self.st.loss, self.st.backward)
+
+
 class Sequential(Module):
     def __init__(self, *layers):
         self.layers = list(layers)
+
+    def train(self, mode: bool = True):
+        for l in self.layers:
+            l.training = mode
+        return self
+
+    def eval(self):
+        return self.train(False)
 
     def params(self):
         return [p for l in self.layers for p in l.params()]
@@ -258,21 +416,30 @@ class SGD:
     """master = sub(master, mul(lr, convert(grad -> p_opt))), copies refreshed
     (Appendix A.7; momentum 0)."""
 
-    def __init__(self, params, lr: float, st: StagePrecisions, grad_scale_log2: int = 0):
+    def __init__(self, params, lr: float, st: StagePrecisions, grad_scale_log2: int = 0,
+                 momentum: float = 0.0):
         from .codec import from_float64_array
 
         self.params = params
         self.st = st
         self.grad_scale_log2 = int(grad_scale_log2)
+        self.momentum = float(momentum)
+        if self.momentum:
+            self.mu_code = int(from_float64_array(np.array([momentum]), st.optimizer)[0])
+            self.velocity = [torch.zeros_like(p.master) for p in params]
         self.lr_code = int(from_float64_array(np.array([lr]), st.optimizer)[0])
 
     def step(self):
         st = self.st
-        for p in self.params:
+        for i, p in enumerate(self.params):
             fmts = p.stage_formats()
             fused = [(c, p.copies[c]) for c in fmts[:2]]  # refreshed inside the SGD kernel
-            ops.sgd_step(st.optimizer, p.master, st.gradient, p.grad, self.lr_code, fused,
-                         grad_scale_log2=self.grad_scale_log2)
+            if self.momentum:
+                ops.sgd_step_momentum(st.optimizer, p.master, self.velocity[i], st.gradient, p.grad,
+                                      self.lr_code, self.mu_code, fused, self.grad_scale_log2)
+            else:
+                ops.sgd_step(st.optimizer, p.master, st.gradient, p.grad, self.lr_code, fused,
+                             grad_scale_log2=self.grad_scale_log2)
             for c in fmts[2:]:
                 p.copies[c] = ops.convert_tensor(p.master, st.optimizer, c)
 
@@ -301,6 +468,33 @@ def cifar_cnn(st: StagePrecisions, seed: int = 0, device="cuda") -> Sequential:
         Conv2d(64, 64, 3, st, pad=1, rng=rng, device=device), ReLU(st), MaxPool2d(2, st),
         Flatten(), Linear(4096, 512, st, rng=rng, device=device), ReLU(st),
         Linear(512, 10, st, rng=rng, device=device))
+
+
+def lenet5_classic(st: StagePrecisions, seed: int = 0, device="cuda") -> Sequential:
+    """The original LeNet-5 activations (SPEC Fig. 2 layer set): tanh and
+    average pooling, sigmoid before the classifier."""
+    rng = np.random.default_rng(seed)
+    return Sequential(
+        Conv2d(1, 6, 5, st, rng=rng, first_layer=True, device=device), Tanh(st), AvgPool2d(2, st),
+        Conv2d(6, 16, 5, st, rng=rng, device=device), Tanh(st), AvgPool2d(2, st), Flatten(),
+        Linear(400, 120, st, rng=rng, device=device), Tanh(st),
+        Linear(120, 84, st, rng=rng, device=device), Sigmoid(st),
+        Linear(84, 10, st, rng=rng, device=device))
+
+
+def cnn_bn_dropout(st: StagePrecisions, seed: int = 0, device="cuda", hw: int = 32) -> Sequential:
+    """A CIFAR-shape CNN (hw x hw inputs) with batch normalisation (2-D and
+    1-D) and dropout."""
+    rng = np.random.default_rng(seed)
+    return Sequential(
+        Conv2d(3, 32, 3, st, pad=1, rng=rng, first_layer=True, device=device), BatchNorm2d(32, st, device=device),
+        ReLU(st), MaxPool2d(2, st),
+        Conv2d(32, 32, 3, st, pad=1, rng=rng, device=device), BatchNorm2d(32, st, device=device), ReLU(st),
+        MaxPool2d(2, st), Flatten(),
+        Linear(32 * (hw // 4) ** 2, 64, st, rng=rng, device=device), BatchNorm2d(64, st, device=device),
+        ReLU(st),
+        Dropout(0.25, st, seed=seed + 1, device=device),
+        Linear(64, 10, st, rng=rng, device=device))
 
 
 def train_step(model: Sequential, loss_fn: CrossEntropyLoss, opt: SGD, x_fwd, labels,
@@ -367,4 +561,18 @@ def layer_description(model: Sequential):
             out.append(("pool", l.k, l.stride))
         elif isinstance(l, Flatten):
             out.append(("flatten",))
+        elif isinstance(l, Tanh):
+            out.append(("tanh",))
+        elif isinstance(l, Sigmoid):
+            out.append(("sigmoid",))
+        elif isinstance(l, AvgPool2d):
+            out.append(("avgpool", l.k, l.stride))
+        elif isinstance(l, Dropout):
+            # the seed the NEXT training forward will use
+            step = int(l.counter.item()) if l.training else None
+            out.append(("dropout", l.p, None if step is None else l.seed + step))
+        elif isinstance(l, BatchNorm2d):
+            out.append(("bn", l.training))
+        else:
+            raise TypeError(f"no oracle description for {type(l).__name__}")
     return out

@@ -528,3 +528,134 @@ def avgpool2d_backward(cfg, dy, k: int, stride: int, x_shape, recip_bits: int, p
     _native.check(_native.lib().pnn_avgpool2d_bwd(cfg.nbits, cfg.es, dy.contiguous().data_ptr(), N, Cc, H, W, k,
                                                   stride, int(recip_bits), dx.data_ptr(), _stream_ptr(dy.device)))
     return dx
+
+
+# ---- remaining SPEC layers (csrc/layers.cu) ---------------
+
+ACT_TANH, ACT_SIGMOID = 1, 2
+
+
+def act_fwd(kind: int, cfg, x):
+    """y = tanh_posit / sigmoid_posit (x) elementwise (posit_math.cpp:109-130)."""
+    cfg = _cfg(cfg)
+    x = x.contiguous()
+    y = torch.empty_like(x)
+    _native.check(_native.lib().pnn_act_fwd(int(kind), cfg.nbits, cfg.es, x.data_ptr(), y.data_ptr(),
+                                            x.numel(), _stream_ptr(x.device)))
+    return y
+
+
+def act_bwd(kind: int, f_cfg, y, b_cfg, dy):
+    """dx from the forward output y: tanh dy*(1-y*y), sigmoid dy*(y*(1-y)), in b."""
+    fc, bc = _cfg(f_cfg), _cfg(b_cfg)
+    y, dy = y.contiguous(), dy.contiguous()
+    if y.numel() != dy.numel():
+        raise _native.PnnInvalidArgument(1, "act_bwd: shape mismatch")
+    dx = torch.empty_like(dy)
+    _native.check(_native.lib().pnn_act_bwd(int(kind), fc.nbits, fc.es, y.data_ptr(), bc.nbits, bc.es,
+                                            dy.data_ptr(), dx.data_ptr(), dy.numel(), _stream_ptr(dy.device)))
+    return dx
+
+
+def dropout_threshold(p: float) -> int:
+    """floor(p * 2^32): element kept iff its 32 mask bits are >= this."""
+    if not (0.0 <= p < 1.0):
+        raise ValueError("dropout probability must be in [0, 1)")
+    return int(p * 4294967296.0)
+
+
+def dropout(cfg, x, seed: int, thresh: int, scale_code: int, seed_offset=None):
+    """y = keep(seed [+ *seed_offset], i) ? x * scale : 0 (the backward: same call
+    on dy).  seed_offset: optional device int64 [1] step counter."""
+    cfg = _cfg(cfg)
+    x = x.contiguous()
+    y = torch.empty_like(x)
+    _native.check(_native.lib().pnn_dropout(cfg.nbits, cfg.es, x.data_ptr(), y.data_ptr(), x.numel(),
+                                            int(seed) & ((1 << 64) - 1),
+                                            seed_offset.data_ptr() if seed_offset is not None else None,
+                                            int(thresh), int(scale_code), _stream_ptr(x.device)))
+    return y
+
+
+def mse(cfg, y, t, global_count: int, grad_scale_log2: int = 0):
+    """-> (loss code tensor [1], grad): loss = sum (y-t)^2 / G, grad = ldexp((y-t)*(2/G), s)."""
+    cfg = _cfg(cfg)
+    y, t = y.contiguous(), t.contiguous()
+    if y.numel() != t.numel():
+        raise _native.PnnInvalidArgument(1, "mse: shape mismatch")
+    g = torch.empty_like(y)
+    loss = torch.empty((1,), dtype=y.dtype, device=y.device)
+    _native.check(_native.lib().pnn_mse(cfg.nbits, cfg.es, y.data_ptr(), t.data_ptr(), y.numel(),
+                                        int(global_count), int(grad_scale_log2), g.data_ptr(),
+                                        loss.data_ptr(), _stream_ptr(y.device)))
+    return loss, g
+
+
+def _bn_shape(x):
+    N, Cc = int(x.shape[0]), int(x.shape[1])
+    HW = int(x.numel() // max(N * Cc, 1))
+    return N, Cc, HW
+
+
+def batchnorm_fwd(f_cfg, x, gamma, beta, eps_code: int, training: bool, o_cfg, run_mean, run_var,
+                  mom_code: int):
+    """-> (y, xhat, inv); run_mean / run_var (optimizer format) updated in place when training."""
+    fc, oc = _cfg(f_cfg), _cfg(o_cfg)
+    x = x.contiguous()
+    N, Cc, HW = _bn_shape(x)
+    n = C.c_size_t()
+    _native.check(_native.lib().pnn_batchnorm_workspace(Cc, C.byref(n)))
+    ws = _ws.get(x.device, n.value)
+    y, xh = torch.empty_like(x), torch.empty_like(x)
+    inv = torch.empty((Cc,), dtype=x.dtype, device=x.device)
+    _native.check(_native.lib().pnn_batchnorm_fwd(fc.nbits, fc.es, x.data_ptr(), N, Cc, HW,
+                                                  gamma.contiguous().data_ptr(), beta.contiguous().data_ptr(),
+                                                  int(eps_code), int(bool(training)), oc.nbits, oc.es,
+                                                  run_mean.data_ptr(), run_var.data_ptr(), int(mom_code),
+                                                  y.data_ptr(), xh.data_ptr(), inv.data_ptr(), ws.data_ptr(),
+                                                  ws.numel(), _stream_ptr(x.device)))
+    return y, xh, inv
+
+
+def batchnorm_bwd(f_cfg, xhat, inv, b_cfg, dy, gamma_b, g_cfg, raw: bool = False):
+    """-> (dx, dgamma, dbeta) or, raw, (dx, (dgamma words, nar), (dbeta words, nar))."""
+    fc, bc, gc = _cfg(f_cfg), _cfg(b_cfg), _cfg(g_cfg)
+    dy = dy.contiguous()
+    N, Cc, HW = _bn_shape(dy)
+    n = C.c_size_t()
+    _native.check(_native.lib().pnn_batchnorm_workspace(Cc, C.byref(n)))
+    ws = _ws.get(dy.device, n.value)
+    dx = torch.empty_like(dy)
+    dev = dy.device
+    if raw:
+        gw = torch.empty((Cc, 2), dtype=torch.int64, device=dev)
+        gn = torch.empty((Cc,), dtype=torch.uint8, device=dev)
+        bw = torch.empty((Cc, 2), dtype=torch.int64, device=dev)
+        bn_ = torch.empty((Cc,), dtype=torch.uint8, device=dev)
+        ptrs = (None, None, gw.data_ptr(), gn.data_ptr(), bw.data_ptr(), bn_.data_ptr())
+    else:
+        dg = torch.empty((Cc,), dtype=gc.code_dtype, device=dev)
+        db = torch.empty((Cc,), dtype=gc.code_dtype, device=dev)
+        ptrs = (dg.data_ptr(), db.data_ptr(), None, None, None, None)
+    _native.check(_native.lib().pnn_batchnorm_bwd(fc.nbits, fc.es, xhat.contiguous().data_ptr(),
+                                                  inv.contiguous().data_ptr(), bc.nbits, bc.es, dy.data_ptr(),
+                                                  N, Cc, HW, gamma_b.contiguous().data_ptr(), gc.nbits, gc.es,
+                                                  dx.data_ptr(), *ptrs, ws.data_ptr(), ws.numel(),
+                                                  _stream_ptr(dev)))
+    if raw:
+        return dx, (gw, gn), (bw, bn_)
+    return dx, dg, db
+
+
+def sgd_step_momentum(opt_cfg, master, velocity, g_cfg, grad, lr_code: int, mu_code: int, copies=(),
+                      grad_scale_log2: int = 0):
+    """v = mu*v + ldexp(convert(grad), -s); master -= lr*v (in place, optimizer format)."""
+    oc, gc = _cfg(opt_cfg), _cfg(g_cfg)
+    cps = [(_cfg(c), t) for c, t in copies] + [(oc, None)] * (2 - len(copies))
+    (c1, t1), (c2, t2) = cps[0], cps[1]
+    _native.check(_native.lib().pnn_sgd_step_momentum(
+        oc.nbits, oc.es, master.data_ptr(), velocity.data_ptr(), gc.nbits, gc.es, grad.contiguous().data_ptr(),
+        master.numel(), int(lr_code), int(mu_code), c1.nbits, c1.es, t1.data_ptr() if t1 is not None else None,
+        c2.nbits, c2.es, t2.data_ptr() if t2 is not None else None, int(grad_scale_log2),
+        _stream_ptr(master.device)))
+    return master
