@@ -12,7 +12,8 @@ import threading
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
 REPO_DIR = os.path.dirname(PKG_DIR)
-LIB_PATH = os.path.join(PKG_DIR, "libpnn_b200.so")
+# PNN_B200_LIB: an alternative build of the same library (A/B experiments)
+LIB_PATH = os.environ.get("PNN_B200_LIB") or os.path.join(PKG_DIR, "libpnn_b200.so")
 HEADER_PATH = os.path.join(REPO_DIR, "include", "pnn_b200.h")
 
 _lock = threading.Lock()

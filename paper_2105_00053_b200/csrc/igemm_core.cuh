@@ -24,8 +24,18 @@
 
 #include <cuda.h>
 
+#include "epilogue.cuh"
 #include "igemm.h"
 #include "quire_gemm_core.cuh"
+
+// PNN_IGEMM_DEBUG_HOOKS: compile the epilogue's profiling switches (a.debug
+// bits 1, 8, 16; tools/igemm_bottleneck.sh).  Off in the product build: they
+// cost branches in the per-output loop.
+#ifdef PNN_IGEMM_DEBUG_HOOKS
+#define PNN_EPI_DEBUG(bit) (a.debug & (bit))
+#else
+#define PNN_EPI_DEBUG(bit) false
+#endif
 
 namespace pnn_b200 {
 
@@ -97,8 +107,9 @@ __global__ void __launch_bounds__(ImplGeo<D, NT_, CPS, ACC>::THREADS, CPS)
     constexpr int SUB = kIEpiWarps / 4;  // warps per lane quarter
     constexpr int COLS = NT / SUB;       // columns per epilogue thread
     static_assert(COLS % 8 == 0, "epilogue chunks");
-    constexpr int GB = G < 8 ? G : (QW == 4 ? 4 : 8);  // TMEM loads per wait (registers)
+    constexpr int GB = G < 4 ? G : 4;  // TMEM loads per wait (registers)
     extern __shared__ uint8_t smem_raw[];
+    __shared__ uint4 s_lut[kPackLutEntries];  // per-scale rounding table (epilogue)
     uint8_t* smem = smem_raw + ((1024 - (ptx::smem_u32(smem_raw) & 1023)) & 1023);
     uint8_t* zero_tile = smem + STAGES * Geo::STAGE_BYTES;
     uint64_t* full = reinterpret_cast<uint64_t*>(zero_tile + kZeroBytes);
@@ -113,6 +124,7 @@ __global__ void __launch_bounds__(ImplGeo<D, NT_, CPS, ACC>::THREADS, CPS)
 
     for (int i = threadIdx.x; i < kZeroBytes / 16; i += kIThreads)
         reinterpret_cast<int4*>(zero_tile)[i] = make_int4(0, 0, 0, 0);
+    build_pack_lut(fixed_fmt<FMT>(a.f), s_lut, threadIdx.x, kIThreads);
     if (warp == 0 && lane == 0) {
         ptx::tma_prefetch_desc(&tmA);
         ptx::tma_prefetch_desc(&tmB);
@@ -258,13 +270,19 @@ __global__ void __launch_bounds__(ImplGeo<D, NT_, CPS, ACC>::THREADS, CPS)
             QT q[COLS];
 #pragma unroll
             for (int c0 = 0; c0 < COLS; c0 += 8) {
-                QAcc<QT> acc[8];
+                QAcc2<QW> acc[8];
 #pragma unroll
                 for (int g0 = 0; g0 < G; g0 += GB) {
                     uint32_t r[GB][8];
 #pragma unroll
                     for (int g = 0; g < GB; ++g)
-                        if (g0 + g < G) { if (a.debug & 8) { for (int x = 0; x < 8; ++x) r[g][x] = 0; } else ptx::tmem_ld8(trow_b + (g0 + g) * NT + SUB * c0, r[g]); }
+                        if (g0 + g < G) {
+                            if (PNN_EPI_DEBUG(8)) {
+                                for (int x = 0; x < 8; ++x) r[g][x] = 0;
+                            } else {
+                                ptx::tmem_ld8(trow_b + (g0 + g) * NT + SUB * c0, r[g]);
+                            }
+                        }
                     ptx::tmem_wait_ld();
 #pragma unroll
                     for (int g = 0; g < GB; ++g)
@@ -278,7 +296,7 @@ __global__ void __launch_bounds__(ImplGeo<D, NT_, CPS, ACC>::THREADS, CPS)
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(&tmem_empty[buf]);
-            if (a.debug & 16) continue;  // profiling: no output
+            if (PNN_EPI_DEBUG(16)) continue;  // profiling: no output
 
             const int64_t row = mt * kBM + quarter * 32 + lane;
             if (row >= a.M) continue;
@@ -286,10 +304,11 @@ __global__ void __launch_bounds__(ImplGeo<D, NT_, CPS, ACC>::THREADS, CPS)
             const int64_t obase = out.row_base(row), ostride = out.col_stride();
             if (obase < 0 && a.partial == nullptr) continue;  // padding row (weight grad)
             if constexpr (MODE == 0) if (a.col_add != nullptr && split == 0) {
+                const int cb = int(colbase), nn = int(a.N);
 #pragma unroll
                 for (int c = 0; c < COLS; ++c)
-                    if (colbase + SUB * (c & ~7) + (c & 7) < a.N) {
-                        const int64_t xb = a.col_add[colbase + SUB * (c & ~7) + (c & 7)];
+                    if (cb + SUB * (c & ~7) + (c & 7) < nn) {
+                        const int64_t xb = a.col_add[cb + SUB * (c & ~7) + (c & 7)];
                         if constexpr (QW == 4) q[c] += QT(__int128(xb)) << f.R;
                         else q[c] += QT(xb) << f.R;
                     }
@@ -314,7 +333,8 @@ __global__ void __launch_bounds__(ImplGeo<D, NT_, CPS, ACC>::THREADS, CPS)
                 uint32_t codes[8];
 #pragma unroll
                 for (int x = 0; x < 8; ++x) {
-                    const uint32_t c = (a.debug & 1) ? uint32_t(q[c0 + x]) : quire_word_to_posit_bf(f, q[c0 + x]);
+                    const uint32_t c =
+                        PNN_EPI_DEBUG(1) ? uint32_t(q[c0 + x]) : q_to_posit_lut(f, q[c0 + x], s_lut);
                     codes[x] = ((cn >> (8 * x)) & 0xFF) ? (1u << (f.nbits - 1)) : c;
                 }
                 CodeT* dst = out.base + obase + col0 * ostride;

@@ -33,6 +33,18 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     const uint32_t addr = smem_u32(bar);
+#ifdef PNN_MBAR_HINT
+    // suspend (rather than spin) until the phase completes or the hint expires
+    asm volatile(
+        "{\n\t"
+        ".reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+        "@!p bra WAIT_%=;\n\t"
+        "}" ::"r"(addr),
+        "r"(parity), "n"(PNN_MBAR_HINT)
+        : "memory");
+#else
     asm volatile(
         "{\n\t"
         ".reg .pred p;\n\t"
@@ -42,6 +54,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "}" ::"r"(addr),
         "r"(parity)
         : "memory");
+#endif
 }
 
 // ---- bulk async copy global -> shared (completes on an mbarrier) ----------

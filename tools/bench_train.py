@@ -98,6 +98,8 @@ CONFIGS = {
               st=(P80, P121, P121, P161, P161), batch=256),
     "3": dict(name="config3 CIFAR CNN B=512 (1 GPU) fwd(8,1) grad(12,1) opt/loss(16,1)", layers="cifar",
               st=(P81, P121, P121, P161, P161), batch=512),
+    "3b": dict(name="config3 formats, B=1024 (the bench.py training leg, 1 GPU)", layers="cifar",
+               st=(P81, P121, P121, P161, P161), batch=1024),
     "4a": dict(name="config4 CIFAR CNN B=1024 (1 GPU) uniform posit(8,0)", layers="cifar",
                st=(P80,) * 5, batch=1024),
     "4b": dict(name="config4 CIFAR CNN B=1024 (1 GPU) uniform posit(8,1)", layers="cifar",
