@@ -183,6 +183,10 @@ bool make_plan(int pass, const PositFmt& f, const ConvGeom& g_real, bool raw, Im
                                        num_sms() * ((pass == 2 || D >= 5) ? 1 : 2));  // CTAs in flight
     a.kb_per_split = a.kbt < kbps ? a.kbt : kbps;
     a.splits = cdiv(a.kbt, a.kb_per_split);
+    a.fd_split = FastDiv(uint32_t(a.mtiles * a.ntiles));
+    a.fd_group = FastDiv(uint32_t(kGroupM * a.ntiles));
+    a.fd_g8 = FastDiv(uint32_t(kGroupM));
+    a.fd_glast = FastDiv(uint32_t(a.mtiles % kGroupM ? a.mtiles % kGroupM : kGroupM));
     if (a.mtiles * a.ntiles * a.splits >= (int64_t(1) << 31) || a.M >= (int64_t(1) << 31)) return false;
     const size_t partial = (a.splits > 1 || raw) ? size_t(a.splits) * a.M * a.N * 16 : 0;
 
@@ -346,12 +350,17 @@ cudaError_t act_digits(int D, const CodeT* x, int64_t N, int64_t C, int64_t H, i
                        int64_t Cp, int pad, const PositFmt& f, uint32_t* lut, bool build_lut, int8_t* dig,
                        uint8_t* pos_nar, uint8_t* chw_nar, uint8_t* chan_nar, uint8_t* any,
                        cudaStream_t st) {
-    const int grid = grid_for(N * H * W * (Cp / 32), 256);  // thread per (pixel, 32 channels)
+    // thread per (pixel, 32 channels): grid (pixel blocks, 32-channel chunks)
+    if (N * H * W >= (int64_t(1) << 31)) return cudaErrorInvalidValue;
+    const dim3 grid(unsigned((grid_for(N * H * W * (Cp / 32), 256) + Cp / 32 - 1) / (Cp / 32)),
+                    unsigned(Cp / 32));
+    const FastDiv fd_hw{uint32_t(H * W)}, fd_w{uint32_t(W)};
     if (lut == nullptr) build_lut = false;
 #define PNN_ACT(DD)                                                                              \
     if (build_lut) digit_lut_kernel<DD><<<16, 256, 0, st>>>(f, lut);                             \
-    act_digits_kernel<DD, CodeT><<<grid, 256, 0, st>>>(x, N, int(C), int(H), int(W), int(Cp), pad, f, \
-                                                       lut, dig, pos_nar, chw_nar, chan_nar, any)
+    act_digits_kernel<DD, CodeT><<<grid, 256, 0, st>>>(x, int(N), int(C), int(H), int(W), int(Cp), \
+                                                       pad, fd_hw, fd_w, f, lut, dig, pos_nar,   \
+                                                       chw_nar, chan_nar, any)
     switch (D) {
         case 2: PNN_ACT(2); break;
         case 3: PNN_ACT(3); break;
@@ -371,11 +380,13 @@ cudaError_t im2col_digits(int D, const CodeT* x, const ConvGeom& g, const PositF
                           int8_t* dig, uint8_t* pos_nar, uint8_t* chw_nar, uint8_t* any,
                           cudaStream_t st) {
     const int grid = grid_for(g.N * g.OH * g.OW, 256);  // thread per output pixel
+    if (g.N * g.OH * g.OW >= (int64_t(1) << 31)) return cudaErrorInvalidValue;
+    const FastDiv fd_p{uint32_t(g.OH * g.OW)}, fd_ow{uint32_t(g.OW)};
 #define PNN_I2C(DD)                                                                          \
     if (lut) digit_lut_kernel<DD><<<16, 256, 0, st>>>(f, lut);                               \
     im2col_digits_kernel<DD, CodeT><<<grid, 256, 0, st>>>(                                   \
-        x, g.N, int(g.C), int(g.H), int(g.W), int(g.KH), int(g.KW), g.pad, int(g.OH), int(g.OW), \
-        f, lut, dig, pos_nar, chw_nar, any)
+        x, int(g.N), int(g.C), int(g.H), int(g.W), int(g.KH), int(g.KW), g.pad, int(g.OH),   \
+        int(g.OW), fd_p, fd_ow, f, lut, dig, pos_nar, chw_nar, any)
     switch (D) {
         case 2: PNN_I2C(2); break;
         case 3: PNN_I2C(3); break;

@@ -25,6 +25,7 @@
 #include <cuda.h>
 
 #include "epilogue.cuh"
+#include "fastdiv.cuh"
 #include "igemm.h"
 #include "quire_gemm_core.cuh"
 
@@ -86,12 +87,28 @@ struct IgemmArgs {
     // mode 2: K blocks of OWb x OHb output pixels; m-tile = one ky, 4 kx, 32 channels
     int taps, C, OWb, OHb, kpr, kpi;  // k-blocks per row-block set / per image
     int KH, kgroups, cgroups, Hp;     // kx groups of 4, 32-channel groups, padded height
+    // tile raster (tile_coords) with launch-constant divisions: by mtiles * ntiles,
+    // by kGroupM * ntiles, and by the group height (kGroupM, or the last group's)
+    FastDiv fd_split, fd_group, fd_g8, fd_glast;
     const int64_t* col_add;  // mode 0: X(bias) per column (added as X * 2^R)
     const uint8_t* col_nar;
     PositFmt f;
     unsigned __int128* partial;
     int debug;  // profiling only (PNN_IGEMM_DEBUG): 1 skip conversion, 2 skip MMA, 4 skip TMA waits
 };
+
+// tile_coords (quire_gemm_core.cuh) with the divisions precomputed per launch.
+__device__ __forceinline__ void itile_coords(int64_t t64, const IgemmArgs& a, int64_t& split,
+                                             int64_t& mt, int64_t& nt) {
+    uint32_t sp, r, group, within, q, rem;
+    a.fd_split.divmod(uint32_t(t64), sp, r);
+    a.fd_group.divmod(r, group, within);
+    const uint32_t left = uint32_t(a.mtiles) - group * kGroupM;
+    (left < uint32_t(kGroupM) ? a.fd_glast : a.fd_g8).divmod(within, q, rem);
+    split = sp;
+    mt = group * kGroupM + rem;
+    nt = q;
+}
 
 // Epilogue warps: 8 (two CTAs per SM) or 16 (one): the epilogue (TMEM drain,
 // quire accumulation, quire -> posit) is latency-bound, so it gets the warps.
@@ -153,7 +170,7 @@ __global__ void __launch_bounds__(ImplGeo<D, NT_, CPS, ACC>::THREADS, CPS)
             uint32_t it = 0;
             for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
                 int64_t split, mt, nt;
-                tile_coords(t, a.mtiles, a.ntiles, split, mt, nt);
+                itile_coords(t, a, split, mt, nt);
                 const int64_t kb0 = split * a.kb_per_split;
                 const int nkb = int(min(a.kbt, kb0 + a.kb_per_split) - kb0);
                 int n0 = 0, y0 = 0;
@@ -216,7 +233,7 @@ __global__ void __launch_bounds__(ImplGeo<D, NT_, CPS, ACC>::THREADS, CPS)
             uint32_t it = 0, j = 0;
             for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++j) {
                 int64_t split, mt, nt;
-                tile_coords(t, a.mtiles, a.ntiles, split, mt, nt);
+                itile_coords(t, a, split, mt, nt);
                 const int64_t kb0 = split * a.kb_per_split;
                 const int nkb = int(min(a.kbt, kb0 + a.kb_per_split) - kb0);
                 const int buf = ACC == 2 ? int(j & 1) : 0;
@@ -262,7 +279,7 @@ __global__ void __launch_bounds__(ImplGeo<D, NT_, CPS, ACC>::THREADS, CPS)
         uint32_t j = 0;
         for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++j) {
             int64_t split, mt, nt;
-            tile_coords(t, a.mtiles, a.ntiles, split, mt, nt);
+            itile_coords(t, a, split, mt, nt);
             const int buf = ACC == 2 ? int(j & 1) : 0;
             ptx::mbar_wait(&tmem_full[buf], ((ACC == 2 ? (j >> 1) : j)) & 1);
             ptx::tc_fence_after();
@@ -428,23 +445,24 @@ __device__ __forceinline__ uint32_t digits4_words(const uint32_t (&c)[4], const 
 // writes 32 contiguous digit bytes per plane (two 16-byte stores), so the
 // warp's stores are 1 KB contiguous per plane.  lut: digit_lut_kernel output
 // (formats up to 12 bits) or null (decode).
+// Grid: (pixel blocks, 32-channel chunks); 32-bit indices (pixels < 2^31,
+// checked by the launcher) with launch-constant divisions by multiplication.
 template <int D, typename CodeT>
 __global__ void __launch_bounds__(256) act_digits_kernel(
-    const CodeT* __restrict__ x, int64_t N, int C, int H, int W, int Cp, int pad, PositFmt f,
-    const uint32_t* __restrict__ lut, int8_t* __restrict__ dig, uint8_t* __restrict__ pos_nar,
-    uint8_t* __restrict__ chw_nar, uint8_t* __restrict__ chan_nar, uint8_t* __restrict__ any) {
-    const int64_t HW = int64_t(H) * W;
-    const int64_t pixels = N * HW;
+    const CodeT* __restrict__ x, int N, int C, int H, int W, int Cp, int pad, FastDiv fd_hw,
+    FastDiv fd_w, PositFmt f, const uint32_t* __restrict__ lut, int8_t* __restrict__ dig,
+    uint8_t* __restrict__ pos_nar, uint8_t* __restrict__ chw_nar, uint8_t* __restrict__ chan_nar,
+    uint8_t* __restrict__ any) {
+    const uint32_t HW = uint32_t(H) * uint32_t(W);
+    const uint32_t pixels = uint32_t(N) * HW;
     const int Hp = H + 2 * pad, Wp = W + 2 * pad;  // zero-padded image (weight grad)
-    const int64_t plane = N * int64_t(Hp) * Wp * Cp;
-    const int chunks = Cp / 32;
-    for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < pixels * chunks;
-         t += int64_t(gridDim.x) * blockDim.x) {
-        const int cc = int(t / pixels);
-        const int64_t r = t - cc * pixels;  // pixel raster index (n, h, w)
-        const int64_t n = r / HW, pix = r - n * HW;
+    const int64_t plane = int64_t(N) * Hp * Wp * Cp;
+    const int cc = blockIdx.y;
+    for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < pixels; r += gridDim.x * blockDim.x) {
+        uint32_t n, pix;  // pixel raster index r = (n, h, w)
+        fd_hw.divmod(r, n, pix);
         const int c0 = cc * 32;
-        const CodeT* src = x + (n * C + c0) * HW + pix;
+        const CodeT* src = x + (int64_t(n) * C + c0) * HW + pix;
         uint32_t code[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) code[j] = c0 + j < C ? uint32_t(src[j * HW]) : 0u;
@@ -456,8 +474,9 @@ __global__ void __launch_bounds__(256) act_digits_kernel(
             nm |= digits4_words<D>(c4, f, lut, words, q) << (4 * q);
         }
         // slice layout [D][N][Hp][Cp/16][Wp][16]: this chunk = slices 2cc, 2cc+1
-        const int h = int(pix / W), w = int(pix - int64_t(h) * W);
-        int8_t* dst = dig + (((n * Hp + h + pad) * (Cp / 16) + 2 * cc) * Wp + w + pad) * 16;
+        uint32_t h, w;
+        fd_w.divmod(pix, h, w);
+        int8_t* dst = dig + (((int64_t(n) * Hp + h + pad) * (Cp / 16) + 2 * cc) * Wp + w + pad) * 16;
 #pragma unroll
         for (int p = 0; p < D; ++p) {
             *reinterpret_cast<uint4*>(dst + p * plane) =
@@ -514,16 +533,31 @@ static __global__ void pad_zero_kernel(uint4* __restrict__ dig, int64_t DN, int 
 // (forward rows) and chw_nar[k][oy][ox] (weight-grad rows).
 template <int D, typename CodeT>
 __global__ void __launch_bounds__(256) im2col_digits_kernel(
-    const CodeT* __restrict__ x, int64_t N, int C, int H, int W, int KH, int KW, int pad, int OH,
-    int OW, PositFmt f, const uint32_t* __restrict__ lut, int8_t* __restrict__ dig,
-    uint8_t* __restrict__ pos_nar, uint8_t* __restrict__ chw_nar, uint8_t* __restrict__ any) {
+    const CodeT* __restrict__ x, int N, int C, int H, int W, int KH, int KW, int pad, int OH,
+    int OW, FastDiv fd_p, FastDiv fd_ow, PositFmt f, const uint32_t* __restrict__ lut,
+    int8_t* __restrict__ dig, uint8_t* __restrict__ pos_nar, uint8_t* __restrict__ chw_nar,
+    uint8_t* __restrict__ any) {
     const int ckk = C * KH * KW, khw = KH * KW;
-    const int64_t P = int64_t(OH) * OW;
-    const int64_t plane = N * P * 32;
-    for (int64_t pos = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; pos < N * P;
-         pos += int64_t(gridDim.x) * blockDim.x) {
-        const int64_t n = pos / P;
-        const int pix = int(pos - n * P), oy = pix / OW, ox = pix - oy * OW;
+    const uint32_t P = uint32_t(OH) * uint32_t(OW);
+    const int64_t plane = int64_t(N) * P * 32;
+    // receptive-field table: K index k -> (offset of (c, ky - pad, kx - pad) in
+    // the image, ky - pad, kx - pad); k >= ckk never loads
+    __shared__ int s_off[32];
+    __shared__ int16_t s_dy[32], s_dx[32];
+    if (threadIdx.x < 32) {
+        const int k = threadIdx.x;
+        const int c = k / khw, t = k - c * khw, ky = t / KW, kx = t - ky * KW;
+        s_off[k] = (c * H + ky - pad) * W + kx - pad;
+        s_dy[k] = int16_t(k < ckk ? ky - pad : -32768);  // padding K: never in range
+        s_dx[k] = int16_t(kx - pad);
+    }
+    __syncthreads();
+    const uint32_t NP = uint32_t(N) * P;
+    for (uint32_t pos = blockIdx.x * blockDim.x + threadIdx.x; pos < NP; pos += gridDim.x * blockDim.x) {
+        uint32_t n, pix, oy, ox;
+        fd_p.divmod(pos, n, pix);
+        fd_ow.divmod(pix, oy, ox);
+        const CodeT* xn = x + int64_t(n) * C * H * W + int(oy) * W + int(ox);
         uint32_t words[D][8];
         uint32_t nm = 0;
 #pragma unroll
@@ -532,19 +566,15 @@ __global__ void __launch_bounds__(256) im2col_digits_kernel(
 #pragma unroll
             for (int jj = 0; jj < 4; ++jj) {
                 const int k = 4 * q + jj;
-                uint32_t code = 0;
-                if (k < ckk) {
-                    const int c = k / khw, t = k - c * khw, ky = t / KW, kx = t - ky * KW;
-                    const int iy = oy + ky - pad, ix = ox + kx - pad;
-                    if (unsigned(iy) < unsigned(H) && unsigned(ix) < unsigned(W))
-                        code = uint32_t(x[((n * C + c) * H + iy) * W + ix]);
-                }
-                c4[jj] = code;
+                const int iy = int(oy) + s_dy[k], ix = int(ox) + s_dx[k];
+                c4[jj] = (unsigned(iy) < unsigned(H) && unsigned(ix) < unsigned(W))
+                             ? uint32_t(xn[s_off[k]])
+                             : 0u;
             }
             nm |= digits4_words<D>(c4, f, lut, words, q) << (4 * q);
         }
         // slice layout of the virtual [N][OH][2 slices][OW][16] image
-        const int64_t row = pos / OW;
+        const int64_t row = int64_t(n) * OH + oy;
         int8_t* dst = dig + ((row * 2) * OW + ox) * 16;
 #pragma unroll
         for (int p = 0; p < D; ++p) {

@@ -37,6 +37,7 @@
 #include <cstdint>
 #include <cstdlib>
 
+#include "fastdiv.cuh"
 #include "posit_device.cuh"
 #include "quire_gemm.h"
 #include "sm100_ptx.cuh"
@@ -326,6 +327,7 @@ struct OutMap {
     // mode 3 (implicit weight grad): 128-row tiles (ky, kx group, 32-channel group),
     // row within a tile = (slice j, kx k, channel c16) -> dw[n][c][ky][kx]
     int kh, kw, kgroups, cgroups, cvalid;
+    FastDiv fd_inner;  // mode 1: division by inner (set when inner < 2^31)
     __device__ __forceinline__ int64_t row_base(int64_t m) const {
         if (mode == 0) return m * ldc;
         if (mode == 3) {
@@ -337,7 +339,12 @@ struct OutMap {
             return int64_t(c) * (kh * kw) + ky * kw + kx;
         }
         int64_t hi, lo;
-        if (m < (int64_t(1) << 31) && inner < (int64_t(1) << 31)) {  // 32-bit division
+        if (mode == 1 && fd_inner.d == uint64_t(inner) && m < (int64_t(1) << 31)) {
+            uint32_t q, r;
+            fd_inner.divmod(uint32_t(m), q, r);
+            hi = q;
+            lo = r;
+        } else if (m < (int64_t(1) << 31) && inner < (int64_t(1) << 31)) {  // 32-bit division
             const uint32_t h32 = uint32_t(m) / uint32_t(inner);
             hi = h32;
             lo = m - int64_t(h32) * inner;
@@ -998,6 +1005,7 @@ inline OutMap<CodeT> out_nchw(void* base, int64_t pixels, int64_t channels) {
     o.inner = pixels;
     o.ncols = channels;
     o.mode = 1;
+    if (pixels < (int64_t(1) << 31)) o.fd_inner = FastDiv(uint32_t(pixels));
     return o;
 }
 
