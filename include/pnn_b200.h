@@ -97,6 +97,38 @@ int pnn_conv2d_wgrad(int nbits, int es, const void* dy, int64_t N, int64_t F, in
                      int64_t OW, const void* x, int64_t C, int64_t H, int64_t W, int64_t KH,
                      int64_t KW, int stride, int pad, void* dw, void* raw_words, void* raw_nar,
                      void* workspace, size_t workspace_bytes, void* stream);
+
+/* Layer-level Conv2d pair (the nn layer's forward / backward, SPEC.md §3.3 and
+ * SURVEY.md Appendix A.6; the reference's layers are placeholders, layers.cpp:1).
+ * Results are bit-identical to the per-pass calls above; what changes is the
+ * data flow:
+ *  - pnn_conv2d_fwd_save = pnn_conv2d_fwd that also leaves x's int8 digit
+ *    planes (+ NaR map) in `saved` (pnn_conv2d_saved_bytes; 0 = geometry has no
+ *    implicit forward/weight-gradient pair), the layer's saved tensor;
+ *  - pnn_conv2d_backward = in one call
+ *        dw = conv2d_weight_grad(p_g, convert(dy, p_b -> p_g), convert(x, p_f -> p_g))
+ *        dx = conv2d_input_grad(p_b, dy, w_bwd)           (dx may be NULL)
+ *    with the weight gradient reading the saved forward digits (same format, or
+ *    an exact widening p_f -> p_g by whole digits), stage conversions folded
+ *    into the digitisers, and dy digitised once for both passes when p_b == p_g.
+ *    dw codes and/or raw quire words + NaR mask as in pnn_conv2d_wgrad.
+ *    PNN_EUNSUPPORTED from the workspace query = use the per-pass calls. */
+int pnn_conv2d_saved_bytes(int nbits, int es, int64_t N, int64_t C, int64_t H, int64_t W, int64_t F,
+                           int64_t KH, int64_t KW, int stride, int pad, size_t* bytes);
+int pnn_conv2d_fwd_save(int nbits, int es, const void* x, int64_t N, int64_t C, int64_t H, int64_t W,
+                        const void* w, int64_t F, int64_t KH, int64_t KW, const void* bias, int stride,
+                        int pad, void* y, void* saved, size_t saved_bytes, void* workspace,
+                        size_t workspace_bytes, void* stream);
+int pnn_conv2d_backward_workspace(int f_nbits, int f_es, int b_nbits, int b_es, int g_nbits, int g_es,
+                                  int64_t N, int64_t C, int64_t H, int64_t W, int64_t F, int64_t KH,
+                                  int64_t KW, int stride, int pad, int raw, int has_dx, int has_saved,
+                                  size_t* bytes);
+int pnn_conv2d_backward(int f_nbits, int f_es, int b_nbits, int b_es, int g_nbits, int g_es,
+                        const void* dy, const void* x, const void* saved, size_t saved_bytes,
+                        const void* w_bwd, int64_t N, int64_t C, int64_t H, int64_t W, int64_t F,
+                        int64_t KH, int64_t KW, int stride, int pad, void* dx, void* dw,
+                        void* raw_words, void* raw_nar, void* workspace, size_t workspace_bytes,
+                        void* stream);
 /* conv2d_bias_grad (tensor_ops.cpp:605-618) for dy [N,F,P] with P = OH*OW,
  * and column_sum (:722-731) with P = 1: db[f] = round(quire sum of dy[:,f,:]). */
 int pnn_bias_grad_workspace(int64_t F, size_t* bytes);

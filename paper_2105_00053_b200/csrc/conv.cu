@@ -549,6 +549,74 @@ int pnn_conv2d_wgrad(int nbits, int es, const void* dy, int64_t N, int64_t F, in
     return status_of(rc, "conv2d_wgrad");
 }
 
+// ---- layer-level pair: forward keeping x's digits, fused backward ----------
+
+int pnn_conv2d_saved_bytes(int nbits, int es, int64_t N, int64_t C, int64_t H, int64_t W, int64_t F,
+                           int64_t KH, int64_t KW, int stride, int pad, size_t* bytes) {
+    if (!conv_fmt_ok(nbits, es)) return set_status(PNN_EUNSUPPORTED, "conv: format not supported");
+    ConvGeom g;
+    if (!bytes || conv_geom(N, C, H, W, F, KH, KW, stride, pad, &g))
+        return set_status(PNN_EINVAL, "conv: invalid shape or argument");
+    *bytes = N > 0 ? igemm_saved_bytes(make_fmt(nbits, es), g) : 0;
+    return PNN_OK;
+}
+
+int pnn_conv2d_fwd_save(int nbits, int es, const void* x, int64_t N, int64_t C, int64_t H, int64_t W,
+                        const void* w, int64_t F, int64_t KH, int64_t KW, const void* bias, int stride,
+                        int pad, void* y, void* saved, size_t saved_bytes, void* workspace,
+                        size_t workspace_bytes, void* stream) {
+    if (saved == nullptr)
+        return pnn_conv2d_fwd(nbits, es, x, N, C, H, W, w, F, KH, KW, bias, stride, pad, y, workspace,
+                              workspace_bytes, stream);
+    if (!conv_fmt_ok(nbits, es)) return set_status(PNN_EUNSUPPORTED, "conv: format not supported");
+    ConvGeom g;
+    if (conv_geom(N, C, H, W, F, KH, KW, stride, pad, &g) || !x || !w || !y)
+        return set_status(PNN_EINVAL, "conv: invalid shape or argument");
+    if (N == 0) return PNN_OK;
+    const PositFmt f = make_fmt(nbits, es);
+    if (igemm_saved_bytes(f, g) == 0)
+        return set_status(PNN_EUNSUPPORTED, "conv2d_fwd_save: no implicit forward/weight-grad pair");
+    return status_of(igemm_conv_fwd(f, g, x, w, bias, y, workspace, workspace_bytes,
+                                    static_cast<cudaStream_t>(stream), saved, saved_bytes),
+                     "conv2d_fwd_save");
+}
+
+int pnn_conv2d_backward_workspace(int f_nbits, int f_es, int b_nbits, int b_es, int g_nbits, int g_es,
+                                  int64_t N, int64_t C, int64_t H, int64_t W, int64_t F, int64_t KH,
+                                  int64_t KW, int stride, int pad, int raw, int has_dx, int has_saved,
+                                  size_t* bytes) {
+    if (!conv_fmt_ok(f_nbits, f_es) || !conv_fmt_ok(b_nbits, b_es) || !conv_fmt_ok(g_nbits, g_es))
+        return set_status(PNN_EUNSUPPORTED, "conv: format not supported");
+    ConvGeom g;
+    if (!bytes || N < 1 || conv_geom(N, C, H, W, F, KH, KW, stride, pad, &g))
+        return set_status(PNN_EINVAL, "conv: invalid shape or argument");
+    if (!igemm_backward_eligible(make_fmt(f_nbits, f_es), make_fmt(b_nbits, b_es), make_fmt(g_nbits, g_es),
+                                 g, raw != 0, has_dx != 0, has_saved != 0, bytes))
+        return set_status(PNN_EUNSUPPORTED, "conv2d_backward: not eligible (use the per-pass calls)");
+    return PNN_OK;
+}
+
+int pnn_conv2d_backward(int f_nbits, int f_es, int b_nbits, int b_es, int g_nbits, int g_es,
+                        const void* dy, const void* x, const void* saved, size_t saved_bytes,
+                        const void* w_bwd, int64_t N, int64_t C, int64_t H, int64_t W, int64_t F,
+                        int64_t KH, int64_t KW, int stride, int pad, void* dx, void* dw,
+                        void* raw_words, void* raw_nar, void* workspace, size_t workspace_bytes,
+                        void* stream) {
+    if (!conv_fmt_ok(f_nbits, f_es) || !conv_fmt_ok(b_nbits, b_es) || !conv_fmt_ok(g_nbits, g_es))
+        return set_status(PNN_EUNSUPPORTED, "conv: format not supported");
+    ConvGeom g;
+    if (N < 1 || conv_geom(N, C, H, W, F, KH, KW, stride, pad, &g) || !dy || (!x && !saved))
+        return set_status(PNN_EINVAL, "conv: invalid shape or argument");
+    if ((!dw && !raw_words) || ((raw_words != nullptr) != (raw_nar != nullptr)) || (dx && !w_bwd))
+        return set_status(PNN_EINVAL, "conv: invalid shape or argument");
+    return status_of(igemm_conv_backward(make_fmt(f_nbits, f_es), make_fmt(b_nbits, b_es),
+                                         make_fmt(g_nbits, g_es), g, dy, x, saved, saved_bytes, w_bwd, dx,
+                                         dw, static_cast<unsigned __int128*>(raw_words),
+                                         static_cast<uint8_t*>(raw_nar), workspace, workspace_bytes,
+                                         static_cast<cudaStream_t>(stream)),
+                     "conv2d_backward");
+}
+
 // workspace: [split partials F x 64 x 16 B][NaR flags F][X table of the format]
 constexpr int kBiasLutBits = 12;
 static size_t bias_lut_offset(int64_t F) {

@@ -52,14 +52,15 @@ bool tile_geom(int64_t Ht, int64_t Wt, int* tpi, int* ipt, int* Hb) {
 
 struct ImplPlan {
     int mode, D, NT;
+    int DA, OFF;            // A digit planes / group offset (mode 2 from saved digits; else D, 0)
     IgemmArgs a;
     int64_t Ca, Wa, Ha;     // A digit tensor [D][N][Ha][Wa][Ca]
     uint32_t boxA[5];       // slice-layout box {2 * w, h, n, slices, planes}
     int64_t Kp, brows;      // modes 0/1: B digits [D][brows][taps * Kp]
     int64_t Fpw;            // mode 2: B digits [D][N][OH][OW][Fpw]
     size_t adig, bdig;      // bytes
-    size_t off_adig, off_bdig, off_col_add, off_lut, off_maps, maps_bytes, off_pos_nar, off_chw_nar,
-        off_col_nar, off_flags, off_partial, total;
+    size_t off_adig, off_bdig, off_col_add, off_lut, off_lut2, off_maps, maps_bytes, off_pos_nar,
+        off_chw_nar, off_col_nar, off_flags, off_partial, total;
     bool fold;    // first-layer tap folding: planned on the virtual 1x1 geometry gv
     int ckk;      // C * KH * KW of the real layer
     ConvGeom gv;  // geometry the plan runs on (== the real one unless folded)
@@ -80,12 +81,15 @@ bool fold_geom(int pass, const ConvGeom& g, ConvGeom* gv) {
     return true;
 }
 
-bool make_plan(int pass, const PositFmt& f, const ConvGeom& g_real, bool raw, ImplPlan* p) {
+bool make_plan(int pass, const PositFmt& f, const ConvGeom& g_real, bool raw, ImplPlan* p,
+               int DA = 0, int OFF = 0) {
     if (conv_algo() == 1 || g_real.stride != 1) return false;
     if (g_real.N < 1 || g_real.N > (1 << 30)) return false;
     const int D = digits_for(f);
     if (D < 2 || D > 8) return false;
     *p = ImplPlan{};
+    p->DA = DA > 0 ? DA : D;
+    p->OFF = OFF;
     p->ckk = int(g_real.C * g_real.KH * g_real.KW);
     p->gv = g_real;
     p->fold = fold_geom(pass, g_real, &p->gv);
@@ -114,14 +118,18 @@ bool make_plan(int pass, const PositFmt& f, const ConvGeom& g_real, bool raw, Im
         a.imgs_per_tile = ipt;
         a.Hb = Hb;
         a.cch = int(Cin / 32);
+        // forward: the x digits carry a stored zero ring (the weight gradient's
+        // layout, so the same digits serve both passes); input grad: TMA OOB fill
+        const int apad = pass == 0 ? g.pad : 0;
+        a.apad = apad;
         a.M = g.N * Ht * Wt;
         a.N = Cout;
         a.mtiles = tpi > 0 ? g.N * tpi : cdiv(g.N, ipt);
         a.ntiles = cdiv(Cout, p->NT);
         a.kbt = taps * Cin / 32;
         p->Ca = Cin;
-        p->Wa = Ws;
-        p->Ha = Hs;
+        p->Wa = Ws + 2 * apad;
+        p->Ha = Hs + 2 * apad;
         p->boxA[0] = uint32_t(2 * Wt);
         p->boxA[1] = uint32_t(Hb);
         p->boxA[2] = uint32_t(tpi > 0 ? 1 : ipt);
@@ -129,7 +137,8 @@ bool make_plan(int pass, const PositFmt& f, const ConvGeom& g_real, bool raw, Im
         p->boxA[4] = uint32_t(D);
         p->Kp = Cin;
         p->brows = Cout;
-        p->adig = size_t(D) * g.N * Hs * Ws * Cin;
+        // + margin: the weight gradient's dummy kx taps read up to 3 pixels past the end
+        p->adig = size_t(D) * g.N * p->Ha * p->Wa * Cin + 64;
         p->bdig = size_t(D) * Cout * taps * Cin;
         pos_nar = size_t(g.N) * Hs * Ws;
         if (pass == 0) {
@@ -170,9 +179,9 @@ bool make_plan(int pass, const PositFmt& f, const ConvGeom& g_real, bool raw, Im
         p->boxA[1] = uint32_t(OHb);
         p->boxA[2] = 4;   // kx taps of one group
         p->boxA[3] = 2;   // one 32-channel group
-        p->boxA[4] = uint32_t(D);
+        p->boxA[4] = uint32_t(p->DA);
         // + margin: the dummy kx taps of the last row read up to 3 pixels past it
-        p->adig = size_t(D) * g.N * p->Ha * p->Wa * g.C + 64;
+        p->adig = size_t(p->DA) * g.N * p->Ha * p->Wa * g.C + 64;
         p->bdig = size_t(D) * g.N * g.OH * g.OW * p->Fpw;
         chw_nar = size_t(g.C) * g.H * g.W;
         col_nar = size_t(p->Fpw);
@@ -199,7 +208,8 @@ bool make_plan(int pass, const PositFmt& f, const ConvGeom& g_real, bool raw, Im
     p->off_adig = take(p->adig);
     p->off_bdig = take(p->bdig);
     p->off_col_add = take(col_add);
-    p->off_lut = take(f.nbits <= kActLutBits ? size_t(8) << f.nbits : 0);
+    p->off_lut = take(size_t(8) << kActLutBits);   // digit LUTs by source code (<= 12 bits)
+    p->off_lut2 = take(size_t(8) << kActLutBits);
     p->off_maps = off;  // NaR maps and flags: zeroed by one memset
     p->off_pos_nar = take(pos_nar);
     p->off_chw_nar = take(chw_nar);
@@ -211,9 +221,14 @@ bool make_plan(int pass, const PositFmt& f, const ConvGeom& g_real, bool raw, Im
     return true;
 }
 
-uint32_t* lut_of(const ImplPlan& p, uint8_t* ws) {
-    return p.a.f.nbits <= kActLutBits ? reinterpret_cast<uint32_t*>(ws + p.off_lut) : nullptr;
+// digit LUT for codes of format fs digitised in the plan's format (null: decode
+// in registers, only when fs == f)
+uint32_t* lut_of(const ImplPlan& p, uint8_t* ws, const PositFmt& fs, int which = 0) {
+    return fs.nbits <= kActLutBits ? reinterpret_cast<uint32_t*>(ws + (which ? p.off_lut2 : p.off_lut))
+                                   : nullptr;
 }
+
+bool same_fmt(const PositFmt& a, const PositFmt& b) { return a.nbits == b.nbits && a.es == b.es; }
 
 PFN_cuTensorMapEncodeTiled_v12000 encoder() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -299,28 +314,30 @@ constexpr int acc_of() { return 1; }
 template <int MODE, int D>
 constexpr int nt_of() { return cps_of<MODE, D>() == 2 ? small_nt(D) : TileCfg<D>::NT; }
 
-template <int D, typename CodeT, int MODE>
+template <int D, typename CodeT, int MODE, int DA = D, int OFF = 0>
 cudaError_t launch_kernel(const CUtensorMap& tA, const CUtensorMap& tB, const IgemmArgs& a,
                           OutMap<CodeT> out, cudaStream_t st) {
     constexpr int NTT = nt_of<MODE, D>(), CPS = cps_of<MODE, D>(), ACC = acc_of<MODE, D>();
-    using Geo = ImplGeo<D, NTT, CPS, ACC>;
+    using Geo = ImplGeo<D, NTT, CPS, ACC, DA>;
     void (*k)(CUtensorMap, CUtensorMap, IgemmArgs, OutMap<CodeT>);
     if constexpr (D <= 3)
-        k = a.f.W <= 32 ? igemm_kernel<D, NTT, CPS, ACC, 1, CodeT, MODE>
-                        : igemm_kernel<D, NTT, CPS, ACC, 2, CodeT, MODE>;
+        k = a.f.W <= 32 ? igemm_kernel<D, NTT, CPS, ACC, 1, CodeT, MODE, 0, DA, OFF>
+                        : igemm_kernel<D, NTT, CPS, ACC, 2, CodeT, MODE, 0, DA, OFF>;
     else
-        k = a.f.W <= 64 ? igemm_kernel<D, NTT, CPS, ACC, 2, CodeT, MODE>
-                        : igemm_kernel<D, NTT, CPS, ACC, 4, CodeT, MODE>;
+        k = a.f.W <= 64 ? igemm_kernel<D, NTT, CPS, ACC, 2, CodeT, MODE, 0, DA, OFF>
+                        : igemm_kernel<D, NTT, CPS, ACC, 4, CodeT, MODE, 0, DA, OFF>;
     // BASELINE formats: epilogue specialised on the compile-time format
     const int fid = fixed_fmt_id(a.f);
-    if constexpr (D == 2 && sizeof(CodeT) == 1)
-        if (fid == 1) k = igemm_kernel<2, NTT, CPS, ACC, 1, CodeT, MODE, 1>;
-    if constexpr (D == 4 && sizeof(CodeT) == 1)
-        if (fid == 2) k = igemm_kernel<4, NTT, CPS, ACC, 2, CodeT, MODE, 2>;
+    if constexpr (DA == D) {
+        if constexpr (D == 2 && sizeof(CodeT) == 1)
+            if (fid == 1) k = igemm_kernel<2, NTT, CPS, ACC, 1, CodeT, MODE, 1>;
+        if constexpr (D == 4 && sizeof(CodeT) == 1)
+            if (fid == 2) k = igemm_kernel<4, NTT, CPS, ACC, 2, CodeT, MODE, 2>;
+        if constexpr (D == 8 && sizeof(CodeT) == 2)
+            if (fid == 4) k = igemm_kernel<8, NTT, CPS, ACC, 4, CodeT, MODE, 4>;
+    }
     if constexpr (D == 6 && sizeof(CodeT) == 2)
-        if (fid == 3) k = igemm_kernel<6, NTT, CPS, ACC, 4, CodeT, MODE, 3>;
-    if constexpr (D == 8 && sizeof(CodeT) == 2)
-        if (fid == 4) k = igemm_kernel<8, NTT, CPS, ACC, 4, CodeT, MODE, 4>;
+        if (fid == 3) k = igemm_kernel<6, NTT, CPS, ACC, 4, CodeT, MODE, 3, DA, OFF>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Geo::SMEM);
     if (e != cudaSuccess) return e;
     const int64_t tiles = a.mtiles * a.ntiles * a.splits;
@@ -345,22 +362,41 @@ cudaError_t dispatch(int D, const CUtensorMap& tA, const CUtensorMap& tB, const 
     }
 }
 
+// Weight-gradient A operands of DA planes at group offset OFF that have a
+// kernel: the symmetric case, and posit(8,1) forward digits under a posit(12,1)
+// gradient (BASELINE config 3: R 12 -> 20, one digit up).
+bool wgrad_variant(int D, int DA, int OFF) {
+    return (DA == D && OFF == 0) || (D == 6 && DA == 4 && OFF == 1);
+}
+
 template <typename CodeT>
-cudaError_t act_digits(int D, const CodeT* x, int64_t N, int64_t C, int64_t H, int64_t W,
-                       int64_t Cp, int pad, const PositFmt& f, uint32_t* lut, bool build_lut, int8_t* dig,
-                       uint8_t* pos_nar, uint8_t* chw_nar, uint8_t* chan_nar, uint8_t* any,
-                       cudaStream_t st) {
+cudaError_t dispatch_wgrad(int D, int DA, int OFF, const CUtensorMap& tA, const CUtensorMap& tB,
+                           const IgemmArgs& a, OutMap<CodeT> out, cudaStream_t st) {
+    if (DA == D && OFF == 0) return dispatch<CodeT, 2>(D, tA, tB, a, out, st);
+    if constexpr (sizeof(CodeT) == 2)
+        if (D == 6 && DA == 4 && OFF == 1) return launch_kernel<6, CodeT, 2, 4, 1>(tA, tB, a, out, st);
+    return cudaErrorInvalidValue;
+}
+
+// ---- digitisers: codes of format fs (uint8 for nbits <= 8, else uint16) ->
+// digits of the plan format f (through the conversion LUT when fs != f)
+
+template <typename SrcT>
+cudaError_t act_digits_t(int D, const SrcT* x, int64_t N, int64_t C, int64_t H, int64_t W, int64_t Cp,
+                         int pad, const PositFmt& f, const PositFmt& fs, uint32_t* lut, bool build_lut,
+                         int8_t* dig, uint8_t* pos_nar, uint8_t* chw_nar, uint8_t* chan_nar,
+                         uint8_t* any, cudaStream_t st) {
     // thread per (pixel, 32 channels): grid (pixel blocks, 32-channel chunks)
     if (N * H * W >= (int64_t(1) << 31)) return cudaErrorInvalidValue;
     const dim3 grid(unsigned((grid_for(N * H * W * (Cp / 32), 256) + Cp / 32 - 1) / (Cp / 32)),
                     unsigned(Cp / 32));
     const FastDiv fd_hw{uint32_t(H * W)}, fd_w{uint32_t(W)};
     if (lut == nullptr) build_lut = false;
-#define PNN_ACT(DD)                                                                              \
-    if (build_lut) digit_lut_kernel<DD><<<16, 256, 0, st>>>(f, lut);                             \
-    act_digits_kernel<DD, CodeT><<<grid, 256, 0, st>>>(x, int(N), int(C), int(H), int(W), int(Cp), \
-                                                       pad, fd_hw, fd_w, f, lut, dig, pos_nar,   \
-                                                       chw_nar, chan_nar, any)
+#define PNN_ACT(DD)                                                                                  \
+    if (build_lut) digit_lut_conv_kernel<DD><<<16, 256, 0, st>>>(fs, f, lut);                        \
+    act_digits_kernel<DD, SrcT><<<grid, 256, 0, st>>>(x, int(N), int(C), int(H), int(W), int(Cp),  \
+                                                      pad, fd_hw, fd_w, f, fs, lut, dig, pos_nar,   \
+                                                      chw_nar, chan_nar, any)
     switch (D) {
         case 2: PNN_ACT(2); break;
         case 3: PNN_ACT(3); break;
@@ -375,18 +411,30 @@ cudaError_t act_digits(int D, const CodeT* x, int64_t N, int64_t C, int64_t H, i
     return cudaGetLastError();
 }
 
-template <typename CodeT>
-cudaError_t im2col_digits(int D, const CodeT* x, const ConvGeom& g, const PositFmt& f, uint32_t* lut,
-                          int8_t* dig, uint8_t* pos_nar, uint8_t* chw_nar, uint8_t* any,
-                          cudaStream_t st) {
+cudaError_t act_digits(int D, const void* x, int64_t N, int64_t C, int64_t H, int64_t W, int64_t Cp,
+                       int pad, const PositFmt& f, const PositFmt& fs, uint32_t* lut, bool build_lut,
+                       int8_t* dig, uint8_t* pos_nar, uint8_t* chw_nar, uint8_t* chan_nar, uint8_t* any,
+                       cudaStream_t st) {
+    if (lut == nullptr && !same_fmt(f, fs)) return cudaErrorInvalidValue;  // no in-register convert
+    if (fs.nbits <= 8)
+        return act_digits_t(D, static_cast<const uint8_t*>(x), N, C, H, W, Cp, pad, f, fs, lut, build_lut,
+                            dig, pos_nar, chw_nar, chan_nar, any, st);
+    return act_digits_t(D, static_cast<const uint16_t*>(x), N, C, H, W, Cp, pad, f, fs, lut, build_lut,
+                        dig, pos_nar, chw_nar, chan_nar, any, st);
+}
+
+template <typename SrcT>
+cudaError_t im2col_digits_t(int D, const SrcT* x, const ConvGeom& g, const PositFmt& f,
+                            const PositFmt& fs, uint32_t* lut, int8_t* dig, uint8_t* pos_nar,
+                            uint8_t* chw_nar, uint8_t* any, cudaStream_t st) {
     const int grid = grid_for(g.N * g.OH * g.OW, 256);  // thread per output pixel
     if (g.N * g.OH * g.OW >= (int64_t(1) << 31)) return cudaErrorInvalidValue;
     const FastDiv fd_p{uint32_t(g.OH * g.OW)}, fd_ow{uint32_t(g.OW)};
 #define PNN_I2C(DD)                                                                          \
-    if (lut) digit_lut_kernel<DD><<<16, 256, 0, st>>>(f, lut);                               \
-    im2col_digits_kernel<DD, CodeT><<<grid, 256, 0, st>>>(                                   \
+    if (lut) digit_lut_conv_kernel<DD><<<16, 256, 0, st>>>(fs, f, lut);                      \
+    im2col_digits_kernel<DD, SrcT><<<grid, 256, 0, st>>>(                                   \
         x, int(g.N), int(g.C), int(g.H), int(g.W), int(g.KH), int(g.KW), g.pad, int(g.OH),   \
-        int(g.OW), fd_p, fd_ow, f, lut, dig, pos_nar, chw_nar, any)
+        int(g.OW), fd_p, fd_ow, f, fs, lut, dig, pos_nar, chw_nar, any)
     switch (D) {
         case 2: PNN_I2C(2); break;
         case 3: PNN_I2C(3); break;
@@ -399,6 +447,15 @@ cudaError_t im2col_digits(int D, const CodeT* x, const ConvGeom& g, const PositF
     }
 #undef PNN_I2C
     return cudaGetLastError();
+}
+
+cudaError_t im2col_digits(int D, const void* x, const ConvGeom& g, const PositFmt& f, const PositFmt& fs,
+                          uint32_t* lut, int8_t* dig, uint8_t* pos_nar, uint8_t* chw_nar, uint8_t* any,
+                          cudaStream_t st) {
+    if (lut == nullptr && !same_fmt(f, fs)) return cudaErrorInvalidValue;
+    if (fs.nbits <= 8)
+        return im2col_digits_t(D, static_cast<const uint8_t*>(x), g, f, fs, lut, dig, pos_nar, chw_nar, any, st);
+    return im2col_digits_t(D, static_cast<const uint16_t*>(x), g, f, fs, lut, dig, pos_nar, chw_nar, any, st);
 }
 
 template <typename CodeT>
@@ -427,31 +484,66 @@ cudaError_t weight_digits(int D, const CodeT* w, const CodeT* bias, int64_t F, i
 
 int rc_of(cudaError_t e) { return e == cudaSuccess ? 0 : 4; }
 
+// The forward pass's activation digits, kept for the weight gradient (the
+// "saved tensor" of the layer): [D_f][N][Ha][Ca/16][Wa][16] digits of x in the
+// forward format (zero ring stored; Ha/Wa/Ca of the wgrad plan), the NaR map
+// chw_nar (any image) and an any-NaR flag.
+struct SavedX {
+    int8_t* dig;
+    uint8_t* chw;
+    uint8_t* flag;
+};
+
+struct SaveLayout {
+    size_t dig, chw, total;  // offsets: chw at dig, flag at chw + chw bytes
+    size_t chw_bytes;
+};
+
+bool save_layout(const PositFmt& f, const ConvGeom& g, SaveLayout* L) {
+    ImplPlan pf, pw;
+    if (!make_plan(0, f, g, false, &pf) || !make_plan(2, f, g, false, &pw)) return false;
+    if (pf.fold != pw.fold) return false;
+    auto r256 = [](size_t b) { return (b + 255) & ~size_t(255); };
+    L->dig = r256(pf.adig);
+    L->chw_bytes = pw.fold ? size_t(pw.ckk) * g.OH * g.OW : size_t(g.C) * g.H * g.W;
+    L->chw = r256(L->chw_bytes);
+    L->total = L->dig + L->chw + 256;
+    return true;
+}
+
+SavedX saved_of(void* base, const SaveLayout& L) {
+    auto* b = static_cast<uint8_t*>(base);
+    return SavedX{reinterpret_cast<int8_t*>(b), b + L.dig, b + L.dig + L.chw};
+}
+
 template <typename CodeT>
 int run_fwd(const ImplPlan& p, const ConvGeom& g, const CodeT* x, const CodeT* w,
-            const CodeT* bias, CodeT* y, uint8_t* ws, cudaStream_t st) {
+            const CodeT* bias, CodeT* y, uint8_t* ws, cudaStream_t st, const SavedX* sv,
+            size_t sv_clear) {
     const PositFmt& f = p.a.f;
-    auto* adig = reinterpret_cast<int8_t*>(ws + p.off_adig);
+    auto* adig = sv ? sv->dig : reinterpret_cast<int8_t*>(ws + p.off_adig);
     auto* bdig = reinterpret_cast<int8_t*>(ws + p.off_bdig);
     auto* col_add = reinterpret_cast<int64_t*>(ws + p.off_col_add);
     uint8_t* pos_nar = ws + p.off_pos_nar;
     uint8_t* col_nar = ws + p.off_col_nar;
     uint8_t* flags = ws + p.off_flags;
+    uint8_t* xflag = sv ? sv->flag : flags;  // any NaR in x
     cudaError_t e;
     if ((e = cudaMemsetAsync(ws + p.off_maps, 0, p.maps_bytes, st)) != cudaSuccess) return 4;
+    if (sv && (e = cudaMemsetAsync(sv->chw, 0, sv_clear, st)) != cudaSuccess) return 4;
     const ConvGeom& gv = p.gv;  // virtual 1x1 geometry when the first layer is folded
     if (p.fold)
-        e = im2col_digits<CodeT>(p.D, x, g, f, lut_of(p, ws), adig, pos_nar, nullptr, flags, st);
+        e = im2col_digits(p.D, x, g, f, f, lut_of(p, ws, f), adig, pos_nar, sv ? sv->chw : nullptr, xflag, st);
     else
-        e = act_digits<CodeT>(p.D, x, g.N, g.C, g.H, g.W, p.Ca, 0, f, lut_of(p, ws), true, adig,
-                              pos_nar, nullptr, nullptr, flags, st);
+        e = act_digits(p.D, x, g.N, g.C, g.H, g.W, p.Ca, g.pad, f, f, lut_of(p, ws, f), true, adig,
+                       pos_nar, sv ? sv->chw : nullptr, nullptr, xflag, st);
     if (e != cudaSuccess) return 4;
     const int64_t taps = gv.KH * gv.KW;  // weights: [F][C*KH*KW] read as [F][ckk][1][1] if folded
     if ((e = weight_digits<CodeT>(p.D, w, bias, g.F, p.fold ? p.ckk : g.C, taps, p.Kp, 0, f, bdig,
                                   col_add, col_nar, flags + 1, st)) != cudaSuccess)
         return 4;
     CUtensorMap tA, tB;
-    if (!map_act(&tA, adig, p.D, gv.N, gv.H, gv.W, p.Ca, p.boxA) ||
+    if (!map_act(&tA, adig, p.D, gv.N, p.Ha, p.Wa, p.Ca, p.boxA) ||
         !map_weights(&tB, bdig, p.D, p.brows, taps * p.Kp, p.NT))
         return 5;
     IgemmArgs a = p.a;
@@ -465,29 +557,43 @@ int run_fwd(const ImplPlan& p, const ConvGeom& g, const CodeT* x, const CodeT* w
         quire_finalize_kernel<CodeT><<<grid_for(a.M * a.N, 256), 256, 0, st>>>(
             a.partial, int(a.splits), nullptr, col_nar, out, a.M, a.N, f, nullptr, nullptr);
     fwd_nar_fixup_kernel<CodeT><<<grid_for(a.M, 256), 256, 0, st>>>(
-        y, pos_nar, flags, g.N, int(g.F), int(gv.H), int(gv.W), int(g.OH), int(g.OW), int(gv.KH),
+        y, pos_nar, xflag, g.N, int(g.F), int(gv.H), int(gv.W), int(g.OH), int(g.OW), int(gv.KH),
         int(gv.KW), gv.pad, 1u << (f.nbits - 1));
     return rc_of(cudaGetLastError());
 }
 
+// Input gradient.  pre: dy already digitised in the plan's layout by the
+// weight-gradient pass (shared operand) -- its digits, pixel NaR map and
+// any-NaR flag; otherwise dy is digitised here.
+struct DyDigits {
+    const int8_t* dig;
+    const uint8_t* pos_nar;
+    const uint8_t* any;
+};
+
 template <typename CodeT>
 int run_dgrad(const ImplPlan& p, const ConvGeom& g, const CodeT* dy, const CodeT* w, CodeT* dx,
-              uint8_t* ws, cudaStream_t st) {
+              uint8_t* ws, cudaStream_t st, const DyDigits* pre = nullptr) {
     const PositFmt& f = p.a.f;
     auto* adig = reinterpret_cast<int8_t*>(ws + p.off_adig);
     auto* bdig = reinterpret_cast<int8_t*>(ws + p.off_bdig);
     uint8_t* pos_nar = ws + p.off_pos_nar;
     uint8_t* flags = ws + p.off_flags;
-    if (cudaMemsetAsync(ws + p.off_maps, 0, p.maps_bytes, st) != cudaSuccess) return 4;
-    if (act_digits<CodeT>(p.D, dy, g.N, g.F, g.OH, g.OW, p.Ca, 0, f, lut_of(p, ws), true, adig, pos_nar, nullptr, nullptr,
-                          flags, st) != cudaSuccess)
+    // (with pre, the caller cleared the maps before dy's digitiser filled pos_nar)
+    if (pre == nullptr && cudaMemsetAsync(ws + p.off_maps, 0, p.maps_bytes, st) != cudaSuccess) return 4;
+    if (pre == nullptr &&
+        act_digits(p.D, dy, g.N, g.F, g.OH, g.OW, p.Ca, 0, f, f, lut_of(p, ws, f), true, adig, pos_nar,
+                   nullptr, nullptr, flags, st) != cudaSuccess)
         return 4;
+    const int8_t* a_dig = pre ? pre->dig : adig;
+    const uint8_t* a_pos = pre ? pre->pos_nar : pos_nar;
+    const uint8_t* a_any = pre ? pre->any : flags;
     const int64_t taps = g.KH * g.KW;
     if (weight_digits<CodeT>(p.D, w, nullptr, g.F, g.C, taps, p.Kp, 1, f, bdig, nullptr, nullptr,
                              flags + 1, st) != cudaSuccess)
         return 4;
     CUtensorMap tA, tB;
-    if (!map_act(&tA, adig, p.D, g.N, g.OH, g.OW, p.Ca, p.boxA) ||
+    if (!map_act(&tA, const_cast<int8_t*>(a_dig), p.D, g.N, g.OH, g.OW, p.Ca, p.boxA) ||
         !map_weights(&tB, bdig, p.D, p.brows, taps * p.Kp, p.NT))
         return 5;
     IgemmArgs a = p.a;
@@ -502,45 +608,48 @@ int run_dgrad(const ImplPlan& p, const ConvGeom& g, const CodeT* dy, const CodeT
             a.partial, int(a.splits), nullptr, nullptr, out, a.M, a.N, f, nullptr, nullptr);
     const uint32_t nar = 1u << (f.nbits - 1);
     dgrad_nar_fixup_kernel<CodeT><<<grid_for(a.M, 256), 256, 0, st>>>(
-        dx, pos_nar, flags, g.N, int(g.C), int(g.H), int(g.W), int(g.OH), int(g.OW), int(g.KH),
+        dx, a_pos, a_any, g.N, int(g.C), int(g.H), int(g.W), int(g.OH), int(g.OW), int(g.KH),
         int(g.KW), g.pad, nar);
     dgrad_weight_nar_kernel<CodeT><<<grid_for(a.M * a.N, 256), 256, 0, st>>>(dx, w, g, flags + 1,
                                                                              nar);
     return rc_of(cudaGetLastError());
 }
 
+// Weight gradient in the plan's format f.  x: codes of format fx (digitised
+// here, converting through the LUT) unless sv holds the forward pass's saved
+// digits (p.DA planes at group offset p.OFF).  dy: codes of format fdy;
+// share_pos_nar != null also records dy's pixel NaR map for an input-gradient
+// pass that reuses these dy digits.
 template <typename CodeT>
-int run_wgrad(const ImplPlan& p, const ConvGeom& g, const CodeT* dy, const CodeT* x, CodeT* dw,
-              unsigned __int128* raw_words, uint8_t* raw_nar, uint8_t* ws, cudaStream_t st) {
+int run_wgrad(const ImplPlan& p, const ConvGeom& g, const void* dy, const PositFmt& fdy,
+              const void* x, const PositFmt& fx, CodeT* dw, unsigned __int128* raw_words,
+              uint8_t* raw_nar, uint8_t* ws, cudaStream_t st, const SavedX* sv = nullptr,
+              uint8_t* share_pos_nar = nullptr) {
     const PositFmt& f = p.a.f;
-    auto* adig = reinterpret_cast<int8_t*>(ws + p.off_adig);
+    auto* adig = sv ? sv->dig : reinterpret_cast<int8_t*>(ws + p.off_adig);
     auto* bdig = reinterpret_cast<int8_t*>(ws + p.off_bdig);
-    uint8_t* chw_nar = ws + p.off_chw_nar;
+    uint8_t* chw_nar = sv ? sv->chw : ws + p.off_chw_nar;
     uint8_t* col_nar = ws + p.off_col_nar;
     uint8_t* flags = ws + p.off_flags;
+    uint8_t* xflag = sv ? sv->flag : flags;
     if (cudaMemsetAsync(ws + p.off_maps, 0, p.maps_bytes, st) != cudaSuccess) return 4;
     const ConvGeom& gv = p.gv;  // virtual 1x1 geometry when the first layer is folded
-    cudaError_t e;
-    if (p.fold)
-        e = im2col_digits<CodeT>(p.D, x, g, f, lut_of(p, ws), adig, nullptr, chw_nar, flags, st);
-    else
-        e = act_digits<CodeT>(p.D, x, g.N, g.C, g.H, g.W, p.Ca, g.pad, f, lut_of(p, ws), true,
-                              adig, nullptr, chw_nar, nullptr, flags, st);
-    if (e != cudaSuccess) return 4;
-    if (!p.fold && g.pad > 0) {  // zero the pad ring of the padded x digits
-        const int64_t cells = int64_t(p.D) * g.N * (p.Ca / 16) *
-                              (int64_t(2 * g.pad) * (g.W + 2 * g.pad) + g.H * 2 * g.pad);
-        pad_zero_kernel<<<grid_for(cells, 256), 256, 0, st>>>(reinterpret_cast<uint4*>(adig),
-                                                              int64_t(p.D) * g.N, int(g.H), int(g.W),
-                                                              int(p.Ca / 16), g.pad);
+    cudaError_t e = cudaSuccess;
+    if (sv == nullptr) {
+        if (p.fold)
+            e = im2col_digits(p.D, x, g, f, fx, lut_of(p, ws, fx), adig, nullptr, chw_nar, flags, st);
+        else
+            e = act_digits(p.D, x, g.N, g.C, g.H, g.W, p.Ca, g.pad, f, fx, lut_of(p, ws, fx), true, adig,
+                           nullptr, chw_nar, nullptr, flags, st);
+        if (e != cudaSuccess) return 4;
     }
-    if (act_digits<CodeT>(p.D, dy, g.N, g.F, g.OH, g.OW, p.Fpw, 0, f, lut_of(p, ws), false, bdig, nullptr, nullptr, col_nar,
-                          flags + 1, st) != cudaSuccess)
+    if (act_digits(p.D, dy, g.N, g.F, g.OH, g.OW, p.Fpw, 0, f, fdy, lut_of(p, ws, fdy, 1), true, bdig,
+                   share_pos_nar, nullptr, col_nar, flags + 1, st) != cudaSuccess)
         return 4;
     CUtensorMap tA, tB;
     const uint32_t boxB[5] = {uint32_t(2 * p.a.OWb), uint32_t(p.a.OHb), 1, uint32_t(p.NT / 16),
                               uint32_t(p.D)};
-    if (!map_wgrad_x(&tA, adig, p.D, gv.N, p.Ha, p.Wa, p.Ca, p.boxA) ||
+    if (!map_wgrad_x(&tA, adig, p.DA, gv.N, p.Ha, p.Wa, p.Ca, p.boxA) ||
         !map_act(&tB, bdig, p.D, g.N, g.OH, g.OW, p.Fpw, boxB))
         return 5;
     IgemmArgs a = p.a;
@@ -557,14 +666,79 @@ int run_wgrad(const ImplPlan& p, const ConvGeom& g, const CodeT* dy, const CodeT
     out.kgroups = p.a.kgroups;
     out.cgroups = p.a.cgroups;
     out.cvalid = p.fold ? p.ckk : int(g.C);
-    if (dispatch<CodeT, 2>(p.D, tA, tB, a, out, st) != cudaSuccess) return 4;
+    if (dispatch_wgrad<CodeT>(p.D, p.DA, p.OFF, tA, tB, a, out, st) != cudaSuccess) return 4;
     if (use_partial)
         quire_finalize_kernel<CodeT><<<grid_for(a.M * a.N, 256), 256, 0, st>>>(
             a.partial, int(a.splits), nullptr, col_nar, out, a.M, a.N, f, raw_words, raw_nar);
     wgrad_nar_fixup_kernel<CodeT><<<grid_for(p.ckk, 128), 128, 0, st>>>(
-        dw, raw_nar, chw_nar, flags, int(g.F), p.fold ? p.ckk : int(g.C), int(gv.H), int(gv.W),
+        dw, raw_nar, chw_nar, xflag, int(g.F), p.fold ? p.ckk : int(g.C), int(gv.H), int(gv.W),
         int(g.OH), int(g.OW), int(gv.KH), int(gv.KW), gv.pad, 1u << (f.nbits - 1));
     return rc_of(cudaGetLastError());
+}
+
+// A saved forward digit tensor of format ff usable as the weight gradient's A
+// operand in format fg: same format, or an exact widening (same es, more bits)
+// by a whole number of digits with a kernel variant.  *DA / *OFF on success.
+bool saved_usable(const PositFmt& ff, const PositFmt& fg, int* DA, int* OFF) {
+    const int DF = digits_for(ff), DG = digits_for(fg);
+    if (same_fmt(ff, fg)) {
+        *DA = DG;
+        *OFF = 0;
+        return true;
+    }
+    if (ff.es != fg.es || fg.nbits <= ff.nbits) return false;
+    const int shift = fg.R - ff.R;  // X_g = X_f * 2^shift exactly
+    if (shift % 8) return false;
+    if (!wgrad_variant(DG, DF, shift / 8)) return false;
+    *DA = DF;
+    *OFF = shift / 8;
+    return true;
+}
+
+// Plans of the fused backward: weight gradient (format fg, A from the saved
+// digits when usable) and, when wanted, the input gradient (format fb).
+struct BwdPlan {
+    ImplPlan pw, pd;
+    bool has_dx, use_saved, share_dy;
+    size_t off_d, total;
+};
+
+bool make_bwd_plan(const PositFmt& ff, const PositFmt& fb, const PositFmt& fg, const ConvGeom& g,
+                   bool raw, bool has_dx, bool saved, BwdPlan* b) {
+    *b = BwdPlan{};
+    int DA = 0, OFF = 0;
+    b->use_saved = saved && saved_usable(ff, fg, &DA, &OFF);
+    if (!make_plan(2, fg, g, raw, &b->pw, b->use_saved ? DA : 0, b->use_saved ? OFF : 0)) return false;
+    // x / dy codes of another format are digitised through a conversion LUT
+    if (!b->use_saved && !same_fmt(ff, fg) && ff.nbits > kActLutBits) return false;
+    if (!same_fmt(fb, fg) && fb.nbits > kActLutBits) return false;
+    b->has_dx = has_dx;
+    if (has_dx && !make_plan(1, fb, g, false, &b->pd)) return false;
+    // dy digits shared when both passes see the same digits in the same layout
+    b->share_dy = has_dx && same_fmt(fb, fg) && b->pw.Fpw == g.F && b->pd.Ca == g.F;
+    b->off_d = (b->pw.total + 255) & ~size_t(255);
+    b->total = b->off_d + (has_dx ? b->pd.total : 0);
+    return true;
+}
+
+template <typename GT, typename BT>
+int run_backward(const BwdPlan& b, const ConvGeom& g, const PositFmt& ff, const PositFmt& fb,
+                 const void* dy, const void* x, const SavedX* sv, const void* w_bwd, void* dx, void* dw,
+                 unsigned __int128* raw_words, uint8_t* raw_nar, uint8_t* ws, cudaStream_t st) {
+    uint8_t* wsd = ws + b.off_d;
+    if (b.share_dy && cudaMemsetAsync(wsd + b.pd.off_maps, 0, b.pd.maps_bytes, st) != cudaSuccess) return 4;
+    int rc = run_wgrad<GT>(b.pw, g, dy, fb, x, ff, static_cast<GT*>(dw), raw_words, raw_nar, ws, st,
+                           b.use_saved ? sv : nullptr,
+                           b.share_dy ? wsd + b.pd.off_pos_nar : nullptr);
+    if (rc != 0 || !b.has_dx) return rc;
+    if (b.share_dy) {
+        const DyDigits pre{reinterpret_cast<const int8_t*>(ws + b.pw.off_bdig), wsd + b.pd.off_pos_nar,
+                           ws + b.pw.off_flags + 1};
+        return run_dgrad<BT>(b.pd, g, static_cast<const BT*>(dy), static_cast<const BT*>(w_bwd),
+                             static_cast<BT*>(dx), wsd, st, &pre);
+    }
+    return run_dgrad<BT>(b.pd, g, static_cast<const BT*>(dy), static_cast<const BT*>(w_bwd),
+                         static_cast<BT*>(dx), wsd, st);
 }
 
 }  // namespace
@@ -577,16 +751,31 @@ bool igemm_eligible(int pass, const PositFmt& f, const ConvGeom& g, bool raw, si
 }
 
 int igemm_conv_fwd(const PositFmt& f, const ConvGeom& g, const void* x, const void* w,
-                   const void* bias, void* y, void* ws, size_t ws_bytes, cudaStream_t st) {
+                   const void* bias, void* y, void* ws, size_t ws_bytes, cudaStream_t st,
+                   void* saved, size_t saved_bytes) {
     ImplPlan p;
     if (!make_plan(0, f, g, false, &p)) return 2;
     if (ws_bytes < p.total) return 3;
+    SaveLayout L{};
+    SavedX sv{};
+    if (saved != nullptr) {
+        if (!save_layout(f, g, &L)) return 2;
+        if (saved_bytes < L.total) return 3;
+        sv = saved_of(saved, L);
+    }
     auto* b = static_cast<uint8_t*>(ws);
+    const SavedX* svp = saved ? &sv : nullptr;
+    const size_t clear = L.chw + 16;  // NaR map + flag
     if (f.nbits <= 8)
         return run_fwd<uint8_t>(p, g, (const uint8_t*)x, (const uint8_t*)w, (const uint8_t*)bias,
-                                (uint8_t*)y, b, st);
+                                (uint8_t*)y, b, st, svp, clear);
     return run_fwd<uint16_t>(p, g, (const uint16_t*)x, (const uint16_t*)w, (const uint16_t*)bias,
-                             (uint16_t*)y, b, st);
+                             (uint16_t*)y, b, st, svp, clear);
+}
+
+size_t igemm_saved_bytes(const PositFmt& f, const ConvGeom& g) {
+    SaveLayout L;
+    return save_layout(f, g, &L) ? L.total : 0;
 }
 
 int igemm_conv_dgrad(const PositFmt& f, const ConvGeom& g, const void* dy, const void* w, void* dx,
@@ -608,10 +797,42 @@ int igemm_conv_wgrad(const PositFmt& f, const ConvGeom& g, const void* dy, const
     if (ws_bytes < p.total) return 3;
     auto* b = static_cast<uint8_t*>(ws);
     if (f.nbits <= 8)
-        return run_wgrad<uint8_t>(p, g, (const uint8_t*)dy, (const uint8_t*)x, (uint8_t*)dw,
-                                  raw_words, raw_nar, b, st);
-    return run_wgrad<uint16_t>(p, g, (const uint16_t*)dy, (const uint16_t*)x, (uint16_t*)dw,
-                               raw_words, raw_nar, b, st);
+        return run_wgrad<uint8_t>(p, g, dy, f, x, f, (uint8_t*)dw, raw_words, raw_nar, b, st);
+    return run_wgrad<uint16_t>(p, g, dy, f, x, f, (uint16_t*)dw, raw_words, raw_nar, b, st);
+}
+
+bool igemm_backward_eligible(const PositFmt& ff, const PositFmt& fb, const PositFmt& fg,
+                             const ConvGeom& g, bool raw, bool has_dx, bool saved, size_t* bytes) {
+    BwdPlan b;
+    if (!make_bwd_plan(ff, fb, fg, g, raw, has_dx, saved, &b)) return false;
+    if (bytes) *bytes = b.total;
+    return true;
+}
+
+int igemm_conv_backward(const PositFmt& ff, const PositFmt& fb, const PositFmt& fg, const ConvGeom& g,
+                        const void* dy, const void* x, const void* saved, size_t saved_bytes,
+                        const void* w_bwd, void* dx, void* dw, unsigned __int128* raw_words,
+                        uint8_t* raw_nar, void* ws, size_t ws_bytes, cudaStream_t st) {
+    BwdPlan b;
+    if (!make_bwd_plan(ff, fb, fg, g, raw_words != nullptr, dx != nullptr, saved != nullptr, &b)) return 2;
+    if (ws_bytes < b.total) return 3;
+    if (!b.use_saved && x == nullptr) return 2;  // saved digits unusable for this format pair
+    SavedX sv{};
+    if (b.use_saved) {
+        SaveLayout L;
+        if (!save_layout(ff, g, &L)) return 2;
+        if (saved_bytes < L.total) return 3;
+        sv = saved_of(const_cast<void*>(saved), L);
+    }
+    auto* w = static_cast<uint8_t*>(ws);
+    const bool g8 = fg.nbits <= 8, b8 = fb.nbits <= 8;
+    if (g8 && b8)
+        return run_backward<uint8_t, uint8_t>(b, g, ff, fb, dy, x, &sv, w_bwd, dx, dw, raw_words, raw_nar, w, st);
+    if (g8)
+        return run_backward<uint8_t, uint16_t>(b, g, ff, fb, dy, x, &sv, w_bwd, dx, dw, raw_words, raw_nar, w, st);
+    if (b8)
+        return run_backward<uint16_t, uint8_t>(b, g, ff, fb, dy, x, &sv, w_bwd, dx, dw, raw_words, raw_nar, w, st);
+    return run_backward<uint16_t, uint16_t>(b, g, ff, fb, dy, x, &sv, w_bwd, dx, dw, raw_words, raw_nar, w, st);
 }
 
 }  // namespace pnn_b200

@@ -27,6 +27,7 @@
 #include "epilogue.cuh"
 #include "fastdiv.cuh"
 #include "igemm.h"
+#include "posit_scalar.cuh"
 #include "quire_gemm_core.cuh"
 
 // PNN_IGEMM_DEBUG_HOOKS: compile the epilogue's profiling switches (a.debug
@@ -48,12 +49,15 @@ constexpr int kActLutBits = 12;  // digitiser LUT up to 4096 codes (32 KB, L1-re
 // flight per SM -- one CTA's TMEM drain and rounding overlap the other's MMAs
 // (a single CTA cannot double-buffer G*NT > 256 columns).  CPS 1 (weight grad,
 // whose few output tiles run long split-K loops): 512 columns, ~200 KB.
-template <int D, int NT_, int CPS, int ACC = 1>
+// DA: digit planes of the A operand (== D except in the weight gradient fed by
+// the forward pass's saved activation digits of a narrower, exactly widening
+// format: DA planes whose groups land OFF digit positions up, igemm_kernel).
+template <int D, int NT_, int CPS, int ACC = 1, int DA = D>
 struct ImplGeo {
     static constexpr int NT = NT_;
-    static constexpr int G = 2 * D - 1;
+    static constexpr int G = DA + D - 1;
     static constexpr int NMMA = D * NT;
-    static constexpr int A_BYTES = D * kBM * kIKB;
+    static constexpr int A_BYTES = DA * kBM * kIKB;
     static constexpr int B_BYTES = D * NT * kIKB;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
     static constexpr int BUDGET = CPS == 2 ? 104 * 1024 : 200 * 1024;
@@ -68,6 +72,7 @@ struct ImplGeo {
     static constexpr int THREADS = 64 + 32 * EPI;
     static_assert(G * NT <= (ACC == 2 ? ACC_STRIDE : int(TMEM_COLS)), "TMEM overflow");
     static_assert(ACC == 1 || CPS == 1, "double buffering needs the whole TMEM");
+    static_assert(DA >= 1 && DA <= D + 1, "zero-MMA initialisation covers DA <= D + 1");
     static_assert(NMMA % 16 == 0 && NMMA <= 256, "bad UMMA N");
     static_assert(STAGES >= 2, "pipeline depth");
     static_assert(A_BYTES % 1024 == 0 && B_BYTES % 512 == 0, "stage alignment");
@@ -87,6 +92,7 @@ struct IgemmArgs {
     // mode 2: K blocks of OWb x OHb output pixels; m-tile = one ky, 4 kx, 32 channels
     int taps, C, OWb, OHb, kpr, kpi;  // k-blocks per row-block set / per image
     int KH, kgroups, cgroups, Hp;     // kx groups of 4, 32-channel groups, padded height
+    int apad;  // mode 0: zero ring stored around the A digits (box coordinates shift by it)
     // tile raster (tile_coords) with launch-constant divisions: by mtiles * ntiles,
     // by kGroupM * ntiles, and by the group height (kGroupM, or the last group's)
     FastDiv fd_split, fd_group, fd_g8, fd_glast;
@@ -112,11 +118,17 @@ __device__ __forceinline__ void itile_coords(int64_t t64, const IgemmArgs& a, in
 
 // Epilogue warps: 8 (two CTAs per SM) or 16 (one): the epilogue (TMEM drain,
 // quire accumulation, quire -> posit) is latency-bound, so it gets the warps.
-template <int D, int NT_, int CPS, int ACC, int QW, typename CodeT, int MODE, int FMT = 0>
-__global__ void __launch_bounds__(ImplGeo<D, NT_, CPS, ACC>::THREADS, CPS)
+//
+// DA / OFF (mode 2 only): the A operand has DA digit planes of X_A * 256^-OFF
+// (the saved forward digits of an exactly widening format, X_g = X_f *
+// 2^(R_g - R_f), R_g - R_f = 8 * OFF); MMA group g is digit position g + OFF.
+template <int D, int NT_, int CPS, int ACC, int QW, typename CodeT, int MODE, int FMT = 0,
+          int DA = D, int OFF = 0>
+__global__ void __launch_bounds__(ImplGeo<D, NT_, CPS, ACC, DA>::THREADS, CPS)
     igemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  const IgemmArgs a, const OutMap<CodeT> out) {
-    using Geo = ImplGeo<D, NT_, CPS, ACC>;
+    static_assert(MODE == 2 || (DA == D && OFF == 0), "asymmetric digits: weight gradient only");
+    using Geo = ImplGeo<D, NT_, CPS, ACC, DA>;
     constexpr int kIEpiWarps = Geo::EPI;
     constexpr int kIThreads = Geo::THREADS;
     using QT = typename QuireWord<QW>::T;
@@ -198,9 +210,9 @@ __global__ void __launch_bounds__(ImplGeo<D, NT_, CPS, ACC>::THREADS, CPS)
                         // A box {w, h, n, 2 slices, D} -> [D][2][pixels][16 B]
                         const int tap = kb / a.cch, cc = kb - tap * a.cch;
                         const int ky = tap / a.KW, kx = tap - ky * a.KW;
-                        if constexpr (MODE == 0)
-                            ptx::tma_load_5d(sa, &tmA, 2 * (kx - a.pad), y0 + ky - a.pad, n0, 2 * cc, 0,
-                                             &full[s]);
+                        if constexpr (MODE == 0)  // apad: zero ring stored around the digits
+                            ptx::tma_load_5d(sa, &tmA, 2 * (kx - a.pad + a.apad), y0 + ky - a.pad + a.apad,
+                                             n0, 2 * cc, 0, &full[s]);
                         else
                             ptx::tma_load_5d(sa, &tmA, 2 * (a.pad - kx), y0 + a.pad - ky, n0, 2 * cc, 0,
                                              &full[s]);
@@ -254,9 +266,9 @@ __global__ void __launch_bounds__(ImplGeo<D, NT_, CPS, ACC>::THREADS, CPS)
                                                ? ptx::smem_desc_kmajor(b_base, 128, kIKB * 16)
                                                : ptx::smem_desc_kmajor(b_base, D * NT * 16, 128);
                     const bool first = i == 0;
-                    if (first) ptx::mma_i8(tacc + (D - 1) * NT, zdesc, bdesc, idesc, 0);
+                    if (first) ptx::mma_i8(tacc + (DA - 1) * NT, zdesc, bdesc, idesc, 0);
 #pragma unroll
-                    for (int p = 0; p < D; ++p) {
+                    for (int p = 0; p < DA; ++p) {
                         const uint32_t ap = a_base + p * (kBM * kIKB);
                         const uint64_t adesc = MODE == 2 ? ptx::smem_desc_kmajor(ap, 128, kIKB * 16)
                                                          : ptx::smem_desc_kmajor(ap, kBM * 16, 128);
@@ -305,7 +317,7 @@ __global__ void __launch_bounds__(ImplGeo<D, NT_, CPS, ACC>::THREADS, CPS)
                     for (int g = 0; g < GB; ++g)
                         if (g0 + g < G)
 #pragma unroll
-                            for (int x = 0; x < 8; ++x) acc[x].add(g0 + g, r[g][x]);
+                            for (int x = 0; x < 8; ++x) acc[x].add(g0 + g + OFF, r[g][x]);
                 }
 #pragma unroll
                 for (int x = 0; x < 8; ++x) q[c0 + x] = acc[x].get();
@@ -372,46 +384,30 @@ __global__ void __launch_bounds__(ImplGeo<D, NT_, CPS, ACC>::THREADS, CPS)
 
 // ------------------------------------------------------------- digitising
 
-// Digits of 4 consecutive channels (codes c[0..3]) written as one 4-byte word
-// per plane at dst + p * plane; returns a mask of NaR codes.
+// Digit words of convert(c, fs -> f) for every code c of the source format
+// fs (== digit_lut_kernel when fs == f): the digitisers then read codes of
+// one stage format and emit the digits of another (SURVEY.md Appendix A.6 stage
+// conversions) without a separate convert pass.
 template <int D>
-__device__ __forceinline__ uint32_t digits4(const uint32_t (&c)[4], const PositFmt& f,
-                                            const uint32_t* __restrict__ lut, int8_t* dst,
-                                            int64_t plane) {
-    const uint32_t nar_code = 1u << (f.nbits - 1);
-    uint32_t lo[4], hi[4], nm = 0;
-#pragma unroll
-    for (int jj = 0; jj < 4; ++jj) {
+__global__ void digit_lut_conv_kernel(PositFmt fs, PositFmt f, uint32_t* __restrict__ lut) {
+    const bool same = fs.nbits == f.nbits && fs.es == f.es;
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < (1 << fs.nbits);
+         c += gridDim.x * blockDim.x) {
+        uint32_t lo, hi;
         bool nar;
-        if (lut != nullptr) {
-            const uint2 v = __ldg(reinterpret_cast<const uint2*>(lut) + c[jj]);
-            lo[jj] = v.x;
-            hi[jj] = v.y;
-            nar = c[jj] == nar_code;
-        } else {
-            digit_words<D>(c[jj], f, lo[jj], hi[jj], nar);
-        }
-        nm |= nar ? 1u << jj : 0u;
+        digit_words<D>(same ? uint32_t(c) : p_convert(fs, f, uint32_t(c)), f, lo, hi, nar);
+        lut[2 * c] = lo;
+        lut[2 * c + 1] = hi;
     }
-    // 4 codes x D digit bytes -> one word per plane (byte transpose)
-#pragma unroll
-    for (int p = 0; p < D; ++p) {
-        const uint32_t* w = p < 4 ? lo : hi;
-        const uint32_t sel = (p & 3) | (((p & 3) + 4) << 4);
-        const uint32_t a = __byte_perm(w[0], w[1], sel);
-        const uint32_t b = __byte_perm(w[2], w[3], sel);
-        *reinterpret_cast<uint32_t*>(dst + p * plane) = __byte_perm(a, b, 0x5410);
-    }
-    return nm;
 }
 
-// As digits4, but the plane words go to registers: words[p][q] for 4-channel
-// group q (the caller stores whole 32-byte rows per plane).
+// Digits of 4 consecutive channels (codes c[0..3]) as one 4-byte word per
+// plane in registers: words[p][q] for 4-channel group q (the caller stores
+// whole 32-byte rows per plane); returns a mask of NaR codes.
 template <int D>
 __device__ __forceinline__ uint32_t digits4_words(const uint32_t (&c)[4], const PositFmt& f,
-                                                  const uint32_t* __restrict__ lut,
+                                                  uint32_t nar_code, const uint32_t* __restrict__ lut,
                                                   uint32_t (&words)[D][8], int q) {
-    const uint32_t nar_code = 1u << (f.nbits - 1);
     uint32_t lo[4], hi[4], nm = 0;
 #pragma unroll
     for (int jj = 0; jj < 4; ++jj) {
@@ -437,27 +433,32 @@ __device__ __forceinline__ uint32_t digits4_words(const uint32_t (&c)[4], const 
     return nm;
 }
 
-// codes [N][C][H][W] -> dig[D][N][H][W][Cp] (balanced int8 digits; channels
-// >= C are zero), plus NaR summaries written only where a NaR is found:
-// pos_nar[n][h][w] (any channel), chw_nar[c][h][w] (any image), chan_nar[c],
-// *any.  A thread owns one pixel x one 32-channel chunk: its 32 loads are
-// coalesced across the warp (consecutive pixels of one channel plane), and it
-// writes 32 contiguous digit bytes per plane (two 16-byte stores), so the
-// warp's stores are 1 KB contiguous per plane.  lut: digit_lut_kernel output
-// (formats up to 12 bits) or null (decode).
+// codes [N][C][H][W] -> dig[D][N][Hp][Cp/16][Wp][16] (slice layout, balanced
+// int8 digits; channels >= C are zero; Hp = H + 2 pad, Wp = W + 2 pad with the
+// pad ring written as zeros by the border pixels' threads), plus NaR summaries
+// written only where a NaR is found: pos_nar[n][h][w] (any channel),
+// chw_nar[c][h][w] (any image), chan_nar[c], *any.  A thread owns one pixel x
+// one 32-channel chunk: its 32 loads are coalesced across the warp
+// (consecutive pixels of one channel plane), and it writes 32 contiguous digit
+// bytes per plane (two 16-byte stores), so the warp's stores are 1 KB
+// contiguous per plane.  lut: digit words per SOURCE code (digit_lut_kernel:
+// the digits of convert(code, fs -> f), formats up to 12 bits) or null
+// (in-register decode; then fs == f).  fs: the codes' format (NaR pattern).
 // Grid: (pixel blocks, 32-channel chunks); 32-bit indices (pixels < 2^31,
 // checked by the launcher) with launch-constant divisions by multiplication.
 template <int D, typename CodeT>
 __global__ void __launch_bounds__(256) act_digits_kernel(
     const CodeT* __restrict__ x, int N, int C, int H, int W, int Cp, int pad, FastDiv fd_hw,
-    FastDiv fd_w, PositFmt f, const uint32_t* __restrict__ lut, int8_t* __restrict__ dig,
-    uint8_t* __restrict__ pos_nar, uint8_t* __restrict__ chw_nar, uint8_t* __restrict__ chan_nar,
-    uint8_t* __restrict__ any) {
+    FastDiv fd_w, PositFmt f, PositFmt fs, const uint32_t* __restrict__ lut,
+    int8_t* __restrict__ dig, uint8_t* __restrict__ pos_nar, uint8_t* __restrict__ chw_nar,
+    uint8_t* __restrict__ chan_nar, uint8_t* __restrict__ any) {
     const uint32_t HW = uint32_t(H) * uint32_t(W);
     const uint32_t pixels = uint32_t(N) * HW;
-    const int Hp = H + 2 * pad, Wp = W + 2 * pad;  // zero-padded image (weight grad)
+    const int Hp = H + 2 * pad, Wp = W + 2 * pad;
     const int64_t plane = int64_t(N) * Hp * Wp * Cp;
     const int cc = blockIdx.y;
+    const int CS = Cp / 16;
+    const uint32_t nar_code = 1u << (fs.nbits - 1);
     for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < pixels; r += gridDim.x * blockDim.x) {
         uint32_t n, pix;  // pixel raster index r = (n, h, w)
         fd_hw.divmod(r, n, pix);
@@ -471,18 +472,36 @@ __global__ void __launch_bounds__(256) act_digits_kernel(
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
             const uint32_t c4[4] = {code[4 * q], code[4 * q + 1], code[4 * q + 2], code[4 * q + 3]};
-            nm |= digits4_words<D>(c4, f, lut, words, q) << (4 * q);
+            nm |= digits4_words<D>(c4, f, nar_code, lut, words, q) << (4 * q);
         }
-        // slice layout [D][N][Hp][Cp/16][Wp][16]: this chunk = slices 2cc, 2cc+1
         uint32_t h, w;
         fd_w.divmod(pix, h, w);
-        int8_t* dst = dig + (((int64_t(n) * Hp + h + pad) * (Cp / 16) + 2 * cc) * Wp + w + pad) * 16;
+        // this chunk = slices 2cc, 2cc + 1 of pixel (h + pad, w + pad)
+        auto cell = [&](int hh, int ww) {
+            return dig + (((int64_t(n) * Hp + hh) * CS + 2 * cc) * Wp + ww) * 16;
+        };
+        int8_t* dst = cell(int(h) + pad, int(w) + pad);
 #pragma unroll
         for (int p = 0; p < D; ++p) {
             *reinterpret_cast<uint4*>(dst + p * plane) =
                 make_uint4(words[p][0], words[p][1], words[p][2], words[p][3]);
             *reinterpret_cast<uint4*>(dst + p * plane + int64_t(Wp) * 16) =
                 make_uint4(words[p][4], words[p][5], words[p][6], words[p][7]);
+        }
+        if (pad > 0 && (h == 0 || w == 0 || int(h) == H - 1 || int(w) == W - 1)) {
+            // border pixel: zero the ring cells of its row / column (corners by
+            // the corner pixels)
+            const int ylo = h == 0 ? 0 : int(h) + pad, yhi = int(h) == H - 1 ? Hp - 1 : int(h) + pad;
+            const int xlo = w == 0 ? 0 : int(w) + pad, xhi = int(w) == W - 1 ? Wp - 1 : int(w) + pad;
+            for (int hh = ylo; hh <= yhi; ++hh)
+                for (int ww = xlo; ww <= xhi; ++ww) {
+                    if (hh == int(h) + pad && ww == int(w) + pad) continue;
+                    int8_t* z = cell(hh, ww);
+                    for (int p = 0; p < D; ++p) {
+                        *reinterpret_cast<uint4*>(z + p * plane) = make_uint4(0, 0, 0, 0);
+                        *reinterpret_cast<uint4*>(z + p * plane + int64_t(Wp) * 16) = make_uint4(0, 0, 0, 0);
+                    }
+                }
         }
         if (nm) {
             for (int j = 0; j < 32; ++j)
@@ -496,34 +515,6 @@ __global__ void __launch_bounds__(256) act_digits_kernel(
     }
 }
 
-// Zero the pad cells of a padded slice-layout digit tensor
-// [D*N][Hp][CS][Wp] (16-byte cells): the top/bottom pad rows and the left/right
-// pad columns of every row.
-static __global__ void pad_zero_kernel(uint4* __restrict__ dig, int64_t DN, int H, int W, int CS,
-                                int pad) {
-    const int Hp = H + 2 * pad, Wp = W + 2 * pad;
-    const int64_t border = int64_t(2 * pad) * Wp + int64_t(H) * 2 * pad;
-    const int64_t total = DN * CS * border;
-    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total;
-         i += int64_t(gridDim.x) * blockDim.x) {
-        const int64_t b = i % border, rest = i / border;
-        const int cs = int(rest % CS);
-        const int64_t dn = rest / CS;
-        int hh, ww;
-        if (b < int64_t(2 * pad) * Wp) {
-            const int r = int(b / Wp);
-            hh = r < pad ? r : H + r;
-            ww = int(b % Wp);
-        } else {
-            const int64_t b2 = b - int64_t(2 * pad) * Wp;
-            hh = pad + int(b2 / (2 * pad));
-            const int c = int(b2 % (2 * pad));
-            ww = c < pad ? c : W + c;
-        }
-        dig[((dn * Hp + hh) * CS + cs) * Wp + ww] = make_uint4(0, 0, 0, 0);
-    }
-}
-
 // First-layer tap folding (C*KH*KW <= 32, stride 1): the receptive field of
 // each output pixel becomes the 32 "channels" of a virtual 1x1 convolution,
 // dig[D][N][OH][OW][32] with channel k = (c, ky, kx) (zero past C*KH*KW and
@@ -534,10 +525,11 @@ static __global__ void pad_zero_kernel(uint4* __restrict__ dig, int64_t DN, int 
 template <int D, typename CodeT>
 __global__ void __launch_bounds__(256) im2col_digits_kernel(
     const CodeT* __restrict__ x, int N, int C, int H, int W, int KH, int KW, int pad, int OH,
-    int OW, FastDiv fd_p, FastDiv fd_ow, PositFmt f, const uint32_t* __restrict__ lut,
+    int OW, FastDiv fd_p, FastDiv fd_ow, PositFmt f, PositFmt fs, const uint32_t* __restrict__ lut,
     int8_t* __restrict__ dig, uint8_t* __restrict__ pos_nar, uint8_t* __restrict__ chw_nar,
     uint8_t* __restrict__ any) {
     const int ckk = C * KH * KW, khw = KH * KW;
+    const uint32_t nar_code = 1u << (fs.nbits - 1);  // fs: the codes' format (lut converts)
     const uint32_t P = uint32_t(OH) * uint32_t(OW);
     const int64_t plane = int64_t(N) * P * 32;
     // receptive-field table: K index k -> (offset of (c, ky - pad, kx - pad) in
@@ -571,7 +563,7 @@ __global__ void __launch_bounds__(256) im2col_digits_kernel(
                              ? uint32_t(xn[s_off[k]])
                              : 0u;
             }
-            nm |= digits4_words<D>(c4, f, lut, words, q) << (4 * q);
+            nm |= digits4_words<D>(c4, f, nar_code, lut, words, q) << (4 * q);
         }
         // slice layout of the virtual [N][OH][2 slices][OW][16] image
         const int64_t row = int64_t(n) * OH + oy;

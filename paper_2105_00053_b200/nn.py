@@ -115,6 +115,7 @@ class Conv2d(Module):
         self.w = MixedParam(torch.from_numpy(w.astype(dt)).to(device), st)
         self.b = MixedParam(torch.from_numpy(b.astype(dt)).to(device), st)
         self.x = None
+        self.saved = None
 
     def params(self):
         return [self.w, self.b]
@@ -122,6 +123,14 @@ class Conv2d(Module):
     def forward(self, x):
         f = self.st.forward
         self.x = x
+        self.saved = None
+        if self.training:
+            # keep x's digit planes for the weight gradient (ops.conv2d_backward)
+            n = ops.conv2d_saved_bytes(f, x.shape, self.w.shape, self.stride, self.pad)
+            if n:
+                self.saved = torch.empty(n, dtype=torch.uint8, device=x.device)
+                return ops.conv2d_fwd_save(f, x, self.w.as_(f), self.b.as_(f), self.stride, self.pad,
+                                           self.saved)
         return ops.conv2d(f, x, self.w.as_(f), self.b.as_(f), self.stride, self.pad)
 
     def backward(self, dy, raw=False):
@@ -129,6 +138,20 @@ class Conv2d(Module):
         st = self.st
         g = st.gradient
         dyg = ops.convert_tensor(dy, st.backward, g)
+        fused = ops.conv2d_backward(st.forward, st.backward, g, dy, self.x, self.saved,
+                                    None if self.first_layer else self.w.as_(st.backward),
+                                    self.x.shape, self.w.shape, self.stride, self.pad,
+                                    need_dx=not self.first_layer, raw=raw)
+        self.saved = None
+        if fused is not None:
+            dx, dw = fused
+            if raw:
+                _, self.w.grad_words, self.w.grad_nar = dw
+                _, self.b.grad_words, self.b.grad_nar = ops.conv2d_bias_grad(g, dyg, raw=True)
+            else:
+                self.w.grad = dw
+                self.b.grad = ops.conv2d_bias_grad(g, dyg)
+            return dx
         xg = ops.convert_tensor(self.x, st.forward, g)
         if raw:
             _, self.w.grad_words, self.w.grad_nar = ops.conv2d_weight_grad(

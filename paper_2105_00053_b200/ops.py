@@ -317,6 +317,87 @@ def conv2d_weight_grad(cfg, dy, x, w_shape, stride: int, pad: int, use_quire: bo
     return (dw, words, nar) if raw else dw
 
 
+def conv2d_saved_bytes(cfg, x_shape, w_shape, stride: int, pad: int) -> int:
+    """Bytes of the forward's saved activation digits (0: no implicit
+    forward / weight-gradient pair for this geometry)."""
+    cfg = _cfg(cfg)
+    N, Cc, H, W = (int(v) for v in x_shape)
+    F, _, KH, KW = (int(v) for v in w_shape)
+    n = C.c_size_t()
+    _native.check(_native.lib().pnn_conv2d_saved_bytes(cfg.nbits, cfg.es, N, Cc, H, W, F, KH, KW, stride,
+                                                       pad, C.byref(n)))
+    return n.value
+
+
+def conv2d_fwd_save(cfg, x, w, bias, stride: int, pad: int, saved):
+    """conv2d that also leaves x's digit planes in `saved` (uint8 device tensor
+    of conv2d_saved_bytes) for conv2d_backward's weight gradient."""
+    cfg = _cfg(cfg)
+    _check_codes(cfg, x, w, bias)
+    x, w = x.contiguous(), w.contiguous()
+    bias = bias.contiguous() if bias is not None else None
+    N, Cc, H, W = x.shape
+    F, _, KH, KW = w.shape
+    OH, OW = (H + 2 * pad - KH) // stride + 1, (W + 2 * pad - KW) // stride + 1
+    y = torch.empty((N, F, OH, OW), dtype=cfg.code_dtype, device=x.device)
+    ws = _ws.get(x.device, _conv_ws(0, cfg, N, Cc, H, W, F, KH, KW, stride, pad, bias is not None))
+    _native.check(_native.lib().pnn_conv2d_fwd_save(
+        cfg.nbits, cfg.es, x.data_ptr(), N, Cc, H, W, w.data_ptr(), F, KH, KW,
+        bias.data_ptr() if bias is not None else None, stride, pad, y.data_ptr(), saved.data_ptr(),
+        saved.numel(), ws.data_ptr(), ws.numel(), _stream_ptr(x.device)))
+    return y
+
+
+def conv2d_backward_eligible(f_cfg, b_cfg, g_cfg, x_shape, w_shape, stride, pad, raw, has_dx, has_saved):
+    f, b, g = _cfg(f_cfg), _cfg(b_cfg), _cfg(g_cfg)
+    N, Cc, H, W = (int(v) for v in x_shape)
+    F, _, KH, KW = (int(v) for v in w_shape)
+    n = C.c_size_t()
+    rc = _native.lib().pnn_conv2d_backward_workspace(f.nbits, f.es, b.nbits, b.es, g.nbits, g.es, N, Cc, H, W,
+                                                     F, KH, KW, stride, pad, int(raw), int(has_dx),
+                                                     int(has_saved), C.byref(n))
+    return n.value if rc == 0 else None
+
+
+def conv2d_backward(f_cfg, b_cfg, g_cfg, dy, x, saved, w_bwd, x_shape, w_shape, stride: int, pad: int,
+                    need_dx: bool, raw: bool = False):
+    """Fused Conv2d layer backward:
+      dw = conv2d_weight_grad(p_g, convert(dy, p_b->p_g), convert(x, p_f->p_g))
+      dx = conv2d_input_grad(p_b, dy, w_bwd)           (need_dx)
+    reading the forward's saved digits (conv2d_fwd_save) when usable; dy digitised
+    once for both passes when p_b == p_g.  Returns (dx | None, dw) or, raw,
+    (dx | None, (None, words, nar)); None when the geometry / formats are not
+    eligible (use the per-pass calls)."""
+    f, b, g = _cfg(f_cfg), _cfg(b_cfg), _cfg(g_cfg)
+    nbytes = conv2d_backward_eligible(f, b, g, x_shape, w_shape, stride, pad, raw, need_dx, saved is not None)
+    if nbytes is None:
+        return None
+    _check_codes(b, dy, w_bwd if need_dx else None)
+    if x is not None:
+        _check_codes(f, x)
+        x = x.contiguous()
+    dy = dy.contiguous()
+    w_bwd = w_bwd.contiguous() if need_dx else None
+    N, Cc, H, W = (int(v) for v in x_shape)
+    F, _, KH, KW = (int(v) for v in w_shape)
+    dev = dy.device
+    dx = torch.empty((N, Cc, H, W), dtype=b.code_dtype, device=dev) if need_dx else None
+    dw = words = nar = None
+    if raw:
+        words = torch.empty((F, Cc, KH, KW, 2), dtype=torch.int64, device=dev)
+        nar = torch.empty((F, Cc, KH, KW), dtype=torch.uint8, device=dev)
+    else:
+        dw = torch.empty((F, Cc, KH, KW), dtype=g.code_dtype, device=dev)
+    ws = _ws.get(dev, nbytes)
+    ptr = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
+    _native.check(_native.lib().pnn_conv2d_backward(
+        f.nbits, f.es, b.nbits, b.es, g.nbits, g.es, dy.data_ptr(), ptr(x), ptr(saved),
+        saved.numel() if saved is not None else 0, ptr(w_bwd),
+        N, Cc, H, W, F, KH, KW, stride, pad, ptr(dx), ptr(dw), ptr(words), ptr(nar), ws.data_ptr(),
+        ws.numel(), _stream_ptr(dev)))
+    return dx, ((None, words, nar) if raw else dw)
+
+
 def _bias_grad(cfg, dy3, raw=False, use_quire=True):
     N, F, P = dy3.shape
     db = torch.empty((F,), dtype=cfg.code_dtype, device=dy3.device)

@@ -1,0 +1,139 @@
+"""Layer-level Conv2d pair (pnn_conv2d_fwd_save / pnn_conv2d_backward): the
+forward keeps x's digit planes, the fused backward reads them for the weight
+gradient (same format, or an exact widening by whole digits: posit(8,1)
+forward digits under a posit(12,1) gradient, BASELINE config 3), folds the
+stage conversions into its digitisers and digitises dy once for both passes.
+Every output must equal the per-pass calls of the same step -- the weight
+gradient of the converted operands (conv2d_weight_grad(p_g, convert(dy),
+convert(x))) and the input gradient (conv2d_input_grad(p_b, dy, w)) --, which
+the implicit-conv tests pin to the oracle; one case is checked against the
+oracle directly."""
+import numpy as np
+import pytest
+import torch
+
+from conftest import rand_codes
+from paper_2105_00053_b200 import ops
+
+pytestmark = pytest.mark.gpu
+
+P80, P81, P121, P161 = (8, 0), (8, 1), (12, 1), (16, 1)
+
+# (forward, backward, gradient) stage formats
+STAGES = [
+    (P81, P121, P121),  # config 3: saved (8,1) digits one digit up, dy shared
+    (P80, P80, P80),    # uniform (config 4)
+    (P81, P81, P81),
+    (P121, P121, P121),
+    (P161, P161, P161),
+    (P80, P121, P121),  # es differs: x digitised through the conversion LUT
+    (P121, P161, P161),  # widening without a kernel variant: LUT path
+    (P121, P81, P121),  # p_b != p_g: dy converted in the weight-gradient digitiser
+]
+
+# (N, C, H, W, F, K, pad)
+SHAPES = [
+    (2, 32, 8, 8, 32, 3, 1),
+    (3, 32, 16, 16, 64, 3, 1),
+    (2, 64, 16, 16, 64, 3, 1),
+    (2, 3, 32, 32, 32, 3, 1),    # folded first layer
+    (2, 32, 10, 10, 32, 3, 0),   # valid conv (fwd box inside the image; no implicit dgrad)
+    (2, 32, 8, 8, 40, 3, 1),     # F not a multiple of the N tile: dy digits not shared
+]
+
+
+def dev(cfg, a):
+    return torch.from_numpy(np.ascontiguousarray(a).astype(ops._cfg(cfg).np_code_dtype)).cuda()
+
+
+def host(t):
+    torch.cuda.synchronize()
+    return t.cpu().numpy().astype(np.int64).astype(np.uint64)
+
+
+def run_pair(ff, fb, fg, x, w, b, dy, wb, K, pad, need_dx, raw):
+    n = ops.conv2d_saved_bytes(ff, x.shape, w.shape, 1, pad)
+    saved = torch.empty(n, dtype=torch.uint8, device="cuda") if n else None
+    y = (ops.conv2d_fwd_save(ff, x, w, b, 1, pad, saved) if saved is not None
+         else ops.conv2d(ff, x, w, b, 1, pad))
+    res = ops.conv2d_backward(ff, fb, fg, dy, x, saved, wb, x.shape, w.shape, 1, pad, need_dx, raw=raw)
+    return y, res
+
+
+@pytest.mark.parametrize("stages", STAGES)
+@pytest.mark.parametrize("shape", SHAPES)
+def test_fused_backward_equals_per_pass(cuda, stages, shape):
+    ff, fb, fg = stages
+    N, C, H, W, F, K, pad = shape
+    rng = np.random.default_rng(hash((stages, shape)) & 0xFFFF)
+    x = dev(ff, rand_codes(rng, ff[0], (N, C, H, W)))
+    w = dev(ff, rand_codes(rng, ff[0], (F, C, K, K)))
+    b = dev(ff, rand_codes(rng, ff[0], (F,)))
+    OH, OW = H + 2 * pad - K + 1, W + 2 * pad - K + 1
+    dy = dev(fb, rand_codes(rng, fb[0], (N, F, OH, OW)))
+    wb = dev(fb, rand_codes(rng, fb[0], (F, C, K, K)))
+    need_dx = C % 32 == 0 and F % 32 == 0 and pad > 0  # implicit input grad: C, F % 32, pad = K // 2
+    y, res = run_pair(ff, fb, fg, x, w, b, dy, wb, K, pad, need_dx, raw=False)
+    assert res is not None, "fused backward should be eligible for this shape"
+    dx, dw = res
+    assert (host(y) == host(ops.conv2d(ff, x, w, b, 1, pad))).all()
+    dyg = ops.convert_tensor(dy, fb, fg)
+    xg = ops.convert_tensor(x, ff, fg)
+    want_dw = host(ops.conv2d_weight_grad(fg, dyg, xg, w.shape, 1, pad))
+    assert (host(dw) == want_dw).all(), int((host(dw) != want_dw).sum())
+    if need_dx:
+        want_dx = host(ops.conv2d_input_grad(fb, dy, wb, x.shape, 1, pad))
+        assert (host(dx) == want_dx).all(), int((host(dx) != want_dx).sum())
+    else:
+        assert dx is None
+    # raw quire words (data-parallel input) equal the per-pass raw words
+    _, res = run_pair(ff, fb, fg, x, w, b, dy, wb, K, pad, False, raw=True)
+    _, words, nar = res[1]
+    _, ww, wn = ops.conv2d_weight_grad(fg, dyg, xg, w.shape, 1, pad, raw=True)
+    assert (host(words) == host(ww)).all() and (host(nar) == host(wn)).all()
+
+
+@pytest.mark.parametrize("stages", [(P81, P121, P121), (P80, P80, P80), (P161, P161, P161)])
+def test_fused_backward_nar(cuda, stages):
+    """NaR in x (saved NaR map), in dy (shared pixel map / channel map), in w."""
+    ff, fb, fg = stages
+    N, C, H, W, F, K, pad = 2, 32, 8, 8, 32, 3, 1
+    rng = np.random.default_rng(7)
+    xa = rand_codes(rng, ff[0], (N, C, H, W))
+    xa[1, 5, 0, 7] = 1 << (ff[0] - 1)
+    dya = rand_codes(rng, fb[0], (N, F, H, W))
+    dya[0, 9, 3, 3] = 1 << (fb[0] - 1)
+    wba = rand_codes(rng, fb[0], (F, C, K, K))
+    wba[4, 2, 1, 1] = 1 << (fb[0] - 1)
+    x, dy, wb = dev(ff, xa), dev(fb, dya), dev(fb, wba)
+    w = dev(ff, rand_codes(rng, ff[0], (F, C, K, K)))
+    y, (dx, dw) = run_pair(ff, fb, fg, x, w, None, dy, wb, K, pad, True, raw=False)
+    dyg, xg = ops.convert_tensor(dy, fb, fg), ops.convert_tensor(x, ff, fg)
+    assert (host(dw) == host(ops.conv2d_weight_grad(fg, dyg, xg, w.shape, 1, pad))).all()
+    assert (host(dx) == host(ops.conv2d_input_grad(fb, dy, wb, x.shape, 1, pad))).all()
+    assert (host(y) == host(ops.conv2d(ff, x, w, None, 1, pad))).all()
+
+
+def test_fused_backward_vs_oracle(cuda, po):
+    """Config-3 stage formats against the oracle restatement directly."""
+    ff, fb, fg = P81, P121, P121
+    N, C, H, W, F, K, pad = 2, 32, 8, 8, 32, 3, 1
+    rng = np.random.default_rng(11)
+    xa = rand_codes(rng, 8, (N, C, H, W))
+    dya = rand_codes(rng, 12, (N, F, H, W))
+    wba = rand_codes(rng, 12, (F, C, K, K))
+    x, dy, wb = dev(ff, xa), dev(fb, dya), dev(fb, wba)
+    w = dev(ff, rand_codes(rng, 8, (F, C, K, K)))
+    _, (dx, dw) = run_pair(ff, fb, fg, x, w, None, dy, wb, K, pad, True, raw=False)
+    xg = po.convert_tensor(8, 1, 12, 1, xa.astype(np.uint64))
+    want_dw = po.conv2d_weight_grad(12, 1, dya.astype(np.uint64), xg, (F, C, K, K), 1, pad)
+    want_dx = po.conv2d_input_grad(12, 1, dya.astype(np.uint64), wba.astype(np.uint64), (N, C, H, W), 1, pad)
+    assert (host(dw).reshape(want_dw.shape) == want_dw).all()
+    assert (host(dx).reshape(want_dx.shape) == want_dx).all()
+
+
+def test_saved_bytes_zero_when_ineligible(cuda):
+    # LeNet conv2 (6 -> 16 channels): no implicit pair, the layer uses the per-pass path
+    assert ops.conv2d_saved_bytes(P161, (4, 6, 14, 14), (16, 6, 5, 5), 1, 0) == 0
+    assert ops.conv2d_backward(P161, P161, P161, torch.zeros((4, 16, 10, 10), dtype=torch.int16).cuda(),
+                               None, None, None, (4, 6, 14, 14), (16, 6, 5, 5), 1, 0, False) is None
