@@ -148,10 +148,18 @@ int pnn_relu_fwd(int nbits, int es, const void* x, void* y, int64_t n, void* str
 /* dx = x > 0 ? dy : 0 with x in (x_nbits, x_es) and dy/dx in (g_nbits, g_es). */
 int pnn_relu_bwd(int x_nbits, int x_es, const void* x, int g_nbits, int g_es, const void* dy,
                  void* dx, int64_t n, void* stream);
+/* argmax may be NULL for 2x2 / stride-2 tiled pooling (the layer then
+ * recomputes it in pnn_maxpool2d_bwd_x instead of storing 8 bytes per output). */
 int pnn_maxpool2d_fwd(int nbits, int es, const void* x, int64_t N, int64_t C, int64_t H,
                       int64_t W, int k, int stride, void* y, int64_t* argmax, void* stream);
 int pnn_maxpool2d_bwd(int nbits, int es, const void* dy, const int64_t* argmax, int64_t N,
                       int64_t C, int64_t H, int64_t W, int k, int stride, void* dx, void* stream);
+/* maxpool2d_backward(dy, argmax of maxpool2d(x)) with the argmax recomputed
+ * from the pooled input x (x in (x_nbits, x_es), dy/dx in (g_nbits, g_es));
+ * 2x2 / stride-2 tiled windows (else PNN_EUNSUPPORTED: use the argmax pair). */
+int pnn_maxpool2d_bwd_x(int x_nbits, int x_es, const void* x, int g_nbits, int g_es, const void* dy,
+                        int64_t N, int64_t C, int64_t H, int64_t W, int k, int stride, void* dx,
+                        void* stream);
 /* logits [B, classes] in the loss format; labels int32 [B]; outputs dlogits
  * [B, classes] (already scaled by 2^-log2_batch), per-row losses [B], the
  * batch loss (1 code, may be NULL) and/or the raw quire word (16 bytes) + NaR
@@ -183,6 +191,13 @@ int pnn_sgd_step_scaled(int opt_nbits, int opt_es, void* master, int g_nbits, in
                         const void* grad, int64_t n, uint32_t lr_code, int c1_nbits, int c1_es,
                         void* copy1, int c2_nbits, int c2_es, void* copy2, int grad_scale_log2,
                         void* stream);
+/* The optimizer step of several parameter tensors (same formats) in one
+ * launch: tensor i is pnn_sgd_step_scaled on (masters[i], grads[i], ns[i],
+ * copy1s[i], copy2s[i]); copy1s / copy2s may be NULL (no such stage copy). */
+int pnn_sgd_step_multi(int opt_nbits, int opt_es, int g_nbits, int g_es, uint32_t lr_code, int c1_nbits,
+                       int c1_es, int c2_nbits, int c2_es, int grad_scale_log2, int count,
+                       void* const* masters, const void* const* grads, void* const* copy1s,
+                       void* const* copy2s, const int64_t* ns, void* stream);
 /* avgpool2d / avgpool2d_backward (tensor_ops.cpp:672-720): window sum (quire
  * when use_quire, else an add chain) times the caller-quantized reciprocal. */
 int pnn_avgpool2d_fwd(int nbits, int es, const void* x, int64_t N, int64_t C, int64_t H,

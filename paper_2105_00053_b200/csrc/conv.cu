@@ -319,6 +319,100 @@ __global__ void __launch_bounds__(256) bias_grad_partial_kernel(
     }
 }
 
+// P > 1 bias gradient in one launch.  grid (slices, F): block (slice, f) sums
+// X over its share of the (image, pixel) range of channel f -- 16-byte loads,
+// X from a shared-memory table (LUTB = 1 << nbits entries, formats up to 12
+// bits; LUTB = 0 decodes in registers) --, writes one 128-bit partial, and the
+// last block of the channel (arrival counter) sums the partials in slice order
+// and rounds once: Q = 2^R * sum X (mod 2^W), the reference's
+// accumulate_value per term (tensor_ops.cpp:605-618, quire.hpp:62-67).
+template <typename CodeT, int LUTB>
+__global__ void __launch_bounds__(256) bias_grad_chan_kernel(
+    const CodeT* __restrict__ dy, int64_t N, int64_t F, int64_t P, PositFmt f, int slices,
+    FastDiv fd_vpr, const int64_t* __restrict__ xlut, unsigned __int128* __restrict__ partial,
+    uint8_t* __restrict__ nar_flag, unsigned int* __restrict__ arrivals, CodeT* __restrict__ out,
+    unsigned __int128* raw_words, uint8_t* raw_nar) {
+    __shared__ int64_t s_lut[LUTB];
+    __shared__ unsigned __int128 warp_s[8];
+    __shared__ bool s_last;
+    // the per-call X table (x_lut_kernel) -> shared memory, 16-byte copies
+    for (int i = threadIdx.x; i < LUTB / 2; i += blockDim.x)
+        reinterpret_cast<int4*>(s_lut)[i] = __ldg(reinterpret_cast<const int4*>(xlut) + i);
+    __syncthreads();
+    const int64_t ch = blockIdx.y, slice = blockIdx.x;
+    const int64_t per = (N + slices - 1) / slices;
+    const int64_t n0 = min(N, slice * per), n1 = min(N, n0 + per);  // trailing slices may be empty
+    const uint32_t nar_code = 1u << (f.nbits - 1);
+    // two independent accumulators of <= 32 terms of |X| <= 2^56 each between
+    // flushes into the 128-bit sum (no int64 wrap)
+    __int128 acc = 0;
+    bool nar = false;
+    constexpr int VE = 16 / int(sizeof(CodeT));
+    auto vsum = [&](const uint4& w) {
+        const uint32_t* ww = reinterpret_cast<const uint32_t*>(&w);
+        int64_t t = 0;
+#pragma unroll
+        for (int j = 0; j < VE; ++j) {
+            const uint32_t code = sizeof(CodeT) == 1 ? (ww[j >> 2] >> (8 * (j & 3))) & 0xFFu
+                                                     : (ww[j >> 1] >> (16 * (j & 1))) & 0xFFFFu;
+            t += s_lut[code];
+            nar |= code == nar_code;
+        }
+        return t;  // |t| <= 16 * 2^56
+    };
+    const uint32_t vpr = uint32_t(P / VE), nv = uint32_t((n1 - n0) * vpr);
+    const CodeT* base = dy + (n0 * F + ch) * P;
+    const int64_t img_stride = F * P;
+    uint32_t i = threadIdx.x;
+    for (; i + blockDim.x < nv; i += 2 * blockDim.x) {
+        uint32_t q0, r0, q1, r1;
+        fd_vpr.divmod(i, q0, r0);
+        fd_vpr.divmod(i + blockDim.x, q1, r1);
+        const uint4 w0 = __ldg(reinterpret_cast<const uint4*>(base + q0 * img_stride) + r0);
+        const uint4 w1 = __ldg(reinterpret_cast<const uint4*>(base + q1 * img_stride) + r1);
+        acc += vsum(w0) + vsum(w1);  // 2 * 16 * 2^56 < 2^62
+    }
+    if (i < nv) {
+        uint32_t q0, r0;
+        fd_vpr.divmod(i, q0, r0);
+        acc += vsum(__ldg(reinterpret_cast<const uint4*>(base + q0 * img_stride) + r0));
+    }
+    unsigned __int128 sum = (unsigned __int128)acc;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const uint64_t l2 = __shfl_xor_sync(0xFFFFFFFFu, uint64_t(sum), o);
+        const uint64_t h2 = __shfl_xor_sync(0xFFFFFFFFu, uint64_t(sum >> 64), o);
+        sum += (unsigned __int128)l2 | ((unsigned __int128)h2 << 64);
+    }
+    nar = __syncthreads_or(nar) != 0;
+    if ((threadIdx.x & 31) == 0) warp_s[threadIdx.x >> 5] = sum;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned __int128 t = 0;
+        for (int k = 0; k < int(blockDim.x >> 5); ++k) t += warp_s[k];
+        partial[ch * slices + slice] = t;
+        if (nar) nar_flag[ch] = 1;
+        __threadfence();
+        s_last = atomicAdd(&arrivals[ch], 1u) == unsigned(slices - 1);
+    }
+    __syncthreads();
+    if (!s_last || threadIdx.x != 0) return;
+    __threadfence();
+    const volatile unsigned __int128* vp = partial + ch * slices;
+    unsigned __int128 tot = 0;
+    for (int k = 0; k < slices; ++k) tot += vp[k];
+    const bool any_nar = *reinterpret_cast<volatile uint8_t*>(nar_flag + ch) != 0;
+    const unsigned __int128 one = 1;
+    const unsigned __int128 wmask = f.W >= 128 ? ~(unsigned __int128)0 : ((one << f.W) - 1);
+    const unsigned __int128 q = (tot << f.R) & wmask;  // accumulate_value: X * 2^R
+    if (raw_words) {
+        raw_words[ch] = q;
+        raw_nar[ch] = any_nar;
+    }
+    if (out) out[ch] = CodeT(any_nar ? nar_code : quire_word_to_posit(f, q));
+    arrivals[ch] = 0;  // ready for the next call (graph replays)
+}
+
 // X (the exact integer image) of every code of a format, for table decode.
 __global__ void x_lut_kernel(PositFmt f, int64_t* __restrict__ lut) {
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
@@ -623,9 +717,11 @@ static size_t bias_lut_offset(int64_t F) {
     return (size_t(F) * 16 * 64 + size_t(F) + 255) & ~size_t(255);
 }
 
+static size_t bias_arrivals_offset(int64_t F) { return bias_lut_offset(F) + (size_t(8) << kBiasLutBits); }
+
 int pnn_bias_grad_workspace(int64_t F, size_t* bytes) {
     if (F < 0 || !bytes) return set_status(PNN_EINVAL, "conv: invalid shape or argument");
-    *bytes = bias_lut_offset(F) + (size_t(8) << kBiasLutBits);
+    *bytes = bias_arrivals_offset(F) + size_t(F) * 4;
     return PNN_OK;
 }
 
@@ -644,10 +740,13 @@ int pnn_bias_grad(int nbits, int es, const void* dy, int64_t N, int64_t F, int64
     auto* nar = static_cast<uint8_t*>(workspace) + size_t(F) * 16 * 64;
     auto st = static_cast<cudaStream_t>(stream);
     cudaMemsetAsync(nar, 0, size_t(F), st);
-    cudaMemsetAsync(partial, 0, size_t(F) * 16 * slices, st);
+    // single-launch path below: table-decoded formats, 16-byte rows
+    const bool chan = P > 1 && nbits <= kBiasLutBits && P % (nbits <= 8 ? 16 : 8) == 0 &&
+                      (reinterpret_cast<uintptr_t>(dy) & 15) == 0;
+    if (!chan) cudaMemsetAsync(partial, 0, size_t(F) * 16 * slices, st);
     const dim3 grid{unsigned(F), unsigned(slices), 1u};
     int64_t* xlut = nullptr;
-    if (nbits <= kBiasLutBits && N * P >= 4096) {  // table pays for itself
+    if (!chan && nbits <= kBiasLutBits && N * P >= 4096) {  // table pays for itself
         xlut = reinterpret_cast<int64_t*>(static_cast<uint8_t*>(workspace) + bias_lut_offset(F));
         x_lut_kernel<<<(1 << nbits) / 256 + 1, 256, 0, st>>>(f, xlut);
     }
@@ -664,6 +763,31 @@ int pnn_bias_grad(int nbits, int es, const void* dy, int64_t N, int64_t F, int64
         bias_grad_final_kernel<uint16_t><<<grid_for(F, 128), 128, 0, st>>>(
             partial, slices, nar, F, f, (uint16_t*)db, (unsigned __int128*)raw_words,
             (uint8_t*)raw_nar);
+    } else if (chan) {
+        // channel-uniform blocks, X table in shared memory, last-block rounding;
+        // >= 8 blocks per SM, each at least one image
+        auto* arrivals = reinterpret_cast<unsigned int*>(static_cast<uint8_t*>(workspace) +
+                                                         bias_arrivals_offset(F));
+        auto* lut = reinterpret_cast<int64_t*>(static_cast<uint8_t*>(workspace) + bias_lut_offset(F));
+        cudaMemsetAsync(arrivals, 0, size_t(F) * 4, st);
+        x_lut_kernel<<<(1 << nbits) / 256 + 1, 256, 0, st>>>(f, lut);
+        int64_t want = (int64_t(8) * 148 + F - 1) / F;
+        int sl = int(want > 64 ? 64 : want);
+        if (sl > N) sl = int(N < 1 ? 1 : N);
+        const int VE = nbits <= 8 ? 16 : 8;
+        const int64_t per = (N + sl - 1) / sl;
+        if (P % VE || per * P / VE >= (int64_t(1) << 31) || (reinterpret_cast<uintptr_t>(dy) & 15))
+            return set_status(PNN_EUNSUPPORTED, "bias_grad: unaligned rows");
+        const FastDiv fd{uint32_t(P / VE)};
+        const dim3 g2{unsigned(sl), unsigned(F), 1u};
+#define PNN_BGC(T, B)                                                                             \
+    bias_grad_chan_kernel<T, B><<<g2, 256, 0, st>>>((const T*)dy, N, F, P, f, sl, fd, lut, partial, \
+                                                    nar, arrivals, (T*)db,                        \
+                                                    (unsigned __int128*)raw_words, (uint8_t*)raw_nar)
+        if (nbits <= 8) PNN_BGC(uint8_t, 256);
+        else if (nbits <= 10) PNN_BGC(uint16_t, 1024);
+        else PNN_BGC(uint16_t, 4096);
+#undef PNN_BGC
     } else if (nbits <= 8) {
         bias_grad_partial_kernel<uint8_t><<<grid, 256, 0, st>>>((const uint8_t*)dy, N, F, P, f,
                                                                  slices, xlut, partial, nar);

@@ -129,6 +129,128 @@ __global__ void maxpool_fwd_tiled_kernel(PositFmt f, int b, const void* x, int N
     }
 }
 
+// ---- 2x2 / stride-2 pooling, 16-byte vectors (the training step's layers) ----
+// Posit order is the order of the sign-extended patterns (NaR lowest,
+// posit.cpp:514-520), so the first-strict-max of a window (row-major window
+// order, tensor_ops.cpp:620-656) is a signed integer compare.  A thread covers
+// WPT = 16 / sizeof(TX) / 2 adjacent windows of one output row: two 16-byte x
+// loads (the window's two input rows).
+
+template <typename TX>
+__device__ __forceinline__ void load_codes16(const TX* p, uint32_t (&c)[16 / sizeof(TX)]) {
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(p));
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int j = 0; j < int(16 / sizeof(TX)); ++j)
+        c[j] = sizeof(TX) == 1 ? (w[j >> 2] >> (8 * (j & 3))) & 0xFFu : (w[j >> 1] >> (16 * (j & 1))) & 0xFFFFu;
+}
+
+__device__ __forceinline__ uint4 pack16_u8(const uint32_t* c) {
+    uint32_t w[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+        w[q] = (c[4 * q] & 0xFF) | (c[4 * q + 1] & 0xFF) << 8 | (c[4 * q + 2] & 0xFF) << 16 |
+               (c[4 * q + 3] & 0xFF) << 24;
+    return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+__device__ __forceinline__ uint4 pack8_u16(const uint32_t* c) {
+    return make_uint4((c[0] & 0xFFFF) | c[1] << 16, (c[2] & 0xFFFF) | c[3] << 16,
+                      (c[4] & 0xFFFF) | c[5] << 16, (c[6] & 0xFFFF) | c[7] << 16);
+}
+
+// window index (0..3, row-major) of the first strict maximum
+__device__ __forceinline__ int argmax4(int32_t a, int32_t b, int32_t c, int32_t d) {
+    int i = 0;
+    int32_t m = a;
+    if (b > m) { m = b; i = 1; }
+    if (c > m) { m = c; i = 2; }
+    if (d > m) { i = 3; }
+    return i;
+}
+
+template <typename TX>
+__global__ void __launch_bounds__(256) maxpool2_fwd_vec_kernel(int nbits, const TX* __restrict__ x,
+                                                               TX* __restrict__ y, int rows, int OW) {
+    constexpr int VE = 16 / sizeof(TX), WPT = VE / 2;
+    const int W = 2 * OW, vpr = OW / WPT;  // vectors per output row
+    const int total = rows * vpr;          // rows = N * C * OH
+    const int sh = 32 - nbits;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+        const int r = i / vpr, v = i - r * vpr;
+        const TX* p0 = x + (int64_t(r) * 2) * W + v * VE;
+        uint32_t a[VE], b[VE];
+        load_codes16<TX>(p0, a);
+        load_codes16<TX>(p0 + W, b);
+        uint32_t out[WPT];
+#pragma unroll
+        for (int j = 0; j < WPT; ++j) {
+            const uint32_t c[4] = {a[2 * j], a[2 * j + 1], b[2 * j], b[2 * j + 1]};
+            const int k = argmax4(int32_t(c[0] << sh), int32_t(c[1] << sh), int32_t(c[2] << sh),
+                                  int32_t(c[3] << sh));
+            out[j] = c[k];
+        }
+        TX* q = y + int64_t(r) * OW + v * WPT;
+        if constexpr (sizeof(TX) == 1) {
+            *reinterpret_cast<uint2*>(q) = make_uint2(out[0] | out[1] << 8 | out[2] << 16 | out[3] << 24,
+                                                      out[4] | out[5] << 8 | out[6] << 16 | out[7] << 24);
+        } else {
+            *reinterpret_cast<uint2*>(q) = make_uint2(out[0] | out[1] << 16, out[2] | out[3] << 16);
+        }
+    }
+}
+
+// dx = maxpool2d_backward(dy, argmax(x)) without a stored argmax: the window's
+// first strict max is recomputed from x; dy (format of TG) lands there, zeros
+// elsewhere (tiled windows: every input lies in exactly one window).
+template <typename TX, typename TG>
+__global__ void __launch_bounds__(256) maxpool2_bwd_x_kernel(int x_nbits, const TX* __restrict__ x,
+                                                             const TG* __restrict__ dy,
+                                                             TG* __restrict__ dx, int rows, int OW) {
+    constexpr int VE = 16 / sizeof(TX), WPT = VE / 2;
+    const int W = 2 * OW, vpr = OW / WPT;
+    const int total = rows * vpr;
+    const int sh = 32 - x_nbits;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+        const int r = i / vpr, v = i - r * vpr;
+        const int64_t in0 = (int64_t(r) * 2) * W + v * VE;
+        uint32_t a[VE], b[VE];
+        load_codes16<TX>(x + in0, a);
+        load_codes16<TX>(x + in0 + W, b);
+        uint32_t g[WPT];
+        const TG* gp = dy + int64_t(r) * OW + v * WPT;
+#pragma unroll
+        for (int j = 0; j < WPT; ++j) g[j] = uint32_t(gp[j]);
+        uint32_t top[16] = {}, bot[16] = {};  // VE used (pack16_u8 reads 16)
+#pragma unroll
+        for (int j = 0; j < WPT; ++j) {
+            const int k = argmax4(int32_t(a[2 * j] << sh), int32_t(a[2 * j + 1] << sh),
+                                  int32_t(b[2 * j] << sh), int32_t(b[2 * j + 1] << sh));
+            top[2 * j] = k == 0 ? g[j] : 0u;
+            top[2 * j + 1] = k == 1 ? g[j] : 0u;
+            bot[2 * j] = k == 2 ? g[j] : 0u;
+            bot[2 * j + 1] = k == 3 ? g[j] : 0u;
+        }
+        // VE codes of TG per row: 16-byte vector stores (VE * sizeof(TG) bytes)
+        TG* o0 = dx + in0;
+        TG* o1 = o0 + W;
+        if constexpr (sizeof(TG) == 1 && VE == 8) {  // 8 bytes per row
+            const uint4 a0 = pack16_u8(top), a1 = pack16_u8(bot);
+            *reinterpret_cast<uint2*>(o0) = make_uint2(a0.x, a0.y);
+            *reinterpret_cast<uint2*>(o1) = make_uint2(a1.x, a1.y);
+        } else if constexpr (sizeof(TG) == 1) {
+            *reinterpret_cast<uint4*>(o0) = pack16_u8(top);
+            *reinterpret_cast<uint4*>(o1) = pack16_u8(bot);
+        } else {
+#pragma unroll
+            for (int h = 0; h < VE / 8; ++h) {
+                reinterpret_cast<uint4*>(o0)[h] = pack8_u16(top + 8 * h);
+                reinterpret_cast<uint4*>(o1)[h] = pack8_u16(bot + 8 * h);
+            }
+        }
+    }
+}
+
 // ---- vectorised elementwise paths (16-byte accesses, 8 codes per thread-step)
 
 template <typename T>
@@ -353,6 +475,42 @@ __global__ void sgd_kernel(PositFmt fo, int bo, void* master, PositFmt fg, int b
     }
 }
 
+// The optimizer step of a whole model in one launch: segments = parameter
+// tensors (same formats), a grid-stride loop over their concatenation, the
+// segment found by binary search in the prefix table (kernel parameter, so the
+// launch needs no host->device copy and is CUDA-graph capturable).
+constexpr int kSgdMaxSeg = 48;
+struct SgdSegs {
+    int count;
+    int64_t start[kSgdMaxSeg + 1];  // prefix offsets
+    void* master[kSgdMaxSeg];
+    const void* grad[kSgdMaxSeg];
+    void* copy1[kSgdMaxSeg];
+    void* copy2[kSgdMaxSeg];
+};
+
+__global__ void sgd_multi_kernel(PositFmt fo, int bo, PositFmt fg, int bg, uint32_t lr, PositFmt f1,
+                                 int b1, PositFmt f2, int b2, int grad_scale_log2,
+                                 const __grid_constant__ SgdSegs segs) {
+    const int64_t total = segs.start[segs.count];
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        int lo = 0, hi = segs.count - 1;  // last segment with start <= i
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (segs.start[mid] <= i) lo = mid;
+            else hi = mid - 1;
+        }
+        const int64_t k = i - segs.start[lo];
+        uint32_t g = p_convert(fg, fo, load_any(segs.grad[lo], k, bg));
+        if (grad_scale_log2 != 0) g = p_ldexp(fo, g, -grad_scale_log2);
+        const uint32_t w = p_sub(fo, load_any(segs.master[lo], k, bo), p_mul(fo, lr, g));
+        store_any(segs.master[lo], k, bo, w);
+        if (segs.copy1[lo]) store_any(segs.copy1[lo], k, b1, p_convert(fo, f1, w));
+        if (segs.copy2[lo]) store_any(segs.copy2[lo], k, b2, p_convert(fo, f2, w));
+    }
+}
+
 // avgpool2d, tensor_ops.cpp:672-691: window sum (quire: exact, one rounding;
 // sequential: add chain in (ky,kx) order) then mul by the caller-quantized
 // reciprocal (scale, :763-769).
@@ -536,6 +694,14 @@ int pnn_relu_bwd(int x_nbits, int x_es, const void* x, int g_nbits, int g_es, co
     return launched("relu_bwd");
 }
 
+// 2x2 / stride 2 exactly tiled, 16-byte vectors of x fit whole output rows
+static bool pool2_vec_ok(int nbits, int64_t N, int64_t C, int64_t H, int64_t W, int k, int stride,
+                         const void* x) {
+    const int64_t wpt = nbits <= 8 ? 8 : 4;
+    return k == 2 && stride == 2 && H % 2 == 0 && W % (2 * wpt) == 0 && aligned16(x) &&
+           N * C * H * W < (int64_t(1) << 31);
+}
+
 int pnn_maxpool2d_fwd(int nbits, int es, const void* x, int64_t N, int64_t C, int64_t H,
                       int64_t W, int k, int stride, void* y, int64_t* argmax, void* stream) {
     CHECK_FMT(nbits, es);
@@ -543,6 +709,19 @@ int pnn_maxpool2d_fwd(int nbits, int es, const void* x, int64_t N, int64_t C, in
         return set_status(PNN_EINVAL, "maxpool2d: window larger than input");
     const int64_t OH = (H - k) / stride + 1, OW = (W - k) / stride + 1;
     if (N == 0) return PNN_OK;
+    if (argmax == nullptr && pool2_vec_ok(nbits, N, C, H, W, k, stride, x) && aligned16(y)) {
+        // no argmax wanted (the layer recomputes it in pnn_maxpool2d_bwd_x)
+        const int rows = int(N * C * OH), wpt = nbits <= 8 ? 8 : 4;
+        const int grid = grid1(int64_t(rows) * (OW / wpt));
+        if (nbits <= 8)
+            maxpool2_fwd_vec_kernel<uint8_t><<<grid, 256, 0, (cudaStream_t)stream>>>(
+                nbits, (const uint8_t*)x, (uint8_t*)y, rows, int(OW));
+        else
+            maxpool2_fwd_vec_kernel<uint16_t><<<grid, 256, 0, (cudaStream_t)stream>>>(
+                nbits, (const uint16_t*)x, (uint16_t*)y, rows, int(OW));
+        return launched("maxpool2d_fwd");
+    }
+    if (argmax == nullptr) return set_status(PNN_EINVAL, "maxpool2d: argmax output required");
     if (k == stride && H == OH * k && W == OW * k && N * C * H * W < (int64_t(1) << 31))
         maxpool_fwd_tiled_kernel<<<grid1(N * C * OH * OW), 256, 0, (cudaStream_t)stream>>>(
             make_fmt(nbits, es), bytes_of(nbits), x, int(N * C), int(OH), int(OW), k, y, argmax);
@@ -550,6 +729,31 @@ int pnn_maxpool2d_fwd(int nbits, int es, const void* x, int64_t N, int64_t C, in
         maxpool_fwd_kernel<<<grid1(N * C * OH * OW), 256, 0, (cudaStream_t)stream>>>(
             make_fmt(nbits, es), bytes_of(nbits), x, N * C, H, W, k, stride, OH, OW, y, argmax);
     return launched("maxpool2d_fwd");
+}
+
+int pnn_maxpool2d_bwd_x(int x_nbits, int x_es, const void* x, int g_nbits, int g_es, const void* dy,
+                        int64_t N, int64_t C, int64_t H, int64_t W, int k, int stride, void* dx,
+                        void* stream) {
+    CHECK_FMT(x_nbits, x_es);
+    CHECK_FMT(g_nbits, g_es);
+    if (N < 0 || C < 1 || k < 1 || stride < 1 || H < k || W < k || !x || !dy || !dx)
+        return set_status(PNN_EINVAL, "maxpool2d_backward: bad shape");
+    if (N == 0) return PNN_OK;
+    if (!pool2_vec_ok(x_nbits, N, C, H, W, k, stride, x))
+        return set_status(PNN_EUNSUPPORTED, "maxpool2d_bwd_x: 2x2/2 tiled, W a multiple of the vector");
+    const int rows = int(N * C * (H / 2)), OW = int(W / 2), wpt = x_nbits <= 8 ? 8 : 4;
+    const int grid = grid1(int64_t(rows) * (OW / wpt));
+    auto st = (cudaStream_t)stream;
+    const bool x8 = x_nbits <= 8, g8 = g_nbits <= 8;
+#define PNN_MPB(TX, TG)                                                                    \
+    maxpool2_bwd_x_kernel<TX, TG><<<grid, 256, 0, st>>>(x_nbits, (const TX*)x, (const TG*)dy, \
+                                                        (TG*)dx, rows, OW)
+    if (x8 && g8) PNN_MPB(uint8_t, uint8_t);
+    else if (x8) PNN_MPB(uint8_t, uint16_t);
+    else if (g8) PNN_MPB(uint16_t, uint8_t);
+    else PNN_MPB(uint16_t, uint16_t);
+#undef PNN_MPB
+    return launched("maxpool2d_bwd_x");
 }
 
 int pnn_maxpool2d_bwd(int nbits, int es, const void* dy, const int64_t* argmax, int64_t N,
@@ -630,6 +834,43 @@ int pnn_sgd_step_scaled(int opt_nbits, int opt_es, void* master, int g_nbits, in
         bytes_of(g_nbits), grad, n, lr_code, f1, bytes_of(f1.nbits), copy1, f2,
         bytes_of(f2.nbits), copy2, grad_scale_log2);
     return launched("sgd_step");
+}
+
+int pnn_sgd_step_multi(int opt_nbits, int opt_es, int g_nbits, int g_es, uint32_t lr_code, int c1_nbits,
+                       int c1_es, int c2_nbits, int c2_es, int grad_scale_log2, int count,
+                       void* const* masters, const void* const* grads, void* const* copy1s,
+                       void* const* copy2s, const int64_t* ns, void* stream) {
+    CHECK_FMT(opt_nbits, opt_es);
+    CHECK_FMT(g_nbits, g_es);
+    if (count < 0 || (count > 0 && (!masters || !grads || !ns)))
+        return set_status(PNN_EINVAL, "sgd_multi: bad arguments");
+    const bool has1 = copy1s != nullptr, has2 = copy2s != nullptr;
+    if (has1) CHECK_FMT(c1_nbits, c1_es);
+    if (has2) CHECK_FMT(c2_nbits, c2_es);
+    const PositFmt fo = make_fmt(opt_nbits, opt_es), fg = make_fmt(g_nbits, g_es);
+    const PositFmt f1 = has1 ? make_fmt(c1_nbits, c1_es) : fo, f2 = has2 ? make_fmt(c2_nbits, c2_es) : fo;
+    for (int base = 0; base < count; base += kSgdMaxSeg) {
+        SgdSegs sg{};
+        sg.count = 0;
+        int64_t tot = 0;
+        for (int i = base; i < count && i < base + kSgdMaxSeg; ++i) {
+            if (ns[i] < 0 || (ns[i] > 0 && (!masters[i] || !grads[i])))
+                return set_status(PNN_EINVAL, "sgd_multi: bad arguments");
+            const int j = sg.count++;
+            sg.start[j] = tot;
+            sg.master[j] = masters[i];
+            sg.grad[j] = grads[i];
+            sg.copy1[j] = has1 ? copy1s[i] : nullptr;
+            sg.copy2[j] = has2 ? copy2s[i] : nullptr;
+            tot += ns[i];
+        }
+        sg.start[sg.count] = tot;
+        if (tot == 0) continue;
+        sgd_multi_kernel<<<grid1(tot), 256, 0, (cudaStream_t)stream>>>(
+            fo, bytes_of(opt_nbits), fg, bytes_of(g_nbits), lr_code, f1, bytes_of(f1.nbits), f2,
+            bytes_of(f2.nbits), grad_scale_log2, sg);
+    }
+    return launched("sgd_step_multi");
 }
 
 int pnn_avgpool2d_fwd(int nbits, int es, const void* x, int64_t N, int64_t C, int64_t H,

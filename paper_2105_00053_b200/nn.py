@@ -199,14 +199,23 @@ class MaxPool2d(Module):
     def __init__(self, k, st: StagePrecisions, stride=None):
         self.k, self.stride, self.st = k, stride or k, st
         self.argmax = None
+        self.x = None
         self.x_shape = None
 
     def forward(self, x):
         self.x_shape = x.shape
+        self.x = self.argmax = None
+        y = ops.maxpool2d_noidx(self.st.forward, x, self.k, self.stride)
+        if y is not None:  # 2x2 tiled: keep x, recompute the argmax in backward
+            self.x = x
+            return y
         y, self.argmax = ops.maxpool2d(self.st.forward, x, self.k, self.stride)
         return y
 
     def backward(self, dy, raw=False):
+        if self.x is not None:
+            return ops.maxpool2d_backward_x(self.st.forward, self.x, self.st.backward, dy, self.k,
+                                            self.stride)
         return ops.maxpool2d_backward(self.st.backward, dy, self.argmax, self.x_shape, self.k,
                                       self.stride)
 
@@ -454,6 +463,19 @@ class SGD:
 
     def step(self):
         st = self.st
+        if not self.momentum and self.params:
+            # one launch for the whole model (all parameters share the stage formats)
+            fmts = self.params[0].stage_formats()
+            if all(p.stage_formats() == fmts for p in self.params):
+                fused = fmts[:2]
+                ops.sgd_step_multi(st.optimizer, st.gradient, self.lr_code, [p.master for p in self.params],
+                                   [p.grad for p in self.params], fused,
+                                   [tuple(p.copies[c] for c in fused) for p in self.params],
+                                   self.grad_scale_log2)
+                for p in self.params:
+                    for c in fmts[2:]:
+                        p.copies[c] = ops.convert_tensor(p.master, st.optimizer, c)
+                return
         for i, p in enumerate(self.params):
             fmts = p.stage_formats()
             fused = [(c, p.copies[c]) for c in fmts[:2]]  # refreshed inside the SGD kernel

@@ -499,6 +499,33 @@ def maxpool2d_backward(cfg, dy, argmax, x_shape, k: int = 2, stride: int = 2):
     return dx
 
 
+def maxpool2d_noidx(cfg, x, k: int, stride: int):
+    """maxpool2d output only (2x2 / stride-2 tiled; None when not eligible):
+    the layer recomputes the argmax in maxpool2d_backward_x."""
+    cfg = _cfg(cfg)
+    x = x.contiguous()
+    N, Cc, H, W = x.shape
+    wpt = 8 if cfg.nbits <= 8 else 4
+    if not (k == 2 and stride == 2 and H % 2 == 0 and W % (2 * wpt) == 0):
+        return None
+    y = torch.empty((N, Cc, H // 2, W // 2), dtype=x.dtype, device=x.device)
+    _native.check(_native.lib().pnn_maxpool2d_fwd(cfg.nbits, cfg.es, x.data_ptr(), N, Cc, H, W, k, stride,
+                                                  y.data_ptr(), None, _stream_ptr(x.device)))
+    return y
+
+
+def maxpool2d_backward_x(x_cfg, x, g_cfg, dy, k: int = 2, stride: int = 2):
+    """maxpool2d_backward(dy, argmax(maxpool2d(x))) with the argmax recomputed from x."""
+    xc, gc = _cfg(x_cfg), _cfg(g_cfg)
+    x = x.contiguous()
+    N, Cc, H, W = x.shape
+    dx = torch.empty((N, Cc, H, W), dtype=gc.code_dtype, device=dy.device)
+    _native.check(_native.lib().pnn_maxpool2d_bwd_x(xc.nbits, xc.es, x.data_ptr(), gc.nbits, gc.es,
+                                                    dy.contiguous().data_ptr(), N, Cc, H, W, k, stride,
+                                                    dx.data_ptr(), _stream_ptr(dy.device)))
+    return dx
+
+
 def softmax_xent(cfg, logits, labels, log2_batch: int, raw: bool = False, grad_scale_log2: int = 0):
     """SURVEY.md Appendix A.5 -> (loss code tensor [1], dlogits, loss_rows[, raw word, raw nar]).
     grad_scale_log2 = s multiplies dlogits by 2^s (loss scaling)."""
@@ -548,6 +575,28 @@ def sgd_step(opt_cfg, master, g_cfg, grad, lr_code: int, copies=(), grad_scale_l
                                                     c2.nbits, c2.es, t2.data_ptr() if t2 is not None else None,
                                                     int(grad_scale_log2), _stream_ptr(master.device)))
     return master
+
+
+def sgd_step_multi(opt_cfg, g_cfg, lr_code: int, masters, grads, copy_cfgs=(), copies=(),
+                   grad_scale_log2: int = 0):
+    """sgd_step over several tensors in one launch; copies[i] = tuple of up to
+    two stage-copy tensors of masters[i] in the formats copy_cfgs."""
+    oc, gc = _cfg(opt_cfg), _cfg(g_cfg)
+    n = len(masters)
+    if n == 0:
+        return
+    cfgs = [_cfg(c) for c in copy_cfgs] + [oc] * (2 - len(copy_cfgs))
+    P = C.c_void_p * n
+    ms = P(*[m.data_ptr() for m in masters])
+    gs = [g.contiguous() for g in grads]
+    gp = P(*[g.data_ptr() for g in gs])
+    c1 = P(*[c[0].data_ptr() for c in copies]) if len(copy_cfgs) > 0 else None
+    c2 = P(*[c[1].data_ptr() for c in copies]) if len(copy_cfgs) > 1 else None
+    ns = (C.c_int64 * n)(*[m.numel() for m in masters])
+    _native.check(_native.lib().pnn_sgd_step_multi(oc.nbits, oc.es, gc.nbits, gc.es, int(lr_code),
+                                                   cfgs[0].nbits, cfgs[0].es, cfgs[1].nbits, cfgs[1].es,
+                                                   int(grad_scale_log2), n, ms, gp, c1, c2, ns,
+                                                   _stream_ptr(masters[0].device)))
 
 
 def scalar_eval(cfg, op: int, a, b=None):
