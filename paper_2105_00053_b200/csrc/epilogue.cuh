@@ -71,35 +71,56 @@ __device__ __forceinline__ uint32_t q_to_posit_lut(const PositFmt& f, uint32_t q
     return mag == 0 ? 0u : c;
 }
 
+// 64-bit word as two 32-bit halves (the SM has no 64-bit integer ALU): sign
+// extension from W bits touches the high half only, |q| by xor + add-carry,
+// the leading one by two FLOs, the top 32 bits by one funnel shift.
 __device__ __forceinline__ uint32_t q_to_posit_lut(const PositFmt& f, uint64_t q, const uint4* lut) {
-    const int64_t v = f.W < 64 ? int64_t(q << (64 - f.W)) >> (64 - f.W) : int64_t(q);
-    const uint64_t s = uint64_t(v >> 63);
-    const uint64_t mag = (uint64_t(v) ^ s) - s;
-    const int lz = __clzll(mag);
-    const uint64_t sig = mag << (lz & 63);
-    const uint32_t c = pack_lut(f, lut, 63 - lz - 2 * f.R, uint32_t(sig >> 32), uint32_t(sig) != 0,
-                                s != 0);
-    return mag == 0 ? 0u : c;
+    uint32_t lo = uint32_t(q);
+    int32_t hi = int32_t(q >> 32);
+    if (f.W < 64) hi = (hi << (64 - f.W)) >> (64 - f.W);
+    const uint32_t s = uint32_t(hi >> 31);  // 0 or ~0
+    uint32_t ml = lo ^ s, mh = uint32_t(hi) ^ s;
+    asm("add.cc.u32 %0, %0, %2;\n\taddc.u32 %1, %1, 0;" : "+r"(ml), "+r"(mh) : "r"(s & 1u));
+    const bool hz = mh == 0;
+    const int lzh = __clz(mh), lzl = __clz(ml);
+    const uint32_t sig = hz ? (ml << (lzl & 31)) : __funnelshift_l(ml, mh, lzh);
+    const bool sticky = !hz && (ml << (lzh & 31)) != 0;  // lzh < 32 when mh != 0
+    const int top = hz ? 31 - lzl : 63 - lzh;
+    const uint32_t c = pack_lut(f, lut, top - 2 * f.R, sig, sticky, s != 0);
+    return (ml | mh) == 0 ? 0u : c;
 }
 
+// 128-bit word as four 32-bit limbs (sign extension from W bits, |q| by xor +
+// carry chain, leading limb selected, top 32 bits by one funnel shift).
 __device__ __forceinline__ uint32_t q_to_posit_lut(const PositFmt& f, unsigned __int128 q,
                                                    const uint4* lut) {
-    uint64_t lo = uint64_t(q), hi = uint64_t(q >> 64);
-    if (f.W < 128) hi = uint64_t(int64_t(hi << (128 - f.W)) >> (128 - f.W));  // W > 64
-    const uint64_t s = uint64_t(int64_t(hi) >> 63);
-    const unsigned __int128 S = ((unsigned __int128)s << 64) | s;
-    const unsigned __int128 m = ((((unsigned __int128)hi << 64) | lo) ^ S) - S;
-    lo = uint64_t(m);
-    hi = uint64_t(m >> 64);
-    const bool hz = hi == 0;
-    const int lzh = __clzll(hi), lzl = __clzll(lo);
-    const uint64_t sig_h = (hi << (lzh & 63)) | ((lo >> 1) >> ((63 - lzh) & 63));
-    const bool st_h = (lo << (lzh & 63)) != 0;
-    const uint64_t sig = hz ? (lo << (lzl & 63)) : sig_h;
-    const bool sticky = (!hz && st_h) || uint32_t(sig) != 0;
-    const int top = hz ? 63 - lzl : 127 - lzh;
-    const uint32_t c = pack_lut(f, lut, top - 2 * f.R, uint32_t(sig >> 32), sticky, s != 0);
-    return (hz && lo == 0) ? 0u : c;
+    uint32_t w0 = uint32_t(q), w1 = uint32_t(uint64_t(q) >> 32);
+    const uint64_t qh = uint64_t(q >> 64);
+    uint32_t w2 = uint32_t(qh);
+    int32_t w3 = int32_t(qh >> 32);
+    if (f.W <= 96) {  // 64 < W <= 96: the sign lives in w2
+        w2 = uint32_t(int32_t(w2 << (96 - f.W)) >> (96 - f.W));
+        w3 = int32_t(w2) >> 31;
+    } else if (f.W < 128) {
+        w3 = (w3 << (128 - f.W)) >> (128 - f.W);
+    }
+    const uint32_t s = uint32_t(w3 >> 31);
+    uint32_t m0 = w0 ^ s, m1 = w1 ^ s, m2 = w2 ^ s, m3 = uint32_t(w3) ^ s;
+    asm("add.cc.u32 %0, %0, %4;\n\taddc.cc.u32 %1, %1, 0;\n\taddc.cc.u32 %2, %2, 0;\n\taddc.u32 %3, %3, 0;"
+        : "+r"(m0), "+r"(m1), "+r"(m2), "+r"(m3)
+        : "r"(s & 1u));
+    // leading limb: (hi, lo, below) = the limb with the leading one, the next, the rest
+    uint32_t hi, lo, below;
+    int base;
+    if (m3) { hi = m3; lo = m2; below = m1 | m0; base = 127; }
+    else if (m2) { hi = m2; lo = m1; below = m0; base = 95; }
+    else if (m1) { hi = m1; lo = m0; below = 0; base = 63; }
+    else { hi = m0; lo = 0; below = 0; base = 31; }
+    const int lz = __clz(hi);
+    const uint32_t sig = __funnelshift_l(lo, hi, lz);
+    const bool sticky = ((lo << (lz & 31)) & (lz == 32 ? 0u : ~0u)) != 0 || below != 0;
+    const uint32_t c = pack_lut(f, lut, base - lz - 2 * f.R, sig, sticky, s != 0);
+    return (m0 | m1 | m2 | m3) == 0 ? 0u : c;
 }
 
 // Quire word of one output, accumulated group by group (mod the word size;
