@@ -392,11 +392,20 @@ cudaError_t act_digits_t(int D, const SrcT* x, int64_t N, int64_t C, int64_t H, 
                     unsigned(Cp / 32));
     const FastDiv fd_hw{uint32_t(H * W)}, fd_w{uint32_t(W)};
     if (lut == nullptr) build_lut = false;
+    // whole 256-pixel tiles per image, 16-byte aligned channel rows: staged loads
+    const bool tiled = (H * W) % 256 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0;
+    const int64_t ntiles = N * H * W / 256;
+    const dim3 tgrid(unsigned(ntiles < 148 * 8 ? ntiles : 148 * 8), unsigned(Cp / 32));
 #define PNN_ACT(DD)                                                                                  \
     if (build_lut) digit_lut_conv_kernel<DD><<<16, 256, 0, st>>>(fs, f, lut);                        \
-    act_digits_kernel<DD, SrcT><<<grid, 256, 0, st>>>(x, int(N), int(C), int(H), int(W), int(Cp),  \
-                                                      pad, fd_hw, fd_w, f, fs, lut, dig, pos_nar,   \
-                                                      chw_nar, chan_nar, any)
+    if (tiled)                                                                                       \
+        act_digits_tiled_kernel<DD, SrcT><<<tgrid, 256, 0, st>>>(                                    \
+            x, int(N), int(C), int(H), int(W), int(Cp), pad, fd_hw, fd_w, f, fs, lut, dig, pos_nar,  \
+            chw_nar, chan_nar, any);                                                                 \
+    else                                                                                             \
+        act_digits_kernel<DD, SrcT><<<grid, 256, 0, st>>>(x, int(N), int(C), int(H), int(W), int(Cp), \
+                                                          pad, fd_hw, fd_w, f, fs, lut, dig, pos_nar, \
+                                                          chw_nar, chan_nar, any)
     switch (D) {
         case 2: PNN_ACT(2); break;
         case 3: PNN_ACT(3); break;

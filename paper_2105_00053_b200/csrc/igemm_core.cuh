@@ -446,6 +446,79 @@ __device__ __forceinline__ uint32_t digits4_words(const uint32_t (&c)[4], const 
 // (in-register decode; then fs == f).  fs: the codes' format (NaR pattern).
 // Grid: (pixel blocks, 32-channel chunks); 32-bit indices (pixels < 2^31,
 // checked by the launcher) with launch-constant divisions by multiplication.
+// One pixel x one 32-channel chunk: digits of code[0..31] -> the slice-layout
+// cells of pixel (n, h, w) (+ the zero ring cells a border pixel owns), NaR
+// summaries.  plane = bytes per digit plane.  Shared by the digitisers below.
+template <int D>
+__device__ __forceinline__ void emit_pixel_digits(const uint32_t (&code)[32], uint32_t r, uint32_t n,
+                                                  uint32_t pix, uint32_t h, uint32_t w, int cc, int C,
+                                                  int H, int W, int Cp, int pad, int64_t plane,
+                                                  uint32_t HW, const PositFmt& f, uint32_t nar_code,
+                                                  const uint32_t* __restrict__ lut,
+                                                  int8_t* __restrict__ dig, uint8_t* __restrict__ pos_nar,
+                                                  uint8_t* __restrict__ chw_nar,
+                                                  uint8_t* __restrict__ chan_nar, uint8_t* __restrict__ any) {
+    const int Hp = H + 2 * pad, Wp = W + 2 * pad;
+    const int CS = Cp / 16;
+    const int c0 = cc * 32;
+    uint32_t words[D][8];
+    uint32_t nm = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const uint32_t c4[4] = {code[4 * q], code[4 * q + 1], code[4 * q + 2], code[4 * q + 3]};
+        nm |= digits4_words<D>(c4, f, nar_code, lut, words, q) << (4 * q);
+    }
+    // this chunk = slices 2cc, 2cc + 1 of pixel (h + pad, w + pad)
+    auto cell = [&](int hh, int ww) {
+        return dig + (((int64_t(n) * Hp + hh) * CS + 2 * cc) * Wp + ww) * 16;
+    };
+    int8_t* dst = cell(int(h) + pad, int(w) + pad);
+#pragma unroll
+    for (int p = 0; p < D; ++p) {
+        *reinterpret_cast<uint4*>(dst + p * plane) =
+            make_uint4(words[p][0], words[p][1], words[p][2], words[p][3]);
+        *reinterpret_cast<uint4*>(dst + p * plane + int64_t(Wp) * 16) =
+            make_uint4(words[p][4], words[p][5], words[p][6], words[p][7]);
+    }
+    if (pad > 0 && (h == 0 || w == 0 || int(h) == H - 1 || int(w) == W - 1)) {
+        // border pixel: zero the ring cells of its row / column (corners by
+        // the corner pixels)
+        const int ylo = h == 0 ? 0 : int(h) + pad, yhi = int(h) == H - 1 ? Hp - 1 : int(h) + pad;
+        const int xlo = w == 0 ? 0 : int(w) + pad, xhi = int(w) == W - 1 ? Wp - 1 : int(w) + pad;
+        for (int hh = ylo; hh <= yhi; ++hh)
+            for (int ww = xlo; ww <= xhi; ++ww) {
+                if (hh == int(h) + pad && ww == int(w) + pad) continue;
+                int8_t* z = cell(hh, ww);
+                for (int p = 0; p < D; ++p) {
+                    *reinterpret_cast<uint4*>(z + p * plane) = make_uint4(0, 0, 0, 0);
+                    *reinterpret_cast<uint4*>(z + p * plane + int64_t(Wp) * 16) = make_uint4(0, 0, 0, 0);
+                }
+            }
+    }
+    if (nm) {
+        for (int j = 0; j < 32; ++j)
+            if (((nm >> j) & 1) && c0 + j < C) {
+                if (pos_nar) pos_nar[r] = 1;
+                if (chw_nar) chw_nar[int64_t(c0 + j) * HW + pix] = 1;
+                if (chan_nar) chan_nar[c0 + j] = 1;
+                *any = 1;
+            }
+    }
+}
+
+// codes [N][C][H][W] -> dig[D][N][Hp][Cp/16][Wp][16] (slice layout, balanced
+// int8 digits; channels >= C are zero; Hp = H + 2 pad, Wp = W + 2 pad with the
+// pad ring written as zeros by the border pixels' threads), plus NaR summaries
+// written only where a NaR is found: pos_nar[n][h][w] (any channel),
+// chw_nar[c][h][w] (any image), chan_nar[c], *any.  A thread owns one pixel x
+// one 32-channel chunk: its 32 loads are coalesced across the warp
+// (consecutive pixels of one channel plane), and it writes 32 contiguous digit
+// bytes per plane (two 16-byte stores), so the warp's stores are 1 KB
+// contiguous per plane.  lut: digit words per SOURCE code (digit_lut_kernel:
+// the digits of convert(code, fs -> f), formats up to 12 bits) or null
+// (in-register decode; then fs == f).  fs: the codes' format (NaR pattern).
+// Grid: (pixel blocks, 32-channel chunks); 32-bit indices (pixels < 2^31,
+// checked by the launcher) with launch-constant divisions by multiplication.
 template <int D, typename CodeT>
 __global__ void __launch_bounds__(256) act_digits_kernel(
     const CodeT* __restrict__ x, int N, int C, int H, int W, int Cp, int pad, FastDiv fd_hw,
@@ -454,10 +527,8 @@ __global__ void __launch_bounds__(256) act_digits_kernel(
     uint8_t* __restrict__ chan_nar, uint8_t* __restrict__ any) {
     const uint32_t HW = uint32_t(H) * uint32_t(W);
     const uint32_t pixels = uint32_t(N) * HW;
-    const int Hp = H + 2 * pad, Wp = W + 2 * pad;
-    const int64_t plane = int64_t(N) * Hp * Wp * Cp;
+    const int64_t plane = int64_t(N) * (H + 2 * pad) * (W + 2 * pad) * Cp;
     const int cc = blockIdx.y;
-    const int CS = Cp / 16;
     const uint32_t nar_code = 1u << (fs.nbits - 1);
     for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < pixels; r += gridDim.x * blockDim.x) {
         uint32_t n, pix;  // pixel raster index r = (n, h, w)
@@ -467,51 +538,54 @@ __global__ void __launch_bounds__(256) act_digits_kernel(
         uint32_t code[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) code[j] = c0 + j < C ? uint32_t(src[j * HW]) : 0u;
-        uint32_t words[D][8];
-        uint32_t nm = 0;
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            const uint32_t c4[4] = {code[4 * q], code[4 * q + 1], code[4 * q + 2], code[4 * q + 3]};
-            nm |= digits4_words<D>(c4, f, nar_code, lut, words, q) << (4 * q);
-        }
         uint32_t h, w;
         fd_w.divmod(pix, h, w);
-        // this chunk = slices 2cc, 2cc + 1 of pixel (h + pad, w + pad)
-        auto cell = [&](int hh, int ww) {
-            return dig + (((int64_t(n) * Hp + hh) * CS + 2 * cc) * Wp + ww) * 16;
-        };
-        int8_t* dst = cell(int(h) + pad, int(w) + pad);
+        emit_pixel_digits<D>(code, r, n, pix, h, w, cc, C, H, W, Cp, pad, plane, HW, f, nar_code, lut,
+                             dig, pos_nar, chw_nar, chan_nar, any);
+    }
+}
+
+// As act_digits_kernel for images of HW % 256 == 0 pixels (16-byte aligned
+// channel planes): a block digitises tiles of 256 pixels x 32 channels; the
+// tile's codes arrive by 16-byte loads of whole channel rows into shared
+// memory (the per-thread strided loads of the generic kernel move 32 or 64
+// bytes per warp instruction), then each thread reads its pixel's 32 codes
+// across the rows.
+template <int D, typename CodeT>
+__global__ void __launch_bounds__(256) act_digits_tiled_kernel(
+    const CodeT* __restrict__ x, int N, int C, int H, int W, int Cp, int pad, FastDiv fd_hw,
+    FastDiv fd_w, PositFmt f, PositFmt fs, const uint32_t* __restrict__ lut,
+    int8_t* __restrict__ dig, uint8_t* __restrict__ pos_nar, uint8_t* __restrict__ chw_nar,
+    uint8_t* __restrict__ chan_nar, uint8_t* __restrict__ any) {
+    constexpr int TP = 256;                                   // pixels per tile
+    constexpr int VPR = TP * int(sizeof(CodeT)) / 16;         // 16-byte vectors per channel row
+    __shared__ uint4 s_tile[32 * VPR];
+    const uint32_t HW = uint32_t(H) * uint32_t(W);
+    const uint32_t tiles = uint32_t(N) * (HW / TP);
+    const int64_t plane = int64_t(N) * (H + 2 * pad) * (W + 2 * pad) * Cp;
+    const int cc = blockIdx.y, c0 = cc * 32;
+    const uint32_t nar_code = 1u << (fs.nbits - 1);
+    for (uint32_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const uint32_t r0 = t * TP;
+        uint32_t n, pix0;
+        fd_hw.divmod(r0, n, pix0);
+        __syncthreads();  // previous tile's readers are done
+        for (int i = threadIdx.x; i < 32 * VPR; i += blockDim.x) {
+            const int c = i / VPR, v = i - c * VPR;
+            s_tile[i] = c0 + c < C ? __ldg(reinterpret_cast<const uint4*>(
+                                         x + (int64_t(n) * C + c0 + c) * HW + pix0) + v)
+                                   : make_uint4(0, 0, 0, 0);
+        }
+        __syncthreads();
+        const CodeT* st = reinterpret_cast<const CodeT*>(s_tile);
+        uint32_t code[32];
 #pragma unroll
-        for (int p = 0; p < D; ++p) {
-            *reinterpret_cast<uint4*>(dst + p * plane) =
-                make_uint4(words[p][0], words[p][1], words[p][2], words[p][3]);
-            *reinterpret_cast<uint4*>(dst + p * plane + int64_t(Wp) * 16) =
-                make_uint4(words[p][4], words[p][5], words[p][6], words[p][7]);
-        }
-        if (pad > 0 && (h == 0 || w == 0 || int(h) == H - 1 || int(w) == W - 1)) {
-            // border pixel: zero the ring cells of its row / column (corners by
-            // the corner pixels)
-            const int ylo = h == 0 ? 0 : int(h) + pad, yhi = int(h) == H - 1 ? Hp - 1 : int(h) + pad;
-            const int xlo = w == 0 ? 0 : int(w) + pad, xhi = int(w) == W - 1 ? Wp - 1 : int(w) + pad;
-            for (int hh = ylo; hh <= yhi; ++hh)
-                for (int ww = xlo; ww <= xhi; ++ww) {
-                    if (hh == int(h) + pad && ww == int(w) + pad) continue;
-                    int8_t* z = cell(hh, ww);
-                    for (int p = 0; p < D; ++p) {
-                        *reinterpret_cast<uint4*>(z + p * plane) = make_uint4(0, 0, 0, 0);
-                        *reinterpret_cast<uint4*>(z + p * plane + int64_t(Wp) * 16) = make_uint4(0, 0, 0, 0);
-                    }
-                }
-        }
-        if (nm) {
-            for (int j = 0; j < 32; ++j)
-                if (((nm >> j) & 1) && c0 + j < C) {
-                    if (pos_nar) pos_nar[r] = 1;
-                    if (chw_nar) chw_nar[int64_t(c0 + j) * HW + pix] = 1;
-                    if (chan_nar) chan_nar[c0 + j] = 1;
-                    *any = 1;
-                }
-        }
+        for (int j = 0; j < 32; ++j) code[j] = uint32_t(st[j * TP + threadIdx.x]);
+        const uint32_t pix = pix0 + threadIdx.x;
+        uint32_t h, w;
+        fd_w.divmod(pix, h, w);
+        emit_pixel_digits<D>(code, r0 + threadIdx.x, n, pix, h, w, cc, C, H, W, Cp, pad, plane, HW, f,
+                             nar_code, lut, dig, pos_nar, chw_nar, chan_nar, any);
     }
 }
 
