@@ -85,6 +85,11 @@ bool make_plan(int pass, const PositFmt& f, const ConvGeom& g_real, bool raw, Im
                int DA = 0, int OFF = 0) {
     if (conv_algo() == 1 || g_real.stride != 1) return false;
     if (g_real.N < 1 || g_real.N > (1 << 30)) return false;
+    // Linear layers (1x1 over 1x1 images): a TMA box would gather one 16-byte
+    // pixel cell per image; the explicit path's contiguous bulk copies win
+    // (fc1 of the CIFAR CNN: ~3x).  Forced implicit (algo 2) still allowed.
+    if (conv_algo() == 0 && g_real.H == 1 && g_real.W == 1 && g_real.KH == 1 && g_real.KW == 1)
+        return false;
     const int D = digits_for(f);
     if (D < 2 || D > 8) return false;
     *p = ImplPlan{};

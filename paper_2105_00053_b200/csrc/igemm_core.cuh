@@ -367,9 +367,14 @@ __global__ void __launch_bounds__(ImplGeo<D, NT_, CPS, ACC, DA>::THREADS, CPS)
                     codes[x] = ((cn >> (8 * x)) & 0xFF) ? (1u << (f.nbits - 1)) : c;
                 }
                 CodeT* dst = out.base + obase + col0 * ostride;
+                if (ostride == 1) {  // contiguous columns (Linear: [N][features]): one vector store
+                    store_codes8(dst, codes, valid,
+                                 (reinterpret_cast<uintptr_t>(dst) & (8 * sizeof(CodeT) - 1)) == 0);
+                } else {
 #pragma unroll
-                for (int x = 0; x < 8; ++x)
-                    if (x < valid) dst[x * ostride] = CodeT(codes[x]);
+                    for (int x = 0; x < 8; ++x)
+                        if (x < valid) dst[x * ostride] = CodeT(codes[x]);
+                }
             }
         }
     }
