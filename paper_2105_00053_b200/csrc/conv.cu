@@ -493,6 +493,56 @@ int status_of(int rc, const char* what) {
 
 uint32_t one_code(const PositFmt& f) { return 1u << (f.nbits - 2); }  // 0b01000.. = 1.0
 
+// ---- Linear layers (1x1 kernels over 1x1 images: plain matrices) -----------
+// x [N][C], w [F][C], y/dy [N][F]: the explicit path's operands are row- or
+// column-major matrices, packed with 16-byte vector loads instead of the
+// im2col gathers (same X[r][k] values, so the same results).
+
+bool is_linear(const ConvGeom& g) {
+    return g.H == 1 && g.W == 1 && g.KH == 1 && g.KW == 1 && g.stride == 1 && g.pad == 0;
+}
+
+// X[r][k] = p[r*C + k] for k < C; column C = the bias column (col[r] or cval)
+template <typename CodeT>
+struct FetchRowsBias {
+    const CodeT* p;
+    int64_t C;
+    const CodeT* col;  // per-row bias codes (weights) or null
+    uint32_t cval;     // constant bias column (activations: the code of 1.0)
+    static constexpr bool kRowFastest = false;
+    static constexpr bool kVecK = true, kVecR = false, kSep = false;
+    __device__ __forceinline__ const CodeT* ptr(int64_t r, int64_t k) const {
+        return k + int64_t(16 / sizeof(CodeT)) <= C ? p + r * C + k : nullptr;  // never spans the bias
+    }
+    __device__ __forceinline__ uint32_t operator()(int64_t r, int64_t k) const {
+        return k < C ? uint32_t(p[r * C + k]) : (col ? uint32_t(col[r]) : cval);
+    }
+};
+
+template <typename T>
+int linear_fwd(GemmArgs& a, const ConvGeom& g, const void* x, const void* w, const void* bias, void* y,
+               void* ws, size_t wsb, cudaStream_t st) {
+    return run_quire_gemm<T>(a, FetchRowsBias<T>{(const T*)x, g.C, nullptr, one_code(a.f)},
+                             FetchRowsBias<T>{(const T*)w, g.C, (const T*)bias, 0u},
+                             out_nchw<T>(y, 1, g.F), ws, wsb, st, nullptr);
+}
+
+template <typename T>
+int linear_dgrad(GemmArgs& a, const ConvGeom& g, const void* dy, const void* w, void* dx, void* ws,
+                 size_t wsb, cudaStream_t st) {
+    // dx[n][c] = sum_f dy[n][f] w[f][c]: A = dy row-major, B[r = c][k = f] = w[f][c]
+    return run_quire_gemm<T>(a, FetchRowMajor<T>{(const T*)dy, g.F}, FetchColMajor<T>{(const T*)w, g.C},
+                             out_nchw<T>(dx, 1, g.C), ws, wsb, st, nullptr);
+}
+
+template <typename T>
+int linear_wgrad(GemmArgs& a, const ConvGeom& g, const void* dy, const void* x, void* dw, void* ws,
+                 size_t wsb, cudaStream_t st) {
+    // dw[f][c] = sum_n dy[n][f] x[n][c]: A[r = c][k = n] = x[n][c], B[r = f][k = n] = dy[n][f]
+    return run_quire_gemm<T>(a, FetchColMajor<T>{(const T*)x, g.C}, FetchColMajor<T>{(const T*)dy, g.F},
+                             out_nchw<T>(dw, a.M, g.F), ws, wsb, st, nullptr);
+}
+
 }  // namespace
 
 extern "C" {
@@ -537,6 +587,10 @@ int pnn_conv2d_fwd(int nbits, int es, const void* x, int64_t N, int64_t C, int64
         return status_of(igemm_conv_fwd(a.f, g, x, w, bias, y, workspace, workspace_bytes, st),
                          "conv2d_fwd");
     if (conv_algo() == 2) return set_status(PNN_EUNSUPPORTED, "conv2d_fwd: implicit path not eligible");
+    if (is_linear(g))
+        return status_of(nbits <= 8 ? linear_fwd<uint8_t>(a, g, x, w, bias, y, workspace, workspace_bytes, st)
+                                    : linear_fwd<uint16_t>(a, g, x, w, bias, y, workspace, workspace_bytes, st),
+                         "conv2d_fwd");
     if (nbits <= 8) {
         using T = uint8_t;
         rc = run_quire_gemm<T>(a, FetchIm2colFwd<T>{(const T*)x, g, kconv, one_code(a.f)},
@@ -573,6 +627,12 @@ int pnn_conv2d_dgrad(int nbits, int es, const void* dy, int64_t N, int64_t F, in
         return status_of(igemm_conv_dgrad(a.f, g, dy, w, dx, workspace, workspace_bytes, st),
                          "conv2d_dgrad");
     if (conv_algo() == 2) return set_status(PNN_EUNSUPPORTED, "conv2d_dgrad: implicit path not eligible");
+    if (is_linear(g)) {  // every tap valid: weight-column NaR is the B-column flag
+        a.col_nar = true;
+        return status_of(nbits <= 8 ? linear_dgrad<uint8_t>(a, g, dy, w, dx, workspace, workspace_bytes, st)
+                                    : linear_dgrad<uint16_t>(a, g, dy, w, dx, workspace, workspace_bytes, st),
+                         "conv2d_dgrad");
+    }
     QuireGemmPlan p;
     if (plan_quire_gemm(a.f, a.M, a.N, a.K, 0, false, &p)) return PNN_EUNSUPPORTED;
     const uint8_t* flag_w = static_cast<const uint8_t*>(workspace) + p.off_flags + 1;
@@ -584,14 +644,14 @@ int pnn_conv2d_dgrad(int nbits, int es, const void* dy, int64_t N, int64_t F, in
         rc = run_quire_gemm<T>(a, FetchDgradDy<T>{(const T*)dy, g}, FetchDgradW<T>{(const T*)w, g},
                                out_nchw<T>(dx, H * W, C), workspace, workspace_bytes, st, nullptr);
         if (rc == 0)
-            dgrad_weight_nar_kernel<T><<<grid_for(total, 256), 256, 0, st>>>((T*)dx, (const T*)w, g,
+            dgrad_weight_nar_kernel<T><<<grid_fixup(total), 256, 0, st>>>((T*)dx, (const T*)w, g,
                                                                              flag_w, nar);
     } else {
         using T = uint16_t;
         rc = run_quire_gemm<T>(a, FetchDgradDy<T>{(const T*)dy, g}, FetchDgradW<T>{(const T*)w, g},
                                out_nchw<T>(dx, H * W, C), workspace, workspace_bytes, st, nullptr);
         if (rc == 0)
-            dgrad_weight_nar_kernel<T><<<grid_for(total, 256), 256, 0, st>>>((T*)dx, (const T*)w, g,
+            dgrad_weight_nar_kernel<T><<<grid_fixup(total), 256, 0, st>>>((T*)dx, (const T*)w, g,
                                                                              flag_w, nar);
     }
     if (rc == 0 && cudaGetLastError() != cudaSuccess) rc = 4;
@@ -629,6 +689,10 @@ int pnn_conv2d_wgrad(int nbits, int es, const void* dy, int64_t N, int64_t F, in
                                           workspace_bytes, st),
                          "conv2d_wgrad");
     if (conv_algo() == 2) return set_status(PNN_EUNSUPPORTED, "conv2d_wgrad: implicit path not eligible");
+    if (is_linear(g))
+        return status_of(nbits <= 8 ? linear_wgrad<uint8_t>(a, g, dy, x, dw, workspace, workspace_bytes, st)
+                                    : linear_wgrad<uint16_t>(a, g, dy, x, dw, workspace, workspace_bytes, st),
+                         "conv2d_wgrad");
     // dw[f][(c,ky,kx)]: output (m=(c,ky,kx), n=f) -> f*M + m  (NCHW map with one "image")
     int rc;
     if (nbits <= 8) {

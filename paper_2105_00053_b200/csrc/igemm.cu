@@ -570,7 +570,7 @@ int run_fwd(const ImplPlan& p, const ConvGeom& g, const CodeT* x, const CodeT* w
     if (use_partial)
         quire_finalize_kernel<CodeT><<<grid_for(a.M * a.N, 256), 256, 0, st>>>(
             a.partial, int(a.splits), nullptr, col_nar, out, a.M, a.N, f, nullptr, nullptr);
-    fwd_nar_fixup_kernel<CodeT><<<grid_for(a.M, 256), 256, 0, st>>>(
+    fwd_nar_fixup_kernel<CodeT><<<grid_fixup(a.M), 256, 0, st>>>(
         y, pos_nar, xflag, g.N, int(g.F), int(gv.H), int(gv.W), int(g.OH), int(g.OW), int(gv.KH),
         int(gv.KW), gv.pad, 1u << (f.nbits - 1));
     return rc_of(cudaGetLastError());
@@ -621,10 +621,10 @@ int run_dgrad(const ImplPlan& p, const ConvGeom& g, const CodeT* dy, const CodeT
         quire_finalize_kernel<CodeT><<<grid_for(a.M * a.N, 256), 256, 0, st>>>(
             a.partial, int(a.splits), nullptr, nullptr, out, a.M, a.N, f, nullptr, nullptr);
     const uint32_t nar = 1u << (f.nbits - 1);
-    dgrad_nar_fixup_kernel<CodeT><<<grid_for(a.M, 256), 256, 0, st>>>(
+    dgrad_nar_fixup_kernel<CodeT><<<grid_fixup(a.M), 256, 0, st>>>(
         dx, a_pos, a_any, g.N, int(g.C), int(g.H), int(g.W), int(g.OH), int(g.OW), int(g.KH),
         int(g.KW), g.pad, nar);
-    dgrad_weight_nar_kernel<CodeT><<<grid_for(a.M * a.N, 256), 256, 0, st>>>(dx, w, g, flags + 1,
+    dgrad_weight_nar_kernel<CodeT><<<grid_fixup(a.M * a.N), 256, 0, st>>>(dx, w, g, flags + 1,
                                                                              nar);
     return rc_of(cudaGetLastError());
 }

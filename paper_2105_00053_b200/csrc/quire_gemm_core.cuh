@@ -789,6 +789,13 @@ inline int grid_for(int64_t items, int threads) {
     return int(b);
 }
 
+// Grid of the NaR fix-up kernels: they exit at once unless a NaR was seen
+// (device flag), so launch few blocks (grid-stride loops cover the rest).
+inline int grid_fixup(int64_t items) {
+    const int g = grid_for(items, 256);
+    return g < 2 * 148 ? g : 2 * 148;
+}
+
 // Arguments of one logical quire GEMM  C[m][n] = round(sum_k A[m][k] B[k][n]).
 struct GemmArgs {
     PositFmt f;
