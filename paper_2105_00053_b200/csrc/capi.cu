@@ -70,6 +70,7 @@ cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
 // Grow-only device scratch for the synchronous host entry points.
 constexpr int64_t kHostChunk = int64_t(1) << 22;  // codes per host narrow/widen chunk
 constexpr int kEvents = 16;
+constexpr int kPanels = 4;  // row panels of the host-entry GEMM (copy/compute pipeline)
 
 // Persistent host worker pool for the synchronous host entry points (the
 // reference's ThreadPool::parallel_for role, thread_pool.hpp:21-48: contiguous
@@ -150,8 +151,10 @@ struct Scratch {
     size_t bytes = 0;
     void* hptr = nullptr;
     size_t hbytes = 0;
-    cudaStream_t stream = nullptr;
+    cudaStream_t stream = nullptr;   // GEMMs
+    cudaStream_t h2d = nullptr, d2h = nullptr;  // copy streams of the host entry
     cudaEvent_t ev[kEvents] = {};
+    cudaEvent_t evB = nullptr, evA[kPanels] = {}, evG[kPanels] = {};
     void* reserve_host(size_t n) {
         if (n <= hbytes) return hptr;
         if (hptr) cudaFreeHost(hptr);
@@ -319,13 +322,20 @@ int pnn_matmul_host(int nbits, int es, const uint64_t* A, const uint64_t* B, uin
     }
     std::lock_guard<std::mutex> lock(g_scratch.mu);
     if (!g_scratch.stream) {
-        if (cudaError_t e = cudaStreamCreateWithFlags(&g_scratch.stream, cudaStreamNonBlocking))
-            return cuda_fail(e, "stream");
+        for (cudaStream_t* sp : {&g_scratch.stream, &g_scratch.h2d, &g_scratch.d2h})
+            if (cudaError_t e = cudaStreamCreateWithFlags(sp, cudaStreamNonBlocking))
+                return cuda_fail(e, "stream");
         for (auto& ev : g_scratch.ev)
             if (cudaError_t e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming))
                 return cuda_fail(e, "event");
+        for (int i = 0; i < kPanels; ++i)
+            for (cudaEvent_t* ep : {&g_scratch.evA[i], &g_scratch.evG[i]})
+                if (cudaError_t e = cudaEventCreateWithFlags(ep, cudaEventDisableTiming))
+                    return cuda_fail(e, "event");
+        if (cudaError_t e = cudaEventCreateWithFlags(&g_scratch.evB, cudaEventDisableTiming))
+            return cuda_fail(e, "event");
     }
-    cudaStream_t st = g_scratch.stream;
+    cudaStream_t st = g_scratch.stream, sh = g_scratch.h2d, sd = g_scratch.d2h;
     QuireGemmPlan p;
     if (quire_gemm_plan(nbits, es, M, N, K, 0, &p)) return fail(PNN_EUNSUPPORTED, "format");
     const int cb = nbits <= 8 ? 1 : 2;
@@ -340,7 +350,8 @@ int pnn_matmul_host(int nbits, int es, const uint64_t* A, const uint64_t* B, uin
     HostPool& pool = host_pool();
     cudaError_t e;
     // Host threads narrow the uint64 Tensor storage (tensor.hpp:10-14) to packed
-    // codes chunk by chunk; each chunk's H2D copy overlaps the next chunk's narrowing.
+    // codes chunk by chunk; each chunk's H2D copy (copy stream) overlaps the
+    // next chunk's narrowing.
     auto upload = [&](const uint64_t* src, uint8_t* hdst, uint8_t* ddst, int64_t n) -> cudaError_t {
         for (int64_t c0 = 0; c0 < n; c0 += kHostChunk) {
             const int64_t c1 = std::min(n, c0 + kHostChunk);
@@ -348,7 +359,7 @@ int pnn_matmul_host(int nbits, int es, const uint64_t* A, const uint64_t* B, uin
                 host_narrow_codes(src + c0 + lo, hdst + (c0 + lo) * cb, hi - lo, cb, mask);
             });
             if (cudaError_t err = cudaMemcpyAsync(ddst + c0 * cb, hdst + c0 * cb, size_t(c1 - c0) * cb,
-                                                  cudaMemcpyHostToDevice, st))
+                                                  cudaMemcpyHostToDevice, sh))
                 return err;
         }
         return cudaSuccess;
@@ -356,36 +367,57 @@ int pnn_matmul_host(int nbits, int es, const uint64_t* A, const uint64_t* B, uin
     static const bool prof = getenv("PNN_HOST_PROFILE") != nullptr;  // phase times to stderr
     auto now = [] { return std::chrono::steady_clock::now(); };
     const auto t0 = now();
-    if ((e = upload(A, hA, dA, M * K))) return cuda_fail(e, "H2D A");
+    // Row panels: GEMM of panel i runs while the host narrows panel i+1 of A,
+    // and while it widens the results of earlier panels (three streams).
+    const int P = M >= 1024 ? kPanels : 1;
+    const int64_t rows = (M + P - 1) / P;
     if ((e = upload(B, hB, dB, K * N))) return cuda_fail(e, "H2D B");
+    cudaEventRecord(g_scratch.evB, sh);
+    cudaStreamWaitEvent(st, g_scratch.evB, 0);
+    for (int i = 0; i < P; ++i) {
+        const int64_t r0 = i * rows, r1 = std::min(M, r0 + rows);
+        if (r0 >= r1) break;
+        if ((e = upload(A + r0 * K, hA + r0 * K * cb, dA + r0 * K * cb, (r1 - r0) * K)))
+            return cuda_fail(e, "H2D A");
+        cudaEventRecord(g_scratch.evA[i], sh);
+        cudaStreamWaitEvent(st, g_scratch.evA[i], 0);
+        int rc = quire_gemm_launch(nbits, es, dA + r0 * K * cb, dB, dC + r0 * N * cb, r1 - r0, N, K, K, N, N,
+                                   ws, p.workspace_bytes, 0, st, nullptr);
+        if (rc) return rc == 4 ? cuda_fail(cudaGetLastError(), "matmul launch") : fail(rc, "matmul");
+        cudaEventRecord(g_scratch.evG[i], st);
+    }
     const auto t1 = now();
-    int rc = quire_gemm_launch(nbits, es, dA, dB, dC, M, N, K, K, N, N, ws, p.workspace_bytes, 0,
-                               st, nullptr);
-    if (rc) return rc == 4 ? cuda_fail(cudaGetLastError(), "matmul launch") : fail(rc, "matmul");
-    // D2H in chunks; widen chunk i on the host while chunk i+1 is in flight.
-    const int64_t n = M * N;
-    const int64_t nch = (n + kHostChunk - 1) / kHostChunk;
-    for (int64_t c = 0; c < nch; c += kEvents) {
-        const int64_t cend = std::min(nch, c + kEvents);
-        for (int64_t k = c; k < cend; ++k) {
-            const int64_t c0 = k * kHostChunk, c1 = std::min(n, c0 + kHostChunk);
-            if ((e = cudaMemcpyAsync(hC + c0 * cb, dC + c0 * cb, size_t(c1 - c0) * cb,
-                                     cudaMemcpyDeviceToHost, st)))
-                return cuda_fail(e, "D2H C");
-            cudaEventRecord(g_scratch.ev[k - c], st);
-        }
-        for (int64_t k = c; k < cend; ++k) {
-            if ((e = cudaEventSynchronize(g_scratch.ev[k - c]))) return cuda_fail(e, "D2H sync");
-            const int64_t c0 = k * kHostChunk, c1 = std::min(n, c0 + kHostChunk);
-            pool.parallel_for(c1 - c0, [&](int64_t lo, int64_t hi) {
-                host_widen_codes(hC + (c0 + lo) * cb, C + c0 + lo, hi - lo, cb);
-            });
+    // D2H per panel (after its GEMM) in chunks; widen chunk j on the host while
+    // chunk j+1 is in flight.
+    for (int i = 0; i < P; ++i) {
+        const int64_t r0 = i * rows, r1 = std::min(M, r0 + rows);
+        if (r0 >= r1) break;
+        cudaStreamWaitEvent(sd, g_scratch.evG[i], 0);
+        const int64_t off = r0 * N, n = (r1 - r0) * N;
+        const int64_t nch = (n + kHostChunk - 1) / kHostChunk;
+        for (int64_t c = 0; c < nch; c += kEvents) {
+            const int64_t cend = std::min(nch, c + kEvents);
+            for (int64_t k = c; k < cend; ++k) {
+                const int64_t c0 = off + k * kHostChunk, c1 = std::min(off + n, c0 + kHostChunk);
+                if ((e = cudaMemcpyAsync(hC + c0 * cb, dC + c0 * cb, size_t(c1 - c0) * cb,
+                                         cudaMemcpyDeviceToHost, sd)))
+                    return cuda_fail(e, "D2H C");
+                cudaEventRecord(g_scratch.ev[k - c], sd);
+            }
+            for (int64_t k = c; k < cend; ++k) {
+                if ((e = cudaEventSynchronize(g_scratch.ev[k - c]))) return cuda_fail(e, "D2H sync");
+                const int64_t c0 = off + k * kHostChunk, c1 = std::min(off + n, c0 + kHostChunk);
+                pool.parallel_for(c1 - c0, [&](int64_t lo, int64_t hi) {
+                    host_widen_codes(hC + (c0 + lo) * cb, C + c0 + lo, hi - lo, cb);
+                });
+            }
         }
     }
-    if ((e = cudaStreamSynchronize(st))) return cuda_fail(e, "matmul_host sync");
+    for (cudaStream_t s2 : {sh, st, sd})
+        if ((e = cudaStreamSynchronize(s2))) return cuda_fail(e, "matmul_host sync");
     if (prof) {
         const auto t2 = now();
-        fprintf(stderr, "[pnn_matmul_host] narrow+H2D issue %.2f ms, GEMM+D2H+widen %.2f ms\n",
+        fprintf(stderr, "[pnn_matmul_host] narrow+H2D+GEMM issue %.2f ms, D2H+widen %.2f ms\n",
                 std::chrono::duration<double, std::milli>(t1 - t0).count(),
                 std::chrono::duration<double, std::milli>(t2 - t1).count());
     }
