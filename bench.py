@@ -455,7 +455,10 @@ def main():
 
     training = None
     if not args.no_train:
-        training = run_training(args, rank, world, dev, dist)
+        try:  # the config-1 line above must survive a failure of the training leg
+            training = run_training(args, rank, world, dev, dist)
+        except Exception as e:  # noqa: BLE001
+            training = {"metric": "CNN training images/s", "error": f"{type(e).__name__}: {e}"[:300]}
 
     if rank == 0:
         line = {
