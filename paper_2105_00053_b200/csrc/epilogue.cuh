@@ -109,18 +109,20 @@ __device__ __forceinline__ uint32_t q_to_posit_lut(const PositFmt& f, unsigned _
     asm("add.cc.u32 %0, %0, %4;\n\taddc.cc.u32 %1, %1, 0;\n\taddc.cc.u32 %2, %2, 0;\n\taddc.u32 %3, %3, 0;"
         : "+r"(m0), "+r"(m1), "+r"(m2), "+r"(m3)
         : "r"(s & 1u));
-    // leading limb: (hi, lo, below) = the limb with the leading one, the next, the rest
-    uint32_t hi, lo, below;
-    int base;
-    if (m3) { hi = m3; lo = m2; below = m1 | m0; base = 127; }
-    else if (m2) { hi = m2; lo = m1; below = m0; base = 95; }
-    else if (m1) { hi = m1; lo = m0; below = 0; base = 63; }
-    else { hi = m0; lo = 0; below = 0; base = 31; }
+    // |q| <= 2^(W-1): for W <= 96 the top limb is zero (compile-time for the
+    // specialised formats).  Leading limb by selects, not branches (the lanes of
+    // a warp disagree on it): (hi, lo, below) = the limb holding the leading
+    // one, the next limb, the OR of the rest.
+    const bool n3 = f.W > 96 && m3 != 0, n2 = m2 != 0, n1 = m1 != 0;
+    const uint32_t hi = n3 ? m3 : n2 ? m2 : n1 ? m1 : m0;
+    const uint32_t lo = n3 ? m2 : n2 ? m1 : n1 ? m0 : 0u;
+    const uint32_t below = n3 ? (m1 | m0) : n2 ? m0 : 0u;
+    const int base = n3 ? 127 : n2 ? 95 : n1 ? 63 : 31;
     const int lz = __clz(hi);
     const uint32_t sig = __funnelshift_l(lo, hi, lz);
-    const bool sticky = ((lo << (lz & 31)) & (lz == 32 ? 0u : ~0u)) != 0 || below != 0;
+    const bool sticky = (lo << (lz & 31)) != 0 || below != 0;  // lz < 32 unless q == 0
     const uint32_t c = pack_lut(f, lut, base - lz - 2 * f.R, sig, sticky, s != 0);
-    return (m0 | m1 | m2 | m3) == 0 ? 0u : c;
+    return hi == 0 ? 0u : c;
 }
 
 // Quire word of one output, accumulated group by group (mod the word size;
