@@ -398,7 +398,8 @@ cudaError_t act_digits_t(int D, const SrcT* x, int64_t N, int64_t C, int64_t H, 
     const FastDiv fd_hw{uint32_t(H * W)}, fd_w{uint32_t(W)};
     if (lut == nullptr) build_lut = false;
     // whole 256-pixel tiles per image, 16-byte aligned channel rows: staged loads
-    const bool tiled = (H * W) % 256 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0;
+    const bool tiled = (H * W) % 256 == 0 && (256 % W == 0 || W % 256 == 0) &&
+                       (reinterpret_cast<uintptr_t>(x) & 15) == 0;
     const int64_t ntiles = N * H * W / 256;
     const dim3 tgrid(unsigned(ntiles < 148 * 8 ? ntiles : 148 * 8), unsigned(Cp / 32));
 #define PNN_ACT(DD)                                                                                  \

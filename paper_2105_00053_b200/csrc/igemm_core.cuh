@@ -462,7 +462,8 @@ __device__ __forceinline__ void emit_pixel_digits(const uint32_t (&code)[32], ui
                                                   const uint32_t* __restrict__ lut,
                                                   int8_t* __restrict__ dig, uint8_t* __restrict__ pos_nar,
                                                   uint8_t* __restrict__ chw_nar,
-                                                  uint8_t* __restrict__ chan_nar, uint8_t* __restrict__ any) {
+                                                  uint8_t* __restrict__ chan_nar, uint8_t* __restrict__ any,
+                                                  bool ring = true) {
     const int Hp = H + 2 * pad, Wp = W + 2 * pad;
     const int CS = Cp / 16;
     const int c0 = cc * 32;
@@ -485,7 +486,7 @@ __device__ __forceinline__ void emit_pixel_digits(const uint32_t (&code)[32], ui
         *reinterpret_cast<uint4*>(dst + p * plane + int64_t(Wp) * 16) =
             make_uint4(words[p][4], words[p][5], words[p][6], words[p][7]);
     }
-    if (pad > 0 && (h == 0 || w == 0 || int(h) == H - 1 || int(w) == W - 1)) {
+    if (ring && pad > 0 && (h == 0 || w == 0 || int(h) == H - 1 || int(w) == W - 1)) {
         // border pixel: zero the ring cells of its row / column (corners by
         // the corner pixels)
         const int ylo = h == 0 ? 0 : int(h) + pad, yhi = int(h) == H - 1 ? Hp - 1 : int(h) + pad;
@@ -589,8 +590,40 @@ __global__ void __launch_bounds__(256) act_digits_tiled_kernel(
         const uint32_t pix = pix0 + threadIdx.x;
         uint32_t h, w;
         fd_w.divmod(pix, h, w);
+        // pixel cells only (pad 0 below); the zero ring of this tile's rows is
+        // written cooperatively afterwards (per-thread ring loops diverge in
+        // every warp: each image row has a first and a last pixel)
         emit_pixel_digits<D>(code, r0 + threadIdx.x, n, pix, h, w, cc, C, H, W, Cp, pad, plane, HW, f,
-                             nar_code, lut, dig, pos_nar, chw_nar, chan_nar, any);
+                             nar_code, lut, dig, pos_nar, chw_nar, chan_nar, any, /*ring=*/false);
+        if (pad > 0) {
+            const int Hp = H + 2 * pad, Wp = W + 2 * pad, CS = Cp / 16;
+            uint32_t hh0, ww0;
+            fd_w.divmod(pix0, hh0, ww0);  // a tile = whole rows (W | 256) or part of one row (256 | W)
+            const int rows = TP / W > 0 ? TP / W : 1;  // (part-row tiles rewrite both side cells: zeros)
+            const int y0 = int(hh0), y1 = y0 + rows - 1;
+            // ring cells: left/right pad cells of rows y0..y1, plus the top pad rows
+            // (tile holds row 0) and the bottom pad rows (tile holds row H-1)
+            const int side = rows * 2 * pad;
+            const int top = y0 == 0 ? pad * Wp : 0, bot = y1 == H - 1 ? pad * Wp : 0;
+            const int cells = side + top + bot;
+            for (int i = threadIdx.x; i < cells * D * 2; i += blockDim.x) {
+                const int cell = i / (D * 2), rest = i - cell * (D * 2), p = rest >> 1, sl = rest & 1;
+                int hh, ww;
+                if (cell < side) {
+                    const int r = cell / (2 * pad), k = cell - r * (2 * pad);
+                    hh = y0 + r + pad;
+                    ww = k < pad ? k : W + k;
+                } else if (cell < side + top) {
+                    hh = (cell - side) / Wp;
+                    ww = (cell - side) % Wp;
+                } else {
+                    hh = H + pad + (cell - side - top) / Wp;
+                    ww = (cell - side - top) % Wp;
+                }
+                int8_t* z = dig + p * plane + (((int64_t(n) * Hp + hh) * CS + 2 * cc + sl) * Wp + ww) * 16;
+                *reinterpret_cast<uint4*>(z) = make_uint4(0, 0, 0, 0);
+            }
+        }
     }
 }
 
