@@ -119,6 +119,14 @@ int pnn_conv2d_fwd_save(int nbits, int es, const void* x, int64_t N, int64_t C, 
                         const void* w, int64_t F, int64_t KH, int64_t KW, const void* bias, int stride,
                         int pad, void* y, void* saved, size_t saved_bytes, void* workspace,
                         size_t workspace_bytes, void* stream);
+/* pnn_conv2d_fwd_save with the following ReLU layer fused (relu != 0: y =
+ * relu(conv), SURVEY.md Appendix A.2 -- relu(NaR) = 0 -- and, if y_pre is
+ * non-NULL, the pre-activation conv output there too).  saved may be NULL.
+ * Implicit-path geometries only (else PNN_EUNSUPPORTED). */
+int pnn_conv2d_fwd_layer(int nbits, int es, const void* x, int64_t N, int64_t C, int64_t H, int64_t W,
+                         const void* w, int64_t F, int64_t KH, int64_t KW, const void* bias, int stride,
+                         int pad, int relu, void* y, void* y_pre, void* saved, size_t saved_bytes,
+                         void* workspace, size_t workspace_bytes, void* stream);
 int pnn_conv2d_backward_workspace(int f_nbits, int f_es, int b_nbits, int b_es, int g_nbits, int g_es,
                                   int64_t N, int64_t C, int64_t H, int64_t W, int64_t F, int64_t KH,
                                   int64_t KW, int stride, int pad, int raw, int has_dx, int has_saved,

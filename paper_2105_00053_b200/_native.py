@@ -45,6 +45,9 @@ _SIGS = {
                                                                            C.POINTER(C.c_size_t)]),
     "pnn_conv2d_fwd_save": (C.c_int, [C.c_int, C.c_int, _vp] + [_i64] * 4 + [_vp] + [_i64] * 3 +
                             [_vp, C.c_int, C.c_int, _vp, _vp, C.c_size_t, _vp, C.c_size_t, _vp]),
+    "pnn_conv2d_fwd_layer": (C.c_int, [C.c_int, C.c_int, _vp] + [_i64] * 4 + [_vp] + [_i64] * 3 +
+                             [_vp, C.c_int, C.c_int, C.c_int, _vp, _vp, _vp, C.c_size_t, _vp, C.c_size_t,
+                              _vp]),
     "pnn_conv2d_backward_workspace": (C.c_int, [C.c_int] * 6 + [_i64] * 7 + [C.c_int] * 5 +
                                       [C.POINTER(C.c_size_t)]),
     "pnn_conv2d_backward": (C.c_int, [C.c_int] * 6 + [_vp, _vp, _vp, C.c_size_t, _vp] + [_i64] * 7 +

@@ -723,7 +723,15 @@ int pnn_conv2d_fwd_save(int nbits, int es, const void* x, int64_t N, int64_t C, 
                         const void* w, int64_t F, int64_t KH, int64_t KW, const void* bias, int stride,
                         int pad, void* y, void* saved, size_t saved_bytes, void* workspace,
                         size_t workspace_bytes, void* stream) {
-    if (saved == nullptr)
+    return pnn_conv2d_fwd_layer(nbits, es, x, N, C, H, W, w, F, KH, KW, bias, stride, pad, 0, y, nullptr,
+                                saved, saved_bytes, workspace, workspace_bytes, stream);
+}
+
+int pnn_conv2d_fwd_layer(int nbits, int es, const void* x, int64_t N, int64_t C, int64_t H, int64_t W,
+                         const void* w, int64_t F, int64_t KH, int64_t KW, const void* bias, int stride,
+                         int pad, int relu, void* y, void* y_pre, void* saved, size_t saved_bytes,
+                         void* workspace, size_t workspace_bytes, void* stream) {
+    if (saved == nullptr && !relu)
         return pnn_conv2d_fwd(nbits, es, x, N, C, H, W, w, F, KH, KW, bias, stride, pad, y, workspace,
                               workspace_bytes, stream);
     if (!conv_fmt_ok(nbits, es)) return set_status(PNN_EUNSUPPORTED, "conv: format not supported");
@@ -732,11 +740,13 @@ int pnn_conv2d_fwd_save(int nbits, int es, const void* x, int64_t N, int64_t C, 
         return set_status(PNN_EINVAL, "conv: invalid shape or argument");
     if (N == 0) return PNN_OK;
     const PositFmt f = make_fmt(nbits, es);
-    if (igemm_saved_bytes(f, g) == 0)
+    if (saved != nullptr && igemm_saved_bytes(f, g) == 0)
         return set_status(PNN_EUNSUPPORTED, "conv2d_fwd_save: no implicit forward/weight-grad pair");
+    if (!igemm_eligible(0, f, g, false, nullptr))
+        return set_status(PNN_EUNSUPPORTED, "conv2d_fwd_layer: implicit forward not eligible");
     return status_of(igemm_conv_fwd(f, g, x, w, bias, y, workspace, workspace_bytes,
-                                    static_cast<cudaStream_t>(stream), saved, saved_bytes),
-                     "conv2d_fwd_save");
+                                    static_cast<cudaStream_t>(stream), saved, saved_bytes, relu, y_pre),
+                     "conv2d_fwd_layer");
 }
 
 int pnn_conv2d_backward_workspace(int f_nbits, int f_es, int b_nbits, int b_es, int g_nbits, int g_es,

@@ -534,7 +534,7 @@ SavedX saved_of(void* base, const SaveLayout& L) {
 template <typename CodeT>
 int run_fwd(const ImplPlan& p, const ConvGeom& g, const CodeT* x, const CodeT* w,
             const CodeT* bias, CodeT* y, uint8_t* ws, cudaStream_t st, const SavedX* sv,
-            size_t sv_clear) {
+            size_t sv_clear, int relu = 0, CodeT* pre = nullptr) {
     const PositFmt& f = p.a.f;
     auto* adig = sv ? sv->dig : reinterpret_cast<int8_t*>(ws + p.off_adig);
     auto* bdig = reinterpret_cast<int8_t*>(ws + p.off_bdig);
@@ -566,14 +566,19 @@ int run_fwd(const ImplPlan& p, const ConvGeom& g, const CodeT* x, const CodeT* w
     a.col_nar = col_nar;
     const bool use_partial = a.splits > 1;
     a.partial = use_partial ? reinterpret_cast<unsigned __int128*>(ws + p.off_partial) : nullptr;
+    a.relu = relu;
+    a.pre_out = pre;
     const OutMap<CodeT> out = out_nchw<CodeT>(y, g.OH * g.OW, g.F);
     if ((e = dispatch<CodeT, 0>(p.D, tA, tB, a, out, st)) != cudaSuccess) return 4;
-    if (use_partial)
+    if (use_partial) {
         quire_finalize_kernel<CodeT><<<grid_for(a.M * a.N, 256), 256, 0, st>>>(
             a.partial, int(a.splits), nullptr, col_nar, out, a.M, a.N, f, nullptr, nullptr);
+        if (relu)
+            relu_codes_kernel<CodeT><<<grid_for(a.M * a.N, 256), 256, 0, st>>>(y, pre, a.M * a.N, f.nbits);
+    }
     fwd_nar_fixup_kernel<CodeT><<<grid_fixup(a.M), 256, 0, st>>>(
         y, pos_nar, xflag, g.N, int(g.F), int(gv.H), int(gv.W), int(g.OH), int(g.OW), int(gv.KH),
-        int(gv.KW), gv.pad, 1u << (f.nbits - 1));
+        int(gv.KW), gv.pad, 1u << (f.nbits - 1), relu, pre);
     return rc_of(cudaGetLastError());
 }
 
@@ -767,7 +772,7 @@ bool igemm_eligible(int pass, const PositFmt& f, const ConvGeom& g, bool raw, si
 
 int igemm_conv_fwd(const PositFmt& f, const ConvGeom& g, const void* x, const void* w,
                    const void* bias, void* y, void* ws, size_t ws_bytes, cudaStream_t st,
-                   void* saved, size_t saved_bytes) {
+                   void* saved, size_t saved_bytes, int relu, void* pre) {
     ImplPlan p;
     if (!make_plan(0, f, g, false, &p)) return 2;
     if (ws_bytes < p.total) return 3;
@@ -783,9 +788,9 @@ int igemm_conv_fwd(const PositFmt& f, const ConvGeom& g, const void* x, const vo
     const size_t clear = L.chw + 16;  // NaR map + flag
     if (f.nbits <= 8)
         return run_fwd<uint8_t>(p, g, (const uint8_t*)x, (const uint8_t*)w, (const uint8_t*)bias,
-                                (uint8_t*)y, b, st, svp, clear);
+                                (uint8_t*)y, b, st, svp, clear, relu, (uint8_t*)pre);
     return run_fwd<uint16_t>(p, g, (const uint16_t*)x, (const uint16_t*)w, (const uint16_t*)bias,
-                             (uint16_t*)y, b, st, svp, clear);
+                             (uint16_t*)y, b, st, svp, clear, relu, (uint16_t*)pre);
 }
 
 size_t igemm_saved_bytes(const PositFmt& f, const ConvGeom& g) {

@@ -29,7 +29,8 @@ bool igemm_eligible(int pass, const PositFmt& f, const ConvGeom& g, bool raw, si
 // geometry has no implicit forward + weight-gradient pair).
 int igemm_conv_fwd(const PositFmt& f, const ConvGeom& g, const void* x, const void* w,
                    const void* bias, void* y, void* ws, size_t ws_bytes, cudaStream_t st,
-                   void* saved = nullptr, size_t saved_bytes = 0);
+                   void* saved = nullptr, size_t saved_bytes = 0, int relu = 0,
+                   void* pre = nullptr);
 size_t igemm_saved_bytes(const PositFmt& f, const ConvGeom& g);
 int igemm_conv_dgrad(const PositFmt& f, const ConvGeom& g, const void* dy, const void* w, void* dx,
                      void* ws, size_t ws_bytes, cudaStream_t st);

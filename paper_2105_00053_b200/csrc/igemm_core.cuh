@@ -93,6 +93,8 @@ struct IgemmArgs {
     int taps, C, OWb, OHb, kpr, kpi;  // k-blocks per row-block set / per image
     int KH, kgroups, cgroups, Hp;     // kx groups of 4, 32-channel groups, padded height
     int apad;  // mode 0: zero ring stored around the A digits (box coordinates shift by it)
+    int relu;       // mode 0: output relu(y) (ReLU layer fused) ...
+    void* pre_out;  // ... and, if non-null, the pre-activation y here (same layout)
     // tile raster (tile_coords) with launch-constant divisions: by mtiles * ntiles,
     // by kGroupM * ntiles, and by the group height (kGroupM, or the last group's)
     FastDiv fd_split, fd_group, fd_g8, fd_glast;
@@ -365,6 +367,19 @@ __global__ void __launch_bounds__(ImplGeo<D, NT_, CPS, ACC, DA>::THREADS, CPS)
                     const uint32_t c =
                         PNN_EPI_DEBUG(1) ? uint32_t(q[c0 + x]) : q_to_posit_lut(f, q[c0 + x], s_lut);
                     codes[x] = ((cn >> (8 * x)) & 0xFF) ? (1u << (f.nbits - 1)) : c;
+                }
+                if constexpr (MODE == 0) if (a.relu) {
+                    // fused ReLU (the layer after the convolution):
+                    // the pre-activation to pre_out when asked, relu(y) to the output
+                    if (a.pre_out != nullptr) {
+                        CodeT* pd = static_cast<CodeT*>(a.pre_out) + obase + col0 * ostride;
+#pragma unroll
+                        for (int x = 0; x < 8; ++x)
+                            if (x < valid) pd[x * ostride] = CodeT(codes[x]);
+                    }
+#pragma unroll
+                    for (int x = 0; x < 8; ++x)
+                        codes[x] = (codes[x] != 0 && ((codes[x] >> (f.nbits - 1)) & 1u) == 0) ? codes[x] : 0u;
                 }
                 CodeT* dst = out.base + obase + col0 * ostride;
                 if (ostride == 1) {  // contiguous columns (Linear: [N][features]): one vector store
@@ -783,7 +798,8 @@ __global__ void dgrad_weight_nar_kernel(CodeT* __restrict__ dx, const CodeT* __r
 template <typename CodeT>
 __global__ void fwd_nar_fixup_kernel(CodeT* __restrict__ y, const uint8_t* __restrict__ pos_nar,
                                      const uint8_t* __restrict__ any, int64_t N, int F, int H,
-                                     int W, int OH, int OW, int KH, int KW, int pad, uint32_t nar) {
+                                     int W, int OH, int OW, int KH, int KW, int pad, uint32_t nar,
+                                     int relu = 0, CodeT* __restrict__ pre = nullptr) {
     if (*any == 0) return;
     const int64_t total = N * OH * OW;
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total;
@@ -798,7 +814,23 @@ __global__ void fwd_nar_fixup_kernel(CodeT* __restrict__ y, const uint8_t* __res
                     hit = pos_nar[(n * H + iy) * W + ix] != 0;
             }
         if (hit)
-            for (int fo = 0; fo < F; ++fo) y[((n * F + fo) * OH + oy) * OW + ox] = CodeT(nar);
+            for (int fo = 0; fo < F; ++fo) {
+                const int64_t o = ((n * F + fo) * OH + oy) * OW + ox;
+                y[o] = CodeT(relu ? 0u : nar);  // relu(NaR) = 0
+                if (pre) pre[o] = CodeT(nar);
+            }
+    }
+}
+
+// relu in place (+ copy of the pre-activation): the split-K forward path of a
+// fused Conv2d + ReLU, after quire_finalize_kernel
+template <typename CodeT>
+__global__ void relu_codes_kernel(CodeT* __restrict__ y, CodeT* __restrict__ pre, int64_t n, int nbits) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        const uint32_t c = uint32_t(y[i]);
+        if (pre) pre[i] = CodeT(c);
+        y[i] = CodeT((c != 0 && ((c >> (nbits - 1)) & 1u) == 0) ? c : 0u);
     }
 }
 

@@ -120,6 +120,21 @@ class Conv2d(Module):
     def params(self):
         return [self.w, self.b]
 
+    def forward_relu(self, x, want_pre=False):
+        """This layer followed by a ReLU in one pass (relu fused into the GEMM
+        epilogue): (relu(y), y if want_pre else None), or None when the
+        geometry has no implicit forward (caller runs the two layers)."""
+        f = self.st.forward
+        n = ops.conv2d_saved_bytes(f, x.shape, self.w.shape, self.stride, self.pad) if self.training else 0
+        saved = torch.empty(n, dtype=torch.uint8, device=x.device) if n else None
+        res = ops.conv2d_fwd_layer(f, x, self.w.as_(f), self.b.as_(f), self.stride, self.pad, saved,
+                                   relu=True, want_pre=want_pre)
+        if res is None:
+            return None
+        self.x = x
+        self.saved = saved
+        return res
+
     def forward(self, x):
         f = self.st.forward
         self.x = x
@@ -428,10 +443,27 @@ class Sequential(Module):
         return [p for l in self.layers for p in l.params()]
 
     def forward(self, x, record=None):
-        for i, l in enumerate(self.layers):
+        i, n = 0, len(self.layers)
+        while i < n:
+            l = self.layers[i]
+            nxt = self.layers[i + 1] if i + 1 < n else None
+            if type(l) is Conv2d and type(nxt) is ReLU:
+                # Conv2d + ReLU in one GEMM epilogue; the ReLU layer's backward gate
+                # reads relu(y) (positive(relu(v)) == positive(v), relu(NaR) = 0)
+                res = l.forward_relu(x, want_pre=record is not None)
+                if res is not None:
+                    y, pre = res
+                    nxt.x = y
+                    if record is not None:
+                        record[f"act{i}"] = pre
+                        record[f"act{i + 1}"] = y
+                    x = y
+                    i += 2
+                    continue
             x = l.forward(x)
             if record is not None:
                 record[f"act{i}"] = x
+            i += 1
         return x
 
     def backward(self, dy, raw=False, record=None):

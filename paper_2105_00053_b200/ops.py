@@ -348,6 +348,37 @@ def conv2d_fwd_save(cfg, x, w, bias, stride: int, pad: int, saved):
     return y
 
 
+def conv2d_fwd_layer(cfg, x, w, bias, stride: int, pad: int, saved=None, relu: bool = False,
+                     want_pre: bool = False):
+    """Forward of a Conv2d layer (optionally keeping x's digits in `saved`) with
+    the following ReLU fused: returns (relu(y), y or None).  None when the
+    geometry has no implicit forward (use conv2d + relu_fwd)."""
+    cfg = _cfg(cfg)
+    _check_codes(cfg, x, w, bias)
+    x, w = x.contiguous(), w.contiguous()
+    bias = bias.contiguous() if bias is not None else None
+    N, Cc, H, W = x.shape
+    F, _, KH, KW = w.shape
+    OH, OW = (H + 2 * pad - KH) // stride + 1, (W + 2 * pad - KW) // stride + 1
+    nb = C.c_size_t()
+    rc = _native.lib().pnn_conv2d_workspace(0, cfg.nbits, cfg.es, N, Cc, H, W, F, KH, KW, stride, pad,
+                                            int(bias is not None), C.byref(nb))
+    if rc != 0:
+        return None
+    y = torch.empty((N, F, OH, OW), dtype=cfg.code_dtype, device=x.device)
+    pre = torch.empty_like(y) if want_pre else None
+    ws = _ws.get(x.device, nb.value)
+    rc = _native.lib().pnn_conv2d_fwd_layer(
+        cfg.nbits, cfg.es, x.data_ptr(), N, Cc, H, W, w.data_ptr(), F, KH, KW,
+        bias.data_ptr() if bias is not None else None, stride, pad, int(relu), y.data_ptr(),
+        pre.data_ptr() if pre is not None else None, saved.data_ptr() if saved is not None else None,
+        saved.numel() if saved is not None else 0, ws.data_ptr(), ws.numel(), _stream_ptr(x.device))
+    if rc == 2:  # PNN_EUNSUPPORTED: not an implicit-path geometry
+        return None
+    _native.check(rc)
+    return y, pre
+
+
 def conv2d_backward_eligible(f_cfg, b_cfg, g_cfg, x_shape, w_shape, stride, pad, raw, has_dx, has_saved):
     f, b, g = _cfg(f_cfg), _cfg(b_cfg), _cfg(g_cfg)
     N, Cc, H, W = (int(v) for v in x_shape)

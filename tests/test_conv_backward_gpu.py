@@ -137,3 +137,27 @@ def test_saved_bytes_zero_when_ineligible(cuda):
     assert ops.conv2d_saved_bytes(P161, (4, 6, 14, 14), (16, 6, 5, 5), 1, 0) == 0
     assert ops.conv2d_backward(P161, P161, P161, torch.zeros((4, 16, 10, 10), dtype=torch.int16).cuda(),
                                None, None, None, (4, 6, 14, 14), (16, 6, 5, 5), 1, 0, False) is None
+
+
+@pytest.mark.parametrize("cfg", [P80, P81, P121, P161])
+@pytest.mark.parametrize("shape", [(2, 32, 8, 8, 32, 3, 1), (2, 3, 32, 32, 32, 3, 1), (1, 256, 4, 4, 32, 3, 1),
+                                   (3, 64, 16, 16, 64, 3, 1)])
+def test_fused_relu_forward(cuda, cfg, shape):
+    """Conv2d + ReLU in one epilogue (pnn_conv2d_fwd_layer) == conv2d then relu_fwd,
+    pre-activation output included; NaR rows (relu(NaR) = 0); the small-image /
+    deep-K shape runs split-K (finalize + relu pass)."""
+    N, C, H, W, F, K, pad = shape
+    rng = np.random.default_rng(hash((cfg, shape)) & 0xFFFF)
+    xa = rand_codes(rng, cfg[0], (N, C, H, W))
+    xa[0, 1, 2, 3] = 1 << (cfg[0] - 1)
+    x = dev(cfg, xa)
+    w = dev(cfg, rand_codes(rng, cfg[0], (F, C, K, K)))
+    b = dev(cfg, rand_codes(rng, cfg[0], (F,)))
+    ref = ops.conv2d(cfg, x, w, b, 1, pad)
+    n = ops.conv2d_saved_bytes(cfg, x.shape, w.shape, 1, pad)
+    saved = torch.empty(n, dtype=torch.uint8, device="cuda") if n else None
+    y, pre = ops.conv2d_fwd_layer(cfg, x, w, b, 1, pad, saved, relu=True, want_pre=True)
+    assert torch.equal(pre, ref)
+    assert torch.equal(y, ops.relu_fwd(cfg, ref))
+    y2, none = ops.conv2d_fwd_layer(cfg, x, w, b, 1, pad, None, relu=True, want_pre=False)
+    assert none is None and torch.equal(y2, y)
