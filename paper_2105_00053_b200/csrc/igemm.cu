@@ -571,8 +571,7 @@ int run_fwd(const ImplPlan& p, const ConvGeom& g, const CodeT* x, const CodeT* w
     const OutMap<CodeT> out = out_nchw<CodeT>(y, g.OH * g.OW, g.F);
     if ((e = dispatch<CodeT, 0>(p.D, tA, tB, a, out, st)) != cudaSuccess) return 4;
     if (use_partial) {
-        quire_finalize_kernel<CodeT><<<grid_for(a.M * a.N, 256), 256, 0, st>>>(
-            a.partial, int(a.splits), nullptr, col_nar, out, a.M, a.N, f, nullptr, nullptr);
+        launch_finalize<CodeT>(a.partial, int(a.splits), nullptr, col_nar, out, a.M, a.N, f, nullptr, nullptr, st);
         if (relu)
             relu_codes_kernel<CodeT><<<grid_for(a.M * a.N, 256), 256, 0, st>>>(y, pre, a.M * a.N, f.nbits);
     }
@@ -624,8 +623,7 @@ int run_dgrad(const ImplPlan& p, const ConvGeom& g, const CodeT* dy, const CodeT
     const OutMap<CodeT> out = out_nchw<CodeT>(dx, g.H * g.W, g.C);
     if (dispatch<CodeT, 1>(p.D, tA, tB, a, out, st) != cudaSuccess) return 4;
     if (use_partial)
-        quire_finalize_kernel<CodeT><<<grid_for(a.M * a.N, 256), 256, 0, st>>>(
-            a.partial, int(a.splits), nullptr, nullptr, out, a.M, a.N, f, nullptr, nullptr);
+        launch_finalize<CodeT>(a.partial, int(a.splits), nullptr, nullptr, out, a.M, a.N, f, nullptr, nullptr, st);
     const uint32_t nar = 1u << (f.nbits - 1);
     dgrad_nar_fixup_kernel<CodeT><<<grid_fixup(a.M), 256, 0, st>>>(
         dx, a_pos, a_any, g.N, int(g.C), int(g.H), int(g.W), int(g.OH), int(g.OW), int(g.KH),
@@ -688,8 +686,7 @@ int run_wgrad(const ImplPlan& p, const ConvGeom& g, const void* dy, const PositF
     out.cvalid = p.fold ? p.ckk : int(g.C);
     if (dispatch_wgrad<CodeT>(p.D, p.DA, p.OFF, tA, tB, a, out, st) != cudaSuccess) return 4;
     if (use_partial)
-        quire_finalize_kernel<CodeT><<<grid_for(a.M * a.N, 256), 256, 0, st>>>(
-            a.partial, int(a.splits), nullptr, col_nar, out, a.M, a.N, f, raw_words, raw_nar);
+        launch_finalize<CodeT>(a.partial, int(a.splits), nullptr, col_nar, out, a.M, a.N, f, raw_words, raw_nar, st);
     wgrad_nar_fixup_kernel<CodeT><<<grid_for(p.ckk, 128), 128, 0, st>>>(
         dw, raw_nar, chw_nar, xflag, int(g.F), p.fold ? p.ckk : int(g.C), int(gv.H), int(gv.W),
         int(g.OH), int(g.OW), int(gv.KH), int(gv.KW), gv.pad, 1u << (f.nbits - 1));

@@ -687,9 +687,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                 } else {
                     const int64_t cs = out.col_stride();
                     CodeT* dst = out.base + out.row_base(row) + col0 * cs;
+                    if (cs == 1) {  // contiguous columns (Linear layers): one vector store
+                        store_codes8(dst, codes, valid,
+                                     (reinterpret_cast<uintptr_t>(dst) & (8 * sizeof(CodeT) - 1)) == 0);
+                    } else {
 #pragma unroll
-                    for (int x = 0; x < 8; ++x)
-                        if (x < valid) dst[x * cs] = CodeT(codes[x]);
+                        for (int x = 0; x < 8; ++x)
+                            if (x < valid) dst[x * cs] = CodeT(codes[x]);
+                    }
                 }
             }
         }
@@ -742,6 +747,60 @@ __global__ void quire_finalize_kernel(const unsigned __int128* __restrict__ part
         if (out.base != nullptr)
             out.base[o] = CodeT(nar ? (1u << (f.nbits - 1)) : quire_word_to_posit(f, q));
     }
+}
+
+// Few outputs, many splits (weight gradients of small layers: thousands of
+// outputs, ~100 splits): a warp per output, lanes over the splits, 128-bit
+// butterfly -- the thread-per-output loop above would be a long serial chain
+// of dependent loads on a handful of blocks.
+template <typename CodeT>
+__global__ void __launch_bounds__(256) quire_finalize_warp_kernel(
+    const unsigned __int128* __restrict__ partial, int splits, const uint8_t* __restrict__ row_nar,
+    const uint8_t* __restrict__ col_nar, OutMap<CodeT> out, int64_t M, int64_t N, PositFmt f,
+    unsigned __int128* __restrict__ raw_words, uint8_t* __restrict__ raw_nar) {
+    const int64_t total = M * N;
+    const unsigned __int128 one = 1;
+    const unsigned __int128 wmask = f.W >= 128 ? ~(unsigned __int128)0 : ((one << f.W) - 1);
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t idx = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5; idx < total; idx += nw) {
+        unsigned __int128 q = 0;
+        for (int sp = lane; sp < splits; sp += 32) q += partial[sp * total + idx];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const uint64_t l2 = __shfl_xor_sync(0xFFFFFFFFu, uint64_t(q), o);
+            const uint64_t h2 = __shfl_xor_sync(0xFFFFFFFFu, uint64_t(q >> 64), o);
+            q += (unsigned __int128)l2 | ((unsigned __int128)h2 << 64);
+        }
+        if (lane != 0) continue;
+        const int64_t i = idx / N, j = idx - (idx / N) * N;
+        const bool nar = (row_nar != nullptr && row_nar[i]) || (col_nar != nullptr && col_nar[j]);
+        const int64_t o = out.index(i, j);
+        if (o < 0) continue;
+        if (raw_words != nullptr) {
+            raw_words[o] = q & wmask;
+            raw_nar[o] = nar ? 1 : 0;
+        }
+        if (out.base != nullptr)
+            out.base[o] = CodeT(nar ? (1u << (f.nbits - 1)) : quire_word_to_posit(f, q));
+    }
+}
+
+inline int grid_for(int64_t items, int threads);
+
+// split-K finalize: the variant by shape
+template <typename CodeT>
+inline void launch_finalize(const unsigned __int128* partial, int splits, const uint8_t* row_nar,
+                            const uint8_t* col_nar, const OutMap<CodeT>& out, int64_t M, int64_t N,
+                            const PositFmt& f, unsigned __int128* raw_words, uint8_t* raw_nar,
+                            cudaStream_t st) {
+    const int64_t total = M * N;
+    if (splits >= 8 && total <= 148 * 256)
+        quire_finalize_warp_kernel<CodeT><<<grid_for(total * 32, 256), 256, 0, st>>>(
+            partial, splits, row_nar, col_nar, out, M, N, f, raw_words, raw_nar);
+    else
+        quire_finalize_kernel<CodeT><<<grid_for(total, 256), 256, 0, st>>>(
+            partial, splits, row_nar, col_nar, out, M, N, f, raw_words, raw_nar);
 }
 
 // ------------------------------------------------------------------ host
@@ -962,9 +1021,8 @@ cudaError_t launch_generic(const QuireGemmPlan& p, const GemmArgs& g, FA fa, FB 
     }
     if (stats) cudaEventRecord(stats->ev[2], st);
     if (use_partial) {
-        quire_finalize_kernel<CodeT><<<grid_for(g.M * g.N, 256), 256, 0, st>>>(
-            partial, int(p.splits), g.row_nar ? rnar : nullptr, g.col_nar ? cnar : nullptr, out,
-            g.M, g.N, f, g.raw_words, g.raw_nar);
+        launch_finalize<CodeT>(partial, int(p.splits), g.row_nar ? rnar : nullptr,
+                               g.col_nar ? cnar : nullptr, out, g.M, g.N, f, g.raw_words, g.raw_nar, st);
     }
     if (stats) cudaEventRecord(stats->ev[3], st);
     return cudaGetLastError();
