@@ -189,6 +189,16 @@ int pnn_softmax_xent_scaled(int nbits, int es, const void* logits, const int32_t
                             int64_t B, int64_t classes, int log2_batch, int grad_scale_log2,
                             void* dlogits, void* loss_rows, void* loss_out, void* raw_word,
                             void* raw_nar, void* stream);
+/* The same step split in two so the loss can run beside the backward pass:
+ * _grad writes dlogits and the rounded row sums S (loss format, [B]); _loss
+ * turns them into the per-row losses log(S) - (z_y - m) and the batch loss /
+ * raw word exactly as pnn_softmax_xent_scaled does. */
+int pnn_softmax_xent_grad(int nbits, int es, const void* logits, const int32_t* labels, int64_t B,
+                          int64_t classes, int log2_batch, int grad_scale_log2, void* dlogits,
+                          void* s_rows, void* stream);
+int pnn_softmax_xent_loss(int nbits, int es, const void* logits, const int32_t* labels,
+                          const void* s_rows, int64_t B, int64_t classes, int log2_batch,
+                          void* loss_rows, void* loss_out, void* raw_word, void* raw_nar, void* stream);
 /* The batch-loss half of pnn_softmax_xent on its own: loss_out[0] =
  * ldexp(round(quire sum of loss_rows[0..B)), -log2_batch).  Data-parallel
  * training gathers the ranks' loss rows through it when the loss format's

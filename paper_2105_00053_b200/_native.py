@@ -64,6 +64,10 @@ _SIGS = {
     "pnn_relu_bwd": (C.c_int, [C.c_int, C.c_int, _vp, C.c_int, C.c_int, _vp, _vp, _i64, _vp]),
     "pnn_maxpool2d_fwd": (C.c_int, [C.c_int, C.c_int, _vp] + [_i64] * 4 + [C.c_int, C.c_int, _vp, _vp, _vp]),
     "pnn_maxpool2d_bwd": (C.c_int, [C.c_int, C.c_int, _vp, _vp] + [_i64] * 4 + [C.c_int, C.c_int, _vp, _vp]),
+    "pnn_softmax_xent_grad": (C.c_int, [C.c_int, C.c_int, _vp, _vp, _i64, _i64, C.c_int, C.c_int, _vp, _vp,
+                                        _vp]),
+    "pnn_softmax_xent_loss": (C.c_int, [C.c_int, C.c_int, _vp, _vp, _vp, _i64, _i64, C.c_int, _vp, _vp, _vp,
+                                        _vp, _vp]),
     "pnn_sgd_step_multi": (C.c_int, [C.c_int] * 4 + [C.c_uint32] + [C.c_int] * 6 +
                            [_vp, _vp, _vp, _vp, _vp, _vp]),
     "pnn_maxpool2d_bwd_x": (C.c_int, [C.c_int, C.c_int, _vp, C.c_int, C.c_int, _vp] + [_i64] * 4 +

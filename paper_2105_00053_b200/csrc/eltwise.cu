@@ -359,7 +359,7 @@ __global__ void relu_bwd_vec_kernel(int x_nbits, const TX* __restrict__ x,
 // (butterfly over 128-bit lanes), one rounding, then p_j per lane.
 __global__ void softmax_xent_kernel(PositFmt f, int b, const void* logits, const int32_t* labels,
                                     int64_t B, int64_t Cn, int log2_batch, int grad_scale_log2,
-                                    void* dlogits, void* loss_rows) {
+                                    void* dlogits, void* loss_rows, void* s_rows = nullptr) {
     const int lane = threadIdx.x & 31;
     const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
     for (int64_t i = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5; i < B; i += nwarps) {
@@ -412,10 +412,28 @@ __global__ void softmax_xent_kernel(PositFmt f, int b, const void* logits, const
             const uint32_t g = p_sub(f, pj, j == y ? one : 0u);
             store_any(dlogits, row + j, b, p_ldexp(f, g, grad_scale_log2 - log2_batch));
         }
-        if (lane == 0) {
+        if (lane == 0 && s_rows != nullptr) store_any(s_rows, i, b, S);
+        if (lane == 0 && loss_rows != nullptr) {
             const uint32_t zy = load_any(logits, row + y, b);
             store_any(loss_rows, i, b, p_sub(f, p_log(f, S), p_sub(f, zy, m)));
         }
+    }
+}
+
+// loss_i = log(S_i) - (z_y - m) from the row sums S the gradient kernel left
+// (same operations as softmax_xent_kernel's last step, Appendix A.5): lets the
+// loss run beside the backward pass instead of on its critical path.
+__global__ void xent_loss_rows_kernel(PositFmt f, int b, const void* logits, const int32_t* labels,
+                                      const void* s_rows, int64_t B, int64_t Cn, void* loss_rows) {
+    GRID_STRIDE(i, B) {
+        const int64_t row = i * Cn;
+        uint32_t m = load_any(logits, row, b);
+        for (int64_t j = 1; j < Cn; ++j) {
+            const uint32_t v = load_any(logits, row + j, b);
+            if (p_compare(f, v, m) > 0) m = v;
+        }
+        const uint32_t zy = load_any(logits, row + labels[i], b);
+        store_any(loss_rows, i, b, p_sub(f, p_log(f, load_any(s_rows, i, b)), p_sub(f, zy, m)));
     }
 }
 
@@ -798,6 +816,36 @@ int pnn_softmax_xent_scaled(int nbits, int es, const void* logits, const int32_t
                                               loss_out, (unsigned __int128*)raw_word,
                                               (uint8_t*)raw_nar);
     return launched("softmax_xent");
+}
+
+int pnn_softmax_xent_grad(int nbits, int es, const void* logits, const int32_t* labels, int64_t B,
+                          int64_t classes, int log2_batch, int grad_scale_log2, void* dlogits,
+                          void* s_rows, void* stream) {
+    CHECK_FMT(nbits, es);
+    if (B < 1 || classes < 1 || !logits || !labels || !dlogits || !s_rows)
+        return set_status(PNN_EINVAL, "softmax_xent_grad: bad arguments");
+    softmax_xent_kernel<<<grid1(B * 32), 256, 0, (cudaStream_t)stream>>>(
+        make_fmt(nbits, es), bytes_of(nbits), logits, labels, B, classes, log2_batch, grad_scale_log2,
+        dlogits, nullptr, s_rows);
+    return launched("softmax_xent_grad");
+}
+
+int pnn_softmax_xent_loss(int nbits, int es, const void* logits, const int32_t* labels,
+                          const void* s_rows, int64_t B, int64_t classes, int log2_batch,
+                          void* loss_rows, void* loss_out, void* raw_word, void* raw_nar, void* stream) {
+    CHECK_FMT(nbits, es);
+    if (B < 1 || classes < 1 || !logits || !labels || !s_rows || !loss_rows)
+        return set_status(PNN_EINVAL, "softmax_xent_loss: bad arguments");
+    const PositFmt f = make_fmt(nbits, es);
+    if (raw_word && f.W > 128)
+        return set_status(PNN_EUNSUPPORTED, "softmax_xent: raw loss words need a quire of <= 128 bits");
+    auto st = (cudaStream_t)stream;
+    xent_loss_rows_kernel<<<grid1(B), 256, 0, st>>>(f, bytes_of(nbits), logits, labels, s_rows, B,
+                                                     classes, loss_rows);
+    if (loss_out || raw_word)
+        loss_reduce_kernel<<<1, 256, 0, st>>>(f, bytes_of(nbits), loss_rows, B, log2_batch, loss_out,
+                                              (unsigned __int128*)raw_word, (uint8_t*)raw_nar);
+    return launched("softmax_xent_loss");
 }
 
 int pnn_loss_reduce(int nbits, int es, const void* loss_rows, int64_t B, int log2_batch,

@@ -117,9 +117,10 @@ def dp_train_step(model: nn.Sequential, loss_fn: nn.CrossEntropyLoss, opt: nn.SG
                   x_shard, labels_shard, global_batch: int, group=None):
     """One data-parallel SGD step on this rank's shard; returns the global loss."""
     logits = model.forward(x_shard)
-    _, dz, word, nar = loss_fn(logits, labels_shard, global_batch, raw=True)
+    _, dz, word, nar = loss_fn(logits, labels_shard, global_batch, raw=True, defer=True)
     model.backward(dz, raw=True)
     reducer.reduce()
+    loss_fn.join()  # the loss words / rows were computed beside the backward pass
     if word is None:  # loss quire wider than the 128-bit raw word
         loss = gather_loss(loss_fn.st.loss, loss_fn.rows, global_batch, group)
     else:

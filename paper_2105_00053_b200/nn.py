@@ -376,12 +376,42 @@ class CrossEntropyLoss(Module):
     def __init__(self, st: StagePrecisions, grad_scale_log2: int = 0):
         self.st = st
         self.grad_scale_log2 = int(grad_scale_log2)
+        self._side = None
+        self._pending = False
 
-    def __call__(self, logits_fwd, labels, global_batch: int, raw=False):
+    def join(self):
+        """Make the current stream wait for a deferred loss (see defer=True)."""
+        if self._pending:
+            torch.cuda.current_stream().wait_stream(self._side)
+            self._pending = False
+
+    def __call__(self, logits_fwd, labels, global_batch: int, raw=False, defer=False):
+        """defer=True: the logit gradient is computed on the current stream and
+        the loss (per-row log, quire sum) on a side stream, off the backward
+        pass's critical path; call join() before reading the loss."""
         lb = int(round(math.log2(global_batch)))
         if 1 << lb != global_batch:
             raise ValueError("global batch must be a power of two (Appendix A.5)")
         z = ops.convert_tensor(logits_fwd, self.st.forward, self.st.loss)
+        if defer:
+            raw_words = raw and ops.quire_bits(self.st.loss) <= 128
+            d, srows = ops.softmax_xent_grad(self.st.loss, z, labels, lb, self.grad_scale_log2)
+            cur = torch.cuda.current_stream(z.device)
+            if self._side is None:
+                self._side = torch.cuda.Stream(device=z.device)
+            self._side.wait_stream(cur)
+            with torch.cuda.stream(self._side):
+                out = ops.softmax_xent_loss(self.st.loss, z, labels, srows, lb, raw=raw_words)
+            for t in (z, srows, labels):
+                t.record_stream(self._side)
+            self._pending = True
+            self.rows = out[1]
+            dz = ops.convert_tensor(d, self.st.loss, self.st.backward)
+            if raw_words:
+                return out[0], dz, out[2], out[3]
+            if raw:
+                return out[0], dz, None, None
+            return out[0], dz
         # raw quire words need W <= 128; wider loss quires (posit(10,2)) hand
         # the data-parallel path the loss rows instead (word = nar = None)
         raw_words = raw and ops.quire_bits(self.st.loss) <= 128
@@ -417,7 +447,10 @@ class MSELoss(Module):
         return self._onehot[key][torch.nn.functional.one_hot(labels.long(), classes)].to(
             self.st.loss.code_dtype)
 
-    def __call__(self, logits_fwd, labels, global_batch: int, raw=False):
+    def join(self):  # the MSE loss is computed in line (no deferred work)
+        pass
+
+    def __call__(self, logits_fwd, labels, global_batch: int, raw=False, defer=False):
         if raw:
             raise NotImplementedError("MSELoss has no data-parallel (raw) mode")
         B, classes = logits_fwd.shape
@@ -578,7 +611,7 @@ def train_step(model: Sequential, loss_fn: CrossEntropyLoss, opt: SGD, x_fwd, la
                global_batch: int, record=None):
     """One SGD step on one device; returns the loss code tensor [1] (p_loss)."""
     logits = model.forward(x_fwd, record)
-    loss, dz = loss_fn(logits, labels, global_batch)
+    loss, dz = loss_fn(logits, labels, global_batch, defer=True)  # loss beside the backward
     if record is not None:
         record["dlogits"] = dz
     model.backward(dz, record=record)
@@ -586,6 +619,7 @@ def train_step(model: Sequential, loss_fn: CrossEntropyLoss, opt: SGD, x_fwd, la
         for i, p in enumerate([q for q in model.params()]):
             record[f"grad_{'wb'[i % 2]}{i // 2}"] = p.grad
     opt.step()
+    loss_fn.join()
     return loss
 
 

@@ -530,6 +530,39 @@ def maxpool2d_backward(cfg, dy, argmax, x_shape, k: int = 2, stride: int = 2):
     return dx
 
 
+def softmax_xent_grad(cfg, logits, labels, log2_batch: int, grad_scale_log2: int = 0):
+    """First half of softmax_xent: (dlogits, S row sums) -- the loss half is
+    softmax_xent_loss, which may run on another stream."""
+    cfg = _cfg(cfg)
+    logits = logits.contiguous()
+    B, Cn = logits.shape
+    labels = labels.to(torch.int32).contiguous()
+    d = torch.empty_like(logits)
+    srows = torch.empty((B,), dtype=logits.dtype, device=logits.device)
+    _native.check(_native.lib().pnn_softmax_xent_grad(cfg.nbits, cfg.es, logits.data_ptr(), labels.data_ptr(),
+                                                      B, Cn, int(log2_batch), int(grad_scale_log2),
+                                                      d.data_ptr(), srows.data_ptr(), _stream_ptr(logits.device)))
+    return d, srows
+
+
+def softmax_xent_loss(cfg, logits, labels, srows, log2_batch: int, raw: bool = False):
+    """Second half: (loss [1], loss rows[, raw word, raw nar]) from softmax_xent_grad's S rows."""
+    cfg = _cfg(cfg)
+    logits = logits.contiguous()
+    B, Cn = logits.shape
+    labels = labels.to(torch.int32).contiguous()
+    rows = torch.empty((B,), dtype=logits.dtype, device=logits.device)
+    loss = torch.empty((1,), dtype=logits.dtype, device=logits.device)
+    word = torch.empty((2,), dtype=torch.int64, device=logits.device) if raw else None
+    nar = torch.empty((1,), dtype=torch.uint8, device=logits.device) if raw else None
+    _native.check(_native.lib().pnn_softmax_xent_loss(cfg.nbits, cfg.es, logits.data_ptr(), labels.data_ptr(),
+                                                      srows.data_ptr(), B, Cn, int(log2_batch), rows.data_ptr(),
+                                                      loss.data_ptr(), word.data_ptr() if raw else None,
+                                                      nar.data_ptr() if raw else None,
+                                                      _stream_ptr(logits.device)))
+    return (loss, rows, word, nar) if raw else (loss, rows)
+
+
 def maxpool2d_noidx(cfg, x, k: int, stride: int):
     """maxpool2d output only (2x2 / stride-2 tiled; None when not eligible):
     the layer recomputes the argmax in maxpool2d_backward_x."""
