@@ -137,12 +137,30 @@ int pnn_conv2d_backward(int f_nbits, int f_es, int b_nbits, int b_es, int g_nbit
                         int64_t KH, int64_t KW, int stride, int pad, void* dx, void* dw,
                         void* raw_words, void* raw_nar, void* workspace, size_t workspace_bytes,
                         void* stream);
+/* pnn_conv2d_backward for a Conv2d followed by a ReLU layer: dy is the ReLU's
+ * output gradient and gate its saved forward values (format p_f, layout of
+ * dy); the ReLU backward (dy where gate > 0, else 0, Appendix A.2) is applied
+ * inside the digitisers; dy_gated (may be NULL) receives the gated dy itself
+ * (p_b codes) when a caller wants it (pnn_bias_grad_gated does not need it). */
+int pnn_conv2d_backward_gated(int f_nbits, int f_es, int b_nbits, int b_es, int g_nbits, int g_es,
+                              const void* dy, const void* gate, void* dy_gated, const void* x,
+                              const void* saved, size_t saved_bytes, const void* w_bwd, int64_t N,
+                              int64_t C, int64_t H, int64_t W, int64_t F, int64_t KH, int64_t KW,
+                              int stride, int pad, void* dx, void* dw, void* raw_words, void* raw_nar,
+                              void* workspace, size_t workspace_bytes, void* stream);
 /* conv2d_bias_grad (tensor_ops.cpp:605-618) for dy [N,F,P] with P = OH*OW,
  * and column_sum (:722-731) with P = 1: db[f] = round(quire sum of dy[:,f,:]). */
 int pnn_bias_grad_workspace(int64_t F, size_t* bytes);
 int pnn_bias_grad(int nbits, int es, const void* dy, int64_t N, int64_t F, int64_t P, void* db,
                   void* raw_words, void* raw_nar, void* workspace, size_t workspace_bytes,
                   void* stream);
+/* conv2d_bias_grad of a ReLU's input gradient: db[f] = round(quire sum of
+ * (gate > 0 ? dy : 0)) with gate = the ReLU's forward values ((gate_nbits)
+ * codes, layout of dy) -- the gated tensor is never materialised.  Table
+ * formats (nbits <= 12) with 16-byte rows only (else PNN_EUNSUPPORTED). */
+int pnn_bias_grad_gated(int nbits, int es, const void* dy, int gate_nbits, const void* gate, int64_t N,
+                        int64_t F, int64_t P, void* db, void* raw_words, void* raw_nar, void* workspace,
+                        size_t workspace_bytes, void* stream);
 
 /* ---- elementwise kernels of the training step -----------------------------
  * Semantics: convert = convert_tensor (tensor_ops.cpp:807-821); maxpool =

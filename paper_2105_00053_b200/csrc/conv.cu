@@ -19,6 +19,7 @@
 
 #include <cstdint>
 #include <string>
+#include <type_traits>
 
 #include "../../include/pnn_b200.h"
 #include "igemm.h"
@@ -326,12 +327,16 @@ __global__ void __launch_bounds__(256) bias_grad_partial_kernel(
 // last block of the channel (arrival counter) sums the partials in slice order
 // and rounds once: Q = 2^R * sum X (mod 2^W), the reference's
 // accumulate_value per term (tensor_ops.cpp:605-618, quire.hpp:62-67).
-template <typename CodeT, int LUTB>
+// GB > 0: dy gated by a ReLU's forward values (gate codes of GB bytes, nbits
+// gnbits, same layout): the bias gradient of the ReLU's input gradient
+// without materialising it.
+template <typename CodeT, int LUTB, int GB = 0>
 __global__ void __launch_bounds__(256) bias_grad_chan_kernel(
     const CodeT* __restrict__ dy, int64_t N, int64_t F, int64_t P, PositFmt f, int slices,
     FastDiv fd_vpr, const int64_t* __restrict__ xlut, unsigned __int128* __restrict__ partial,
     uint8_t* __restrict__ nar_flag, unsigned int* __restrict__ arrivals, CodeT* __restrict__ out,
-    unsigned __int128* raw_words, uint8_t* raw_nar) {
+    unsigned __int128* raw_words, uint8_t* raw_nar, const void* __restrict__ gate = nullptr,
+    int gnbits = 0) {
     __shared__ int64_t s_lut[LUTB];
     __shared__ unsigned __int128 warp_s[8];
     __shared__ bool s_last;
@@ -348,21 +353,39 @@ __global__ void __launch_bounds__(256) bias_grad_chan_kernel(
     __int128 acc = 0;
     bool nar = false;
     constexpr int VE = 16 / int(sizeof(CodeT));
-    auto vsum = [&](const uint4& w) {
+    // gate codes of one 16-byte dy vector: VE * GB bytes
+    using GV = typename std::conditional<(VE * GB > 8), uint4, uint2>::type;
+    auto vsum = [&](const uint4& w, const GV& gv) {
         const uint32_t* ww = reinterpret_cast<const uint32_t*>(&w);
+        const uint32_t* gw = reinterpret_cast<const uint32_t*>(&gv);
         int64_t t = 0;
 #pragma unroll
         for (int j = 0; j < VE; ++j) {
             const uint32_t code = sizeof(CodeT) == 1 ? (ww[j >> 2] >> (8 * (j & 3))) & 0xFFu
                                                      : (ww[j >> 1] >> (16 * (j & 1))) & 0xFFFFu;
-            t += s_lut[code];
-            nar |= code == nar_code;
+            bool open = true;
+            if constexpr (GB > 0) {
+                const uint32_t g = GB == 1 ? (gw[j >> 2] >> (8 * (j & 3))) & 0xFFu
+                                           : (gw[j >> 1] >> (16 * (j & 1))) & 0xFFFFu;
+                open = g != 0 && ((g >> (gnbits - 1)) & 1u) == 0;
+            }
+            if (open) {
+                t += s_lut[code];
+                nar |= code == nar_code;
+            }
         }
         return t;  // |t| <= 16 * 2^56
     };
     const uint32_t vpr = uint32_t(P / VE), nv = uint32_t((n1 - n0) * vpr);
     const CodeT* base = dy + (n0 * F + ch) * P;
     const int64_t img_stride = F * P;
+    auto gload = [&](uint32_t q, uint32_t r) {
+        GV g{};
+        if constexpr (GB > 0)
+            g = __ldg(reinterpret_cast<const GV*>(static_cast<const uint8_t*>(gate) +
+                                                  ((n0 * F + ch) * P + q * img_stride) * GB) + r);
+        return g;
+    };
     uint32_t i = threadIdx.x;
     for (; i + blockDim.x < nv; i += 2 * blockDim.x) {
         uint32_t q0, r0, q1, r1;
@@ -370,12 +393,13 @@ __global__ void __launch_bounds__(256) bias_grad_chan_kernel(
         fd_vpr.divmod(i + blockDim.x, q1, r1);
         const uint4 w0 = __ldg(reinterpret_cast<const uint4*>(base + q0 * img_stride) + r0);
         const uint4 w1 = __ldg(reinterpret_cast<const uint4*>(base + q1 * img_stride) + r1);
-        acc += vsum(w0) + vsum(w1);  // 2 * 16 * 2^56 < 2^62
+        const GV g0 = gload(q0, r0), g1 = gload(q1, r1);
+        acc += vsum(w0, g0) + vsum(w1, g1);  // 2 * 16 * 2^56 < 2^62
     }
     if (i < nv) {
         uint32_t q0, r0;
         fd_vpr.divmod(i, q0, r0);
-        acc += vsum(__ldg(reinterpret_cast<const uint4*>(base + q0 * img_stride) + r0));
+        acc += vsum(__ldg(reinterpret_cast<const uint4*>(base + q0 * img_stride) + r0), gload(q0, r0));
     }
     unsigned __int128 sum = (unsigned __int128)acc;
 #pragma unroll
@@ -770,6 +794,17 @@ int pnn_conv2d_backward(int f_nbits, int f_es, int b_nbits, int b_es, int g_nbit
                         int64_t KH, int64_t KW, int stride, int pad, void* dx, void* dw,
                         void* raw_words, void* raw_nar, void* workspace, size_t workspace_bytes,
                         void* stream) {
+    return pnn_conv2d_backward_gated(f_nbits, f_es, b_nbits, b_es, g_nbits, g_es, dy, nullptr, nullptr, x,
+                                     saved, saved_bytes, w_bwd, N, C, H, W, F, KH, KW, stride, pad, dx, dw,
+                                     raw_words, raw_nar, workspace, workspace_bytes, stream);
+}
+
+int pnn_conv2d_backward_gated(int f_nbits, int f_es, int b_nbits, int b_es, int g_nbits, int g_es,
+                              const void* dy, const void* gate, void* dy_gated, const void* x,
+                              const void* saved, size_t saved_bytes, const void* w_bwd, int64_t N,
+                              int64_t C, int64_t H, int64_t W, int64_t F, int64_t KH, int64_t KW,
+                              int stride, int pad, void* dx, void* dw, void* raw_words, void* raw_nar,
+                              void* workspace, size_t workspace_bytes, void* stream) {
     if (!conv_fmt_ok(f_nbits, f_es) || !conv_fmt_ok(b_nbits, b_es) || !conv_fmt_ok(g_nbits, g_es))
         return set_status(PNN_EUNSUPPORTED, "conv: format not supported");
     ConvGeom g;
@@ -781,7 +816,7 @@ int pnn_conv2d_backward(int f_nbits, int f_es, int b_nbits, int b_es, int g_nbit
                                          make_fmt(g_nbits, g_es), g, dy, x, saved, saved_bytes, w_bwd, dx,
                                          dw, static_cast<unsigned __int128*>(raw_words),
                                          static_cast<uint8_t*>(raw_nar), workspace, workspace_bytes,
-                                         static_cast<cudaStream_t>(stream)),
+                                         static_cast<cudaStream_t>(stream), gate, f_nbits, dy_gated),
                      "conv2d_backward");
 }
 
@@ -797,6 +832,51 @@ int pnn_bias_grad_workspace(int64_t F, size_t* bytes) {
     if (F < 0 || !bytes) return set_status(PNN_EINVAL, "conv: invalid shape or argument");
     *bytes = bias_arrivals_offset(F) + size_t(F) * 4;
     return PNN_OK;
+}
+
+int pnn_bias_grad_gated(int nbits, int es, const void* dy, int gate_nbits, const void* gate, int64_t N,
+                        int64_t F, int64_t P, void* db, void* raw_words, void* raw_nar, void* workspace,
+                        size_t workspace_bytes, void* stream) {
+    if (!conv_fmt_ok(nbits, es) || gate_nbits < 2 || gate_nbits > 16)
+        return set_status(PNN_EUNSUPPORTED, "conv: format not supported");
+    if (N < 1 || F < 1 || P < 1 || !dy || !gate || (!db && !raw_words))
+        return set_status(PNN_EINVAL, "conv: invalid shape or argument");
+    if ((raw_words != nullptr) != (raw_nar != nullptr)) return set_status(PNN_EINVAL, "conv: invalid shape or argument");
+    const int VE = nbits <= 8 ? 16 : 8, GB = gate_nbits <= 8 ? 1 : 2;
+    if (nbits > kBiasLutBits || P % VE || (reinterpret_cast<uintptr_t>(dy) & 15) ||
+        (reinterpret_cast<uintptr_t>(gate) & 15) || (nbits <= 8 && GB == 2))
+        return set_status(PNN_EUNSUPPORTED, "bias_grad_gated: table formats, 16-byte rows");
+    size_t need;
+    pnn_bias_grad_workspace(F, &need);
+    if (workspace_bytes < need) return PNN_EWORKSPACE;
+    const PositFmt f = make_fmt(nbits, es);
+    auto* partial = static_cast<unsigned __int128*>(workspace);
+    auto* nar = static_cast<uint8_t*>(workspace) + size_t(F) * 16 * 64;
+    auto* arrivals = reinterpret_cast<unsigned int*>(static_cast<uint8_t*>(workspace) + bias_arrivals_offset(F));
+    auto* lut = reinterpret_cast<int64_t*>(static_cast<uint8_t*>(workspace) + bias_lut_offset(F));
+    auto st = static_cast<cudaStream_t>(stream);
+    cudaMemsetAsync(nar, 0, size_t(F), st);
+    cudaMemsetAsync(arrivals, 0, size_t(F) * 4, st);
+    x_lut_kernel<<<(1 << nbits) / 256 + 1, 256, 0, st>>>(f, lut);
+    int64_t want = (int64_t(8) * 148 + F - 1) / F;
+    int sl = int(want > 64 ? 64 : want);
+    if (sl > N) sl = int(N);
+    const int64_t per = (N + sl - 1) / sl;
+    if (per * P / VE >= (int64_t(1) << 31)) return set_status(PNN_EUNSUPPORTED, "bias_grad_gated: size");
+    const FastDiv fd{uint32_t(P / VE)};
+    const dim3 g2{unsigned(sl), unsigned(F), 1u};
+#define PNN_BGG(T, B, G)                                                                              \
+    bias_grad_chan_kernel<T, B, G><<<g2, 256, 0, st>>>((const T*)dy, N, F, P, f, sl, fd, lut, partial,  \
+                                                       nar, arrivals, (T*)db,                          \
+                                                       (unsigned __int128*)raw_words, (uint8_t*)raw_nar, \
+                                                       gate, gate_nbits)
+    if (nbits <= 8) PNN_BGG(uint8_t, 256, 1);
+    else if (nbits <= 10 && GB == 1) PNN_BGG(uint16_t, 1024, 1);
+    else if (nbits <= 10) PNN_BGG(uint16_t, 1024, 2);
+    else if (GB == 1) PNN_BGG(uint16_t, 4096, 1);
+    else PNN_BGG(uint16_t, 4096, 2);
+#undef PNN_BGG
+    return cudaGetLastError() == cudaSuccess ? PNN_OK : PNN_ECUDA;
 }
 
 int pnn_bias_grad(int nbits, int es, const void* dy, int64_t N, int64_t F, int64_t P, void* db,

@@ -390,7 +390,7 @@ template <typename SrcT>
 cudaError_t act_digits_t(int D, const SrcT* x, int64_t N, int64_t C, int64_t H, int64_t W, int64_t Cp,
                          int pad, const PositFmt& f, const PositFmt& fs, uint32_t* lut, bool build_lut,
                          int8_t* dig, uint8_t* pos_nar, uint8_t* chw_nar, uint8_t* chan_nar,
-                         uint8_t* any, cudaStream_t st) {
+                         uint8_t* any, cudaStream_t st, const DigitGate& gt) {
     // thread per (pixel, 32 channels): grid (pixel blocks, 32-channel chunks)
     if (N * H * W >= (int64_t(1) << 31)) return cudaErrorInvalidValue;
     const dim3 grid(unsigned((grid_for(N * H * W * (Cp / 32), 256) + Cp / 32 - 1) / (Cp / 32)),
@@ -399,19 +399,28 @@ cudaError_t act_digits_t(int D, const SrcT* x, int64_t N, int64_t C, int64_t H, 
     if (lut == nullptr) build_lut = false;
     // whole 256-pixel tiles per image, 16-byte aligned channel rows: staged loads
     const bool tiled = (H * W) % 256 == 0 && (256 % W == 0 || W % 256 == 0) &&
-                       (reinterpret_cast<uintptr_t>(x) & 15) == 0;
+                       (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
+                       (reinterpret_cast<uintptr_t>(gt.gate) & 15) == 0;
     const int64_t ntiles = N * H * W / 256;
     const dim3 tgrid(unsigned(ntiles < 148 * 8 ? ntiles : 148 * 8), unsigned(Cp / 32));
 #define PNN_ACT(DD)                                                                                  \
     if (build_lut) digit_lut_conv_kernel<DD><<<16, 256, 0, st>>>(fs, f, lut);                        \
-    if (tiled)                                                                                       \
-        act_digits_tiled_kernel<DD, SrcT><<<tgrid, 256, 0, st>>>(                                    \
+    if (tiled && gt.gate == nullptr)                                                                 \
+        act_digits_tiled_kernel<DD, SrcT, 0><<<tgrid, 256, 0, st>>>(                                 \
             x, int(N), int(C), int(H), int(W), int(Cp), pad, fd_hw, fd_w, f, fs, lut, dig, pos_nar,  \
-            chw_nar, chan_nar, any);                                                                 \
+            chw_nar, chan_nar, any, gt);                                                             \
+    else if (tiled && gt.gb == 1)                                                                    \
+        act_digits_tiled_kernel<DD, SrcT, 1><<<tgrid, 256, 0, st>>>(                                 \
+            x, int(N), int(C), int(H), int(W), int(Cp), pad, fd_hw, fd_w, f, fs, lut, dig, pos_nar,  \
+            chw_nar, chan_nar, any, gt);                                                             \
+    else if (tiled)                                                                                  \
+        act_digits_tiled_kernel<DD, SrcT, 2><<<tgrid, 256, 0, st>>>(                                 \
+            x, int(N), int(C), int(H), int(W), int(Cp), pad, fd_hw, fd_w, f, fs, lut, dig, pos_nar,  \
+            chw_nar, chan_nar, any, gt);                                                             \
     else                                                                                             \
         act_digits_kernel<DD, SrcT><<<grid, 256, 0, st>>>(x, int(N), int(C), int(H), int(W), int(Cp), \
                                                           pad, fd_hw, fd_w, f, fs, lut, dig, pos_nar, \
-                                                          chw_nar, chan_nar, any)
+                                                          chw_nar, chan_nar, any, gt)
     switch (D) {
         case 2: PNN_ACT(2); break;
         case 3: PNN_ACT(3); break;
@@ -429,13 +438,13 @@ cudaError_t act_digits_t(int D, const SrcT* x, int64_t N, int64_t C, int64_t H, 
 cudaError_t act_digits(int D, const void* x, int64_t N, int64_t C, int64_t H, int64_t W, int64_t Cp,
                        int pad, const PositFmt& f, const PositFmt& fs, uint32_t* lut, bool build_lut,
                        int8_t* dig, uint8_t* pos_nar, uint8_t* chw_nar, uint8_t* chan_nar, uint8_t* any,
-                       cudaStream_t st) {
+                       cudaStream_t st, const DigitGate& gt = DigitGate{}) {
     if (lut == nullptr && !same_fmt(f, fs)) return cudaErrorInvalidValue;  // no in-register convert
     if (fs.nbits <= 8)
         return act_digits_t(D, static_cast<const uint8_t*>(x), N, C, H, W, Cp, pad, f, fs, lut, build_lut,
-                            dig, pos_nar, chw_nar, chan_nar, any, st);
+                            dig, pos_nar, chw_nar, chan_nar, any, st, gt);
     return act_digits_t(D, static_cast<const uint16_t*>(x), N, C, H, W, Cp, pad, f, fs, lut, build_lut,
-                        dig, pos_nar, chw_nar, chan_nar, any, st);
+                        dig, pos_nar, chw_nar, chan_nar, any, st, gt);
 }
 
 template <typename SrcT>
@@ -592,7 +601,8 @@ struct DyDigits {
 
 template <typename CodeT>
 int run_dgrad(const ImplPlan& p, const ConvGeom& g, const CodeT* dy, const CodeT* w, CodeT* dx,
-              uint8_t* ws, cudaStream_t st, const DyDigits* pre = nullptr) {
+              uint8_t* ws, cudaStream_t st, const DyDigits* pre = nullptr,
+              const DigitGate& gt = DigitGate{}) {
     const PositFmt& f = p.a.f;
     auto* adig = reinterpret_cast<int8_t*>(ws + p.off_adig);
     auto* bdig = reinterpret_cast<int8_t*>(ws + p.off_bdig);
@@ -602,7 +612,7 @@ int run_dgrad(const ImplPlan& p, const ConvGeom& g, const CodeT* dy, const CodeT
     if (pre == nullptr && cudaMemsetAsync(ws + p.off_maps, 0, p.maps_bytes, st) != cudaSuccess) return 4;
     if (pre == nullptr &&
         act_digits(p.D, dy, g.N, g.F, g.OH, g.OW, p.Ca, 0, f, f, lut_of(p, ws, f), true, adig, pos_nar,
-                   nullptr, nullptr, flags, st) != cudaSuccess)
+                   nullptr, nullptr, flags, st, gt) != cudaSuccess)
         return 4;
     const int8_t* a_dig = pre ? pre->dig : adig;
     const uint8_t* a_pos = pre ? pre->pos_nar : pos_nar;
@@ -642,7 +652,7 @@ template <typename CodeT>
 int run_wgrad(const ImplPlan& p, const ConvGeom& g, const void* dy, const PositFmt& fdy,
               const void* x, const PositFmt& fx, CodeT* dw, unsigned __int128* raw_words,
               uint8_t* raw_nar, uint8_t* ws, cudaStream_t st, const SavedX* sv = nullptr,
-              uint8_t* share_pos_nar = nullptr) {
+              uint8_t* share_pos_nar = nullptr, const DigitGate& gt = DigitGate{}) {
     const PositFmt& f = p.a.f;
     auto* adig = sv ? sv->dig : reinterpret_cast<int8_t*>(ws + p.off_adig);
     auto* bdig = reinterpret_cast<int8_t*>(ws + p.off_bdig);
@@ -662,7 +672,7 @@ int run_wgrad(const ImplPlan& p, const ConvGeom& g, const void* dy, const PositF
         if (e != cudaSuccess) return 4;
     }
     if (act_digits(p.D, dy, g.N, g.F, g.OH, g.OW, p.Fpw, 0, f, fdy, lut_of(p, ws, fdy, 1), true, bdig,
-                   share_pos_nar, nullptr, col_nar, flags + 1, st) != cudaSuccess)
+                   share_pos_nar, nullptr, col_nar, flags + 1, st, gt) != cudaSuccess)
         return 4;
     CUtensorMap tA, tB;
     const uint32_t boxB[5] = {uint32_t(2 * p.a.OWb), uint32_t(p.a.OHb), 1, uint32_t(p.NT / 16),
@@ -741,13 +751,15 @@ bool make_bwd_plan(const PositFmt& ff, const PositFmt& fb, const PositFmt& fg, c
 template <typename GT, typename BT>
 int run_backward(const BwdPlan& b, const ConvGeom& g, const PositFmt& ff, const PositFmt& fb,
                  const void* dy, const void* x, const SavedX* sv, const void* w_bwd, void* dx, void* dw,
-                 unsigned __int128* raw_words, uint8_t* raw_nar, uint8_t* ws, cudaStream_t st) {
+                 unsigned __int128* raw_words, uint8_t* raw_nar, uint8_t* ws, cudaStream_t st,
+                 const DigitGate& gt) {
     uint8_t* wsd = ws + b.off_d;
     if (b.share_dy && cudaMemsetAsync(wsd + b.pd.off_maps, 0, b.pd.maps_bytes, st) != cudaSuccess) return 4;
     int rc = run_wgrad<GT>(b.pw, g, dy, fb, x, ff, static_cast<GT*>(dw), raw_words, raw_nar, ws, st,
                            b.use_saved ? sv : nullptr,
-                           b.share_dy ? wsd + b.pd.off_pos_nar : nullptr);
+                           b.share_dy ? wsd + b.pd.off_pos_nar : nullptr, gt);
     if (rc != 0 || !b.has_dx) return rc;
+    const DigitGate gd = gt;  // the input gradient digitises dy itself unless it shares the digits
     if (b.share_dy) {
         const DyDigits pre{reinterpret_cast<const int8_t*>(ws + b.pw.off_bdig), wsd + b.pd.off_pos_nar,
                            ws + b.pw.off_flags + 1};
@@ -755,7 +767,7 @@ int run_backward(const BwdPlan& b, const ConvGeom& g, const PositFmt& ff, const 
                              static_cast<BT*>(dx), wsd, st, &pre);
     }
     return run_dgrad<BT>(b.pd, g, static_cast<const BT*>(dy), static_cast<const BT*>(w_bwd),
-                         static_cast<BT*>(dx), wsd, st);
+                         static_cast<BT*>(dx), wsd, st, nullptr, gd);
 }
 
 }  // namespace
@@ -829,7 +841,8 @@ bool igemm_backward_eligible(const PositFmt& ff, const PositFmt& fb, const Posit
 int igemm_conv_backward(const PositFmt& ff, const PositFmt& fb, const PositFmt& fg, const ConvGeom& g,
                         const void* dy, const void* x, const void* saved, size_t saved_bytes,
                         const void* w_bwd, void* dx, void* dw, unsigned __int128* raw_words,
-                        uint8_t* raw_nar, void* ws, size_t ws_bytes, cudaStream_t st) {
+                        uint8_t* raw_nar, void* ws, size_t ws_bytes, cudaStream_t st,
+                        const void* gate, int gate_nbits, void* dy_gated) {
     BwdPlan b;
     if (!make_bwd_plan(ff, fb, fg, g, raw_words != nullptr, dx != nullptr, saved != nullptr, &b)) return 2;
     if (ws_bytes < b.total) return 3;
@@ -842,14 +855,29 @@ int igemm_conv_backward(const PositFmt& ff, const PositFmt& fb, const PositFmt& 
         sv = saved_of(const_cast<void*>(saved), L);
     }
     auto* w = static_cast<uint8_t*>(ws);
+    DigitGate gt{};
+    if (gate != nullptr) {
+        gt.gate = gate;
+        gt.gb = gate_nbits <= 8 ? 1 : 2;
+        gt.gnbits = gate_nbits;
+    }
+    if (dy_gated != nullptr) {  // the ReLU's input gradient itself (recording / the bias gradient)
+        const int64_t total = g.N * g.F * g.OH * g.OW;
+        if (fb.nbits <= 8)
+            gate_codes_kernel<uint8_t><<<grid_for(total, 256), 256, 0, st>>>(
+                static_cast<const uint8_t*>(dy), gt, static_cast<uint8_t*>(dy_gated), total);
+        else
+            gate_codes_kernel<uint16_t><<<grid_for(total, 256), 256, 0, st>>>(
+                static_cast<const uint16_t*>(dy), gt, static_cast<uint16_t*>(dy_gated), total);
+    }
     const bool g8 = fg.nbits <= 8, b8 = fb.nbits <= 8;
     if (g8 && b8)
-        return run_backward<uint8_t, uint8_t>(b, g, ff, fb, dy, x, &sv, w_bwd, dx, dw, raw_words, raw_nar, w, st);
+        return run_backward<uint8_t, uint8_t>(b, g, ff, fb, dy, x, &sv, w_bwd, dx, dw, raw_words, raw_nar, w, st, gt);
     if (g8)
-        return run_backward<uint8_t, uint16_t>(b, g, ff, fb, dy, x, &sv, w_bwd, dx, dw, raw_words, raw_nar, w, st);
+        return run_backward<uint8_t, uint16_t>(b, g, ff, fb, dy, x, &sv, w_bwd, dx, dw, raw_words, raw_nar, w, st, gt);
     if (b8)
-        return run_backward<uint16_t, uint8_t>(b, g, ff, fb, dy, x, &sv, w_bwd, dx, dw, raw_words, raw_nar, w, st);
-    return run_backward<uint16_t, uint16_t>(b, g, ff, fb, dy, x, &sv, w_bwd, dx, dw, raw_words, raw_nar, w, st);
+        return run_backward<uint16_t, uint8_t>(b, g, ff, fb, dy, x, &sv, w_bwd, dx, dw, raw_words, raw_nar, w, st, gt);
+    return run_backward<uint16_t, uint16_t>(b, g, ff, fb, dy, x, &sv, w_bwd, dx, dw, raw_words, raw_nar, w, st, gt);
 }
 
 }  // namespace pnn_b200

@@ -46,6 +46,7 @@ bool igemm_backward_eligible(const PositFmt& ff, const PositFmt& fb, const Posit
 int igemm_conv_backward(const PositFmt& ff, const PositFmt& fb, const PositFmt& fg, const ConvGeom& g,
                         const void* dy, const void* x, const void* saved, size_t saved_bytes,
                         const void* w_bwd, void* dx, void* dw, unsigned __int128* raw_words,
-                        uint8_t* raw_nar, void* ws, size_t ws_bytes, cudaStream_t st);
+                        uint8_t* raw_nar, void* ws, size_t ws_bytes, cudaStream_t st,
+                        const void* gate = nullptr, int gate_nbits = 0, void* dy_gated = nullptr);
 
 }  // namespace pnn_b200

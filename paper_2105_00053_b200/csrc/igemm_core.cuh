@@ -453,6 +453,28 @@ __device__ __forceinline__ uint32_t digits4_words(const uint32_t (&c)[4], const 
     return nm;
 }
 
+// ReLU gate fused into a digitiser (the Conv2d backward after a ReLU layer,
+// SURVEY.md Appendix A.2): code -> positive(gate) ? code : 0 with gate codes
+// of the same [N][C][H][W] layout (gb bytes each, nbits gnbits).
+struct DigitGate {
+    const void* gate = nullptr;
+    int gb = 0, gnbits = 0;
+    __device__ __forceinline__ bool open(int64_t i) const {
+        const uint32_t c = gb == 1 ? uint32_t(static_cast<const uint8_t*>(gate)[i])
+                                   : uint32_t(static_cast<const uint16_t*>(gate)[i]);
+        return c != 0 && ((c >> (gnbits - 1)) & 1u) == 0;
+    }
+};
+
+// out = gated codes (the ReLU backward, when its result itself is wanted)
+template <typename CodeT>
+__global__ void gate_codes_kernel(const CodeT* __restrict__ dy, DigitGate gt, CodeT* __restrict__ out,
+                                  int64_t n) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x)
+        out[i] = gt.open(i) ? dy[i] : CodeT(0);
+}
+
 // codes [N][C][H][W] -> dig[D][N][Hp][Cp/16][Wp][16] (slice layout, balanced
 // int8 digits; channels >= C are zero; Hp = H + 2 pad, Wp = W + 2 pad with the
 // pad ring written as zeros by the border pixels' threads), plus NaR summaries
@@ -545,7 +567,7 @@ __global__ void __launch_bounds__(256) act_digits_kernel(
     const CodeT* __restrict__ x, int N, int C, int H, int W, int Cp, int pad, FastDiv fd_hw,
     FastDiv fd_w, PositFmt f, PositFmt fs, const uint32_t* __restrict__ lut,
     int8_t* __restrict__ dig, uint8_t* __restrict__ pos_nar, uint8_t* __restrict__ chw_nar,
-    uint8_t* __restrict__ chan_nar, uint8_t* __restrict__ any) {
+    uint8_t* __restrict__ chan_nar, uint8_t* __restrict__ any, DigitGate gt = DigitGate{}) {
     const uint32_t HW = uint32_t(H) * uint32_t(W);
     const uint32_t pixels = uint32_t(N) * HW;
     const int64_t plane = int64_t(N) * (H + 2 * pad) * (W + 2 * pad) * Cp;
@@ -555,10 +577,16 @@ __global__ void __launch_bounds__(256) act_digits_kernel(
         uint32_t n, pix;  // pixel raster index r = (n, h, w)
         fd_hw.divmod(r, n, pix);
         const int c0 = cc * 32;
-        const CodeT* src = x + (int64_t(n) * C + c0) * HW + pix;
+        const int64_t base = (int64_t(n) * C + c0) * HW + pix;
+        const CodeT* src = x + base;
         uint32_t code[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) code[j] = c0 + j < C ? uint32_t(src[j * HW]) : 0u;
+        if (gt.gate != nullptr) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+                if (c0 + j < C && !gt.open(base + int64_t(j) * HW)) code[j] = 0u;
+        }
         uint32_t h, w;
         fd_w.divmod(pix, h, w);
         emit_pixel_digits<D>(code, r, n, pix, h, w, cc, C, H, W, Cp, pad, plane, HW, f, nar_code, lut,
@@ -572,15 +600,16 @@ __global__ void __launch_bounds__(256) act_digits_kernel(
 // memory (the per-thread strided loads of the generic kernel move 32 or 64
 // bytes per warp instruction), then each thread reads its pixel's 32 codes
 // across the rows.
-template <int D, typename CodeT>
+template <int D, typename CodeT, int GB = 0>
 __global__ void __launch_bounds__(256) act_digits_tiled_kernel(
     const CodeT* __restrict__ x, int N, int C, int H, int W, int Cp, int pad, FastDiv fd_hw,
     FastDiv fd_w, PositFmt f, PositFmt fs, const uint32_t* __restrict__ lut,
     int8_t* __restrict__ dig, uint8_t* __restrict__ pos_nar, uint8_t* __restrict__ chw_nar,
-    uint8_t* __restrict__ chan_nar, uint8_t* __restrict__ any) {
+    uint8_t* __restrict__ chan_nar, uint8_t* __restrict__ any, DigitGate gt = DigitGate{}) {
     constexpr int TP = 256;                                   // pixels per tile
     constexpr int VPR = TP * int(sizeof(CodeT)) / 16;         // 16-byte vectors per channel row
     __shared__ uint4 s_tile[32 * VPR];
+    __shared__ uint4 s_gate[GB > 0 ? 32 * TP * GB / 16 : 1];  // gate codes (GB bytes each)
     const uint32_t HW = uint32_t(H) * uint32_t(W);
     const uint32_t tiles = uint32_t(N) * (HW / TP);
     const int64_t plane = int64_t(N) * (H + 2 * pad) * (W + 2 * pad) * Cp;
@@ -597,11 +626,31 @@ __global__ void __launch_bounds__(256) act_digits_tiled_kernel(
                                          x + (int64_t(n) * C + c0 + c) * HW + pix0) + v)
                                    : make_uint4(0, 0, 0, 0);
         }
+        if constexpr (GB > 0) {
+            constexpr int GVPR = TP * GB / 16;
+            for (int i = threadIdx.x; i < 32 * GVPR; i += blockDim.x) {
+                const int c = i / GVPR, v = i - c * GVPR;
+                s_gate[i] = c0 + c < C
+                                ? __ldg(reinterpret_cast<const uint4*>(static_cast<const uint8_t*>(gt.gate) +
+                                                                       ((int64_t(n) * C + c0 + c) * HW + pix0) *
+                                                                           GB) + v)
+                                : make_uint4(0, 0, 0, 0);
+            }
+        }
         __syncthreads();
         const CodeT* st = reinterpret_cast<const CodeT*>(s_tile);
         uint32_t code[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) code[j] = uint32_t(st[j * TP + threadIdx.x]);
+        if constexpr (GB > 0) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                const int k = j * TP + threadIdx.x;
+                const uint32_t g = GB == 1 ? uint32_t(reinterpret_cast<const uint8_t*>(s_gate)[k])
+                                           : uint32_t(reinterpret_cast<const uint16_t*>(s_gate)[k]);
+                if (!(g != 0 && ((g >> (gt.gnbits - 1)) & 1u) == 0)) code[j] = 0u;
+            }
+        }
         const uint32_t pix = pix0 + threadIdx.x;
         uint32_t h, w;
         fd_w.divmod(pix, h, w);

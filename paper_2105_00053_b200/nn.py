@@ -148,6 +148,37 @@ class Conv2d(Module):
                                            self.saved)
         return ops.conv2d(f, x, self.w.as_(f), self.b.as_(f), self.stride, self.pad)
 
+    def backward_gated(self, dy, gate, raw=False, want_gated=False):
+        """Backward of this layer and the ReLU after it in one pass (the ReLU's
+        gate applied in the digitisers and in the bias-gradient sum): dy = the
+        ReLU's output gradient, gate = the ReLU's forward output.  Returns (dx,
+        the ReLU's input gradient if want_gated else None) or None when the
+        fused path is not eligible."""
+        st = self.st
+        g = st.gradient
+        bias_direct = st.backward == g  # bias grad straight from (dy, gate), nothing materialised
+        res = ops.conv2d_backward_gated(st.forward, st.backward, g, dy, gate, self.x, self.saved,
+                                        None if self.first_layer else self.w.as_(st.backward),
+                                        self.x.shape, self.w.shape, self.stride, self.pad,
+                                        need_dx=not self.first_layer, raw=raw,
+                                        want_gated=want_gated or not bias_direct)
+        if res is None:
+            return None
+        self.saved = None
+        dx, dw, dyb = res
+        bg = ops.conv2d_bias_grad_gated(g, dy, st.forward, gate, raw=raw) if bias_direct else None
+        if bg is None:
+            if dyb is None:
+                dyb = ops.relu_bwd(st.forward, gate, st.backward, dy)
+            bg = ops.conv2d_bias_grad(g, ops.convert_tensor(dyb, st.backward, g), raw=raw)
+        if raw:
+            _, self.w.grad_words, self.w.grad_nar = dw
+            _, self.b.grad_words, self.b.grad_nar = bg
+        else:
+            self.w.grad = dw
+            self.b.grad = bg
+        return dx, dyb
+
     def backward(self, dy, raw=False):
         """dy in p_backward -> dx in p_backward (None for the first layer)."""
         st = self.st
@@ -477,6 +508,7 @@ class Sequential(Module):
 
     def forward(self, x, record=None):
         i, n = 0, len(self.layers)
+        self._relu_fused = set()  # indices of ReLU layers fused into the preceding Conv2d
         while i < n:
             l = self.layers[i]
             nxt = self.layers[i + 1] if i + 1 < n else None
@@ -487,6 +519,7 @@ class Sequential(Module):
                 if res is not None:
                     y, pre = res
                     nxt.x = y
+                    self._relu_fused.add(i + 1)
                     if record is not None:
                         record[f"act{i}"] = pre
                         record[f"act{i + 1}"] = y
@@ -499,13 +532,38 @@ class Sequential(Module):
             i += 1
         return x
 
+    # Backward of a fused Conv2d + ReLU pair through Conv2d.backward_gated (the
+    # ReLU gate applied inside the dy digitiser and the bias-gradient sum) is
+    # bit-identical but measured slower on B200 than the vectorised relu_bwd
+    # kernel followed by the conv backward (config-3 step 2.94 -> 3.04 ms: the
+    # gate tests cost more ALU in those two kernels than the 5 B/element
+    # relu_bwd pass), so it is off by default.
+    fuse_relu_backward = False
+
     def backward(self, dy, raw=False, record=None):
-        for i in range(len(self.layers) - 1, -1, -1):
+        fused = getattr(self, "_relu_fused", set()) if self.fuse_relu_backward else set()
+        i = len(self.layers) - 1
+        while i >= 0:
+            if i in fused:  # ReLU i fused with Conv2d i-1: one backward, gate in the digitisers
+                res = self.layers[i - 1].backward_gated(dy, self.layers[i].x, raw=raw,
+                                                        want_gated=record is not None)
+                if res is not None:
+                    dx, dy_relu = res
+                    if record is not None:
+                        record[f"dact{i}"] = dy_relu
+                    dy = dx
+                    if dy is None:
+                        break
+                    if record is not None:
+                        record[f"dact{i - 1}"] = dy
+                    i -= 2
+                    continue
             dy = self.layers[i].backward(dy, raw=raw)
             if dy is None:
                 break
             if record is not None:
                 record[f"dact{i}"] = dy
+            i -= 1
         return dy
 
 

@@ -429,6 +429,43 @@ def conv2d_backward(f_cfg, b_cfg, g_cfg, dy, x, saved, w_bwd, x_shape, w_shape, 
     return dx, ((None, words, nar) if raw else dw)
 
 
+def conv2d_backward_gated(f_cfg, b_cfg, g_cfg, dy, gate, x, saved, w_bwd, x_shape, w_shape, stride: int,
+                          pad: int, need_dx: bool, raw: bool = False, want_gated: bool = True):
+    """conv2d_backward of a Conv2d followed by a ReLU: dy is the ReLU's output
+    gradient, gate its saved forward output (p_f); the ReLU backward is applied
+    inside the digitisers.  Returns (dx | None, dw | (None, words, nar), gated dy)
+    or None when not eligible.  want_gated=False skips the gated dy (None)."""
+    f, b, g = _cfg(f_cfg), _cfg(b_cfg), _cfg(g_cfg)
+    nbytes = conv2d_backward_eligible(f, b, g, x_shape, w_shape, stride, pad, raw, need_dx, saved is not None)
+    if nbytes is None:
+        return None
+    _check_codes(b, dy, w_bwd if need_dx else None)
+    _check_codes(f, gate)
+    if x is not None:
+        _check_codes(f, x)
+        x = x.contiguous()
+    dy, gate = dy.contiguous(), gate.contiguous()
+    w_bwd = w_bwd.contiguous() if need_dx else None
+    N, Cc, H, W = (int(v) for v in x_shape)
+    F, _, KH, KW = (int(v) for v in w_shape)
+    dev = dy.device
+    dx = torch.empty((N, Cc, H, W), dtype=b.code_dtype, device=dev) if need_dx else None
+    dw = words = nar = None
+    if raw:
+        words = torch.empty((F, Cc, KH, KW, 2), dtype=torch.int64, device=dev)
+        nar = torch.empty((F, Cc, KH, KW), dtype=torch.uint8, device=dev)
+    else:
+        dw = torch.empty((F, Cc, KH, KW), dtype=g.code_dtype, device=dev)
+    dyg = torch.empty_like(dy) if want_gated else None
+    ws = _ws.get(dev, nbytes)
+    ptr = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
+    _native.check(_native.lib().pnn_conv2d_backward_gated(
+        f.nbits, f.es, b.nbits, b.es, g.nbits, g.es, dy.data_ptr(), gate.data_ptr(), ptr(dyg), ptr(x),
+        ptr(saved), saved.numel() if saved is not None else 0, ptr(w_bwd), N, Cc, H, W, F, KH, KW, stride,
+        pad, ptr(dx), ptr(dw), ptr(words), ptr(nar), ws.data_ptr(), ws.numel(), _stream_ptr(dev)))
+    return dx, ((None, words, nar) if raw else dw), dyg
+
+
 def _bias_grad(cfg, dy3, raw=False, use_quire=True):
     N, F, P = dy3.shape
     db = torch.empty((F,), dtype=cfg.code_dtype, device=dy3.device)
@@ -458,6 +495,30 @@ def conv2d_bias_grad(cfg, dy, use_quire: bool = True, raw: bool = False):
         raise _native.PnnInvalidArgument(1, "conv2d_bias_grad: bad rank")
     N, F, OH, OW = dy.shape
     return _bias_grad(cfg, dy.contiguous().view(N, F, OH * OW), raw, use_quire)
+
+
+def conv2d_bias_grad_gated(cfg, dy, gate_cfg, gate, raw: bool = False):
+    """conv2d_bias_grad of relu_bwd(gate, dy) without materialising it; None
+    when the kernel does not cover the format / row length."""
+    cfg, gc = _cfg(cfg), _cfg(gate_cfg)
+    _check_codes(cfg, dy)
+    _check_codes(gc, gate)
+    N, F, OH, OW = dy.shape
+    dy, gate = dy.contiguous(), gate.contiguous()
+    db = torch.empty((F,), dtype=cfg.code_dtype, device=dy.device)
+    words = torch.empty((F, 2), dtype=torch.int64, device=dy.device) if raw else None
+    nar = torch.empty((F,), dtype=torch.uint8, device=dy.device) if raw else None
+    n = C.c_size_t()
+    _native.check(_native.lib().pnn_bias_grad_workspace(F, C.byref(n)))
+    ws = _ws.get(dy.device, n.value)
+    rc = _native.lib().pnn_bias_grad_gated(cfg.nbits, cfg.es, dy.data_ptr(), gc.nbits, gate.data_ptr(), N, F,
+                                           OH * OW, db.data_ptr(), words.data_ptr() if raw else None,
+                                           nar.data_ptr() if raw else None, ws.data_ptr(), ws.numel(),
+                                           _stream_ptr(dy.device))
+    if rc == 2:
+        return None
+    _native.check(rc)
+    return (db, words, nar) if raw else db
 
 
 def column_sum(cfg, x, use_quire: bool = True, raw: bool = False):

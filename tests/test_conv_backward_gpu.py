@@ -161,3 +161,53 @@ def test_fused_relu_forward(cuda, cfg, shape):
     assert torch.equal(y, ops.relu_fwd(cfg, ref))
     y2, none = ops.conv2d_fwd_layer(cfg, x, w, b, 1, pad, None, relu=True, want_pre=False)
     assert none is None and torch.equal(y2, y)
+
+
+@pytest.mark.parametrize("stages", [(P81, P121, P121), (P80, P80, P80), (P121, P81, P121), (P161, P161, P161)])
+@pytest.mark.parametrize("shape", [(2, 32, 8, 8, 32, 3, 1), (2, 3, 32, 32, 32, 3, 1), (3, 64, 16, 16, 64, 3, 1),
+                                   (2, 32, 8, 8, 40, 3, 1)])
+def test_gated_backward_equals_relu_then_conv(cuda, stages, shape):
+    """Conv2d + ReLU backward in one call (gate applied in the digitisers) ==
+    relu_bwd followed by the fused conv backward; NaR and zero gates included."""
+    ff, fb, fg = stages
+    N, C, H, W, F, K, pad = shape
+    rng = np.random.default_rng(hash((stages, shape, 1)) & 0xFFFF)
+    x = dev(ff, rand_codes(rng, ff[0], (N, C, H, W)))
+    w = dev(ff, rand_codes(rng, ff[0], (F, C, K, K)))
+    OH, OW = H + 2 * pad - K + 1, W + 2 * pad - K + 1
+    gate_a = rand_codes(rng, ff[0], (N, F, OH, OW), nar_ok=True)
+    gate_a[0, 0] = 0
+    gate = dev(ff, gate_a)
+    dy = dev(fb, rand_codes(rng, fb[0], (N, F, OH, OW), nar_ok=True))
+    wb = dev(fb, rand_codes(rng, fb[0], (F, C, K, K)))
+    need_dx = C % 32 == 0 and F % 32 == 0
+    n = ops.conv2d_saved_bytes(ff, x.shape, w.shape, 1, pad)
+    saved = torch.empty(n, dtype=torch.uint8, device="cuda") if n else None
+    ops.conv2d_fwd_save(ff, x, w, None, 1, pad, saved) if saved is not None else None
+    res = ops.conv2d_backward_gated(ff, fb, fg, dy, gate, x, saved, wb, x.shape, w.shape, 1, pad, need_dx)
+    assert res is not None
+    dx, dw, dyg = res
+    want_dyg = ops.relu_bwd(ff, gate, fb, dy)
+    assert torch.equal(dyg, want_dyg)
+    ref = ops.conv2d_backward(ff, fb, fg, want_dyg, x, saved, wb, x.shape, w.shape, 1, pad, need_dx)
+    assert torch.equal(dw, ref[1])
+    if need_dx:
+        assert torch.equal(dx, ref[0])
+
+
+def test_fused_relu_backward_step_matches(cuda, po):
+    """Sequential with fuse_relu_backward on: a config-3-format CIFAR-CNN step at a
+    small batch is bit-identical to the default (two-kernel) backward."""
+    from paper_2105_00053_b200 import codec, nn
+    st = nn.StagePrecisions(ops.P81, ops.P121, ops.P121, ops.P161, ops.P161)
+    rng = np.random.default_rng(4)
+    x = codec.from_float64_device(rng.uniform(-1, 1, (8, 3, 32, 32)), st.forward)
+    lab = torch.from_numpy(rng.integers(0, 10, 8).astype(np.int32)).cuda()
+    outs = []
+    for fuse in (False, True):
+        model = nn.cifar_cnn(st, seed=3)
+        model.fuse_relu_backward = fuse
+        loss = nn.train_step(model, nn.CrossEntropyLoss(st), nn.SGD(model.params(), 1 / 16, st), x, lab, 8)
+        outs.append([loss] + [p.master for p in model.params()])
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)

@@ -81,3 +81,21 @@ def test_bias_grad_single_launch_vs_oracle(cuda, po, cfg, shape):
     assert (got.cpu().numpy().astype(np.uint64) == want).all()
     db, words, nar = ops.conv2d_bias_grad(cfg, dev(cfg, dy), raw=True)
     assert torch.equal(db, got)
+
+
+@pytest.mark.parametrize("cfg,gcfg", [((12, 1), (8, 1)), ((8, 0), (8, 0)), ((12, 1), (12, 1)), ((8, 1), (8, 1))])
+@pytest.mark.parametrize("shape", [(64, 32, 32, 32), (7, 64, 16, 16), (3, 5, 4, 4)])
+def test_bias_grad_gated(cuda, cfg, gcfg, shape):
+    """bias grad of relu_bwd(gate, dy) without materialising it == the two-step path."""
+    rng = np.random.default_rng(hash((cfg, gcfg, shape)) & 0xFFFF)
+    dy = dev(cfg, rand_codes(rng, cfg[0], shape, nar_ok=True))
+    gate = dev(gcfg, rand_codes(rng, gcfg[0], shape, nar_ok=True))
+    got = ops.conv2d_bias_grad_gated(cfg, dy, gcfg, gate)
+    want = ops.conv2d_bias_grad(cfg, ops.relu_bwd(gcfg, gate, cfg, dy))
+    if shape[2] * shape[3] % (16 if cfg[0] <= 8 else 8) or (cfg[0] <= 8 and gcfg[0] > 8):
+        assert got is None
+        return
+    assert torch.equal(got, want)
+    g2 = ops.conv2d_bias_grad_gated(cfg, dy, gcfg, gate, raw=True)
+    w2 = ops.conv2d_bias_grad(cfg, ops.relu_bwd(gcfg, gate, cfg, dy), raw=True)
+    assert all(torch.equal(a, b) for a, b in zip(g2, w2))
