@@ -186,6 +186,12 @@ int pnn_maxpool2d_bwd(int nbits, int es, const void* dy, const int64_t* argmax, 
 int pnn_maxpool2d_bwd_x(int x_nbits, int x_es, const void* x, int g_nbits, int g_es, const void* dy,
                         int64_t N, int64_t C, int64_t H, int64_t W, int k, int stride, void* dx,
                         void* stream);
+/* Same, for a MaxPool2d fed by a ReLU (x = the ReLU's output): relu_gate != 0
+ * also applies the ReLU backward (zero unless the window max is > 0), i.e.
+ * relu_bwd(maxpool2d_backward(dy)) in one pass. */
+int pnn_maxpool2d_relu_bwd_x(int x_nbits, int x_es, const void* x, int g_nbits, int g_es, const void* dy,
+                             int64_t N, int64_t C, int64_t H, int64_t W, int k, int stride, int relu_gate,
+                             void* dx, void* stream);
 /* logits [B, classes] in the loss format; labels int32 [B]; outputs dlogits
  * [B, classes] (already scaled by 2^-log2_batch), per-row losses [B], the
  * batch loss (1 code, may be NULL) and/or the raw quire word (16 bytes) + NaR

@@ -74,6 +74,8 @@ _SIGS = {
                                       _vp, C.c_size_t, _vp]),
     "pnn_sgd_step_multi": (C.c_int, [C.c_int] * 4 + [C.c_uint32] + [C.c_int] * 6 +
                            [_vp, _vp, _vp, _vp, _vp, _vp]),
+    "pnn_maxpool2d_relu_bwd_x": (C.c_int, [C.c_int, C.c_int, _vp, C.c_int, C.c_int, _vp] + [_i64] * 4 +
+                                 [C.c_int, C.c_int, C.c_int, _vp, _vp]),
     "pnn_maxpool2d_bwd_x": (C.c_int, [C.c_int, C.c_int, _vp, C.c_int, C.c_int, _vp] + [_i64] * 4 +
                             [C.c_int, C.c_int, _vp, _vp]),
     "pnn_softmax_xent": (C.c_int, [C.c_int, C.c_int, _vp, _vp, _i64, _i64, C.c_int, _vp, _vp, _vp, _vp, _vp,

@@ -203,10 +203,13 @@ __global__ void __launch_bounds__(256) maxpool2_fwd_vec_kernel(int nbits, const 
 // dx = maxpool2d_backward(dy, argmax(x)) without a stored argmax: the window's
 // first strict max is recomputed from x; dy (format of TG) lands there, zeros
 // elsewhere (tiled windows: every input lies in exactly one window).
+// relu_gate: also apply the backward of a ReLU whose output x is (x > 0 at the
+// argmax, Appendix A.2) -- the ReLU -> MaxPool pair's backward in one pass.
 template <typename TX, typename TG>
 __global__ void __launch_bounds__(256) maxpool2_bwd_x_kernel(int x_nbits, const TX* __restrict__ x,
                                                              const TG* __restrict__ dy,
-                                                             TG* __restrict__ dx, int rows, int OW) {
+                                                             TG* __restrict__ dx, int rows, int OW,
+                                                             int relu_gate = 0) {
     constexpr int VE = 16 / sizeof(TX), WPT = VE / 2;
     const int W = 2 * OW, vpr = OW / WPT;
     const int total = rows * vpr;
@@ -221,11 +224,16 @@ __global__ void __launch_bounds__(256) maxpool2_bwd_x_kernel(int x_nbits, const 
         const TG* gp = dy + int64_t(r) * OW + v * WPT;
 #pragma unroll
         for (int j = 0; j < WPT; ++j) g[j] = uint32_t(gp[j]);
+        const uint32_t sign = 1u << (x_nbits - 1);
         uint32_t top[16] = {}, bot[16] = {};  // VE used (pack16_u8 reads 16)
 #pragma unroll
         for (int j = 0; j < WPT; ++j) {
             const int k = argmax4(int32_t(a[2 * j] << sh), int32_t(a[2 * j + 1] << sh),
                                   int32_t(b[2 * j] << sh), int32_t(b[2 * j + 1] << sh));
+            if (relu_gate) {  // the window max is the ReLU output at the argmax
+                const uint32_t mx = k == 0 ? a[2 * j] : k == 1 ? a[2 * j + 1] : k == 2 ? b[2 * j] : b[2 * j + 1];
+                if (mx == 0 || (mx & sign)) g[j] = 0u;
+            }
             top[2 * j] = k == 0 ? g[j] : 0u;
             top[2 * j + 1] = k == 1 ? g[j] : 0u;
             bot[2 * j] = k == 2 ? g[j] : 0u;
@@ -752,6 +760,13 @@ int pnn_maxpool2d_fwd(int nbits, int es, const void* x, int64_t N, int64_t C, in
 int pnn_maxpool2d_bwd_x(int x_nbits, int x_es, const void* x, int g_nbits, int g_es, const void* dy,
                         int64_t N, int64_t C, int64_t H, int64_t W, int k, int stride, void* dx,
                         void* stream) {
+    return pnn_maxpool2d_relu_bwd_x(x_nbits, x_es, x, g_nbits, g_es, dy, N, C, H, W, k, stride, 0, dx,
+                                    stream);
+}
+
+int pnn_maxpool2d_relu_bwd_x(int x_nbits, int x_es, const void* x, int g_nbits, int g_es, const void* dy,
+                             int64_t N, int64_t C, int64_t H, int64_t W, int k, int stride, int relu_gate,
+                             void* dx, void* stream) {
     CHECK_FMT(x_nbits, x_es);
     CHECK_FMT(g_nbits, g_es);
     if (N < 0 || C < 1 || k < 1 || stride < 1 || H < k || W < k || !x || !dy || !dx)
@@ -765,7 +780,7 @@ int pnn_maxpool2d_bwd_x(int x_nbits, int x_es, const void* x, int g_nbits, int g
     const bool x8 = x_nbits <= 8, g8 = g_nbits <= 8;
 #define PNN_MPB(TX, TG)                                                                    \
     maxpool2_bwd_x_kernel<TX, TG><<<grid, 256, 0, st>>>(x_nbits, (const TX*)x, (const TG*)dy, \
-                                                        (TG*)dx, rows, OW)
+                                                        (TG*)dx, rows, OW, relu_gate)
     if (x8 && g8) PNN_MPB(uint8_t, uint8_t);
     else if (x8) PNN_MPB(uint8_t, uint16_t);
     else if (g8) PNN_MPB(uint16_t, uint8_t);

@@ -258,6 +258,14 @@ class MaxPool2d(Module):
         y, self.argmax = ops.maxpool2d(self.st.forward, x, self.k, self.stride)
         return y
 
+    def backward_relu(self, dy, relu):
+        """Backward of this pool and the ReLU before it in one pass (the pool's
+        input is that ReLU's output); None when the pool keeps an argmax."""
+        if self.x is None or relu.x is None or (relu.x is not self.x and relu.x.data_ptr() != self.x.data_ptr()):
+            return None
+        return ops.maxpool2d_backward_x(self.st.forward, self.x, self.st.backward, dy, self.k, self.stride,
+                                        relu_gate=True)
+
     def backward(self, dy, raw=False):
         if self.x is not None:
             return ops.maxpool2d_backward_x(self.st.forward, self.x, self.st.backward, dy, self.k,
@@ -556,6 +564,14 @@ class Sequential(Module):
                         break
                     if record is not None:
                         record[f"dact{i - 1}"] = dy
+                    i -= 2
+                    continue
+            if (record is None and isinstance(self.layers[i], MaxPool2d) and i >= 1
+                    and type(self.layers[i - 1]) is ReLU):
+                # ReLU -> MaxPool: one backward pass (the pool's input is the ReLU's output)
+                d2 = self.layers[i].backward_relu(dy, self.layers[i - 1])
+                if d2 is not None:
+                    dy = d2
                     i -= 2
                     continue
             dy = self.layers[i].backward(dy, raw=raw)

@@ -639,15 +639,16 @@ def maxpool2d_noidx(cfg, x, k: int, stride: int):
     return y
 
 
-def maxpool2d_backward_x(x_cfg, x, g_cfg, dy, k: int = 2, stride: int = 2):
-    """maxpool2d_backward(dy, argmax(maxpool2d(x))) with the argmax recomputed from x."""
+def maxpool2d_backward_x(x_cfg, x, g_cfg, dy, k: int = 2, stride: int = 2, relu_gate: bool = False):
+    """maxpool2d_backward(dy, argmax(maxpool2d(x))) with the argmax recomputed from x;
+    relu_gate: x is a ReLU's output and the ReLU's backward is applied too."""
     xc, gc = _cfg(x_cfg), _cfg(g_cfg)
     x = x.contiguous()
     N, Cc, H, W = x.shape
     dx = torch.empty((N, Cc, H, W), dtype=gc.code_dtype, device=dy.device)
-    _native.check(_native.lib().pnn_maxpool2d_bwd_x(xc.nbits, xc.es, x.data_ptr(), gc.nbits, gc.es,
-                                                    dy.contiguous().data_ptr(), N, Cc, H, W, k, stride,
-                                                    dx.data_ptr(), _stream_ptr(dy.device)))
+    _native.check(_native.lib().pnn_maxpool2d_relu_bwd_x(xc.nbits, xc.es, x.data_ptr(), gc.nbits, gc.es,
+                                                         dy.contiguous().data_ptr(), N, Cc, H, W, k, stride,
+                                                         int(relu_gate), dx.data_ptr(), _stream_ptr(dy.device)))
     return dx
 
 

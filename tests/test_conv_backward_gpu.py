@@ -211,3 +211,24 @@ def test_fused_relu_backward_step_matches(cuda, po):
         outs.append([loss] + [p.master for p in model.params()])
     for a, b in zip(*outs):
         assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("st_fmt", ["config3", "uniform80"])
+def test_unrecorded_step_equals_recorded_step(cuda, st_fmt):
+    """The fusions the layer path takes only when it does not record (ReLU ->
+    MaxPool backward in one pass) leave every parameter bit-identical to the
+    recorded (per-layer, oracle-checked) step."""
+    from paper_2105_00053_b200 import codec, nn
+    st = (nn.StagePrecisions(ops.P81, ops.P121, ops.P121, ops.P161, ops.P161) if st_fmt == "config3"
+          else nn.StagePrecisions.uniform(ops.P80))
+    rng = np.random.default_rng(9)
+    x = codec.from_float64_device(rng.uniform(-1, 1, (8, 3, 32, 32)), st.forward)
+    lab = torch.from_numpy(rng.integers(0, 10, 8).astype(np.int32)).cuda()
+    outs = []
+    for record in ({}, None):
+        model = nn.cifar_cnn(st, seed=5)
+        loss = nn.train_step(model, nn.CrossEntropyLoss(st), nn.SGD(model.params(), 1 / 16, st), x, lab, 8,
+                             record=record)
+        outs.append([loss] + [p.master for p in model.params()])
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
