@@ -13,6 +13,7 @@
 
 #include "../../include/pnn_b200.h"
 #include "eltwise_common.cuh"
+#include "epilogue.cuh"
 #include "posit_scalar.cuh"
 #include "status.h"
 
@@ -515,9 +516,36 @@ struct SgdSegs {
     void* copy2[kSgdMaxSeg];
 };
 
+// The SGD update on integer images (exact), each rounding by the quire
+// rounding table -- the same correctly rounded results as the scalar ops
+// p_convert, p_mul, p_sub (posit arithmetic rounds the exact value once, like
+// the quire's to_posit): g' = round_o(X_g 2^-R_g), m = round_o(lr g'),
+// w' = round_o(w - m).  Valid when every image fits 64 bits and every exact
+// intermediate its quire word (sgd_fast_ok).
+__device__ __forceinline__ uint32_t sgd_fast(const PositFmt& fo, const PositFmt& fg, int64_t X_lr,
+                                             uint32_t w, uint32_t gcode, const uint4* lut) {
+    int64_t Xg, Xw;
+    const bool gnar = decode_x(gcode, fg, Xg);
+    const bool wnar = decode_x(w, fo, Xw);
+    if (gnar || wnar) return 1u << (fo.nbits - 1);
+    const unsigned __int128 qg = (unsigned __int128)((__int128)Xg << (2 * fo.R - fg.R));
+    int64_t Xg16;
+    decode_x(q_to_posit_lut(fo, qg, lut), fo, Xg16);
+    int64_t Xm;
+    decode_x(q_to_posit_lut(fo, (unsigned __int128)((__int128)X_lr * Xg16), lut), fo, Xm);
+    return q_to_posit_lut(fo, (unsigned __int128)((__int128)(Xw - Xm) << fo.R), lut);
+}
+
 __global__ void sgd_multi_kernel(PositFmt fo, int bo, PositFmt fg, int bg, uint32_t lr, PositFmt f1,
                                  int b1, PositFmt f2, int b2, int grad_scale_log2,
-                                 const __grid_constant__ SgdSegs segs) {
+                                 const __grid_constant__ SgdSegs segs, int fast) {
+    __shared__ uint4 s_lut[kPackLutEntries];
+    int64_t X_lr = 0;
+    if (fast) {
+        build_pack_lut(fo, s_lut, threadIdx.x, blockDim.x);
+        decode_x(lr, fo, X_lr);
+        __syncthreads();
+    }
     const int64_t total = segs.start[segs.count];
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total;
          i += int64_t(gridDim.x) * blockDim.x) {
@@ -528,9 +556,14 @@ __global__ void sgd_multi_kernel(PositFmt fo, int bo, PositFmt fg, int bg, uint3
             else hi = mid - 1;
         }
         const int64_t k = i - segs.start[lo];
-        uint32_t g = p_convert(fg, fo, load_any(segs.grad[lo], k, bg));
-        if (grad_scale_log2 != 0) g = p_ldexp(fo, g, -grad_scale_log2);
-        const uint32_t w = p_sub(fo, load_any(segs.master[lo], k, bo), p_mul(fo, lr, g));
+        uint32_t w;
+        if (fast) {
+            w = sgd_fast(fo, fg, X_lr, load_any(segs.master[lo], k, bo), load_any(segs.grad[lo], k, bg), s_lut);
+        } else {
+            uint32_t g = p_convert(fg, fo, load_any(segs.grad[lo], k, bg));
+            if (grad_scale_log2 != 0) g = p_ldexp(fo, g, -grad_scale_log2);
+            w = p_sub(fo, load_any(segs.master[lo], k, bo), p_mul(fo, lr, g));
+        }
         store_any(segs.master[lo], k, bo, w);
         if (segs.copy1[lo]) store_any(segs.copy1[lo], k, b1, p_convert(fo, f1, w));
         if (segs.copy2[lo]) store_any(segs.copy2[lo], k, b2, p_convert(fo, f2, w));
@@ -912,6 +945,12 @@ int pnn_sgd_step_multi(int opt_nbits, int opt_es, int g_nbits, int g_es, uint32_
     if (has2) CHECK_FMT(c2_nbits, c2_es);
     const PositFmt fo = make_fmt(opt_nbits, opt_es), fg = make_fmt(g_nbits, g_es);
     const PositFmt f1 = has1 ? make_fmt(c1_nbits, c1_es) : fo, f2 = has2 ? make_fmt(c2_nbits, c2_es) : fo;
+    // integer-image update (sgd_fast): images within 64 bits, exact intermediates
+    // within the optimizer quire word (|X_g| 2^(2Ro-Rg), lr * g', (w - m) 2^Ro)
+    const bool lr_nar = lr_code == (1u << (opt_nbits - 1));
+    const int fast = grad_scale_log2 == 0 && !lr_nar && 2 * fo.R <= 62 && 2 * fg.R <= 62 &&
+                     2 * fo.R >= fg.R && 2 * fo.R <= 60 && fo.W <= 128 && fg.R + 2 * fo.R + 1 < fo.W &&
+                     4 * fo.R + 1 < fo.W && 3 * fo.R + 2 < fo.W;
     for (int base = 0; base < count; base += kSgdMaxSeg) {
         SgdSegs sg{};
         sg.count = 0;
@@ -931,7 +970,7 @@ int pnn_sgd_step_multi(int opt_nbits, int opt_es, int g_nbits, int g_es, uint32_
         if (tot == 0) continue;
         sgd_multi_kernel<<<grid1(tot), 256, 0, (cudaStream_t)stream>>>(
             fo, bytes_of(opt_nbits), fg, bytes_of(g_nbits), lr_code, f1, bytes_of(f1.nbits), f2,
-            bytes_of(f2.nbits), grad_scale_log2, sg);
+            bytes_of(f2.nbits), grad_scale_log2, sg, fast);
     }
     return launched("sgd_step_multi");
 }

@@ -43,8 +43,10 @@ def test_pool_recompute_equals_argmax(cuda, xf, gf, shape, ties):
 
 @pytest.mark.parametrize("opt,grad,copies", [((16, 1), (12, 1), [(8, 1), (12, 1)]),
                                              ((16, 1), (16, 1), []),
-                                             ((12, 2), (8, 2), [(8, 2)])])
-def test_sgd_multi_equals_per_tensor(cuda, opt, grad, copies):
+                                             ((12, 2), (8, 2), [(8, 2)]),
+                                             ((16, 1), (8, 0), [(8, 0)])])
+@pytest.mark.parametrize("scale", [0, 1])
+def test_sgd_multi_equals_per_tensor(cuda, opt, grad, copies, scale):
     """The whole-model optimizer launch == pnn_sgd_step_scaled per tensor."""
     rng = np.random.default_rng(5)
     sizes = [150, 6, 2400, 16, 48000, 120, 10081, 84, 1, 10]
@@ -55,8 +57,8 @@ def test_sgd_multi_equals_per_tensor(cuda, opt, grad, copies):
     ref_c = [tuple(torch.zeros(n, dtype=ops._cfg(c).code_dtype, device="cuda") for c in copies) for n in sizes]
     got_c = [tuple(torch.zeros(n, dtype=ops._cfg(c).code_dtype, device="cuda") for c in copies) for n in sizes]
     for m, g, cs in zip(ref_m, grads, ref_c):
-        ops.sgd_step(opt, m, grad, g, lr, list(zip(copies, cs)), grad_scale_log2=1)
-    ops.sgd_step_multi(opt, grad, lr, masters, grads, copies, got_c, grad_scale_log2=1)
+        ops.sgd_step(opt, m, grad, g, lr, list(zip(copies, cs)), grad_scale_log2=scale)
+    ops.sgd_step_multi(opt, grad, lr, masters, grads, copies, got_c, grad_scale_log2=scale)
     for a, b in zip(masters, ref_m):
         assert torch.equal(a, b)
     for a, b in zip(got_c, ref_c):
