@@ -291,13 +291,13 @@ bool map_wgrad_x(CUtensorMap* m, void* base, int D, int64_t N, int64_t Hp, int64
 // Weight digits dig[D][K/16][rows][16] as a 3-D map {2 * rows, D, K/16} of
 // 8-byte elements; box {2 * NT, D, 2} -> smem [2 slices][D][NT][16 B], i.e. the
 // D planes concatenated along N with a uniform 128-byte 8-row stride.
-bool map_weights(CUtensorMap* m, void* base, int D, int64_t rows, int64_t K, int NT) {
+bool map_weights(CUtensorMap* m, void* base, int D, int64_t rows, int64_t K, int NT, int box_planes = 0) {
     auto enc = encoder();
     if (!enc) return false;
     const int64_t KS = K / 16;
     const cuuint64_t dims[3] = {cuuint64_t(2 * rows), cuuint64_t(D), cuuint64_t(KS)};
     const cuuint64_t strides[2] = {cuuint64_t(KS * rows * 16), cuuint64_t(rows * 16)};
-    const cuuint32_t boxd[3] = {cuuint32_t(2 * NT), cuuint32_t(D), 2};
+    const cuuint32_t boxd[3] = {cuuint32_t(2 * NT), cuuint32_t(box_planes > 0 ? box_planes : D), 2};
     const cuuint32_t es[3] = {1, 1, 1};
     return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, base, dims, strides, boxd, es,
                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -319,21 +319,21 @@ constexpr int acc_of() { return 1; }
 template <int MODE, int D>
 constexpr int nt_of() { return cps_of<MODE, D>() == 2 ? small_nt(D) : TileCfg<D>::NT; }
 
-template <int D, typename CodeT, int MODE, int DA = D, int OFF = 0>
+template <int D, typename CodeT, int MODE, int DA = D, int OFF = 0, int DB = D>
 cudaError_t launch_kernel(const CUtensorMap& tA, const CUtensorMap& tB, const IgemmArgs& a,
                           OutMap<CodeT> out, cudaStream_t st) {
     constexpr int NTT = nt_of<MODE, D>(), CPS = cps_of<MODE, D>(), ACC = acc_of<MODE, D>();
-    using Geo = ImplGeo<D, NTT, CPS, ACC, DA>;
+    using Geo = ImplGeo<D, NTT, CPS, ACC, DA, DB>;
     void (*k)(CUtensorMap, CUtensorMap, IgemmArgs, OutMap<CodeT>);
     if constexpr (D <= 3)
-        k = a.f.W <= 32 ? igemm_kernel<D, NTT, CPS, ACC, 1, CodeT, MODE, 0, DA, OFF>
-                        : igemm_kernel<D, NTT, CPS, ACC, 2, CodeT, MODE, 0, DA, OFF>;
+        k = a.f.W <= 32 ? igemm_kernel<D, NTT, CPS, ACC, 1, CodeT, MODE, 0, DA, OFF, DB>
+                        : igemm_kernel<D, NTT, CPS, ACC, 2, CodeT, MODE, 0, DA, OFF, DB>;
     else
-        k = a.f.W <= 64 ? igemm_kernel<D, NTT, CPS, ACC, 2, CodeT, MODE, 0, DA, OFF>
-                        : igemm_kernel<D, NTT, CPS, ACC, 4, CodeT, MODE, 0, DA, OFF>;
+        k = a.f.W <= 64 ? igemm_kernel<D, NTT, CPS, ACC, 2, CodeT, MODE, 0, DA, OFF, DB>
+                        : igemm_kernel<D, NTT, CPS, ACC, 4, CodeT, MODE, 0, DA, OFF, DB>;
     // BASELINE formats: epilogue specialised on the compile-time format
     const int fid = fixed_fmt_id(a.f);
-    if constexpr (DA == D) {
+    if constexpr (DA == D && DB == D) {
         if constexpr (D == 2 && sizeof(CodeT) == 1)
             if (fid == 1) k = igemm_kernel<2, NTT, CPS, ACC, 1, CodeT, MODE, 1>;
         if constexpr (D == 4 && sizeof(CodeT) == 1)
@@ -342,7 +342,7 @@ cudaError_t launch_kernel(const CUtensorMap& tA, const CUtensorMap& tB, const Ig
             if (fid == 4) k = igemm_kernel<8, NTT, CPS, ACC, 4, CodeT, MODE, 4>;
     }
     if constexpr (D == 6 && sizeof(CodeT) == 2)
-        if (fid == 3) k = igemm_kernel<6, NTT, CPS, ACC, 4, CodeT, MODE, 3, DA, OFF>;
+        if (fid == 3) k = igemm_kernel<6, NTT, CPS, ACC, 4, CodeT, MODE, 3, DA, OFF, DB>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Geo::SMEM);
     if (e != cudaSuccess) return e;
     const int64_t tiles = a.mtiles * a.ntiles * a.splits;
@@ -370,6 +370,22 @@ cudaError_t dispatch(int D, const CUtensorMap& tA, const CUtensorMap& tB, const 
 // Weight-gradient A operands of DA planes at group offset OFF that have a
 // kernel: the symmetric case, and posit(8,1) forward digits under a posit(12,1)
 // gradient (BASELINE config 3: R 12 -> 20, one digit up).
+// Input gradients whose weights all fit kDgradDB digits (|X_w| within the
+// 3-digit balanced capacity, i.e. |w| < 8 in posit(12,1)): a variant with
+// DB = 3 weight planes (half the MMAs, 8 instead of 11 TMEM groups) runs;
+// the weight digitiser's flag selects it on the device (both variants are
+// launched, the other exits at once), so no host round trip is needed.
+constexpr int kDgradDB = 3;
+bool dgrad_reduced(int D) { return D == 6; }
+
+template <typename CodeT>
+cudaError_t dispatch_dgrad_reduced(int D, const CUtensorMap& tA, const CUtensorMap& tB, const IgemmArgs& a,
+                                   OutMap<CodeT> out, cudaStream_t st) {
+    if constexpr (sizeof(CodeT) == 2)
+        if (D == 6) return launch_kernel<6, CodeT, 1, 6, 0, kDgradDB>(tA, tB, a, out, st);
+    return cudaErrorInvalidValue;
+}
+
 bool wgrad_variant(int D, int DA, int OFF) {
     return (DA == D && OFF == 0) || (D == 6 && DA == 4 && OFF == 1);
 }
@@ -485,13 +501,14 @@ cudaError_t im2col_digits(int D, const void* x, const ConvGeom& g, const PositFm
 template <typename CodeT>
 cudaError_t weight_digits(int D, const CodeT* w, const CodeT* bias, int64_t F, int64_t C,
                           int64_t taps, int64_t Kp, int transpose, const PositFmt& f, int8_t* dig,
-                          int64_t* col_add, uint8_t* col_nar, uint8_t* any, cudaStream_t st) {
+                          int64_t* col_add, uint8_t* col_nar, uint8_t* any, cudaStream_t st,
+                          uint8_t* wide = nullptr, int wide_planes = 0) {
     const int64_t total = (transpose ? C : F) * taps * Kp;
     const int grid = grid_for(total > F ? total : F, 256);
 #define PNN_WD(DD)                                                                              \
     weight_digits_kernel<DD, CodeT><<<grid, 256, 0, st>>>(w, bias, int(F), int(C), int(taps),  \
                                                           int(Kp), transpose, f, dig, col_add, \
-                                                          col_nar, any)
+                                                          col_nar, any, wide, wide_planes)
     switch (D) {
         case 2: PNN_WD(2); break;
         case 3: PNN_WD(3); break;
@@ -618,12 +635,15 @@ int run_dgrad(const ImplPlan& p, const ConvGeom& g, const CodeT* dy, const CodeT
     const uint8_t* a_pos = pre ? pre->pos_nar : pos_nar;
     const uint8_t* a_any = pre ? pre->any : flags;
     const int64_t taps = g.KH * g.KW;
+    const bool reduced = dgrad_reduced(p.D) && sizeof(CodeT) == 2;
+    uint8_t* wide = flags + 2;  // weights need more than kDgradDB digit planes
     if (weight_digits<CodeT>(p.D, w, nullptr, g.F, g.C, taps, p.Kp, 1, f, bdig, nullptr, nullptr,
-                             flags + 1, st) != cudaSuccess)
+                             flags + 1, st, reduced ? wide : nullptr, kDgradDB) != cudaSuccess)
         return 4;
-    CUtensorMap tA, tB;
+    CUtensorMap tA, tB, tB3;
     if (!map_act(&tA, const_cast<int8_t*>(a_dig), p.D, g.N, g.OH, g.OW, p.Ca, p.boxA) ||
-        !map_weights(&tB, bdig, p.D, p.brows, taps * p.Kp, p.NT))
+        !map_weights(&tB, bdig, p.D, p.brows, taps * p.Kp, p.NT) ||
+        (reduced && !map_weights(&tB3, bdig, p.D, p.brows, taps * p.Kp, p.NT, kDgradDB)))
         return 5;
     IgemmArgs a = p.a;
     a.col_add = nullptr;
@@ -631,6 +651,12 @@ int run_dgrad(const ImplPlan& p, const ConvGeom& g, const CodeT* dy, const CodeT
     const bool use_partial = a.splits > 1;
     a.partial = use_partial ? reinterpret_cast<unsigned __int128*>(ws + p.off_partial) : nullptr;
     const OutMap<CodeT> out = out_nchw<CodeT>(dx, g.H * g.W, g.C);
+    if (reduced) {  // both variants launched; the flag lets exactly one of them run
+        a.vflag = wide;
+        a.vexpect = 0;
+        if (dispatch_dgrad_reduced<CodeT>(p.D, tA, tB3, a, out, st) != cudaSuccess) return 4;
+        a.vexpect = 1;
+    }
     if (dispatch<CodeT, 1>(p.D, tA, tB, a, out, st) != cudaSuccess) return 4;
     if (use_partial)
         launch_finalize<CodeT>(a.partial, int(a.splits), nullptr, nullptr, out, a.M, a.N, f, nullptr, nullptr, st);

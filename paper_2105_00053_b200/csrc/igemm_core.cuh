@@ -52,13 +52,15 @@ constexpr int kActLutBits = 12;  // digitiser LUT up to 4096 codes (32 KB, L1-re
 // DA: digit planes of the A operand (== D except in the weight gradient fed by
 // the forward pass's saved activation digits of a narrower, exactly widening
 // format: DA planes whose groups land OFF digit positions up, igemm_kernel).
-template <int D, int NT_, int CPS, int ACC = 1, int DA = D>
+// DB: digit planes of the B operand (== D except for an input gradient whose
+// weights all fit DB < D digits, run_dgrad's device-selected variant).
+template <int D, int NT_, int CPS, int ACC = 1, int DA = D, int DB = D>
 struct ImplGeo {
     static constexpr int NT = NT_;
-    static constexpr int G = DA + D - 1;
-    static constexpr int NMMA = D * NT;
+    static constexpr int G = DA + DB - 1;
+    static constexpr int NMMA = DB * NT;
     static constexpr int A_BYTES = DA * kBM * kIKB;
-    static constexpr int B_BYTES = D * NT * kIKB;
+    static constexpr int B_BYTES = DB * NT * kIKB;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
     static constexpr int BUDGET = CPS == 2 ? 104 * 1024 : 200 * 1024;
     static constexpr int STAGES_FIT = BUDGET / STAGE_BYTES;
@@ -72,7 +74,7 @@ struct ImplGeo {
     static constexpr int THREADS = 64 + 32 * EPI;
     static_assert(G * NT <= (ACC == 2 ? ACC_STRIDE : int(TMEM_COLS)), "TMEM overflow");
     static_assert(ACC == 1 || CPS == 1, "double buffering needs the whole TMEM");
-    static_assert(DA >= 1 && DA <= D + 1, "zero-MMA initialisation covers DA <= D + 1");
+    static_assert(DA >= 1 && DB >= 1 && DB <= D, "digit planes");
     static_assert(NMMA % 16 == 0 && NMMA <= 256, "bad UMMA N");
     static_assert(STAGES >= 2, "pipeline depth");
     static_assert(A_BYTES % 1024 == 0 && B_BYTES % 512 == 0, "stage alignment");
@@ -93,6 +95,8 @@ struct IgemmArgs {
     int taps, C, OWb, OHb, kpr, kpi;  // k-blocks per row-block set / per image
     int KH, kgroups, cgroups, Hp;     // kx groups of 4, 32-channel groups, padded height
     int apad;  // mode 0: zero ring stored around the A digits (box coordinates shift by it)
+    const uint8_t* vflag;  // variant selection (see igemm_kernel): run iff (*vflag != 0) == vexpect
+    int vexpect;
     int relu;       // mode 0: output relu(y) (ReLU layer fused) ...
     void* pre_out;  // ... and, if non-null, the pre-activation y here (same layout)
     // tile raster (tile_coords) with launch-constant divisions: by mtiles * ntiles,
@@ -125,12 +129,16 @@ __device__ __forceinline__ void itile_coords(int64_t t64, const IgemmArgs& a, in
 // (the saved forward digits of an exactly widening format, X_g = X_f *
 // 2^(R_g - R_f), R_g - R_f = 8 * OFF); MMA group g is digit position g + OFF.
 template <int D, int NT_, int CPS, int ACC, int QW, typename CodeT, int MODE, int FMT = 0,
-          int DA = D, int OFF = 0>
-__global__ void __launch_bounds__(ImplGeo<D, NT_, CPS, ACC, DA>::THREADS, CPS)
+          int DA = D, int OFF = 0, int DB = D>
+__global__ void __launch_bounds__(ImplGeo<D, NT_, CPS, ACC, DA, DB>::THREADS, CPS)
     igemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  const IgemmArgs a, const OutMap<CodeT> out) {
     static_assert(MODE == 2 || (DA == D && OFF == 0), "asymmetric digits: weight gradient only");
-    using Geo = ImplGeo<D, NT_, CPS, ACC, DA>;
+    static_assert(MODE == 1 || DB == D, "reduced B digits: input gradient only");
+    using Geo = ImplGeo<D, NT_, CPS, ACC, DA, DB>;
+    // device-selected variant: exit at once unless the flag (written by the
+    // weight digitiser on this stream) matches
+    if (a.vflag != nullptr && int(*a.vflag != 0) != a.vexpect) return;
     constexpr int kIEpiWarps = Geo::EPI;
     constexpr int kIThreads = Geo::THREADS;
     using QT = typename QuireWord<QW>::T;
@@ -266,9 +274,15 @@ __global__ void __launch_bounds__(ImplGeo<D, NT_, CPS, ACC, DA>::THREADS, CPS)
                     // MN-major: LBO = next 8 K rows (128 B), SBO = next 16-wide MN atom.
                     const uint64_t bdesc = MODE == 2
                                                ? ptx::smem_desc_kmajor(b_base, 128, kIKB * 16)
-                                               : ptx::smem_desc_kmajor(b_base, D * NT * 16, 128);
+                                               : ptx::smem_desc_kmajor(b_base, DB * NT * 16, 128);
                     const bool first = i == 0;
-                    if (first) ptx::mma_i8(tacc + (DA - 1) * NT, zdesc, bdesc, idesc, 0);
+                    if (first) {  // zero groups DB .. G-1 (plane 0's MMA initialises 0 .. DB-1)
+#pragma unroll
+                        for (int z = DB; z < Geo::G; z += DB) {
+                            const int off = z < Geo::G - DB ? z : Geo::G - DB;
+                            ptx::mma_i8(tacc + off * NT, zdesc, bdesc, idesc, 0);
+                        }
+                    }
 #pragma unroll
                     for (int p = 0; p < DA; ++p) {
                         const uint32_t ap = a_base + p * (kBM * kIKB);
@@ -770,7 +784,8 @@ template <int D, typename CodeT>
 __global__ void weight_digits_kernel(const CodeT* __restrict__ w, const CodeT* __restrict__ bias,
                                      int F, int C, int taps, int Kp, int transpose, PositFmt f,
                                      int8_t* __restrict__ dig, int64_t* __restrict__ col_add,
-                                     uint8_t* __restrict__ col_nar, uint8_t* __restrict__ any) {
+                                     uint8_t* __restrict__ col_nar, uint8_t* __restrict__ any,
+                                     uint8_t* __restrict__ wide = nullptr, int wide_planes = 0) {
     const int rows = transpose ? C : F;
     const int inner = transpose ? F : C;
     const int64_t total = int64_t(rows) * taps * Kp;
@@ -791,6 +806,10 @@ __global__ void weight_digits_kernel(const CodeT* __restrict__ w, const CodeT* _
         if (nar) {
             if (col_nar && !transpose) col_nar[r] = 1;
             *any = 1;
+        }
+        if (wide != nullptr) {  // a digit plane >= wide_planes in use
+            const uint64_t y = (uint64_t(hi) << 32) | lo;
+            if (y >> (8 * wide_planes)) *wide = 1;
         }
 #pragma unroll
         for (int p = 0; p < D; ++p)
