@@ -322,7 +322,11 @@ constexpr int nt_of() { return cps_of<MODE, D>() == 2 ? small_nt(D) : TileCfg<D>
 template <int D, typename CodeT, int MODE, int DA = D, int OFF = 0, int DB = D>
 cudaError_t launch_kernel(const CUtensorMap& tA, const CUtensorMap& tB, const IgemmArgs& a,
                           OutMap<CodeT> out, cudaStream_t st) {
-    constexpr int NTT = nt_of<MODE, D>(), CPS = cps_of<MODE, D>(), ACC = acc_of<MODE, D>();
+    // reduced-digit input gradient: (DA + DB - 1) * 32 <= 256 TMEM columns, so
+    // two CTAs per SM overlap one's TMEM drain with the other's MMAs
+    constexpr bool kPairSM = MODE == 1 && DB < D && (DA + DB - 1) * 32 <= 256;
+    constexpr int NTT = kPairSM ? 32 : nt_of<MODE, D>();
+    constexpr int CPS = kPairSM ? 2 : cps_of<MODE, D>(), ACC = acc_of<MODE, D>();
     using Geo = ImplGeo<D, NTT, CPS, ACC, DA, DB>;
     void (*k)(CUtensorMap, CUtensorMap, IgemmArgs, OutMap<CodeT>);
     if constexpr (D <= 3)
