@@ -319,7 +319,7 @@ constexpr int acc_of() { return 1; }
 template <int MODE, int D>
 constexpr int nt_of() { return cps_of<MODE, D>() == 2 ? small_nt(D) : TileCfg<D>::NT; }
 
-template <int D, typename CodeT, int MODE, int DA = D, int OFF = 0, int DB = D>
+template <int D, typename CodeT, int MODE, int DA = D, int OFF = 0, int DB = D, int QWF = 0>
 cudaError_t launch_kernel(const CUtensorMap& tA, const CUtensorMap& tB, const IgemmArgs& a,
                           OutMap<CodeT> out, cudaStream_t st) {
     // reduced-digit input gradient: (DA + DB - 1) * 32 <= 256 TMEM columns, so
@@ -329,6 +329,18 @@ cudaError_t launch_kernel(const CUtensorMap& tA, const CUtensorMap& tB, const Ig
     constexpr int CPS = kPairSM ? 2 : cps_of<MODE, D>(), ACC = acc_of<MODE, D>();
     using Geo = ImplGeo<D, NTT, CPS, ACC, DA, DB>;
     void (*k)(CUtensorMap, CUtensorMap, IgemmArgs, OutMap<CodeT>);
+    const int fid = fixed_fmt_id(a.f);
+    if constexpr (QWF != 0) {  // quire word forced by the caller (reduced-digit variants)
+        k = igemm_kernel<D, NTT, CPS, ACC, QWF, CodeT, MODE, 0, DA, OFF, DB>;
+        if constexpr (D == 6 && sizeof(CodeT) == 2)
+            if (fid == 3) k = igemm_kernel<6, NTT, CPS, ACC, QWF, CodeT, MODE, 3, DA, OFF, DB>;
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Geo::SMEM);
+        if (e != cudaSuccess) return e;
+        const int64_t tiles = a.mtiles * a.ntiles * a.splits;
+        const int64_t slots = int64_t(CPS) * num_sms();
+        k<<<int(tiles < slots ? tiles : slots), Geo::THREADS, Geo::SMEM, st>>>(tA, tB, a, out);
+        return cudaGetLastError();
+    }
     if constexpr (D <= 3)
         k = a.f.W <= 32 ? igemm_kernel<D, NTT, CPS, ACC, 1, CodeT, MODE, 0, DA, OFF, DB>
                         : igemm_kernel<D, NTT, CPS, ACC, 2, CodeT, MODE, 0, DA, OFF, DB>;
@@ -336,7 +348,6 @@ cudaError_t launch_kernel(const CUtensorMap& tA, const CUtensorMap& tB, const Ig
         k = a.f.W <= 64 ? igemm_kernel<D, NTT, CPS, ACC, 2, CodeT, MODE, 0, DA, OFF, DB>
                         : igemm_kernel<D, NTT, CPS, ACC, 4, CodeT, MODE, 0, DA, OFF, DB>;
     // BASELINE formats: epilogue specialised on the compile-time format
-    const int fid = fixed_fmt_id(a.f);
     if constexpr (DA == D && DB == D) {
         if constexpr (D == 2 && sizeof(CodeT) == 1)
             if (fid == 1) k = igemm_kernel<2, NTT, CPS, ACC, 1, CodeT, MODE, 1>;
@@ -390,6 +401,20 @@ cudaError_t dispatch_dgrad_reduced(int D, const CUtensorMap& tA, const CUtensorM
     return cudaErrorInvalidValue;
 }
 
+// Both operands within 3 digits (dy too: |dy| < 8 in posit(12,1)): 3 x 3 digit
+// MMAs, 5 TMEM groups; the exact sum then fits 64 bits for chunks below 2^17
+// terms (|X| < 2^23 each), so a 64-bit quire word serves (single split only:
+// split-K partials are 128-bit words).
+template <typename CodeT>
+cudaError_t dispatch_dgrad_33(int D, bool narrow_word, const CUtensorMap& tA, const CUtensorMap& tB,
+                              const IgemmArgs& a, OutMap<CodeT> out, cudaStream_t st) {
+    if constexpr (sizeof(CodeT) == 2)
+        if (D == 6)
+            return narrow_word ? launch_kernel<6, CodeT, 1, kDgradDB, 0, kDgradDB, 2>(tA, tB, a, out, st)
+                               : launch_kernel<6, CodeT, 1, kDgradDB, 0, kDgradDB, 4>(tA, tB, a, out, st);
+    return cudaErrorInvalidValue;
+}
+
 bool wgrad_variant(int D, int DA, int OFF) {
     return (DA == D && OFF == 0) || (D == 6 && DA == 4 && OFF == 1);
 }
@@ -410,7 +435,7 @@ template <typename SrcT>
 cudaError_t act_digits_t(int D, const SrcT* x, int64_t N, int64_t C, int64_t H, int64_t W, int64_t Cp,
                          int pad, const PositFmt& f, const PositFmt& fs, uint32_t* lut, bool build_lut,
                          int8_t* dig, uint8_t* pos_nar, uint8_t* chw_nar, uint8_t* chan_nar,
-                         uint8_t* any, cudaStream_t st, const DigitGate& gt) {
+                         uint8_t* any, cudaStream_t st, const DigitGate& gt, uint8_t* wide, int wide_planes) {
     // thread per (pixel, 32 channels): grid (pixel blocks, 32-channel chunks)
     if (N * H * W >= (int64_t(1) << 31)) return cudaErrorInvalidValue;
     const dim3 grid(unsigned((grid_for(N * H * W * (Cp / 32), 256) + Cp / 32 - 1) / (Cp / 32)),
@@ -428,19 +453,19 @@ cudaError_t act_digits_t(int D, const SrcT* x, int64_t N, int64_t C, int64_t H, 
     if (tiled && gt.gate == nullptr)                                                                 \
         act_digits_tiled_kernel<DD, SrcT, 0><<<tgrid, 256, 0, st>>>(                                 \
             x, int(N), int(C), int(H), int(W), int(Cp), pad, fd_hw, fd_w, f, fs, lut, dig, pos_nar,  \
-            chw_nar, chan_nar, any, gt);                                                             \
+            chw_nar, chan_nar, any, gt, wide, wide_planes);                                          \
     else if (tiled && gt.gb == 1)                                                                    \
         act_digits_tiled_kernel<DD, SrcT, 1><<<tgrid, 256, 0, st>>>(                                 \
             x, int(N), int(C), int(H), int(W), int(Cp), pad, fd_hw, fd_w, f, fs, lut, dig, pos_nar,  \
-            chw_nar, chan_nar, any, gt);                                                             \
+            chw_nar, chan_nar, any, gt, wide, wide_planes);                                          \
     else if (tiled)                                                                                  \
         act_digits_tiled_kernel<DD, SrcT, 2><<<tgrid, 256, 0, st>>>(                                 \
             x, int(N), int(C), int(H), int(W), int(Cp), pad, fd_hw, fd_w, f, fs, lut, dig, pos_nar,  \
-            chw_nar, chan_nar, any, gt);                                                             \
+            chw_nar, chan_nar, any, gt, wide, wide_planes);                                          \
     else                                                                                             \
         act_digits_kernel<DD, SrcT><<<grid, 256, 0, st>>>(x, int(N), int(C), int(H), int(W), int(Cp), \
                                                           pad, fd_hw, fd_w, f, fs, lut, dig, pos_nar, \
-                                                          chw_nar, chan_nar, any, gt)
+                                                          chw_nar, chan_nar, any, gt, wide, wide_planes)
     switch (D) {
         case 2: PNN_ACT(2); break;
         case 3: PNN_ACT(3); break;
@@ -458,13 +483,14 @@ cudaError_t act_digits_t(int D, const SrcT* x, int64_t N, int64_t C, int64_t H, 
 cudaError_t act_digits(int D, const void* x, int64_t N, int64_t C, int64_t H, int64_t W, int64_t Cp,
                        int pad, const PositFmt& f, const PositFmt& fs, uint32_t* lut, bool build_lut,
                        int8_t* dig, uint8_t* pos_nar, uint8_t* chw_nar, uint8_t* chan_nar, uint8_t* any,
-                       cudaStream_t st, const DigitGate& gt = DigitGate{}) {
+                       cudaStream_t st, const DigitGate& gt = DigitGate{}, uint8_t* wide = nullptr,
+                       int wide_planes = 0) {
     if (lut == nullptr && !same_fmt(f, fs)) return cudaErrorInvalidValue;  // no in-register convert
     if (fs.nbits <= 8)
         return act_digits_t(D, static_cast<const uint8_t*>(x), N, C, H, W, Cp, pad, f, fs, lut, build_lut,
-                            dig, pos_nar, chw_nar, chan_nar, any, st, gt);
+                            dig, pos_nar, chw_nar, chan_nar, any, st, gt, wide, wide_planes);
     return act_digits_t(D, static_cast<const uint16_t*>(x), N, C, H, W, Cp, pad, f, fs, lut, build_lut,
-                        dig, pos_nar, chw_nar, chan_nar, any, st, gt);
+                        dig, pos_nar, chw_nar, chan_nar, any, st, gt, wide, wide_planes);
 }
 
 template <typename SrcT>
@@ -618,6 +644,7 @@ struct DyDigits {
     const int8_t* dig;
     const uint8_t* pos_nar;
     const uint8_t* any;
+    const uint8_t* wide;  // dy uses digit planes >= kDgradDB (null: unknown)
 };
 
 template <typename CodeT>
@@ -631,23 +658,28 @@ int run_dgrad(const ImplPlan& p, const ConvGeom& g, const CodeT* dy, const CodeT
     uint8_t* flags = ws + p.off_flags;
     // (with pre, the caller cleared the maps before dy's digitiser filled pos_nar)
     if (pre == nullptr && cudaMemsetAsync(ws + p.off_maps, 0, p.maps_bytes, st) != cudaSuccess) return 4;
+    const bool reduced = dgrad_reduced(p.D) && sizeof(CodeT) == 2;
     if (pre == nullptr &&
         act_digits(p.D, dy, g.N, g.F, g.OH, g.OW, p.Ca, 0, f, f, lut_of(p, ws, f), true, adig, pos_nar,
-                   nullptr, nullptr, flags, st, gt) != cudaSuccess)
+                   nullptr, nullptr, flags, st, gt, reduced ? flags + 3 : nullptr, kDgradDB) != cudaSuccess)
         return 4;
     const int8_t* a_dig = pre ? pre->dig : adig;
     const uint8_t* a_pos = pre ? pre->pos_nar : pos_nar;
     const uint8_t* a_any = pre ? pre->any : flags;
+    const uint8_t* dy_wide = pre ? pre->wide : (reduced ? flags + 3 : nullptr);
     const int64_t taps = g.KH * g.KW;
-    const bool reduced = dgrad_reduced(p.D) && sizeof(CodeT) == 2;
     uint8_t* wide = flags + 2;  // weights need more than kDgradDB digit planes
     if (weight_digits<CodeT>(p.D, w, nullptr, g.F, g.C, taps, p.Kp, 1, f, bdig, nullptr, nullptr,
                              flags + 1, st, reduced ? wide : nullptr, kDgradDB) != cudaSuccess)
         return 4;
-    CUtensorMap tA, tB, tB3;
+    CUtensorMap tA, tA3, tB, tB3;
+    uint32_t box3[5];
+    for (int i = 0; i < 5; ++i) box3[i] = p.boxA[i];
+    box3[4] = kDgradDB;  // A box of the 3-plane variant: planes 0..2 of dy's digits
     if (!map_act(&tA, const_cast<int8_t*>(a_dig), p.D, g.N, g.OH, g.OW, p.Ca, p.boxA) ||
         !map_weights(&tB, bdig, p.D, p.brows, taps * p.Kp, p.NT) ||
-        (reduced && !map_weights(&tB3, bdig, p.D, p.brows, taps * p.Kp, p.NT, kDgradDB)))
+        (reduced && !map_weights(&tB3, bdig, p.D, p.brows, taps * p.Kp, p.NT, kDgradDB)) ||
+        (reduced && dy_wide && !map_act(&tA3, const_cast<int8_t*>(a_dig), p.D, g.N, g.OH, g.OW, p.Ca, box3)))
         return 5;
     IgemmArgs a = p.a;
     a.col_add = nullptr;
@@ -655,10 +687,18 @@ int run_dgrad(const ImplPlan& p, const ConvGeom& g, const CodeT* dy, const CodeT
     const bool use_partial = a.splits > 1;
     a.partial = use_partial ? reinterpret_cast<unsigned __int128*>(ws + p.off_partial) : nullptr;
     const OutMap<CodeT> out = out_nchw<CodeT>(dx, g.H * g.W, g.C);
-    if (reduced) {  // both variants launched; the flag lets exactly one of them run
-        a.vflag = wide;
+    if (reduced) {  // all variants launched; the digitisers' flags let exactly one run
+        a.vflag = wide;  // weights need more than 3 planes?
         a.vexpect = 0;
+        if (dy_wide) {
+            a.vflag2 = dy_wide;  // dy needs more than 3 planes?
+            a.vexpect2 = 0;
+            const bool narrow_word = a.splits == 1 && a.kb_per_split * kIKB < (int64_t(1) << 17);
+            if (dispatch_dgrad_33<CodeT>(p.D, narrow_word, tA3, tB3, a, out, st) != cudaSuccess) return 4;
+            a.vexpect2 = 1;
+        }
         if (dispatch_dgrad_reduced<CodeT>(p.D, tA, tB3, a, out, st) != cudaSuccess) return 4;
+        a.vflag2 = nullptr;
         a.vexpect = 1;
     }
     if (dispatch<CodeT, 1>(p.D, tA, tB, a, out, st) != cudaSuccess) return 4;
@@ -682,7 +722,8 @@ template <typename CodeT>
 int run_wgrad(const ImplPlan& p, const ConvGeom& g, const void* dy, const PositFmt& fdy,
               const void* x, const PositFmt& fx, CodeT* dw, unsigned __int128* raw_words,
               uint8_t* raw_nar, uint8_t* ws, cudaStream_t st, const SavedX* sv = nullptr,
-              uint8_t* share_pos_nar = nullptr, const DigitGate& gt = DigitGate{}) {
+              uint8_t* share_pos_nar = nullptr, const DigitGate& gt = DigitGate{},
+              uint8_t* dy_wide = nullptr) {
     const PositFmt& f = p.a.f;
     auto* adig = sv ? sv->dig : reinterpret_cast<int8_t*>(ws + p.off_adig);
     auto* bdig = reinterpret_cast<int8_t*>(ws + p.off_bdig);
@@ -702,7 +743,7 @@ int run_wgrad(const ImplPlan& p, const ConvGeom& g, const void* dy, const PositF
         if (e != cudaSuccess) return 4;
     }
     if (act_digits(p.D, dy, g.N, g.F, g.OH, g.OW, p.Fpw, 0, f, fdy, lut_of(p, ws, fdy, 1), true, bdig,
-                   share_pos_nar, nullptr, col_nar, flags + 1, st, gt) != cudaSuccess)
+                   share_pos_nar, nullptr, col_nar, flags + 1, st, gt, dy_wide, kDgradDB) != cudaSuccess)
         return 4;
     CUtensorMap tA, tB;
     const uint32_t boxB[5] = {uint32_t(2 * p.a.OWb), uint32_t(p.a.OHb), 1, uint32_t(p.NT / 16),
@@ -785,14 +826,15 @@ int run_backward(const BwdPlan& b, const ConvGeom& g, const PositFmt& ff, const 
                  const DigitGate& gt) {
     uint8_t* wsd = ws + b.off_d;
     if (b.share_dy && cudaMemsetAsync(wsd + b.pd.off_maps, 0, b.pd.maps_bytes, st) != cudaSuccess) return 4;
+    uint8_t* dy_wide = b.share_dy ? wsd + b.pd.off_flags + 3 : nullptr;  // cleared with the dgrad maps
     int rc = run_wgrad<GT>(b.pw, g, dy, fb, x, ff, static_cast<GT*>(dw), raw_words, raw_nar, ws, st,
                            b.use_saved ? sv : nullptr,
-                           b.share_dy ? wsd + b.pd.off_pos_nar : nullptr, gt);
+                           b.share_dy ? wsd + b.pd.off_pos_nar : nullptr, gt, dy_wide);
     if (rc != 0 || !b.has_dx) return rc;
     const DigitGate gd = gt;  // the input gradient digitises dy itself unless it shares the digits
     if (b.share_dy) {
         const DyDigits pre{reinterpret_cast<const int8_t*>(ws + b.pw.off_bdig), wsd + b.pd.off_pos_nar,
-                           ws + b.pw.off_flags + 1};
+                           ws + b.pw.off_flags + 1, dy_wide};
         return run_dgrad<BT>(b.pd, g, static_cast<const BT*>(dy), static_cast<const BT*>(w_bwd),
                              static_cast<BT*>(dx), wsd, st, &pre);
     }

@@ -96,7 +96,9 @@ struct IgemmArgs {
     int KH, kgroups, cgroups, Hp;     // kx groups of 4, 32-channel groups, padded height
     int apad;  // mode 0: zero ring stored around the A digits (box coordinates shift by it)
     const uint8_t* vflag;  // variant selection (see igemm_kernel): run iff (*vflag != 0) == vexpect
-    int vexpect;
+    int vexpect;           // and (*vflag2 != 0) == vexpect2 (null flags: no condition)
+    const uint8_t* vflag2;
+    int vexpect2;
     int relu;       // mode 0: output relu(y) (ReLU layer fused) ...
     void* pre_out;  // ... and, if non-null, the pre-activation y here (same layout)
     // tile raster (tile_coords) with launch-constant divisions: by mtiles * ntiles,
@@ -133,12 +135,12 @@ template <int D, int NT_, int CPS, int ACC, int QW, typename CodeT, int MODE, in
 __global__ void __launch_bounds__(ImplGeo<D, NT_, CPS, ACC, DA, DB>::THREADS, CPS)
     igemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  const IgemmArgs a, const OutMap<CodeT> out) {
-    static_assert(MODE == 2 || (DA == D && OFF == 0), "asymmetric digits: weight gradient only");
-    static_assert(MODE == 1 || DB == D, "reduced B digits: input gradient only");
+    static_assert(MODE == 2 || OFF == 0, "digit offset: weight gradient only");
     using Geo = ImplGeo<D, NT_, CPS, ACC, DA, DB>;
     // device-selected variant: exit at once unless the flag (written by the
     // weight digitiser on this stream) matches
     if (a.vflag != nullptr && int(*a.vflag != 0) != a.vexpect) return;
+    if (a.vflag2 != nullptr && int(*a.vflag2 != 0) != a.vexpect2) return;
     constexpr int kIEpiWarps = Geo::EPI;
     constexpr int kIThreads = Geo::THREADS;
     using QT = typename QuireWord<QW>::T;
@@ -514,7 +516,8 @@ __device__ __forceinline__ void emit_pixel_digits(const uint32_t (&code)[32], ui
                                                   int8_t* __restrict__ dig, uint8_t* __restrict__ pos_nar,
                                                   uint8_t* __restrict__ chw_nar,
                                                   uint8_t* __restrict__ chan_nar, uint8_t* __restrict__ any,
-                                                  bool ring = true) {
+                                                  bool ring = true, uint8_t* __restrict__ wide = nullptr,
+                                                  int wide_planes = 0) {
     const int Hp = H + 2 * pad, Wp = W + 2 * pad;
     const int CS = Cp / 16;
     const int c0 = cc * 32;
@@ -524,6 +527,14 @@ __device__ __forceinline__ void emit_pixel_digits(const uint32_t (&code)[32], ui
     for (int q = 0; q < 8; ++q) {
         const uint32_t c4[4] = {code[4 * q], code[4 * q + 1], code[4 * q + 2], code[4 * q + 3]};
         nm |= digits4_words<D>(c4, f, nar_code, lut, words, q) << (4 * q);
+    }
+    if (wide != nullptr) {  // digit planes >= wide_planes in use (reduced-digit variants)
+        uint32_t o = 0;
+#pragma unroll
+        for (int p = 0; p < D; ++p)
+#pragma unroll
+            for (int q = 0; q < 8; ++q) o |= p >= wide_planes ? words[p][q] : 0u;
+        if (o) *wide = 1;
     }
     // this chunk = slices 2cc, 2cc + 1 of pixel (h + pad, w + pad)
     auto cell = [&](int hh, int ww) {
@@ -581,7 +592,8 @@ __global__ void __launch_bounds__(256) act_digits_kernel(
     const CodeT* __restrict__ x, int N, int C, int H, int W, int Cp, int pad, FastDiv fd_hw,
     FastDiv fd_w, PositFmt f, PositFmt fs, const uint32_t* __restrict__ lut,
     int8_t* __restrict__ dig, uint8_t* __restrict__ pos_nar, uint8_t* __restrict__ chw_nar,
-    uint8_t* __restrict__ chan_nar, uint8_t* __restrict__ any, DigitGate gt = DigitGate{}) {
+    uint8_t* __restrict__ chan_nar, uint8_t* __restrict__ any, DigitGate gt = DigitGate{},
+    uint8_t* __restrict__ wide = nullptr, int wide_planes = 0) {
     const uint32_t HW = uint32_t(H) * uint32_t(W);
     const uint32_t pixels = uint32_t(N) * HW;
     const int64_t plane = int64_t(N) * (H + 2 * pad) * (W + 2 * pad) * Cp;
@@ -604,7 +616,7 @@ __global__ void __launch_bounds__(256) act_digits_kernel(
         uint32_t h, w;
         fd_w.divmod(pix, h, w);
         emit_pixel_digits<D>(code, r, n, pix, h, w, cc, C, H, W, Cp, pad, plane, HW, f, nar_code, lut,
-                             dig, pos_nar, chw_nar, chan_nar, any);
+                             dig, pos_nar, chw_nar, chan_nar, any, true, wide, wide_planes);
     }
 }
 
@@ -619,7 +631,8 @@ __global__ void __launch_bounds__(256) act_digits_tiled_kernel(
     const CodeT* __restrict__ x, int N, int C, int H, int W, int Cp, int pad, FastDiv fd_hw,
     FastDiv fd_w, PositFmt f, PositFmt fs, const uint32_t* __restrict__ lut,
     int8_t* __restrict__ dig, uint8_t* __restrict__ pos_nar, uint8_t* __restrict__ chw_nar,
-    uint8_t* __restrict__ chan_nar, uint8_t* __restrict__ any, DigitGate gt = DigitGate{}) {
+    uint8_t* __restrict__ chan_nar, uint8_t* __restrict__ any, DigitGate gt = DigitGate{},
+    uint8_t* __restrict__ wide = nullptr, int wide_planes = 0) {
     constexpr int TP = 256;                                   // pixels per tile
     constexpr int VPR = TP * int(sizeof(CodeT)) / 16;         // 16-byte vectors per channel row
     __shared__ uint4 s_tile[32 * VPR];
@@ -672,7 +685,8 @@ __global__ void __launch_bounds__(256) act_digits_tiled_kernel(
         // written cooperatively afterwards (per-thread ring loops diverge in
         // every warp: each image row has a first and a last pixel)
         emit_pixel_digits<D>(code, r0 + threadIdx.x, n, pix, h, w, cc, C, H, W, Cp, pad, plane, HW, f,
-                             nar_code, lut, dig, pos_nar, chw_nar, chan_nar, any, /*ring=*/false);
+                             nar_code, lut, dig, pos_nar, chw_nar, chan_nar, any, /*ring=*/false, wide,
+                             wide_planes);
         if (pad > 0) {
             const int Hp = H + 2 * pad, Wp = W + 2 * pad, CS = Cp / 16;
             uint32_t hh0, ww0;

@@ -234,9 +234,10 @@ def test_unrecorded_step_equals_recorded_step(cuda, st_fmt):
         assert torch.equal(a, b)
 
 
+@pytest.mark.parametrize("dy_small", [False, True])
 @pytest.mark.parametrize("big", [False, True])
 @pytest.mark.parametrize("shape", [(2, 32, 8, 8, 32, 3, 1), (3, 64, 16, 16, 64, 3, 1)])
-def test_dgrad_reduced_weight_digits(cuda, po, big, shape):
+def test_dgrad_reduced_weight_digits(cuda, po, big, shape, dy_small):
     """posit(12,1) input gradient: weights within 3 digits (|w| < 8) take the
     device-selected reduced-digit kernel (DB = 3); one large weight switches to
     the full kernel.  Both against the oracle."""
@@ -248,6 +249,10 @@ def test_dgrad_reduced_weight_digits(cuda, po, big, shape):
     if big:
         small[1, 2, 0, 0] = po.from_float64(12, 1, 100.0)
     dya = rand_codes(rng, 12, (N, F, H, W))
+    if dy_small:  # gradient-like values: within 3 digits -> the 3 x 3 digit kernel
+        dya = np.array([po.from_float64(12, 1, float(v)) for v in rng.normal(0, 0.01, dya.size)],
+                       np.uint64).reshape(dya.shape)
+        dya[0, 0, 0, :3] = [0, 1, (1 << 12) - 1]  # zero, minpos, -minpos
     dx = ops.conv2d_input_grad(cfg, dev(cfg, dya), dev(cfg, small), (N, C, H, W), 1, pad)
     want = po.conv2d_input_grad(12, 1, dya, small, (N, C, H, W), 1, pad)
     assert (host(dx).reshape(want.shape) == want).all()
