@@ -324,7 +324,7 @@ cudaError_t launch_kernel(const CUtensorMap& tA, const CUtensorMap& tB, const Ig
                           OutMap<CodeT> out, cudaStream_t st) {
     // reduced-digit input gradient: (DA + DB - 1) * 32 <= 256 TMEM columns, so
     // two CTAs per SM overlap one's TMEM drain with the other's MMAs
-    constexpr bool kPairSM = MODE == 1 && DB < D && (DA + DB - 1) * 32 <= 256;
+    constexpr bool kPairSM = (MODE == 1 || MODE == 2) && DB < D && (DA + DB - 1) * 32 <= 256;
     constexpr int NTT = kPairSM ? 32 : nt_of<MODE, D>();
     constexpr int CPS = kPairSM ? 2 : cps_of<MODE, D>(), ACC = acc_of<MODE, D>();
     using Geo = ImplGeo<D, NTT, CPS, ACC, DA, DB>;
@@ -496,7 +496,7 @@ cudaError_t act_digits(int D, const void* x, int64_t N, int64_t C, int64_t H, in
 template <typename SrcT>
 cudaError_t im2col_digits_t(int D, const SrcT* x, const ConvGeom& g, const PositFmt& f,
                             const PositFmt& fs, uint32_t* lut, int8_t* dig, uint8_t* pos_nar,
-                            uint8_t* chw_nar, uint8_t* any, cudaStream_t st) {
+                            uint8_t* chw_nar, uint8_t* any, cudaStream_t st, uint8_t* wide, int wide_planes) {
     const int grid = grid_for(g.N * g.OH * g.OW, 256);  // thread per output pixel
     if (g.N * g.OH * g.OW >= (int64_t(1) << 31)) return cudaErrorInvalidValue;
     const FastDiv fd_p{uint32_t(g.OH * g.OW)}, fd_ow{uint32_t(g.OW)};
@@ -504,7 +504,7 @@ cudaError_t im2col_digits_t(int D, const SrcT* x, const ConvGeom& g, const Posit
     if (lut) digit_lut_conv_kernel<DD><<<16, 256, 0, st>>>(fs, f, lut);                      \
     im2col_digits_kernel<DD, SrcT><<<grid, 256, 0, st>>>(                                   \
         x, int(g.N), int(g.C), int(g.H), int(g.W), int(g.KH), int(g.KW), g.pad, int(g.OH),   \
-        int(g.OW), fd_p, fd_ow, f, fs, lut, dig, pos_nar, chw_nar, any)
+        int(g.OW), fd_p, fd_ow, f, fs, lut, dig, pos_nar, chw_nar, any, wide, wide_planes)
     switch (D) {
         case 2: PNN_I2C(2); break;
         case 3: PNN_I2C(3); break;
@@ -521,11 +521,13 @@ cudaError_t im2col_digits_t(int D, const SrcT* x, const ConvGeom& g, const Posit
 
 cudaError_t im2col_digits(int D, const void* x, const ConvGeom& g, const PositFmt& f, const PositFmt& fs,
                           uint32_t* lut, int8_t* dig, uint8_t* pos_nar, uint8_t* chw_nar, uint8_t* any,
-                          cudaStream_t st) {
+                          cudaStream_t st, uint8_t* wide = nullptr, int wide_planes = 0) {
     if (lut == nullptr && !same_fmt(f, fs)) return cudaErrorInvalidValue;
     if (fs.nbits <= 8)
-        return im2col_digits_t(D, static_cast<const uint8_t*>(x), g, f, fs, lut, dig, pos_nar, chw_nar, any, st);
-    return im2col_digits_t(D, static_cast<const uint16_t*>(x), g, f, fs, lut, dig, pos_nar, chw_nar, any, st);
+        return im2col_digits_t(D, static_cast<const uint8_t*>(x), g, f, fs, lut, dig, pos_nar, chw_nar, any, st,
+                               wide, wide_planes);
+    return im2col_digits_t(D, static_cast<const uint16_t*>(x), g, f, fs, lut, dig, pos_nar, chw_nar, any, st,
+                           wide, wide_planes);
 }
 
 template <typename CodeT>
@@ -562,7 +564,7 @@ int rc_of(cudaError_t e) { return e == cudaSuccess ? 0 : 4; }
 struct SavedX {
     int8_t* dig;
     uint8_t* chw;
-    uint8_t* flag;
+    uint8_t* flag;  // [0] any NaR in x, [1] x uses digit planes >= kDgradDB
 };
 
 struct SaveLayout {
@@ -603,11 +605,13 @@ int run_fwd(const ImplPlan& p, const ConvGeom& g, const CodeT* x, const CodeT* w
     if ((e = cudaMemsetAsync(ws + p.off_maps, 0, p.maps_bytes, st)) != cudaSuccess) return 4;
     if (sv && (e = cudaMemsetAsync(sv->chw, 0, sv_clear, st)) != cudaSuccess) return 4;
     const ConvGeom& gv = p.gv;  // virtual 1x1 geometry when the first layer is folded
+    uint8_t* xwide = sv ? sv->flag + 1 : nullptr;  // for the weight gradient's reduced-digit variant
     if (p.fold)
-        e = im2col_digits(p.D, x, g, f, f, lut_of(p, ws, f), adig, pos_nar, sv ? sv->chw : nullptr, xflag, st);
+        e = im2col_digits(p.D, x, g, f, f, lut_of(p, ws, f), adig, pos_nar, sv ? sv->chw : nullptr, xflag, st,
+                          xwide, kDgradDB);
     else
         e = act_digits(p.D, x, g.N, g.C, g.H, g.W, p.Ca, g.pad, f, f, lut_of(p, ws, f), true, adig,
-                       pos_nar, sv ? sv->chw : nullptr, nullptr, xflag, st);
+                       pos_nar, sv ? sv->chw : nullptr, nullptr, xflag, st, DigitGate{}, xwide, kDgradDB);
     if (e != cudaSuccess) return 4;
     const int64_t taps = gv.KH * gv.KW;  // weights: [F][C*KH*KW] read as [F][ckk][1][1] if folded
     if ((e = weight_digits<CodeT>(p.D, w, bias, g.F, p.fold ? p.ckk : g.C, taps, p.Kp, 0, f, bdig,
@@ -742,14 +746,25 @@ int run_wgrad(const ImplPlan& p, const ConvGeom& g, const void* dy, const PositF
                            nullptr, chw_nar, nullptr, flags, st);
         if (e != cudaSuccess) return 4;
     }
+    // reduced-digit variant: saved (8,1)-format x one digit up, both operands in 3 planes
+    const bool reduced = sv != nullptr && sizeof(CodeT) == 2 && p.D == 6 && p.DA == 4 && p.OFF == 1;
+    if (reduced && dy_wide == nullptr) dy_wide = flags + 3;
     if (act_digits(p.D, dy, g.N, g.F, g.OH, g.OW, p.Fpw, 0, f, fdy, lut_of(p, ws, fdy, 1), true, bdig,
                    share_pos_nar, nullptr, col_nar, flags + 1, st, gt, dy_wide, kDgradDB) != cudaSuccess)
         return 4;
-    CUtensorMap tA, tB;
+    CUtensorMap tA, tB, tA3, tB3;
     const uint32_t boxB[5] = {uint32_t(2 * p.a.OWb), uint32_t(p.a.OHb), 1, uint32_t(p.NT / 16),
                               uint32_t(p.D)};
+    uint32_t boxA3[5], boxB3[5];
+    for (int i = 0; i < 5; ++i) {
+        boxA3[i] = p.boxA[i];
+        boxB3[i] = boxB[i];
+    }
+    boxA3[4] = boxB3[4] = kDgradDB;
     if (!map_wgrad_x(&tA, adig, p.DA, gv.N, p.Ha, p.Wa, p.Ca, p.boxA) ||
-        !map_act(&tB, bdig, p.D, g.N, g.OH, g.OW, p.Fpw, boxB))
+        !map_act(&tB, bdig, p.D, g.N, g.OH, g.OW, p.Fpw, boxB) ||
+        (reduced && (!map_wgrad_x(&tA3, adig, p.DA, gv.N, p.Ha, p.Wa, p.Ca, boxA3) ||
+                     !map_act(&tB3, bdig, p.D, g.N, g.OH, g.OW, p.Fpw, boxB3))))
         return 5;
     IgemmArgs a = p.a;
     a.col_add = nullptr;
@@ -765,6 +780,16 @@ int run_wgrad(const ImplPlan& p, const ConvGeom& g, const void* dy, const PositF
     out.kgroups = p.a.kgroups;
     out.cgroups = p.a.cgroups;
     out.cvalid = p.fold ? p.ckk : int(g.C);
+    if (reduced) {  // both launched; the x / dy plane flags let exactly one run
+        a.vflag = sv->flag + 1;
+        a.vflag2 = dy_wide;
+        a.vexpect = a.vexpect2 = 0;
+        if constexpr (sizeof(CodeT) == 2)
+            if (launch_kernel<6, CodeT, 2, kDgradDB, 1, kDgradDB, 4>(tA3, tB3, a, out, st) != cudaSuccess)
+                return 4;
+        a.vor = 1;
+        a.vexpect = 1;
+    }
     if (dispatch_wgrad<CodeT>(p.D, p.DA, p.OFF, tA, tB, a, out, st) != cudaSuccess) return 4;
     if (use_partial)
         launch_finalize<CodeT>(a.partial, int(a.splits), nullptr, col_nar, out, a.M, a.N, f, raw_words, raw_nar, st);

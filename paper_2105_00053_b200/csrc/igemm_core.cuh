@@ -99,6 +99,7 @@ struct IgemmArgs {
     int vexpect;           // and (*vflag2 != 0) == vexpect2 (null flags: no condition)
     const uint8_t* vflag2;
     int vexpect2;
+    int vor;               // 1: run iff (*vflag | *vflag2 != 0) == vexpect
     int relu;       // mode 0: output relu(y) (ReLU layer fused) ...
     void* pre_out;  // ... and, if non-null, the pre-activation y here (same layout)
     // tile raster (tile_coords) with launch-constant divisions: by mtiles * ntiles,
@@ -139,8 +140,12 @@ __global__ void __launch_bounds__(ImplGeo<D, NT_, CPS, ACC, DA, DB>::THREADS, CP
     using Geo = ImplGeo<D, NT_, CPS, ACC, DA, DB>;
     // device-selected variant: exit at once unless the flag (written by the
     // weight digitiser on this stream) matches
-    if (a.vflag != nullptr && int(*a.vflag != 0) != a.vexpect) return;
-    if (a.vflag2 != nullptr && int(*a.vflag2 != 0) != a.vexpect2) return;
+    if (a.vor) {  // run iff (either flag set) == vexpect
+        if (int(*a.vflag != 0 || *a.vflag2 != 0) != a.vexpect) return;
+    } else {
+        if (a.vflag != nullptr && int(*a.vflag != 0) != a.vexpect) return;
+        if (a.vflag2 != nullptr && int(*a.vflag2 != 0) != a.vexpect2) return;
+    }
     constexpr int kIEpiWarps = Geo::EPI;
     constexpr int kIThreads = Geo::THREADS;
     using QT = typename QuireWord<QW>::T;
@@ -731,7 +736,7 @@ __global__ void __launch_bounds__(256) im2col_digits_kernel(
     const CodeT* __restrict__ x, int N, int C, int H, int W, int KH, int KW, int pad, int OH,
     int OW, FastDiv fd_p, FastDiv fd_ow, PositFmt f, PositFmt fs, const uint32_t* __restrict__ lut,
     int8_t* __restrict__ dig, uint8_t* __restrict__ pos_nar, uint8_t* __restrict__ chw_nar,
-    uint8_t* __restrict__ any) {
+    uint8_t* __restrict__ any, uint8_t* __restrict__ wide = nullptr, int wide_planes = 0) {
     const int ckk = C * KH * KW, khw = KH * KW;
     const uint32_t nar_code = 1u << (fs.nbits - 1);  // fs: the codes' format (lut converts)
     const uint32_t P = uint32_t(OH) * uint32_t(OW);
@@ -768,6 +773,14 @@ __global__ void __launch_bounds__(256) im2col_digits_kernel(
                              : 0u;
             }
             nm |= digits4_words<D>(c4, f, nar_code, lut, words, q) << (4 * q);
+        }
+        if (wide != nullptr) {  // digit planes >= wide_planes in use
+            uint32_t o = 0;
+#pragma unroll
+            for (int p = 0; p < D; ++p)
+#pragma unroll
+                for (int q = 0; q < 8; ++q) o |= p >= wide_planes ? words[p][q] : 0u;
+            if (o) *wide = 1;
         }
         // slice layout of the virtual [N][OH][2 slices][OW][16] image
         const int64_t row = int64_t(n) * OH + oy;

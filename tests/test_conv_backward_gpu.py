@@ -256,3 +256,34 @@ def test_dgrad_reduced_weight_digits(cuda, po, big, shape, dy_small):
     dx = ops.conv2d_input_grad(cfg, dev(cfg, dya), dev(cfg, small), (N, C, H, W), 1, pad)
     want = po.conv2d_input_grad(12, 1, dya, small, (N, C, H, W), 1, pad)
     assert (host(dx).reshape(want.shape) == want).all()
+
+
+@pytest.mark.parametrize("wide", ["none", "x", "dy"])
+@pytest.mark.parametrize("shape", [(2, 32, 8, 8, 32, 3, 1), (3, 64, 16, 16, 64, 3, 1), (2, 3, 32, 32, 32, 3, 1)])
+def test_wgrad_reduced_digits(cuda, po, wide, shape):
+    """Config-3 stages with activation / gradient values within 3 digits: the
+    weight gradient takes the device-selected 3 x 3 digit kernel (saved (8,1)
+    digits one digit up); one wide value in x or dy switches to the full
+    kernel.  Against the per-pass weight gradient (full digits) and the oracle."""
+    ff, fb, fg = P81, P121, P121
+    N, C, H, W, F, K, pad = shape
+    rng = np.random.default_rng(23)
+    xa = np.array([po.from_float64(8, 1, float(v)) for v in np.abs(rng.normal(0, 1.0, N * C * H * W))],
+                  np.uint64).reshape(N, C, H, W)
+    dya = np.array([po.from_float64(12, 1, float(v)) for v in rng.normal(0, 0.01, N * F * H * W)],
+                   np.uint64).reshape(N, F, H, W)
+    if wide == "x":
+        xa[1, 0, 3, 3] = po.from_float64(8, 1, 4000.0)
+    if wide == "dy":
+        dya[0, 1, 2, 2] = po.from_float64(12, 1, 50.0)
+    x, dy = dev(ff, xa), dev(fb, dya)
+    w = dev(ff, rand_codes(rng, 8, (F, C, K, K)))
+    n = ops.conv2d_saved_bytes(ff, x.shape, w.shape, 1, pad)
+    saved = torch.empty(n, dtype=torch.uint8, device="cuda")
+    ops.conv2d_fwd_save(ff, x, w, None, 1, pad, saved)
+    _, dw = ops.conv2d_backward(ff, fb, fg, dy, x, saved, None, x.shape, w.shape, 1, pad, False)
+    want = ops.conv2d_weight_grad(fg, dy, ops.convert_tensor(x, ff, fg), w.shape, 1, pad)
+    assert torch.equal(dw, want)
+    if N * H * W <= 512:
+        ref = po.conv2d_weight_grad(12, 1, dya, po.convert_tensor(8, 1, 12, 1, xa), (F, C, K, K), 1, pad)
+        assert (host(dw).reshape(ref.shape) == ref).all()
