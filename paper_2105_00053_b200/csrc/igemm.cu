@@ -351,11 +351,11 @@ cudaError_t launch_kernel(const CUtensorMap& tA, const CUtensorMap& tB, const Ig
     if constexpr (DA == D && DB == D) {
         if constexpr (D == 2 && sizeof(CodeT) == 1)
             if (fid == 1) k = igemm_kernel<2, NTT, CPS, ACC, 1, CodeT, MODE, 1>;
-        if constexpr (D == 4 && sizeof(CodeT) == 1)
-            if (fid == 2) k = igemm_kernel<4, NTT, CPS, ACC, 2, CodeT, MODE, 2>;
         if constexpr (D == 8 && sizeof(CodeT) == 2)
             if (fid == 4) k = igemm_kernel<8, NTT, CPS, ACC, 4, CodeT, MODE, 4>;
     }
+    if constexpr (D == 4 && sizeof(CodeT) == 1)
+        if (fid == 2) k = igemm_kernel<4, NTT, CPS, ACC, 2, CodeT, MODE, 2, DA, OFF, DB>;
     if constexpr (D == 6 && sizeof(CodeT) == 2)
         if (fid == 3) k = igemm_kernel<6, NTT, CPS, ACC, 4, CodeT, MODE, 3, DA, OFF, DB>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Geo::SMEM);
@@ -605,7 +605,8 @@ int run_fwd(const ImplPlan& p, const ConvGeom& g, const CodeT* x, const CodeT* w
     if ((e = cudaMemsetAsync(ws + p.off_maps, 0, p.maps_bytes, st)) != cudaSuccess) return 4;
     if (sv && (e = cudaMemsetAsync(sv->chw, 0, sv_clear, st)) != cudaSuccess) return 4;
     const ConvGeom& gv = p.gv;  // virtual 1x1 geometry when the first layer is folded
-    uint8_t* xwide = sv ? sv->flag + 1 : nullptr;  // for the weight gradient's reduced-digit variant
+    // x's digit-plane flag (the reduced-digit variants of this pass and of the weight gradient)
+    uint8_t* xwide = sv ? sv->flag + 1 : flags + 3;
     if (p.fold)
         e = im2col_digits(p.D, x, g, f, f, lut_of(p, ws, f), adig, pos_nar, sv ? sv->chw : nullptr, xflag, st,
                           xwide, kDgradDB);
@@ -614,12 +615,21 @@ int run_fwd(const ImplPlan& p, const ConvGeom& g, const CodeT* x, const CodeT* w
                        pos_nar, sv ? sv->chw : nullptr, nullptr, xflag, st, DigitGate{}, xwide, kDgradDB);
     if (e != cudaSuccess) return 4;
     const int64_t taps = gv.KH * gv.KW;  // weights: [F][C*KH*KW] read as [F][ckk][1][1] if folded
+    // reduced-digit variant (posit(8,1): x and w within 3 balanced digits)
+    const bool reduced = p.D == 4 && sizeof(CodeT) == 1;
+    uint8_t* wwide = flags + 2;
     if ((e = weight_digits<CodeT>(p.D, w, bias, g.F, p.fold ? p.ckk : g.C, taps, p.Kp, 0, f, bdig,
-                                  col_add, col_nar, flags + 1, st)) != cudaSuccess)
+                                  col_add, col_nar, flags + 1, st, reduced ? wwide : nullptr, kDgradDB)) !=
+        cudaSuccess)
         return 4;
-    CUtensorMap tA, tB;
+    CUtensorMap tA, tB, tA3, tB3;
+    uint32_t boxA3[5];
+    for (int i = 0; i < 5; ++i) boxA3[i] = p.boxA[i];
+    boxA3[4] = kDgradDB;
     if (!map_act(&tA, adig, p.D, gv.N, p.Ha, p.Wa, p.Ca, p.boxA) ||
-        !map_weights(&tB, bdig, p.D, p.brows, taps * p.Kp, p.NT))
+        !map_weights(&tB, bdig, p.D, p.brows, taps * p.Kp, p.NT) ||
+        (reduced && (!map_act(&tA3, adig, p.D, gv.N, p.Ha, p.Wa, p.Ca, boxA3) ||
+                     !map_weights(&tB3, bdig, p.D, p.brows, taps * p.Kp, p.NT, kDgradDB))))
         return 5;
     IgemmArgs a = p.a;
     a.col_add = bias ? col_add : nullptr;
@@ -629,6 +639,16 @@ int run_fwd(const ImplPlan& p, const ConvGeom& g, const CodeT* x, const CodeT* w
     a.relu = relu;
     a.pre_out = pre;
     const OutMap<CodeT> out = out_nchw<CodeT>(y, g.OH * g.OW, g.F);
+    if (reduced) {  // both launched; the x / w plane flags let exactly one run
+        a.vflag = xwide;
+        a.vflag2 = wwide;
+        a.vexpect = a.vexpect2 = 0;
+        if constexpr (sizeof(CodeT) == 1)
+            if ((e = launch_kernel<4, CodeT, 0, kDgradDB, 0, kDgradDB>(tA3, tB3, a, out, st)) != cudaSuccess)
+                return 4;
+        a.vor = 1;
+        a.vexpect = 1;
+    }
     if ((e = dispatch<CodeT, 0>(p.D, tA, tB, a, out, st)) != cudaSuccess) return 4;
     if (use_partial) {
         launch_finalize<CodeT>(a.partial, int(a.splits), nullptr, col_nar, out, a.M, a.N, f, nullptr, nullptr, st);

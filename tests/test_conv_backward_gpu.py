@@ -287,3 +287,35 @@ def test_wgrad_reduced_digits(cuda, po, wide, shape):
     if N * H * W <= 512:
         ref = po.conv2d_weight_grad(12, 1, dya, po.convert_tensor(8, 1, 12, 1, xa), (F, C, K, K), 1, pad)
         assert (host(dw).reshape(ref.shape) == ref).all()
+
+
+@pytest.mark.parametrize("wide", ["none", "x", "w"])
+@pytest.mark.parametrize("shape", [(2, 32, 8, 8, 32, 3, 1), (3, 64, 16, 16, 64, 3, 1), (2, 3, 32, 32, 32, 3, 1)])
+def test_fwd_reduced_digits(cuda, po, wide, shape):
+    """posit(8,1) forward with x and w within 3 digits takes the device-selected
+    3 x 3 digit kernel; one wide value switches to the full kernel.  Against
+    the explicit path and the oracle (with bias, relu fused or not)."""
+    N, C, H, W, F, K, pad = shape
+    rng = np.random.default_rng(29)
+    xa = np.array([po.from_float64(8, 1, float(v)) for v in rng.normal(0, 2.0, N * C * H * W)],
+                  np.uint64).reshape(N, C, H, W)
+    wa = np.array([po.from_float64(8, 1, float(v)) for v in rng.normal(0, 0.2, F * C * K * K)],
+                  np.uint64).reshape(F, C, K, K)
+    ba = np.array([po.from_float64(8, 1, float(v)) for v in rng.normal(0, 0.1, F)], np.uint64)
+    if wide == "x":
+        xa[1, 0, 3, 3] = po.from_float64(8, 1, 3000.0)
+    if wide == "w":
+        wa[2, 1, 1, 1] = po.from_float64(8, 1, -3000.0)
+    x, w, b = dev(P81, xa), dev(P81, wa), dev(P81, ba)
+    y = ops.conv2d(P81, x, w, b, 1, pad)
+    prev = ops.conv_algo(1)
+    try:
+        ref = ops.conv2d(P81, x, w, b, 1, pad)
+    finally:
+        ops.conv_algo(prev)
+    assert torch.equal(y, ref)
+    yr, pre = ops.conv2d_fwd_layer(P81, x, w, b, 1, pad, None, relu=True, want_pre=True)
+    assert torch.equal(pre, ref) and torch.equal(yr, ops.relu_fwd(P81, ref))
+    if N * H * W <= 128:
+        want = po.conv2d(8, 1, xa, wa, ba, 1, pad)
+        assert (host(y).reshape(want.shape) == want).all()
