@@ -414,9 +414,9 @@ def main():
         # torch's own CPU worker threads (used by pin_memory above) must not spin
         # against the library's host pool inside the timed region
         torch.set_num_threads(1)
-        for _ in range(2):
+        for _ in range(3):
             e2e_step()
-        e_steps = max(1, min(args.steps, 5))
+        e_steps = max(1, min(args.steps, 10))
         if dist:
             dist.barrier()
         t0 = time.perf_counter()
