@@ -435,7 +435,8 @@ template <typename SrcT>
 cudaError_t act_digits_t(int D, const SrcT* x, int64_t N, int64_t C, int64_t H, int64_t W, int64_t Cp,
                          int pad, const PositFmt& f, const PositFmt& fs, uint32_t* lut, bool build_lut,
                          int8_t* dig, uint8_t* pos_nar, uint8_t* chw_nar, uint8_t* chan_nar,
-                         uint8_t* any, cudaStream_t st, const DigitGate& gt, uint8_t* wide, int wide_planes) {
+                         uint8_t* any, cudaStream_t st, const DigitGate& gt, uint8_t* wide, int wide_planes,
+                         int store_planes, const uint8_t* only_if, const uint8_t* only_if2) {
     // thread per (pixel, 32 channels): grid (pixel blocks, 32-channel chunks)
     if (N * H * W >= (int64_t(1) << 31)) return cudaErrorInvalidValue;
     const dim3 grid(unsigned((grid_for(N * H * W * (Cp / 32), 256) + Cp / 32 - 1) / (Cp / 32)),
@@ -453,19 +454,20 @@ cudaError_t act_digits_t(int D, const SrcT* x, int64_t N, int64_t C, int64_t H, 
     if (tiled && gt.gate == nullptr)                                                                 \
         act_digits_tiled_kernel<DD, SrcT, 0><<<tgrid, 256, 0, st>>>(                                 \
             x, int(N), int(C), int(H), int(W), int(Cp), pad, fd_hw, fd_w, f, fs, lut, dig, pos_nar,  \
-            chw_nar, chan_nar, any, gt, wide, wide_planes);                                          \
+            chw_nar, chan_nar, any, gt, wide, wide_planes, store_planes, only_if, only_if2);         \
     else if (tiled && gt.gb == 1)                                                                    \
         act_digits_tiled_kernel<DD, SrcT, 1><<<tgrid, 256, 0, st>>>(                                 \
             x, int(N), int(C), int(H), int(W), int(Cp), pad, fd_hw, fd_w, f, fs, lut, dig, pos_nar,  \
-            chw_nar, chan_nar, any, gt, wide, wide_planes);                                          \
+            chw_nar, chan_nar, any, gt, wide, wide_planes, store_planes, only_if, only_if2);         \
     else if (tiled)                                                                                  \
         act_digits_tiled_kernel<DD, SrcT, 2><<<tgrid, 256, 0, st>>>(                                 \
             x, int(N), int(C), int(H), int(W), int(Cp), pad, fd_hw, fd_w, f, fs, lut, dig, pos_nar,  \
-            chw_nar, chan_nar, any, gt, wide, wide_planes);                                          \
+            chw_nar, chan_nar, any, gt, wide, wide_planes, store_planes, only_if, only_if2);         \
     else                                                                                             \
         act_digits_kernel<DD, SrcT><<<grid, 256, 0, st>>>(x, int(N), int(C), int(H), int(W), int(Cp), \
                                                           pad, fd_hw, fd_w, f, fs, lut, dig, pos_nar, \
-                                                          chw_nar, chan_nar, any, gt, wide, wide_planes)
+                                                          chw_nar, chan_nar, any, gt, wide, wide_planes, \
+                                                          store_planes, only_if, only_if2)
     switch (D) {
         case 2: PNN_ACT(2); break;
         case 3: PNN_ACT(3); break;
@@ -484,13 +486,29 @@ cudaError_t act_digits(int D, const void* x, int64_t N, int64_t C, int64_t H, in
                        int pad, const PositFmt& f, const PositFmt& fs, uint32_t* lut, bool build_lut,
                        int8_t* dig, uint8_t* pos_nar, uint8_t* chw_nar, uint8_t* chan_nar, uint8_t* any,
                        cudaStream_t st, const DigitGate& gt = DigitGate{}, uint8_t* wide = nullptr,
-                       int wide_planes = 0) {
+                       int wide_planes = 0, bool reduce_stores = false, const uint8_t* also_if = nullptr,
+                       const uint8_t* only_if = nullptr) {
     if (lut == nullptr && !same_fmt(f, fs)) return cudaErrorInvalidValue;  // no in-register convert
-    if (fs.nbits <= 8)
-        return act_digits_t(D, static_cast<const uint8_t*>(x), N, C, H, W, Cp, pad, f, fs, lut, build_lut,
-                            dig, pos_nar, chw_nar, chan_nar, any, st, gt, wide, wide_planes);
-    return act_digits_t(D, static_cast<const uint16_t*>(x), N, C, H, W, Cp, pad, f, fs, lut, build_lut,
-                        dig, pos_nar, chw_nar, chan_nar, any, st, gt, wide, wide_planes);
+    // reduce_stores (every consumer of these digits is a flag-selected variant):
+    // store only the planes the reduced-digit kernels read, then a completion
+    // pass (exits at once unless the wide flag is set) writes all planes
+    // (also_if: a second flag whose consumers read the high planes too.)
+    // only_if alone: a single full pass that runs iff *only_if (a later completion).
+    const int sp = reduce_stores && wide != nullptr && wide_planes > 0 && wide_planes < D ? wide_planes : D;
+    for (int pass = 0; pass < (sp < D ? 2 : 1); ++pass) {
+        const int store = pass == 0 ? sp : D;
+        const uint8_t* oi = pass == 0 ? only_if : wide;
+        const uint8_t* oi2 = pass == 0 ? nullptr : also_if;
+        const bool lut_now = build_lut && pass == 0;
+        cudaError_t e =
+            fs.nbits <= 8
+                ? act_digits_t(D, static_cast<const uint8_t*>(x), N, C, H, W, Cp, pad, f, fs, lut, lut_now, dig,
+                               pos_nar, chw_nar, chan_nar, any, st, gt, wide, wide_planes, store, oi, oi2)
+                : act_digits_t(D, static_cast<const uint16_t*>(x), N, C, H, W, Cp, pad, f, fs, lut, lut_now, dig,
+                               pos_nar, chw_nar, chan_nar, any, st, gt, wide, wide_planes, store, oi, oi2);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
 }
 
 template <typename SrcT>
@@ -685,7 +703,7 @@ int run_dgrad(const ImplPlan& p, const ConvGeom& g, const CodeT* dy, const CodeT
     const bool reduced = dgrad_reduced(p.D) && sizeof(CodeT) == 2;
     if (pre == nullptr &&
         act_digits(p.D, dy, g.N, g.F, g.OH, g.OW, p.Ca, 0, f, f, lut_of(p, ws, f), true, adig, pos_nar,
-                   nullptr, nullptr, flags, st, gt, reduced ? flags + 3 : nullptr, kDgradDB) != cudaSuccess)
+                   nullptr, nullptr, flags, st, gt, reduced ? flags + 3 : nullptr, kDgradDB, reduced) != cudaSuccess)
         return 4;
     const int8_t* a_dig = pre ? pre->dig : adig;
     const uint8_t* a_pos = pre ? pre->pos_nar : pos_nar;
@@ -695,6 +713,13 @@ int run_dgrad(const ImplPlan& p, const ConvGeom& g, const CodeT* dy, const CodeT
     uint8_t* wide = flags + 2;  // weights need more than kDgradDB digit planes
     if (weight_digits<CodeT>(p.D, w, nullptr, g.F, g.C, taps, p.Kp, 1, f, bdig, nullptr, nullptr,
                              flags + 1, st, reduced ? wide : nullptr, kDgradDB) != cudaSuccess)
+        return 4;
+    // dy's digits were stored without the high planes (narrow dy): the full
+    // variant, selected by wide weights, reads them -- complete dy then
+    if (reduced && dy_wide != nullptr &&
+        act_digits(p.D, dy, g.N, g.F, g.OH, g.OW, p.Ca, 0, f, f, lut_of(p, ws, f), true,
+                   const_cast<int8_t*>(a_dig), nullptr, nullptr, nullptr, flags + 4, st, gt, nullptr, 0, false,
+                   nullptr, wide) != cudaSuccess)
         return 4;
     CUtensorMap tA, tA3, tB, tB3;
     uint32_t box3[5];
@@ -747,7 +772,7 @@ int run_wgrad(const ImplPlan& p, const ConvGeom& g, const void* dy, const PositF
               const void* x, const PositFmt& fx, CodeT* dw, unsigned __int128* raw_words,
               uint8_t* raw_nar, uint8_t* ws, cudaStream_t st, const SavedX* sv = nullptr,
               uint8_t* share_pos_nar = nullptr, const DigitGate& gt = DigitGate{},
-              uint8_t* dy_wide = nullptr) {
+              uint8_t* dy_wide = nullptr, bool share_gated = true) {
     const PositFmt& f = p.a.f;
     auto* adig = sv ? sv->dig : reinterpret_cast<int8_t*>(ws + p.off_adig);
     auto* bdig = reinterpret_cast<int8_t*>(ws + p.off_bdig);
@@ -769,8 +794,13 @@ int run_wgrad(const ImplPlan& p, const ConvGeom& g, const void* dy, const PositF
     // reduced-digit variant: saved (8,1)-format x one digit up, both operands in 3 planes
     const bool reduced = sv != nullptr && sizeof(CodeT) == 2 && p.D == 6 && p.DA == 4 && p.OFF == 1;
     if (reduced && dy_wide == nullptr) dy_wide = flags + 3;
+    // dy's high digit planes only when used: every consumer (this pass, and the
+    // input gradient sharing the digits) is a flag-selected variant
+    const bool reduce_dy = reduced && (share_pos_nar == nullptr || share_gated);
+    // (the full weight-gradient variant also runs when x alone is wide: complete dy then too)
     if (act_digits(p.D, dy, g.N, g.F, g.OH, g.OW, p.Fpw, 0, f, fdy, lut_of(p, ws, fdy, 1), true, bdig,
-                   share_pos_nar, nullptr, col_nar, flags + 1, st, gt, dy_wide, kDgradDB) != cudaSuccess)
+                   share_pos_nar, nullptr, col_nar, flags + 1, st, gt, dy_wide, kDgradDB, reduce_dy,
+                   reduced ? sv->flag + 1 : nullptr) != cudaSuccess)
         return 4;
     CUtensorMap tA, tB, tA3, tB3;
     const uint32_t boxB[5] = {uint32_t(2 * p.a.OWb), uint32_t(p.a.OHb), 1, uint32_t(p.NT / 16),
@@ -872,16 +902,17 @@ int run_backward(const BwdPlan& b, const ConvGeom& g, const PositFmt& ff, const 
     uint8_t* wsd = ws + b.off_d;
     if (b.share_dy && cudaMemsetAsync(wsd + b.pd.off_maps, 0, b.pd.maps_bytes, st) != cudaSuccess) return 4;
     uint8_t* dy_wide = b.share_dy ? wsd + b.pd.off_flags + 3 : nullptr;  // cleared with the dgrad maps
+    const bool dgrad_gated = dgrad_reduced(b.pd.D) && sizeof(BT) == 2;
     int rc = run_wgrad<GT>(b.pw, g, dy, fb, x, ff, static_cast<GT*>(dw), raw_words, raw_nar, ws, st,
                            b.use_saved ? sv : nullptr,
-                           b.share_dy ? wsd + b.pd.off_pos_nar : nullptr, gt, dy_wide);
+                           b.share_dy ? wsd + b.pd.off_pos_nar : nullptr, gt, dy_wide, dgrad_gated);
     if (rc != 0 || !b.has_dx) return rc;
     const DigitGate gd = gt;  // the input gradient digitises dy itself unless it shares the digits
     if (b.share_dy) {
         const DyDigits pre{reinterpret_cast<const int8_t*>(ws + b.pw.off_bdig), wsd + b.pd.off_pos_nar,
                            ws + b.pw.off_flags + 1, dy_wide};
         return run_dgrad<BT>(b.pd, g, static_cast<const BT*>(dy), static_cast<const BT*>(w_bwd),
-                             static_cast<BT*>(dx), wsd, st, &pre);
+                             static_cast<BT*>(dx), wsd, st, &pre, gd);
     }
     return run_dgrad<BT>(b.pd, g, static_cast<const BT*>(dy), static_cast<const BT*>(w_bwd),
                          static_cast<BT*>(dx), wsd, st, nullptr, gd);

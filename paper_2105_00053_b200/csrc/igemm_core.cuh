@@ -522,7 +522,7 @@ __device__ __forceinline__ void emit_pixel_digits(const uint32_t (&code)[32], ui
                                                   uint8_t* __restrict__ chw_nar,
                                                   uint8_t* __restrict__ chan_nar, uint8_t* __restrict__ any,
                                                   bool ring = true, uint8_t* __restrict__ wide = nullptr,
-                                                  int wide_planes = 0) {
+                                                  int wide_planes = 0, int store_planes = D) {
     const int Hp = H + 2 * pad, Wp = W + 2 * pad;
     const int CS = Cp / 16;
     const int c0 = cc * 32;
@@ -548,6 +548,7 @@ __device__ __forceinline__ void emit_pixel_digits(const uint32_t (&code)[32], ui
     int8_t* dst = cell(int(h) + pad, int(w) + pad);
 #pragma unroll
     for (int p = 0; p < D; ++p) {
+        if (p >= store_planes) break;  // high planes: written by the completion pass if used
         *reinterpret_cast<uint4*>(dst + p * plane) =
             make_uint4(words[p][0], words[p][1], words[p][2], words[p][3]);
         *reinterpret_cast<uint4*>(dst + p * plane + int64_t(Wp) * 16) =
@@ -562,7 +563,7 @@ __device__ __forceinline__ void emit_pixel_digits(const uint32_t (&code)[32], ui
             for (int ww = xlo; ww <= xhi; ++ww) {
                 if (hh == int(h) + pad && ww == int(w) + pad) continue;
                 int8_t* z = cell(hh, ww);
-                for (int p = 0; p < D; ++p) {
+                for (int p = 0; p < store_planes; ++p) {
                     *reinterpret_cast<uint4*>(z + p * plane) = make_uint4(0, 0, 0, 0);
                     *reinterpret_cast<uint4*>(z + p * plane + int64_t(Wp) * 16) = make_uint4(0, 0, 0, 0);
                 }
@@ -598,7 +599,10 @@ __global__ void __launch_bounds__(256) act_digits_kernel(
     FastDiv fd_w, PositFmt f, PositFmt fs, const uint32_t* __restrict__ lut,
     int8_t* __restrict__ dig, uint8_t* __restrict__ pos_nar, uint8_t* __restrict__ chw_nar,
     uint8_t* __restrict__ chan_nar, uint8_t* __restrict__ any, DigitGate gt = DigitGate{},
-    uint8_t* __restrict__ wide = nullptr, int wide_planes = 0) {
+    uint8_t* __restrict__ wide = nullptr, int wide_planes = 0, int store_planes = D,
+    const uint8_t* __restrict__ only_if = nullptr, const uint8_t* __restrict__ only_if2 = nullptr) {
+    // completion pass: runs iff a consumer reads the high planes
+    if (only_if != nullptr && *only_if == 0 && (only_if2 == nullptr || *only_if2 == 0)) return;
     const uint32_t HW = uint32_t(H) * uint32_t(W);
     const uint32_t pixels = uint32_t(N) * HW;
     const int64_t plane = int64_t(N) * (H + 2 * pad) * (W + 2 * pad) * Cp;
@@ -621,7 +625,7 @@ __global__ void __launch_bounds__(256) act_digits_kernel(
         uint32_t h, w;
         fd_w.divmod(pix, h, w);
         emit_pixel_digits<D>(code, r, n, pix, h, w, cc, C, H, W, Cp, pad, plane, HW, f, nar_code, lut,
-                             dig, pos_nar, chw_nar, chan_nar, any, true, wide, wide_planes);
+                             dig, pos_nar, chw_nar, chan_nar, any, true, wide, wide_planes, store_planes);
     }
 }
 
@@ -637,7 +641,10 @@ __global__ void __launch_bounds__(256) act_digits_tiled_kernel(
     FastDiv fd_w, PositFmt f, PositFmt fs, const uint32_t* __restrict__ lut,
     int8_t* __restrict__ dig, uint8_t* __restrict__ pos_nar, uint8_t* __restrict__ chw_nar,
     uint8_t* __restrict__ chan_nar, uint8_t* __restrict__ any, DigitGate gt = DigitGate{},
-    uint8_t* __restrict__ wide = nullptr, int wide_planes = 0) {
+    uint8_t* __restrict__ wide = nullptr, int wide_planes = 0, int store_planes = D,
+    const uint8_t* __restrict__ only_if = nullptr, const uint8_t* __restrict__ only_if2 = nullptr) {
+    // completion pass: runs iff a consumer reads the high planes
+    if (only_if != nullptr && *only_if == 0 && (only_if2 == nullptr || *only_if2 == 0)) return;
     constexpr int TP = 256;                                   // pixels per tile
     constexpr int VPR = TP * int(sizeof(CodeT)) / 16;         // 16-byte vectors per channel row
     __shared__ uint4 s_tile[32 * VPR];
@@ -691,7 +698,7 @@ __global__ void __launch_bounds__(256) act_digits_tiled_kernel(
         // every warp: each image row has a first and a last pixel)
         emit_pixel_digits<D>(code, r0 + threadIdx.x, n, pix, h, w, cc, C, H, W, Cp, pad, plane, HW, f,
                              nar_code, lut, dig, pos_nar, chw_nar, chan_nar, any, /*ring=*/false, wide,
-                             wide_planes);
+                             wide_planes, store_planes);
         if (pad > 0) {
             const int Hp = H + 2 * pad, Wp = W + 2 * pad, CS = Cp / 16;
             uint32_t hh0, ww0;
@@ -703,8 +710,9 @@ __global__ void __launch_bounds__(256) act_digits_tiled_kernel(
             const int side = rows * 2 * pad;
             const int top = y0 == 0 ? pad * Wp : 0, bot = y1 == H - 1 ? pad * Wp : 0;
             const int cells = side + top + bot;
-            for (int i = threadIdx.x; i < cells * D * 2; i += blockDim.x) {
-                const int cell = i / (D * 2), rest = i - cell * (D * 2), p = rest >> 1, sl = rest & 1;
+            const int SP = store_planes;
+            for (int i = threadIdx.x; i < cells * SP * 2; i += blockDim.x) {
+                const int cell = i / (SP * 2), rest = i - cell * (SP * 2), p = rest >> 1, sl = rest & 1;
                 int hh, ww;
                 if (cell < side) {
                     const int r = cell / (2 * pad), k = cell - r * (2 * pad);
