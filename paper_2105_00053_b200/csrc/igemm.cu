@@ -193,8 +193,12 @@ bool make_plan(int pass, const PositFmt& f, const ConvGeom& g_real, bool raw, Im
     }
     // split-K: int32 group sums exact for <= 131071 / D terms (W > 32), SM fill
     const int64_t cap = f.W <= 32 ? a.kbt : (131071 / D) / kIKB;
+    // CTAs in flight: two per SM for the two-CTA kernels -- including the weight
+    // gradient's reduced-digit variant (saved (8,1) digits under (12,1)), which
+    // needs the second CTA's stages to keep enough TMA boxes in flight
+    const bool wg_pair = pass == 2 && D == 6 && p->DA == 4 && p->OFF == 1;
     const int64_t kbps = split_kblocks(a.kbt, cap < 1 ? 1 : cap, a.mtiles * a.ntiles,
-                                       num_sms() * ((pass == 2 || D >= 5) ? 1 : 2));  // CTAs in flight
+                                       num_sms() * (((pass == 2 && !wg_pair) || (pass != 2 && D >= 5)) ? 1 : 2));
     a.kb_per_split = a.kbt < kbps ? a.kbt : kbps;
     a.splits = cdiv(a.kbt, a.kb_per_split);
     a.fd_split = FastDiv(uint32_t(a.mtiles * a.ntiles));
