@@ -383,7 +383,9 @@ __device__ __forceinline__ void store_codes8(CodeT* dst, const uint32_t (&c)[8],
             *reinterpret_cast<uint4*>(dst) = v;
         }
     } else {
-        for (int j = 0; j < valid; ++j) dst[j] = CodeT(c[j]);
+#pragma unroll
+        for (int j = 0; j < 8; ++j)  // unrolled: c[] stays in registers
+            if (j < valid) dst[j] = CodeT(c[j]);
     }
 }
 
