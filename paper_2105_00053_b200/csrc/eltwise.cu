@@ -536,13 +536,37 @@ __device__ __forceinline__ uint32_t sgd_fast(const PositFmt& fo, const PositFmt&
     return q_to_posit_lut(fo, (unsigned __int128)((__int128)(Xw - Xm) << fo.R), lut);
 }
 
+// Stage copy of an optimizer-format value by its integer image: round
+// X_w 2^-R_o into format fc -- X shifted to fc's quire units, bits shifted out
+// jammed into the LSB (they lie below every rounding position, or the value
+// is below minpos and rounds to +-minpos either way), then the quire rounding
+// (= p_convert, a correctly rounded conversion).
+__device__ __forceinline__ uint32_t copy_fast(const PositFmt& fo, const PositFmt& fc, uint32_t w, int64_t Xw,
+                                              const uint4* lut) {
+    if (w == (1u << (fo.nbits - 1))) return 1u << (fc.nbits - 1);
+    const int sh = 2 * fc.R - fo.R;
+    __int128 q;
+    if (sh >= 0) {
+        q = (__int128)Xw << sh;
+    } else {
+        const int64_t a = Xw < 0 ? -Xw : Xw;
+        const int64_t m = (a >> -sh) | ((a & ((int64_t(1) << -sh) - 1)) != 0 ? 1 : 0);
+        q = Xw < 0 ? -(__int128)m : (__int128)m;
+    }
+    // (the 128-bit rounding takes W > 64; narrower words hold the value in 64 bits)
+    return fc.W <= 64 ? q_to_posit_lut(fc, uint64_t(int64_t(q)), lut)
+                      : q_to_posit_lut(fc, (unsigned __int128)q, lut);
+}
+
 __global__ void sgd_multi_kernel(PositFmt fo, int bo, PositFmt fg, int bg, uint32_t lr, PositFmt f1,
                                  int b1, PositFmt f2, int b2, int grad_scale_log2,
                                  const __grid_constant__ SgdSegs segs, int fast) {
-    __shared__ uint4 s_lut[kPackLutEntries];
+    __shared__ uint4 s_lut[kPackLutEntries], s_lut1[kPackLutEntries], s_lut2[kPackLutEntries];
     int64_t X_lr = 0;
     if (fast) {
         build_pack_lut(fo, s_lut, threadIdx.x, blockDim.x);
+        if (fast & 2) build_pack_lut(f1, s_lut1, threadIdx.x, blockDim.x);
+        if (fast & 4) build_pack_lut(f2, s_lut2, threadIdx.x, blockDim.x);
         decode_x(lr, fo, X_lr);
         __syncthreads();
     }
@@ -565,8 +589,12 @@ __global__ void sgd_multi_kernel(PositFmt fo, int bo, PositFmt fg, int bg, uint3
             w = p_sub(fo, load_any(segs.master[lo], k, bo), p_mul(fo, lr, g));
         }
         store_any(segs.master[lo], k, bo, w);
-        if (segs.copy1[lo]) store_any(segs.copy1[lo], k, b1, p_convert(fo, f1, w));
-        if (segs.copy2[lo]) store_any(segs.copy2[lo], k, b2, p_convert(fo, f2, w));
+        int64_t Xw = 0;
+        if (fast & 6) decode_x(w, fo, Xw);
+        if (segs.copy1[lo])
+            store_any(segs.copy1[lo], k, b1, (fast & 2) ? copy_fast(fo, f1, w, Xw, s_lut1) : p_convert(fo, f1, w));
+        if (segs.copy2[lo])
+            store_any(segs.copy2[lo], k, b2, (fast & 4) ? copy_fast(fo, f2, w, Xw, s_lut2) : p_convert(fo, f2, w));
     }
 }
 
@@ -948,9 +976,14 @@ int pnn_sgd_step_multi(int opt_nbits, int opt_es, int g_nbits, int g_es, uint32_
     // integer-image update (sgd_fast): images within 64 bits, exact intermediates
     // within the optimizer quire word (|X_g| 2^(2Ro-Rg), lr * g', (w - m) 2^Ro)
     const bool lr_nar = lr_code == (1u << (opt_nbits - 1));
-    const int fast = grad_scale_log2 == 0 && !lr_nar && 2 * fo.R <= 62 && 2 * fg.R <= 62 &&
+    // copies by integer image: the shifted image stays within the copy format's quire word
+    auto copy_ok = [&](const PositFmt& fc) {
+        return 2 * fc.R <= 60 && fc.W <= 128 && fo.R + 2 * fc.R + 1 < fc.W && 2 * fo.R <= 60;
+    };
+    int fast = grad_scale_log2 == 0 && !lr_nar && fo.W > 64 && 2 * fo.R <= 62 && 2 * fg.R <= 62 &&
                      2 * fo.R >= fg.R && 2 * fo.R <= 60 && fo.W <= 128 && fg.R + 2 * fo.R + 1 < fo.W &&
                      4 * fo.R + 1 < fo.W && 3 * fo.R + 2 < fo.W;
+    if (fast) fast |= (has1 && copy_ok(f1) ? 2 : 0) | (has2 && copy_ok(f2) ? 4 : 0);
     for (int base = 0; base < count; base += kSgdMaxSeg) {
         SgdSegs sg{};
         sg.count = 0;

@@ -44,7 +44,9 @@ def test_pool_recompute_equals_argmax(cuda, xf, gf, shape, ties):
 @pytest.mark.parametrize("opt,grad,copies", [((16, 1), (12, 1), [(8, 1), (12, 1)]),
                                              ((16, 1), (16, 1), []),
                                              ((12, 2), (8, 2), [(8, 2)]),
-                                             ((16, 1), (8, 0), [(8, 0)])])
+                                             ((16, 1), (8, 0), [(8, 0)]),
+                                             ((16, 1), (12, 1), [(8, 1), (8, 0)]),
+                                             ((16, 1), (16, 1), [(12, 1), (16, 1)])])
 @pytest.mark.parametrize("scale", [0, 1])
 def test_sgd_multi_equals_per_tensor(cuda, opt, grad, copies, scale):
     """The whole-model optimizer launch == pnn_sgd_step_scaled per tensor."""
