@@ -443,8 +443,8 @@ cudaError_t act_digits_t(int D, const SrcT* x, int64_t N, int64_t C, int64_t H, 
                          int store_planes, const uint8_t* only_if, const uint8_t* only_if2) {
     // thread per (pixel, 32 channels): grid (pixel blocks, 32-channel chunks)
     if (N * H * W >= (int64_t(1) << 31)) return cudaErrorInvalidValue;
-    const dim3 grid(unsigned((grid_for(N * H * W * (Cp / 32), 256) + Cp / 32 - 1) / (Cp / 32)),
-                    unsigned(Cp / 32));
+    const int64_t gx = (grid_for(N * H * W * (Cp / 32), 256) + Cp / 32 - 1) / (Cp / 32);
+    const dim3 grid(unsigned(only_if != nullptr && gx > 148 ? 148 : gx), unsigned(Cp / 32));
     const FastDiv fd_hw{uint32_t(H * W)}, fd_w{uint32_t(W)};
     if (lut == nullptr) build_lut = false;
     // whole 256-pixel tiles per image, 16-byte aligned channel rows: staged loads
@@ -452,7 +452,10 @@ cudaError_t act_digits_t(int D, const SrcT* x, int64_t N, int64_t C, int64_t H, 
                        (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
                        (reinterpret_cast<uintptr_t>(gt.gate) & 15) == 0;
     const int64_t ntiles = N * H * W / 256;
-    const dim3 tgrid(unsigned(ntiles < 148 * 8 ? ntiles : 148 * 8), unsigned(Cp / 32));
+    // a completion pass (only_if) usually exits at once: few blocks (grid-stride
+    // loops cover the work when it does run)
+    const int64_t tcap = only_if != nullptr ? 148 : 148 * 8;
+    const dim3 tgrid(unsigned(ntiles < tcap ? ntiles : tcap), unsigned(Cp / 32));
 #define PNN_ACT(DD)                                                                                  \
     if (build_lut) digit_lut_conv_kernel<DD><<<16, 256, 0, st>>>(fs, f, lut);                        \
     if (tiled && gt.gate == nullptr)                                                                 \
