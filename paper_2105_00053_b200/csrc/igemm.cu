@@ -82,7 +82,7 @@ bool fold_geom(int pass, const ConvGeom& g, ConvGeom* gv) {
 }
 
 bool make_plan(int pass, const PositFmt& f, const ConvGeom& g_real, bool raw, ImplPlan* p,
-               int DA = 0, int OFF = 0) {
+               int DA = 0, int OFF = 0, bool saved_x = false) {
     if (conv_algo() == 1 || g_real.stride != 1) return false;
     if (g_real.N < 1 || g_real.N > (1 << 30)) return false;
     // Linear layers (1x1 over 1x1 images): a TMA box would gather one 16-byte
@@ -196,7 +196,8 @@ bool make_plan(int pass, const PositFmt& f, const ConvGeom& g_real, bool raw, Im
     // CTAs in flight: two per SM for the two-CTA kernels -- including the weight
     // gradient's reduced-digit variant (saved (8,1) digits under (12,1)), which
     // needs the second CTA's stages to keep enough TMA boxes in flight
-    const bool wg_pair = pass == 2 && D == 6 && p->DA == 4 && p->OFF == 1;
+    const bool wg_pair = pass == 2 && saved_x && D == 6 &&
+                         ((p->DA == 4 && p->OFF == 1) || (p->DA == 6 && p->OFF == 0));
     const int64_t kbps = split_kblocks(a.kbt, cap < 1 ? 1 : cap, a.mtiles * a.ntiles,
                                        num_sms() * (((pass == 2 && !wg_pair) || (pass != 2 && D >= 5)) ? 1 : 2));
     a.kb_per_split = a.kbt < kbps ? a.kbt : kbps;
@@ -328,7 +329,7 @@ cudaError_t launch_kernel(const CUtensorMap& tA, const CUtensorMap& tB, const Ig
                           OutMap<CodeT> out, cudaStream_t st) {
     // reduced-digit input gradient: (DA + DB - 1) * 32 <= 256 TMEM columns, so
     // two CTAs per SM overlap one's TMEM drain with the other's MMAs
-    constexpr bool kPairSM = (MODE == 1 || MODE == 2) && DB < D && (DA + DB - 1) * 32 <= 256;
+    constexpr bool kPairSM = DB < D && (DA + DB - 1) * 32 <= 256;
     constexpr int NTT = kPairSM ? 32 : nt_of<MODE, D>();
     constexpr int CPS = kPairSM ? 2 : cps_of<MODE, D>(), ACC = acc_of<MODE, D>();
     using Geo = ImplGeo<D, NTT, CPS, ACC, DA, DB>;
@@ -640,8 +641,8 @@ int run_fwd(const ImplPlan& p, const ConvGeom& g, const CodeT* x, const CodeT* w
                        pos_nar, sv ? sv->chw : nullptr, nullptr, xflag, st, DigitGate{}, xwide, kDgradDB);
     if (e != cudaSuccess) return 4;
     const int64_t taps = gv.KH * gv.KW;  // weights: [F][C*KH*KW] read as [F][ckk][1][1] if folded
-    // reduced-digit variant (posit(8,1): x and w within 3 balanced digits)
-    const bool reduced = p.D == 4 && sizeof(CodeT) == 1;
+    // reduced-digit variant (posit(8,1) / posit(12,1): x and w within 3 balanced digits)
+    const bool reduced = (p.D == 4 && sizeof(CodeT) == 1) || (p.D == 6 && sizeof(CodeT) == 2);
     uint8_t* wwide = flags + 2;
     if ((e = weight_digits<CodeT>(p.D, w, bias, g.F, p.fold ? p.ckk : g.C, taps, p.Kp, 0, f, bdig,
                                   col_add, col_nar, flags + 1, st, reduced ? wwide : nullptr, kDgradDB)) !=
@@ -671,6 +672,12 @@ int run_fwd(const ImplPlan& p, const ConvGeom& g, const CodeT* x, const CodeT* w
         if constexpr (sizeof(CodeT) == 1)
             if ((e = launch_kernel<4, CodeT, 0, kDgradDB, 0, kDgradDB>(tA3, tB3, a, out, st)) != cudaSuccess)
                 return 4;
+        if constexpr (sizeof(CodeT) == 2) {  // 64-bit quire word when a single chunk's exact sum fits
+            const bool narrow_word = a.splits == 1 && a.kb_per_split * kIKB < (int64_t(1) << 17);
+            e = narrow_word ? launch_kernel<6, CodeT, 0, kDgradDB, 0, kDgradDB, 2>(tA3, tB3, a, out, st)
+                            : launch_kernel<6, CodeT, 0, kDgradDB, 0, kDgradDB, 4>(tA3, tB3, a, out, st);
+            if (e != cudaSuccess) return 4;
+        }
         a.vor = 1;
         a.vexpect = 1;
     }
@@ -799,7 +806,9 @@ int run_wgrad(const ImplPlan& p, const ConvGeom& g, const void* dy, const PositF
         if (e != cudaSuccess) return 4;
     }
     // reduced-digit variant: saved (8,1)-format x one digit up, both operands in 3 planes
-    const bool reduced = sv != nullptr && sizeof(CodeT) == 2 && p.D == 6 && p.DA == 4 && p.OFF == 1;
+    // ((8,1) saved digits one digit up, or same-format (12,1) saved digits)
+    const bool reduced = sv != nullptr && sizeof(CodeT) == 2 && p.D == 6 &&
+                         ((p.DA == 4 && p.OFF == 1) || (p.DA == 6 && p.OFF == 0));
     if (reduced && dy_wide == nullptr) dy_wide = flags + 3;
     // dy's high digit planes only when used: every consumer (this pass, and the
     // input gradient sharing the digits) is a flag-selected variant
@@ -841,9 +850,12 @@ int run_wgrad(const ImplPlan& p, const ConvGeom& g, const void* dy, const PositF
         a.vflag = sv->flag + 1;
         a.vflag2 = dy_wide;
         a.vexpect = a.vexpect2 = 0;
-        if constexpr (sizeof(CodeT) == 2)
-            if (launch_kernel<6, CodeT, 2, kDgradDB, 1, kDgradDB, 4>(tA3, tB3, a, out, st) != cudaSuccess)
-                return 4;
+        if constexpr (sizeof(CodeT) == 2) {
+            const cudaError_t er = p.OFF == 1
+                                       ? launch_kernel<6, CodeT, 2, kDgradDB, 1, kDgradDB, 4>(tA3, tB3, a, out, st)
+                                       : launch_kernel<6, CodeT, 2, kDgradDB, 0, kDgradDB, 4>(tA3, tB3, a, out, st);
+            if (er != cudaSuccess) return 4;
+        }
         a.vor = 1;
         a.vexpect = 1;
     }
@@ -888,7 +900,8 @@ bool make_bwd_plan(const PositFmt& ff, const PositFmt& fb, const PositFmt& fg, c
     *b = BwdPlan{};
     int DA = 0, OFF = 0;
     b->use_saved = saved && saved_usable(ff, fg, &DA, &OFF);
-    if (!make_plan(2, fg, g, raw, &b->pw, b->use_saved ? DA : 0, b->use_saved ? OFF : 0)) return false;
+    if (!make_plan(2, fg, g, raw, &b->pw, b->use_saved ? DA : 0, b->use_saved ? OFF : 0, b->use_saved))
+        return false;
     // x / dy codes of another format are digitised through a conversion LUT
     if (!b->use_saved && !same_fmt(ff, fg) && ff.nbits > kActLutBits) return false;
     if (!same_fmt(fb, fg) && fb.nbits > kActLutBits) return false;

@@ -319,3 +319,39 @@ def test_fwd_reduced_digits(cuda, po, wide, shape):
     if N * H * W <= 128:
         want = po.conv2d(8, 1, xa, wa, ba, 1, pad)
         assert (host(y).reshape(want.shape) == want).all()
+
+
+@pytest.mark.parametrize("wide", ["none", "x", "dy", "w"])
+def test_uniform_121_reduced_digits(cuda, wide):
+    """Uniform posit(12,1) layer (BASELINE config 4): forward and weight gradient
+    take the 3-digit variants for narrow values (same-format saved digits, no
+    offset); one wide value selects the full kernels.  Against the explicit /
+    per-pass paths."""
+    from paper_2105_00053_b200 import codec
+    N, C, H, W, F, K, pad = 2, 32, 16, 16, 64, 3, 1
+    rng = np.random.default_rng(31)
+    x64 = np.abs(rng.normal(0, 1.0, (N, C, H, W)))
+    w64 = rng.normal(0, 0.2, (F, C, K, K))
+    dy64 = rng.normal(0, 0.01, (N, F, H, W))
+    if wide == "x":
+        x64[1, 3, 4, 5] = 100.0
+    if wide == "w":
+        w64[0, 0, 1, 1] = -100.0
+    if wide == "dy":
+        dy64[0, 2, 3, 3] = 50.0
+    x, w, dy = (codec.from_float64_device(a, ops.P121) for a in (x64, w64, dy64))
+    b = codec.from_float64_device(rng.normal(0, 0.1, F), ops.P121)
+    n = ops.conv2d_saved_bytes(P121, x.shape, w.shape, 1, pad)
+    saved = torch.empty(n, dtype=torch.uint8, device="cuda")
+    y = ops.conv2d_fwd_save(P121, x, w, b, 1, pad, saved)
+    prev = ops.conv_algo(1)
+    try:
+        yref = ops.conv2d(P121, x, w, b, 1, pad)
+        dwref = ops.conv2d_weight_grad(P121, dy, x, w.shape, 1, pad)
+        dxref = ops.conv2d_input_grad(P121, dy, w, x.shape, 1, pad)
+    finally:
+        ops.conv_algo(prev)
+    assert torch.equal(y, yref)
+    dx, dw = ops.conv2d_backward(P121, P121, P121, dy, x, saved, w, x.shape, w.shape, 1, pad, True)
+    assert torch.equal(dw, dwref)
+    assert torch.equal(dx, dxref)
