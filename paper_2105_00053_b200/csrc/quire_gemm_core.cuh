@@ -62,15 +62,20 @@ constexpr int kEpiWarps = 8;      // epilogue warps (2 per TMEM lane quarter)
 constexpr int kThreads = 64 + 32 * kEpiWarps;  // producer + MMA + epilogue
 constexpr int kZeroBytes = kBM * 32;
 
-template <int D>
+// DR < D: the reduced-digit variant -- operands use only their first DR digit
+// planes (every value within DR balanced digits, flags from the pack kernels);
+// the packed images keep D planes per chunk (IMG_*), stages hold DR.
+template <int D, int DR = D>
 struct Geometry {
     static constexpr int NT = TileCfg<D>::NT;
     static constexpr int KB = TileCfg<D>::KB;
-    static constexpr int STAGES = TileCfg<D>::STAGES;
-    static constexpr int G = 2 * D - 1;
-    static constexpr int NMMA = D * NT;
-    static constexpr int A_BYTES = D * kBM * KB;
-    static constexpr int B_BYTES = D * NT * KB;
+    static constexpr int STAGES = TileCfg<D>::STAGES * D / DR > 12 ? 12 : TileCfg<D>::STAGES * D / DR;
+    static constexpr int G = 2 * DR - 1;
+    static constexpr int NMMA = DR * NT;
+    static constexpr int A_BYTES = DR * kBM * KB;
+    static constexpr int B_BYTES = DR * NT * KB;
+    static constexpr int IMG_A = D * kBM * KB;  // packed chunk strides in the workspace
+    static constexpr int IMG_B = D * NT * KB;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
     static constexpr int SMEM = STAGES * STAGE_BYTES + kZeroBytes + 256;
     static_assert((NT / 2) % 8 == 0, "epilogue column split");
@@ -150,7 +155,9 @@ __global__ void __launch_bounds__(256) pack_kernel(Fetch fetch, int64_t rows_tot
                                                    int8_t* __restrict__ img,
                                                    uint8_t* __restrict__ nar_flags,
                                                    uint8_t* __restrict__ any_nar_flag, int64_t tiles,
-                                                   int64_t kbt, const uint2* __restrict__ glut) {
+                                                   int64_t kbt, const uint2* __restrict__ glut,
+                                                   uint8_t* __restrict__ wide_flag = nullptr,
+                                                   int wide_planes = 0) {
     constexpr int KB = Geometry<D>::KB;
     constexpr int KC = KB / 16;
     // k-blocks per pass, so that every thread owns at least one 16-code unit
@@ -290,6 +297,13 @@ __global__ void __launch_bounds__(256) pack_kernel(Fetch fetch, int64_t rows_tot
             if (any_nar && r0 + r < rows_total) {
                 nar_flags[r0 + r] = 1;
                 *any_nar_flag = 1;
+            }
+            if (wide_flag != nullptr) {  // a digit plane >= wide_planes in use
+                uint32_t o = 0;
+#pragma unroll
+                for (int j = 0; j < 16; ++j)
+                    o |= uint32_t(((uint64_t(hi[j]) << 32 | lo[j]) >> (8 * wide_planes)) != 0);
+                if (o) *wide_flag = 1;
             }
             int8_t* chunk = img + (t * kbt + kb0 + kbl) * int64_t(D * ROWS * KB);
 #pragma unroll
@@ -468,19 +482,25 @@ __device__ __forceinline__ void tile_coords(int64_t t64, int64_t mtiles64, int64
 // issuer, warps 2..9 = epilogue (2 warps per TMEM lane quarter, each owning
 // half of the tile's columns).  The epilogue drains TMEM into registers,
 // releases it (tmem_empty), and rounds/stores while the next tile's MMAs run.
-template <int D, int QW, typename CodeT, bool kPair, int FMT = 0>
+template <int D, int QW, typename CodeT, bool kPair, int FMT = 0, int DR = D>
 __global__ void __launch_bounds__(kThreads, 1)
     quire_gemm_tc_kernel(const int8_t* __restrict__ a_img, const int8_t* __restrict__ b_img,
                          int64_t kbt, int64_t kb_per_split, const uint8_t* __restrict__ row_nar,
                          const uint8_t* __restrict__ col_nar, OutMap<CodeT> out, int64_t M,
                          int64_t N, PositFmt f_arg,
                          unsigned __int128* __restrict__ partial, int64_t mtiles, int64_t ntiles,
-                         int64_t splits) {
+                         int64_t splits, const uint8_t* __restrict__ vflags = nullptr, int vmode = 0) {
+    // device-selected variant (vflags = {A wide, B wide} from the pack kernels):
+    // vmode 1 runs iff neither operand is wide, 2 iff either is; exit at once otherwise
+    if (vmode != 0) {
+        const bool wide = vflags[0] != 0 || vflags[1] != 0;
+        if (wide != (vmode == 2)) return;
+    }
     // kPair: clusters of 2 CTAs run one M=256 tcgen05.mma.cta_group::2 per
     // digit plane; each CTA stages its own 128-row A tile and HALF of the
     // concatenated B rows, halving each SM's shared-memory operand traffic.
     const PositFmt f = fixed_fmt<FMT>(f_arg);  // compile-time for the BASELINE formats
-    using Geo = Geometry<D>;
+    using Geo = Geometry<D, DR>;
     using QT = typename QuireWord<QW>::T;
     constexpr int NT = Geo::NT, KB = Geo::KB, STAGES = Geo::STAGES, G = Geo::G;
     constexpr int COLS = NT / 2;                 // columns per epilogue thread
@@ -538,8 +558,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int64_t mt = kPair ? 2 * um + rank : um;
                 const int64_t kb0 = split * kb_per_split;
                 const int nkb = int(min(kbt, kb0 + kb_per_split) - kb0);
-                const int8_t* a_src = a_img + (mt * kbt + kb0) * int64_t(Geo::A_BYTES);
-                const int8_t* b_src = b_img + (nt * kbt + kb0) * int64_t(Geo::B_BYTES) +
+                const int8_t* a_src = a_img + (mt * kbt + kb0) * int64_t(Geo::IMG_A);
+                const int8_t* b_src = b_img + (nt * kbt + kb0) * int64_t(Geo::IMG_B) +
                                       (kPair ? rank * B_LOCAL : 0);
                 for (int i = 0; i < nkb; ++i, ++it) {
                     const int s = it % STAGES;
@@ -547,8 +567,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     ptx::mbar_wait(&empty[s], ph ^ 1);
                     uint8_t* sa = smem + s * Geo::STAGE_BYTES;
                     ptx::mbar_arrive_expect_tx(&full[s], STAGE_TX);
-                    ptx::bulk_g2s(sa, a_src + int64_t(i) * Geo::A_BYTES, Geo::A_BYTES, &full[s]);
-                    ptx::bulk_g2s(sa + Geo::A_BYTES, b_src + int64_t(i) * Geo::B_BYTES, B_LOCAL,
+                    ptx::bulk_g2s(sa, a_src + int64_t(i) * Geo::IMG_A, Geo::A_BYTES, &full[s]);
+                    ptx::bulk_g2s(sa + Geo::A_BYTES, b_src + int64_t(i) * Geo::IMG_B, B_LOCAL,
                                   &full[s]);
                 }
             }
@@ -593,12 +613,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                     for (int ks = 0; ks < KB / 32; ++ks) {
                         const uint64_t bdesc = ptx::smem_desc_kmajor(b_base + ks * 256, LBO, SBO);
                         const bool first = (i == 0 && ks == 0);
-                        if (first) {  // zero groups D-1 .. 2D-2 (plane 0 initialises 0 .. D-1)
-                            if constexpr (kPair) ptx::mma_i8_pair(tmem + (D - 1) * NT, zdesc, bdesc, idesc, 0);
-                            else ptx::mma_i8(tmem + (D - 1) * NT, zdesc, bdesc, idesc, 0);
+                        if (first) {  // zero groups DR-1 .. 2DR-2 (plane 0 initialises 0 .. DR-1)
+                            if constexpr (kPair) ptx::mma_i8_pair(tmem + (DR - 1) * NT, zdesc, bdesc, idesc, 0);
+                            else ptx::mma_i8(tmem + (DR - 1) * NT, zdesc, bdesc, idesc, 0);
                         }
 #pragma unroll
-                        for (int p = 0; p < D; ++p) {
+                        for (int p = 0; p < DR; ++p) {
                             const uint64_t adesc = ptx::smem_desc_kmajor(
                                 a_base + p * (kBM * KB) + ks * 256, LBO, SBO);
                             if constexpr (kPair)
@@ -956,15 +976,19 @@ cudaError_t launch_generic(const QuireGemmPlan& p, const GemmArgs& g, FA fa, FB 
     // 2^16-entry digit table (glut) measured slower for posit(16,1) (L2-latency
     // bound lookups: 176 vs 133 us for the 4096^2 pair of packs).
     const uint2* glut = nullptr;
+    // reduced-digit variant (posit(12,1)-class D = 6 operands within 3 digits):
+    // the packs flag wide operands in flags[2], flags[3]
+    constexpr int kRed = 3;
+    const bool reduced = D == 6 && !p.pair && sizeof(CodeT) == 2;
     pack_kernel<D, kBM, CodeT, FA><<<int(a_work < 148 * 8 ? a_work : 148 * 8), 256, 0, st>>>(
-        fa, g.M, g.K, f, a_img, rnar, flags, p.mtiles_alloc, p.kbt, glut);
+        fa, g.M, g.K, f, a_img, rnar, flags, p.mtiles_alloc, p.kbt, glut, reduced ? flags + 2 : nullptr, kRed);
     pack_kernel<D, Geo::NT, CodeT, FB><<<int(b_work < 148 * 8 ? b_work : 148 * 8), 256, 0, st>>>(
-        fb, g.N, g.K, f, b_img, cnar, flags + 1, p.ntiles, p.kbt, glut);
+        fb, g.N, g.K, f, b_img, cnar, flags + 1, p.ntiles, p.kbt, glut, reduced ? flags + 3 : nullptr, kRed);
     if (stats) cudaEventRecord(stats->ev[1], st);
     // D <= 3 implies R <= 11, hence W <= 64: no 128-bit instantiation needed.
     using KernFn = void (*)(const int8_t*, const int8_t*, int64_t, int64_t, const uint8_t*,
                             const uint8_t*, OutMap<CodeT>, int64_t, int64_t, PositFmt,
-                            unsigned __int128*, int64_t, int64_t, int64_t);
+                            unsigned __int128*, int64_t, int64_t, int64_t, const uint8_t*, int);
     KernFn kern;
     if (p.pair) {
         if constexpr (D <= 3)
@@ -1013,13 +1037,27 @@ cudaError_t launch_generic(const QuireGemmPlan& p, const GemmArgs& g, FA fa, FB 
         cfg.numAttrs = 1;
         if ((e = cudaLaunchKernelEx(&cfg, kern, (const int8_t*)a_img, (const int8_t*)b_img, p.kbt,
                                     p.kb_per_split, rn, cn, out, g.M, g.N, f, partial, p.mtiles,
-                                    p.ntiles, p.splits)) != cudaSuccess)
+                                    p.ntiles, p.splits, (const uint8_t*)nullptr, 0)) != cudaSuccess)
             return e;
     } else {
         const int64_t tiles = p.mtiles * p.ntiles * p.splits;
         const int grid = int(tiles < num_sms() ? tiles : num_sms());
+        if constexpr (D == 6 && sizeof(CodeT) == 2) {
+            if (reduced) {  // both launched; the pack flags let exactly one run
+                using GR = Geometry<6, kRed>;
+                // (128-bit word: this epilogue's quire_word_to_posit_bf takes W <= word bits)
+                KernFn kr = fixed_fmt_id(f) == 3 ? quire_gemm_tc_kernel<6, 4, CodeT, false, 3, kRed>
+                                                 : quire_gemm_tc_kernel<6, 4, CodeT, false, 0, kRed>;
+                if ((e = cudaFuncSetAttribute(kr, cudaFuncAttributeMaxDynamicSharedMemorySize, GR::SMEM)) !=
+                    cudaSuccess)
+                    return e;
+                kr<<<grid, kThreads, GR::SMEM, st>>>(a_img, b_img, p.kbt, p.kb_per_split, rn, cn, out, g.M,
+                                                     g.N, f, partial, p.mtiles, p.ntiles, p.splits, flags + 2, 1);
+            }
+        }
         kern<<<grid, kThreads, Geo::SMEM, st>>>(a_img, b_img, p.kbt, p.kb_per_split, rn, cn, out,
-                                                g.M, g.N, f, partial, p.mtiles, p.ntiles, p.splits);
+                                                g.M, g.N, f, partial, p.mtiles, p.ntiles, p.splits,
+                                                reduced ? flags + 2 : nullptr, reduced ? 2 : 0);
     }
     if (stats) cudaEventRecord(stats->ev[2], st);
     if (use_partial) {

@@ -355,3 +355,22 @@ def test_uniform_121_reduced_digits(cuda, wide):
     dx, dw = ops.conv2d_backward(P121, P121, P121, dy, x, saved, w, x.shape, w.shape, 1, pad, True)
     assert torch.equal(dw, dwref)
     assert torch.equal(dx, dxref)
+
+
+@pytest.mark.parametrize("wide", ["none", "A", "B"])
+@pytest.mark.parametrize("shape", [(256, 512, 384), (130, 4096, 96)])
+def test_gemm_reduced_digits(cuda, po, wide, shape):
+    """Explicit quire GEMM in posit(12,1) (the Linear layers' path) with values
+    within 3 digits takes the device-selected 3 x 3 digit kernel; one wide value
+    selects the full kernel.  Against the oracle."""
+    M, K, N = shape
+    rng = np.random.default_rng(37)
+    A = np.array([po.from_float64(12, 1, float(v)) for v in rng.normal(0, 0.5, M * K)], np.uint64).reshape(M, K)
+    B = np.array([po.from_float64(12, 1, float(v)) for v in rng.normal(0, 0.05, K * N)], np.uint64).reshape(K, N)
+    if wide == "A":
+        A[3, 7] = po.from_float64(12, 1, 300.0)
+    if wide == "B":
+        B[5, 1] = po.from_float64(12, 1, -300.0)
+    got = ops.quire_gemm(P121, dev(P121, A), dev(P121, B))
+    want = po.matmul(12, 1, A, B)
+    assert (host(got) == want).all()
