@@ -80,6 +80,10 @@ int pnn_matmul_host(int nbits, int es, const uint64_t* A, const uint64_t* B, uin
  * (ineligible shapes fail with PNN_EUNSUPPORTED).  Returns the previous
  * setting, or -1 for an invalid value.  Query the workspace after setting. */
 int pnn_conv_algo(int algo);
+/* Reduced-digit GEMM variants (flag-selected 3/4-digit kernels) are
+ * launched for passes of at least `macs` posit MACs (default 2^27); returns the
+ * previous threshold (macs < 0: query only).  Results never depend on it. */
+int64_t pnn_variant_min_work(int64_t macs);
 int pnn_conv2d_workspace(int pass, int nbits, int es, int64_t N, int64_t C, int64_t H, int64_t W,
                          int64_t F, int64_t KH, int64_t KW, int stride, int pad, int has_bias,
                          size_t* bytes);

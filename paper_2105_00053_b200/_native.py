@@ -72,6 +72,7 @@ _SIGS = {
                                   [_i64] * 7 + [C.c_int, C.c_int, _vp, _vp, _vp, _vp, _vp, C.c_size_t, _vp]),
     "pnn_bias_grad_gated": (C.c_int, [C.c_int, C.c_int, _vp, C.c_int, _vp, _i64, _i64, _i64, _vp, _vp, _vp,
                                       _vp, C.c_size_t, _vp]),
+    "pnn_variant_min_work": (C.c_int64, [C.c_int64]),
     "pnn_sgd_step_multi": (C.c_int, [C.c_int] * 4 + [C.c_uint32] + [C.c_int] * 6 +
                            [_vp, _vp, _vp, _vp, _vp, _vp]),
     "pnn_maxpool2d_relu_bwd_x": (C.c_int, [C.c_int, C.c_int, _vp, C.c_int, C.c_int, _vp] + [_i64] * 4 +

@@ -14,6 +14,13 @@
 namespace pnn_b200 {
 
 static int g_conv_algo = 0;
+static int64_t g_variant_min_work = int64_t(1) << 27;  // MACs below which no reduced variant launches
+int64_t variant_min_work() { return g_variant_min_work; }
+int64_t set_variant_min_work(int64_t v) {
+    const int64_t prev = g_variant_min_work;
+    g_variant_min_work = v;
+    return prev;
+}
 int conv_algo() { return g_conv_algo; }
 int set_conv_algo(int a) {
     const int prev = g_conv_algo;
@@ -196,8 +203,9 @@ bool make_plan(int pass, const PositFmt& f, const ConvGeom& g_real, bool raw, Im
     // CTAs in flight: two per SM for the two-CTA kernels -- including the weight
     // gradient's reduced-digit variant (saved (8,1) digits under (12,1)), which
     // needs the second CTA's stages to keep enough TMA boxes in flight
-    const bool wg_pair = pass == 2 && saved_x && D == 6 &&
-                         ((p->DA == 4 && p->OFF == 1) || (p->DA == 6 && p->OFF == 0));
+    const bool wg_pair = pass == 2 && saved_x &&
+                         ((D == 6 && ((p->DA == 4 && p->OFF == 1) || (p->DA == 6 && p->OFF == 0))) ||
+                          (D == 8 && p->DA == 8 && p->OFF == 0));
     const int64_t kbps = split_kblocks(a.kbt, cap < 1 ? 1 : cap, a.mtiles * a.ntiles,
                                        num_sms() * (((pass == 2 && !wg_pair) || (pass != 2 && D >= 5)) ? 1 : 2));
     a.kb_per_split = a.kbt < kbps ? a.kbt : kbps;
@@ -396,7 +404,12 @@ cudaError_t dispatch(int D, const CUtensorMap& tA, const CUtensorMap& tB, const 
 // the weight digitiser's flag selects it on the device (both variants are
 // launched, the other exits at once), so no host round trip is needed.
 constexpr int kDgradDB = 3;
-bool dgrad_reduced(int D) { return D == 6; }
+// digit planes of the reduced variants: 3 (posit(8,1) / posit(12,1) classes),
+// 4 for the 8-digit posit(16,1) class (|X| < 2^31: |v| < 8)
+inline int red_planes(int D) { return D == 8 ? 4 : kDgradDB; }
+bool dgrad_reduced(int D) { return D == 6 || D == 8; }
+// the variants cost an extra (exiting) launch: only for passes with real work
+inline bool variant_worthy(const IgemmArgs& a) { return a.M * a.N * a.kbt * kIKB >= variant_min_work(); }
 
 template <typename CodeT>
 cudaError_t dispatch_dgrad_reduced(int D, const CUtensorMap& tA, const CUtensorMap& tB, const IgemmArgs& a,
@@ -635,27 +648,29 @@ int run_fwd(const ImplPlan& p, const ConvGeom& g, const CodeT* x, const CodeT* w
     uint8_t* xwide = sv ? sv->flag + 1 : flags + 3;
     if (p.fold)
         e = im2col_digits(p.D, x, g, f, f, lut_of(p, ws, f), adig, pos_nar, sv ? sv->chw : nullptr, xflag, st,
-                          xwide, kDgradDB);
+                          xwide, red_planes(p.D));
     else
         e = act_digits(p.D, x, g.N, g.C, g.H, g.W, p.Ca, g.pad, f, f, lut_of(p, ws, f), true, adig,
-                       pos_nar, sv ? sv->chw : nullptr, nullptr, xflag, st, DigitGate{}, xwide, kDgradDB);
+                       pos_nar, sv ? sv->chw : nullptr, nullptr, xflag, st, DigitGate{}, xwide, red_planes(p.D));
     if (e != cudaSuccess) return 4;
     const int64_t taps = gv.KH * gv.KW;  // weights: [F][C*KH*KW] read as [F][ckk][1][1] if folded
     // reduced-digit variant (posit(8,1) / posit(12,1): x and w within 3 balanced digits)
-    const bool reduced = (p.D == 4 && sizeof(CodeT) == 1) || (p.D == 6 && sizeof(CodeT) == 2);
+    const bool reduced = ((p.D == 4 && sizeof(CodeT) == 1) ||
+                          ((p.D == 6 || p.D == 8) && sizeof(CodeT) == 2)) && variant_worthy(p.a);
+    const int RP = red_planes(p.D);
     uint8_t* wwide = flags + 2;
     if ((e = weight_digits<CodeT>(p.D, w, bias, g.F, p.fold ? p.ckk : g.C, taps, p.Kp, 0, f, bdig,
-                                  col_add, col_nar, flags + 1, st, reduced ? wwide : nullptr, kDgradDB)) !=
+                                  col_add, col_nar, flags + 1, st, reduced ? wwide : nullptr, RP)) !=
         cudaSuccess)
         return 4;
     CUtensorMap tA, tB, tA3, tB3;
     uint32_t boxA3[5];
     for (int i = 0; i < 5; ++i) boxA3[i] = p.boxA[i];
-    boxA3[4] = kDgradDB;
+    boxA3[4] = RP;
     if (!map_act(&tA, adig, p.D, gv.N, p.Ha, p.Wa, p.Ca, p.boxA) ||
         !map_weights(&tB, bdig, p.D, p.brows, taps * p.Kp, p.NT) ||
         (reduced && (!map_act(&tA3, adig, p.D, gv.N, p.Ha, p.Wa, p.Ca, boxA3) ||
-                     !map_weights(&tB3, bdig, p.D, p.brows, taps * p.Kp, p.NT, kDgradDB))))
+                     !map_weights(&tB3, bdig, p.D, p.brows, taps * p.Kp, p.NT, RP))))
         return 5;
     IgemmArgs a = p.a;
     a.col_add = bias ? col_add : nullptr;
@@ -672,10 +687,14 @@ int run_fwd(const ImplPlan& p, const ConvGeom& g, const CodeT* x, const CodeT* w
         if constexpr (sizeof(CodeT) == 1)
             if ((e = launch_kernel<4, CodeT, 0, kDgradDB, 0, kDgradDB>(tA3, tB3, a, out, st)) != cudaSuccess)
                 return 4;
-        if constexpr (sizeof(CodeT) == 2) {  // 64-bit quire word when a single chunk's exact sum fits
-            const bool narrow_word = a.splits == 1 && a.kb_per_split * kIKB < (int64_t(1) << 17);
-            e = narrow_word ? launch_kernel<6, CodeT, 0, kDgradDB, 0, kDgradDB, 2>(tA3, tB3, a, out, st)
-                            : launch_kernel<6, CodeT, 0, kDgradDB, 0, kDgradDB, 4>(tA3, tB3, a, out, st);
+        if constexpr (sizeof(CodeT) == 2) {
+            if (p.D == 6) {  // 64-bit quire word when a single chunk's exact sum fits
+                const bool narrow_word = a.splits == 1 && a.kb_per_split * kIKB < (int64_t(1) << 17);
+                e = narrow_word ? launch_kernel<6, CodeT, 0, kDgradDB, 0, kDgradDB, 2>(tA3, tB3, a, out, st)
+                                : launch_kernel<6, CodeT, 0, kDgradDB, 0, kDgradDB, 4>(tA3, tB3, a, out, st);
+            } else {
+                e = launch_kernel<8, CodeT, 0, 4, 0, 4, 4>(tA3, tB3, a, out, st);
+            }
             if (e != cudaSuccess) return 4;
         }
         a.vor = 1;
@@ -714,10 +733,11 @@ int run_dgrad(const ImplPlan& p, const ConvGeom& g, const CodeT* dy, const CodeT
     uint8_t* flags = ws + p.off_flags;
     // (with pre, the caller cleared the maps before dy's digitiser filled pos_nar)
     if (pre == nullptr && cudaMemsetAsync(ws + p.off_maps, 0, p.maps_bytes, st) != cudaSuccess) return 4;
-    const bool reduced = dgrad_reduced(p.D) && sizeof(CodeT) == 2;
+    const bool reduced = dgrad_reduced(p.D) && sizeof(CodeT) == 2 && variant_worthy(p.a);
+    const int RP = red_planes(p.D);
     if (pre == nullptr &&
         act_digits(p.D, dy, g.N, g.F, g.OH, g.OW, p.Ca, 0, f, f, lut_of(p, ws, f), true, adig, pos_nar,
-                   nullptr, nullptr, flags, st, gt, reduced ? flags + 3 : nullptr, kDgradDB, reduced) != cudaSuccess)
+                   nullptr, nullptr, flags, st, gt, reduced ? flags + 3 : nullptr, RP, reduced) != cudaSuccess)
         return 4;
     const int8_t* a_dig = pre ? pre->dig : adig;
     const uint8_t* a_pos = pre ? pre->pos_nar : pos_nar;
@@ -726,7 +746,7 @@ int run_dgrad(const ImplPlan& p, const ConvGeom& g, const CodeT* dy, const CodeT
     const int64_t taps = g.KH * g.KW;
     uint8_t* wide = flags + 2;  // weights need more than kDgradDB digit planes
     if (weight_digits<CodeT>(p.D, w, nullptr, g.F, g.C, taps, p.Kp, 1, f, bdig, nullptr, nullptr,
-                             flags + 1, st, reduced ? wide : nullptr, kDgradDB) != cudaSuccess)
+                             flags + 1, st, reduced ? wide : nullptr, RP) != cudaSuccess)
         return 4;
     // dy's digits were stored without the high planes (narrow dy): the full
     // variant, selected by wide weights, reads them -- complete dy then
@@ -738,10 +758,10 @@ int run_dgrad(const ImplPlan& p, const ConvGeom& g, const CodeT* dy, const CodeT
     CUtensorMap tA, tA3, tB, tB3;
     uint32_t box3[5];
     for (int i = 0; i < 5; ++i) box3[i] = p.boxA[i];
-    box3[4] = kDgradDB;  // A box of the 3-plane variant: planes 0..2 of dy's digits
+    box3[4] = RP;  // A box of the reduced variant: dy's low digit planes
     if (!map_act(&tA, const_cast<int8_t*>(a_dig), p.D, g.N, g.OH, g.OW, p.Ca, p.boxA) ||
         !map_weights(&tB, bdig, p.D, p.brows, taps * p.Kp, p.NT) ||
-        (reduced && !map_weights(&tB3, bdig, p.D, p.brows, taps * p.Kp, p.NT, kDgradDB)) ||
+        (reduced && !map_weights(&tB3, bdig, p.D, p.brows, taps * p.Kp, p.NT, RP)) ||
         (reduced && dy_wide && !map_act(&tA3, const_cast<int8_t*>(a_dig), p.D, g.N, g.OH, g.OW, p.Ca, box3)))
         return 5;
     IgemmArgs a = p.a;
@@ -750,7 +770,7 @@ int run_dgrad(const ImplPlan& p, const ConvGeom& g, const CodeT* dy, const CodeT
     const bool use_partial = a.splits > 1;
     a.partial = use_partial ? reinterpret_cast<unsigned __int128*>(ws + p.off_partial) : nullptr;
     const OutMap<CodeT> out = out_nchw<CodeT>(dx, g.H * g.W, g.C);
-    if (reduced) {  // all variants launched; the digitisers' flags let exactly one run
+    if (reduced && p.D == 6) {  // all variants launched; the digitisers' flags let exactly one run
         a.vflag = wide;  // weights need more than 3 planes?
         a.vexpect = 0;
         if (dy_wide) {
@@ -762,6 +782,14 @@ int run_dgrad(const ImplPlan& p, const ConvGeom& g, const CodeT* dy, const CodeT
         }
         if (dispatch_dgrad_reduced<CodeT>(p.D, tA, tB3, a, out, st) != cudaSuccess) return 4;
         a.vflag2 = nullptr;
+        a.vexpect = 1;
+    } else if (reduced && dy_wide) {  // posit(16,1) class: 4 x 4 digits or the full kernel
+        a.vflag = wide;
+        a.vflag2 = dy_wide;
+        a.vexpect = a.vexpect2 = 0;
+        if constexpr (sizeof(CodeT) == 2)
+            if (launch_kernel<8, CodeT, 1, 4, 0, 4, 4>(tA3, tB3, a, out, st) != cudaSuccess) return 4;
+        a.vor = 1;
         a.vexpect = 1;
     }
     if (dispatch<CodeT, 1>(p.D, tA, tB, a, out, st) != cudaSuccess) return 4;
@@ -807,15 +835,18 @@ int run_wgrad(const ImplPlan& p, const ConvGeom& g, const void* dy, const PositF
     }
     // reduced-digit variant: saved (8,1)-format x one digit up, both operands in 3 planes
     // ((8,1) saved digits one digit up, or same-format (12,1) saved digits)
-    const bool reduced = sv != nullptr && sizeof(CodeT) == 2 && p.D == 6 &&
-                         ((p.DA == 4 && p.OFF == 1) || (p.DA == 6 && p.OFF == 0));
+    const bool reduced = sv != nullptr && sizeof(CodeT) == 2 &&
+                         ((p.D == 6 && ((p.DA == 4 && p.OFF == 1) || (p.DA == 6 && p.OFF == 0))) ||
+                          (p.D == 8 && p.DA == 8 && p.OFF == 0)) &&
+                         variant_worthy(p.a);
+    const int RP = red_planes(p.D);
     if (reduced && dy_wide == nullptr) dy_wide = flags + 3;
     // dy's high digit planes only when used: every consumer (this pass, and the
     // input gradient sharing the digits) is a flag-selected variant
     const bool reduce_dy = reduced && (share_pos_nar == nullptr || share_gated);
     // (the full weight-gradient variant also runs when x alone is wide: complete dy then too)
     if (act_digits(p.D, dy, g.N, g.F, g.OH, g.OW, p.Fpw, 0, f, fdy, lut_of(p, ws, fdy, 1), true, bdig,
-                   share_pos_nar, nullptr, col_nar, flags + 1, st, gt, dy_wide, kDgradDB, reduce_dy,
+                   share_pos_nar, nullptr, col_nar, flags + 1, st, gt, dy_wide, RP, reduce_dy,
                    reduced ? sv->flag + 1 : nullptr) != cudaSuccess)
         return 4;
     CUtensorMap tA, tB, tA3, tB3;
@@ -826,7 +857,7 @@ int run_wgrad(const ImplPlan& p, const ConvGeom& g, const void* dy, const PositF
         boxA3[i] = p.boxA[i];
         boxB3[i] = boxB[i];
     }
-    boxA3[4] = boxB3[4] = kDgradDB;
+    boxA3[4] = boxB3[4] = RP;
     if (!map_wgrad_x(&tA, adig, p.DA, gv.N, p.Ha, p.Wa, p.Ca, p.boxA) ||
         !map_act(&tB, bdig, p.D, g.N, g.OH, g.OW, p.Fpw, boxB) ||
         (reduced && (!map_wgrad_x(&tA3, adig, p.DA, gv.N, p.Ha, p.Wa, p.Ca, boxA3) ||
@@ -851,9 +882,10 @@ int run_wgrad(const ImplPlan& p, const ConvGeom& g, const void* dy, const PositF
         a.vflag2 = dy_wide;
         a.vexpect = a.vexpect2 = 0;
         if constexpr (sizeof(CodeT) == 2) {
-            const cudaError_t er = p.OFF == 1
-                                       ? launch_kernel<6, CodeT, 2, kDgradDB, 1, kDgradDB, 4>(tA3, tB3, a, out, st)
-                                       : launch_kernel<6, CodeT, 2, kDgradDB, 0, kDgradDB, 4>(tA3, tB3, a, out, st);
+            const cudaError_t er =
+                p.D == 8 ? launch_kernel<8, CodeT, 2, 4, 0, 4, 4>(tA3, tB3, a, out, st)
+                : p.OFF == 1 ? launch_kernel<6, CodeT, 2, kDgradDB, 1, kDgradDB, 4>(tA3, tB3, a, out, st)
+                             : launch_kernel<6, CodeT, 2, kDgradDB, 0, kDgradDB, 4>(tA3, tB3, a, out, st);
             if (er != cudaSuccess) return 4;
         }
         a.vor = 1;
@@ -922,7 +954,7 @@ int run_backward(const BwdPlan& b, const ConvGeom& g, const PositFmt& ff, const 
     uint8_t* wsd = ws + b.off_d;
     if (b.share_dy && cudaMemsetAsync(wsd + b.pd.off_maps, 0, b.pd.maps_bytes, st) != cudaSuccess) return 4;
     uint8_t* dy_wide = b.share_dy ? wsd + b.pd.off_flags + 3 : nullptr;  // cleared with the dgrad maps
-    const bool dgrad_gated = dgrad_reduced(b.pd.D) && sizeof(BT) == 2;
+    const bool dgrad_gated = dgrad_reduced(b.pd.D) && sizeof(BT) == 2 && variant_worthy(b.pd.a);
     int rc = run_wgrad<GT>(b.pw, g, dy, fb, x, ff, static_cast<GT*>(dw), raw_words, raw_nar, ws, st,
                            b.use_saved ? sv : nullptr,
                            b.share_dy ? wsd + b.pd.off_pos_nar : nullptr, gt, dy_wide, dgrad_gated);
@@ -1049,6 +1081,10 @@ int igemm_conv_backward(const PositFmt& ff, const PositFmt& fb, const PositFmt& 
 }
 
 }  // namespace pnn_b200
+
+extern "C" int64_t pnn_variant_min_work(int64_t macs) {
+    return macs < 0 ? pnn_b200::variant_min_work() : pnn_b200::set_variant_min_work(macs);
+}
 
 extern "C" int pnn_conv_algo(int algo) {
     if (algo < 0 || algo > 2) return -1;

@@ -18,6 +18,8 @@ struct ConvGeom {
 // Conv algorithm selection (pnn_conv_algo): 0 auto (implicit where eligible),
 // 1 always the explicit pack path, 2 implicit only (ineligible -> error).
 int conv_algo();
+int64_t variant_min_work();
+int64_t set_variant_min_work(int64_t v);
 
 // Whether pass (0 fwd, 1 input grad, 2 weight grad) runs implicitly for this
 // geometry / format under the current algorithm setting; *bytes = workspace.

@@ -809,6 +809,7 @@ __global__ void __launch_bounds__(256) quire_finalize_warp_kernel(
 }
 
 inline int grid_for(int64_t items, int threads);
+int64_t variant_min_work();  // igemm.cu: work (MACs) below which no reduced-digit variant launches
 
 // split-K finalize: the variant by shape
 template <typename CodeT>
@@ -978,8 +979,9 @@ cudaError_t launch_generic(const QuireGemmPlan& p, const GemmArgs& g, FA fa, FB 
     const uint2* glut = nullptr;
     // reduced-digit variant (posit(12,1)-class D = 6 operands within 3 digits):
     // the packs flag wide operands in flags[2], flags[3]
-    constexpr int kRed = 3;
-    const bool reduced = D == 6 && !p.pair && sizeof(CodeT) == 2;
+    constexpr int kRed = D == 8 ? 4 : 3;
+    const bool reduced = (D == 6 || D == 8) && !p.pair && sizeof(CodeT) == 2 &&
+                         g.M * g.N * g.K >= variant_min_work();  // the extra launch pays off
     pack_kernel<D, kBM, CodeT, FA><<<int(a_work < 148 * 8 ? a_work : 148 * 8), 256, 0, st>>>(
         fa, g.M, g.K, f, a_img, rnar, flags, p.mtiles_alloc, p.kbt, glut, reduced ? flags + 2 : nullptr, kRed);
     pack_kernel<D, Geo::NT, CodeT, FB><<<int(b_work < 148 * 8 ? b_work : 148 * 8), 256, 0, st>>>(
@@ -1042,12 +1044,13 @@ cudaError_t launch_generic(const QuireGemmPlan& p, const GemmArgs& g, FA fa, FB 
     } else {
         const int64_t tiles = p.mtiles * p.ntiles * p.splits;
         const int grid = int(tiles < num_sms() ? tiles : num_sms());
-        if constexpr (D == 6 && sizeof(CodeT) == 2) {
+        if constexpr ((D == 6 || D == 8) && sizeof(CodeT) == 2) {
             if (reduced) {  // both launched; the pack flags let exactly one run
-                using GR = Geometry<6, kRed>;
+                using GR = Geometry<D, kRed>;
                 // (128-bit word: this epilogue's quire_word_to_posit_bf takes W <= word bits)
-                KernFn kr = fixed_fmt_id(f) == 3 ? quire_gemm_tc_kernel<6, 4, CodeT, false, 3, kRed>
-                                                 : quire_gemm_tc_kernel<6, 4, CodeT, false, 0, kRed>;
+                constexpr int kFmt = D == 6 ? 3 : 4;
+                KernFn kr = fixed_fmt_id(f) == kFmt ? quire_gemm_tc_kernel<D, 4, CodeT, false, kFmt, kRed>
+                                                    : quire_gemm_tc_kernel<D, 4, CodeT, false, 0, kRed>;
                 if ((e = cudaFuncSetAttribute(kr, cudaFuncAttributeMaxDynamicSharedMemorySize, GR::SMEM)) !=
                     cudaSuccess)
                     return e;

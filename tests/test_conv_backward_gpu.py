@@ -17,6 +17,15 @@ from paper_2105_00053_b200 import ops
 
 pytestmark = pytest.mark.gpu
 
+
+@pytest.fixture(autouse=True)
+def all_variants():
+    """Launch the reduced-digit variants even for these small test problems."""
+    from paper_2105_00053_b200 import _native
+    prev = _native.lib().pnn_variant_min_work(0)
+    yield
+    _native.lib().pnn_variant_min_work(prev)
+
 P80, P81, P121, P161 = (8, 0), (8, 1), (12, 1), (16, 1)
 
 # (forward, backward, gradient) stage formats
@@ -321,8 +330,9 @@ def test_fwd_reduced_digits(cuda, po, wide, shape):
         assert (host(y).reshape(want.shape) == want).all()
 
 
+@pytest.mark.parametrize("cfg", [P121, P161])
 @pytest.mark.parametrize("wide", ["none", "x", "dy", "w"])
-def test_uniform_121_reduced_digits(cuda, wide):
+def test_uniform_121_reduced_digits(cuda, wide, cfg):
     """Uniform posit(12,1) layer (BASELINE config 4): forward and weight gradient
     take the 3-digit variants for narrow values (same-format saved digits, no
     offset); one wide value selects the full kernels.  Against the explicit /
@@ -339,38 +349,55 @@ def test_uniform_121_reduced_digits(cuda, wide):
         w64[0, 0, 1, 1] = -100.0
     if wide == "dy":
         dy64[0, 2, 3, 3] = 50.0
-    x, w, dy = (codec.from_float64_device(a, ops.P121) for a in (x64, w64, dy64))
-    b = codec.from_float64_device(rng.normal(0, 0.1, F), ops.P121)
-    n = ops.conv2d_saved_bytes(P121, x.shape, w.shape, 1, pad)
+    x, w, dy = (codec.from_float64_device(a, cfg) for a in (x64, w64, dy64))
+    b = codec.from_float64_device(rng.normal(0, 0.1, F), cfg)
+    n = ops.conv2d_saved_bytes(cfg, x.shape, w.shape, 1, pad)
     saved = torch.empty(n, dtype=torch.uint8, device="cuda")
-    y = ops.conv2d_fwd_save(P121, x, w, b, 1, pad, saved)
+    y = ops.conv2d_fwd_save(cfg, x, w, b, 1, pad, saved)
     prev = ops.conv_algo(1)
     try:
-        yref = ops.conv2d(P121, x, w, b, 1, pad)
-        dwref = ops.conv2d_weight_grad(P121, dy, x, w.shape, 1, pad)
-        dxref = ops.conv2d_input_grad(P121, dy, w, x.shape, 1, pad)
+        yref = ops.conv2d(cfg, x, w, b, 1, pad)
+        dwref = ops.conv2d_weight_grad(cfg, dy, x, w.shape, 1, pad)
+        dxref = ops.conv2d_input_grad(cfg, dy, w, x.shape, 1, pad)
     finally:
         ops.conv_algo(prev)
     assert torch.equal(y, yref)
-    dx, dw = ops.conv2d_backward(P121, P121, P121, dy, x, saved, w, x.shape, w.shape, 1, pad, True)
+    dx, dw = ops.conv2d_backward(cfg, cfg, cfg, dy, x, saved, w, x.shape, w.shape, 1, pad, True)
     assert torch.equal(dw, dwref)
     assert torch.equal(dx, dxref)
 
 
+@pytest.mark.parametrize("cfg", [P121, P161])
 @pytest.mark.parametrize("wide", ["none", "A", "B"])
 @pytest.mark.parametrize("shape", [(256, 512, 384), (130, 4096, 96)])
-def test_gemm_reduced_digits(cuda, po, wide, shape):
+def test_gemm_reduced_digits(cuda, po, wide, shape, cfg):
     """Explicit quire GEMM in posit(12,1) (the Linear layers' path) with values
     within 3 digits takes the device-selected 3 x 3 digit kernel; one wide value
     selects the full kernel.  Against the oracle."""
     M, K, N = shape
     rng = np.random.default_rng(37)
-    A = np.array([po.from_float64(12, 1, float(v)) for v in rng.normal(0, 0.5, M * K)], np.uint64).reshape(M, K)
-    B = np.array([po.from_float64(12, 1, float(v)) for v in rng.normal(0, 0.05, K * N)], np.uint64).reshape(K, N)
+    A = np.array([po.from_float64(cfg[0], cfg[1], float(v)) for v in rng.normal(0, 0.5, M * K)], np.uint64).reshape(M, K)
+    B = np.array([po.from_float64(cfg[0], cfg[1], float(v)) for v in rng.normal(0, 0.05, K * N)], np.uint64).reshape(K, N)
     if wide == "A":
-        A[3, 7] = po.from_float64(12, 1, 300.0)
+        A[3, 7] = po.from_float64(cfg[0], cfg[1], 300.0)
     if wide == "B":
-        B[5, 1] = po.from_float64(12, 1, -300.0)
-    got = ops.quire_gemm(P121, dev(P121, A), dev(P121, B))
-    want = po.matmul(12, 1, A, B)
+        B[5, 1] = po.from_float64(cfg[0], cfg[1], -300.0)
+    got = ops.quire_gemm(cfg, dev(cfg, A), dev(cfg, B))
+    want = po.matmul(cfg[0], cfg[1], A, B)
     assert (host(got) == want).all()
+
+
+@pytest.mark.parametrize("fmt", ["config3", "uniform161"])
+def test_cifar_step_with_variants_vs_oracle(cuda, po, fmt):
+    """A whole CIFAR-CNN training step with every reduced-digit variant enabled
+    (this module's fixture) -- every activation, gradient, loss and updated
+    weight against the CPU oracle step."""
+    from test_train_gpu import run_and_compare
+    from paper_2105_00053_b200 import nn
+    st = (nn.StagePrecisions(ops.P81, ops.P121, ops.P121, ops.P161, ops.P161) if fmt == "config3"
+          else nn.StagePrecisions.uniform(ops.P161))
+    rng = np.random.default_rng(41)
+    x = rng.uniform(-1.0, 1.0, (4, 3, 32, 32))
+    labels = rng.integers(0, 10, 4)
+    model = nn.cifar_cnn(st, seed=5)
+    run_and_compare(po, model, st, x, labels, 1.0 / 16, steps=1)
