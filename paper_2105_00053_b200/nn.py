@@ -548,14 +548,18 @@ class Sequential(Module):
     # relu_bwd pass), so it is off by default.
     fuse_relu_backward = False
 
-    def backward(self, dy, raw=False, record=None):
+    def backward(self, dy, raw=False, record=None, on_layer=None):
+        """on_layer(layer): called once each parameter-holding layer's gradients
+        exist (the data-parallel exchange starts there, dp.QuireAllReduce)."""
         fused = getattr(self, "_relu_fused", set()) if self.fuse_relu_backward else set()
+        notify = (lambda l: on_layer(l) if l.params() else None) if on_layer is not None else (lambda l: None)
         i = len(self.layers) - 1
         while i >= 0:
             if i in fused:  # ReLU i fused with Conv2d i-1: one backward, gate in the digitisers
                 res = self.layers[i - 1].backward_gated(dy, self.layers[i].x, raw=raw,
                                                         want_gated=record is not None)
                 if res is not None:
+                    notify(self.layers[i - 1])
                     dx, dy_relu = res
                     if record is not None:
                         record[f"dact{i}"] = dy_relu
@@ -575,6 +579,7 @@ class Sequential(Module):
                     i -= 2
                     continue
             dy = self.layers[i].backward(dy, raw=raw)
+            notify(self.layers[i])
             if dy is None:
                 break
             if record is not None:
