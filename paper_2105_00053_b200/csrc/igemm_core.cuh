@@ -539,7 +539,7 @@ __device__ __forceinline__ void emit_pixel_digits(const uint32_t (&code)[32], ui
         for (int p = 0; p < D; ++p)
 #pragma unroll
             for (int q = 0; q < 8; ++q) o |= p >= wide_planes ? words[p][q] : 0u;
-        if (o) *wide = 1;
+        if (o && *reinterpret_cast<volatile uint8_t*>(wide) == 0) *wide = 1;  // read first: no same-address store storm
     }
     // this chunk = slices 2cc, 2cc + 1 of pixel (h + pad, w + pad)
     auto cell = [&](int hh, int ww) {
@@ -788,7 +788,7 @@ __global__ void __launch_bounds__(256) im2col_digits_kernel(
             for (int p = 0; p < D; ++p)
 #pragma unroll
                 for (int q = 0; q < 8; ++q) o |= p >= wide_planes ? words[p][q] : 0u;
-            if (o) *wide = 1;
+            if (o && *reinterpret_cast<volatile uint8_t*>(wide) == 0) *wide = 1;  // read first: no same-address store storm
         }
         // slice layout of the virtual [N][OH][2 slices][OW][16] image
         const int64_t row = int64_t(n) * OH + oy;
@@ -844,7 +844,7 @@ __global__ void weight_digits_kernel(const CodeT* __restrict__ w, const CodeT* _
         }
         if (wide != nullptr) {  // a digit plane >= wide_planes in use
             const uint64_t y = (uint64_t(hi) << 32) | lo;
-            if (y >> (8 * wide_planes)) *wide = 1;
+            if ((y >> (8 * wide_planes)) && *reinterpret_cast<volatile uint8_t*>(wide) == 0) *wide = 1;
         }
 #pragma unroll
         for (int p = 0; p < D; ++p)

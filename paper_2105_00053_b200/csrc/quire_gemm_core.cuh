@@ -149,15 +149,18 @@ struct FetchColMajor {  // X[r][k] = p[k*ld + r]
 // no-swizzle UMMA image [D][ROWS/8][KB/16][8][16], and flags X rows that
 // contain a NaR.  Loads go through a shared-memory tile (coalesced for either
 // fetch order), decode is a shared-memory LUT for nbits <= 10.
-template <int D, int ROWS, typename CodeT, class Fetch>
+// FMT: the format as a compile-time constant (BASELINE formats; fixed_fmt):
+// the in-register decode of the 16-bit formats folds its shifts and masks.
+template <int D, int ROWS, typename CodeT, class Fetch, int FMT = 0>
 __global__ void __launch_bounds__(256) pack_kernel(Fetch fetch, int64_t rows_total, int64_t K,
-                                                   PositFmt f,
+                                                   PositFmt f_arg,
                                                    int8_t* __restrict__ img,
                                                    uint8_t* __restrict__ nar_flags,
                                                    uint8_t* __restrict__ any_nar_flag, int64_t tiles,
                                                    int64_t kbt, const uint2* __restrict__ glut,
                                                    uint8_t* __restrict__ wide_flag = nullptr,
                                                    int wide_planes = 0) {
+    const PositFmt f = fixed_fmt<FMT>(f_arg);
     constexpr int KB = Geometry<D>::KB;
     constexpr int KC = KB / 16;
     // k-blocks per pass, so that every thread owns at least one 16-code unit
@@ -298,12 +301,13 @@ __global__ void __launch_bounds__(256) pack_kernel(Fetch fetch, int64_t rows_tot
                 nar_flags[r0 + r] = 1;
                 *any_nar_flag = 1;
             }
-            if (wide_flag != nullptr) {  // a digit plane >= wide_planes in use
+            if (wide_flag != nullptr) {  // a digit plane >= wide_planes in use (digit bytes != 0)
+                const uint32_t mlo = wide_planes >= 4 ? 0u : ~0u << (8 * wide_planes);
+                const uint32_t mhi = wide_planes >= 4 ? ~0u << (8 * (wide_planes - 4)) : ~0u;
                 uint32_t o = 0;
 #pragma unroll
-                for (int j = 0; j < 16; ++j)
-                    o |= uint32_t(((uint64_t(hi[j]) << 32 | lo[j]) >> (8 * wide_planes)) != 0);
-                if (o) *wide_flag = 1;
+                for (int j = 0; j < 16; ++j) o |= (lo[j] & mlo) | (hi[j] & mhi);
+                if (o && *reinterpret_cast<volatile uint8_t*>(wide_flag) == 0) *wide_flag = 1;  // read first: no same-address store storm
             }
             int8_t* chunk = img + (t * kbt + kb0 + kbl) * int64_t(D * ROWS * KB);
 #pragma unroll
@@ -982,10 +986,20 @@ cudaError_t launch_generic(const QuireGemmPlan& p, const GemmArgs& g, FA fa, FB 
     constexpr int kRed = D == 8 ? 4 : 3;
     const bool reduced = (D == 6 || D == 8) && !p.pair && sizeof(CodeT) == 2 &&
                          g.M * g.N * g.K >= variant_min_work();  // the extra launch pays off
-    pack_kernel<D, kBM, CodeT, FA><<<int(a_work < 148 * 8 ? a_work : 148 * 8), 256, 0, st>>>(
-        fa, g.M, g.K, f, a_img, rnar, flags, p.mtiles_alloc, p.kbt, glut, reduced ? flags + 2 : nullptr, kRed);
-    pack_kernel<D, Geo::NT, CodeT, FB><<<int(b_work < 148 * 8 ? b_work : 148 * 8), 256, 0, st>>>(
-        fb, g.N, g.K, f, b_img, cnar, flags + 1, p.ntiles, p.kbt, glut, reduced ? flags + 3 : nullptr, kRed);
+    const int ga = int(a_work < 148 * 8 ? a_work : 148 * 8), gb = int(b_work < 148 * 8 ? b_work : 148 * 8);
+    if (D == 8 && sizeof(CodeT) == 2 && fixed_fmt_id(f) == 4) {  // posit(16,1): compile-time decode
+        pack_kernel<D, kBM, CodeT, FA, 4><<<ga, 256, 0, st>>>(fa, g.M, g.K, f, a_img, rnar, flags,
+                                                               p.mtiles_alloc, p.kbt, glut,
+                                                               reduced ? flags + 2 : nullptr, kRed);
+        pack_kernel<D, Geo::NT, CodeT, FB, 4><<<gb, 256, 0, st>>>(fb, g.N, g.K, f, b_img, cnar, flags + 1,
+                                                                   p.ntiles, p.kbt, glut,
+                                                                   reduced ? flags + 3 : nullptr, kRed);
+    } else {
+        pack_kernel<D, kBM, CodeT, FA><<<ga, 256, 0, st>>>(fa, g.M, g.K, f, a_img, rnar, flags, p.mtiles_alloc,
+                                                           p.kbt, glut, reduced ? flags + 2 : nullptr, kRed);
+        pack_kernel<D, Geo::NT, CodeT, FB><<<gb, 256, 0, st>>>(fb, g.N, g.K, f, b_img, cnar, flags + 1, p.ntiles,
+                                                               p.kbt, glut, reduced ? flags + 3 : nullptr, kRed);
+    }
     if (stats) cudaEventRecord(stats->ev[1], st);
     // D <= 3 implies R <= 11, hence W <= 64: no 128-bit instantiation needed.
     using KernFn = void (*)(const int8_t*, const int8_t*, int64_t, int64_t, const uint8_t*,
