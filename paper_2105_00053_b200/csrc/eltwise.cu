@@ -570,31 +570,47 @@ __global__ void sgd_multi_kernel(PositFmt fo, int bo, PositFmt fg, int bg, uint3
         decode_x(lr, fo, X_lr);
         __syncthreads();
     }
-    const int64_t total = segs.start[segs.count];
+    // the segment table in shared memory: lane-divergent indexing of the kernel
+    // parameter space would serialise on the constant cache
+    __shared__ int64_t s_start[kSgdMaxSeg + 1];
+    __shared__ const void* s_ptr[4][kSgdMaxSeg];
+    for (int t = threadIdx.x; t <= segs.count; t += blockDim.x) s_start[t] = segs.start[t];
+    for (int t = threadIdx.x; t < segs.count; t += blockDim.x) {
+        s_ptr[0][t] = segs.master[t];
+        s_ptr[1][t] = segs.grad[t];
+        s_ptr[2][t] = segs.copy1[t];
+        s_ptr[3][t] = segs.copy2[t];
+    }
+    __syncthreads();
+    const int64_t total = s_start[segs.count];
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total;
          i += int64_t(gridDim.x) * blockDim.x) {
         int lo = 0, hi = segs.count - 1;  // last segment with start <= i
         while (lo < hi) {
             const int mid = (lo + hi + 1) >> 1;
-            if (segs.start[mid] <= i) lo = mid;
+            if (s_start[mid] <= i) lo = mid;
             else hi = mid - 1;
         }
-        const int64_t k = i - segs.start[lo];
+        const int64_t k = i - s_start[lo];
+        void* const master = const_cast<void*>(s_ptr[0][lo]);
+        const void* const grad = s_ptr[1][lo];
+        void* const copy1 = const_cast<void*>(s_ptr[2][lo]);
+        void* const copy2 = const_cast<void*>(s_ptr[3][lo]);
         uint32_t w;
         if (fast) {
-            w = sgd_fast(fo, fg, X_lr, load_any(segs.master[lo], k, bo), load_any(segs.grad[lo], k, bg), s_lut);
+            w = sgd_fast(fo, fg, X_lr, load_any(master, k, bo), load_any(grad, k, bg), s_lut);
         } else {
-            uint32_t g = p_convert(fg, fo, load_any(segs.grad[lo], k, bg));
+            uint32_t g = p_convert(fg, fo, load_any(grad, k, bg));
             if (grad_scale_log2 != 0) g = p_ldexp(fo, g, -grad_scale_log2);
-            w = p_sub(fo, load_any(segs.master[lo], k, bo), p_mul(fo, lr, g));
+            w = p_sub(fo, load_any(master, k, bo), p_mul(fo, lr, g));
         }
-        store_any(segs.master[lo], k, bo, w);
+        store_any(master, k, bo, w);
         int64_t Xw = 0;
         if (fast & 6) decode_x(w, fo, Xw);
-        if (segs.copy1[lo])
-            store_any(segs.copy1[lo], k, b1, (fast & 2) ? copy_fast(fo, f1, w, Xw, s_lut1) : p_convert(fo, f1, w));
-        if (segs.copy2[lo])
-            store_any(segs.copy2[lo], k, b2, (fast & 4) ? copy_fast(fo, f2, w, Xw, s_lut2) : p_convert(fo, f2, w));
+        if (copy1)
+            store_any(copy1, k, b1, (fast & 2) ? copy_fast(fo, f1, w, Xw, s_lut1) : p_convert(fo, f1, w));
+        if (copy2)
+            store_any(copy2, k, b2, (fast & 4) ? copy_fast(fo, f2, w, Xw, s_lut2) : p_convert(fo, f2, w));
     }
 }
 
