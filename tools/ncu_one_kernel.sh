@@ -10,4 +10,5 @@ ncu --set full --import-source on --clock-control none --kernel-name-base demang
     python tools/bench_train.py --configs $cfg --steps 1 --warmup 0 > gpurun_out/${tag}_ncu.log 2>&1
 ncu -i /tmp/${tag}.ncu-rep --page details --csv > gpurun_out/${tag}_details.csv
 ncu -i /tmp/${tag}.ncu-rep --page source --csv --print-source sass > gpurun_out/${tag}_sass.csv
+ncu -i /tmp/${tag}.ncu-rep --page raw --csv > gpurun_out/${tag}_raw.csv
 rm -f /tmp/${tag}.ncu-rep
