@@ -182,8 +182,21 @@ int pnn_relu_bwd(int x_nbits, int x_es, const void* x, int g_nbits, int g_es, co
  * recomputes it in pnn_maxpool2d_bwd_x instead of storing 8 bytes per output). */
 int pnn_maxpool2d_fwd(int nbits, int es, const void* x, int64_t N, int64_t C, int64_t H,
                       int64_t W, int k, int stride, void* y, int64_t* argmax, void* stream);
+/* Window-specialised backward: dy and argmax MUST be the (N, C, OH, OW) output
+ * of pnn_maxpool2d_fwd with the same k / stride (each argmax inside its own
+ * window); any other argmax: pnn_maxpool2d_bwd_scatter. */
 int pnn_maxpool2d_bwd(int nbits, int es, const void* dy, const int64_t* argmax, int64_t N,
                       int64_t C, int64_t H, int64_t W, int k, int stride, void* dx, void* stream);
+/* maxpool2d_backward(dy, argmax, x_shape) exactly as tensor_ops.cpp:658-670:
+ * dx = 0, then for i = 0..n_out-1 in order dx[argmax[i]] = add(dx[argmax[i]], dy[i]),
+ * for ANY argmax (no window assumed; n_in = numel(x_shape)).  Indices outside
+ * [0, n_in) are dropped (the reference's behaviour there is undefined; the host
+ * mirrors reject them).  n_out, n_in < 2^31.  Replaces maxpool2d_backward
+ * (tensor_ops.hpp:50-51). */
+int pnn_maxpool2d_bwd_scatter_workspace(int64_t n_out, int64_t n_in, size_t* bytes);
+int pnn_maxpool2d_bwd_scatter(int nbits, int es, const void* dy, const int64_t* argmax, int64_t n_out,
+                              void* dx, int64_t n_in, void* workspace, size_t workspace_bytes,
+                              void* stream);
 /* maxpool2d_backward(dy, argmax of maxpool2d(x)) with the argmax recomputed
  * from the pooled input x (x in (x_nbits, x_es), dy/dx in (g_nbits, g_es));
  * 2x2 / stride-2 tiled windows (else PNN_EUNSUPPORTED: use the argmax pair). */

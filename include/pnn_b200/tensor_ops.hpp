@@ -65,8 +65,14 @@ struct MaxPoolResult {
     std::vector<int64_t> argmax;  // flat input index per output element
 };
 MaxPoolResult maxpool2d(const Tensor& x, int k, int stride, const void* pool = nullptr);
+// Reference signature (tensor_ops.hpp:50-51): any argmax, outputs added per
+// target in increasing output order; out-of-range indices throw.
 Tensor maxpool2d_backward(const Tensor& dy, const std::vector<int64_t>& argmax,
-                          const std::vector<int64_t>& x_shape, int k = 2, int stride = 2);
+                          const std::vector<int64_t>& x_shape);
+// Window-specialised: dy must be the (N, C, OH, OW) output of maxpool2d(x, k,
+// stride) and every argmax inside its window (else std::invalid_argument).
+Tensor maxpool2d_backward(const Tensor& dy, const std::vector<int64_t>& argmax,
+                          const std::vector<int64_t>& x_shape, int k, int stride);
 Tensor convert_tensor(const Tensor& t, const PositConfig& target);
 
 }  // namespace pnn_b200

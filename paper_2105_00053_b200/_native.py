@@ -64,6 +64,9 @@ _SIGS = {
     "pnn_relu_bwd": (C.c_int, [C.c_int, C.c_int, _vp, C.c_int, C.c_int, _vp, _vp, _i64, _vp]),
     "pnn_maxpool2d_fwd": (C.c_int, [C.c_int, C.c_int, _vp] + [_i64] * 4 + [C.c_int, C.c_int, _vp, _vp, _vp]),
     "pnn_maxpool2d_bwd": (C.c_int, [C.c_int, C.c_int, _vp, _vp] + [_i64] * 4 + [C.c_int, C.c_int, _vp, _vp]),
+    "pnn_maxpool2d_bwd_scatter_workspace": (C.c_int, [_i64, _i64, C.POINTER(C.c_size_t)]),
+    "pnn_maxpool2d_bwd_scatter": (C.c_int, [C.c_int, C.c_int, _vp, _vp, _i64, _vp, _i64, _vp, C.c_size_t,
+                                            _vp]),
     "pnn_softmax_xent_grad": (C.c_int, [C.c_int, C.c_int, _vp, _vp, _i64, _i64, C.c_int, C.c_int, _vp, _vp,
                                         _vp]),
     "pnn_softmax_xent_loss": (C.c_int, [C.c_int, C.c_int, _vp, _vp, _vp, _i64, _i64, C.c_int, _vp, _vp, _vp,

@@ -5,7 +5,9 @@ patterns packed little-endian in ceil(nbits/8) bytes each}).
 
 Field widths (the SPEC leaves them open; fixed here): name length uint32 LE,
 name UTF-8, nbits uint8, es uint8, rank uint8, extents int64 LE, then the codes.
-Records follow each other to the end of the file.  save -> load -> save is
+Records follow each other to the end of the file.  save_model() adds a config
+record (meta.stage_precisions: (nbits, es) of the five stages) checked on
+load, and the momentum velocities of an SGD optimizer (meta.sgd + velocityI).  save -> load -> save is
 byte-identical; a truncated file, a bad magic or a record that does not match
 the model (name, shape, posit format) raises ValueError.
 
@@ -86,39 +88,89 @@ def load_tensors(path: str):
         return loads(f.read())
 
 
-def _param_records(model):
+STAGES = ("forward", "backward", "gradient", "optimizer", "loss")
+META_STAGES = "meta.stage_precisions"   # uint8 [5, 2]: (nbits, es) per stage, STAGES order
+META_SGD = "meta.sgd"                   # uint8 [1]: 1 = momentum velocity records follow
+
+
+def _model_stages(model):
+    params = model.params()
+    sts = {tuple((getattr(p.st, k).nbits, getattr(p.st, k).es) for k in STAGES) for p in params}
+    if len(sts) != 1:
+        raise ValueError("model parameters disagree on their stage precisions")
+    return np.array(sorted(sts)[0], np.uint64).ravel()
+
+
+def _records(model, optimizer=None):
     from .codec import to_host
 
-    recs = []
-    for i, p in enumerate(model.params()):
+    recs = [(META_STAGES, (8, 0), _model_stages(model))]
+    params = model.params()
+    for i, p in enumerate(params):
         cfg = p.st.optimizer
         recs.append((f"param{i}", (cfg.nbits, cfg.es), to_host(p.master)))
+    vel = getattr(optimizer, "velocity", None) if optimizer is not None and optimizer.momentum else None
+    recs.append((META_SGD, (8, 0), np.array([1 if vel is not None else 0], np.uint64)))
+    if vel is not None:
+        for i, (p, v) in enumerate(zip(params, vel)):
+            cfg = p.st.optimizer
+            recs.append((f"velocity{i}", (cfg.nbits, cfg.es), to_host(v)))
     return recs
 
 
-def save_model(model, path: str) -> None:
-    """Master weights (p_optimizer codes) of every parameter, in order."""
-    save_tensors(path, _param_records(model))
+def save_model(model, path: str, optimizer=None) -> None:
+    """Stage precisions of the model (a config record checked on load), the
+    master weights (p_optimizer codes) of every parameter in order, and -- for
+    an SGD with momentum -- its velocity tensors, so training resumes bit-exactly."""
+    save_tensors(path, _records(model, optimizer))
 
 
-def load_model(model, path: str) -> None:
+def load_model(model, path: str, optimizer=None) -> None:
     """Restore the master weights in place (device tensors keep their storage,
-    so a captured CUDA graph stays valid) and refresh every stage copy."""
+    so a captured CUDA graph stays valid) and refresh every stage copy.  A
+    checkpoint written for other stage precisions, another architecture, or
+    without the velocity a momentum optimizer needs is rejected (ValueError)."""
     import torch
 
     from . import ops
 
     recs = load_tensors(path)
     params = model.params()
-    if len(recs) != len(params):
-        raise ValueError(f"checkpoint has {len(recs)} tensors, model {len(params)}")
-    for i, ((name, fmt, codes), p) in enumerate(zip(recs, params)):
+    byname = {}
+    for name, fmt, codes in recs:
+        if name in byname:
+            raise ValueError(f"checkpoint record {name} appears twice")
+        byname[name] = (fmt, codes)
+    if META_STAGES in byname:  # files written before the config record carry none
+        got = byname[META_STAGES][1].ravel()
+        want = _model_stages(model)
+        if got.shape != want.shape or (got != want).any():
+            raise ValueError(f"checkpoint stage precisions {got.reshape(-1, 2).tolist()} differ from the "
+                             f"model's {want.reshape(-1, 2).tolist()} ({', '.join(STAGES)})")
+    weights = [r for r in recs if r[0].startswith("param")]
+    if len(weights) != len(params):
+        raise ValueError(f"checkpoint has {len(weights)} tensors, model {len(params)}")
+    for i, ((name, fmt, codes), p) in enumerate(zip(weights, params)):
         cfg = p.st.optimizer
         if name != f"param{i}" or fmt != (cfg.nbits, cfg.es) or tuple(codes.shape) != p.shape:
             raise ValueError(f"checkpoint record {name} {fmt} {tuple(codes.shape)} does not match "
                              f"param{i} posit({cfg.nbits},{cfg.es}) {p.shape}")
-    for (_, _, codes), p in zip(recs, params):
+    has_vel = META_SGD in byname and int(byname[META_SGD][1].ravel()[0]) == 1
+    want_vel = optimizer is not None and bool(optimizer.momentum)
+    if want_vel and not has_vel:
+        raise ValueError("checkpoint has no momentum velocity for this optimizer")
+    if want_vel:
+        for i, p in enumerate(params):
+            rec = byname.get(f"velocity{i}")
+            cfg = p.st.optimizer
+            if rec is None or rec[0] != (cfg.nbits, cfg.es) or tuple(rec[1].shape) != p.shape:
+                raise ValueError(f"checkpoint velocity{i} missing or does not match param{i}")
+    for (_, _, codes), p in zip(weights, params):
         cfg = p.st.optimizer
         p.master.copy_(torch.from_numpy(codes.astype(cfg.np_code_dtype)).to(p.master.device))
         for c in p.stage_formats():
             p.copies[c].copy_(ops.convert_tensor(p.master, cfg, c))
+    if want_vel:
+        for i, (p, v) in enumerate(zip(params, optimizer.velocity)):
+            codes = byname[f"velocity{i}"][1]
+            v.copy_(torch.from_numpy(codes.astype(p.st.optimizer.np_code_dtype)).to(v.device))

@@ -152,6 +152,13 @@ Tensor conv2d_input_grad(const Tensor& dy, const Tensor& w, const std::vector<in
     same_cfg(dy, w, "conv2d_input_grad");
     const auto& f = dy.config();
     const int64_t N = x_shape[0], C = x_shape[1], H = x_shape[2], W = x_shape[3];
+    require(stride >= 1 && pad >= 0, "conv2d_input_grad: bad stride/pad");
+    require(N >= 0 && C >= 1 && H >= 1 && W >= 1, "conv2d_input_grad: bad x_shape");
+    require(w.dim(1) == C, "conv2d_input_grad: channel mismatch (w vs x_shape)");
+    require(dy.dim(0) == N && dy.dim(1) == w.dim(0), "conv2d_input_grad: dy does not match x_shape / w");
+    require(H + 2 * pad >= w.dim(2) && W + 2 * pad >= w.dim(3), "conv2d_input_grad: kernel larger than input");
+    require(dy.dim(2) == (H + 2 * pad - w.dim(2)) / stride + 1 && dy.dim(3) == (W + 2 * pad - w.dim(3)) / stride + 1,
+            "conv2d_input_grad: dy spatial size does not match the convolution");
     Tensor dx(f, x_shape);
     auto ddy = upload(dy), dw = upload(w);
     Dev out(size_t(dx.numel()) * cb(f));
@@ -178,6 +185,15 @@ Tensor conv2d_weight_grad(const Tensor& dy, const Tensor& x, const std::vector<i
     require(dy.rank() == 4 && x.rank() == 4 && w_shape.size() == 4, "conv2d_weight_grad: bad ranks");
     same_cfg(dy, x, "conv2d_weight_grad");
     const auto& f = dy.config();
+    require(stride >= 1 && pad >= 0, "conv2d_weight_grad: bad stride/pad");
+    require(w_shape[0] == dy.dim(1) && w_shape[1] == x.dim(1), "conv2d_weight_grad: w_shape does not match dy / x");
+    require(dy.dim(0) == x.dim(0), "conv2d_weight_grad: batch mismatch");
+    require(w_shape[2] >= 1 && w_shape[3] >= 1 && x.dim(2) + 2 * pad >= w_shape[2] &&
+                x.dim(3) + 2 * pad >= w_shape[3],
+            "conv2d_weight_grad: kernel larger than input");
+    require(dy.dim(2) == (x.dim(2) + 2 * pad - w_shape[2]) / stride + 1 &&
+                dy.dim(3) == (x.dim(3) + 2 * pad - w_shape[3]) / stride + 1,
+            "conv2d_weight_grad: dy spatial size does not match the convolution");
     Tensor dw(f, w_shape);
     auto ddy = upload(dy), dx = upload(x);
     Dev out(size_t(dw.numel()) * cb(f));
@@ -249,10 +265,46 @@ MaxPoolResult maxpool2d(const Tensor& x, int k, int stride, const void*) {
     return r;
 }
 
+// tensor_ops.cpp:658-670: window-independent, outputs added per target in
+// increasing output order (pnn_maxpool2d_bwd_scatter).
+Tensor maxpool2d_backward(const Tensor& dy, const std::vector<int64_t>& argmax,
+                          const std::vector<int64_t>& x_shape) {
+    require(size_t(dy.numel()) == argmax.size(), "maxpool2d_backward: argmax mismatch");
+    const auto& f = dy.config();
+    Tensor dx(f, x_shape);
+    for (int64_t t : argmax)  // undefined behaviour in the reference: rejected here
+        require(t >= 0 && t < dx.numel(), "maxpool2d_backward: argmax index out of range");
+    auto ddy = upload(dy);
+    Dev am(argmax.size() * 8), out(size_t(dx.numel()) * cb(f));
+    if (!argmax.empty())
+        cuda(cudaMemcpy(am.p, argmax.data(), am.bytes, cudaMemcpyHostToDevice), "H2D argmax");
+    size_t ws = 0;
+    check(pnn_maxpool2d_bwd_scatter_workspace(dy.numel(), dx.numel(), &ws));
+    Dev work(ws);
+    check(pnn_maxpool2d_bwd_scatter(f.nbits, f.es, ddy->p, static_cast<const int64_t*>(am.p), dy.numel(),
+                                    out.p, dx.numel(), work.p, ws, nullptr));
+    sync();
+    download(out, dx);
+    return dx;
+}
+
 Tensor maxpool2d_backward(const Tensor& dy, const std::vector<int64_t>& argmax,
                           const std::vector<int64_t>& x_shape, int k, int stride) {
     require(size_t(dy.numel()) == argmax.size(), "maxpool2d_backward: argmax mismatch");
     require(x_shape.size() == 4, "maxpool2d_backward: NCHW shape required");
+    require(k >= 1 && stride >= 1 && x_shape[2] >= k && x_shape[3] >= k, "maxpool2d_backward: bad window");
+    const int64_t OH = (x_shape[2] - k) / stride + 1, OW = (x_shape[3] - k) / stride + 1;
+    require(dy.rank() == 4 && dy.dim(0) == x_shape[0] && dy.dim(1) == x_shape[1] && dy.dim(2) == OH &&
+                dy.dim(3) == OW,
+            "maxpool2d_backward: dy is not the (N, C, OH, OW) output of this window");
+    // every argmax must lie in its own window (else the 3-argument scatter applies)
+    for (int64_t o = 0; o < dy.numel(); ++o) {
+        const int64_t ox = o % OW, oy = (o / OW) % OH, nc = o / (OW * OH);
+        const int64_t t = argmax[size_t(o)], ix = t % x_shape[3], iy = (t / x_shape[3]) % x_shape[2];
+        require(t >= 0 && t / (x_shape[2] * x_shape[3]) == nc && iy >= oy * stride && iy < oy * stride + k &&
+                    ix >= ox * stride && ix < ox * stride + k,
+                "maxpool2d_backward: argmax outside its window");
+    }
     const auto& f = dy.config();
     Tensor dx(f, x_shape);
     auto ddy = upload(dy);

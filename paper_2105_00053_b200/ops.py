@@ -580,14 +580,44 @@ def maxpool2d(cfg, x, k: int, stride: int, pool=None):
     return y, am
 
 
-def maxpool2d_backward(cfg, dy, argmax, x_shape, k: int = 2, stride: int = 2):
-    """tensor_ops.hpp:50-51 (window geometry passed explicitly)."""
+def maxpool2d_backward(cfg, dy, argmax, x_shape, k=None, stride=None):
+    """tensor_ops.hpp:50-51 / tensor_ops.cpp:658-670.
+
+    Reference signature (k, stride omitted): window-independent scatter,
+    dx[argmax[i]] = add(dx[argmax[i]], dy[i]) for i in increasing order, for any
+    argmax.  Indices outside [0, numel(x_shape)) raise PnnInvalidArgument (the
+    reference has undefined behaviour there).  With k and stride given, dy and
+    argmax must be the (N, C, OH, OW) result of maxpool2d(x, k, stride): the
+    window-specialised kernel runs after a shape check."""
     cfg = _cfg(cfg)
     N, Cc, H, W = (int(v) for v in x_shape)
+    dy, argmax = dy.contiguous(), argmax.contiguous()
+    if dy.numel() != argmax.numel():
+        raise _native.PnnInvalidArgument(1, "maxpool2d_backward: argmax mismatch")
     dx = torch.empty((N, Cc, H, W), dtype=cfg.code_dtype, device=dy.device)
-    _native.check(_native.lib().pnn_maxpool2d_bwd(cfg.nbits, cfg.es, dy.contiguous().data_ptr(),
-                                                  argmax.contiguous().data_ptr(), N, Cc, H, W, k, stride,
-                                                  dx.data_ptr(), _stream_ptr(dy.device)))
+    if (k is None) != (stride is None):
+        raise _native.PnnInvalidArgument(1, "maxpool2d_backward: give both k and stride, or neither")
+    if k is not None:
+        if H < k or W < k or k < 1 or stride < 1:
+            raise _native.PnnInvalidArgument(1, "maxpool2d_backward: bad window")
+        OH, OW = (H - k) // stride + 1, (W - k) // stride + 1
+        if tuple(dy.shape) != (N, Cc, OH, OW):
+            raise _native.PnnInvalidArgument(
+                1, f"maxpool2d_backward: dy shape {tuple(dy.shape)} is not {(N, Cc, OH, OW)}")
+        _native.check(_native.lib().pnn_maxpool2d_bwd(cfg.nbits, cfg.es, dy.data_ptr(), argmax.data_ptr(),
+                                                      N, Cc, H, W, k, stride, dx.data_ptr(),
+                                                      _stream_ptr(dy.device)))
+        return dx
+    n_in = N * Cc * H * W
+    if argmax.numel() and (int(argmax.min()) < 0 or int(argmax.max()) >= n_in):
+        raise _native.PnnInvalidArgument(1, "maxpool2d_backward: argmax index out of range")
+    n = C.c_size_t()
+    _native.check(_native.lib().pnn_maxpool2d_bwd_scatter_workspace(dy.numel(), n_in, C.byref(n)))
+    ws = _ws.get(dy.device, n.value)
+    _native.check(_native.lib().pnn_maxpool2d_bwd_scatter(cfg.nbits, cfg.es, dy.data_ptr(),
+                                                          argmax.to(torch.int64).data_ptr(), dy.numel(),
+                                                          dx.data_ptr(), n_in, ws.data_ptr(), ws.numel(),
+                                                          _stream_ptr(dy.device)))
     return dx
 
 

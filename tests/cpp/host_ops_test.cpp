@@ -103,6 +103,67 @@ int main() {
         po_bias_grad_seq(f.nbits, f.es, dy.data(), 2, 4, 9 * 8, dbw.data());
         for (int i = 0; i < 4; ++i) EXPECT(dbs.bits_at(i) == dbw[size_t(i)]);
     }
+    // maxpool2d_backward, reference signature (tensor_ops.cpp:658-670): any
+    // window -- overlapping 3x3/2 and tiled 3x3/3 -- and an arbitrary argmax
+    // with collisions, each vs the oracle's sequential scatter.
+    for (PositConfig f : {p80, p121, p161}) {
+        for (int k : {2, 3}) {
+            for (int s : {1, 2, 3}) {
+                Tensor x = rand_tensor(f, {2, 3, 6, 7}, 40 + k * 3 + s);
+                auto mp = pnn_b200::maxpool2d(x, k, s);
+                std::vector<uint64_t> yw(size_t(mp.out.numel()));
+                std::vector<int64_t> amw(size_t(mp.out.numel()));
+                po_maxpool2d(f.nbits, f.es, x.data(), 2, 3, 6, 7, k, s, yw.data(), amw.data());
+                for (int64_t i = 0; i < mp.out.numel(); ++i) {
+                    EXPECT(mp.out.bits_at(i) == yw[size_t(i)]);
+                    EXPECT(mp.argmax[size_t(i)] == amw[size_t(i)]);
+                }
+                Tensor dy = rand_tensor(f, mp.out.shape(), 50 + k * 3 + s);
+                std::vector<uint64_t> dxw(size_t(x.numel()));
+                po_maxpool2d_backward(f.nbits, f.es, dy.data(), dy.numel(), mp.argmax.data(), x.numel(),
+                                      dxw.data());
+                Tensor dx = pnn_b200::maxpool2d_backward(dy, mp.argmax, x.shape());
+                for (int64_t i = 0; i < x.numel(); ++i) EXPECT(dx.bits_at(i) == dxw[size_t(i)]);
+                Tensor dx2 = pnn_b200::maxpool2d_backward(dy, mp.argmax, x.shape(), k, s);
+                for (int64_t i = 0; i < x.numel(); ++i) EXPECT(dx2.bits_at(i) == dxw[size_t(i)]);
+            }
+        }
+        // arbitrary argmax: 500 outputs onto 40 targets (many collisions)
+        Tensor dy = rand_tensor(f, {500}, 61);
+        std::vector<int64_t> am(500);
+        std::mt19937_64 rng(62);
+        for (auto& t : am) t = int64_t(rng() % 40);
+        std::vector<uint64_t> dxw(40);
+        po_maxpool2d_backward(f.nbits, f.es, dy.data(), 500, am.data(), 40, dxw.data());
+        Tensor dx = pnn_b200::maxpool2d_backward(dy, am, {1, 1, 5, 8});
+        for (int i = 0; i < 40; ++i) EXPECT(dx.bits_at(i) == dxw[size_t(i)]);
+        // window mismatch / out-of-range targets throw instead of reading past dy
+        Tensor x = rand_tensor(f, {1, 2, 6, 6}, 63);
+        auto mp = pnn_b200::maxpool2d(x, 3, 3);
+        bool threw = false;
+        try { pnn_b200::maxpool2d_backward(mp.out, mp.argmax, x.shape(), 2, 2); }
+        catch (const std::invalid_argument&) { threw = true; }
+        EXPECT(threw);
+        threw = false;
+        am.assign(500, 40);
+        try { pnn_b200::maxpool2d_backward(dy, am, {1, 1, 5, 8}); }
+        catch (const std::invalid_argument&) { threw = true; }
+        EXPECT(threw);
+    }
+    // conv gradient shape cross-checks (std::invalid_argument, no device access)
+    {
+        Tensor x = rand_tensor(p80, {2, 3, 9, 8}, 70), w = rand_tensor(p80, {4, 3, 3, 3}, 71);
+        Tensor dy = rand_tensor(p80, {2, 4, 9, 8}, 72), dy_bad = rand_tensor(p80, {2, 5, 9, 8}, 73);
+        int throws = 0;
+        try { pnn_b200::conv2d_weight_grad(dy, x, {5, 3, 3, 3}, 1, 1, true); } catch (const std::invalid_argument&) { ++throws; }
+        try { pnn_b200::conv2d_weight_grad(dy, x, {4, 2, 3, 3}, 1, 1, true); } catch (const std::invalid_argument&) { ++throws; }
+        try { pnn_b200::conv2d_weight_grad(rand_tensor(p80, {3, 4, 9, 8}, 74), x, w.shape(), 1, 1, true); } catch (const std::invalid_argument&) { ++throws; }
+        try { pnn_b200::conv2d_weight_grad(dy, x, w.shape(), 1, 0, true); } catch (const std::invalid_argument&) { ++throws; }
+        try { pnn_b200::conv2d_input_grad(dy_bad, w, x.shape(), 1, 1, true); } catch (const std::invalid_argument&) { ++throws; }
+        try { pnn_b200::conv2d_input_grad(dy, w, {2, 2, 9, 8}, 1, 1, true); } catch (const std::invalid_argument&) { ++throws; }
+        try { pnn_b200::conv2d_input_grad(dy, w, {2, 3, 9, 8}, 2, 1, true); } catch (const std::invalid_argument&) { ++throws; }
+        EXPECT(throws == 7);
+    }
     std::printf("host_ops_test: %s (%d failures)\n", failures ? "FAILED" : "ok", failures);
     return failures ? 1 : 0;
 }

@@ -134,4 +134,47 @@ def test_model_checkpoint_round_trip(cuda, tmp_path):
         checkpoint.load_model(nn.cifar_cnn(st, seed=0), path)
     with pytest.raises(ValueError):
         checkpoint.load_model(nn.lenet5(nn.StagePrecisions.uniform(ops.P121)), path)
+    # same optimizer format and shapes, other stage precisions: the config record rejects it
+    with pytest.raises(ValueError, match="stage precisions"):
+        checkpoint.load_model(nn.lenet5(nn.StagePrecisions(ops.P81, ops.P121, ops.P121, ops.P161, ops.P161)),
+                              path)
     del torch
+
+
+@pytest.mark.gpu
+def test_checkpoint_resumes_momentum_bit_exactly(cuda, tmp_path):
+    """SGD with momentum: save after step 1 (weights + velocity), load into a
+    fresh model and optimizer, run step 2 on both: identical weights, velocity
+    and loss (bit-exact persistence)."""
+    import torch
+
+    from paper_2105_00053_b200 import codec, nn, ops
+
+    st = nn.StagePrecisions(ops.P80, ops.P121, ops.P121, ops.P161, ops.P161)
+    rng = np.random.default_rng(9)
+    B = 16
+    xs = [codec.from_float64_device(rng.random((B, 1, 32, 32)), st.forward) for _ in range(2)]
+    ys = [torch.from_numpy(rng.integers(0, 10, B).astype(np.int32)).cuda() for _ in range(2)]
+    a = nn.lenet5(st, seed=3)
+    opt_a = nn.SGD(a.params(), 1.0 / 16, st, momentum=0.5)
+    nn.train_step(a, nn.CrossEntropyLoss(st), opt_a, xs[0], ys[0], B)
+    path = str(tmp_path / "mom.pnn1")
+    checkpoint.save_model(a, path, opt_a)
+    b = nn.lenet5(st, seed=4)
+    opt_b = nn.SGD(b.params(), 1.0 / 16, st, momentum=0.5)
+    with pytest.raises(ValueError, match="velocity"):
+        checkpoint.load_model(b, _save_plain(a, tmp_path), opt_b)
+    checkpoint.load_model(b, path, opt_b)
+    la = nn.train_step(a, nn.CrossEntropyLoss(st), opt_a, xs[1], ys[1], B)
+    lb = nn.train_step(b, nn.CrossEntropyLoss(st), opt_b, xs[1], ys[1], B)
+    assert (codec.to_host(la) == codec.to_host(lb)).all()
+    for p, q, u, v in zip(a.params(), b.params(), opt_a.velocity, opt_b.velocity):
+        assert (codec.to_host(p.master) == codec.to_host(q.master)).all()
+        assert (codec.to_host(u) == codec.to_host(v)).all()
+    assert any(codec.to_host(v).any() for v in opt_b.velocity)
+
+
+def _save_plain(model, tmp_path):
+    path = str(tmp_path / "plain.pnn1")
+    checkpoint.save_model(model, path)  # no optimizer: no velocity records
+    return path

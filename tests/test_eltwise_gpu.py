@@ -135,7 +135,42 @@ def test_maxpool(cuda, po, cfg, geom):
     assert (host(y) == yw).all() and (am.cpu().numpy() == amw).all()
     dy = rand_codes(rng, n, yw.shape)
     dx = ops.maxpool2d_backward(cfg, dev(cfg, dy), am, x.shape, k, s)
-    assert (host(dx) == po.maxpool2d_backward(n, es, dy, amw, x.shape)).all()
+    want = po.maxpool2d_backward(n, es, dy, amw, x.shape)
+    assert (host(dx) == want).all()
+    # reference signature: window-independent scatter
+    dx = ops.maxpool2d_backward(cfg, dev(cfg, dy), am, x.shape)
+    assert (host(dx) == want).all()
+
+
+@pytest.mark.parametrize("cfg", FORMATS + [(12, 2)])
+@pytest.mark.parametrize("shape", [(1, 1, 5, 8), (3, 7, 33, 17), (1, 1, 1, 1)])
+def test_maxpool_backward_scatter_any_argmax(cuda, po, cfg, shape):
+    """maxpool2d_backward(dy, argmax, x_shape) for an arbitrary argmax (not
+    produced by a window): collisions add in increasing output order
+    (tensor_ops.cpp:665-668), untouched targets stay 0, NaR is sticky."""
+    n, es = cfg
+    rng = np.random.default_rng(n * 7 + es + shape[1])
+    n_in = int(np.prod(shape))
+    for n_out in (0, 1, 37, 5000):
+        am = rng.integers(0, max(1, n_in // 3), n_out).astype(np.int64)
+        dy = rand_codes(rng, n, (n_out,), nar_ok=True)
+        dx = ops.maxpool2d_backward(cfg, dev(cfg, dy), torch.from_numpy(am).cuda(), shape)
+        assert (host(dx).ravel() == po.maxpool2d_backward(n, es, dy, am, shape).ravel()).all(), n_out
+
+
+def test_maxpool_backward_rejects_bad_window_and_index(cuda):
+    """The window-specialised form checks dy against (N, C, OH, OW) instead of
+    reading past it (k=3, s=3 on 6x6 has 4 outputs per plane, not 9); the
+    scatter rejects indices outside the input."""
+    cfg = (8, 0)
+    x = torch.randint(0, 255, (1, 2, 6, 6), dtype=torch.uint8).cuda()
+    y, am = ops.maxpool2d(cfg, x, 3, 3)
+    with pytest.raises(ops._native.PnnInvalidArgument):
+        ops.maxpool2d_backward(cfg, y, am, x.shape, 2, 2)
+    with pytest.raises(ops._native.PnnInvalidArgument):
+        ops.maxpool2d_backward(cfg, y, am + 72, x.shape)
+    with pytest.raises(ops._native.PnnInvalidArgument):
+        ops.maxpool2d_backward(cfg, y, am - 100, x.shape)
 
 
 @pytest.mark.parametrize("cfg", [(16, 1), (12, 1), (8, 0), (10, 2), (12, 2)])
