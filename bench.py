@@ -39,6 +39,15 @@ UNIT = "posit-MAC/s"
 L2_FLUSH_BYTES = 512 << 20  # > 126 MB L2
 
 
+def workload_config(world: int) -> dict:
+    """The `config` both arms print (ours and --impl reference): the same workload."""
+    return {"workload": "BASELINE config 1: exact quire GEMM C=round(A.B), "
+                        "M=N=K=4096, posit(8,0) then posit(16,1)",
+            "M": M, "N": N, "K": K, "formats": ["posit(8,0)", "posit(16,1)"],
+            "l2": "flushed between timed steps (512 MiB write, untimed)",
+            "parallelism": f"replicas x{world}"}
+
+
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
@@ -294,10 +303,9 @@ def run_reference_impl(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * tsum / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int (posit codes)",
         "data": "synthetic (seeded uniform non-NaR codes)",
-        "config": {"workload": "BASELINE config 1: quire GEMM 4096^3, posit(8,0) then posit(16,1)",
-                   "parallelism": "reference ThreadPool (row split)"},
+        "config": workload_config(world),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
-                         "sample": sample},
+                         "sample": sample + " (reference ThreadPool row split)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -466,11 +474,7 @@ def main():
             "warmup": max(args.warmup, 3), "ms_per_step": t_ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "int8 digit MMA -> exact int quire",
             "data": "synthetic (seeded uniform over non-NaR codes)",
-            "config": {"workload": "BASELINE config 1: exact quire GEMM C=round(A.B), "
-                                   "M=N=K=4096, posit(8,0) then posit(16,1)",
-                       "M": M, "N": N, "K": K, "formats": ["posit(8,0)", "posit(16,1)"],
-                       "l2": "flushed between timed steps (512 MiB write, untimed)",
-                       "parallelism": f"replicas x{world}"},
+            "config": workload_config(world),
             "per_format": {f"posit({f[0]},{f[1]})": per_fmt[f] for f in FORMATS},
             "roofline": {"bound": "tensor", "kernel": f"quire_gemm_tc_kernel posit({dom[0]},{dom[1]})",
                          "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
