@@ -70,7 +70,8 @@ cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
 // Grow-only device scratch for the synchronous host entry points.
 constexpr int64_t kHostChunk = int64_t(1) << 22;  // codes per host narrow/widen chunk
 constexpr int kEvents = 16;
-constexpr int kPanels = 4;  // row panels of the host-entry GEMM (copy/compute pipeline)
+constexpr int kPanels = 4;  // default row panels of the host-entry GEMM (copy/compute pipeline)
+constexpr int kMaxPanels = 16;
 
 // Persistent host worker pool for the synchronous host entry points (the
 // reference's ThreadPool::parallel_for role, thread_pool.hpp:21-48: contiguous
@@ -79,7 +80,8 @@ class HostPool {
 public:
     HostPool() {
         unsigned n = std::thread::hardware_concurrency();
-        nworkers_ = int(n < 2 ? 1 : (n > 32 ? 32 : n));
+        if (const char* v = getenv("PNN_HOST_THREADS")) n = unsigned(atoi(v) > 0 ? atoi(v) : 1);
+        nworkers_ = int(n < 2 ? 1 : (n > 64 ? 64 : n));
         for (int i = 1; i < nworkers_; ++i) threads_.emplace_back([this, i] { loop(i); });
     }
     ~HostPool() {
@@ -109,6 +111,8 @@ public:
         done_cv_.wait(l, [this] { return pending_ == 0; });
         fn_ = nullptr;
     }
+
+    int workers() const { return nworkers_; }
 
 private:
     void loop(int idx) {
@@ -151,10 +155,24 @@ struct Scratch {
     size_t bytes = 0;
     void* hptr = nullptr;
     size_t hbytes = 0;
-    cudaStream_t stream = nullptr;   // GEMMs
-    cudaStream_t h2d = nullptr, d2h = nullptr;  // copy streams of the host entry
+    cudaStream_t stream = nullptr;                  // GEMMs + narrow / widen kernels
+    cudaStream_t h2d = nullptr, d2h = nullptr;      // packed-code copies (host-narrowed rows)
+    cudaStream_t h2d_raw = nullptr, d2h_raw = nullptr;  // uint64 copies (device-narrowed rows)
     cudaEvent_t ev[kEvents] = {};
-    cudaEvent_t evB = nullptr, evA[kPanels] = {}, evG[kPanels] = {};
+    cudaEvent_t evB = nullptr, evBr = nullptr, evA[kMaxPanels] = {}, evAr[kMaxPanels] = {},
+                evG[kMaxPanels] = {};
+    bool init() {
+        if (stream) return true;
+        for (cudaStream_t* sp : {&stream, &h2d, &d2h, &h2d_raw, &d2h_raw})
+            if (cudaStreamCreateWithFlags(sp, cudaStreamNonBlocking) != cudaSuccess) return false;
+        std::vector<cudaEvent_t*> evs = {&evB, &evBr};
+        for (auto& e : ev) evs.push_back(&e);
+        for (int i = 0; i < kMaxPanels; ++i)
+            for (cudaEvent_t* ep : {&evA[i], &evAr[i], &evG[i]}) evs.push_back(ep);
+        for (cudaEvent_t* ep : evs)
+            if (cudaEventCreateWithFlags(ep, cudaEventDisableTiming) != cudaSuccess) return false;
+        return true;
+    }
     void* reserve_host(size_t n) {
         if (n <= hbytes) return hptr;
         if (hptr) cudaFreeHost(hptr);
@@ -176,24 +194,62 @@ struct Scratch {
 };
 Scratch g_scratch;
 
-__global__ void narrow_codes_kernel(const uint64_t* __restrict__ src, void* __restrict__ dst,
-                                    int64_t n, int code_bytes, uint64_t mask) {
-    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+// Device halves of the host-entry copies: rows whose uint64 Tensor storage is
+// moved by the copy engine as is (pinned user buffers) are narrowed / widened
+// here, so the DMA engines carry part of the host-memory traffic that the host
+// threads would otherwise do alone.  n % 2 == 0 handled by the tail loop.
+template <typename CodeT>
+__global__ void narrow_codes_kernel(const uint64_t* __restrict__ src, CodeT* __restrict__ dst, int64_t n,
+                                    uint64_t mask) {
+    const int64_t n2 = n / 2;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n2;
          i += int64_t(gridDim.x) * blockDim.x) {
-        const uint64_t c = src[i] & mask;
-        if (code_bytes == 1) static_cast<uint8_t*>(dst)[i] = uint8_t(c);
-        else static_cast<uint16_t*>(dst)[i] = uint16_t(c);
+        const ulonglong2 v = reinterpret_cast<const ulonglong2*>(src)[i];
+        dst[2 * i] = CodeT(v.x & mask);
+        dst[2 * i + 1] = CodeT(v.y & mask);
     }
+    if (blockIdx.x == 0 && threadIdx.x == 0 && (n & 1)) dst[n - 1] = CodeT(src[n - 1] & mask);
 }
 
-__global__ void widen_codes_kernel(const void* __restrict__ src, uint64_t* __restrict__ dst,
-                                   int64_t n, int code_bytes) {
-    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
-         i += int64_t(gridDim.x) * blockDim.x) {
-        dst[i] = code_bytes == 1 ? uint64_t(static_cast<const uint8_t*>(src)[i])
-                                 : uint64_t(static_cast<const uint16_t*>(src)[i]);
-    }
+template <typename CodeT>
+__global__ void widen_codes_kernel(const CodeT* __restrict__ src, uint64_t* __restrict__ dst, int64_t n) {
+    const int64_t n2 = n / 2;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n2;
+         i += int64_t(gridDim.x) * blockDim.x)
+        reinterpret_cast<ulonglong2*>(dst)[i] = make_ulonglong2(src[2 * i], src[2 * i + 1]);
+    if (blockIdx.x == 0 && threadIdx.x == 0 && (n & 1)) dst[n - 1] = src[n - 1];
 }
+
+void launch_narrow(const uint64_t* src, void* dst, int64_t n, int cb, uint64_t mask, cudaStream_t st) {
+    if (n <= 0) return;
+    const int grid = int(std::min<int64_t>(148 * 8, (n / 2 + 255) / 256 + 1));
+    if (cb == 1) narrow_codes_kernel<uint8_t><<<grid, 256, 0, st>>>(src, static_cast<uint8_t*>(dst), n, mask);
+    else narrow_codes_kernel<uint16_t><<<grid, 256, 0, st>>>(src, static_cast<uint16_t*>(dst), n, mask);
+}
+
+void launch_widen(const void* src, uint64_t* dst, int64_t n, int cb, cudaStream_t st) {
+    if (n <= 0) return;
+    const int grid = int(std::min<int64_t>(148 * 8, (n / 2 + 255) / 256 + 1));
+    if (cb == 1) widen_codes_kernel<uint8_t><<<grid, 256, 0, st>>>(static_cast<const uint8_t*>(src), dst, n);
+    else widen_codes_kernel<uint16_t><<<grid, 256, 0, st>>>(static_cast<const uint16_t*>(src), dst, n);
+}
+
+bool host_pinned(const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
+double env_frac(const char* name, double dflt) {
+    const char* v = getenv(name);
+    if (!v) return dflt;
+    const double x = atof(v);
+    return x < 0 ? 0 : (x > 1 ? 1 : x);
+}
+
 
 int blocks_for(int64_t n) {
     int64_t b = (n + 255) / 256;
@@ -311,6 +367,19 @@ int pnn_quire_gemm_profiled(int nbits, int es, const void* A, const void* B, voi
     return rc;
 }
 
+// Reference-facing host entry (matmul over uint64 Tensor storage, tensor.hpp:10-14).
+// The call is bound by host-memory traffic (8 bytes per code in, 8 out), so
+// three resources share it, each on its own rows:
+//   * host threads narrow rows to packed codes in pinned staging (packed H2D)
+//     and widen packed results (packed D2H);
+//   * when the user buffers are pinned, the copy engines move a fraction of the
+//     rows as raw uint64 (H2D of inputs, D2H of results) and the GPU narrows /
+//     widens them -- PCIe and the DMA engines add bandwidth the host cores
+//     cannot reach on their own;
+//   * the GEMM runs per row panel as soon as the panel's A rows (both halves)
+//     and all of B are on the device.
+// Fractions: PNN_HOST_DMA_IN / PNN_HOST_DMA_OUT (share of rows moved raw),
+// PNN_HOST_PANELS; defaults measured on the B200 box.
 int pnn_matmul_host(int nbits, int es, const uint64_t* A, const uint64_t* B, uint64_t* C,
                     int64_t M, int64_t K, int64_t N) {
     if (int rc = check_fmt(nbits, es)) return rc;
@@ -321,37 +390,90 @@ int pnn_matmul_host(int nbits, int es, const uint64_t* A, const uint64_t* B, uin
         return PNN_OK;
     }
     std::lock_guard<std::mutex> lock(g_scratch.mu);
-    if (!g_scratch.stream) {
-        for (cudaStream_t* sp : {&g_scratch.stream, &g_scratch.h2d, &g_scratch.d2h})
-            if (cudaError_t e = cudaStreamCreateWithFlags(sp, cudaStreamNonBlocking))
-                return cuda_fail(e, "stream");
-        for (auto& ev : g_scratch.ev)
-            if (cudaError_t e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming))
-                return cuda_fail(e, "event");
-        for (int i = 0; i < kPanels; ++i)
-            for (cudaEvent_t* ep : {&g_scratch.evA[i], &g_scratch.evG[i]})
-                if (cudaError_t e = cudaEventCreateWithFlags(ep, cudaEventDisableTiming))
-                    return cuda_fail(e, "event");
-        if (cudaError_t e = cudaEventCreateWithFlags(&g_scratch.evB, cudaEventDisableTiming))
-            return cuda_fail(e, "event");
-    }
+    if (!g_scratch.init()) return cuda_fail(cudaGetLastError(), "matmul_host streams");
     cudaStream_t st = g_scratch.stream, sh = g_scratch.h2d, sd = g_scratch.d2h;
+    cudaStream_t shr = g_scratch.h2d_raw, sdr = g_scratch.d2h_raw;
     QuireGemmPlan p;
     if (quire_gemm_plan(nbits, es, M, N, K, 0, &p)) return fail(PNN_EUNSUPPORTED, "format");
     const int cb = nbits <= 8 ? 1 : 2;
+    const uint64_t mask = (uint64_t(1) << nbits) - 1;
+    // raw (DMA) shares: only for pinned user buffers and large operands
+    const bool big = M * K + K * N >= (int64_t(1) << 21);
+    // defaults balance PCIe (raw: 8 B per code, packed: cb) against the host
+    // threads (8 B per code): f = (8 Rp - cb Rc) / (8 Rp + (8 - cb) Rc) with the
+    // box's measured Rp ~ 51 GB/s (pinned H2D) and Rc ~ 100 GB/s (narrowing)
+    const double f_in_env = env_frac("PNN_HOST_DMA_IN", cb == 1 ? 0.28 : 0.20);
+    const double f_out_env = env_frac("PNN_HOST_DMA_OUT", cb == 1 ? 0.30 : 0.20);
+    const double f_in = big && host_pinned(A) && host_pinned(B) ? f_in_env : 0.0;
+    const double f_out = big && host_pinned(C) ? f_out_env : 0.0;
+    static const int panels_env = [] {
+        const char* v = getenv("PNN_HOST_PANELS");
+        const int x = v ? atoi(v) : kPanels;
+        return x < 1 ? 1 : (x > kMaxPanels ? kMaxPanels : x);
+    }();
+    const int P = M >= 256 * panels_env ? panels_env : 1;
+    const int64_t rows = (M + P - 1) / P;
+    const int64_t kc = K - int64_t(double(K) * f_in);  // B rows [0, kc) host-narrowed, [kc, K) raw
+    auto split_in = [&](int64_t r0, int64_t r1) { return r1 - int64_t(double(r1 - r0) * f_in); };
+    auto split_out = [&](int64_t r0, int64_t r1) { return r1 - int64_t(double(r1 - r0) * f_out); };
+    // raw staging: each segment starts 256-byte aligned (vector loads / stores)
+    auto seg = [](int64_t n) { return (n + 31) & ~int64_t(31); };
+    int64_t raw_in = seg((K - kc) * N), raw_out = 0;
+    for (int i = 0; i < P; ++i) {
+        const int64_t r0 = i * rows, r1 = std::min(M, r0 + rows);
+        if (r0 >= r1) break;
+        raw_in += seg((r1 - split_in(r0, r1)) * K);
+        raw_out += seg((r1 - split_out(r0, r1)) * N);
+    }
+    // GEMM workspace: the largest panel plan (a short panel may split K to fill the SMs)
+    size_t ws_bytes = 0;
+    for (int i = 0; i < P; ++i) {
+        const int64_t r0 = i * rows, r1 = std::min(M, r0 + rows);
+        if (r0 >= r1) break;
+        QuireGemmPlan pp;
+        quire_gemm_plan(nbits, es, r1 - r0, N, K, 0, &pp);
+        ws_bytes = std::max(ws_bytes, pp.workspace_bytes);
+    }
     auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
     const size_t pa = al(size_t(M * K) * cb), pb = al(size_t(K * N) * cb), pc = al(size_t(M * N) * cb);
-    uint8_t* base = static_cast<uint8_t*>(g_scratch.reserve(pa + pb + pc + p.workspace_bytes));
+    const size_t pri = al(size_t(raw_in) * 8), pro = al(size_t(raw_out) * 8);
+    uint8_t* base = static_cast<uint8_t*>(g_scratch.reserve(pa + pb + pc + pri + pro + ws_bytes));
     uint8_t* hbase = static_cast<uint8_t*>(g_scratch.reserve_host(pa + pb + pc));
     if (!base || !hbase) return fail(PNN_ECUDA, "matmul_host: allocation failed");
-    uint8_t *dA = base, *dB = base + pa, *dC = base + pa + pb, *ws = base + pa + pb + pc;
+    uint8_t *dA = base, *dB = base + pa, *dC = base + pa + pb;
+    uint64_t* rin = reinterpret_cast<uint64_t*>(base + pa + pb + pc);
+    uint64_t* rout = reinterpret_cast<uint64_t*>(base + pa + pb + pc + pri);
+    uint8_t* ws = base + pa + pb + pc + pri + pro;
     uint8_t *hA = hbase, *hB = hbase + pa, *hC = hbase + pa + pb;
-    const uint64_t mask = (uint64_t(1) << nbits) - 1;
     HostPool& pool = host_pool();
     cudaError_t e;
-    // Host threads narrow the uint64 Tensor storage (tensor.hpp:10-14) to packed
-    // codes chunk by chunk; each chunk's H2D copy (copy stream) overlaps the
-    // next chunk's narrowing.
+    static const bool prof = getenv("PNN_HOST_PROFILE") != nullptr;  // phase times to stderr
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    const auto t0 = now();
+    cudaEvent_t tev[2 * kMaxPanels + 1] = {};
+    if (prof) {
+        for (int i = 0; i <= 2 * P; ++i) cudaEventCreate(&tev[i]);
+        cudaEventRecord(tev[0], st);
+    }
+
+    // 1. every raw input share goes to the copy engine first (own stream: the
+    //    host-narrowed chunks do not queue behind it); the GPU narrows each.
+    uint64_t* rcur = rin;
+    auto raw_upload = [&](const uint64_t* src, uint8_t* ddst, int64_t n, cudaEvent_t ev) -> cudaError_t {
+        if (n > 0) {
+            if (cudaError_t err = cudaMemcpyAsync(rcur, src, size_t(n) * 8, cudaMemcpyHostToDevice, shr))
+                return err;
+        }
+        cudaEventRecord(ev, shr);
+        cudaStreamWaitEvent(st, ev, 0);
+        launch_narrow(rcur, ddst, n, cb, mask, st);
+        rcur += seg(n);
+        return cudaSuccess;
+    };
+    if ((e = raw_upload(B + kc * N, dB + kc * N * cb, (K - kc) * N, g_scratch.evBr)))
+        return cuda_fail(e, "H2D B raw");
+    // (the A raw shares follow B's packed chunks, below)
+    // 2. host-narrowed chunks: packed H2D overlaps the next chunk's narrowing
     auto upload = [&](const uint64_t* src, uint8_t* hdst, uint8_t* ddst, int64_t n) -> cudaError_t {
         for (int64_t c0 = 0; c0 < n; c0 += kHostChunk) {
             const int64_t c1 = std::min(n, c0 + kHostChunk);
@@ -364,36 +486,70 @@ int pnn_matmul_host(int nbits, int es, const uint64_t* A, const uint64_t* B, uin
         }
         return cudaSuccess;
     };
-    static const bool prof = getenv("PNN_HOST_PROFILE") != nullptr;  // phase times to stderr
-    auto now = [] { return std::chrono::steady_clock::now(); };
-    const auto t0 = now();
-    // Row panels: GEMM of panel i runs while the host narrows panel i+1 of A,
-    // and while it widens the results of earlier panels (three streams).
-    const int P = M >= 1024 ? kPanels : 1;
-    const int64_t rows = (M + P - 1) / P;
-    if ((e = upload(B, hB, dB, K * N))) return cuda_fail(e, "H2D B");
+    if ((e = upload(B, hB, dB, kc * N))) return cuda_fail(e, "H2D B");
     cudaEventRecord(g_scratch.evB, sh);
     cudaStreamWaitEvent(st, g_scratch.evB, 0);
+    // B gates every panel: the A raw shares start once B's packed chunks are
+    // queued, so they do not take PCIe bandwidth from B
+    cudaStreamWaitEvent(shr, g_scratch.evB, 0);
+    // queue all A raw shares now (the copy engine runs ahead of the host threads)
     for (int i = 0; i < P; ++i) {
         const int64_t r0 = i * rows, r1 = std::min(M, r0 + rows);
         if (r0 >= r1) break;
-        if ((e = upload(A + r0 * K, hA + r0 * K * cb, dA + r0 * K * cb, (r1 - r0) * K)))
+        const int64_t s = split_in(r0, r1);
+        if (r1 > s) {
+            if ((e = cudaMemcpyAsync(rcur, A + s * K, size_t((r1 - s) * K) * 8, cudaMemcpyHostToDevice, shr)))
+                return cuda_fail(e, "H2D A raw");
+        }
+        cudaEventRecord(g_scratch.evAr[i], shr);
+        rcur += seg((r1 - s) * K);
+    }
+    uint64_t* acur = rin + seg((K - kc) * N);
+    QuireGemmPlan p0{};
+    uint64_t* ocur = rout;
+    for (int i = 0; i < P; ++i) {
+        const int64_t r0 = i * rows, r1 = std::min(M, r0 + rows);
+        if (r0 >= r1) break;
+        const int64_t s = split_in(r0, r1);
+        if ((e = upload(A + r0 * K, hA + r0 * K * cb, dA + r0 * K * cb, (s - r0) * K)))
             return cuda_fail(e, "H2D A");
         cudaEventRecord(g_scratch.evA[i], sh);
         cudaStreamWaitEvent(st, g_scratch.evA[i], 0);
+        cudaStreamWaitEvent(st, g_scratch.evAr[i], 0);
+        launch_narrow(acur, dA + s * K * cb, (r1 - s) * K, cb, mask, st);
+        acur += seg((r1 - s) * K);
+        if (prof) cudaEventRecord(tev[2 * i + 1], st);
+        // B's digit image is packed by the first panel and reused while the
+        // panel plans share the workspace layout
+        QuireGemmPlan pp;
+        quire_gemm_plan(nbits, es, r1 - r0, N, K, 0, &pp);
+        const bool same = i > 0 && pp.off_b == p0.off_b && pp.b_img_bytes == p0.b_img_bytes &&
+                          pp.off_col_nar == p0.off_col_nar && pp.off_flags == p0.off_flags &&
+                          pp.D == p0.D && pp.kbt == p0.kbt && pp.ntiles == p0.ntiles;
+        if (i == 0) p0 = pp;
         int rc = quire_gemm_launch(nbits, es, dA + r0 * K * cb, dB, dC + r0 * N * cb, r1 - r0, N, K, K, N, N,
-                                   ws, p.workspace_bytes, 0, st, nullptr);
+                                   ws, ws_bytes, 0, st, nullptr, /*pack_b=*/!same);
         if (rc) return rc == 4 ? cuda_fail(cudaGetLastError(), "matmul launch") : fail(rc, "matmul");
+        // raw output share of this panel: widened on the GPU, DMA'd into C
+        const int64_t so = split_out(r0, r1);
+        launch_widen(dC + so * N * cb, ocur, (r1 - so) * N, cb, st);
         cudaEventRecord(g_scratch.evG[i], st);
+        if (r1 > so) {
+            cudaStreamWaitEvent(sdr, g_scratch.evG[i], 0);
+            if ((e = cudaMemcpyAsync(C + so * N, ocur, size_t((r1 - so) * N) * 8, cudaMemcpyDeviceToHost, sdr)))
+                return cuda_fail(e, "D2H C raw");
+        }
+        ocur += seg((r1 - so) * N);
+        if (prof) cudaEventRecord(tev[2 * i + 2], st);
     }
     const auto t1 = now();
-    // D2H per panel (after its GEMM) in chunks; widen chunk j on the host while
-    // chunk j+1 is in flight.
+    // 3. host-widened share of each panel: chunked packed D2H, widen chunk j
+    //    while chunk j+1 is in flight
     for (int i = 0; i < P; ++i) {
         const int64_t r0 = i * rows, r1 = std::min(M, r0 + rows);
         if (r0 >= r1) break;
         cudaStreamWaitEvent(sd, g_scratch.evG[i], 0);
-        const int64_t off = r0 * N, n = (r1 - r0) * N;
+        const int64_t off = r0 * N, n = (split_out(r0, r1) - r0) * N;
         const int64_t nch = (n + kHostChunk - 1) / kHostChunk;
         for (int64_t c = 0; c < nch; c += kEvents) {
             const int64_t cend = std::min(nch, c + kEvents);
@@ -413,13 +569,30 @@ int pnn_matmul_host(int nbits, int es, const uint64_t* A, const uint64_t* B, uin
             }
         }
     }
-    for (cudaStream_t s2 : {sh, st, sd})
+    const auto t2 = now();
+    for (cudaStream_t s2 : {sh, shr, st, sd, sdr})
         if ((e = cudaStreamSynchronize(s2))) return cuda_fail(e, "matmul_host sync");
     if (prof) {
-        const auto t2 = now();
-        fprintf(stderr, "[pnn_matmul_host] narrow+H2D+GEMM issue %.2f ms, D2H+widen %.2f ms\n",
+        const auto t3 = now();
+        fprintf(stderr,
+                "[pnn_matmul_host] posit(%d,%d) P=%d f_in=%.2f f_out=%.2f threads=%d: narrow+issue %.2f ms, "
+                "widen %.2f ms, final sync %.2f ms\n",
+                nbits, es, P, f_in, f_out, pool.workers(),
                 std::chrono::duration<double, std::milli>(t1 - t0).count(),
-                std::chrono::duration<double, std::milli>(t2 - t1).count());
+                std::chrono::duration<double, std::milli>(t2 - t1).count(),
+                std::chrono::duration<double, std::milli>(t3 - t2).count());
+        // device timeline: panel i's GEMM starts after its inputs (tev[2i+1]), ends at tev[2i+2]
+        std::string tl;
+        for (int i = 0; i < P; ++i) {
+            float a = 0, b = 0;
+            cudaEventElapsedTime(&a, tev[0], tev[2 * i + 1]);
+            cudaEventElapsedTime(&b, tev[0], tev[2 * i + 2]);
+            char buf[64];
+            snprintf(buf, sizeof buf, " [%.2f..%.2f]", a, b);
+            tl += buf;
+        }
+        fprintf(stderr, "[pnn_matmul_host]   gemm panels (ms from issue start):%s\n", tl.c_str());
+        for (int i = 0; i <= 2 * P; ++i) cudaEventDestroy(tev[i]);
     }
     return PNN_OK;
 }

@@ -13,8 +13,9 @@ int quire_gemm_plan(int nbits, int es, int64_t M, int64_t N, int64_t K, int64_t 
 int quire_gemm_launch(int nbits, int es, const void* A, const void* B, void* C, int64_t M,
                       int64_t N, int64_t K, int64_t lda, int64_t ldb, int64_t ldc, void* workspace,
                       size_t workspace_bytes, int64_t max_kb_per_split, cudaStream_t st,
-                      QuireGemmStats* stats) {
+                      QuireGemmStats* stats, bool pack_b) {
     GemmArgs g;
+    g.pack_b = pack_b;
     g.f = make_fmt(nbits, es);
     g.M = M;
     g.N = N;

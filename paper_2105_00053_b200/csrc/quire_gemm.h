@@ -30,10 +30,12 @@ int quire_gemm_plan(int nbits, int es, int64_t M, int64_t N, int64_t K, int64_t 
 
 // A (M x K, lda), B (K x N, ldb), C (M x N, ldc): device pointers to packed
 // codes (uint8 for nbits <= 8, else uint16).  0 ok, 2 unsupported format,
-// 3 workspace too small, 4 CUDA launch error.
+// 3 workspace too small, 4 CUDA launch error.  pack_b = false reuses B's
+// digit image and NaR flags left in the workspace by an earlier launch of the
+// same B whose plan had the same workspace layout (row panels of one GEMM).
 int quire_gemm_launch(int nbits, int es, const void* A, const void* B, void* C, int64_t M,
                       int64_t N, int64_t K, int64_t lda, int64_t ldb, int64_t ldc, void* workspace,
                       size_t workspace_bytes, int64_t max_kb_per_split, cudaStream_t st,
-                      QuireGemmStats* stats);
+                      QuireGemmStats* stats, bool pack_b = true);
 
 }  // namespace pnn_b200

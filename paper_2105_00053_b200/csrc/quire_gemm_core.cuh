@@ -890,6 +890,8 @@ struct GemmArgs {
     bool row_nar, col_nar;     // apply operand NaR flags in the epilogue
     unsigned __int128* raw_words = nullptr;  // raw mode: exact W-bit quire words out
     uint8_t* raw_nar = nullptr;              //           and the NaR mask
+    bool pack_b = true;  // false: B's digit image, column NaR flags and B flags are already in
+                         // the workspace (an earlier launch with the same plan layout and B)
 };
 
 template <int D>
@@ -974,7 +976,13 @@ cudaError_t launch_generic(const QuireGemmPlan& p, const GemmArgs& g, FA fa, FB 
     const bool use_partial = p.splits > 1 || g.raw_words != nullptr;
     auto* partial = use_partial ? reinterpret_cast<unsigned __int128*>(ws + p.off_partial) : nullptr;
     cudaError_t e;
-    if ((e = cudaMemsetAsync(rnar, 0, p.off_flags + 16 - p.off_row_nar, st)) != cudaSuccess) return e;
+    if (g.pack_b) {
+        if ((e = cudaMemsetAsync(rnar, 0, p.off_flags + 16 - p.off_row_nar, st)) != cudaSuccess) return e;
+    } else {  // keep B's column NaR flags and flags[1], flags[3]
+        if ((e = cudaMemsetAsync(rnar, 0, p.off_col_nar - p.off_row_nar, st)) != cudaSuccess) return e;
+        if ((e = cudaMemsetAsync(flags, 0, 1, st)) != cudaSuccess) return e;
+        if ((e = cudaMemsetAsync(flags + 2, 0, 1, st)) != cudaSuccess) return e;
+    }
     if (stats) cudaEventRecord(stats->ev[0], st);
     const int64_t a_work = p.mtiles_alloc * p.kbt, b_work = p.ntiles * p.kbt;  // upper bounds
     // Formats wider than the shared-memory LUT decode arithmetically: a global
@@ -991,14 +999,17 @@ cudaError_t launch_generic(const QuireGemmPlan& p, const GemmArgs& g, FA fa, FB 
         pack_kernel<D, kBM, CodeT, FA, 4><<<ga, 256, 0, st>>>(fa, g.M, g.K, f, a_img, rnar, flags,
                                                                p.mtiles_alloc, p.kbt, glut,
                                                                reduced ? flags + 2 : nullptr, kRed);
-        pack_kernel<D, Geo::NT, CodeT, FB, 4><<<gb, 256, 0, st>>>(fb, g.N, g.K, f, b_img, cnar, flags + 1,
-                                                                   p.ntiles, p.kbt, glut,
-                                                                   reduced ? flags + 3 : nullptr, kRed);
+        if (g.pack_b)
+            pack_kernel<D, Geo::NT, CodeT, FB, 4><<<gb, 256, 0, st>>>(fb, g.N, g.K, f, b_img, cnar, flags + 1,
+                                                                       p.ntiles, p.kbt, glut,
+                                                                       reduced ? flags + 3 : nullptr, kRed);
     } else {
         pack_kernel<D, kBM, CodeT, FA><<<ga, 256, 0, st>>>(fa, g.M, g.K, f, a_img, rnar, flags, p.mtiles_alloc,
                                                            p.kbt, glut, reduced ? flags + 2 : nullptr, kRed);
-        pack_kernel<D, Geo::NT, CodeT, FB><<<gb, 256, 0, st>>>(fb, g.N, g.K, f, b_img, cnar, flags + 1, p.ntiles,
-                                                               p.kbt, glut, reduced ? flags + 3 : nullptr, kRed);
+        if (g.pack_b)
+            pack_kernel<D, Geo::NT, CodeT, FB><<<gb, 256, 0, st>>>(fb, g.N, g.K, f, b_img, cnar, flags + 1,
+                                                                   p.ntiles, p.kbt, glut,
+                                                                   reduced ? flags + 3 : nullptr, kRed);
     }
     if (stats) cudaEventRecord(stats->ev[1], st);
     // D <= 3 implies R <= 11, hence W <= 64: no 128-bit instantiation needed.

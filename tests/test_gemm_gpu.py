@@ -290,3 +290,49 @@ def test_cta_pair_kernel_parity(cuda, po):
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300, env=env,
                        cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     assert r.returncode == 0 and "pair ok" in r.stdout, r.stderr[-2000:]
+
+
+_HOST_SPLIT_CODE = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, '.')
+from paper_2105_00053_b200 import _native, ops
+L = _native.lib()
+rng = np.random.default_rng(11)
+for (n, es) in [(8, 0), (16, 1)]:
+    M, K, N = 1536, 1031, 1037
+    nar = 1 << (n - 1)
+    A = rng.integers(0, 1 << n, (M, K)).astype(np.uint64); A[A == nar] = 0
+    B = rng.integers(0, 1 << n, (K, N)).astype(np.uint64); B[B == nar] = 0
+    A[5, 7] = nar  # one NaR row
+    cfg = ops.PositConfig(n, es)
+    want = ops.quire_gemm(cfg, torch.from_numpy(A.astype(cfg.np_code_dtype)).cuda(),
+                          torch.from_numpy(B.astype(cfg.np_code_dtype)).cuda()).cpu().numpy().astype(np.uint64)
+    pa = torch.from_numpy(A.view(np.int64)).pin_memory()
+    pb = torch.from_numpy(B.view(np.int64)).pin_memory()
+    pc = torch.full((M, N), -1, dtype=torch.int64).pin_memory()
+    _native.check(L.pnn_matmul_host(n, es, pa.data_ptr(), pb.data_ptr(), pc.data_ptr(), M, K, N))
+    assert (pc.numpy().view(np.uint64) == want).all(), ("pinned", n, es)
+    C2 = np.full((M, N), 7, np.uint64)  # pageable: host threads only
+    _native.check(L.pnn_matmul_host(n, es, A.ctypes.data, B.ctypes.data, C2.ctypes.data, M, K, N))
+    assert (C2 == want).all(), ("pageable", n, es)
+print('split ok')
+"""
+
+
+@pytest.mark.parametrize("env", [{}, {"PNN_HOST_DMA_IN": "1", "PNN_HOST_DMA_OUT": "1", "PNN_HOST_PANELS": "3"},
+                                 {"PNN_HOST_DMA_IN": "0", "PNN_HOST_DMA_OUT": "0", "PNN_HOST_PANELS": "1",
+                                  "PNN_HOST_THREADS": "3"},
+                                 {"PNN_HOST_DMA_IN": "0.77", "PNN_HOST_DMA_OUT": "0.13", "PNN_HOST_PANELS": "5"}])
+def test_matmul_host_dma_split(cuda, po, env):
+    """pnn_matmul_host with pinned Tensor storage: rows moved raw by the copy
+    engines (device-narrowed / -widened) and rows narrowed / widened by host
+    threads give the device GEMM's result for every split, panel count and
+    thread count; pageable buffers take the host-thread path."""
+    import os
+    import subprocess
+    import sys
+
+    r = subprocess.run([sys.executable, "-c", _HOST_SPLIT_CODE], capture_output=True, text=True, timeout=600,
+                       env=dict(os.environ, **env),
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0 and "split ok" in r.stdout, r.stderr[-3000:]
