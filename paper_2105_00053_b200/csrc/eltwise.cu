@@ -10,6 +10,9 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <map>
+#include <mutex>
+#include <tuple>
 
 #include "../../include/pnn_b200.h"
 #include "eltwise_common.cuh"
@@ -614,6 +617,87 @@ __global__ void sgd_multi_kernel(PositFmt fo, int bo, PositFmt fg, int bg, uint3
     }
 }
 
+// ---- SGD through per-format tables (the optimizer step's rounding work is
+// per element ALU-bound, not HBM-bound: a table per format pair replaces the
+// two code-only operations and leaves one exact subtraction + one rounding):
+//   m_lut[g]  = p_mul(fo, lr, p_convert(fg, fo, g))   (lr fixed per call)
+//   c_lut[w]  = p_convert(fo, fc, w)                   (stage copies)
+//   w' = p_sub(fo, w, m) = round_o(X_w - X_m), the exact difference of the
+//   integer images (|X| <= 2^2R, 2R + 1 <= 63) rounded once (posit.cpp:437-457
+//   rounds the exact result of every op once; x_to_posit_lut = pack_round).
+// Each table entry is computed by the scalar ops themselves, so the path is
+// the sgd_kernel arithmetic, entry for entry.
+__global__ void sgd_m_lut_kernel(PositFmt fo, PositFmt fg, uint32_t lr, uint16_t* __restrict__ lut) {
+    GRID_STRIDE(c, int64_t(1) << fg.nbits) { lut[c] = uint16_t(p_mul(fo, lr, p_convert(fg, fo, uint32_t(c)))); }
+}
+__global__ void copy_lut_kernel(PositFmt fo, PositFmt fc, uint16_t* __restrict__ lut) {
+    GRID_STRIDE(c, int64_t(1) << fo.nbits) { lut[c] = uint16_t(p_convert(fo, fc, uint32_t(c))); }
+}
+
+// round(X 2^-R) for an int64 integer image (|X| < 2^63) through the rounding table
+__device__ __forceinline__ uint32_t x_to_posit_lut(const PositFmt& f, int64_t X, const uint4* lut) {
+    uint32_t lo = uint32_t(uint64_t(X)), hi = uint32_t(uint64_t(X) >> 32);
+    const uint32_t s = uint32_t(int32_t(hi) >> 31);
+    uint32_t ml = lo ^ s, mh = hi ^ s;
+    asm("add.cc.u32 %0, %0, %2;\n\taddc.u32 %1, %1, 0;" : "+r"(ml), "+r"(mh) : "r"(s & 1u));
+    const bool hz = mh == 0;
+    const int lzh = __clz(mh), lzl = __clz(ml);
+    const uint32_t sig = hz ? (ml << (lzl & 31)) : __funnelshift_l(ml, mh, lzh);
+    const bool sticky = !hz && (ml << (lzh & 31)) != 0;
+    const int top = hz ? 31 - lzl : 63 - lzh;
+    const uint32_t c = pack_lut(f, lut, top - f.R, sig, sticky, s != 0);
+    return (ml | mh) == 0 ? 0u : c;
+}
+
+struct SgdLuts {
+    const uint16_t* m;   // [2^fg.nbits]
+    const uint16_t* c1;  // [2^fo.nbits] or null
+    const uint16_t* c2;
+};
+
+__global__ void sgd_lut_kernel(PositFmt fo, int bo, int bg, int b1, int b2, const __grid_constant__ SgdSegs segs,
+                               SgdLuts t) {
+    __shared__ uint4 s_lut[kPackLutEntries];
+    build_pack_lut(fo, s_lut, threadIdx.x, blockDim.x);
+    __shared__ int64_t s_start[kSgdMaxSeg + 1];
+    __shared__ const void* s_ptr[4][kSgdMaxSeg];
+    for (int i = threadIdx.x; i <= segs.count; i += blockDim.x) s_start[i] = segs.start[i];
+    for (int i = threadIdx.x; i < segs.count; i += blockDim.x) {
+        s_ptr[0][i] = segs.master[i];
+        s_ptr[1][i] = segs.grad[i];
+        s_ptr[2][i] = segs.copy1[i];
+        s_ptr[3][i] = segs.copy2[i];
+    }
+    __syncthreads();
+    const uint32_t nar = 1u << (fo.nbits - 1);
+    const int64_t total = s_start[segs.count];
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        int lo = 0, hi = segs.count - 1;  // last segment with start <= i
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (s_start[mid] <= i) lo = mid;
+            else hi = mid - 1;
+        }
+        const int64_t k = i - s_start[lo];
+        void* const master = const_cast<void*>(s_ptr[0][lo]);
+        const uint32_t m = __ldg(t.m + load_any(s_ptr[1][lo], k, bg));
+        const uint32_t w = load_any(master, k, bo);
+        uint32_t r;
+        if (w == nar || m == nar) {
+            r = nar;
+        } else {
+            int64_t Xw, Xm;
+            decode_x(w, fo, Xw);
+            decode_x(m, fo, Xm);
+            r = x_to_posit_lut(fo, Xw - Xm, s_lut);
+        }
+        store_any(master, k, bo, r);
+        if (s_ptr[2][lo]) store_any(const_cast<void*>(s_ptr[2][lo]), k, b1, __ldg(t.c1 + r));
+        if (s_ptr[3][lo]) store_any(const_cast<void*>(s_ptr[3][lo]), k, b2, __ldg(t.c2 + r));
+    }
+}
+
 // avgpool2d, tensor_ops.cpp:672-691: window sum (quire: exact, one rounding;
 // sequential: add chain in (ky,kx) order) then mul by the caller-quantized
 // reciprocal (scale, :763-769).
@@ -716,6 +800,46 @@ int grid1(int64_t n) {
 }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+// SGD tables per (fo, fg, lr) and per (fo, copy format), device-resident for the
+// life of the process.  Built synchronously on the caller's stream the first
+// time; during stream capture a missing table means "use the scalar path".
+bool sgd_luts(const PositFmt& fo, const PositFmt& fg, uint32_t lr, const PositFmt* f1, const PositFmt* f2,
+              cudaStream_t st, SgdLuts* out) {
+    static std::mutex mu;
+    static std::map<std::tuple<int, int, int, int, int, uint32_t>, uint16_t*> cache;
+    std::lock_guard<std::mutex> lock(mu);
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    const bool capturing = cs != cudaStreamCaptureStatusNone;
+    auto get = [&](int kind, const PositFmt& a, const PositFmt& b, uint32_t l) -> uint16_t* {
+        const auto key = std::make_tuple(kind, a.nbits, a.es, b.nbits, b.es, l);
+        auto it = cache.find(key);
+        if (it != cache.end()) return it->second;
+        if (capturing) return nullptr;
+        uint16_t* p = nullptr;
+        const int64_t n = int64_t(1) << (kind == 0 ? b.nbits : a.nbits);
+        if (cudaMalloc(&p, size_t(n) * 2) != cudaSuccess) {
+            cudaGetLastError();
+            return nullptr;
+        }
+        if (kind == 0) sgd_m_lut_kernel<<<grid1(n), 256, 0, st>>>(a, b, l, p);
+        else copy_lut_kernel<<<grid1(n), 256, 0, st>>>(a, b, p);
+        if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(st) != cudaSuccess) {
+            cudaFree(p);
+            return nullptr;
+        }
+        cache[key] = p;
+        return p;
+    };
+    out->m = get(0, fo, fg, lr);
+    out->c1 = f1 ? get(1, fo, *f1, 0) : nullptr;
+    out->c2 = f2 ? get(1, fo, *f2, 0) : nullptr;
+    return out->m && (!f1 || out->c1) && (!f2 || out->c2);
+}
 
 int launched(const char* what) {
     const cudaError_t e = cudaGetLastError();
@@ -1000,6 +1124,13 @@ int pnn_sgd_step_multi(int opt_nbits, int opt_es, int g_nbits, int g_es, uint32_
                      2 * fo.R >= fg.R && 2 * fo.R <= 60 && fo.W <= 128 && fg.R + 2 * fo.R + 1 < fo.W &&
                      4 * fo.R + 1 < fo.W && 3 * fo.R + 2 < fo.W;
     if (fast) fast |= (has1 && copy_ok(f1) ? 2 : 0) | (has2 && copy_ok(f2) ? 4 : 0);
+    // table path: images within int64 (2R_o + 1 <= 63), 16-bit tables; the
+    // tables are built on first use outside stream capture (a CUDA graph
+    // replays the launch with the tables already resident)
+    SgdLuts luts{};
+    const bool lut_path = grad_scale_log2 == 0 && 2 * fo.R + 1 <= 63 &&
+                          sgd_luts(fo, fg, lr_code, has1 ? &f1 : nullptr, has2 ? &f2 : nullptr,
+                                   (cudaStream_t)stream, &luts);
     for (int base = 0; base < count; base += kSgdMaxSeg) {
         SgdSegs sg{};
         sg.count = 0;
@@ -1017,6 +1148,11 @@ int pnn_sgd_step_multi(int opt_nbits, int opt_es, int g_nbits, int g_es, uint32_
         }
         sg.start[sg.count] = tot;
         if (tot == 0) continue;
+        if (lut_path) {
+            sgd_lut_kernel<<<grid1(tot), 256, 0, (cudaStream_t)stream>>>(
+                fo, bytes_of(opt_nbits), bytes_of(g_nbits), bytes_of(f1.nbits), bytes_of(f2.nbits), sg, luts);
+            continue;
+        }
         sgd_multi_kernel<<<grid1(tot), 256, 0, (cudaStream_t)stream>>>(
             fo, bytes_of(opt_nbits), fg, bytes_of(g_nbits), lr_code, f1, bytes_of(f1.nbits), f2,
             bytes_of(f2.nbits), grad_scale_log2, sg, fast);

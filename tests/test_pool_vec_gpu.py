@@ -103,3 +103,35 @@ def test_bias_grad_gated(cuda, cfg, gcfg, shape):
     g2 = ops.conv2d_bias_grad_gated(cfg, dy, gcfg, gate, raw=True)
     w2 = ops.conv2d_bias_grad(cfg, ops.relu_bwd(gcfg, gate, cfg, dy), raw=True)
     assert all(torch.equal(a, b) for a, b in zip(g2, w2))
+
+
+@pytest.mark.parametrize("opt,grad,copies", [((16, 1), (12, 1), [(8, 1), (12, 1)]),
+                                             ((12, 1), (8, 0), [(8, 0)]),
+                                             ((16, 1), (16, 1), [(8, 0), (16, 1)])])
+def test_sgd_table_path_exhaustive_master_codes(cuda, opt, grad, copies):
+    """The table-driven SGD launch (m = lr * convert(g) by table, w - m exact on
+    integer images, copies by table) == the scalar-op SGD for every master code
+    against a spread of gradient codes (incl. NaR, 0, extremes) and several lr."""
+    rng = np.random.default_rng(17)
+    n_o = 1 << opt[0]
+    gsel = np.concatenate([[0, 1, (1 << grad[0]) - 1, 1 << (grad[0] - 1), (1 << (grad[0] - 1)) - 1,
+                            (1 << (grad[0] - 1)) + 1], rng.integers(0, 1 << grad[0], 10)])
+    w = np.tile(np.arange(n_o, dtype=np.uint64), len(gsel))
+    g = np.repeat(gsel.astype(np.uint64), n_o)
+    one = 1 << (opt[0] - 2)
+    for lr in (one >> 4, one, rng.integers(1, 1 << (opt[0] - 1))):
+        ms = [dev(opt, w[:len(w) // 2]), dev(opt, w[len(w) // 2:])]
+        gs = [dev(grad, g[:len(g) // 2]), dev(grad, g[len(g) // 2:])]
+        ref_m = [m.clone() for m in ms]
+        ref_c = [tuple(torch.zeros(m.numel(), dtype=ops._cfg(c).code_dtype, device="cuda") for c in copies)
+                 for m in ms]
+        got_c = [tuple(torch.zeros(m.numel(), dtype=ops._cfg(c).code_dtype, device="cuda") for c in copies)
+                 for m in ms]
+        for m, gg, cs in zip(ref_m, gs, ref_c):
+            ops.sgd_step(opt, m, grad, gg, int(lr), list(zip(copies, cs)))
+        ops.sgd_step_multi(opt, grad, int(lr), ms, gs, copies, got_c)
+        for a, b in zip(ms, ref_m):
+            assert torch.equal(a, b), lr
+        for a, b in zip(got_c, ref_c):
+            for x, y in zip(a, b):
+                assert torch.equal(x, y), lr

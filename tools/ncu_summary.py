@@ -47,6 +47,22 @@ def launches(path):
     return {"total_us": round(tot, 1), "kernels": out}
 
 
+def sequence(path):
+    """Every launch in order: kernel, grid, time (us) -- maps launches to layers."""
+    rows = list(csv.reader(open(path)))
+    h = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
+    hdr = rows[h]
+    ki, vi = hdr.index("Kernel Name"), hdr.index("Metric Value")
+    gi = hdr.index("Grid Size") if "Grid Size" in hdr else None
+    out = []
+    for r in rows[h + 1:]:
+        if len(r) <= vi:
+            continue
+        out.append({"kernel": r[ki].split("(")[0].replace("void ", "").strip()[:90],
+                    "grid": r[gi] if gi is not None else "", "us": round(float(r[vi].replace(",", "")) / 1e3, 2)})
+    return out
+
+
 def report(path):
     txt = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(txt)))
@@ -69,6 +85,10 @@ def report(path):
 
 
 if __name__ == "__main__":
+    if sys.argv[1] == "sequence":
+        for x in sequence(sys.argv[2]):
+            print(f"{x['us']:9.2f}  {x['grid']:>16s}  {x['kernel']}")
+        sys.exit(0)
     if sys.argv[1] == "launches":
         print(json.dumps(launches(sys.argv[2]), indent=1))
     else:
