@@ -241,10 +241,11 @@ __global__ void __launch_bounds__(256) bias_grad_cols_kernel(
     const int64_t slice = blockIdx.y, per = (N + slices - 1) / slices;
     const int64_t n0 = slice * per, n1 = min(N, n0 + per);
     const uint32_t nar_code = 1u << (f.nbits - 1);
+    // four independent load -> decode chains per step (the row loop is latency bound)
     __int128 acc = 0;
     bool nar = false;
-    for (int64_t n = n0; n < n1; ++n) {
-        const uint32_t code = uint32_t(dy[n * F + ch]);
+    int64_t n = n0;
+    auto term = [&](uint32_t code) -> int64_t {
         int64_t X;
         if (xlut != nullptr) {
             X = __ldg(xlut + code);
@@ -252,8 +253,15 @@ __global__ void __launch_bounds__(256) bias_grad_cols_kernel(
         } else {
             nar |= decode_x(code, f, X);
         }
-        acc += X;
+        return X;
+    };
+    for (; n + 4 <= n1; n += 4) {
+        const uint32_t c0 = uint32_t(dy[n * F + ch]), c1 = uint32_t(dy[(n + 1) * F + ch]);
+        const uint32_t c2 = uint32_t(dy[(n + 2) * F + ch]), c3 = uint32_t(dy[(n + 3) * F + ch]);
+        const int64_t x0 = term(c0), x1 = term(c1), x2 = term(c2), x3 = term(c3);
+        acc += (__int128)x0 + x1 + (__int128)x2 + x3;
     }
+    for (; n < n1; ++n) acc += term(uint32_t(dy[n * F + ch]));
     partial[ch * slices + slice] = (unsigned __int128)acc;
     if (nar) nar_out[ch] = 1;
 }
@@ -452,12 +460,22 @@ __global__ void bias_grad_final_kernel(const unsigned __int128* __restrict__ par
                                        const uint8_t* __restrict__ nar_in, int64_t F, PositFmt f,
                                        CodeT* __restrict__ out, unsigned __int128* raw_words,
                                        uint8_t* raw_nar) {
+    // a warp per channel: lanes sum interleaved partials (coalesced 16-byte
+    // loads), then a shuffle tree; exact 128-bit integer sums in any order
     const unsigned __int128 one = 1;
     const unsigned __int128 wmask = f.W >= 128 ? ~(unsigned __int128)0 : ((one << f.W) - 1);
-    for (int64_t ch = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; ch < F;
-         ch += int64_t(gridDim.x) * blockDim.x) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t ch = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5; ch < F;
+         ch += (int64_t(gridDim.x) * blockDim.x) >> 5) {
         unsigned __int128 s = 0;
-        for (int i = 0; i < slices; ++i) s += partial[ch * slices + i];
+        for (int i = lane; i < slices; i += 32) s += partial[ch * slices + i];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const uint64_t l2 = __shfl_xor_sync(0xFFFFFFFFu, uint64_t(s), o);
+            const uint64_t h2 = __shfl_xor_sync(0xFFFFFFFFu, uint64_t(s >> 64), o);
+            s += (unsigned __int128)l2 | ((unsigned __int128)h2 << 64);
+        }
+        if (lane != 0) continue;
         const unsigned __int128 q = (s << f.R) & wmask;  // accumulate_value: X * 2^R
         if (raw_words) {
             raw_words[ch] = q;
@@ -908,13 +926,13 @@ int pnn_bias_grad(int nbits, int es, const void* dy, int64_t N, int64_t F, int64
     if (P == 1 && nbits <= 8) {
         bias_grad_cols_kernel<uint8_t><<<cgrid, 256, 0, st>>>((const uint8_t*)dy, N, F, f, slices,
                                                               xlut, partial, nar);
-        bias_grad_final_kernel<uint8_t><<<grid_for(F, 128), 128, 0, st>>>(
+        bias_grad_final_kernel<uint8_t><<<grid_for(F * 32, 256), 256, 0, st>>>(
             partial, slices, nar, F, f, (uint8_t*)db, (unsigned __int128*)raw_words,
             (uint8_t*)raw_nar);
     } else if (P == 1) {
         bias_grad_cols_kernel<uint16_t><<<cgrid, 256, 0, st>>>((const uint16_t*)dy, N, F, f,
                                                                slices, xlut, partial, nar);
-        bias_grad_final_kernel<uint16_t><<<grid_for(F, 128), 128, 0, st>>>(
+        bias_grad_final_kernel<uint16_t><<<grid_for(F * 32, 256), 256, 0, st>>>(
             partial, slices, nar, F, f, (uint16_t*)db, (unsigned __int128*)raw_words,
             (uint8_t*)raw_nar);
     } else if (chan) {
@@ -945,13 +963,13 @@ int pnn_bias_grad(int nbits, int es, const void* dy, int64_t N, int64_t F, int64
     } else if (nbits <= 8) {
         bias_grad_partial_kernel<uint8_t><<<grid, 256, 0, st>>>((const uint8_t*)dy, N, F, P, f,
                                                                  slices, xlut, partial, nar);
-        bias_grad_final_kernel<uint8_t><<<grid_for(F, 128), 128, 0, st>>>(
+        bias_grad_final_kernel<uint8_t><<<grid_for(F * 32, 256), 256, 0, st>>>(
             partial, slices, nar, F, f, (uint8_t*)db, (unsigned __int128*)raw_words,
             (uint8_t*)raw_nar);
     } else {
         bias_grad_partial_kernel<uint16_t><<<grid, 256, 0, st>>>((const uint16_t*)dy, N, F, P, f,
                                                                   slices, xlut, partial, nar);
-        bias_grad_final_kernel<uint16_t><<<grid_for(F, 128), 128, 0, st>>>(
+        bias_grad_final_kernel<uint16_t><<<grid_for(F * 32, 256), 256, 0, st>>>(
             partial, slices, nar, F, f, (uint16_t*)db, (unsigned __int128*)raw_words,
             (uint8_t*)raw_nar);
     }

@@ -371,7 +371,10 @@ __global__ void relu_bwd_vec_kernel(int x_nbits, const TX* __restrict__ x,
 // (butterfly over 128-bit lanes), one rounding, then p_j per lane.
 __global__ void softmax_xent_kernel(PositFmt f, int b, const void* logits, const int32_t* labels,
                                     int64_t B, int64_t Cn, int log2_batch, int grad_scale_log2,
-                                    void* dlogits, void* loss_rows, void* s_rows = nullptr) {
+                                    void* dlogits, void* loss_rows, void* s_rows = nullptr,
+                                    const uint16_t* __restrict__ exp_lut = nullptr,
+                                    const uint16_t* __restrict__ log_lut = nullptr) {
+    auto pexp = [&](uint32_t x) { return exp_lut ? uint32_t(__ldg(exp_lut + x)) : p_exp(f, x); };
     const int lane = threadIdx.x & 31;
     const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
     for (int64_t i = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5; i < B; i += nwarps) {
@@ -391,7 +394,7 @@ __global__ void softmax_xent_kernel(PositFmt f, int b, const void* logits, const
         bool nar = false;
         uint32_t e0 = 0;  // this lane's first e_j, reused below
         for (int64_t j = lane; j < Cn; j += 32) {
-            const uint32_t e = p_exp(f, p_sub(f, load_any(logits, row + j, b), m));
+            const uint32_t e = pexp(p_sub(f, load_any(logits, row + j, b), m));
             if (j == lane) e0 = e;
             __int128 X;
             nar |= decode_x128(e, f, X);
@@ -419,7 +422,7 @@ __global__ void softmax_xent_kernel(PositFmt f, int b, const void* logits, const
         const int32_t y = labels[i];
         const uint32_t one = p_from_int64(f, 1);
         for (int64_t j = lane; j < Cn; j += 32) {
-            const uint32_t e = j == lane ? e0 : p_exp(f, p_sub(f, load_any(logits, row + j, b), m));
+            const uint32_t e = j == lane ? e0 : pexp(p_sub(f, load_any(logits, row + j, b), m));
             const uint32_t pj = p_div(f, e, S);
             const uint32_t g = p_sub(f, pj, j == y ? one : 0u);
             store_any(dlogits, row + j, b, p_ldexp(f, g, grad_scale_log2 - log2_batch));
@@ -427,7 +430,7 @@ __global__ void softmax_xent_kernel(PositFmt f, int b, const void* logits, const
         if (lane == 0 && s_rows != nullptr) store_any(s_rows, i, b, S);
         if (lane == 0 && loss_rows != nullptr) {
             const uint32_t zy = load_any(logits, row + y, b);
-            store_any(loss_rows, i, b, p_sub(f, p_log(f, S), p_sub(f, zy, m)));
+            store_any(loss_rows, i, b, p_sub(f, log_lut ? uint32_t(__ldg(log_lut + S)) : p_log(f, S), p_sub(f, zy, m)));
         }
     }
 }
@@ -436,7 +439,8 @@ __global__ void softmax_xent_kernel(PositFmt f, int b, const void* logits, const
 // (same operations as softmax_xent_kernel's last step, Appendix A.5): lets the
 // loss run beside the backward pass instead of on its critical path.
 __global__ void xent_loss_rows_kernel(PositFmt f, int b, const void* logits, const int32_t* labels,
-                                      const void* s_rows, int64_t B, int64_t Cn, void* loss_rows) {
+                                      const void* s_rows, int64_t B, int64_t Cn, void* loss_rows,
+                                      const uint16_t* __restrict__ log_lut = nullptr) {
     GRID_STRIDE(i, B) {
         const int64_t row = i * Cn;
         uint32_t m = load_any(logits, row, b);
@@ -445,7 +449,8 @@ __global__ void xent_loss_rows_kernel(PositFmt f, int b, const void* logits, con
             if (p_compare(f, v, m) > 0) m = v;
         }
         const uint32_t zy = load_any(logits, row + labels[i], b);
-        store_any(loss_rows, i, b, p_sub(f, p_log(f, load_any(s_rows, i, b)), p_sub(f, zy, m)));
+        const uint32_t Sv = load_any(s_rows, i, b);
+        store_any(loss_rows, i, b, p_sub(f, log_lut ? uint32_t(__ldg(log_lut + Sv)) : p_log(f, Sv), p_sub(f, zy, m)));
     }
 }
 
@@ -633,6 +638,13 @@ __global__ void sgd_m_lut_kernel(PositFmt fo, PositFmt fg, uint32_t lr, uint16_t
 __global__ void copy_lut_kernel(PositFmt fo, PositFmt fc, uint16_t* __restrict__ lut) {
     GRID_STRIDE(c, int64_t(1) << fo.nbits) { lut[c] = uint16_t(p_convert(fo, fc, uint32_t(c))); }
 }
+// exp / log of every code (posit_math.cpp:67-107 through p_exp / p_log): the
+// softmax cross-entropy's transcendental steps by table
+__global__ void fn_lut_kernel(PositFmt f, int which, uint16_t* __restrict__ lut) {
+    GRID_STRIDE(c, int64_t(1) << f.nbits) {
+        lut[c] = uint16_t(which == 0 ? p_exp(f, uint32_t(c)) : p_log(f, uint32_t(c)));
+    }
+}
 
 // round(X 2^-R) for an int64 integer image (|X| < 2^63) through the rounding table
 __device__ __forceinline__ uint32_t x_to_posit_lut(const PositFmt& f, int64_t X, const uint4* lut) {
@@ -655,10 +667,19 @@ struct SgdLuts {
     const uint16_t* c2;
 };
 
-__global__ void sgd_lut_kernel(PositFmt fo, int bo, int bg, int b1, int b2, const __grid_constant__ SgdSegs segs,
-                               SgdLuts t) {
+// U elements per thread per grid-stride round (independent load -> table ->
+// round chains in flight); the m table in shared memory for gradient formats
+// up to 12 bits.
+constexpr int kSgdU = 4;
+constexpr int kSgdSmemM = 4096;
+__global__ void __launch_bounds__(256) sgd_lut_kernel(PositFmt fo, int bo, int bg, int gbits, int b1, int b2,
+                                                      const __grid_constant__ SgdSegs segs, SgdLuts t) {
     __shared__ uint4 s_lut[kPackLutEntries];
+    __shared__ uint16_t s_m[kSgdSmemM];
     build_pack_lut(fo, s_lut, threadIdx.x, blockDim.x);
+    const bool msm = gbits <= 12;
+    if (msm)
+        for (int i = threadIdx.x; i < (1 << gbits); i += blockDim.x) s_m[i] = t.m[i];
     __shared__ int64_t s_start[kSgdMaxSeg + 1];
     __shared__ const void* s_ptr[4][kSgdMaxSeg];
     for (int i = threadIdx.x; i <= segs.count; i += blockDim.x) s_start[i] = segs.start[i];
@@ -671,30 +692,49 @@ __global__ void sgd_lut_kernel(PositFmt fo, int bo, int bg, int b1, int b2, cons
     __syncthreads();
     const uint32_t nar = 1u << (fo.nbits - 1);
     const int64_t total = s_start[segs.count];
-    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total;
-         i += int64_t(gridDim.x) * blockDim.x) {
-        int lo = 0, hi = segs.count - 1;  // last segment with start <= i
-        while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (s_start[mid] <= i) lo = mid;
-            else hi = mid - 1;
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    for (int64_t i0 = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i0 < total; i0 += kSgdU * stride) {
+        int seg[kSgdU];
+        int64_t k[kSgdU];
+        uint32_t g[kSgdU], w[kSgdU];
+#pragma unroll
+        for (int u = 0; u < kSgdU; ++u) {
+            const int64_t i = i0 + u * stride;
+            int lo = 0, hi = segs.count - 1;  // last segment with start <= i
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (s_start[mid] <= i) lo = mid;
+                else hi = mid - 1;
+            }
+            seg[u] = i < total ? lo : -1;
+            k[u] = i - s_start[lo];
+            if (seg[u] >= 0) {
+                g[u] = load_any(s_ptr[1][lo], k[u], bg);
+                w[u] = load_any(s_ptr[0][lo], k[u], bo);
+            }
         }
-        const int64_t k = i - s_start[lo];
-        void* const master = const_cast<void*>(s_ptr[0][lo]);
-        const uint32_t m = __ldg(t.m + load_any(s_ptr[1][lo], k, bg));
-        const uint32_t w = load_any(master, k, bo);
-        uint32_t r;
-        if (w == nar || m == nar) {
-            r = nar;
-        } else {
-            int64_t Xw, Xm;
-            decode_x(w, fo, Xw);
-            decode_x(m, fo, Xm);
-            r = x_to_posit_lut(fo, Xw - Xm, s_lut);
+#pragma unroll
+        for (int u = 0; u < kSgdU; ++u) {
+            if (seg[u] < 0) continue;
+            const uint32_t m = msm ? uint32_t(s_m[g[u]]) : uint32_t(__ldg(t.m + g[u]));
+            uint32_t r;
+            if (w[u] == nar || m == nar) {
+                r = nar;
+            } else {
+                int64_t Xw, Xm;
+                decode_x(w[u], fo, Xw);
+                decode_x(m, fo, Xm);
+                r = x_to_posit_lut(fo, Xw - Xm, s_lut);
+            }
+            w[u] = r;
+            store_any(const_cast<void*>(s_ptr[0][seg[u]]), k[u], bo, r);
         }
-        store_any(master, k, bo, r);
-        if (s_ptr[2][lo]) store_any(const_cast<void*>(s_ptr[2][lo]), k, b1, __ldg(t.c1 + r));
-        if (s_ptr[3][lo]) store_any(const_cast<void*>(s_ptr[3][lo]), k, b2, __ldg(t.c2 + r));
+#pragma unroll
+        for (int u = 0; u < kSgdU; ++u) {
+            if (seg[u] < 0) continue;
+            if (s_ptr[2][seg[u]]) store_any(const_cast<void*>(s_ptr[2][seg[u]]), k[u], b1, __ldg(t.c1 + w[u]));
+            if (s_ptr[3][seg[u]]) store_any(const_cast<void*>(s_ptr[3][seg[u]]), k[u], b2, __ldg(t.c2 + w[u]));
+        }
     }
 }
 
@@ -801,39 +841,45 @@ int grid1(int64_t n) {
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
-// SGD tables per (fo, fg, lr) and per (fo, copy format), device-resident for the
-// life of the process.  Built synchronously on the caller's stream the first
-// time; during stream capture a missing table means "use the scalar path".
-bool sgd_luts(const PositFmt& fo, const PositFmt& fg, uint32_t lr, const PositFmt* f1, const PositFmt* f2,
-              cudaStream_t st, SgdLuts* out) {
+// Code tables (one uint16 entry per source code), device-resident for the life
+// of the process: kind 0 = SGD m[g] per (fo, fg, lr), 1 = convert per (fo, fc),
+// 2 = exp / 3 = log per format.  Built synchronously on the caller's stream the
+// first time; during stream capture a missing table returns null ("use the
+// scalar path"), so a CUDA graph replays launches with the tables resident.
+uint16_t* code_table(int kind, const PositFmt& a, const PositFmt& b, uint32_t l, cudaStream_t st) {
     static std::mutex mu;
     static std::map<std::tuple<int, int, int, int, int, uint32_t>, uint16_t*> cache;
     std::lock_guard<std::mutex> lock(mu);
+    const auto key = std::make_tuple(kind, a.nbits, a.es, b.nbits, b.es, l);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     if (cudaStreamIsCapturing(st, &cs) != cudaSuccess) {
         cudaGetLastError();
-        return false;
+        return nullptr;
     }
-    const bool capturing = cs != cudaStreamCaptureStatusNone;
-    auto get = [&](int kind, const PositFmt& a, const PositFmt& b, uint32_t l) -> uint16_t* {
-        const auto key = std::make_tuple(kind, a.nbits, a.es, b.nbits, b.es, l);
-        auto it = cache.find(key);
-        if (it != cache.end()) return it->second;
-        if (capturing) return nullptr;
-        uint16_t* p = nullptr;
-        const int64_t n = int64_t(1) << (kind == 0 ? b.nbits : a.nbits);
-        if (cudaMalloc(&p, size_t(n) * 2) != cudaSuccess) {
-            cudaGetLastError();
-            return nullptr;
-        }
-        if (kind == 0) sgd_m_lut_kernel<<<grid1(n), 256, 0, st>>>(a, b, l, p);
-        else copy_lut_kernel<<<grid1(n), 256, 0, st>>>(a, b, p);
-        if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(st) != cudaSuccess) {
-            cudaFree(p);
-            return nullptr;
-        }
-        cache[key] = p;
-        return p;
+    if (cs != cudaStreamCaptureStatusNone) return nullptr;
+    uint16_t* p = nullptr;
+    const int64_t n = int64_t(1) << (kind == 0 ? b.nbits : a.nbits);
+    if (cudaMalloc(&p, size_t(n) * 2) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    if (kind == 0) sgd_m_lut_kernel<<<grid1(n), 256, 0, st>>>(a, b, l, p);
+    else if (kind == 1) copy_lut_kernel<<<grid1(n), 256, 0, st>>>(a, b, p);
+    else fn_lut_kernel<<<grid1(n), 256, 0, st>>>(a, kind - 2, p);
+    if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(st) != cudaSuccess) {
+        cudaFree(p);
+        return nullptr;
+    }
+    cache[key] = p;
+    return p;
+}
+
+bool sgd_luts(const PositFmt& fo, const PositFmt& fg, uint32_t lr, const PositFmt* f1, const PositFmt* f2,
+              cudaStream_t st, SgdLuts* out) {
+    auto get = [&](int kind, const PositFmt& a, const PositFmt& b, uint32_t l) {
+        return code_table(kind, a, b, l, st);
     };
     out->m = get(0, fo, fg, lr);
     out->c1 = f1 ? get(1, fo, *f1, 0) : nullptr;
@@ -1026,7 +1072,8 @@ int pnn_softmax_xent_scaled(int nbits, int es, const void* logits, const int32_t
     auto st = (cudaStream_t)stream;
     softmax_xent_kernel<<<grid1(B * 32), 256, 0, st>>>(f, bytes_of(nbits), logits, labels, B, classes,
                                                       log2_batch, grad_scale_log2, dlogits,
-                                                      loss_rows);
+                                                      loss_rows, nullptr, code_table(2, f, f, 0, st),
+                                                      code_table(3, f, f, 0, st));
     if (loss_out || raw_word)
         loss_reduce_kernel<<<1, 256, 0, st>>>(f, bytes_of(nbits), loss_rows, B, log2_batch,
                                               loss_out, (unsigned __int128*)raw_word,
@@ -1040,9 +1087,10 @@ int pnn_softmax_xent_grad(int nbits, int es, const void* logits, const int32_t* 
     CHECK_FMT(nbits, es);
     if (B < 1 || classes < 1 || !logits || !labels || !dlogits || !s_rows)
         return set_status(PNN_EINVAL, "softmax_xent_grad: bad arguments");
+    const PositFmt f = make_fmt(nbits, es);
     softmax_xent_kernel<<<grid1(B * 32), 256, 0, (cudaStream_t)stream>>>(
-        make_fmt(nbits, es), bytes_of(nbits), logits, labels, B, classes, log2_batch, grad_scale_log2,
-        dlogits, nullptr, s_rows);
+        f, bytes_of(nbits), logits, labels, B, classes, log2_batch, grad_scale_log2,
+        dlogits, nullptr, s_rows, code_table(2, f, f, 0, (cudaStream_t)stream));
     return launched("softmax_xent_grad");
 }
 
@@ -1057,7 +1105,7 @@ int pnn_softmax_xent_loss(int nbits, int es, const void* logits, const int32_t* 
         return set_status(PNN_EUNSUPPORTED, "softmax_xent: raw loss words need a quire of <= 128 bits");
     auto st = (cudaStream_t)stream;
     xent_loss_rows_kernel<<<grid1(B), 256, 0, st>>>(f, bytes_of(nbits), logits, labels, s_rows, B,
-                                                     classes, loss_rows);
+                                                     classes, loss_rows, code_table(3, f, f, 0, st));
     if (loss_out || raw_word)
         loss_reduce_kernel<<<1, 256, 0, st>>>(f, bytes_of(nbits), loss_rows, B, log2_batch, loss_out,
                                               (unsigned __int128*)raw_word, (uint8_t*)raw_nar);
@@ -1149,8 +1197,9 @@ int pnn_sgd_step_multi(int opt_nbits, int opt_es, int g_nbits, int g_es, uint32_
         sg.start[sg.count] = tot;
         if (tot == 0) continue;
         if (lut_path) {
-            sgd_lut_kernel<<<grid1(tot), 256, 0, (cudaStream_t)stream>>>(
-                fo, bytes_of(opt_nbits), bytes_of(g_nbits), bytes_of(f1.nbits), bytes_of(f2.nbits), sg, luts);
+            sgd_lut_kernel<<<grid1((tot + kSgdU - 1) / kSgdU), 256, 0, (cudaStream_t)stream>>>(
+                fo, bytes_of(opt_nbits), bytes_of(g_nbits), g_nbits, bytes_of(f1.nbits), bytes_of(f2.nbits), sg,
+                luts);
             continue;
         }
         sgd_multi_kernel<<<grid1(tot), 256, 0, (cudaStream_t)stream>>>(

@@ -812,6 +812,47 @@ __global__ void __launch_bounds__(256) quire_finalize_warp_kernel(
     }
 }
 
+// Many splits: a block = 32 consecutive outputs x 8 split groups.  Loads are
+// coalesced along the outputs (32 x 16 bytes per warp instruction), every
+// thread runs two independent chains over its splits, and the 8 group sums
+// meet in shared memory -- exact 128-bit integer sums, any order.
+template <typename CodeT>
+__global__ void __launch_bounds__(256) quire_finalize_2d_kernel(
+    const unsigned __int128* __restrict__ partial, int splits, const uint8_t* __restrict__ row_nar,
+    const uint8_t* __restrict__ col_nar, OutMap<CodeT> out, int64_t M, int64_t N, PositFmt f,
+    unsigned __int128* __restrict__ raw_words, uint8_t* __restrict__ raw_nar) {
+    __shared__ unsigned __int128 s_q[8][32];
+    const int64_t total = M * N;
+    const int x = threadIdx.x & 31, y = threadIdx.x >> 5;
+    const int64_t idx = blockIdx.x * int64_t(32) + x;
+    unsigned __int128 q0 = 0, q1 = 0;
+    if (idx < total) {
+        int sp = y;
+        for (; sp + 8 < splits; sp += 16) {
+            q0 += partial[sp * total + idx];
+            q1 += partial[(sp + 8) * total + idx];
+        }
+        if (sp < splits) q0 += partial[sp * total + idx];
+    }
+    s_q[y][x] = q0 + q1;
+    __syncthreads();
+    if (y != 0 || idx >= total) return;
+    unsigned __int128 q = s_q[0][x];
+#pragma unroll
+    for (int g = 1; g < 8; ++g) q += s_q[g][x];
+    const unsigned __int128 one = 1;
+    const unsigned __int128 wmask = f.W >= 128 ? ~(unsigned __int128)0 : ((one << f.W) - 1);
+    const int64_t i = idx / N, j = idx - (idx / N) * N;
+    const bool nar = (row_nar != nullptr && row_nar[i]) || (col_nar != nullptr && col_nar[j]);
+    const int64_t o = out.index(i, j);
+    if (o < 0) return;
+    if (raw_words != nullptr) {
+        raw_words[o] = q & wmask;
+        raw_nar[o] = nar ? 1 : 0;
+    }
+    if (out.base != nullptr) out.base[o] = CodeT(nar ? (1u << (f.nbits - 1)) : quire_word_to_posit(f, q));
+}
+
 inline int grid_for(int64_t items, int threads);
 int64_t variant_min_work();  // igemm.cu: work (MACs) below which no reduced-digit variant launches
 
@@ -822,8 +863,8 @@ inline void launch_finalize(const unsigned __int128* partial, int splits, const 
                             const PositFmt& f, unsigned __int128* raw_words, uint8_t* raw_nar,
                             cudaStream_t st) {
     const int64_t total = M * N;
-    if (splits >= 8 && total <= 148 * 256)
-        quire_finalize_warp_kernel<CodeT><<<grid_for(total * 32, 256), 256, 0, st>>>(
+    if (splits >= 8)
+        quire_finalize_2d_kernel<CodeT><<<unsigned((total + 31) / 32), 256, 0, st>>>(
             partial, splits, row_nar, col_nar, out, M, N, f, raw_words, raw_nar);
     else
         quire_finalize_kernel<CodeT><<<grid_for(total, 256), 256, 0, st>>>(
