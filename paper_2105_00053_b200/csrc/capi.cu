@@ -12,6 +12,7 @@
 #include <cstdint>
 #include <cstring>
 #include <functional>
+#include <map>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -21,6 +22,7 @@
 #include "posit_device.cuh"
 #include "quire_gemm.h"
 #include "status.h"
+#include "tables.h"
 
 using namespace pnn_b200;
 
@@ -36,6 +38,33 @@ int fail(int code, const std::string& msg) {
 }  // namespace
 
 namespace pnn_b200 {
+void* persistent_table(uint64_t key, size_t bytes, cudaStream_t st,
+                       const std::function<void(void*, cudaStream_t)>& build) {
+    static std::mutex mu;
+    static std::map<uint64_t, void*>* cache = new std::map<uint64_t, void*>();  // lives with the process
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache->find(key);
+    if (it != cache->end()) return it->second;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    if (cs != cudaStreamCaptureStatusNone) return nullptr;
+    void* p = nullptr;
+    if (cudaMalloc(&p, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    build(p, st);
+    if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(st) != cudaSuccess) {
+        cudaFree(p);
+        return nullptr;
+    }
+    (*cache)[key] = p;
+    return p;
+}
+
 void set_last_error(const std::string& msg) { g_err = msg; }
 int set_status(int code, const std::string& msg) {
     g_err = msg;

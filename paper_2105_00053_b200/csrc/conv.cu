@@ -25,6 +25,7 @@
 #include "igemm.h"
 #include "igemm_core.cuh"
 #include "status.h"
+#include "tables.h"
 
 namespace pnn_b200 {
 
@@ -339,14 +340,14 @@ __global__ void __launch_bounds__(256) bias_grad_partial_kernel(
 // gnbits, same layout): the bias gradient of the ReLU's input gradient
 // without materialising it.
 template <typename CodeT, int LUTB, int GB = 0>
-__global__ void __launch_bounds__(256) bias_grad_chan_kernel(
+__global__ void __launch_bounds__(512) bias_grad_chan_kernel(
     const CodeT* __restrict__ dy, int64_t N, int64_t F, int64_t P, PositFmt f, int slices,
     FastDiv fd_vpr, const int64_t* __restrict__ xlut, unsigned __int128* __restrict__ partial,
     uint8_t* __restrict__ nar_flag, unsigned int* __restrict__ arrivals, CodeT* __restrict__ out,
     unsigned __int128* raw_words, uint8_t* raw_nar, const void* __restrict__ gate = nullptr,
     int gnbits = 0) {
     __shared__ int64_t s_lut[LUTB];
-    __shared__ unsigned __int128 warp_s[8];
+    __shared__ unsigned __int128 warp_s[16];
     __shared__ bool s_last;
     // the per-call X table (x_lut_kernel) -> shared memory, 16-byte copies
     for (int i = threadIdx.x; i < LUTB / 2; i += blockDim.x)
@@ -453,6 +454,18 @@ __global__ void x_lut_kernel(PositFmt f, int64_t* __restrict__ lut) {
         decode_x(uint32_t(c), f, X);
         lut[c] = X;
     }
+}
+
+// the X table of a format for the life of the process (tables.h), else the
+// per-call table in the workspace
+inline int64_t* x_table(const PositFmt& f, int64_t* ws_lut, cudaStream_t st) {
+    void* p = persistent_table(table_key(2, f.nbits, f.es, 0, 0, 0), (size_t(1) << f.nbits) * 8, st,
+                               [&](void* q, cudaStream_t s) {
+                                   x_lut_kernel<<<(1 << f.nbits) / 256 + 1, 256, 0, s>>>(f, static_cast<int64_t*>(q));
+                               });
+    if (p) return static_cast<int64_t*>(p);
+    x_lut_kernel<<<(1 << f.nbits) / 256 + 1, 256, 0, st>>>(f, ws_lut);
+    return ws_lut;
 }
 
 template <typename CodeT>
@@ -875,8 +888,8 @@ int pnn_bias_grad_gated(int nbits, int es, const void* dy, int gate_nbits, const
     auto st = static_cast<cudaStream_t>(stream);
     cudaMemsetAsync(nar, 0, size_t(F), st);
     cudaMemsetAsync(arrivals, 0, size_t(F) * 4, st);
-    x_lut_kernel<<<(1 << nbits) / 256 + 1, 256, 0, st>>>(f, lut);
-    int64_t want = (int64_t(8) * 148 + F - 1) / F;
+    lut = x_table(f, lut, st);
+    int64_t want = (int64_t(2) * 148 + F - 1) / F;  // ~2 blocks of 512 per SM: the X table loads once per block
     int sl = int(want > 64 ? 64 : want);
     if (sl > N) sl = int(N);
     const int64_t per = (N + sl - 1) / sl;
@@ -884,7 +897,7 @@ int pnn_bias_grad_gated(int nbits, int es, const void* dy, int gate_nbits, const
     const FastDiv fd{uint32_t(P / VE)};
     const dim3 g2{unsigned(sl), unsigned(F), 1u};
 #define PNN_BGG(T, B, G)                                                                              \
-    bias_grad_chan_kernel<T, B, G><<<g2, 256, 0, st>>>((const T*)dy, N, F, P, f, sl, fd, lut, partial,  \
+    bias_grad_chan_kernel<T, B, G><<<g2, 512, 0, st>>>((const T*)dy, N, F, P, f, sl, fd, lut, partial,  \
                                                        nar, arrivals, (T*)db,                          \
                                                        (unsigned __int128*)raw_words, (uint8_t*)raw_nar, \
                                                        gate, gate_nbits)
@@ -919,8 +932,7 @@ int pnn_bias_grad(int nbits, int es, const void* dy, int64_t N, int64_t F, int64
     const dim3 grid{unsigned(F), unsigned(slices), 1u};
     int64_t* xlut = nullptr;
     if (!chan && nbits <= kBiasLutBits && N * P >= 4096) {  // table pays for itself
-        xlut = reinterpret_cast<int64_t*>(static_cast<uint8_t*>(workspace) + bias_lut_offset(F));
-        x_lut_kernel<<<(1 << nbits) / 256 + 1, 256, 0, st>>>(f, xlut);
+        xlut = x_table(f, reinterpret_cast<int64_t*>(static_cast<uint8_t*>(workspace) + bias_lut_offset(F)), st);
     }
     const dim3 cgrid{unsigned((F + 255) / 256), unsigned(slices), 1u};
     if (P == 1 && nbits <= 8) {
@@ -942,8 +954,8 @@ int pnn_bias_grad(int nbits, int es, const void* dy, int64_t N, int64_t F, int64
                                                          bias_arrivals_offset(F));
         auto* lut = reinterpret_cast<int64_t*>(static_cast<uint8_t*>(workspace) + bias_lut_offset(F));
         cudaMemsetAsync(arrivals, 0, size_t(F) * 4, st);
-        x_lut_kernel<<<(1 << nbits) / 256 + 1, 256, 0, st>>>(f, lut);
-        int64_t want = (int64_t(8) * 148 + F - 1) / F;
+        lut = x_table(f, lut, st);
+        int64_t want = (int64_t(2) * 148 + F - 1) / F;  // ~2 blocks of 512 per SM: the X table loads once per block
         int sl = int(want > 64 ? 64 : want);
         if (sl > N) sl = int(N < 1 ? 1 : N);
         const int VE = nbits <= 8 ? 16 : 8;
@@ -953,7 +965,7 @@ int pnn_bias_grad(int nbits, int es, const void* dy, int64_t N, int64_t F, int64
         const FastDiv fd{uint32_t(P / VE)};
         const dim3 g2{unsigned(sl), unsigned(F), 1u};
 #define PNN_BGC(T, B)                                                                             \
-    bias_grad_chan_kernel<T, B><<<g2, 256, 0, st>>>((const T*)dy, N, F, P, f, sl, fd, lut, partial, \
+    bias_grad_chan_kernel<T, B><<<g2, 512, 0, st>>>((const T*)dy, N, F, P, f, sl, fd, lut, partial, \
                                                     nar, arrivals, (T*)db,                        \
                                                     (unsigned __int128*)raw_words, (uint8_t*)raw_nar)
         if (nbits <= 8) PNN_BGC(uint8_t, 256);

@@ -19,6 +19,7 @@
 #include "epilogue.cuh"
 #include "posit_scalar.cuh"
 #include "status.h"
+#include "tables.h"
 
 namespace pnn_b200 {
 
@@ -625,15 +626,20 @@ __global__ void sgd_multi_kernel(PositFmt fo, int bo, PositFmt fg, int bg, uint3
 // ---- SGD through per-format tables (the optimizer step's rounding work is
 // per element ALU-bound, not HBM-bound: a table per format pair replaces the
 // two code-only operations and leaves one exact subtraction + one rounding):
-//   m_lut[g]  = p_mul(fo, lr, p_convert(fg, fo, g))   (lr fixed per call)
-//   c_lut[w]  = p_convert(fo, fc, w)                   (stage copies)
+//   xm_lut[g] = X(p_mul(fo, lr, p_convert(fg, fo, g)))  (lr fixed per call;
+//               the integer image of m, INT64_MIN for NaR)
+//   c_lut[w]  = p_convert(fo, fc, w)                     (stage copies)
 //   w' = p_sub(fo, w, m) = round_o(X_w - X_m), the exact difference of the
 //   integer images (|X| <= 2^2R, 2R + 1 <= 63) rounded once (posit.cpp:437-457
 //   rounds the exact result of every op once; x_to_posit_lut = pack_round).
 // Each table entry is computed by the scalar ops themselves, so the path is
 // the sgd_kernel arithmetic, entry for entry.
-__global__ void sgd_m_lut_kernel(PositFmt fo, PositFmt fg, uint32_t lr, uint16_t* __restrict__ lut) {
-    GRID_STRIDE(c, int64_t(1) << fg.nbits) { lut[c] = uint16_t(p_mul(fo, lr, p_convert(fg, fo, uint32_t(c)))); }
+__global__ void sgd_xm_lut_kernel(PositFmt fo, PositFmt fg, uint32_t lr, int64_t* __restrict__ lut) {
+    GRID_STRIDE(c, int64_t(1) << fg.nbits) {
+        int64_t X;
+        const bool nar = decode_x(p_mul(fo, lr, p_convert(fg, fo, uint32_t(c))), fo, X);
+        lut[c] = nar ? INT64_MIN : X;
+    }
 }
 __global__ void copy_lut_kernel(PositFmt fo, PositFmt fc, uint16_t* __restrict__ lut) {
     GRID_STRIDE(c, int64_t(1) << fo.nbits) { lut[c] = uint16_t(p_convert(fo, fc, uint32_t(c))); }
@@ -662,24 +668,19 @@ __device__ __forceinline__ uint32_t x_to_posit_lut(const PositFmt& f, int64_t X,
 }
 
 struct SgdLuts {
-    const uint16_t* m;   // [2^fg.nbits]
+    const int64_t* m;    // [2^fg.nbits] X_m (INT64_MIN = NaR)
     const uint16_t* c1;  // [2^fo.nbits] or null
     const uint16_t* c2;
 };
 
 // U elements per thread per grid-stride round (independent load -> table ->
-// round chains in flight); the m table in shared memory for gradient formats
-// up to 12 bits.
+// round chains in flight); a few blocks per SM, each looping (the per-block
+// setup -- rounding table, segment table -- is paid once per block).
 constexpr int kSgdU = 4;
-constexpr int kSgdSmemM = 4096;
-__global__ void __launch_bounds__(256) sgd_lut_kernel(PositFmt fo, int bo, int bg, int gbits, int b1, int b2,
+__global__ void __launch_bounds__(256) sgd_lut_kernel(PositFmt fo, int bo, int bg, int b1, int b2,
                                                       const __grid_constant__ SgdSegs segs, SgdLuts t) {
     __shared__ uint4 s_lut[kPackLutEntries];
-    __shared__ uint16_t s_m[kSgdSmemM];
     build_pack_lut(fo, s_lut, threadIdx.x, blockDim.x);
-    const bool msm = gbits <= 12;
-    if (msm)
-        for (int i = threadIdx.x; i < (1 << gbits); i += blockDim.x) s_m[i] = t.m[i];
     __shared__ int64_t s_start[kSgdMaxSeg + 1];
     __shared__ const void* s_ptr[4][kSgdMaxSeg];
     for (int i = threadIdx.x; i <= segs.count; i += blockDim.x) s_start[i] = segs.start[i];
@@ -692,48 +693,47 @@ __global__ void __launch_bounds__(256) sgd_lut_kernel(PositFmt fo, int bo, int b
     __syncthreads();
     const uint32_t nar = 1u << (fo.nbits - 1);
     const int64_t total = s_start[segs.count];
-    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-    for (int64_t i0 = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i0 < total; i0 += kSgdU * stride) {
-        int seg[kSgdU];
+    // a contiguous range per block, walked in rounds of kSgdU x blockDim
+    // elements: the thread's segment only moves forward (no search per element)
+    const int64_t per = (total + gridDim.x - 1) / gridDim.x;
+    const int64_t r0 = blockIdx.x * per, r1 = min(total, r0 + per);
+    int seg = 0;
+    while (seg + 1 < segs.count && s_start[seg + 1] <= r0 + threadIdx.x) ++seg;
+    for (int64_t i0 = r0 + threadIdx.x; i0 < r1; i0 += kSgdU * int64_t(blockDim.x)) {
+        int sg[kSgdU];
         int64_t k[kSgdU];
-        uint32_t g[kSgdU], w[kSgdU];
+        uint32_t w[kSgdU];
+        int64_t xm[kSgdU];
 #pragma unroll
         for (int u = 0; u < kSgdU; ++u) {
-            const int64_t i = i0 + u * stride;
-            int lo = 0, hi = segs.count - 1;  // last segment with start <= i
-            while (lo < hi) {
-                const int mid = (lo + hi + 1) >> 1;
-                if (s_start[mid] <= i) lo = mid;
-                else hi = mid - 1;
-            }
-            seg[u] = i < total ? lo : -1;
-            k[u] = i - s_start[lo];
-            if (seg[u] >= 0) {
-                g[u] = load_any(s_ptr[1][lo], k[u], bg);
-                w[u] = load_any(s_ptr[0][lo], k[u], bo);
+            const int64_t i = i0 + u * int64_t(blockDim.x);
+            while (seg + 1 < segs.count && s_start[seg + 1] <= i) ++seg;
+            sg[u] = i < r1 ? seg : -1;
+            k[u] = i - s_start[seg];
+            if (sg[u] >= 0) {
+                xm[u] = __ldg(t.m + load_any(s_ptr[1][seg], k[u], bg));
+                w[u] = load_any(s_ptr[0][seg], k[u], bo);
             }
         }
 #pragma unroll
         for (int u = 0; u < kSgdU; ++u) {
-            if (seg[u] < 0) continue;
-            const uint32_t m = msm ? uint32_t(s_m[g[u]]) : uint32_t(__ldg(t.m + g[u]));
+            if (sg[u] < 0) continue;
             uint32_t r;
-            if (w[u] == nar || m == nar) {
+            if (w[u] == nar || xm[u] == INT64_MIN) {
                 r = nar;
             } else {
-                int64_t Xw, Xm;
+                int64_t Xw;
                 decode_x(w[u], fo, Xw);
-                decode_x(m, fo, Xm);
-                r = x_to_posit_lut(fo, Xw - Xm, s_lut);
+                r = x_to_posit_lut(fo, Xw - xm[u], s_lut);
             }
             w[u] = r;
-            store_any(const_cast<void*>(s_ptr[0][seg[u]]), k[u], bo, r);
+            store_any(const_cast<void*>(s_ptr[0][sg[u]]), k[u], bo, r);
         }
 #pragma unroll
         for (int u = 0; u < kSgdU; ++u) {
-            if (seg[u] < 0) continue;
-            if (s_ptr[2][seg[u]]) store_any(const_cast<void*>(s_ptr[2][seg[u]]), k[u], b1, __ldg(t.c1 + w[u]));
-            if (s_ptr[3][seg[u]]) store_any(const_cast<void*>(s_ptr[3][seg[u]]), k[u], b2, __ldg(t.c2 + w[u]));
+            if (sg[u] < 0) continue;
+            if (s_ptr[2][sg[u]]) store_any(const_cast<void*>(s_ptr[2][sg[u]]), k[u], b1, __ldg(t.c1 + w[u]));
+            if (s_ptr[3][sg[u]]) store_any(const_cast<void*>(s_ptr[3][sg[u]]), k[u], b2, __ldg(t.c2 + w[u]));
         }
     }
 }
@@ -842,38 +842,19 @@ int grid1(int64_t n) {
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 // Code tables (one uint16 entry per source code), device-resident for the life
-// of the process: kind 0 = SGD m[g] per (fo, fg, lr), 1 = convert per (fo, fc),
+// of the process: kind 0 = SGD X_m[g] (int64 entries) per (fo, fg, lr), 1 = convert per (fo, fc),
 // 2 = exp / 3 = log per format.  Built synchronously on the caller's stream the
 // first time; during stream capture a missing table returns null ("use the
 // scalar path"), so a CUDA graph replays launches with the tables resident.
 uint16_t* code_table(int kind, const PositFmt& a, const PositFmt& b, uint32_t l, cudaStream_t st) {
-    static std::mutex mu;
-    static std::map<std::tuple<int, int, int, int, int, uint32_t>, uint16_t*> cache;
-    std::lock_guard<std::mutex> lock(mu);
-    const auto key = std::make_tuple(kind, a.nbits, a.es, b.nbits, b.es, l);
-    auto it = cache.find(key);
-    if (it != cache.end()) return it->second;
-    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess) {
-        cudaGetLastError();
-        return nullptr;
-    }
-    if (cs != cudaStreamCaptureStatusNone) return nullptr;
-    uint16_t* p = nullptr;
     const int64_t n = int64_t(1) << (kind == 0 ? b.nbits : a.nbits);
-    if (cudaMalloc(&p, size_t(n) * 2) != cudaSuccess) {
-        cudaGetLastError();
-        return nullptr;
-    }
-    if (kind == 0) sgd_m_lut_kernel<<<grid1(n), 256, 0, st>>>(a, b, l, p);
-    else if (kind == 1) copy_lut_kernel<<<grid1(n), 256, 0, st>>>(a, b, p);
-    else fn_lut_kernel<<<grid1(n), 256, 0, st>>>(a, kind - 2, p);
-    if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(st) != cudaSuccess) {
-        cudaFree(p);
-        return nullptr;
-    }
-    cache[key] = p;
-    return p;
+    return static_cast<uint16_t*>(persistent_table(
+        table_key(16 + kind, a.nbits, a.es, b.nbits, b.es, 0, l), size_t(n) * (kind == 0 ? 8 : 2), st,
+        [&](void* p, cudaStream_t s) {
+            if (kind == 0) sgd_xm_lut_kernel<<<grid1(n), 256, 0, s>>>(a, b, l, static_cast<int64_t*>(p));
+            else if (kind == 1) copy_lut_kernel<<<grid1(n), 256, 0, s>>>(a, b, static_cast<uint16_t*>(p));
+            else fn_lut_kernel<<<grid1(n), 256, 0, s>>>(a, kind - 2, static_cast<uint16_t*>(p));
+        }));
 }
 
 bool sgd_luts(const PositFmt& fo, const PositFmt& fg, uint32_t lr, const PositFmt* f1, const PositFmt* f2,
@@ -881,7 +862,7 @@ bool sgd_luts(const PositFmt& fo, const PositFmt& fg, uint32_t lr, const PositFm
     auto get = [&](int kind, const PositFmt& a, const PositFmt& b, uint32_t l) {
         return code_table(kind, a, b, l, st);
     };
-    out->m = get(0, fo, fg, lr);
+    out->m = reinterpret_cast<const int64_t*>(get(0, fo, fg, lr));
     out->c1 = f1 ? get(1, fo, *f1, 0) : nullptr;
     out->c2 = f2 ? get(1, fo, *f2, 0) : nullptr;
     return out->m && (!f1 || out->c1) && (!f2 || out->c2);
@@ -1197,9 +1178,9 @@ int pnn_sgd_step_multi(int opt_nbits, int opt_es, int g_nbits, int g_es, uint32_
         sg.start[sg.count] = tot;
         if (tot == 0) continue;
         if (lut_path) {
-            sgd_lut_kernel<<<grid1((tot + kSgdU - 1) / kSgdU), 256, 0, (cudaStream_t)stream>>>(
-                fo, bytes_of(opt_nbits), bytes_of(g_nbits), g_nbits, bytes_of(f1.nbits), bytes_of(f2.nbits), sg,
-                luts);
+            const int gr = grid1((tot + kSgdU - 1) / kSgdU);
+            sgd_lut_kernel<<<gr < 148 * 4 ? gr : 148 * 4, 256, 0, (cudaStream_t)stream>>>(
+                fo, bytes_of(opt_nbits), bytes_of(g_nbits), bytes_of(f1.nbits), bytes_of(f2.nbits), sg, luts);
             continue;
         }
         sgd_multi_kernel<<<grid1(tot), 256, 0, (cudaStream_t)stream>>>(

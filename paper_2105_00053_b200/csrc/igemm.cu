@@ -9,6 +9,7 @@
 #include <cstdlib>
 
 #include "igemm.h"
+#include "tables.h"
 #include "igemm_core.cuh"
 
 namespace pnn_b200 {
@@ -449,6 +450,26 @@ cudaError_t dispatch_wgrad(int D, int DA, int OFF, const CUtensorMap& tA, const 
 // ---- digitisers: codes of format fs (uint8 for nbits <= 8, else uint16) ->
 // digits of the plan format f (through the conversion LUT when fs != f)
 
+// The digit table of (D, fs -> f) for the life of the process (tables.h);
+// nullptr: build the per-call table in the workspace instead.
+uint32_t* cached_digit_lut(int D, const PositFmt& fs, const PositFmt& f, cudaStream_t st) {
+    if (D < 2 || D > 8) return nullptr;
+    return static_cast<uint32_t*>(persistent_table(
+        table_key(1, D, fs.nbits, fs.es, f.nbits, f.es), (size_t(2) << fs.nbits) * 4, st,
+        [&](void* p, cudaStream_t s) {
+            auto* l = static_cast<uint32_t*>(p);
+            switch (D) {
+                case 2: digit_lut_conv_kernel<2><<<16, 256, 0, s>>>(fs, f, l); break;
+                case 3: digit_lut_conv_kernel<3><<<16, 256, 0, s>>>(fs, f, l); break;
+                case 4: digit_lut_conv_kernel<4><<<16, 256, 0, s>>>(fs, f, l); break;
+                case 5: digit_lut_conv_kernel<5><<<16, 256, 0, s>>>(fs, f, l); break;
+                case 6: digit_lut_conv_kernel<6><<<16, 256, 0, s>>>(fs, f, l); break;
+                case 7: digit_lut_conv_kernel<7><<<16, 256, 0, s>>>(fs, f, l); break;
+                default: digit_lut_conv_kernel<8><<<16, 256, 0, s>>>(fs, f, l); break;
+            }
+        }));
+}
+
 template <typename SrcT>
 cudaError_t act_digits_t(int D, const SrcT* x, int64_t N, int64_t C, int64_t H, int64_t W, int64_t Cp,
                          int pad, const PositFmt& f, const PositFmt& fs, uint32_t* lut, bool build_lut,
@@ -510,6 +531,11 @@ cudaError_t act_digits(int D, const void* x, int64_t N, int64_t C, int64_t H, in
                        int wide_planes = 0, bool reduce_stores = false, const uint8_t* also_if = nullptr,
                        const uint8_t* only_if = nullptr) {
     if (lut == nullptr && !same_fmt(f, fs)) return cudaErrorInvalidValue;  // no in-register convert
+    if (lut != nullptr && build_lut)
+        if (uint32_t* c = cached_digit_lut(D, fs, f, st)) {
+            lut = c;
+            build_lut = false;
+        }
     // reduce_stores (every consumer of these digits is a flag-selected variant):
     // store only the planes the reduced-digit kernels read, then a completion
     // pass (exits at once unless the wide flag is set) writes all planes
@@ -539,8 +565,14 @@ cudaError_t im2col_digits_t(int D, const SrcT* x, const ConvGeom& g, const Posit
     const int grid = grid_for(g.N * g.OH * g.OW, 256);  // thread per output pixel
     if (g.N * g.OH * g.OW >= (int64_t(1) << 31)) return cudaErrorInvalidValue;
     const FastDiv fd_p{uint32_t(g.OH * g.OW)}, fd_ow{uint32_t(g.OW)};
+    bool build = lut != nullptr;
+    if (build)
+        if (uint32_t* c = cached_digit_lut(D, fs, f, st)) {
+            lut = c;
+            build = false;
+        }
 #define PNN_I2C(DD)                                                                          \
-    if (lut) digit_lut_conv_kernel<DD><<<16, 256, 0, st>>>(fs, f, lut);                      \
+    if (build) digit_lut_conv_kernel<DD><<<16, 256, 0, st>>>(fs, f, lut);                    \
     im2col_digits_kernel<DD, SrcT><<<grid, 256, 0, st>>>(                                   \
         x, int(g.N), int(g.C), int(g.H), int(g.W), int(g.KH), int(g.KW), g.pad, int(g.OH),   \
         int(g.OW), fd_p, fd_ow, f, fs, lut, dig, pos_nar, chw_nar, any, wide, wide_planes)
