@@ -677,19 +677,18 @@ struct SgdLuts {
 // round chains in flight); a few blocks per SM, each looping (the per-block
 // setup -- rounding table, segment table -- is paid once per block).
 constexpr int kSgdU = 4;
-__global__ void __launch_bounds__(256) sgd_lut_kernel(PositFmt fo, int bo, int bg, int b1, int b2,
-                                                      const __grid_constant__ SgdSegs segs, SgdLuts t) {
+// TO / TG / T1 / T2: code types of master, gradient, copies (compile-time
+// widths: no per-element width branches); FMT: fixed_fmt id of the optimizer
+// format (compile-time decode / rounding) or 0.  Segment pointers are global
+// memory: loads by __ldg, stores by st.global (no generic LD/ST).
+template <typename TO, typename TG, typename T1, typename T2, int FMT>
+__global__ void __launch_bounds__(256) sgd_lut_kernel(PositFmt fo_rt, const __grid_constant__ SgdSegs segs,
+                                                      SgdLuts t) {
+    const PositFmt fo = fixed_fmt<FMT>(fo_rt);
     __shared__ uint4 s_lut[kPackLutEntries];
     build_pack_lut(fo, s_lut, threadIdx.x, blockDim.x);
     __shared__ int64_t s_start[kSgdMaxSeg + 1];
-    __shared__ const void* s_ptr[4][kSgdMaxSeg];
     for (int i = threadIdx.x; i <= segs.count; i += blockDim.x) s_start[i] = segs.start[i];
-    for (int i = threadIdx.x; i < segs.count; i += blockDim.x) {
-        s_ptr[0][i] = segs.master[i];
-        s_ptr[1][i] = segs.grad[i];
-        s_ptr[2][i] = segs.copy1[i];
-        s_ptr[3][i] = segs.copy2[i];
-    }
     __syncthreads();
     const uint32_t nar = 1u << (fo.nbits - 1);
     const int64_t total = s_start[segs.count];
@@ -700,24 +699,29 @@ __global__ void __launch_bounds__(256) sgd_lut_kernel(PositFmt fo, int bo, int b
     int seg = 0;
     while (seg + 1 < segs.count && s_start[seg + 1] <= r0 + threadIdx.x) ++seg;
     for (int64_t i0 = r0 + threadIdx.x; i0 < r1; i0 += kSgdU * int64_t(blockDim.x)) {
-        int sg[kSgdU];
-        int64_t k[kSgdU];
+        TO* mp[kSgdU];
+        T1* c1p[kSgdU];
+        T2* c2p[kSgdU];
         uint32_t w[kSgdU];
         int64_t xm[kSgdU];
+        bool on[kSgdU];
 #pragma unroll
         for (int u = 0; u < kSgdU; ++u) {
             const int64_t i = i0 + u * int64_t(blockDim.x);
             while (seg + 1 < segs.count && s_start[seg + 1] <= i) ++seg;
-            sg[u] = i < r1 ? seg : -1;
-            k[u] = i - s_start[seg];
-            if (sg[u] >= 0) {
-                xm[u] = __ldg(t.m + load_any(s_ptr[1][seg], k[u], bg));
-                w[u] = load_any(s_ptr[0][seg], k[u], bo);
+            on[u] = i < r1;
+            const int64_t k = i - s_start[seg];
+            mp[u] = static_cast<TO*>(segs.master[seg]) + k;
+            c1p[u] = segs.copy1[seg] ? static_cast<T1*>(segs.copy1[seg]) + k : nullptr;
+            c2p[u] = segs.copy2[seg] ? static_cast<T2*>(segs.copy2[seg]) + k : nullptr;
+            if (on[u]) {
+                xm[u] = __ldg(t.m + uint32_t(__ldg(static_cast<const TG*>(segs.grad[seg]) + k)));
+                w[u] = uint32_t(__ldg(mp[u]));
             }
         }
 #pragma unroll
         for (int u = 0; u < kSgdU; ++u) {
-            if (sg[u] < 0) continue;
+            if (!on[u]) continue;
             uint32_t r;
             if (w[u] == nar || xm[u] == INT64_MIN) {
                 r = nar;
@@ -727,15 +731,31 @@ __global__ void __launch_bounds__(256) sgd_lut_kernel(PositFmt fo, int bo, int b
                 r = x_to_posit_lut(fo, Xw - xm[u], s_lut);
             }
             w[u] = r;
-            store_any(const_cast<void*>(s_ptr[0][sg[u]]), k[u], bo, r);
+            __stcg(mp[u], TO(r));
         }
 #pragma unroll
         for (int u = 0; u < kSgdU; ++u) {
-            if (sg[u] < 0) continue;
-            if (s_ptr[2][sg[u]]) store_any(const_cast<void*>(s_ptr[2][sg[u]]), k[u], b1, __ldg(t.c1 + w[u]));
-            if (s_ptr[3][sg[u]]) store_any(const_cast<void*>(s_ptr[3][sg[u]]), k[u], b2, __ldg(t.c2 + w[u]));
+            if (!on[u]) continue;
+            if (c1p[u]) __stcg(c1p[u], T1(__ldg(t.c1 + w[u])));
+            if (c2p[u]) __stcg(c2p[u], T2(__ldg(t.c2 + w[u])));
         }
     }
+}
+
+template <typename TO, typename TG, typename T1, typename T2>
+void launch_sgd_lut(int grid, cudaStream_t st, const PositFmt& fo, const SgdSegs& sg, const SgdLuts& t) {
+    if (fixed_fmt_id(fo) == 4) sgd_lut_kernel<TO, TG, T1, T2, 4><<<grid, 256, 0, st>>>(fo, sg, t);
+    else if (fixed_fmt_id(fo) == 3) sgd_lut_kernel<TO, TG, T1, T2, 3><<<grid, 256, 0, st>>>(fo, sg, t);
+    else sgd_lut_kernel<TO, TG, T1, T2, 0><<<grid, 256, 0, st>>>(fo, sg, t);
+}
+
+template <typename TO, typename TG>
+void launch_sgd_lut_c(int b1, int b2, int grid, cudaStream_t st, const PositFmt& fo, const SgdSegs& sg,
+                      const SgdLuts& t) {
+    if (b1 == 1 && b2 == 1) launch_sgd_lut<TO, TG, uint8_t, uint8_t>(grid, st, fo, sg, t);
+    else if (b1 == 1) launch_sgd_lut<TO, TG, uint8_t, uint16_t>(grid, st, fo, sg, t);
+    else if (b2 == 1) launch_sgd_lut<TO, TG, uint16_t, uint8_t>(grid, st, fo, sg, t);
+    else launch_sgd_lut<TO, TG, uint16_t, uint16_t>(grid, st, fo, sg, t);
 }
 
 // avgpool2d, tensor_ops.cpp:672-691: window sum (quire: exact, one rounding;
@@ -1178,9 +1198,18 @@ int pnn_sgd_step_multi(int opt_nbits, int opt_es, int g_nbits, int g_es, uint32_
         sg.start[sg.count] = tot;
         if (tot == 0) continue;
         if (lut_path) {
-            const int gr = grid1((tot + kSgdU - 1) / kSgdU);
-            sgd_lut_kernel<<<gr < 148 * 4 ? gr : 148 * 4, 256, 0, (cudaStream_t)stream>>>(
-                fo, bytes_of(opt_nbits), bytes_of(g_nbits), bytes_of(f1.nbits), bytes_of(f2.nbits), sg, luts);
+            int gr = grid1((tot + kSgdU - 1) / kSgdU);
+            gr = gr < 148 * 4 ? gr : 148 * 4;
+            const int b1 = bytes_of(f1.nbits), b2 = bytes_of(f2.nbits);
+            const auto st = (cudaStream_t)stream;
+            if (bytes_of(opt_nbits) == 2 && bytes_of(g_nbits) == 2)
+                launch_sgd_lut_c<uint16_t, uint16_t>(b1, b2, gr, st, fo, sg, luts);
+            else if (bytes_of(opt_nbits) == 2)
+                launch_sgd_lut_c<uint16_t, uint8_t>(b1, b2, gr, st, fo, sg, luts);
+            else if (bytes_of(g_nbits) == 2)
+                launch_sgd_lut_c<uint8_t, uint16_t>(b1, b2, gr, st, fo, sg, luts);
+            else
+                launch_sgd_lut_c<uint8_t, uint8_t>(b1, b2, gr, st, fo, sg, luts);
             continue;
         }
         sgd_multi_kernel<<<grid1(tot), 256, 0, (cudaStream_t)stream>>>(
