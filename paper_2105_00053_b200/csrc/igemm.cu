@@ -10,6 +10,7 @@
 
 #include "igemm.h"
 #include "tables.h"
+#include "pdl.cuh"
 #include "igemm_core.cuh"
 
 namespace pnn_b200 {
@@ -352,8 +353,8 @@ cudaError_t launch_kernel(const CUtensorMap& tA, const CUtensorMap& tB, const Ig
         if (e != cudaSuccess) return e;
         const int64_t tiles = a.mtiles * a.ntiles * a.splits;
         const int64_t slots = int64_t(CPS) * num_sms();
-        k<<<int(tiles < slots ? tiles : slots), Geo::THREADS, Geo::SMEM, st>>>(tA, tB, a, out);
-        return cudaGetLastError();
+        return launch_pdl(k, dim3(unsigned(tiles < slots ? tiles : slots)), dim3(Geo::THREADS), Geo::SMEM, st,
+                          tA, tB, a, out);
     }
     if constexpr (D <= 3)
         k = a.f.W <= 32 ? igemm_kernel<D, NTT, CPS, ACC, 1, CodeT, MODE, 0, DA, OFF, DB>
@@ -377,8 +378,7 @@ cudaError_t launch_kernel(const CUtensorMap& tA, const CUtensorMap& tB, const Ig
     const int64_t tiles = a.mtiles * a.ntiles * a.splits;
     const int64_t slots = int64_t(CPS) * num_sms();
     const int grid = int(tiles < slots ? tiles : slots);
-    k<<<grid, Geo::THREADS, Geo::SMEM, st>>>(tA, tB, a, out);
-    return cudaGetLastError();
+    return launch_pdl(k, dim3(unsigned(grid)), dim3(Geo::THREADS), Geo::SMEM, st, tA, tB, a, out);
 }
 
 template <typename CodeT, int MODE>
@@ -494,19 +494,19 @@ cudaError_t act_digits_t(int D, const SrcT* x, int64_t N, int64_t C, int64_t H, 
 #define PNN_ACT(DD)                                                                                  \
     if (build_lut) digit_lut_conv_kernel<DD><<<16, 256, 0, st>>>(fs, f, lut);                        \
     if (tiled && gt.gate == nullptr)                                                                 \
-        act_digits_tiled_kernel<DD, SrcT, 0><<<tgrid, 256, 0, st>>>(                                 \
+        launch_pdl(act_digits_tiled_kernel<DD, SrcT, 0>, dim3(tgrid), dim3(256), 0, st,                                  \
             x, int(N), int(C), int(H), int(W), int(Cp), pad, fd_hw, fd_w, f, fs, lut, dig, pos_nar,  \
             chw_nar, chan_nar, any, gt, wide, wide_planes, store_planes, only_if, only_if2);         \
     else if (tiled && gt.gb == 1)                                                                    \
-        act_digits_tiled_kernel<DD, SrcT, 1><<<tgrid, 256, 0, st>>>(                                 \
+        launch_pdl(act_digits_tiled_kernel<DD, SrcT, 1>, dim3(tgrid), dim3(256), 0, st,                                  \
             x, int(N), int(C), int(H), int(W), int(Cp), pad, fd_hw, fd_w, f, fs, lut, dig, pos_nar,  \
             chw_nar, chan_nar, any, gt, wide, wide_planes, store_planes, only_if, only_if2);         \
     else if (tiled)                                                                                  \
-        act_digits_tiled_kernel<DD, SrcT, 2><<<tgrid, 256, 0, st>>>(                                 \
+        launch_pdl(act_digits_tiled_kernel<DD, SrcT, 2>, dim3(tgrid), dim3(256), 0, st,                                  \
             x, int(N), int(C), int(H), int(W), int(Cp), pad, fd_hw, fd_w, f, fs, lut, dig, pos_nar,  \
             chw_nar, chan_nar, any, gt, wide, wide_planes, store_planes, only_if, only_if2);         \
     else                                                                                             \
-        act_digits_kernel<DD, SrcT><<<grid, 256, 0, st>>>(x, int(N), int(C), int(H), int(W), int(Cp), \
+        launch_pdl(act_digits_kernel<DD, SrcT>, dim3(grid), dim3(256), 0, st, x, int(N), int(C), int(H), int(W), int(Cp), \
                                                           pad, fd_hw, fd_w, f, fs, lut, dig, pos_nar, \
                                                           chw_nar, chan_nar, any, gt, wide, wide_planes, \
                                                           store_planes, only_if, only_if2)
@@ -573,7 +573,7 @@ cudaError_t im2col_digits_t(int D, const SrcT* x, const ConvGeom& g, const Posit
         }
 #define PNN_I2C(DD)                                                                          \
     if (build) digit_lut_conv_kernel<DD><<<16, 256, 0, st>>>(fs, f, lut);                    \
-    im2col_digits_kernel<DD, SrcT><<<grid, 256, 0, st>>>(                                   \
+    launch_pdl(im2col_digits_kernel<DD, SrcT>, dim3(grid), dim3(256), 0, st,                                    \
         x, int(g.N), int(g.C), int(g.H), int(g.W), int(g.KH), int(g.KW), g.pad, int(g.OH),   \
         int(g.OW), fd_p, fd_ow, f, fs, lut, dig, pos_nar, chw_nar, any, wide, wide_planes)
     switch (D) {
@@ -609,7 +609,7 @@ cudaError_t weight_digits(int D, const CodeT* w, const CodeT* bias, int64_t F, i
     const int64_t total = (transpose ? C : F) * taps * Kp;
     const int grid = grid_for(total > F ? total : F, 256);
 #define PNN_WD(DD)                                                                              \
-    weight_digits_kernel<DD, CodeT><<<grid, 256, 0, st>>>(w, bias, int(F), int(C), int(taps),  \
+    launch_pdl(weight_digits_kernel<DD, CodeT>, dim3(grid), dim3(256), 0, st, w, bias, int(F), int(C), int(taps),  \
                                                           int(Kp), transpose, f, dig, col_add, \
                                                           col_nar, any, wide, wide_planes)
     switch (D) {
@@ -736,9 +736,9 @@ int run_fwd(const ImplPlan& p, const ConvGeom& g, const CodeT* x, const CodeT* w
     if (use_partial) {
         launch_finalize<CodeT>(a.partial, int(a.splits), nullptr, col_nar, out, a.M, a.N, f, nullptr, nullptr, st);
         if (relu)
-            relu_codes_kernel<CodeT><<<grid_for(a.M * a.N, 256), 256, 0, st>>>(y, pre, a.M * a.N, f.nbits);
+            launch_pdl(relu_codes_kernel<CodeT>, dim3(grid_for(a.M * a.N, 256)), dim3(256), 0, st, y, pre, a.M * a.N, f.nbits);
     }
-    fwd_nar_fixup_kernel<CodeT><<<grid_fixup(a.M), 256, 0, st>>>(
+    launch_pdl(fwd_nar_fixup_kernel<CodeT>, dim3(grid_fixup(a.M)), dim3(256), 0, st, 
         y, pos_nar, xflag, g.N, int(g.F), int(gv.H), int(gv.W), int(g.OH), int(g.OW), int(gv.KH),
         int(gv.KW), gv.pad, 1u << (f.nbits - 1), relu, pre);
     return rc_of(cudaGetLastError());
@@ -828,10 +828,10 @@ int run_dgrad(const ImplPlan& p, const ConvGeom& g, const CodeT* dy, const CodeT
     if (use_partial)
         launch_finalize<CodeT>(a.partial, int(a.splits), nullptr, nullptr, out, a.M, a.N, f, nullptr, nullptr, st);
     const uint32_t nar = 1u << (f.nbits - 1);
-    dgrad_nar_fixup_kernel<CodeT><<<grid_fixup(a.M), 256, 0, st>>>(
+    launch_pdl(dgrad_nar_fixup_kernel<CodeT>, dim3(grid_fixup(a.M)), dim3(256), 0, st, 
         dx, a_pos, a_any, g.N, int(g.C), int(g.H), int(g.W), int(g.OH), int(g.OW), int(g.KH),
         int(g.KW), g.pad, nar);
-    dgrad_weight_nar_kernel<CodeT><<<grid_fixup(a.M * a.N), 256, 0, st>>>(dx, w, g, flags + 1,
+    launch_pdl(dgrad_weight_nar_kernel<CodeT>, dim3(grid_fixup(a.M * a.N)), dim3(256), 0, st, dx, w, g, flags + 1,
                                                                              nar);
     return rc_of(cudaGetLastError());
 }
@@ -926,7 +926,7 @@ int run_wgrad(const ImplPlan& p, const ConvGeom& g, const void* dy, const PositF
     if (dispatch_wgrad<CodeT>(p.D, p.DA, p.OFF, tA, tB, a, out, st) != cudaSuccess) return 4;
     if (use_partial)
         launch_finalize<CodeT>(a.partial, int(a.splits), nullptr, col_nar, out, a.M, a.N, f, raw_words, raw_nar, st);
-    wgrad_nar_fixup_kernel<CodeT><<<grid_for(p.ckk, 128), 128, 0, st>>>(
+    launch_pdl(wgrad_nar_fixup_kernel<CodeT>, dim3(grid_for(p.ckk, 128)), dim3(128), 0, st, 
         dw, raw_nar, chw_nar, xflag, int(g.F), p.fold ? p.ckk : int(g.C), int(gv.H), int(gv.W),
         int(g.OH), int(g.OW), int(gv.KH), int(gv.KW), gv.pad, 1u << (f.nbits - 1));
     return rc_of(cudaGetLastError());
@@ -1096,10 +1096,10 @@ int igemm_conv_backward(const PositFmt& ff, const PositFmt& fb, const PositFmt& 
     if (dy_gated != nullptr) {  // the ReLU's input gradient itself (recording / the bias gradient)
         const int64_t total = g.N * g.F * g.OH * g.OW;
         if (fb.nbits <= 8)
-            gate_codes_kernel<uint8_t><<<grid_for(total, 256), 256, 0, st>>>(
+            launch_pdl(gate_codes_kernel<uint8_t>, dim3(grid_for(total, 256)), dim3(256), 0, st, 
                 static_cast<const uint8_t*>(dy), gt, static_cast<uint8_t*>(dy_gated), total);
         else
-            gate_codes_kernel<uint16_t><<<grid_for(total, 256), 256, 0, st>>>(
+            launch_pdl(gate_codes_kernel<uint16_t>, dim3(grid_for(total, 256)), dim3(256), 0, st, 
                 static_cast<const uint16_t*>(dy), gt, static_cast<uint16_t*>(dy_gated), total);
     }
     const bool g8 = fg.nbits <= 8, b8 = fb.nbits <= 8;

@@ -26,6 +26,7 @@
 
 #include "epilogue.cuh"
 #include "fastdiv.cuh"
+#include "pdl.cuh"
 #include "igemm.h"
 #include "posit_scalar.cuh"
 #include "quire_gemm_core.cuh"
@@ -138,14 +139,7 @@ __global__ void __launch_bounds__(ImplGeo<D, NT_, CPS, ACC, DA, DB>::THREADS, CP
                  const IgemmArgs a, const OutMap<CodeT> out) {
     static_assert(MODE == 2 || OFF == 0, "digit offset: weight gradient only");
     using Geo = ImplGeo<D, NT_, CPS, ACC, DA, DB>;
-    // device-selected variant: exit at once unless the flag (written by the
-    // weight digitiser on this stream) matches
-    if (a.vor) {  // run iff (either flag set) == vexpect
-        if (int(*a.vflag != 0 || *a.vflag2 != 0) != a.vexpect) return;
-    } else {
-        if (a.vflag != nullptr && int(*a.vflag != 0) != a.vexpect) return;
-        if (a.vflag2 != nullptr && int(*a.vflag2 != 0) != a.vexpect2) return;
-    }
+    pdl_trigger();  // the next kernel's CTAs may start their prologue in this grid's tail
     constexpr int kIEpiWarps = Geo::EPI;
     constexpr int kIThreads = Geo::THREADS;
     using QT = typename QuireWord<QW>::T;
@@ -183,6 +177,16 @@ __global__ void __launch_bounds__(ImplGeo<D, NT_, CPS, ACC, DA, DB>::THREADS, CP
             ptx::mbar_init(&tmem_empty[b], kIEpiWarps);
         }
         ptx::fence_barrier_init();
+    }
+    // everything above touched only shared memory and parameters (PDL prologue)
+    pdl_wait();
+    // device-selected variant: exit at once unless the flag (written by the
+    // weight digitiser on this stream) matches
+    if (a.vor) {  // run iff (either flag set) == vexpect
+        if (int(*a.vflag != 0 || *a.vflag2 != 0) != a.vexpect) return;
+    } else {
+        if (a.vflag != nullptr && int(*a.vflag != 0) != a.vexpect) return;
+        if (a.vflag2 != nullptr && int(*a.vflag2 != 0) != a.vexpect2) return;
     }
     if (warp == 1) ptx::tmem_alloc<Geo::TMEM_COLS>(tmem_slot);
     ptx::fence_proxy_async_smem();
@@ -431,6 +435,8 @@ __global__ void __launch_bounds__(ImplGeo<D, NT_, CPS, ACC, DA, DB>::THREADS, CP
 // conversions) without a separate convert pass.
 template <int D>
 __global__ void digit_lut_conv_kernel(PositFmt fs, PositFmt f, uint32_t* __restrict__ lut) {
+    pdl_trigger();
+    pdl_wait();  // PDL: nothing above touches global memory (pdl.cuh)
     const bool same = fs.nbits == f.nbits && fs.es == f.es;
     for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < (1 << fs.nbits);
          c += gridDim.x * blockDim.x) {
@@ -491,6 +497,8 @@ struct DigitGate {
 template <typename CodeT>
 __global__ void gate_codes_kernel(const CodeT* __restrict__ dy, DigitGate gt, CodeT* __restrict__ out,
                                   int64_t n) {
+    pdl_trigger();
+    pdl_wait();  // PDL: nothing above touches global memory (pdl.cuh)
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
          i += int64_t(gridDim.x) * blockDim.x)
         out[i] = gt.open(i) ? dy[i] : CodeT(0);
@@ -601,6 +609,8 @@ __global__ void __launch_bounds__(256) act_digits_kernel(
     uint8_t* __restrict__ chan_nar, uint8_t* __restrict__ any, DigitGate gt = DigitGate{},
     uint8_t* __restrict__ wide = nullptr, int wide_planes = 0, int store_planes = D,
     const uint8_t* __restrict__ only_if = nullptr, const uint8_t* __restrict__ only_if2 = nullptr) {
+    pdl_trigger();
+    pdl_wait();  // PDL: nothing above touches global memory (pdl.cuh)
     // completion pass: runs iff a consumer reads the high planes
     if (only_if != nullptr && *only_if == 0 && (only_if2 == nullptr || *only_if2 == 0)) return;
     const uint32_t HW = uint32_t(H) * uint32_t(W);
@@ -643,6 +653,8 @@ __global__ void __launch_bounds__(256) act_digits_tiled_kernel(
     uint8_t* __restrict__ chan_nar, uint8_t* __restrict__ any, DigitGate gt = DigitGate{},
     uint8_t* __restrict__ wide = nullptr, int wide_planes = 0, int store_planes = D,
     const uint8_t* __restrict__ only_if = nullptr, const uint8_t* __restrict__ only_if2 = nullptr) {
+    pdl_trigger();
+    pdl_wait();  // PDL: nothing above touches global memory (pdl.cuh)
     // completion pass: runs iff a consumer reads the high planes
     if (only_if != nullptr && *only_if == 0 && (only_if2 == nullptr || *only_if2 == 0)) return;
     constexpr int TP = 256;                                   // pixels per tile
@@ -745,6 +757,8 @@ __global__ void __launch_bounds__(256) im2col_digits_kernel(
     int OW, FastDiv fd_p, FastDiv fd_ow, PositFmt f, PositFmt fs, const uint32_t* __restrict__ lut,
     int8_t* __restrict__ dig, uint8_t* __restrict__ pos_nar, uint8_t* __restrict__ chw_nar,
     uint8_t* __restrict__ any, uint8_t* __restrict__ wide = nullptr, int wide_planes = 0) {
+    pdl_trigger();
+    pdl_wait();  // PDL: nothing above touches global memory (pdl.cuh)
     const int ckk = C * KH * KW, khw = KH * KW;
     const uint32_t nar_code = 1u << (fs.nbits - 1);  // fs: the codes' format (lut converts)
     const uint32_t P = uint32_t(OH) * uint32_t(OW);
@@ -821,6 +835,8 @@ __global__ void weight_digits_kernel(const CodeT* __restrict__ w, const CodeT* _
                                      int8_t* __restrict__ dig, int64_t* __restrict__ col_add,
                                      uint8_t* __restrict__ col_nar, uint8_t* __restrict__ any,
                                      uint8_t* __restrict__ wide = nullptr, int wide_planes = 0) {
+    pdl_trigger();
+    pdl_wait();  // PDL: nothing above touches global memory (pdl.cuh)
     const int rows = transpose ? C : F;
     const int inner = transpose ? F : C;
     const int64_t total = int64_t(rows) * taps * Kp;
@@ -870,6 +886,8 @@ template <typename CodeT>
 __global__ void dgrad_weight_nar_kernel(CodeT* __restrict__ dx, const CodeT* __restrict__ w,
                                         ConvGeom g, const uint8_t* __restrict__ any_nar_w,
                                         uint32_t nar) {
+    pdl_trigger();
+    pdl_wait();  // PDL: nothing above touches global memory (pdl.cuh)
     if (*any_nar_w == 0) return;
     const int64_t total = g.N * g.C * g.H * g.W;
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total;
@@ -903,6 +921,8 @@ __global__ void fwd_nar_fixup_kernel(CodeT* __restrict__ y, const uint8_t* __res
                                      const uint8_t* __restrict__ any, int64_t N, int F, int H,
                                      int W, int OH, int OW, int KH, int KW, int pad, uint32_t nar,
                                      int relu = 0, CodeT* __restrict__ pre = nullptr) {
+    pdl_trigger();
+    pdl_wait();  // PDL: nothing above touches global memory (pdl.cuh)
     if (*any == 0) return;
     const int64_t total = N * OH * OW;
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total;
@@ -929,6 +949,8 @@ __global__ void fwd_nar_fixup_kernel(CodeT* __restrict__ y, const uint8_t* __res
 // fused Conv2d + ReLU, after quire_finalize_kernel
 template <typename CodeT>
 __global__ void relu_codes_kernel(CodeT* __restrict__ y, CodeT* __restrict__ pre, int64_t n, int nbits) {
+    pdl_trigger();
+    pdl_wait();  // PDL: nothing above touches global memory (pdl.cuh)
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
          i += int64_t(gridDim.x) * blockDim.x) {
         const uint32_t c = uint32_t(y[i]);
@@ -942,6 +964,8 @@ template <typename CodeT>
 __global__ void dgrad_nar_fixup_kernel(CodeT* __restrict__ dx, const uint8_t* __restrict__ pos_nar,
                                        const uint8_t* __restrict__ any, int64_t N, int C, int H,
                                        int W, int OH, int OW, int KH, int KW, int pad, uint32_t nar) {
+    pdl_trigger();
+    pdl_wait();  // PDL: nothing above touches global memory (pdl.cuh)
     if (*any == 0) return;
     const int64_t total = N * H * W;
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total;
@@ -966,6 +990,8 @@ __global__ void wgrad_nar_fixup_kernel(CodeT* __restrict__ dw, uint8_t* __restri
                                        const uint8_t* __restrict__ chw_nar,
                                        const uint8_t* __restrict__ any, int F, int C, int H, int W,
                                        int OH, int OW, int KH, int KW, int pad, uint32_t nar) {
+    pdl_trigger();
+    pdl_wait();  // PDL: nothing above touches global memory (pdl.cuh)
     if (*any == 0) return;
     const int taps = KH * KW;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < C * taps; i += gridDim.x * blockDim.x) {
