@@ -659,23 +659,52 @@ __global__ void __launch_bounds__(256) act_digits_tiled_kernel(
     if (only_if != nullptr && *only_if == 0 && (only_if2 == nullptr || *only_if2 == 0)) return;
     constexpr int TP = 256;                                   // pixels per tile
     constexpr int VPR = TP * int(sizeof(CodeT)) / 16;         // 16-byte vectors per channel row
-    __shared__ uint4 s_tile[32 * VPR];
+    // ungated: two tile buffers, the next tile's rows in flight (cp.async)
+    // while this tile is digitised
+    constexpr int NB = GB == 0 ? 2 : 1;
+    __shared__ uint4 s_tile[NB][32 * VPR];
     __shared__ uint4 s_gate[GB > 0 ? 32 * TP * GB / 16 : 1];  // gate codes (GB bytes each)
     const uint32_t HW = uint32_t(H) * uint32_t(W);
     const uint32_t tiles = uint32_t(N) * (HW / TP);
     const int64_t plane = int64_t(N) * (H + 2 * pad) * (W + 2 * pad) * Cp;
     const int cc = blockIdx.y, c0 = cc * 32;
     const uint32_t nar_code = 1u << (fs.nbits - 1);
-    for (uint32_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+    auto load_async = [&](uint32_t t, int b) {
+        uint32_t n, pix0;
+        fd_hw.divmod(t * TP, n, pix0);
+        for (int i = threadIdx.x; i < 32 * VPR; i += blockDim.x) {
+            const int c = i / VPR, v = i - c * VPR;
+            if (c0 + c < C)
+                ptx::cp_async16(&s_tile[b][i],
+                                reinterpret_cast<const uint4*>(x + (int64_t(n) * C + c0 + c) * HW + pix0) + v);
+            else
+                s_tile[b][i] = make_uint4(0, 0, 0, 0);
+        }
+        ptx::cp_async_commit();
+    };
+    if constexpr (GB == 0)
+        if (blockIdx.x < tiles) load_async(blockIdx.x, 0);
+    int buf = 0;
+    for (uint32_t t = blockIdx.x; t < tiles; t += gridDim.x, buf ^= NB - 1) {
         const uint32_t r0 = t * TP;
         uint32_t n, pix0;
         fd_hw.divmod(r0, n, pix0);
         __syncthreads();  // previous tile's readers are done
-        for (int i = threadIdx.x; i < 32 * VPR; i += blockDim.x) {
-            const int c = i / VPR, v = i - c * VPR;
-            s_tile[i] = c0 + c < C ? __ldg(reinterpret_cast<const uint4*>(
-                                         x + (int64_t(n) * C + c0 + c) * HW + pix0) + v)
-                                   : make_uint4(0, 0, 0, 0);
+        if constexpr (GB == 0) {
+            if (t + gridDim.x < tiles) {
+                load_async(t + gridDim.x, buf ^ 1);
+                ptx::cp_async_wait<1>();  // this tile's group has landed
+            } else {
+                ptx::cp_async_wait<0>();
+            }
+            __syncthreads();
+        } else {
+            for (int i = threadIdx.x; i < 32 * VPR; i += blockDim.x) {
+                const int c = i / VPR, v = i - c * VPR;
+                s_tile[0][i] = c0 + c < C ? __ldg(reinterpret_cast<const uint4*>(
+                                                x + (int64_t(n) * C + c0 + c) * HW + pix0) + v)
+                                          : make_uint4(0, 0, 0, 0);
+            }
         }
         if constexpr (GB > 0) {
             constexpr int GVPR = TP * GB / 16;
@@ -688,8 +717,8 @@ __global__ void __launch_bounds__(256) act_digits_tiled_kernel(
                                 : make_uint4(0, 0, 0, 0);
             }
         }
-        __syncthreads();
-        const CodeT* st = reinterpret_cast<const CodeT*>(s_tile);
+        if constexpr (GB > 0) __syncthreads();
+        const CodeT* st = reinterpret_cast<const CodeT*>(s_tile[buf]);
         uint32_t code[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) code[j] = uint32_t(st[j * TP + threadIdx.x]);
