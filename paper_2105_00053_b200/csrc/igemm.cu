@@ -575,7 +575,8 @@ cudaError_t im2col_digits_t(int D, const SrcT* x, const ConvGeom& g, const Posit
     if (build) digit_lut_conv_kernel<DD><<<16, 256, 0, st>>>(fs, f, lut);                    \
     launch_pdl(im2col_digits_kernel<DD, SrcT>, dim3(grid), dim3(256), 0, st,                                    \
         x, int(g.N), int(g.C), int(g.H), int(g.W), int(g.KH), int(g.KW), g.pad, int(g.OH),   \
-        int(g.OW), fd_p, fd_ow, f, fs, lut, dig, pos_nar, chw_nar, any, wide, wide_planes)
+        int(g.OW), fd_p, fd_ow, f, fs, lut, dig, pos_nar, chw_nar, any, wide, wide_planes, DD,     \
+        static_cast<const uint8_t*>(nullptr))
     switch (D) {
         case 2: PNN_I2C(2); break;
         case 3: PNN_I2C(3); break;

@@ -451,7 +451,7 @@ __global__ void digit_lut_conv_kernel(PositFmt fs, PositFmt f, uint32_t* __restr
 // Digits of 4 consecutive channels (codes c[0..3]) as one 4-byte word per
 // plane in registers: words[p][q] for 4-channel group q (the caller stores
 // whole 32-byte rows per plane); returns a mask of NaR codes.
-template <int D>
+template <int D, bool kSmemLut = false>
 __device__ __forceinline__ uint32_t digits4_words(const uint32_t (&c)[4], const PositFmt& f,
                                                   uint32_t nar_code, const uint32_t* __restrict__ lut,
                                                   uint32_t (&words)[D][8], int q) {
@@ -460,7 +460,8 @@ __device__ __forceinline__ uint32_t digits4_words(const uint32_t (&c)[4], const 
     for (int jj = 0; jj < 4; ++jj) {
         bool nar;
         if (lut != nullptr) {
-            const uint2 v = __ldg(reinterpret_cast<const uint2*>(lut) + c[jj]);
+            const uint2 v = kSmemLut ? reinterpret_cast<const uint2*>(lut)[c[jj]]  // shared-memory table
+                                     : __ldg(reinterpret_cast<const uint2*>(lut) + c[jj]);
             lo[jj] = v.x;
             hi[jj] = v.y;
             nar = c[jj] == nar_code;
@@ -520,7 +521,7 @@ __global__ void gate_codes_kernel(const CodeT* __restrict__ dy, DigitGate gt, Co
 // One pixel x one 32-channel chunk: digits of code[0..31] -> the slice-layout
 // cells of pixel (n, h, w) (+ the zero ring cells a border pixel owns), NaR
 // summaries.  plane = bytes per digit plane.  Shared by the digitisers below.
-template <int D>
+template <int D, bool kSmemLut = false>
 __device__ __forceinline__ void emit_pixel_digits(const uint32_t (&code)[32], uint32_t r, uint32_t n,
                                                   uint32_t pix, uint32_t h, uint32_t w, int cc, int C,
                                                   int H, int W, int Cp, int pad, int64_t plane,
@@ -536,10 +537,18 @@ __device__ __forceinline__ void emit_pixel_digits(const uint32_t (&code)[32], ui
     const int c0 = cc * 32;
     uint32_t words[D][8];
     uint32_t nm = 0;
+    if (lut != nullptr) {  // (branch hoisted out of the per-code loop)
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-        const uint32_t c4[4] = {code[4 * q], code[4 * q + 1], code[4 * q + 2], code[4 * q + 3]};
-        nm |= digits4_words<D>(c4, f, nar_code, lut, words, q) << (4 * q);
+        for (int q = 0; q < 8; ++q) {
+            const uint32_t c4[4] = {code[4 * q], code[4 * q + 1], code[4 * q + 2], code[4 * q + 3]};
+            nm |= digits4_words<D, kSmemLut>(c4, f, nar_code, lut, words, q) << (4 * q);
+        }
+    } else {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const uint32_t c4[4] = {code[4 * q], code[4 * q + 1], code[4 * q + 2], code[4 * q + 3]};
+            nm |= digits4_words<D>(c4, f, nar_code, nullptr, words, q) << (4 * q);
+        }
     }
     if (wide != nullptr) {  // digit planes >= wide_planes in use (reduced-digit variants)
         uint32_t o = 0;
@@ -669,6 +678,14 @@ __global__ void __launch_bounds__(256) act_digits_tiled_kernel(
     const int64_t plane = int64_t(N) * (H + 2 * pad) * (W + 2 * pad) * Cp;
     const int cc = blockIdx.y, c0 = cc * 32;
     const uint32_t nar_code = 1u << (fs.nbits - 1);
+    // 8-bit source codes: the digit table (<= 256 x 8 bytes) in shared memory
+    constexpr bool kSL = sizeof(CodeT) == 1;
+    __shared__ uint2 s_dlut[kSL ? 256 : 1];
+    if constexpr (kSL)
+        if (lut != nullptr)
+            for (int i = threadIdx.x; i < (1 << fs.nbits); i += blockDim.x)
+                s_dlut[i] = __ldg(reinterpret_cast<const uint2*>(lut) + i);
+    const uint32_t* lut_use = kSL && lut != nullptr ? reinterpret_cast<const uint32_t*>(s_dlut) : lut;
     auto load_async = [&](uint32_t t, int b) {
         uint32_t n, pix0;
         fd_hw.divmod(t * TP, n, pix0);
@@ -737,8 +754,8 @@ __global__ void __launch_bounds__(256) act_digits_tiled_kernel(
         // pixel cells only (pad 0 below); the zero ring of this tile's rows is
         // written cooperatively afterwards (per-thread ring loops diverge in
         // every warp: each image row has a first and a last pixel)
-        emit_pixel_digits<D>(code, r0 + threadIdx.x, n, pix, h, w, cc, C, H, W, Cp, pad, plane, HW, f,
-                             nar_code, lut, dig, pos_nar, chw_nar, chan_nar, any, /*ring=*/false, wide,
+        emit_pixel_digits<D, kSL>(code, r0 + threadIdx.x, n, pix, h, w, cc, C, H, W, Cp, pad, plane, HW, f,
+                                  nar_code, lut_use, dig, pos_nar, chw_nar, chan_nar, any, /*ring=*/false, wide,
                              wide_planes, store_planes);
         if (pad > 0) {
             const int Hp = H + 2 * pad, Wp = W + 2 * pad, CS = Cp / 16;
@@ -785,9 +802,20 @@ __global__ void __launch_bounds__(256) im2col_digits_kernel(
     const CodeT* __restrict__ x, int N, int C, int H, int W, int KH, int KW, int pad, int OH,
     int OW, FastDiv fd_p, FastDiv fd_ow, PositFmt f, PositFmt fs, const uint32_t* __restrict__ lut,
     int8_t* __restrict__ dig, uint8_t* __restrict__ pos_nar, uint8_t* __restrict__ chw_nar,
-    uint8_t* __restrict__ any, uint8_t* __restrict__ wide = nullptr, int wide_planes = 0) {
+    uint8_t* __restrict__ any, uint8_t* __restrict__ wide = nullptr, int wide_planes = 0,
+    int store_planes = D, const uint8_t* __restrict__ only_if = nullptr) {
     pdl_trigger();
     pdl_wait();  // PDL: nothing above touches global memory (pdl.cuh)
+    // completion pass: runs iff a consumer reads the high planes
+    if (only_if != nullptr && *only_if == 0) return;
+    // 8-bit source codes: the digit table in shared memory
+    constexpr bool kSL = sizeof(CodeT) == 1;
+    __shared__ uint2 s_dlut[kSL ? 256 : 1];
+    if constexpr (kSL)
+        if (lut != nullptr)
+            for (int i = threadIdx.x; i < (1 << fs.nbits); i += blockDim.x)
+                s_dlut[i] = __ldg(reinterpret_cast<const uint2*>(lut) + i);
+    const uint32_t* lut_use = kSL && lut != nullptr ? reinterpret_cast<const uint32_t*>(s_dlut) : lut;
     const int ckk = C * KH * KW, khw = KH * KW;
     const uint32_t nar_code = 1u << (fs.nbits - 1);  // fs: the codes' format (lut converts)
     const uint32_t P = uint32_t(OH) * uint32_t(OW);
@@ -823,9 +851,10 @@ __global__ void __launch_bounds__(256) im2col_digits_kernel(
                              ? uint32_t(xn[s_off[k]])
                              : 0u;
             }
-            nm |= digits4_words<D>(c4, f, nar_code, lut, words, q) << (4 * q);
+            nm |= lut_use != nullptr ? digits4_words<D, kSL>(c4, f, nar_code, lut_use, words, q) << (4 * q)
+                                     : digits4_words<D>(c4, f, nar_code, nullptr, words, q) << (4 * q);
         }
-        if (wide != nullptr) {  // digit planes >= wide_planes in use
+        if (wide != nullptr && only_if == nullptr) {  // digit planes >= wide_planes in use
             uint32_t o = 0;
 #pragma unroll
             for (int p = 0; p < D; ++p)
@@ -838,6 +867,7 @@ __global__ void __launch_bounds__(256) im2col_digits_kernel(
         int8_t* dst = dig + ((row * 2) * OW + ox) * 16;
 #pragma unroll
         for (int p = 0; p < D; ++p) {
+            if (p >= store_planes) break;  // high planes: written by the completion pass if used
             *reinterpret_cast<uint4*>(dst + p * plane) =
                 make_uint4(words[p][0], words[p][1], words[p][2], words[p][3]);
             *reinterpret_cast<uint4*>(dst + p * plane + int64_t(OW) * 16) =
