@@ -1033,8 +1033,9 @@ cudaError_t launch_generic(const QuireGemmPlan& p, const GemmArgs& g, FA fa, FB 
     // reduced-digit variant (posit(12,1)-class D = 6 operands within 3 digits):
     // the packs flag wide operands in flags[2], flags[3]
     constexpr int kRed = D == 8 ? 4 : 3;
-    const bool reduced = (D == 6 || D == 8) && !p.pair && sizeof(CodeT) == 2 &&
-                         g.M * g.N * g.K >= variant_min_work();  // the extra launch pays off
+    // (D = 4: posit(8,1)-class operands within 3 digits, 9 instead of 16 digit MMAs)
+    const bool reduced = ((D == 6 || D == 8) && sizeof(CodeT) == 2 || D == 4 && sizeof(CodeT) == 1) &&
+                         !p.pair && g.M * g.N * g.K >= variant_min_work();  // the extra launch pays off
     const int ga = int(a_work < 148 * 8 ? a_work : 148 * 8), gb = int(b_work < 148 * 8 ? b_work : 148 * 8);
     if (D == 8 && sizeof(CodeT) == 2 && fixed_fmt_id(f) == 4) {  // posit(16,1): compile-time decode
         pack_kernel<D, kBM, CodeT, FA, 4><<<ga, 256, 0, st>>>(fa, g.M, g.K, f, a_img, rnar, flags,
@@ -1110,13 +1111,14 @@ cudaError_t launch_generic(const QuireGemmPlan& p, const GemmArgs& g, FA fa, FB 
     } else {
         const int64_t tiles = p.mtiles * p.ntiles * p.splits;
         const int grid = int(tiles < num_sms() ? tiles : num_sms());
-        if constexpr ((D == 6 || D == 8) && sizeof(CodeT) == 2) {
+        if constexpr ((D == 6 || D == 8) && sizeof(CodeT) == 2 || D == 4 && sizeof(CodeT) == 1) {
             if (reduced) {  // both launched; the pack flags let exactly one run
                 using GR = Geometry<D, kRed>;
                 // (128-bit word: this epilogue's quire_word_to_posit_bf takes W <= word bits)
-                constexpr int kFmt = D == 6 ? 3 : 4;
-                KernFn kr = fixed_fmt_id(f) == kFmt ? quire_gemm_tc_kernel<D, 4, CodeT, false, kFmt, kRed>
-                                                    : quire_gemm_tc_kernel<D, 4, CodeT, false, 0, kRed>;
+                constexpr int kFmt = D == 4 ? 2 : D == 6 ? 3 : 4;
+                constexpr int kQW = D == 4 ? 2 : 4;  // posit(8,1)-class: W <= 64
+                KernFn kr = fixed_fmt_id(f) == kFmt ? quire_gemm_tc_kernel<D, kQW, CodeT, false, kFmt, kRed>
+                                                    : quire_gemm_tc_kernel<D, kQW, CodeT, false, 0, kRed>;
                 if ((e = cudaFuncSetAttribute(kr, cudaFuncAttributeMaxDynamicSharedMemorySize, GR::SMEM)) !=
                     cudaSuccess)
                     return e;

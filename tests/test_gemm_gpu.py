@@ -336,3 +336,27 @@ def test_matmul_host_dma_split(cuda, po, env):
                        env=dict(os.environ, **env),
                        cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     assert r.returncode == 0 and "split ok" in r.stdout, r.stderr[-3000:]
+
+
+@pytest.mark.parametrize("cfg,limit", [((8, 1), 2.0 ** 11), ((12, 1), 8.0), ((16, 1), 8.0)])
+@pytest.mark.parametrize("small", [True, False])
+def test_reduced_digit_gemm_variants(cuda, po, cfg, limit, small):
+    """Device-selected reduced-digit variants of the explicit quire GEMM
+    (posit(8,1) in 3 of 4 digits, (12,1) in 3 of 6, (16,1) in 4 of 8), forced
+    on for small problems: operands within the reduced digits take the reduced
+    kernel, a single wide value the full one -- both equal the oracle."""
+    n, es = cfg
+    lib = _native.lib()
+    prev = lib.pnn_variant_min_work(0)
+    try:
+        rng = np.random.default_rng(n * 10 + small)
+        codes = np.arange(1 << n, dtype=np.uint64)
+        vals = np.array([po.to_float64(n, es, int(c)) for c in codes])
+        ok = codes[(np.abs(vals) < limit) & np.isfinite(vals)] if small else codes[codes != (1 << (n - 1))]
+        A = rng.choice(ok, (300, 200)).astype(np.uint64)
+        B = rng.choice(ok, (200, 140)).astype(np.uint64)
+        A[7, 3] = 1 << (n - 1)  # a NaR row
+        got = gemm(cfg, A, B)
+        assert (got == po.matmul(n, es, A, B)).all()
+    finally:
+        lib.pnn_variant_min_work(prev)
