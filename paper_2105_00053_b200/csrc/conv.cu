@@ -24,6 +24,7 @@
 #include "../../include/pnn_b200.h"
 #include "igemm.h"
 #include "igemm_core.cuh"
+#include "pdl.cuh"
 #include "status.h"
 #include "tables.h"
 
@@ -237,6 +238,8 @@ __global__ void __launch_bounds__(256) bias_grad_cols_kernel(
     const CodeT* __restrict__ dy, int64_t N, int64_t F, PositFmt f, int slices,
     const int64_t* __restrict__ xlut, unsigned __int128* __restrict__ partial,
     uint8_t* __restrict__ nar_out) {
+    pdl_trigger();
+    pdl_wait();  // PDL: nothing above touches global memory (pdl.cuh)
     const int64_t ch = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
     if (ch >= F) return;
     const int64_t slice = blockIdx.y, per = (N + slices - 1) / slices;
@@ -272,6 +275,8 @@ __global__ void __launch_bounds__(256) bias_grad_partial_kernel(
     const CodeT* __restrict__ dy, int64_t N, int64_t F, int64_t P, PositFmt f, int slices,
     const int64_t* __restrict__ xlut, unsigned __int128* __restrict__ partial,
     uint8_t* __restrict__ nar_out) {
+    pdl_trigger();
+    pdl_wait();  // PDL: nothing above touches global memory (pdl.cuh)
     const int64_t ch = blockIdx.x, slice = blockIdx.y;
     const int64_t per = (N + slices - 1) / slices;
     const int64_t n0 = slice * per, n1 = min(N, n0 + per);
@@ -346,6 +351,8 @@ __global__ void __launch_bounds__(512) bias_grad_chan_kernel(
     uint8_t* __restrict__ nar_flag, unsigned int* __restrict__ arrivals, CodeT* __restrict__ out,
     unsigned __int128* raw_words, uint8_t* raw_nar, const void* __restrict__ gate = nullptr,
     int gnbits = 0) {
+    pdl_trigger();
+    pdl_wait();  // PDL: nothing above touches global memory (pdl.cuh)
     __shared__ int64_t s_lut[LUTB];
     __shared__ unsigned __int128 warp_s[16];
     __shared__ bool s_last;
@@ -448,6 +455,8 @@ __global__ void __launch_bounds__(512) bias_grad_chan_kernel(
 
 // X (the exact integer image) of every code of a format, for table decode.
 __global__ void x_lut_kernel(PositFmt f, int64_t* __restrict__ lut) {
+    pdl_trigger();
+    pdl_wait();  // PDL: nothing above touches global memory (pdl.cuh)
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c < (1 << f.nbits)) {
         int64_t X;
@@ -473,6 +482,8 @@ __global__ void bias_grad_final_kernel(const unsigned __int128* __restrict__ par
                                        const uint8_t* __restrict__ nar_in, int64_t F, PositFmt f,
                                        CodeT* __restrict__ out, unsigned __int128* raw_words,
                                        uint8_t* raw_nar) {
+    pdl_trigger();
+    pdl_wait();  // PDL: nothing above touches global memory (pdl.cuh)
     // a warp per channel: lanes sum interleaved partials (coalesced 16-byte
     // loads), then a shuffle tree; exact 128-bit integer sums in any order
     const unsigned __int128 one = 1;
@@ -699,14 +710,14 @@ int pnn_conv2d_dgrad(int nbits, int es, const void* dy, int64_t N, int64_t F, in
         rc = run_quire_gemm<T>(a, FetchDgradDy<T>{(const T*)dy, g}, FetchDgradW<T>{(const T*)w, g},
                                out_nchw<T>(dx, H * W, C), workspace, workspace_bytes, st, nullptr);
         if (rc == 0)
-            dgrad_weight_nar_kernel<T><<<grid_fixup(total), 256, 0, st>>>((T*)dx, (const T*)w, g,
+            launch_pdl(dgrad_weight_nar_kernel<T>, dim3(grid_fixup(total)), dim3(256), 0, st, (T*)dx, (const T*)w, g,
                                                                              flag_w, nar);
     } else {
         using T = uint16_t;
         rc = run_quire_gemm<T>(a, FetchDgradDy<T>{(const T*)dy, g}, FetchDgradW<T>{(const T*)w, g},
                                out_nchw<T>(dx, H * W, C), workspace, workspace_bytes, st, nullptr);
         if (rc == 0)
-            dgrad_weight_nar_kernel<T><<<grid_fixup(total), 256, 0, st>>>((T*)dx, (const T*)w, g,
+            launch_pdl(dgrad_weight_nar_kernel<T>, dim3(grid_fixup(total)), dim3(256), 0, st, (T*)dx, (const T*)w, g,
                                                                              flag_w, nar);
     }
     if (rc == 0 && cudaGetLastError() != cudaSuccess) rc = 4;
@@ -897,7 +908,7 @@ int pnn_bias_grad_gated(int nbits, int es, const void* dy, int gate_nbits, const
     const FastDiv fd{uint32_t(P / VE)};
     const dim3 g2{unsigned(sl), unsigned(F), 1u};
 #define PNN_BGG(T, B, G)                                                                              \
-    bias_grad_chan_kernel<T, B, G><<<g2, 512, 0, st>>>((const T*)dy, N, F, P, f, sl, fd, lut, partial,  \
+    launch_pdl(bias_grad_chan_kernel<T, B, G>, dim3(g2), dim3(512), 0, st, (const T*)dy, N, F, P, f, sl, fd, lut, partial,  \
                                                        nar, arrivals, (T*)db,                          \
                                                        (unsigned __int128*)raw_words, (uint8_t*)raw_nar, \
                                                        gate, gate_nbits)
@@ -936,15 +947,15 @@ int pnn_bias_grad(int nbits, int es, const void* dy, int64_t N, int64_t F, int64
     }
     const dim3 cgrid{unsigned((F + 255) / 256), unsigned(slices), 1u};
     if (P == 1 && nbits <= 8) {
-        bias_grad_cols_kernel<uint8_t><<<cgrid, 256, 0, st>>>((const uint8_t*)dy, N, F, f, slices,
+        launch_pdl(bias_grad_cols_kernel<uint8_t>, dim3(cgrid), dim3(256), 0, st, (const uint8_t*)dy, N, F, f, slices,
                                                               xlut, partial, nar);
-        bias_grad_final_kernel<uint8_t><<<grid_for(F * 32, 256), 256, 0, st>>>(
+        launch_pdl(bias_grad_final_kernel<uint8_t>, dim3(grid_for(F * 32, 256)), dim3(256), 0, st, 
             partial, slices, nar, F, f, (uint8_t*)db, (unsigned __int128*)raw_words,
             (uint8_t*)raw_nar);
     } else if (P == 1) {
-        bias_grad_cols_kernel<uint16_t><<<cgrid, 256, 0, st>>>((const uint16_t*)dy, N, F, f,
+        launch_pdl(bias_grad_cols_kernel<uint16_t>, dim3(cgrid), dim3(256), 0, st, (const uint16_t*)dy, N, F, f,
                                                                slices, xlut, partial, nar);
-        bias_grad_final_kernel<uint16_t><<<grid_for(F * 32, 256), 256, 0, st>>>(
+        launch_pdl(bias_grad_final_kernel<uint16_t>, dim3(grid_for(F * 32, 256)), dim3(256), 0, st, 
             partial, slices, nar, F, f, (uint16_t*)db, (unsigned __int128*)raw_words,
             (uint8_t*)raw_nar);
     } else if (chan) {
@@ -965,23 +976,24 @@ int pnn_bias_grad(int nbits, int es, const void* dy, int64_t N, int64_t F, int64
         const FastDiv fd{uint32_t(P / VE)};
         const dim3 g2{unsigned(sl), unsigned(F), 1u};
 #define PNN_BGC(T, B)                                                                             \
-    bias_grad_chan_kernel<T, B><<<g2, 512, 0, st>>>((const T*)dy, N, F, P, f, sl, fd, lut, partial, \
+    launch_pdl(bias_grad_chan_kernel<T, B>, dim3(g2), dim3(512), 0, st, (const T*)dy, N, F, P, f, sl, fd, lut, partial, \
                                                     nar, arrivals, (T*)db,                        \
-                                                    (unsigned __int128*)raw_words, (uint8_t*)raw_nar)
+                                                    (unsigned __int128*)raw_words, (uint8_t*)raw_nar, \
+                                                    static_cast<const void*>(nullptr), 0)
         if (nbits <= 8) PNN_BGC(uint8_t, 256);
         else if (nbits <= 10) PNN_BGC(uint16_t, 1024);
         else PNN_BGC(uint16_t, 4096);
 #undef PNN_BGC
     } else if (nbits <= 8) {
-        bias_grad_partial_kernel<uint8_t><<<grid, 256, 0, st>>>((const uint8_t*)dy, N, F, P, f,
+        launch_pdl(bias_grad_partial_kernel<uint8_t>, dim3(grid), dim3(256), 0, st, (const uint8_t*)dy, N, F, P, f,
                                                                  slices, xlut, partial, nar);
-        bias_grad_final_kernel<uint8_t><<<grid_for(F * 32, 256), 256, 0, st>>>(
+        launch_pdl(bias_grad_final_kernel<uint8_t>, dim3(grid_for(F * 32, 256)), dim3(256), 0, st, 
             partial, slices, nar, F, f, (uint8_t*)db, (unsigned __int128*)raw_words,
             (uint8_t*)raw_nar);
     } else {
-        bias_grad_partial_kernel<uint16_t><<<grid, 256, 0, st>>>((const uint16_t*)dy, N, F, P, f,
+        launch_pdl(bias_grad_partial_kernel<uint16_t>, dim3(grid), dim3(256), 0, st, (const uint16_t*)dy, N, F, P, f,
                                                                   slices, xlut, partial, nar);
-        bias_grad_final_kernel<uint16_t><<<grid_for(F * 32, 256), 256, 0, st>>>(
+        launch_pdl(bias_grad_final_kernel<uint16_t>, dim3(grid_for(F * 32, 256)), dim3(256), 0, st, 
             partial, slices, nar, F, f, (uint16_t*)db, (unsigned __int128*)raw_words,
             (uint8_t*)raw_nar);
     }

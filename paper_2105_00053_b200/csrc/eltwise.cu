@@ -18,6 +18,7 @@
 #include "eltwise_common.cuh"
 #include "epilogue.cuh"
 #include "posit_scalar.cuh"
+#include "pdl.cuh"
 #include "status.h"
 #include "tables.h"
 
@@ -25,11 +26,15 @@ namespace pnn_b200 {
 
 __global__ void convert_kernel(PositFmt s, int sb, const void* src, PositFmt d, int db, void* dst,
                                int64_t n) {
+    pdl_trigger();
+    pdl_wait();  // PDL: nothing above touches global memory (pdl.cuh)
     GRID_STRIDE(i, n) { store_any(dst, i, db, p_convert(s, d, load_any(src, i, sb))); }
 }
 
 // ReLU: x > 0 ? x : 0 by signed-pattern compare (NaR sorts lowest -> 0).
 __global__ void relu_fwd_kernel(PositFmt f, int b, const void* x, void* y, int64_t n) {
+    pdl_trigger();
+    pdl_wait();  // PDL: nothing above touches global memory (pdl.cuh)
     GRID_STRIDE(i, n) {
         const uint32_t c = load_any(x, i, b);
         store_any(y, i, b, p_compare(f, c, 0) > 0 ? c : 0u);
@@ -39,6 +44,8 @@ __global__ void relu_fwd_kernel(PositFmt f, int b, const void* x, void* y, int64
 // dx = x > 0 ? dy : 0 (x in the forward format, dy/dx in the backward format).
 __global__ void relu_bwd_kernel(PositFmt fx, int bx, const void* x, int bg, const void* dy,
                                 void* dx, int64_t n) {
+    pdl_trigger();
+    pdl_wait();  // PDL: nothing above touches global memory (pdl.cuh)
     GRID_STRIDE(i, n) {
         const uint32_t c = load_any(x, i, bx);
         store_any(dx, i, bg, p_compare(fx, c, 0) > 0 ? load_any(dy, i, bg) : 0u);
@@ -48,6 +55,8 @@ __global__ void relu_bwd_kernel(PositFmt fx, int bx, const void* x, int bg, cons
 __global__ void maxpool_fwd_kernel(PositFmt f, int b, const void* x, int64_t NC, int64_t H,
                                    int64_t W, int k, int s, int64_t OH, int64_t OW, void* y,
                                    int64_t* argmax) {
+    pdl_trigger();
+    pdl_wait();  // PDL: nothing above touches global memory (pdl.cuh)
     GRID_STRIDE(o, NC * OH * OW) {
         const int64_t ox = o % OW, oy = (o / OW) % OH, nc = o / (OW * OH);
         const int64_t base = nc * H * W;
@@ -72,6 +81,8 @@ __global__ void maxpool_fwd_kernel(PositFmt f, int b, const void* x, int64_t NC,
 __global__ void maxpool_bwd_kernel(PositFmt f, int b, const void* dy, const int64_t* argmax,
                                    int64_t NC, int64_t H, int64_t W, int k, int s, int64_t OH,
                                    int64_t OW, void* dx) {
+    pdl_trigger();
+    pdl_wait();  // PDL: nothing above touches global memory (pdl.cuh)
     GRID_STRIDE(t, NC * H * W) {
         const int64_t ix = t % W, iy = (t / W) % H, nc = t / (W * H);
         const int64_t oy0 = iy - k + 1 > 0 ? (iy - k + 1 + s - 1) / s : 0;
@@ -96,6 +107,8 @@ __global__ void maxpool_bwd_kernel(PositFmt f, int b, const void* dy, const int6
 // 32-bit index math (the callers check the sizes).
 __global__ void maxpool_bwd_tiled_kernel(int b, const void* dy, const int64_t* argmax, int NC,
                                          int OH, int OW, int k, void* dx) {
+    pdl_trigger();
+    pdl_wait();  // PDL: nothing above touches global memory (pdl.cuh)
     const int W = OW * k, H = OH * k;
     const int total = NC * OH * OW;
     for (int o = blockIdx.x * blockDim.x + threadIdx.x; o < total; o += gridDim.x * blockDim.x) {
@@ -113,6 +126,8 @@ __global__ void maxpool_bwd_tiled_kernel(int b, const void* dy, const int64_t* a
 
 __global__ void maxpool_fwd_tiled_kernel(PositFmt f, int b, const void* x, int NC, int OH, int OW,
                                          int k, void* y, int64_t* argmax) {
+    pdl_trigger();
+    pdl_wait();  // PDL: nothing above touches global memory (pdl.cuh)
     const int W = OW * k, H = OH * k;
     const int total = NC * OH * OW;
     for (int o = blockIdx.x * blockDim.x + threadIdx.x; o < total; o += gridDim.x * blockDim.x) {
@@ -177,6 +192,8 @@ __device__ __forceinline__ int argmax4(int32_t a, int32_t b, int32_t c, int32_t 
 template <typename TX>
 __global__ void __launch_bounds__(256) maxpool2_fwd_vec_kernel(int nbits, const TX* __restrict__ x,
                                                                TX* __restrict__ y, int rows, int OW) {
+    pdl_trigger();
+    pdl_wait();  // PDL: nothing above touches global memory (pdl.cuh)
     constexpr int VE = 16 / sizeof(TX), WPT = VE / 2;
     const int W = 2 * OW, vpr = OW / WPT;  // vectors per output row
     const int total = rows * vpr;          // rows = N * C * OH
@@ -215,6 +232,8 @@ __global__ void __launch_bounds__(256) maxpool2_bwd_x_kernel(int x_nbits, const 
                                                              const TG* __restrict__ dy,
                                                              TG* __restrict__ dx, int rows, int OW,
                                                              int relu_gate = 0) {
+    pdl_trigger();
+    pdl_wait();  // PDL: nothing above touches global memory (pdl.cuh)
     constexpr int VE = 16 / sizeof(TX), WPT = VE / 2;
     const int W = 2 * OW, vpr = OW / WPT;
     const int total = rows * vpr;
@@ -309,6 +328,8 @@ template <typename S, typename Dt>
 __global__ void __launch_bounds__(256) convert_vec_kernel(PositFmt s, const S* __restrict__ src,
                                                           PositFmt d, Dt* __restrict__ dst,
                                                           int64_t n) {
+    pdl_trigger();
+    pdl_wait();  // PDL: nothing above touches global memory (pdl.cuh)
     __shared__ uint16_t lut[1 << 12];
     const bool use_lut = s.nbits <= 12;
     if (use_lut) {
@@ -331,6 +352,8 @@ __global__ void __launch_bounds__(256) convert_vec_kernel(PositFmt s, const S* _
 
 template <typename T>
 __global__ void relu_fwd_vec_kernel(int nbits, const T* __restrict__ x, T* __restrict__ y, int64_t n) {
+    pdl_trigger();
+    pdl_wait();  // PDL: nothing above touches global memory (pdl.cuh)
     const int64_t n8 = n / 8;
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n8;
          i += int64_t(gridDim.x) * blockDim.x) {
@@ -348,6 +371,8 @@ __global__ void relu_fwd_vec_kernel(int nbits, const T* __restrict__ x, T* __res
 template <typename TX, typename TG>
 __global__ void relu_bwd_vec_kernel(int x_nbits, const TX* __restrict__ x,
                                     const TG* __restrict__ dy, TG* __restrict__ dx, int64_t n) {
+    pdl_trigger();
+    pdl_wait();  // PDL: nothing above touches global memory (pdl.cuh)
     const int64_t n8 = n / 8;
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n8;
          i += int64_t(gridDim.x) * blockDim.x) {
@@ -375,6 +400,8 @@ __global__ void softmax_xent_kernel(PositFmt f, int b, const void* logits, const
                                     void* dlogits, void* loss_rows, void* s_rows = nullptr,
                                     const uint16_t* __restrict__ exp_lut = nullptr,
                                     const uint16_t* __restrict__ log_lut = nullptr) {
+    pdl_trigger();
+    pdl_wait();  // PDL: nothing above touches global memory (pdl.cuh)
     auto pexp = [&](uint32_t x) { return exp_lut ? uint32_t(__ldg(exp_lut + x)) : p_exp(f, x); };
     const int lane = threadIdx.x & 31;
     const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
@@ -442,6 +469,8 @@ __global__ void softmax_xent_kernel(PositFmt f, int b, const void* logits, const
 __global__ void xent_loss_rows_kernel(PositFmt f, int b, const void* logits, const int32_t* labels,
                                       const void* s_rows, int64_t B, int64_t Cn, void* loss_rows,
                                       const uint16_t* __restrict__ log_lut = nullptr) {
+    pdl_trigger();
+    pdl_wait();  // PDL: nothing above touches global memory (pdl.cuh)
     GRID_STRIDE(i, B) {
         const int64_t row = i * Cn;
         uint32_t m = load_any(logits, row, b);
@@ -460,6 +489,8 @@ __global__ void xent_loss_rows_kernel(PositFmt f, int b, const void* logits, con
 __global__ void loss_reduce_kernel(PositFmt f, int b, const void* loss_rows, int64_t B,
                                    int log2_batch, void* loss_out, unsigned __int128* raw_word,
                                    uint8_t* raw_nar) {
+    pdl_trigger();
+    pdl_wait();  // PDL: nothing above touches global memory (pdl.cuh)
     __shared__ unsigned long long lo_s[256], hi_s[256];
     __shared__ int nar_s;
     if (threadIdx.x == 0) nar_s = 0;
@@ -501,6 +532,8 @@ __global__ void loss_reduce_kernel(PositFmt f, int b, const void* loss_rows, int
 __global__ void sgd_kernel(PositFmt fo, int bo, void* master, PositFmt fg, int bg, const void* grad,
                            int64_t n, uint32_t lr, PositFmt f1, int b1, void* copy1, PositFmt f2,
                            int b2, void* copy2, int grad_scale_log2) {
+    pdl_trigger();
+    pdl_wait();  // PDL: nothing above touches global memory (pdl.cuh)
     GRID_STRIDE(i, n) {
         uint32_t g = p_convert(fg, fo, load_any(grad, i, bg));
         if (grad_scale_log2 != 0) g = p_ldexp(fo, g, -grad_scale_log2);  // loss-scale undo
@@ -570,6 +603,8 @@ __device__ __forceinline__ uint32_t copy_fast(const PositFmt& fo, const PositFmt
 __global__ void sgd_multi_kernel(PositFmt fo, int bo, PositFmt fg, int bg, uint32_t lr, PositFmt f1,
                                  int b1, PositFmt f2, int b2, int grad_scale_log2,
                                  const __grid_constant__ SgdSegs segs, int fast) {
+    pdl_trigger();
+    pdl_wait();  // PDL: nothing above touches global memory (pdl.cuh)
     __shared__ uint4 s_lut[kPackLutEntries], s_lut1[kPackLutEntries], s_lut2[kPackLutEntries];
     int64_t X_lr = 0;
     if (fast) {
@@ -635,6 +670,8 @@ __global__ void sgd_multi_kernel(PositFmt fo, int bo, PositFmt fg, int bg, uint3
 // Each table entry is computed by the scalar ops themselves, so the path is
 // the sgd_kernel arithmetic, entry for entry.
 __global__ void sgd_xm_lut_kernel(PositFmt fo, PositFmt fg, uint32_t lr, int64_t* __restrict__ lut) {
+    pdl_trigger();
+    pdl_wait();  // PDL: nothing above touches global memory (pdl.cuh)
     GRID_STRIDE(c, int64_t(1) << fg.nbits) {
         int64_t X;
         const bool nar = decode_x(p_mul(fo, lr, p_convert(fg, fo, uint32_t(c))), fo, X);
@@ -642,11 +679,15 @@ __global__ void sgd_xm_lut_kernel(PositFmt fo, PositFmt fg, uint32_t lr, int64_t
     }
 }
 __global__ void copy_lut_kernel(PositFmt fo, PositFmt fc, uint16_t* __restrict__ lut) {
+    pdl_trigger();
+    pdl_wait();  // PDL: nothing above touches global memory (pdl.cuh)
     GRID_STRIDE(c, int64_t(1) << fo.nbits) { lut[c] = uint16_t(p_convert(fo, fc, uint32_t(c))); }
 }
 // exp / log of every code (posit_math.cpp:67-107 through p_exp / p_log): the
 // softmax cross-entropy's transcendental steps by table
 __global__ void fn_lut_kernel(PositFmt f, int which, uint16_t* __restrict__ lut) {
+    pdl_trigger();
+    pdl_wait();  // PDL: nothing above touches global memory (pdl.cuh)
     GRID_STRIDE(c, int64_t(1) << f.nbits) {
         lut[c] = uint16_t(which == 0 ? p_exp(f, uint32_t(c)) : p_log(f, uint32_t(c)));
     }
@@ -684,6 +725,8 @@ constexpr int kSgdU = 4;
 template <typename TO, typename TG, typename T1, typename T2, int FMT>
 __global__ void __launch_bounds__(256) sgd_lut_kernel(PositFmt fo_rt, const __grid_constant__ SgdSegs segs,
                                                       SgdLuts t) {
+    pdl_trigger();
+    pdl_wait();  // PDL: nothing above touches global memory (pdl.cuh)
     const PositFmt fo = fixed_fmt<FMT>(fo_rt);
     __shared__ uint4 s_lut[kPackLutEntries];
     build_pack_lut(fo, s_lut, threadIdx.x, blockDim.x);
@@ -744,9 +787,9 @@ __global__ void __launch_bounds__(256) sgd_lut_kernel(PositFmt fo_rt, const __gr
 
 template <typename TO, typename TG, typename T1, typename T2>
 void launch_sgd_lut(int grid, cudaStream_t st, const PositFmt& fo, const SgdSegs& sg, const SgdLuts& t) {
-    if (fixed_fmt_id(fo) == 4) sgd_lut_kernel<TO, TG, T1, T2, 4><<<grid, 256, 0, st>>>(fo, sg, t);
-    else if (fixed_fmt_id(fo) == 3) sgd_lut_kernel<TO, TG, T1, T2, 3><<<grid, 256, 0, st>>>(fo, sg, t);
-    else sgd_lut_kernel<TO, TG, T1, T2, 0><<<grid, 256, 0, st>>>(fo, sg, t);
+    if (fixed_fmt_id(fo) == 4) launch_pdl(sgd_lut_kernel<TO, TG, T1, T2, 4>, dim3(grid), dim3(256), 0, st, fo, sg, t);
+    else if (fixed_fmt_id(fo) == 3) launch_pdl(sgd_lut_kernel<TO, TG, T1, T2, 3>, dim3(grid), dim3(256), 0, st, fo, sg, t);
+    else launch_pdl(sgd_lut_kernel<TO, TG, T1, T2, 0>, dim3(grid), dim3(256), 0, st, fo, sg, t);
 }
 
 template <typename TO, typename TG>
@@ -764,6 +807,8 @@ void launch_sgd_lut_c(int b1, int b2, int grid, cudaStream_t st, const PositFmt&
 __global__ void avgpool_fwd_kernel(PositFmt f, int b, const void* x, int64_t NC, int64_t H,
                                    int64_t W, int k, int s, int64_t OH, int64_t OW, int use_quire,
                                    uint32_t recip, void* y) {
+    pdl_trigger();
+    pdl_wait();  // PDL: nothing above touches global memory (pdl.cuh)
     GRID_STRIDE(o, NC * OH * OW) {
         const int64_t ox = o % OW, oy = (o / OW) % OH, nc = o / (OW * OH);
         const int64_t base = nc * H * W + (oy * s) * W + ox * s;
@@ -798,6 +843,8 @@ __global__ void avgpool_fwd_kernel(PositFmt f, int b, const void* x, int64_t NC,
 __global__ void avgpool_bwd_kernel(PositFmt f, int b, const void* dy, int64_t NC, int64_t H,
                                    int64_t W, int k, int s, int64_t OH, int64_t OW, uint32_t recip,
                                    void* dx) {
+    pdl_trigger();
+    pdl_wait();  // PDL: nothing above touches global memory (pdl.cuh)
     GRID_STRIDE(t, NC * H * W) {
         const int64_t ix = t % W, iy = (t / W) % H, nc = t / (W * H);
         const int64_t oy0 = iy - k + 1 > 0 ? (iy - k + 1 + s - 1) / s : 0;
@@ -812,11 +859,15 @@ __global__ void avgpool_bwd_kernel(PositFmt f, int b, const void* dy, int64_t NC
 }
 
 __global__ void from_float64_kernel(PositFmt f, int b, const double* x, void* out, int64_t n) {
+    pdl_trigger();
+    pdl_wait();  // PDL: nothing above touches global memory (pdl.cuh)
     GRID_STRIDE(i, n) { store_any(out, i, b, p_from_float64(f, x[i])); }
 }
 
 __global__ void scalar_eval_kernel(PositFmt f, int op, const uint32_t* a, const uint32_t* b,
                                    uint32_t* out, int64_t n) {
+    pdl_trigger();
+    pdl_wait();  // PDL: nothing above touches global memory (pdl.cuh)
     GRID_STRIDE(i, n) {
         const uint32_t x = a[i], y = b ? b[i] : 0u;
         uint32_t r;
@@ -871,9 +922,9 @@ uint16_t* code_table(int kind, const PositFmt& a, const PositFmt& b, uint32_t l,
     return static_cast<uint16_t*>(persistent_table(
         table_key(16 + kind, a.nbits, a.es, b.nbits, b.es, 0, l), size_t(n) * (kind == 0 ? 8 : 2), st,
         [&](void* p, cudaStream_t s) {
-            if (kind == 0) sgd_xm_lut_kernel<<<grid1(n), 256, 0, s>>>(a, b, l, static_cast<int64_t*>(p));
-            else if (kind == 1) copy_lut_kernel<<<grid1(n), 256, 0, s>>>(a, b, static_cast<uint16_t*>(p));
-            else fn_lut_kernel<<<grid1(n), 256, 0, s>>>(a, kind - 2, static_cast<uint16_t*>(p));
+            if (kind == 0) launch_pdl(sgd_xm_lut_kernel, dim3(grid1(n)), dim3(256), 0, s, a, b, l, static_cast<int64_t*>(p));
+            else if (kind == 1) launch_pdl(copy_lut_kernel, dim3(grid1(n)), dim3(256), 0, s, a, b, static_cast<uint16_t*>(p));
+            else launch_pdl(fn_lut_kernel, dim3(grid1(n)), dim3(256), 0, s, a, kind - 2, static_cast<uint16_t*>(p));
         }));
 }
 
@@ -913,15 +964,15 @@ int pnn_convert(int src_nbits, int src_es, int dst_nbits, int dst_es, const void
         const int grid = grid1(n / 8 + 1) < 148 * 4 ? grid1(n / 8 + 1) : 148 * 4;
         const int sb = bytes_of(src_nbits), db = bytes_of(dst_nbits);
         if (sb == 1 && db == 1)
-            convert_vec_kernel<uint8_t, uint8_t><<<grid, 256, 0, st>>>(s, (const uint8_t*)src, d, (uint8_t*)dst, n);
+            launch_pdl(convert_vec_kernel<uint8_t, uint8_t>, dim3(grid), dim3(256), 0, st, s, (const uint8_t*)src, d, (uint8_t*)dst, n);
         else if (sb == 1)
-            convert_vec_kernel<uint8_t, uint16_t><<<grid, 256, 0, st>>>(s, (const uint8_t*)src, d, (uint16_t*)dst, n);
+            launch_pdl(convert_vec_kernel<uint8_t, uint16_t>, dim3(grid), dim3(256), 0, st, s, (const uint8_t*)src, d, (uint16_t*)dst, n);
         else if (db == 1)
-            convert_vec_kernel<uint16_t, uint8_t><<<grid, 256, 0, st>>>(s, (const uint16_t*)src, d, (uint8_t*)dst, n);
+            launch_pdl(convert_vec_kernel<uint16_t, uint8_t>, dim3(grid), dim3(256), 0, st, s, (const uint16_t*)src, d, (uint8_t*)dst, n);
         else
-            convert_vec_kernel<uint16_t, uint16_t><<<grid, 256, 0, st>>>(s, (const uint16_t*)src, d, (uint16_t*)dst, n);
+            launch_pdl(convert_vec_kernel<uint16_t, uint16_t>, dim3(grid), dim3(256), 0, st, s, (const uint16_t*)src, d, (uint16_t*)dst, n);
     } else {
-        convert_kernel<<<grid1(n), 256, 0, st>>>(s, bytes_of(src_nbits), src, d, bytes_of(dst_nbits),
+        launch_pdl(convert_kernel, dim3(grid1(n)), dim3(256), 0, st, s, bytes_of(src_nbits), src, d, bytes_of(dst_nbits),
                                                  dst, n);
     }
     return launched("convert");
@@ -934,11 +985,11 @@ int pnn_relu_fwd(int nbits, int es, const void* x, void* y, int64_t n, void* str
     auto st = (cudaStream_t)stream;
     if (aligned16(x) && aligned16(y)) {
         if (bytes_of(nbits) == 1)
-            relu_fwd_vec_kernel<uint8_t><<<grid1(n / 8 + 1), 256, 0, st>>>(nbits, (const uint8_t*)x, (uint8_t*)y, n);
+            launch_pdl(relu_fwd_vec_kernel<uint8_t>, dim3(grid1(n / 8 + 1)), dim3(256), 0, st, nbits, (const uint8_t*)x, (uint8_t*)y, n);
         else
-            relu_fwd_vec_kernel<uint16_t><<<grid1(n / 8 + 1), 256, 0, st>>>(nbits, (const uint16_t*)x, (uint16_t*)y, n);
+            launch_pdl(relu_fwd_vec_kernel<uint16_t>, dim3(grid1(n / 8 + 1)), dim3(256), 0, st, nbits, (const uint16_t*)x, (uint16_t*)y, n);
     } else {
-        relu_fwd_kernel<<<grid1(n), 256, 0, st>>>(make_fmt(nbits, es), bytes_of(nbits), x, y, n);
+        launch_pdl(relu_fwd_kernel, dim3(grid1(n)), dim3(256), 0, st, make_fmt(nbits, es), bytes_of(nbits), x, y, n);
     }
     return launched("relu_fwd");
 }
@@ -954,15 +1005,15 @@ int pnn_relu_bwd(int x_nbits, int x_es, const void* x, int g_nbits, int g_es, co
         const int grid = grid1(n / 8 + 1);
         const int xb = bytes_of(x_nbits), gb = bytes_of(g_nbits);
         if (xb == 1 && gb == 1)
-            relu_bwd_vec_kernel<uint8_t, uint8_t><<<grid, 256, 0, st>>>(x_nbits, (const uint8_t*)x, (const uint8_t*)dy, (uint8_t*)dx, n);
+            launch_pdl(relu_bwd_vec_kernel<uint8_t, uint8_t>, dim3(grid), dim3(256), 0, st, x_nbits, (const uint8_t*)x, (const uint8_t*)dy, (uint8_t*)dx, n);
         else if (xb == 1)
-            relu_bwd_vec_kernel<uint8_t, uint16_t><<<grid, 256, 0, st>>>(x_nbits, (const uint8_t*)x, (const uint16_t*)dy, (uint16_t*)dx, n);
+            launch_pdl(relu_bwd_vec_kernel<uint8_t, uint16_t>, dim3(grid), dim3(256), 0, st, x_nbits, (const uint8_t*)x, (const uint16_t*)dy, (uint16_t*)dx, n);
         else if (gb == 1)
-            relu_bwd_vec_kernel<uint16_t, uint8_t><<<grid, 256, 0, st>>>(x_nbits, (const uint16_t*)x, (const uint8_t*)dy, (uint8_t*)dx, n);
+            launch_pdl(relu_bwd_vec_kernel<uint16_t, uint8_t>, dim3(grid), dim3(256), 0, st, x_nbits, (const uint16_t*)x, (const uint8_t*)dy, (uint8_t*)dx, n);
         else
-            relu_bwd_vec_kernel<uint16_t, uint16_t><<<grid, 256, 0, st>>>(x_nbits, (const uint16_t*)x, (const uint16_t*)dy, (uint16_t*)dx, n);
+            launch_pdl(relu_bwd_vec_kernel<uint16_t, uint16_t>, dim3(grid), dim3(256), 0, st, x_nbits, (const uint16_t*)x, (const uint16_t*)dy, (uint16_t*)dx, n);
     } else {
-        relu_bwd_kernel<<<grid1(n), 256, 0, st>>>(make_fmt(x_nbits, x_es), bytes_of(x_nbits), x,
+        launch_pdl(relu_bwd_kernel, dim3(grid1(n)), dim3(256), 0, st, make_fmt(x_nbits, x_es), bytes_of(x_nbits), x,
                                                   bytes_of(g_nbits), dy, dx, n);
     }
     return launched("relu_bwd");
@@ -988,19 +1039,19 @@ int pnn_maxpool2d_fwd(int nbits, int es, const void* x, int64_t N, int64_t C, in
         const int rows = int(N * C * OH), wpt = nbits <= 8 ? 8 : 4;
         const int grid = grid1(int64_t(rows) * (OW / wpt));
         if (nbits <= 8)
-            maxpool2_fwd_vec_kernel<uint8_t><<<grid, 256, 0, (cudaStream_t)stream>>>(
+            launch_pdl(maxpool2_fwd_vec_kernel<uint8_t>, dim3(grid), dim3(256), 0, (cudaStream_t)stream, 
                 nbits, (const uint8_t*)x, (uint8_t*)y, rows, int(OW));
         else
-            maxpool2_fwd_vec_kernel<uint16_t><<<grid, 256, 0, (cudaStream_t)stream>>>(
+            launch_pdl(maxpool2_fwd_vec_kernel<uint16_t>, dim3(grid), dim3(256), 0, (cudaStream_t)stream, 
                 nbits, (const uint16_t*)x, (uint16_t*)y, rows, int(OW));
         return launched("maxpool2d_fwd");
     }
     if (argmax == nullptr) return set_status(PNN_EINVAL, "maxpool2d: argmax output required");
     if (k == stride && H == OH * k && W == OW * k && N * C * H * W < (int64_t(1) << 31))
-        maxpool_fwd_tiled_kernel<<<grid1(N * C * OH * OW), 256, 0, (cudaStream_t)stream>>>(
+        launch_pdl(maxpool_fwd_tiled_kernel, dim3(grid1(N * C * OH * OW)), dim3(256), 0, (cudaStream_t)stream, 
             make_fmt(nbits, es), bytes_of(nbits), x, int(N * C), int(OH), int(OW), k, y, argmax);
     else
-        maxpool_fwd_kernel<<<grid1(N * C * OH * OW), 256, 0, (cudaStream_t)stream>>>(
+        launch_pdl(maxpool_fwd_kernel, dim3(grid1(N * C * OH * OW)), dim3(256), 0, (cudaStream_t)stream, 
             make_fmt(nbits, es), bytes_of(nbits), x, N * C, H, W, k, stride, OH, OW, y, argmax);
     return launched("maxpool2d_fwd");
 }
@@ -1027,7 +1078,7 @@ int pnn_maxpool2d_relu_bwd_x(int x_nbits, int x_es, const void* x, int g_nbits, 
     auto st = (cudaStream_t)stream;
     const bool x8 = x_nbits <= 8, g8 = g_nbits <= 8;
 #define PNN_MPB(TX, TG)                                                                    \
-    maxpool2_bwd_x_kernel<TX, TG><<<grid, 256, 0, st>>>(x_nbits, (const TX*)x, (const TG*)dy, \
+    launch_pdl(maxpool2_bwd_x_kernel<TX, TG>, dim3(grid), dim3(256), 0, st, x_nbits, (const TX*)x, (const TG*)dy, \
                                                         (TG*)dx, rows, OW, relu_gate)
     if (x8 && g8) PNN_MPB(uint8_t, uint8_t);
     else if (x8) PNN_MPB(uint8_t, uint16_t);
@@ -1045,10 +1096,10 @@ int pnn_maxpool2d_bwd(int nbits, int es, const void* dy, const int64_t* argmax, 
     const int64_t OH = (H - k) / stride + 1, OW = (W - k) / stride + 1;
     if (N == 0) return PNN_OK;
     if (k == stride && H == OH * k && W == OW * k && N * C * H * W < (int64_t(1) << 31))
-        maxpool_bwd_tiled_kernel<<<grid1(N * C * OH * OW), 256, 0, (cudaStream_t)stream>>>(
+        launch_pdl(maxpool_bwd_tiled_kernel, dim3(grid1(N * C * OH * OW)), dim3(256), 0, (cudaStream_t)stream, 
             bytes_of(nbits), dy, argmax, int(N * C), int(OH), int(OW), k, dx);
     else
-        maxpool_bwd_kernel<<<grid1(N * C * H * W), 256, 0, (cudaStream_t)stream>>>(
+        launch_pdl(maxpool_bwd_kernel, dim3(grid1(N * C * H * W)), dim3(256), 0, (cudaStream_t)stream, 
             make_fmt(nbits, es), bytes_of(nbits), dy, argmax, N * C, H, W, k, stride, OH, OW, dx);
     return launched("maxpool2d_bwd");
 }
@@ -1071,12 +1122,12 @@ int pnn_softmax_xent_scaled(int nbits, int es, const void* logits, const int32_t
     if (raw_word && f.W > 128)
         return set_status(PNN_EUNSUPPORTED, "softmax_xent: raw loss words need a quire of <= 128 bits");
     auto st = (cudaStream_t)stream;
-    softmax_xent_kernel<<<grid1(B * 32), 256, 0, st>>>(f, bytes_of(nbits), logits, labels, B, classes,
+    launch_pdl(softmax_xent_kernel, dim3(grid1(B * 32)), dim3(256), 0, st, f, bytes_of(nbits), logits, labels, B, classes,
                                                       log2_batch, grad_scale_log2, dlogits,
                                                       loss_rows, nullptr, code_table(2, f, f, 0, st),
                                                       code_table(3, f, f, 0, st));
     if (loss_out || raw_word)
-        loss_reduce_kernel<<<1, 256, 0, st>>>(f, bytes_of(nbits), loss_rows, B, log2_batch,
+        launch_pdl(loss_reduce_kernel, dim3(1), dim3(256), 0, st, f, bytes_of(nbits), loss_rows, B, log2_batch,
                                               loss_out, (unsigned __int128*)raw_word,
                                               (uint8_t*)raw_nar);
     return launched("softmax_xent");
@@ -1089,9 +1140,10 @@ int pnn_softmax_xent_grad(int nbits, int es, const void* logits, const int32_t* 
     if (B < 1 || classes < 1 || !logits || !labels || !dlogits || !s_rows)
         return set_status(PNN_EINVAL, "softmax_xent_grad: bad arguments");
     const PositFmt f = make_fmt(nbits, es);
-    softmax_xent_kernel<<<grid1(B * 32), 256, 0, (cudaStream_t)stream>>>(
+    launch_pdl(softmax_xent_kernel, dim3(grid1(B * 32)), dim3(256), 0, (cudaStream_t)stream, 
         f, bytes_of(nbits), logits, labels, B, classes, log2_batch, grad_scale_log2,
-        dlogits, nullptr, s_rows, code_table(2, f, f, 0, (cudaStream_t)stream));
+        dlogits, nullptr, s_rows, code_table(2, f, f, 0, (cudaStream_t)stream),
+        static_cast<const uint16_t*>(nullptr));
     return launched("softmax_xent_grad");
 }
 
@@ -1105,10 +1157,10 @@ int pnn_softmax_xent_loss(int nbits, int es, const void* logits, const int32_t* 
     if (raw_word && f.W > 128)
         return set_status(PNN_EUNSUPPORTED, "softmax_xent: raw loss words need a quire of <= 128 bits");
     auto st = (cudaStream_t)stream;
-    xent_loss_rows_kernel<<<grid1(B), 256, 0, st>>>(f, bytes_of(nbits), logits, labels, s_rows, B,
+    launch_pdl(xent_loss_rows_kernel, dim3(grid1(B)), dim3(256), 0, st, f, bytes_of(nbits), logits, labels, s_rows, B,
                                                      classes, loss_rows, code_table(3, f, f, 0, st));
     if (loss_out || raw_word)
-        loss_reduce_kernel<<<1, 256, 0, st>>>(f, bytes_of(nbits), loss_rows, B, log2_batch, loss_out,
+        launch_pdl(loss_reduce_kernel, dim3(1), dim3(256), 0, st, f, bytes_of(nbits), loss_rows, B, log2_batch, loss_out,
                                               (unsigned __int128*)raw_word, (uint8_t*)raw_nar);
     return launched("softmax_xent_loss");
 }
@@ -1117,7 +1169,7 @@ int pnn_loss_reduce(int nbits, int es, const void* loss_rows, int64_t B, int log
                     void* loss_out, void* stream) {
     CHECK_FMT(nbits, es);
     if (B < 1 || !loss_rows || !loss_out) return set_status(PNN_EINVAL, "loss_reduce: bad arguments");
-    loss_reduce_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(make_fmt(nbits, es), bytes_of(nbits),
+    launch_pdl(loss_reduce_kernel, dim3(1), dim3(256), 0, (cudaStream_t)stream, make_fmt(nbits, es), bytes_of(nbits),
                                                             loss_rows, B, log2_batch, loss_out,
                                                             nullptr, nullptr);
     return launched("loss_reduce");
@@ -1142,7 +1194,7 @@ int pnn_sgd_step_scaled(int opt_nbits, int opt_es, void* master, int g_nbits, in
     if (n == 0) return PNN_OK;
     const PositFmt f1 = copy1 ? make_fmt(c1_nbits, c1_es) : make_fmt(opt_nbits, opt_es);
     const PositFmt f2 = copy2 ? make_fmt(c2_nbits, c2_es) : make_fmt(opt_nbits, opt_es);
-    sgd_kernel<<<grid1(n), 256, 0, (cudaStream_t)stream>>>(
+    launch_pdl(sgd_kernel, dim3(grid1(n)), dim3(256), 0, (cudaStream_t)stream, 
         make_fmt(opt_nbits, opt_es), bytes_of(opt_nbits), master, make_fmt(g_nbits, g_es),
         bytes_of(g_nbits), grad, n, lr_code, f1, bytes_of(f1.nbits), copy1, f2,
         bytes_of(f2.nbits), copy2, grad_scale_log2);
@@ -1212,7 +1264,7 @@ int pnn_sgd_step_multi(int opt_nbits, int opt_es, int g_nbits, int g_es, uint32_
                 launch_sgd_lut_c<uint8_t, uint8_t>(b1, b2, gr, st, fo, sg, luts);
             continue;
         }
-        sgd_multi_kernel<<<grid1(tot), 256, 0, (cudaStream_t)stream>>>(
+        launch_pdl(sgd_multi_kernel, dim3(grid1(tot)), dim3(256), 0, (cudaStream_t)stream, 
             fo, bytes_of(opt_nbits), fg, bytes_of(g_nbits), lr_code, f1, bytes_of(f1.nbits), f2,
             bytes_of(f2.nbits), grad_scale_log2, sg, fast);
     }
@@ -1227,7 +1279,7 @@ int pnn_avgpool2d_fwd(int nbits, int es, const void* x, int64_t N, int64_t C, in
         return set_status(PNN_EINVAL, "avgpool2d: window larger than input");
     const int64_t OH = (H - k) / stride + 1, OW = (W - k) / stride + 1;
     if (N == 0) return PNN_OK;
-    avgpool_fwd_kernel<<<grid1(N * C * OH * OW), 256, 0, (cudaStream_t)stream>>>(
+    launch_pdl(avgpool_fwd_kernel, dim3(grid1(N * C * OH * OW)), dim3(256), 0, (cudaStream_t)stream, 
         make_fmt(nbits, es), bytes_of(nbits), x, N * C, H, W, k, stride, OH, OW, use_quire,
         recip_code, y);
     return launched("avgpool2d_fwd");
@@ -1240,7 +1292,7 @@ int pnn_avgpool2d_bwd(int nbits, int es, const void* dy, int64_t N, int64_t C, i
         return set_status(PNN_EINVAL, "avgpool2d_backward: bad shape");
     const int64_t OH = (H - k) / stride + 1, OW = (W - k) / stride + 1;
     if (N == 0) return PNN_OK;
-    avgpool_bwd_kernel<<<grid1(N * C * H * W), 256, 0, (cudaStream_t)stream>>>(
+    launch_pdl(avgpool_bwd_kernel, dim3(grid1(N * C * H * W)), dim3(256), 0, (cudaStream_t)stream, 
         make_fmt(nbits, es), bytes_of(nbits), dy, N * C, H, W, k, stride, OH, OW, recip_code, dx);
     return launched("avgpool2d_bwd");
 }
@@ -1249,7 +1301,7 @@ int pnn_from_float64(int nbits, int es, const double* x, void* codes, int64_t n,
     CHECK_FMT(nbits, es);
     if (n < 0 || (n > 0 && (!x || !codes))) return set_status(PNN_EINVAL, "from_float64: bad args");
     if (n == 0) return PNN_OK;
-    from_float64_kernel<<<grid1(n), 256, 0, (cudaStream_t)stream>>>(make_fmt(nbits, es),
+    launch_pdl(from_float64_kernel, dim3(grid1(n)), dim3(256), 0, (cudaStream_t)stream, make_fmt(nbits, es),
                                                                     bytes_of(nbits), x, codes, n);
     return launched("from_float64");
 }
@@ -1258,7 +1310,7 @@ int pnn_scalar_eval(int nbits, int es, int op, const uint32_t* a, const uint32_t
                     uint32_t* out, int64_t n, void* stream) {
     CHECK_FMT(nbits, es);
     if (n <= 0) return PNN_OK;
-    scalar_eval_kernel<<<grid1(n), 256, 0, (cudaStream_t)stream>>>(make_fmt(nbits, es), op, a, b,
+    launch_pdl(scalar_eval_kernel, dim3(grid1(n)), dim3(256), 0, (cudaStream_t)stream, make_fmt(nbits, es), op, a, b,
                                                                    out, n);
     return launched("scalar_eval");
 }

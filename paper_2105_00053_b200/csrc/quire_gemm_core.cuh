@@ -40,6 +40,7 @@
 #include "fastdiv.cuh"
 #include "posit_device.cuh"
 #include "quire_gemm.h"
+#include "pdl.cuh"
 #include "sm100_ptx.cuh"
 
 namespace pnn_b200 {
@@ -160,6 +161,8 @@ __global__ void __launch_bounds__(256) pack_kernel(Fetch fetch, int64_t rows_tot
                                                    int64_t kbt, const uint2* __restrict__ glut,
                                                    uint8_t* __restrict__ wide_flag = nullptr,
                                                    int wide_planes = 0) {
+    pdl_trigger();
+    pdl_wait();  // PDL: nothing above touches global memory (pdl.cuh)
     const PositFmt f = fixed_fmt<FMT>(f_arg);
     constexpr int KB = Geometry<D>::KB;
     constexpr int KC = KB / 16;
@@ -494,12 +497,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                          int64_t N, PositFmt f_arg,
                          unsigned __int128* __restrict__ partial, int64_t mtiles, int64_t ntiles,
                          int64_t splits, const uint8_t* __restrict__ vflags = nullptr, int vmode = 0) {
-    // device-selected variant (vflags = {A wide, B wide} from the pack kernels):
-    // vmode 1 runs iff neither operand is wide, 2 iff either is; exit at once otherwise
-    if (vmode != 0) {
-        const bool wide = vflags[0] != 0 || vflags[1] != 0;
-        if (wide != (vmode == 2)) return;
-    }
+    pdl_trigger();  // the next kernel's CTAs may start their prologue in this grid's tail
     // kPair: clusters of 2 CTAs run one M=256 tcgen05.mma.cta_group::2 per
     // digit plane; each CTA stages its own 128-row A tile and HALF of the
     // concatenated B rows, halving each SM's shared-memory operand traffic.
@@ -540,6 +538,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::mbar_init(tmem_full, 1);
         ptx::mbar_init(tmem_empty, kPair ? 2 * kEpiWarps : kEpiWarps);
         ptx::fence_barrier_init();
+    }
+    // everything above touched only shared memory and parameters (PDL prologue)
+    pdl_wait();
+    // device-selected variant (vflags = {A wide, B wide} from the pack kernels):
+    // vmode 1 runs iff neither operand is wide, 2 iff either is; exit at once otherwise
+    if (vmode != 0) {
+        const bool wide = vflags[0] != 0 || vflags[1] != 0;
+        if (wide != (vmode == 2)) return;
     }
     if (warp == 1) {
         if constexpr (kPair) ptx::tmem_alloc2<Geo::TMEM_COLS>(tmem_slot);
@@ -746,6 +752,8 @@ __global__ void quire_finalize_kernel(const unsigned __int128* __restrict__ part
                                       int64_t M, int64_t N, PositFmt f,
                                       unsigned __int128* __restrict__ raw_words,
                                       uint8_t* __restrict__ raw_nar) {
+    pdl_trigger();
+    pdl_wait();  // PDL: nothing above touches global memory (pdl.cuh)
     const int64_t total = M * N;
     const unsigned __int128 one = 1;
     const unsigned __int128 wmask = f.W >= 128 ? ~(unsigned __int128)0 : ((one << f.W) - 1);
@@ -784,6 +792,8 @@ __global__ void __launch_bounds__(256) quire_finalize_warp_kernel(
     const unsigned __int128* __restrict__ partial, int splits, const uint8_t* __restrict__ row_nar,
     const uint8_t* __restrict__ col_nar, OutMap<CodeT> out, int64_t M, int64_t N, PositFmt f,
     unsigned __int128* __restrict__ raw_words, uint8_t* __restrict__ raw_nar) {
+    pdl_trigger();
+    pdl_wait();  // PDL: nothing above touches global memory (pdl.cuh)
     const int64_t total = M * N;
     const unsigned __int128 one = 1;
     const unsigned __int128 wmask = f.W >= 128 ? ~(unsigned __int128)0 : ((one << f.W) - 1);
@@ -821,6 +831,8 @@ __global__ void __launch_bounds__(256) quire_finalize_2d_kernel(
     const unsigned __int128* __restrict__ partial, int splits, const uint8_t* __restrict__ row_nar,
     const uint8_t* __restrict__ col_nar, OutMap<CodeT> out, int64_t M, int64_t N, PositFmt f,
     unsigned __int128* __restrict__ raw_words, uint8_t* __restrict__ raw_nar) {
+    pdl_trigger();
+    pdl_wait();  // PDL: nothing above touches global memory (pdl.cuh)
     __shared__ unsigned __int128 s_q[8][32];
     const int64_t total = M * N;
     const int x = threadIdx.x & 31, y = threadIdx.x >> 5;
@@ -864,10 +876,10 @@ inline void launch_finalize(const unsigned __int128* partial, int splits, const 
                             cudaStream_t st) {
     const int64_t total = M * N;
     if (splits >= 8)
-        quire_finalize_2d_kernel<CodeT><<<unsigned((total + 31) / 32), 256, 0, st>>>(
+        launch_pdl(quire_finalize_2d_kernel<CodeT>, dim3(unsigned((total + 31) / 32)), dim3(256), 0, st, 
             partial, splits, row_nar, col_nar, out, M, N, f, raw_words, raw_nar);
     else
-        quire_finalize_kernel<CodeT><<<grid_for(total, 256), 256, 0, st>>>(
+        launch_pdl(quire_finalize_kernel<CodeT>, dim3(grid_for(total, 256)), dim3(256), 0, st, 
             partial, splits, row_nar, col_nar, out, M, N, f, raw_words, raw_nar);
 }
 
@@ -1038,18 +1050,18 @@ cudaError_t launch_generic(const QuireGemmPlan& p, const GemmArgs& g, FA fa, FB 
                          !p.pair && g.M * g.N * g.K >= variant_min_work();  // the extra launch pays off
     const int ga = int(a_work < 148 * 8 ? a_work : 148 * 8), gb = int(b_work < 148 * 8 ? b_work : 148 * 8);
     if (D == 8 && sizeof(CodeT) == 2 && fixed_fmt_id(f) == 4) {  // posit(16,1): compile-time decode
-        pack_kernel<D, kBM, CodeT, FA, 4><<<ga, 256, 0, st>>>(fa, g.M, g.K, f, a_img, rnar, flags,
+        launch_pdl(pack_kernel<D, kBM, CodeT, FA, 4>, dim3(ga), dim3(256), 0, st, fa, g.M, g.K, f, a_img, rnar, flags,
                                                                p.mtiles_alloc, p.kbt, glut,
                                                                reduced ? flags + 2 : nullptr, kRed);
         if (g.pack_b)
-            pack_kernel<D, Geo::NT, CodeT, FB, 4><<<gb, 256, 0, st>>>(fb, g.N, g.K, f, b_img, cnar, flags + 1,
+            launch_pdl(pack_kernel<D, Geo::NT, CodeT, FB, 4>, dim3(gb), dim3(256), 0, st, fb, g.N, g.K, f, b_img, cnar, flags + 1,
                                                                        p.ntiles, p.kbt, glut,
                                                                        reduced ? flags + 3 : nullptr, kRed);
     } else {
-        pack_kernel<D, kBM, CodeT, FA><<<ga, 256, 0, st>>>(fa, g.M, g.K, f, a_img, rnar, flags, p.mtiles_alloc,
+        launch_pdl(pack_kernel<D, kBM, CodeT, FA>, dim3(ga), dim3(256), 0, st, fa, g.M, g.K, f, a_img, rnar, flags, p.mtiles_alloc,
                                                            p.kbt, glut, reduced ? flags + 2 : nullptr, kRed);
         if (g.pack_b)
-            pack_kernel<D, Geo::NT, CodeT, FB><<<gb, 256, 0, st>>>(fb, g.N, g.K, f, b_img, cnar, flags + 1,
+            launch_pdl(pack_kernel<D, Geo::NT, CodeT, FB>, dim3(gb), dim3(256), 0, st, fb, g.N, g.K, f, b_img, cnar, flags + 1,
                                                                    p.ntiles, p.kbt, glut,
                                                                    reduced ? flags + 3 : nullptr, kRed);
     }
@@ -1122,11 +1134,11 @@ cudaError_t launch_generic(const QuireGemmPlan& p, const GemmArgs& g, FA fa, FB 
                 if ((e = cudaFuncSetAttribute(kr, cudaFuncAttributeMaxDynamicSharedMemorySize, GR::SMEM)) !=
                     cudaSuccess)
                     return e;
-                kr<<<grid, kThreads, GR::SMEM, st>>>(a_img, b_img, p.kbt, p.kb_per_split, rn, cn, out, g.M,
+                launch_pdl(kr, dim3(grid), dim3(kThreads), GR::SMEM, st, a_img, b_img, p.kbt, p.kb_per_split, rn, cn, out, g.M,
                                                      g.N, f, partial, p.mtiles, p.ntiles, p.splits, flags + 2, 1);
             }
         }
-        kern<<<grid, kThreads, Geo::SMEM, st>>>(a_img, b_img, p.kbt, p.kb_per_split, rn, cn, out,
+        launch_pdl(kern, dim3(grid), dim3(kThreads), Geo::SMEM, st, a_img, b_img, p.kbt, p.kb_per_split, rn, cn, out,
                                                 g.M, g.N, f, partial, p.mtiles, p.ntiles, p.splits,
                                                 reduced ? flags + 2 : nullptr, reduced ? 2 : 0);
     }
