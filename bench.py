@@ -159,14 +159,15 @@ _REF_CACHE = {}
 
 def ncu_traffic(kernel_prefix: str):
     """DRAM bytes (read + write) per launch of the kernel from the committed
-    `ncu --set full` capture summary (profiles/ncu_full_r01.json)."""
-    p = os.path.join(REPO, "profiles", "ncu_full_r01.json")
-    if not os.path.exists(p):
-        return None
-    for rep, ks in json.load(open(p)).items():
-        for k in ks:
-            if k["kernel"].startswith(kernel_prefix) and "dram_traffic_bytes" in k:
-                return {"bytes_per_launch": k["dram_traffic_bytes"], "source": f"profiles/ncu_full_r01.json:{rep}"}
+    `ncu --set full` capture summaries (profiles/ncu_full_r02.json, else r01)."""
+    for name in ("ncu_full_r02.json", "ncu_full_r01.json"):
+        p = os.path.join(REPO, "profiles", name)
+        if not os.path.exists(p):
+            continue
+        for rep, ks in json.load(open(p)).items():
+            for k in ks:
+                if k["kernel"].startswith(kernel_prefix) and "dram_traffic_bytes" in k:
+                    return {"bytes_per_launch": k["dram_traffic_bytes"], "source": f"profiles/{name}:{rep}"}
     return None
 
 
@@ -481,6 +482,7 @@ def main():
                          "frac": achieved / peak,
                          "traffic": traffic["bytes_per_launch"] if traffic else None,
                          "traffic_unit": "bytes/launch (dram read+write, ncu --set full)",
+                         "traffic_source": traffic["source"] if traffic else None,
                          "note": f"int8 tensor ops (2/MAC) on tcgen05 kind::i8, {D}x{D} digit "
                                  f"MMAs per posit MAC; peak = {peak_src}"},
             "gpu_launches": args.steps * len(FORMATS) * 3,
