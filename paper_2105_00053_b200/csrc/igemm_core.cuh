@@ -189,6 +189,16 @@ __global__ void __launch_bounds__(ImplGeo<D, NT_, CPS, ACC, DA, DB>::THREADS, CP
         if (a.vflag2 != nullptr && int(*a.vflag2 != 0) != a.vexpect2) return;
     }
     if (warp == 1) ptx::tmem_alloc<Geo::TMEM_COLS>(tmem_slot);
+    // forward bias: X(bias) * 2^R per column, once per CTA in shared memory
+    // (zero past N: the epilogue adds without bounds tests)
+    constexpr int kColSmem = MODE == 0 ? 256 : 1;
+    __shared__ int64_t s_colx[kColSmem];
+    const bool col_smem = MODE == 0 && a.col_add != nullptr && a.N <= kColSmem;
+    if (col_smem)
+        for (int i = threadIdx.x; i < kColSmem; i += kIThreads) {
+            const int64_t xb = i < a.N ? a.col_add[i] : 0;
+            s_colx[i] = QW <= 2 ? int64_t(uint64_t(xb) << fixed_fmt<FMT>(a.f).R) : xb;
+        }
     ptx::fence_proxy_async_smem();
     ptx::tc_fence_before();
     __syncthreads();
@@ -361,13 +371,22 @@ __global__ void __launch_bounds__(ImplGeo<D, NT_, CPS, ACC, DA, DB>::THREADS, CP
             if (obase < 0 && a.partial == nullptr) continue;  // padding row (weight grad)
             if constexpr (MODE == 0) if (a.col_add != nullptr && split == 0) {
                 const int cb = int(colbase), nn = int(a.N);
+                if (col_smem) {  // (columns past N read zeros)
 #pragma unroll
-                for (int c = 0; c < COLS; ++c)
-                    if (cb + SUB * (c & ~7) + (c & 7) < nn) {
-                        const int64_t xb = a.col_add[cb + SUB * (c & ~7) + (c & 7)];
-                        if constexpr (QW == 4) q[c] += QT(__int128(xb)) << f.R;
-                        else q[c] += QT(xb) << f.R;
+                    for (int c = 0; c < COLS; ++c) {
+                        const int64_t xs = s_colx[cb + SUB * (c & ~7) + (c & 7)];
+                        if constexpr (QW == 4) q[c] += QT(__int128(xs)) << f.R;
+                        else q[c] += QT(xs);
                     }
+                } else {
+#pragma unroll
+                    for (int c = 0; c < COLS; ++c)
+                        if (cb + SUB * (c & ~7) + (c & 7) < nn) {
+                            const int64_t xb = a.col_add[cb + SUB * (c & ~7) + (c & 7)];
+                            if constexpr (QW == 4) q[c] += QT(__int128(xb)) << f.R;
+                            else q[c] += QT(xb) << f.R;
+                        }
+                }
             }
 #pragma unroll
             for (int c0 = 0; c0 < COLS; c0 += 8) {
