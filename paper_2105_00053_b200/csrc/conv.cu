@@ -403,6 +403,21 @@ __global__ void __launch_bounds__(512) bias_grad_chan_kernel(
         return g;
     };
     uint32_t i = threadIdx.x;
+    // four 16-byte loads in flight per thread (the loop is load-latency bound)
+    for (; i + 3 * blockDim.x < nv; i += 4 * blockDim.x) {
+        uint32_t q0, r0, q1, r1, q2, r2, q3, r3;
+        fd_vpr.divmod(i, q0, r0);
+        fd_vpr.divmod(i + blockDim.x, q1, r1);
+        fd_vpr.divmod(i + 2 * blockDim.x, q2, r2);
+        fd_vpr.divmod(i + 3 * blockDim.x, q3, r3);
+        const uint4 w0 = __ldg(reinterpret_cast<const uint4*>(base + q0 * img_stride) + r0);
+        const uint4 w1 = __ldg(reinterpret_cast<const uint4*>(base + q1 * img_stride) + r1);
+        const uint4 w2 = __ldg(reinterpret_cast<const uint4*>(base + q2 * img_stride) + r2);
+        const uint4 w3 = __ldg(reinterpret_cast<const uint4*>(base + q3 * img_stride) + r3);
+        const GV g0 = gload(q0, r0), g1 = gload(q1, r1), g2 = gload(q2, r2), g3 = gload(q3, r3);
+        acc += vsum(w0, g0) + vsum(w1, g1);  // 2 * 16 * 2^56 < 2^62
+        acc += vsum(w2, g2) + vsum(w3, g3);
+    }
     for (; i + blockDim.x < nv; i += 2 * blockDim.x) {
         uint32_t q0, r0, q1, r1;
         fd_vpr.divmod(i, q0, r0);

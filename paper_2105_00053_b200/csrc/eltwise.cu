@@ -238,6 +238,9 @@ __global__ void __launch_bounds__(256) maxpool2_bwd_x_kernel(int x_nbits, const 
     const int W = 2 * OW, vpr = OW / WPT;
     const int total = rows * vpr;
     const int sh = 32 - x_nbits;
+    // vector loads of dy when every thread's WPT gradients are aligned
+    const bool gvec = (reinterpret_cast<uintptr_t>(dy) % (WPT * sizeof(TG))) == 0 &&
+                      (int64_t(OW) * sizeof(TG)) % (WPT * sizeof(TG)) == 0;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
         const int r = i / vpr, v = i - r * vpr;
         const int64_t in0 = (int64_t(r) * 2) * W + v * VE;
@@ -246,8 +249,27 @@ __global__ void __launch_bounds__(256) maxpool2_bwd_x_kernel(int x_nbits, const 
         load_codes16<TX>(x + in0 + W, b);
         uint32_t g[WPT];
         const TG* gp = dy + int64_t(r) * OW + v * WPT;
+        if (!gvec) {
 #pragma unroll
-        for (int j = 0; j < WPT; ++j) g[j] = uint32_t(gp[j]);
+            for (int j = 0; j < WPT; ++j) g[j] = uint32_t(gp[j]);
+        } else if constexpr (WPT * sizeof(TG) == 16 || WPT * sizeof(TG) == 8) {
+            // one 16- or 8-byte load of the WPT gradients
+            uint32_t gw[4];
+            if constexpr (WPT * sizeof(TG) == 16) {
+                const uint4 gv = __ldg(reinterpret_cast<const uint4*>(gp));
+                gw[0] = gv.x, gw[1] = gv.y, gw[2] = gv.z, gw[3] = gv.w;
+            } else {
+                const uint2 gv = __ldg(reinterpret_cast<const uint2*>(gp));
+                gw[0] = gv.x, gw[1] = gv.y, gw[2] = gw[3] = 0u;
+            }
+#pragma unroll
+            for (int j = 0; j < WPT; ++j)
+                g[j] = sizeof(TG) == 2 ? (gw[j >> 1] >> (16 * (j & 1))) & 0xFFFFu
+                                       : (gw[j >> 2] >> (8 * (j & 3))) & 0xFFu;
+        } else {
+#pragma unroll
+            for (int j = 0; j < WPT; ++j) g[j] = uint32_t(gp[j]);
+        }
         const uint32_t sign = 1u << (x_nbits - 1);
         uint32_t top[16] = {}, bot[16] = {};  // VE used (pack16_u8 reads 16)
 #pragma unroll
