@@ -31,6 +31,7 @@
 // epilogue (TMEM -> registers -> 128-bit quire -> posit code).
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -496,7 +497,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                          const uint8_t* __restrict__ col_nar, OutMap<CodeT> out, int64_t M,
                          int64_t N, PositFmt f_arg,
                          unsigned __int128* __restrict__ partial, int64_t mtiles, int64_t ntiles,
-                         int64_t splits, const uint8_t* __restrict__ vflags = nullptr, int vmode = 0) {
+                         int64_t splits, const uint8_t* __restrict__ vflags, int vmode,
+                         const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB) {
     pdl_trigger();  // the next kernel's CTAs may start their prologue in this grid's tail
     // kPair: clusters of 2 CTAs run one M=256 tcgen05.mma.cta_group::2 per
     // digit plane; each CTA stages its own 128-row A tile and HALF of the
@@ -531,8 +533,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         reinterpret_cast<int4*>(zero_tile)[i] = make_int4(0, 0, 0, 0);
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < STAGES; ++s) {
-            // leader: own expect_tx arrive + the follower's "landed" forward
-            ptx::mbar_init(&full[s], (kPair && leader) ? 2 : 1);
+            // (pair: both CTAs' tensor loads complete_tx on the leader's barrier;
+            // its one arrival is the leader's expect_tx)
+            ptx::mbar_init(&full[s], 1);
             ptx::mbar_init(&empty[s], 1);
         }
         ptx::mbar_init(tmem_full, 1);
@@ -576,30 +579,25 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const uint32_t ph = (it / STAGES) & 1;
                     ptx::mbar_wait(&empty[s], ph ^ 1);
                     uint8_t* sa = smem + s * Geo::STAGE_BYTES;
-                    ptx::mbar_arrive_expect_tx(&full[s], STAGE_TX);
-                    ptx::bulk_g2s(sa, a_src + int64_t(i) * Geo::IMG_A, Geo::A_BYTES, &full[s]);
-                    ptx::bulk_g2s(sa + Geo::A_BYTES, b_src + int64_t(i) * Geo::IMG_B, B_LOCAL,
-                                  &full[s]);
+                    if constexpr (kPair) {
+                        // 2-D tensor boxes of the packed images (rows of 256 bytes), each CTA
+                        // its own A tile and half of B, both signalling the leader's barrier
+                        if (leader) ptx::mbar_arrive_expect_tx(&full[s], 2 * STAGE_TX);
+                        const int64_t ra = ((mt * kbt + kb0 + i) * int64_t(Geo::IMG_A)) >> 8;
+                        const int64_t rb = ((nt * kbt + kb0 + i) * int64_t(Geo::IMG_B) + rank * B_LOCAL) >> 8;
+                        ptx::tma_load_2d_pair(sa, &tmA, 0, int(ra), &full[s]);
+                        ptx::tma_load_2d_pair(sa + Geo::A_BYTES, &tmB, 0, int(rb), &full[s]);
+                    } else {
+                        ptx::mbar_arrive_expect_tx(&full[s], STAGE_TX);
+                        ptx::bulk_g2s(sa, a_src + int64_t(i) * Geo::IMG_A, Geo::A_BYTES, &full[s]);
+                        ptx::bulk_g2s(sa + Geo::A_BYTES, b_src + int64_t(i) * Geo::IMG_B, B_LOCAL,
+                                      &full[s]);
+                    }
                 }
             }
         }
     } else if (warp == 1) {
-        if (lane == 0 && kPair && !leader) {
-            // ===== follower: forward "stage landed" to the leader's barrier =====
-            uint32_t it = 0;
-            for (int64_t t = unit0; t < tiles; t += ustride) {
-                int64_t split, um, nt;
-                tile_coords(t, unit_m, ntiles, split, um, nt);
-                const int64_t kb0 = split * kb_per_split;
-                const int nkb = int(min(kbt, kb0 + kb_per_split) - kb0);
-                for (int i = 0; i < nkb; ++i, ++it) {
-                    const int s = it % STAGES;
-                    const uint32_t ph = (it / STAGES) & 1;
-                    ptx::mbar_wait(&full[s], ph);
-                    ptx::mbar_arrive_remote(ptx::mapa(ptx::smem_u32(&full[s]), 0));
-                }
-            }
-        } else if (lane == 0 && leader) {
+        if (lane == 0 && leader) {
             // ===== MMA issuer =====
             constexpr uint32_t idesc = ptx::idesc_i8(kPair ? 2 * kBM : kBM, Geo::NMMA);
             constexpr uint32_t SBO = 8 * KB, LBO = 128;
@@ -1015,6 +1013,32 @@ inline int plan_quire_gemm(const PositFmt& f, int64_t M, int64_t N, int64_t K,
     return 0;
 }
 
+// A packed operand image as a 2-D uint8 tensor of 256-byte rows, box = one
+// stage's bytes (rows of the box = bytes / 256): the CTA-pair producer's
+// cp.async.bulk.tensor boxes.  (Driver entry point, resolved once.)
+inline bool encode_rows256(CUtensorMap* m, const void* base, size_t bytes, int box_bytes) {
+    using Enc = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                             const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                             CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    static Enc enc = [] {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &fn, 12000, cudaEnableDefault, &q) !=
+                cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return Enc(nullptr);
+        return reinterpret_cast<Enc>(fn);
+    }();
+    if (enc == nullptr || bytes % 256 || box_bytes % 256 || box_bytes / 256 > 256) return false;
+    const cuuint64_t dims[2] = {256, cuuint64_t(bytes / 256)};
+    const cuuint64_t strides[1] = {256};
+    const cuuint32_t box[2] = {256, cuuint32_t(box_bytes / 256)};
+    const cuuint32_t estr[2] = {1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <int D, typename CodeT, class FA, class FB>
 cudaError_t launch_generic(const QuireGemmPlan& p, const GemmArgs& g, FA fa, FB fb,
                            OutMap<CodeT> out, uint8_t* ws, cudaStream_t st,
@@ -1069,8 +1093,17 @@ cudaError_t launch_generic(const QuireGemmPlan& p, const GemmArgs& g, FA fa, FB 
     // D <= 3 implies R <= 11, hence W <= 64: no 128-bit instantiation needed.
     using KernFn = void (*)(const int8_t*, const int8_t*, int64_t, int64_t, const uint8_t*,
                             const uint8_t*, OutMap<CodeT>, int64_t, int64_t, PositFmt,
-                            unsigned __int128*, int64_t, int64_t, int64_t, const uint8_t*, int);
+                            unsigned __int128*, int64_t, int64_t, int64_t, const uint8_t*, int, CUtensorMap,
+                            CUtensorMap);
     KernFn kern;
+    // CTA pairs: 2-D tensor maps over the packed images (256-byte rows; boxes
+    // = one CTA's A tile / half B tile per stage); unused otherwise
+    CUtensorMap tmA{}, tmB{};
+    if (p.pair) {
+        if (!encode_rows256(&tmA, a_img, p.a_img_bytes, Geo::A_BYTES) ||
+            !encode_rows256(&tmB, b_img, p.b_img_bytes, Geo::B_BYTES / 2))
+            return cudaErrorInvalidValue;
+    }
     if (p.pair) {
         if constexpr (D <= 3)
             kern = f.W <= 32 ? quire_gemm_tc_kernel<D, 1, CodeT, true>
@@ -1118,7 +1151,7 @@ cudaError_t launch_generic(const QuireGemmPlan& p, const GemmArgs& g, FA fa, FB 
         cfg.numAttrs = 1;
         if ((e = cudaLaunchKernelEx(&cfg, kern, (const int8_t*)a_img, (const int8_t*)b_img, p.kbt,
                                     p.kb_per_split, rn, cn, out, g.M, g.N, f, partial, p.mtiles,
-                                    p.ntiles, p.splits, (const uint8_t*)nullptr, 0)) != cudaSuccess)
+                                    p.ntiles, p.splits, (const uint8_t*)nullptr, 0, tmA, tmB)) != cudaSuccess)
             return e;
     } else {
         const int64_t tiles = p.mtiles * p.ntiles * p.splits;
@@ -1135,12 +1168,13 @@ cudaError_t launch_generic(const QuireGemmPlan& p, const GemmArgs& g, FA fa, FB 
                     cudaSuccess)
                     return e;
                 launch_pdl(kr, dim3(grid), dim3(kThreads), GR::SMEM, st, a_img, b_img, p.kbt, p.kb_per_split, rn, cn, out, g.M,
-                                                     g.N, f, partial, p.mtiles, p.ntiles, p.splits, flags + 2, 1);
+                                                     g.N, f, partial, p.mtiles, p.ntiles, p.splits, flags + 2, 1,
+                                                     tmA, tmB);
             }
         }
         launch_pdl(kern, dim3(grid), dim3(kThreads), Geo::SMEM, st, a_img, b_img, p.kbt, p.kb_per_split, rn, cn, out,
                                                 g.M, g.N, f, partial, p.mtiles, p.ntiles, p.splits,
-                                                reduced ? flags + 2 : nullptr, reduced ? 2 : 0);
+                                                reduced ? flags + 2 : nullptr, reduced ? 2 : 0, tmA, tmB);
     }
     if (stats) cudaEventRecord(stats->ev[2], st);
     if (use_partial) {

@@ -280,6 +280,20 @@ __device__ __forceinline__ void tma_load_3d(void* smem_dst, const void* tmap, in
         : "memory");
 }
 
+// CTA-pair (cta_group::2) 2-D tensor load: the bytes land in this CTA's
+// shared memory and complete_tx on the mbarrier of the pair's leader (rank 0):
+// the local mbarrier address with the peer bit (bit 24 of the shared::cluster
+// window) cleared, as CUTLASS's SM100_TMA_2SM_LOAD does.
+__device__ __forceinline__ void tma_load_2d_pair(void* smem_dst, const void* tmap, int c0, int c1,
+                                                 uint64_t* bar) {
+    const uint32_t leader_bar = smem_u32(bar) & 0xFEFFFFFFu;
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(smem_dst)),
+        "l"(tmap), "r"(c0), "r"(c1), "r"(leader_bar)
+        : "memory");
+}
+
 __device__ __forceinline__ void tma_prefetch_desc(const void* tmap) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(tmap) : "memory");
 }
