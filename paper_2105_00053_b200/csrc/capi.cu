@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "../../include/pnn_b200.h"
+#include "epilogue.cuh"
 #include "posit_device.cuh"
 #include "quire_gemm.h"
 #include "status.h"
@@ -624,6 +625,28 @@ int pnn_matmul_host(int nbits, int es, const uint64_t* A, const uint64_t* B, uin
         for (int i = 0; i <= 2 * P; ++i) cudaEventDestroy(tev[i]);
     }
     return PNN_OK;
+}
+
+// Internal test hook (not part of include/pnn_b200.h): the epilogue's two
+// 64-bit quire-word roundings (integer leading-one search vs the FP64
+// converter) on the same words, for tests/test_epilogue_gpu.py.
+__global__ void round64_check_kernel(PositFmt f, const uint64_t* q, int64_t n, uint32_t* a, uint32_t* b) {
+    __shared__ uint4 s_lut[kPackLutEntries];
+    build_pack_lut(f, s_lut, threadIdx.x, blockDim.x);
+    __syncthreads();
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+        a[i] = q_to_posit_lut(f, q[i], s_lut);
+        b[i] = q_to_posit_lut_f64(f, q[i], s_lut);
+    }
+}
+
+int pnn_internal_round64_check(int nbits, int es, const uint64_t* q, int64_t n, uint32_t* a, uint32_t* b,
+                               void* stream) {
+    if (int rc = check_fmt(nbits, es)) return rc;
+    const PositFmt f = make_fmt(nbits, es);
+    if (n <= 0) return PNN_OK;  // (W > 64: the word is the exact value as int64, no wrap)
+    round64_check_kernel<<<148 * 4, 256, 0, as_stream(stream)>>>(f, q, n, a, b);
+    return cudaGetLastError() == cudaSuccess ? PNN_OK : cuda_fail(cudaGetLastError(), "round64_check");
 }
 
 int pnn_decode_x(int nbits, int es, const uint32_t* codes, int64_t n, int64_t* X, uint8_t* nar,

@@ -77,7 +77,12 @@ __device__ __forceinline__ uint32_t q_to_posit_lut(const PositFmt& f, uint32_t q
 __device__ __forceinline__ uint32_t q_to_posit_lut(const PositFmt& f, uint64_t q, const uint4* lut) {
     uint32_t lo = uint32_t(q);
     int32_t hi = int32_t(q >> 32);
-    if (f.W < 64) hi = (hi << (64 - f.W)) >> (64 - f.W);
+    if (f.W <= 32) {  // the whole word lives in the low half (no shift by >= 32)
+        lo = uint32_t(int32_t(lo << (32 - f.W)) >> (32 - f.W));
+        hi = int32_t(lo) >> 31;
+    } else if (f.W < 64) {
+        hi = (hi << (64 - f.W)) >> (64 - f.W);
+    }
     const uint32_t s = uint32_t(hi >> 31);  // 0 or ~0
     uint32_t ml = lo ^ s, mh = uint32_t(hi) ^ s;
     asm("add.cc.u32 %0, %0, %2;\n\taddc.u32 %1, %1, 0;" : "+r"(ml), "+r"(mh) : "r"(s & 1u));
@@ -88,6 +93,25 @@ __device__ __forceinline__ uint32_t q_to_posit_lut(const PositFmt& f, uint64_t q
     const int top = hz ? 31 - lzl : 63 - lzh;
     const uint32_t c = pack_lut(f, lut, top - 2 * f.R, sig, sticky, s != 0);
     return (ml | mh) == 0 ? 0u : c;
+}
+
+// The same rounding of a 64-bit word (W <= 64) with the leading-one search and
+// the normalisation done by the FP64 converter: I2F.F64 (toward zero) of the
+// W-bit value gives |q|'s exponent and its top 53 bits; the bits it drops
+// (|q| >= 2^53) are detected by converting back (exact for an integral double)
+// and OR-ed into the sticky bit.  Same pack_lut call, same result
+// (tests/test_epilogue_gpu.py compares both on edge and random words).
+__device__ __forceinline__ uint32_t q_to_posit_lut_f64(const PositFmt& f, uint64_t q, const uint4* lut) {
+    int64_t v = int64_t(q);
+    if (f.W < 64) v = (v << (64 - f.W)) >> (64 - f.W);
+    const double d = __ll2double_rz(v);
+    const bool lost = __double2ll_rz(d) != v;
+    const uint32_t hi = uint32_t(__double2hiint(d)), lo = uint32_t(__double2loint(d));
+    const int top = int((hi >> 20) & 0x7FFu) - 1023;
+    const uint32_t sig = 0x80000000u | ((hi & 0xFFFFFu) << 11) | (lo >> 21);
+    const bool sticky = (lo & 0x1FFFFFu) != 0 || lost;
+    const uint32_t c = pack_lut(f, lut, top - 2 * f.R, sig, sticky, (hi >> 31) != 0);
+    return v == 0 ? 0u : c;
 }
 
 // 128-bit word as four 32-bit limbs (sign extension from W bits, |q| by xor +

@@ -126,6 +126,25 @@ __device__ __forceinline__ void itile_coords(int64_t t64, const IgemmArgs& a, in
     nt = q;
 }
 
+// quire word -> posit code in the epilogue: 64-bit words through the FP64
+// converter (PNN_EPI_INT_ROUND: the integer leading-one search), the other
+// widths through the integer paths
+#ifndef PNN_EPI_INT_ROUND
+__device__ __forceinline__ uint32_t epi_round(const PositFmt& f, uint64_t q, const uint4* lut) {
+    return q_to_posit_lut_f64(f, q, lut);
+}
+#else
+__device__ __forceinline__ uint32_t epi_round(const PositFmt& f, uint64_t q, const uint4* lut) {
+    return q_to_posit_lut(f, q, lut);
+}
+#endif
+__device__ __forceinline__ uint32_t epi_round(const PositFmt& f, uint32_t q, const uint4* lut) {
+    return q_to_posit_lut(f, q, lut);
+}
+__device__ __forceinline__ uint32_t epi_round(const PositFmt& f, unsigned __int128 q, const uint4* lut) {
+    return q_to_posit_lut(f, q, lut);
+}
+
 // Epilogue warps: 8 (two CTAs per SM) or 16 (one): the epilogue (TMEM drain,
 // quire accumulation, quire -> posit) is latency-bound, so it gets the warps.
 //
@@ -409,7 +428,7 @@ __global__ void __launch_bounds__(ImplGeo<D, NT_, CPS, ACC, DA, DB>::THREADS, CP
 #pragma unroll
                 for (int x = 0; x < 8; ++x) {
                     const uint32_t c =
-                        PNN_EPI_DEBUG(1) ? uint32_t(q[c0 + x]) : q_to_posit_lut(f, q[c0 + x], s_lut);
+                        PNN_EPI_DEBUG(1) ? uint32_t(q[c0 + x]) : epi_round(f, q[c0 + x], s_lut);
                     codes[x] = ((cn >> (8 * x)) & 0xFF) ? (1u << (f.nbits - 1)) : c;
                 }
                 if constexpr (MODE == 0) if (a.relu) {
