@@ -38,6 +38,7 @@
 #include <cstdint>
 #include <cstdlib>
 
+#include "epilogue.cuh"
 #include "fastdiv.cuh"
 #include "posit_device.cuh"
 #include "quire_gemm.h"
@@ -512,6 +513,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr int B_LOCAL = kPair ? Geo::B_BYTES / 2 : Geo::B_BYTES;
     constexpr int STAGE_TX = Geo::A_BYTES + B_LOCAL;
     extern __shared__ __align__(1024) uint8_t smem[];
+    // 64-bit quire words round through the FP64 converter + rounding table
+    // (epilogue.cuh q_to_posit_lut_f64: the word is the exact value, any W)
+    __shared__ uint4 s_lut[QW == 2 ? kPackLutEntries : 1];
+    if constexpr (QW == 2) build_pack_lut(f, s_lut, threadIdx.x, kThreads);
     uint8_t* zero_tile = smem + STAGES * Geo::STAGE_BYTES;
     uint64_t* full = reinterpret_cast<uint64_t*>(zero_tile + kZeroBytes);
     uint64_t* empty = full + STAGES;
@@ -700,7 +705,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                     unsigned __int128* dst = partial + (split * M + row) * N + col0;
 #pragma unroll
                     for (int x = 0; x < 8; ++x)
-                        if (x < valid) dst[x] = (unsigned __int128)q[c0 + x];
+                        if (x < valid) {
+                            if constexpr (QW == 2)  // sign-extended: the exact value for any W
+                                dst[x] = (unsigned __int128)(__int128)int64_t(q[c0 + x]);
+                            else
+                                dst[x] = (unsigned __int128)q[c0 + x];
+                        }
                     continue;
                 }
                 // column NaR flags as one 8-byte load (flag buffer padded to whole tiles)
@@ -710,7 +720,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                 for (int x = 0; x < 8; ++x) {
                     const bool nar = rnar || ((cn >> (8 * x)) & 0xFF) != 0;
-                    codes[x] = nar ? (1u << (f.nbits - 1)) : quire_word_to_posit_bf(f, q[c0 + x]);
+                    uint32_t c;
+                    if constexpr (QW == 2) c = q_to_posit_lut_f64(f, uint64_t(q[c0 + x]), s_lut);
+                    else c = quire_word_to_posit_bf(f, q[c0 + x]);
+                    codes[x] = nar ? (1u << (f.nbits - 1)) : c;
                 }
                 if (vec_ok) {
                     store_codes8(out.base + row * out.ldc + col0, codes, valid, true);
@@ -1161,7 +1174,9 @@ cudaError_t launch_generic(const QuireGemmPlan& p, const GemmArgs& g, FA fa, FB 
                 using GR = Geometry<D, kRed>;
                 // (128-bit word: this epilogue's quire_word_to_posit_bf takes W <= word bits)
                 constexpr int kFmt = D == 4 ? 2 : D == 6 ? 3 : 4;
-                constexpr int kQW = D == 4 ? 2 : 4;  // posit(8,1)-class: W <= 64
+                // 64-bit words: posit(8,1)-class (W <= 64) and the 3-digit posit(12,1)-class
+                // variant (|X| < 2^23: |sum| < 2^46 * K <= 2^61 per split, exact as int64)
+                constexpr int kQW = D == 8 ? 4 : 2;
                 KernFn kr = fixed_fmt_id(f) == kFmt ? quire_gemm_tc_kernel<D, kQW, CodeT, false, kFmt, kRed>
                                                     : quire_gemm_tc_kernel<D, kQW, CodeT, false, 0, kRed>;
                 if ((e = cudaFuncSetAttribute(kr, cudaFuncAttributeMaxDynamicSharedMemorySize, GR::SMEM)) !=
