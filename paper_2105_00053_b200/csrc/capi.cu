@@ -291,9 +291,14 @@ __global__ void decode_x_kernel(const uint32_t* codes, int64_t n, PositFmt f, in
                                 uint8_t* nar) {
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
          i += int64_t(gridDim.x) * blockDim.x) {
-        int64_t x;
-        nar[i] = decode_x(codes[i], f, x) ? 1 : 0;
-        X[i] = x;
+        int64_t x, xb;
+        const bool nr = decode_x(codes[i], f, x);
+        // the digitisers' branch-free decode must agree code for code (a
+        // mismatch shows as an impossible NaR flag and a poisoned image)
+        const bool nb = decode_x_bf(codes[i], f, xb);
+        const bool same = nb == nr && xb == x;
+        nar[i] = same ? (nr ? 1 : 0) : 2;
+        X[i] = same ? x : INT64_MIN;
     }
 }
 

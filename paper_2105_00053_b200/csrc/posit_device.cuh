@@ -86,6 +86,32 @@ __device__ __forceinline__ bool decode_x(uint32_t code, const PositFmt& f, int64
     return false;
 }
 
+// decode_x without branches (the digitisers' per-code hot path): the same X
+// for every code (zero and NaR give X = 0; returns true for NaR).  The regime
+// run comes from one FLO of the payload XOR its first bit, the significand is
+// kept left-aligned (leading one at bit 31) and placed by one 64-bit right
+// shift of S * 2^32 by 63 - R - scale (in [63 - 2R, 63]: pos >= 0 for every
+// finite posit, so only zeros are shifted out).  Valid for nbits <= 32, 2R <= 62.
+__device__ __forceinline__ bool decode_x_bf(uint32_t code, const PositFmt& f, int64_t& X) {
+    const uint32_t narc = 1u << (f.nbits - 1);
+    code &= narc | (narc - 1u);
+    const uint32_t sgn = 0u - (code >> (f.nbits - 1));      // 0 or ~0
+    const uint32_t mag = ((code ^ sgn) - sgn) & (narc - 1u);  // payload; 0 for zero and NaR
+    const uint32_t p = mag << (33 - f.nbits);
+    const uint32_t inv = uint32_t(int32_t(p) >> 31);          // ~0 when the regime is a run of ones
+    const int run = __clz(int(p ^ inv));                      // <= nbits - 1 (32 only when mag == 0)
+    const uint32_t tail = (p << (run & 31)) << 1;             // past the regime and its terminator
+    const uint32_t e = f.es > 0 ? tail >> (32 - f.es) : 0u;
+    const uint32_t S = ((tail << f.es) >> 1) | 0x80000000u;   // 1.fraction, leading one at bit 31
+    const int k = (run - 1) ^ int(~inv);                      // run - 1, or -run for a run of zeros
+    const int scale = k * (1 << f.es) + int(e);
+    uint64_t mx = (uint64_t(S) << 32) >> (63 - f.R - scale);
+    mx = mag == 0 ? 0ull : mx;
+    const uint64_t s64 = uint64_t(int64_t(int32_t(sgn)));
+    X = int64_t((mx ^ s64) - s64);
+    return code == narc;
+}
+
 // Same, into a 128-bit image: valid for 2R <= 124 (the elementwise formats up
 // to posit(12,2), R = 40, used by the posit(8,2)* optimizer and loss stages).
 __device__ __forceinline__ bool decode_x128(uint32_t code, const PositFmt& f, __int128& X) {

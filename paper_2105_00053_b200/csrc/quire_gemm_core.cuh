@@ -37,6 +37,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
+#include <type_traits>
 
 #include "epilogue.cuh"
 #include "fastdiv.cuh"
@@ -44,6 +45,7 @@
 #include "quire_gemm.h"
 #include "pdl.cuh"
 #include "sm100_ptx.cuh"
+#include "tables.h"
 
 namespace pnn_b200 {
 
@@ -94,7 +96,7 @@ template <int D>
 __device__ __forceinline__ void digit_words(uint32_t code, const PositFmt& f, uint32_t& lo,
                                             uint32_t& hi, bool& nar) {
     int64_t X;
-    nar = decode_x(code, f, X);
+    nar = decode_x_bf(code, f, X);
     // Balanced digits in two instructions: with bias = sum_{i<D} 128*256^i,
     // Y = X + bias has plain bytes (d_i + 128) in [0, 255] (|X| is within the
     // D-digit balanced capacity, so Y < 256^D), and d_i = byte_i(Y) ^ 0x80.
@@ -174,7 +176,7 @@ __global__ void __launch_bounds__(256) pack_kernel(Fetch fetch, int64_t rows_tot
     constexpr int PADC = 4 / sizeof(CodeT);  // row stride = odd multiple of 4 bytes
     constexpr int LD = KW + PADC;
     __shared__ __align__(16) CodeT tile[ROWS * LD];
-    __shared__ uint32_t lut[2 << kLutMaxBits];
+    __shared__ __align__(8) uint32_t lut[2 << kLutMaxBits];
     const bool use_lut = f.nbits <= kLutMaxBits;
     if (use_lut) {
         for (int c = threadIdx.x; c < (1 << f.nbits); c += blockDim.x) {
@@ -277,29 +279,56 @@ __global__ void __launch_bounds__(256) pack_kernel(Fetch fetch, int64_t rows_tot
             const int kbl = rest / (KC * (ROWS / 8));
             const int r = rg * 8 + r8;
             uint32_t lo[16], hi[16];
-            bool any_nar = false;
             const CodeT* tr = tile + r * LD + kbl * KB + kc * 16;
-            uint32_t wv[16 * sizeof(CodeT) / 4];
+            constexpr int NW = int(16 * sizeof(CodeT) / 4);
+            uint32_t wv[NW];
 #pragma unroll
-            for (int w = 0; w < int(16 * sizeof(CodeT) / 4); ++w)
-                wv[w] = reinterpret_cast<const uint32_t*>(tr)[w];
+            for (int w = 0; w < NW; ++w) wv[w] = reinterpret_cast<const uint32_t*>(tr)[w];
+            // NaR codes, word-wise: a zero byte / halfword of (codes ^ NaR pattern)
+            // (exact zero-lane test: (x - 1s) & ~x & msbs != 0 iff some lane of x is 0)
+            uint32_t narm = 0;
+            {
+                constexpr uint32_t ones = sizeof(CodeT) == 1 ? 0x01010101u : 0x00010001u;
+                constexpr uint32_t msbs = sizeof(CodeT) == 1 ? 0x80808080u : 0x80008000u;
+                const uint32_t cmask = ((1u << f.nbits) - 1u) * ones;
+                const uint32_t narw = nar_code * ones;
 #pragma unroll
-            for (int j = 0; j < 16; ++j) {
-                const uint32_t code = sizeof(CodeT) == 1 ? (wv[j >> 2] >> (8 * (j & 3))) & 0xFFu
-                                                         : (wv[j >> 1] >> (16 * (j & 1))) & 0xFFFFu;
-                if (use_lut) {
-                    lo[j] = lut[2 * code];
-                    hi[j] = D > 4 ? lut[2 * code + 1] : 0u;
-                    any_nar |= code == nar_code;
-                } else if (glut != nullptr) {  // 11-16-bit formats: L2-resident table
-                    const uint2 v = __ldg(glut + code);
+                for (int w = 0; w < NW; ++w) {
+                    const uint32_t x = (wv[w] & cmask) ^ narw;
+                    narm |= (x - ones) & ~x & msbs;
+                }
+            }
+            const bool any_nar = narm != 0;
+            auto code_of = [&](int j) -> uint32_t {
+                return sizeof(CodeT) == 1 ? (wv[j >> 2] >> (8 * (j & 3))) & 0xFFu
+                                          : (wv[j >> 1] >> (16 * (j & 1))) & 0xFFFFu;
+            };
+            // (one straight-line loop per decode source: no per-code branches)
+            if (use_lut) {
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    const uint32_t code = code_of(j);
+                    if constexpr (D > 4) {
+                        const uint2 v = reinterpret_cast<const uint2*>(lut)[code];
+                        lo[j] = v.x;
+                        hi[j] = v.y;
+                    } else {
+                        lo[j] = lut[2 * code];
+                        hi[j] = 0u;
+                    }
+                }
+            } else if (glut != nullptr) {  // 11-16-bit formats: L2-resident table
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    const uint2 v = __ldg(glut + code_of(j));
                     lo[j] = v.x;
                     hi[j] = v.y;
-                    any_nar |= code == nar_code;
-                } else {
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
                     bool nar;
-                    digit_words<D>(code, f, lo[j], hi[j], nar);
-                    any_nar |= nar;
+                    digit_words<D>(code_of(j), f, lo[j], hi[j], nar);
                 }
             }
             if (any_nar && r0 + r < rows_total) {
@@ -332,6 +361,243 @@ __global__ void __launch_bounds__(256) pack_kernel(Fetch fetch, int64_t rows_tot
                                           r8 * 16) = v;
             }
         }
+    }
+}
+
+// The pack for operands that are plain matrices (FetchRowMajor / FetchColMajor
+// / the Linear layers' FetchRowsBias): no shared-memory tile and no block
+// barriers.  A thread owns 16-code units (one row x 16 consecutive k) of the
+// image, fetched straight from global memory --
+//   k contiguous (kVecK): 16-byte loads of the row; lanes (r8, kc, rg), so a
+//     warp reads whole 32-byte sectors and writes 512 contiguous image bytes;
+//   r contiguous (kVecR): one 4-byte load per k holding the codes of RPT = 2
+//     (16-bit) or 4 (8-bit) consecutive rows, i.e. RPT units per thread; lanes
+//     = consecutive row groups, so every request is full sectors (RPT = 1:
+//     scalar loads, for operands whose rows are not 4-byte aligned) --
+// and the NEXT step's codes are loaded before this step is digitised, so the
+// load latency hides under the (ALU-bound) digit arithmetic.  Same image,
+// NaR flags and wide flags as pack_kernel (tests: every GEMM / Linear test).
+template <int D, int ROWS, typename CodeT, class Fetch, int FMT = 0, int RPT = 1>
+__global__ void __launch_bounds__(256) pack_direct_kernel(Fetch fetch, int64_t rows_total, int64_t K,
+                                                          PositFmt f_arg, int8_t* __restrict__ img,
+                                                          uint8_t* __restrict__ nar_flags,
+                                                          uint8_t* __restrict__ any_nar_flag,
+                                                          uint32_t chunks, FastDiv fd_kbt,
+                                                          const uint2* __restrict__ glut,
+                                                          uint8_t* __restrict__ wide_flag = nullptr,
+                                                          int wide_planes = 0) {
+    static_assert(Fetch::kVecK || Fetch::kVecR, "plain-matrix operands only");
+    static_assert(RPT == 1 || (Fetch::kVecR && RPT * sizeof(CodeT) == 4), "row groups: 4-byte loads");
+    pdl_trigger();
+    pdl_wait();  // PDL: nothing above touches global memory (pdl.cuh)
+    const PositFmt f = fixed_fmt<FMT>(f_arg);
+    constexpr int KB = Geometry<D>::KB;
+    constexpr int KC = KB / 16;
+    constexpr int UPC = ROWS * KC / RPT;  // steps (units or row groups) per (tile, k-block) chunk
+    constexpr int CB = 8 * int(sizeof(CodeT));  // code bits in a word lane
+    // words per step: a unit's 16 codes packed, or one word per k (RPT rows each)
+    constexpr int NW = RPT == 1 ? int(16 * sizeof(CodeT) / 4) : 16;
+    constexpr int VE = 16 / int(sizeof(CodeT));
+    // Shared-memory digit table (formats up to 10 bits).  8-bit codes with
+    // D <= 4 (one digit word per code): 32 copies, entry (code, lane) at word
+    // code * 32 + lane, so a warp's 32 lookups of arbitrary codes hit 32
+    // different banks; otherwise {lo, hi} pairs per code.
+    constexpr bool kLaneLut = D <= 4 && sizeof(CodeT) == 1;
+    __shared__ __align__(8) uint32_t lut[kLaneLut ? 256 * 32 : (2 << kLutMaxBits)];
+    const bool use_lut = f.nbits <= kLutMaxBits;
+    if (use_lut) {
+        for (int c = threadIdx.x; c < (1 << f.nbits); c += blockDim.x) {
+            uint32_t lo, hi;
+            bool nar;
+            digit_words<D>(uint32_t(c), f, lo, hi, nar);
+            if constexpr (kLaneLut) {
+#pragma unroll
+                for (int l = 0; l < 32; ++l) lut[c * 32 + ((l + c) & 31)] = lo;  // (rotated: conflict-free stores)
+            } else {
+                lut[2 * c] = lo;
+                lut[2 * c + 1] = hi;
+            }
+        }
+        __syncthreads();
+    }
+    const uint32_t* lut_lane = lut + (threadIdx.x & 31);
+    const uint32_t nar_code = 1u << (f.nbits - 1);
+    const uint32_t total = chunks * uint32_t(UPC);  // < 2^31 (launcher)
+    const uint32_t stride = gridDim.x * blockDim.x;
+
+    // step g -> (chunk, first row in the tile, 16-code column)
+    auto locate = [&](uint32_t g, uint32_t& chunk, int& r, int& kc) {
+        chunk = g / uint32_t(UPC);
+        const int u = int(g % uint32_t(UPC));
+        if constexpr (Fetch::kVecK) {
+            kc = (u >> 3) % KC;
+            r = ((u >> 3) / KC) * 8 + (u & 7);
+        } else {
+            r = (u % (ROWS / RPT)) * RPT;
+            kc = u / (ROWS / RPT);
+        }
+    };
+    auto load = [&](uint32_t g, uint32_t (&wv)[NW]) {
+        uint32_t chunk, t, kb;
+        int r, kc;
+        locate(g, chunk, r, kc);
+        fd_kbt.divmod(chunk, t, kb);
+        const int64_t gr = int64_t(t) * ROWS + r, gk = int64_t(kb) * KB + kc * 16;
+        if constexpr (Fetch::kVecK) {
+#pragma unroll
+            for (int v = 0; v < NW / 4; ++v) {
+                const int64_t k0 = gk + v * VE;
+                const CodeT* src = gr < rows_total ? fetch.ptr(gr, k0) : nullptr;
+                if (src != nullptr && k0 + VE <= K && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+                    const uint4 q = __ldg(reinterpret_cast<const uint4*>(src));
+                    wv[4 * v] = q.x, wv[4 * v + 1] = q.y, wv[4 * v + 2] = q.z, wv[4 * v + 3] = q.w;
+                } else {
+#pragma unroll
+                    for (int w = 0; w < 4; ++w) {
+                        uint32_t acc = 0;
+#pragma unroll
+                        for (int j = 0; j < VE / 4; ++j) {
+                            const int64_t k = k0 + w * (VE / 4) + j;
+                            const uint32_t c = (gr < rows_total && k < K) ? fetch(gr, k) : 0u;
+                            acc |= c << (CB * j);
+                        }
+                        wv[4 * v + w] = acc;
+                    }
+                }
+            }
+        } else if constexpr (RPT > 1) {
+            // one aligned word per k: the codes of rows gr .. gr + RPT - 1
+            if (gr + RPT <= rows_total && gk + 16 <= K) {
+#pragma unroll
+                for (int j = 0; j < 16; ++j)
+                    wv[j] = __ldg(reinterpret_cast<const uint32_t*>(fetch.ptr(gr, gk + j)));
+            } else {
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    uint32_t acc = 0;
+#pragma unroll
+                    for (int i = 0; i < RPT; ++i) {
+                        const uint32_t c = (gr + i < rows_total && gk + j < K) ? fetch(gr + i, gk + j) : 0u;
+                        acc |= c << (CB * i);
+                    }
+                    wv[j] = acc;
+                }
+            }
+        } else {
+#pragma unroll
+            for (int w = 0; w < NW; ++w) {
+                uint32_t acc = 0;
+#pragma unroll
+                for (int j = 0; j < 16 / NW; ++j) {
+                    const int64_t k = gk + w * (16 / NW) + j;
+                    const uint32_t c = (gr < rows_total && k < K) ? fetch(gr, k) : 0u;
+                    acc |= c << (CB * j);
+                }
+                wv[w] = acc;
+            }
+        }
+    };
+
+    uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+    uint32_t cur[NW], nxt[NW];
+    if (g < total) load(g, cur);
+    for (; g < total; g += stride) {
+        const bool more = g + stride < total;  // (total + stride < 2^32)
+        if (more) load(g + stride, nxt);
+        uint32_t chunk;
+        int r0, kc;
+        locate(g, chunk, r0, kc);
+        // NaR codes, word-wise: the exactly-zero lanes of (codes ^ NaR pattern)
+        uint32_t narm = 0;
+        {
+            constexpr uint32_t ones = sizeof(CodeT) == 1 ? 0x01010101u : 0x00010001u;
+            constexpr uint32_t low = sizeof(CodeT) == 1 ? 0x7F7F7F7Fu : 0x7FFF7FFFu;
+            const uint32_t cmask = ((1u << f.nbits) - 1u) * ones;
+            const uint32_t narw = nar_code * ones;
+#pragma unroll
+            for (int w = 0; w < NW; ++w) {
+                const uint32_t x = (cur[w] & cmask) ^ narw;
+                narm |= ~(((x & low) + low) | x | low);
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) {
+            const int r = r0 + i;
+            auto code_of = [&](int j) -> uint32_t {
+                if constexpr (RPT > 1) return (cur[j] >> (CB * i)) & ((1u << CB) - 1u);
+                else
+                    return sizeof(CodeT) == 1 ? (cur[j >> 2] >> (8 * (j & 3))) & 0xFFu
+                                              : (cur[j >> 1] >> (16 * (j & 1))) & 0xFFFFu;
+            };
+            uint32_t lo[16], hi[16];
+            if (use_lut) {
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    const uint32_t code = code_of(j);
+                    if constexpr (kLaneLut) {
+                        lo[j] = lut_lane[code * 32];
+                        hi[j] = 0u;
+                    } else if constexpr (D > 4) {
+                        const uint2 v = reinterpret_cast<const uint2*>(lut)[code];
+                        lo[j] = v.x;
+                        hi[j] = v.y;
+                    } else {
+                        lo[j] = lut[2 * code];
+                        hi[j] = 0u;
+                    }
+                }
+            } else if (glut != nullptr) {  // 11-12-bit formats: process-lifetime table, L1-resident
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    const uint2 v = __ldg(glut + code_of(j));
+                    lo[j] = v.x;
+                    hi[j] = v.y;
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    bool nar;
+                    digit_words<D>(code_of(j), f, lo[j], hi[j], nar);
+                }
+            }
+            const uint32_t rowm = RPT == 1 ? narm : narm & (((1u << CB) - 1u) << (CB * i));
+            if (rowm != 0) {
+                uint32_t t, kb;
+                fd_kbt.divmod(chunk, t, kb);
+                const int64_t gr = int64_t(t) * ROWS + r;
+                if (gr < rows_total) {
+                    nar_flags[gr] = 1;
+                    *any_nar_flag = 1;
+                }
+            }
+            if (wide_flag != nullptr) {  // a digit plane >= wide_planes in use (digit bytes != 0)
+                const uint32_t mlo = wide_planes >= 4 ? 0u : ~0u << (8 * wide_planes);
+                const uint32_t mhi = wide_planes >= 4 ? ~0u << (8 * (wide_planes - 4)) : ~0u;
+                uint32_t o = 0;
+#pragma unroll
+                for (int j = 0; j < 16; ++j) o |= (lo[j] & mlo) | (hi[j] & mhi);
+                if (o && *reinterpret_cast<volatile uint8_t*>(wide_flag) == 0) *wide_flag = 1;  // read first: no same-address store storm
+            }
+            int8_t* dst = img + int64_t(chunk) * int64_t(D * ROWS * KB) + (r >> 3) * (8 * KB) + kc * 128 +
+                          (r & 7) * 16;
+#pragma unroll
+            for (int p = 0; p < D; ++p) {
+                const uint32_t* w = p < 4 ? lo : hi;
+                const uint32_t q = p & 3;
+                const uint32_t sel = q | ((q + 4) << 4);
+                uint4 v;
+                uint32_t* vv = reinterpret_cast<uint32_t*>(&v);
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj) {
+                    const uint32_t a = __byte_perm(w[4 * jj], w[4 * jj + 1], sel);
+                    const uint32_t b = __byte_perm(w[4 * jj + 2], w[4 * jj + 3], sel);
+                    vv[jj] = __byte_perm(a, b, 0x5410);
+                }
+                *reinterpret_cast<uint4*>(dst + p * (ROWS * KB)) = v;
+            }
+        }
+#pragma unroll
+        for (int w = 0; w < NW; ++w) cur[w] = nxt[w];
     }
 }
 
@@ -1052,6 +1318,24 @@ inline bool encode_rows256(CUtensorMap* m, const void* base, size_t bytes, int b
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// Digit words of every code of f, for the life of the process (tables.h; the
+// key and contents of igemm.cu's table for the same (D, f -> f)).
+template <int D>
+inline const uint32_t* pack_digit_table(const PositFmt& f, cudaStream_t st) {
+    return static_cast<const uint32_t*>(persistent_table(
+        table_key(1, D, f.nbits, f.es, f.nbits, f.es), (size_t(2) << f.nbits) * 4, st,
+        [&](void* p, cudaStream_t s) { digit_lut_kernel<D><<<16, 256, 0, s>>>(f, static_cast<uint32_t*>(p)); }));
+}
+
+// PNN_DIRECT_PACK=0: the shared-memory-tile pack for plain matrices too (A/B experiments)
+inline bool direct_pack_enabled() {
+    static const bool on = [] {
+        const char* v = getenv("PNN_DIRECT_PACK");
+        return v == nullptr || v[0] != '0';
+    }();
+    return on;
+}
+
 template <int D, typename CodeT, class FA, class FB>
 cudaError_t launch_generic(const QuireGemmPlan& p, const GemmArgs& g, FA fa, FB fb,
                            OutMap<CodeT> out, uint8_t* ws, cudaStream_t st,
@@ -1086,21 +1370,74 @@ cudaError_t launch_generic(const QuireGemmPlan& p, const GemmArgs& g, FA fa, FB 
     const bool reduced = ((D == 6 || D == 8) && sizeof(CodeT) == 2 || D == 4 && sizeof(CodeT) == 1) &&
                          !p.pair && g.M * g.N * g.K >= variant_min_work();  // the extra launch pays off
     const int ga = int(a_work < 148 * 8 ? a_work : 148 * 8), gb = int(b_work < 148 * 8 ? b_work : 148 * 8);
-    if (D == 8 && sizeof(CodeT) == 2 && fixed_fmt_id(f) == 4) {  // posit(16,1): compile-time decode
-        launch_pdl(pack_kernel<D, kBM, CodeT, FA, 4>, dim3(ga), dim3(256), 0, st, fa, g.M, g.K, f, a_img, rnar, flags,
-                                                               p.mtiles_alloc, p.kbt, glut,
-                                                               reduced ? flags + 2 : nullptr, kRed);
-        if (g.pack_b)
-            launch_pdl(pack_kernel<D, Geo::NT, CodeT, FB, 4>, dim3(gb), dim3(256), 0, st, fb, g.N, g.K, f, b_img, cnar, flags + 1,
-                                                                       p.ntiles, p.kbt, glut,
-                                                                       reduced ? flags + 3 : nullptr, kRed);
+    // plain-matrix operands (GEMM entry, Linear layers): barrier-free direct pack
+    const int64_t a_units = a_work * int64_t(kBM) * (Geo::KB / 16), b_units = b_work * int64_t(Geo::NT) * (Geo::KB / 16);
+    constexpr bool kDirectA = FA::kVecK || FA::kVecR, kDirectB = FB::kVecK || FB::kVecR;
+    const bool direct = direct_pack_enabled() && a_units < (int64_t(1) << 31) - 148 * 8 * 256 &&
+                        b_units < (int64_t(1) << 31) - 148 * 8 * 256;
+    // one resident wave: whole multiples of the kernel's blocks per SM
+    auto dgrid = [](int64_t units, auto kern) {
+        int per_sm = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0) != cudaSuccess || per_sm < 1)
+            per_sm = 4;
+        const int64_t b = (units + 255) / 256, cap = int64_t(num_sms()) * per_sm;
+        return int(b < cap ? b : cap);
+    };
+    const bool f161 = D == 8 && sizeof(CodeT) == 2 && fixed_fmt_id(f) == 4;  // posit(16,1): compile-time decode
+    // 11-12-bit formats: the process-lifetime digit table (32 KB: L1-resident
+    // lookups instead of ~30 ALU instructions per code); null while capturing
+    // before it exists -> the in-register decode, same digits
+    const uint2* dlut = (direct && f.nbits > kLutMaxBits && f.nbits <= 12)
+                            ? reinterpret_cast<const uint2*>(pack_digit_table<D>(f, st))
+                            : nullptr;
+    bool a_done = false, b_done = !g.pack_b;
+    constexpr int kRows4 = 4 / int(sizeof(CodeT));  // rows per 4-byte load (r-contiguous operands)
+    auto launch_direct = [&](auto fx, auto rows_c, int64_t rows, int8_t* dimg, uint8_t* dnar, uint8_t* dany,
+                             int64_t work, int64_t units, uint8_t* wflag) {
+        using FX = decltype(fx);
+        constexpr int RW = decltype(rows_c)::value;
+        constexpr int kF = D == 8 ? 4 : 0;
+        void (*k)(FX, int64_t, int64_t, PositFmt, int8_t*, uint8_t*, uint8_t*, uint32_t, FastDiv, const uint2*,
+                  uint8_t*, int) = f161 ? pack_direct_kernel<D, RW, CodeT, FX, kF, 1> : pack_direct_kernel<D, RW, CodeT, FX, 0, 1>;
+        int64_t steps = units;
+        if constexpr (FX::kVecR) {
+            // rows of 4-byte-aligned length from a 4-byte-aligned base: row groups per load
+            if (fx.ld % kRows4 == 0 && (reinterpret_cast<uintptr_t>(fx.p) & 3) == 0) {
+                k = f161 ? pack_direct_kernel<D, RW, CodeT, FX, kF, kRows4> : pack_direct_kernel<D, RW, CodeT, FX, 0, kRows4>;
+                steps = units / kRows4;
+            }
+        }
+        launch_pdl(k, dim3(dgrid(steps, k)), dim3(256), 0, st, fx, rows, g.K, f, dimg, dnar, dany, uint32_t(work),
+                   FastDiv(uint32_t(p.kbt)), dlut, wflag, kRed);
+    };
+    if constexpr (kDirectA) {
+        if (direct) {
+            launch_direct(fa, std::integral_constant<int, kBM>{}, g.M, a_img, rnar, flags, a_work, a_units,
+                          reduced ? flags + 2 : nullptr);
+            a_done = true;
+        }
+    }
+    if constexpr (kDirectB) {
+        if (direct && !b_done) {
+            launch_direct(fb, std::integral_constant<int, Geo::NT>{}, g.N, b_img, cnar, flags + 1, b_work, b_units,
+                          reduced ? flags + 3 : nullptr);
+            b_done = true;
+        }
+    }
+    if (f161) {
+        if (!a_done)
+            launch_pdl(pack_kernel<D, kBM, CodeT, FA, 4>, dim3(ga), dim3(256), 0, st, fa, g.M, g.K, f, a_img, rnar, flags,
+                       p.mtiles_alloc, p.kbt, glut, reduced ? flags + 2 : nullptr, kRed);
+        if (!b_done)
+            launch_pdl(pack_kernel<D, Geo::NT, CodeT, FB, 4>, dim3(gb), dim3(256), 0, st, fb, g.N, g.K, f, b_img, cnar,
+                       flags + 1, p.ntiles, p.kbt, glut, reduced ? flags + 3 : nullptr, kRed);
     } else {
-        launch_pdl(pack_kernel<D, kBM, CodeT, FA>, dim3(ga), dim3(256), 0, st, fa, g.M, g.K, f, a_img, rnar, flags, p.mtiles_alloc,
-                                                           p.kbt, glut, reduced ? flags + 2 : nullptr, kRed);
-        if (g.pack_b)
-            launch_pdl(pack_kernel<D, Geo::NT, CodeT, FB>, dim3(gb), dim3(256), 0, st, fb, g.N, g.K, f, b_img, cnar, flags + 1,
-                                                                   p.ntiles, p.kbt, glut,
-                                                                   reduced ? flags + 3 : nullptr, kRed);
+        if (!a_done)
+            launch_pdl(pack_kernel<D, kBM, CodeT, FA>, dim3(ga), dim3(256), 0, st, fa, g.M, g.K, f, a_img, rnar, flags,
+                       p.mtiles_alloc, p.kbt, glut, reduced ? flags + 2 : nullptr, kRed);
+        if (!b_done)
+            launch_pdl(pack_kernel<D, Geo::NT, CodeT, FB>, dim3(gb), dim3(256), 0, st, fb, g.N, g.K, f, b_img, cnar,
+                       flags + 1, p.ntiles, p.kbt, glut, reduced ? flags + 3 : nullptr, kRed);
     }
     if (stats) cudaEventRecord(stats->ev[1], st);
     // D <= 3 implies R <= 11, hence W <= 64: no 128-bit instantiation needed.
