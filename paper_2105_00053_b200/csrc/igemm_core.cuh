@@ -229,7 +229,12 @@ __global__ void __launch_bounds__(ImplGeo<D, NT_, CPS, ACC, DA, DB>::THREADS, CP
             // ===== producer: TMA tile boxes (the im2col gather) =====
             // Slice layout: every box row is a run of pixels x 16 channel bytes,
             // contiguous in HBM (up to 2 KB), so a stage is a few dozen requests.
-            uint32_t it = 0;
+            // The stage index / phase and the k-block's tap / chunk / pixel-block
+            // coordinates are running counters (one division set per tile, none
+            // per k-block): this single thread's instruction chain, not the TMA
+            // unit, paced the short K loops of the convolution tiles.
+            int s = 0;
+            uint32_t ph = 0;
             for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
                 int64_t split, mt, nt;
                 itile_coords(t, a, split, mt, nt);
@@ -244,43 +249,63 @@ __global__ void __launch_bounds__(ImplGeo<D, NT_, CPS, ACC, DA, DB>::THREADS, CP
                         n0 = int(mt) * a.imgs_per_tile;
                     }
                 }
-                for (int i = 0; i < nkb; ++i, ++it) {
-                    const int s = it % STAGES;
-                    const uint32_t ph = (it / STAGES) & 1;
+                // modes 0/1: k-block = (tap (ky, kx), 32-channel chunk cc)
+                int cc = 0, kx = 0, ky = 0;
+                // mode 2: k-block = (image n, pixel-row block yb, pixel-column block xb);
+                // the m-tile's (ky, kx group, channel group) is fixed per tile
+                int wn = 0, wy = 0, wx = 0, mky = 0, mkg = 0, mcg = 0;
+                if constexpr (MODE != 2) {
+                    const int tap = int(kb0) / a.cch;
+                    cc = int(kb0) - tap * a.cch;
+                    ky = tap / a.KW;
+                    kx = tap - ky * a.KW;
+                } else {
+                    wn = int(kb0) / a.kpi;
+                    const int r = int(kb0) - wn * a.kpi;
+                    wy = r / a.kpr;
+                    wx = r - wy * a.kpr;
+                    const int kc = a.kgroups * a.cgroups;
+                    mky = int(mt) / kc;
+                    mkg = (int(mt) % kc) / a.cgroups;
+                    mcg = int(mt) % a.cgroups;
+                }
+                const int kpc = MODE == 2 ? a.kpi / a.kpr : 0;  // pixel-row blocks per image
+                for (int i = 0; i < nkb; ++i) {
                     ptx::mbar_wait(&empty[s], ph ^ 1);
                     uint8_t* sa = smem + s * Geo::STAGE_BYTES;
                     uint8_t* sb = sa + Geo::A_BYTES;
+                    uint64_t* fb = &full[s];
+                    if (++s == STAGES) s = 0, ph ^= 1;
                     if (a.debug & 4) {  // profiling: no operand traffic
-                        ptx::mbar_arrive(&full[s]);
+                        ptx::mbar_arrive(fb);
                         continue;
                     }
-                    ptx::mbar_arrive_expect_tx(&full[s], Geo::STAGE_BYTES);
-                    const int kb = int(kb0 + i);
+                    ptx::mbar_arrive_expect_tx(fb, Geo::STAGE_BYTES);
                     if constexpr (MODE != 2) {
                         // A box {w, h, n, 2 slices, D} -> [D][2][pixels][16 B]
-                        const int tap = kb / a.cch, cc = kb - tap * a.cch;
-                        const int ky = tap / a.KW, kx = tap - ky * a.KW;
                         if constexpr (MODE == 0)  // apad: zero ring stored around the digits
                             ptx::tma_load_5d(sa, &tmA, 2 * (kx - a.pad + a.apad), y0 + ky - a.pad + a.apad,
-                                             n0, 2 * cc, 0, &full[s]);
+                                             n0, 2 * cc, 0, fb);
                         else
-                            ptx::tma_load_5d(sa, &tmA, 2 * (a.pad - kx), y0 + a.pad - ky, n0, 2 * cc, 0,
-                                             &full[s]);
+                            ptx::tma_load_5d(sa, &tmA, 2 * (a.pad - kx), y0 + a.pad - ky, n0, 2 * cc, 0, fb);
                         // B box {NT rows, D, 2 slices} -> [2][D][NT][16 B]
-                        ptx::tma_load_3d(sb, &tmB, 2 * int(nt) * NT, 0, 2 * kb, &full[s]);
+                        ptx::tma_load_3d(sb, &tmB, 2 * int(nt) * NT, 0, 2 * int(kb0 + i), fb);
+                        if (++cc == a.cch) {
+                            cc = 0;
+                            if (++kx == a.KW) kx = 0, ++ky;
+                        }
                     } else {
-                        const int n = kb / a.kpi, r = kb - n * a.kpi;
-                        const int yb = (r / a.kpr) * a.OHb, xb = (r % a.kpr) * a.OWb;
-                        const int kc = a.kgroups * a.cgroups;
-                        const int ky = int(mt) / kc, kg = (int(mt) % kc) / a.cgroups,
-                                  cg = int(mt) % a.cgroups;
+                        const int yb = wy * a.OHb, xb = wx * a.OWb;
                         // A: ONE box {pixels, rows, 4 kx taps, 2 slices, D} of the
                         // zero-padded x digits; the kx dimension is an overlapping view
                         // (stride = one 16-byte pixel) -> [D][2][4][OHb][OWb][16 B]
-                        ptx::tma_load_5d(sa, &tmA, 2 * (xb + 4 * kg), n * a.Hp + yb + ky, 0, 2 * cg, 0,
-                                         &full[s]);
+                        ptx::tma_load_5d(sa, &tmA, 2 * (xb + 4 * mkg), wn * a.Hp + yb + mky, 0, 2 * mcg, 0, fb);
                         // B box {pixels, rows, 1, NT/16 slices, D} -> [D][NT/16][32][16 B]
-                        ptx::tma_load_5d(sb, &tmB, 2 * xb, yb, n, int(nt) * (NT / 16), 0, &full[s]);
+                        ptx::tma_load_5d(sb, &tmB, 2 * xb, yb, wn, int(nt) * (NT / 16), 0, fb);
+                        if (++wx == a.kpr) {
+                            wx = 0;
+                            if (++wy == kpc) wy = 0, ++wn;
+                        }
                     }
                 }
             }
@@ -292,7 +317,9 @@ __global__ void __launch_bounds__(ImplGeo<D, NT_, CPS, ACC, DA, DB>::THREADS, CP
             // all-zero A operand for initialising groups D-1 .. 2D-2; footprint <= 4 KB
             const uint64_t zdesc = MODE == 2 ? ptx::smem_desc_kmajor(ptx::smem_u32(zero_tile), 128, 512)
                                              : ptx::smem_desc_kmajor(ptx::smem_u32(zero_tile), 128, 256);
-            uint32_t it = 0, j = 0;
+            uint32_t j = 0, ph = 0;
+            int s = 0;
+            const uint32_t smem0 = ptx::smem_u32(smem);
             for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++j) {
                 int64_t split, mt, nt;
                 itile_coords(t, a, split, mt, nt);
@@ -303,12 +330,12 @@ __global__ void __launch_bounds__(ImplGeo<D, NT_, CPS, ACC, DA, DB>::THREADS, CP
                 ptx::mbar_wait(&tmem_empty[buf], (jb & 1) ^ 1);
                 ptx::tc_fence_after();
                 const uint32_t tacc = tmem + buf * Geo::ACC_STRIDE;
-                for (int i = 0; i < nkb; ++i, ++it) {
-                    const int s = it % STAGES;
-                    const uint32_t ph = (it / STAGES) & 1;
+                for (int i = 0; i < nkb; ++i) {
                     ptx::mbar_wait(&full[s], ph);
                     ptx::tc_fence_after();
-                    const uint32_t a_base = ptx::smem_u32(smem + s * Geo::STAGE_BYTES);
+                    const uint32_t a_base = smem0 + s * Geo::STAGE_BYTES;
+                    uint64_t* eb = &empty[s];
+                    if (++s == STAGES) s = 0, ph ^= 1;
                     const uint32_t b_base = a_base + Geo::A_BYTES;
                     // K-major: LBO = next 16 K bytes (next slice), SBO = next 8 rows (128 B).
                     // MN-major: LBO = next 8 K rows (128 B), SBO = next 16-wide MN atom.
@@ -331,7 +358,7 @@ __global__ void __launch_bounds__(ImplGeo<D, NT_, CPS, ACC, DA, DB>::THREADS, CP
                         if (!(a.debug & 2))
                             ptx::mma_i8(tacc + p * NT, adesc, bdesc, idesc, (first && p == 0) ? 0u : 1u);
                     }
-                    ptx::mma_commit(&empty[s]);
+                    ptx::mma_commit(eb);
                 }
                 ptx::mma_commit(&tmem_full[buf]);
             }

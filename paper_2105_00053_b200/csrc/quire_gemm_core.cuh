@@ -817,9 +817,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     pdl_wait();
     // device-selected variant (vflags = {A wide, B wide} from the pack kernels):
     // vmode 1 runs iff neither operand is wide, 2 iff either is; exit at once otherwise
-    if (vmode != 0) {
+    if ((vmode & 0xFF) != 0) {
         const bool wide = vflags[0] != 0 || vflags[1] != 0;
-        if (wide != (vmode == 2)) return;
+        if (wide != ((vmode & 0xFF) == 2)) return;
     }
     if (warp == 1) {
         if constexpr (kPair) ptx::tmem_alloc2<Geo::TMEM_COLS>(tmem_slot);
@@ -940,7 +940,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                     uint32_t r[GB][8];
 #pragma unroll
                     for (int g = 0; g < GB; ++g)
-                        if (g0 + g < G) ptx::tmem_ld8(trow + (g0 + g) * NT + 2 * c0, r[g]);
+                        if (g0 + g < G) {
+#ifdef PNN_GEMM_DEBUG_HOOKS  // profiling (tools/probes/gemm_drain.sh): no TMEM loads
+                            if (vmode & 0x100) {
+                                for (int x = 0; x < 8; ++x) r[g][x] = 0;
+                                continue;
+                            }
+#endif
+                            ptx::tmem_ld8(trow + (g0 + g) * NT + 2 * c0, r[g]);
+                        }
                     ptx::tmem_wait_ld();
 #pragma unroll
                     for (int g = 0; g < GB; ++g)
@@ -960,6 +968,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 
             const int64_t row = mt * kBM + quarter * 32 + lane;
             if (row >= M) continue;
+#ifdef PNN_GEMM_DEBUG_HOOKS  // profiling: no rounding, no stores
+            if (vmode & 0x200) continue;
+#endif
             const bool rnar = row_nar != nullptr && row_nar[row] != 0;
             const int64_t colbase = nt * NT + half * 8;  // + 2 * c0 for chunk c0 / 8
 #pragma unroll
@@ -1327,6 +1338,17 @@ inline const uint32_t* pack_digit_table(const PositFmt& f, cudaStream_t st) {
         [&](void* p, cudaStream_t s) { digit_lut_kernel<D><<<16, 256, 0, s>>>(f, static_cast<uint32_t*>(p)); }));
 }
 
+// PNN_GEMM_DEBUG (profiling builds with -DPNN_GEMM_DEBUG_HOOKS): 1 = no TMEM
+// loads in the epilogue, 2 = no rounding / stores; results are then garbage
+inline int gemm_debug_bits() {
+#ifdef PNN_GEMM_DEBUG_HOOKS
+    const char* v = getenv("PNN_GEMM_DEBUG");
+    return v ? (atoi(v) & 3) << 8 : 0;
+#else
+    return 0;
+#endif
+}
+
 // PNN_DIRECT_PACK=0: the shared-memory-tile pack for plain matrices too (A/B experiments)
 inline bool direct_pack_enabled() {
     static const bool on = [] {
@@ -1526,7 +1548,7 @@ cudaError_t launch_generic(const QuireGemmPlan& p, const GemmArgs& g, FA fa, FB 
         }
         launch_pdl(kern, dim3(grid), dim3(kThreads), Geo::SMEM, st, a_img, b_img, p.kbt, p.kb_per_split, rn, cn, out,
                                                 g.M, g.N, f, partial, p.mtiles, p.ntiles, p.splits,
-                                                reduced ? flags + 2 : nullptr, reduced ? 2 : 0, tmA, tmB);
+                                                reduced ? flags + 2 : nullptr, (reduced ? 2 : 0) | gemm_debug_bits(), tmA, tmB);
     }
     if (stats) cudaEventRecord(stats->ev[2], st);
     if (use_partial) {
