@@ -114,6 +114,34 @@ __device__ __forceinline__ uint32_t q_to_posit_lut_f64(const PositFmt& f, uint64
     return v == 0 ? 0u : c;
 }
 
+// The same conversion with what the caller knows folded in:
+//  * kNoWrap: q already is the exact value (the pass's |sum| bound is below
+//    2^(W-1)), so no sign extension from W bits;
+//  * kRelu: the caller stores relu(code) only: negative values and zero give 0,
+//    so the rounding runs on the magnitude path alone (the sign of a nonzero
+//    converted integer is the sign of the double's high word; zero has hi == 0);
+//  * a value of 2^53 or more saturates to +-maxpos whenever 3R <= 52 (maxpos =
+//    2^R is 2^(3R) quire units), so the dropped-bit check is skipped there.
+// Same codes as q_to_posit_lut_f64 (tests/test_epilogue_gpu.py, conv tests).
+template <bool kRelu, bool kNoWrap>
+__device__ __forceinline__ uint32_t q_to_posit_lut_f64x(const PositFmt& f, uint64_t q, const uint4* lut) {
+    int64_t v = int64_t(q);
+    if (!kNoWrap && f.W < 64) v = (v << (64 - f.W)) >> (64 - f.W);
+    const double d = __ll2double_rz(v);
+    const uint32_t hi = uint32_t(__double2hiint(d)), lo = uint32_t(__double2loint(d));
+    const bool lost = 3 * f.R > 52 && __double2ll_rz(d) != v;
+    const int top = int((hi >> 20) & 0x7FFu) - 1023;
+    const uint32_t sig = 0x80000000u | ((hi & 0xFFFFFu) << 11) | (lo >> 21);
+    const bool sticky = (lo & 0x1FFFFFu) != 0 || lost;
+    if constexpr (kRelu) {
+        const uint32_t c = pack_lut(f, lut, top - 2 * f.R, sig, sticky, false);
+        return int32_t(hi) > 0 ? c : 0u;
+    } else {
+        const uint32_t c = pack_lut(f, lut, top - 2 * f.R, sig, sticky, (hi >> 31) != 0);
+        return hi == 0 ? 0u : c;
+    }
+}
+
 // 128-bit word as four 32-bit limbs (sign extension from W bits, |q| by xor +
 // carry chain, leading limb selected, top 32 bits by one funnel shift).
 __device__ __forceinline__ uint32_t q_to_posit_lut(const PositFmt& f, unsigned __int128 q,

@@ -5,6 +5,7 @@
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
+#include <cmath>
 #include <cstdint>
 #include <cstdlib>
 
@@ -334,6 +335,21 @@ constexpr int acc_of() { return 1; }
 template <int MODE, int D>
 constexpr int nt_of() { return cps_of<MODE, D>() == 2 ? small_nt(D) : TileCfg<D>::NT; }
 
+// PNN_IGEMM_ACC2=1: the reduced-digit forward / input-gradient kernels as ONE CTA
+// per SM with two TMEM accumulator buffers and 16 epilogue warps (instead of
+// two single-buffer CTAs): the MMA thread runs a whole tile ahead of the epilogue
+inline bool igemm_acc2() {
+    static const bool on = [] {
+        const char* v = getenv("PNN_IGEMM_ACC2");
+        return v != nullptr && v[0] == '1';
+    }();
+    return on;
+}
+
+template <int D, typename CodeT, int MODE, int DA, int OFF, int DB, int QWF, int NTT, int CPS, int ACC>
+cudaError_t launch_kernel_geo(const CUtensorMap& tA, const CUtensorMap& tB, const IgemmArgs& a,
+                              OutMap<CodeT> out, cudaStream_t st);
+
 template <int D, typename CodeT, int MODE, int DA = D, int OFF = 0, int DB = D, int QWF = 0>
 cudaError_t launch_kernel(const CUtensorMap& tA, const CUtensorMap& tB, const IgemmArgs& a,
                           OutMap<CodeT> out, cudaStream_t st) {
@@ -342,8 +358,26 @@ cudaError_t launch_kernel(const CUtensorMap& tA, const CUtensorMap& tB, const Ig
     constexpr bool kPairSM = DB < D && (DA + DB - 1) * 32 <= 256;
     constexpr int NTT = kPairSM ? 32 : nt_of<MODE, D>();
     constexpr int CPS = kPairSM ? 2 : cps_of<MODE, D>(), ACC = acc_of<MODE, D>();
+    if constexpr (kPairSM && MODE != 2)
+        if (igemm_acc2()) return launch_kernel_geo<D, CodeT, MODE, DA, OFF, DB, QWF, NTT, 1, 2>(tA, tB, a, out, st);
+    return launch_kernel_geo<D, CodeT, MODE, DA, OFF, DB, QWF, NTT, CPS, ACC>(tA, tB, a, out, st);
+}
+
+template <int D, typename CodeT, int MODE, int DA, int OFF, int DB, int QWF, int NTT, int CPS, int ACC>
+cudaError_t launch_kernel_geo(const CUtensorMap& tA, const CUtensorMap& tB, const IgemmArgs& a_in,
+                              OutMap<CodeT> out, cudaStream_t st) {
     using Geo = ImplGeo<D, NTT, CPS, ACC, DA, DB>;
     void (*k)(CUtensorMap, CUtensorMap, IgemmArgs, OutMap<CodeT>);
+    IgemmArgs a = a_in;
+    // 64-bit words of a W < 64 quire: with DA / DB-digit operands (|X| <= 128 *
+    // (256^D - 1) / 255) the exact sum of K products (+ the bias term) stays
+    // below 2^(W-1) for short K -- then the word is the value, no wrap to undo
+    {
+        const double ma = std::log2(128.0 * (std::pow(256.0, DA) - 1.0) / 255.0);
+        const double mb = std::log2(128.0 * (std::pow(256.0, DB) - 1.0) / 255.0);
+        const double k_terms = double(a.kbt) * kIKB + 1.0;
+        a.nowrap = (MODE != 2 && a.f.W < 64 && ma + mb + std::log2(k_terms) < double(a.f.W - 1) - 0.01) ? 1 : 0;
+    }
     const int fid = fixed_fmt_id(a.f);
     if constexpr (QWF != 0) {  // quire word forced by the caller (reduced-digit variants)
         k = igemm_kernel<D, NTT, CPS, ACC, QWF, CodeT, MODE, 0, DA, OFF, DB>;

@@ -71,7 +71,7 @@ struct ImplGeo {
     // ACC = 2: two accumulator buffers (at columns 0 and 256): tile t+1's MMAs
     // run while the epilogue drains and rounds tile t.
     static constexpr int ACC_STRIDE = 256;
-    static constexpr int EPI = (CPS == 2 || ACC == 2) ? 8 : 16;  // epilogue warps
+    static constexpr int EPI = CPS == 2 ? 8 : 16;  // epilogue warps
     static constexpr int THREADS = 64 + 32 * EPI;
     static_assert(G * NT <= (ACC == 2 ? ACC_STRIDE : int(TMEM_COLS)), "TMEM overflow");
     static_assert(ACC == 1 || CPS == 1, "double buffering needs the whole TMEM");
@@ -101,6 +101,7 @@ struct IgemmArgs {
     const uint8_t* vflag2;
     int vexpect2;
     int vor;               // 1: run iff (*vflag | *vflag2 != 0) == vexpect
+    int nowrap;     // 64-bit quire words: |sum| < 2^(W-1) for this pass, q is the exact value
     int relu;       // mode 0: output relu(y) (ReLU layer fused) ...
     void* pre_out;  // ... and, if non-null, the pre-activation y here (same layout)
     // tile raster (tile_coords) with launch-constant divisions: by mtiles * ntiles,
@@ -452,13 +453,37 @@ __global__ void __launch_bounds__(ImplGeo<D, NT_, CPS, ACC, DA, DB>::THREADS, CP
                                         ? *reinterpret_cast<const uint64_t*>(a.col_nar + col0)
                                         : 0ull;
                 uint32_t codes[8];
+#ifndef PNN_EPI_INT_ROUND
+                // relu(y) is the only output: magnitude-only rounding, NaR -> 0
+                const bool relu_only = MODE == 0 && QW == 2 && a.relu && a.pre_out == nullptr;
+                if (QW == 2 && relu_only && !PNN_EPI_DEBUG(1)) {
+                    if (a.nowrap) {
 #pragma unroll
-                for (int x = 0; x < 8; ++x) {
-                    const uint32_t c =
-                        PNN_EPI_DEBUG(1) ? uint32_t(q[c0 + x]) : epi_round(f, q[c0 + x], s_lut);
-                    codes[x] = ((cn >> (8 * x)) & 0xFF) ? (1u << (f.nbits - 1)) : c;
+                        for (int x = 0; x < 8; ++x)
+                            codes[x] = q_to_posit_lut_f64x<true, true>(f, uint64_t(q[c0 + x]), s_lut);
+                    } else {
+#pragma unroll
+                        for (int x = 0; x < 8; ++x)
+                            codes[x] = q_to_posit_lut_f64x<true, false>(f, uint64_t(q[c0 + x]), s_lut);
+                    }
+                    if (cn != 0) {  // (warp-uniform: the flags are per column)
+#pragma unroll
+                        for (int x = 0; x < 8; ++x)
+                            if ((cn >> (8 * x)) & 0xFF) codes[x] = 0u;
+                    }
+                } else
+#endif
+                {
+#pragma unroll
+                    for (int x = 0; x < 8; ++x)
+                        codes[x] = PNN_EPI_DEBUG(1) ? uint32_t(q[c0 + x]) : epi_round(f, q[c0 + x], s_lut);
+                    if (cn != 0) {  // (warp-uniform: the flags are per column)
+#pragma unroll
+                        for (int x = 0; x < 8; ++x)
+                            if ((cn >> (8 * x)) & 0xFF) codes[x] = 1u << (f.nbits - 1);
+                    }
                 }
-                if constexpr (MODE == 0) if (a.relu) {
+                if constexpr (MODE == 0) if (a.relu && !relu_only) {
                     // fused ReLU (the layer after the convolution):
                     // the pre-activation to pre_out when asked, relu(y) to the output
                     if (a.pre_out != nullptr) {

@@ -325,9 +325,45 @@ def test_fwd_reduced_digits(cuda, po, wide, shape):
     assert torch.equal(y, ref)
     yr, pre = ops.conv2d_fwd_layer(P81, x, w, b, 1, pad, None, relu=True, want_pre=True)
     assert torch.equal(pre, ref) and torch.equal(yr, ops.relu_fwd(P81, ref))
+    # relu(y) as the only output: the magnitude-only / no-wrap epilogue rounding
+    yo, none = ops.conv2d_fwd_layer(P81, x, w, b, 1, pad, None, relu=True, want_pre=False)
+    assert none is None and torch.equal(yo, yr)
     if N * H * W <= 128:
         want = po.conv2d(8, 1, xa, wa, ba, 1, pad)
         assert (host(y).reshape(want.shape) == want).all()
+
+
+@pytest.mark.parametrize("cfg", [P80, P81])
+@pytest.mark.parametrize("shape", [(2, 32, 8, 8, 32, 3, 1), (1, 64, 8, 8, 64, 3, 1)])
+def test_fwd_relu_only_extremes(cuda, po, cfg, shape):
+    """The relu-only epilogue on sums far beyond maxpos (|quire| >= 2^53, where
+    the FP64 conversion drops bits and the dropped-bit check is skipped because
+    the value saturates), on wrapped W-bit quires and on exact cancellations:
+    operands drawn from {+-maxpos, +-1, +-minpos, 0, NaR}.  Against the explicit
+    path and, on the small shape, the oracle."""
+    N, C, H, W, F, K, pad = shape
+    n = cfg[0]
+    maxpos, minpos, one, nar = (1 << (n - 1)) - 1, 1, 1 << (n - 2), 1 << (n - 1)
+    neg = lambda c: (-c) & ((1 << n) - 1)
+    pool = np.array([maxpos, neg(maxpos), one, neg(one), minpos, neg(minpos), 0, maxpos, neg(maxpos)], np.uint64)
+    rng = np.random.default_rng(n * 131 + C)
+    xa = pool[rng.integers(0, len(pool), (N, C, H, W))]
+    wa = pool[rng.integers(0, len(pool), (F, C, K, K))]
+    ba = pool[rng.integers(0, len(pool), (F,))]
+    xa[0, 3, 2, 2] = nar
+    x, w, b = dev(cfg, xa), dev(cfg, wa), dev(cfg, ba)
+    prev = ops.conv_algo(1)
+    try:
+        ref = ops.conv2d(cfg, x, w, b, 1, pad)
+    finally:
+        ops.conv_algo(prev)
+    yo, none = ops.conv2d_fwd_layer(cfg, x, w, b, 1, pad, None, relu=True, want_pre=False)
+    assert none is None and torch.equal(yo, ops.relu_fwd(cfg, ref))
+    y, pre = ops.conv2d_fwd_layer(cfg, x, w, b, 1, pad, None, relu=True, want_pre=True)
+    assert torch.equal(pre, ref) and torch.equal(y, yo)
+    if C <= 32:
+        want = po.conv2d(cfg[0], cfg[1], xa, wa, ba, 1, pad)
+        assert (host(pre).reshape(want.shape) == want).all()
 
 
 @pytest.mark.parametrize("cfg", [P121, P161])
