@@ -142,6 +142,47 @@ __device__ __forceinline__ uint32_t q_to_posit_lut_f64x(const PositFmt& f, uint6
     }
 }
 
+// 8-bit output formats: the whole of pack_lut tabulated.  pack_lut's result
+// depends on the significand only through its top FB = 6 - es fraction bits
+// (the bits that can reach the pattern or the guard position: head >= 2 + es)
+// and on whether anything below them is set, so
+//     code = tab[((scale index) * 2^FB + top FB fraction bits) * 2 + (rest != 0)]
+// with every entry computed by pack_lut itself (build_pack_tab8, after
+// build_pack_lut and a barrier).  (scale index, top bits) is one field of the
+// double's high word: (hi >> (20 - FB)) minus a constant, clamped -- the rows at
+// both ends are the constant minpos / maxpos saturations.
+constexpr int kTab8Bytes = kPackLutEntries * 64 * 2;
+__device__ __forceinline__ void build_pack_tab8(const PositFmt& f, const uint4* lut, uint8_t* tab, int tid,
+                                                int nthr) {
+    const int FB = 6 - f.es, rows = 2 * f.R + 2;
+    for (int i = tid; i < (rows << FB) * 2; i += nthr) {
+        const int st = i & 1, m = (i >> 1) & ((1 << FB) - 1), row = i >> (FB + 1);
+        const uint32_t sig = 0x80000000u | (uint32_t(m) << (31 - FB));
+        tab[i] = uint8_t(pack_lut(f, lut, row - 1 - f.R, sig, st != 0, false));
+    }
+}
+
+// 64-bit quire word -> 8-bit posit code through the FP64 converter and the
+// table (same codes as q_to_posit_lut_f64; flags as q_to_posit_lut_f64x).
+template <bool kRelu, bool kNoWrap>
+__device__ __forceinline__ uint32_t q_to_posit_tab8(const PositFmt& f, uint64_t q, const uint8_t* tab) {
+    int64_t v = int64_t(q);
+    if (!kNoWrap && f.W < 64) v = (v << (64 - f.W)) >> (64 - f.W);
+    const double d = __ll2double_rz(v);
+    const uint32_t hi = uint32_t(__double2hiint(d)), lo = uint32_t(__double2loint(d));
+    const int FB = 6 - f.es;
+    const bool lost = 3 * f.R > 52 && __double2ll_rz(d) != v;
+    const uint32_t mag = kRelu ? hi : (hi & 0x7FFFFFFFu);  // (relu: negative values are discarded)
+    // row = top - 2R + R + 1 with top = exponent - 1023
+    int idx = int(mag >> (20 - FB)) - ((1023 + f.R - 1) << FB);
+    const int last = ((2 * f.R + 2) << FB) - 1;
+    idx = idx < 0 ? 0 : (idx > last ? last : idx);
+    const uint32_t rest = (hi & ((1u << (20 - FB)) - 1u)) | lo | uint32_t(lost);
+    const uint32_t c = tab[2 * idx + int(rest != 0)];
+    if constexpr (kRelu) return int32_t(hi) > 0 ? c : 0u;
+    else return hi == 0 ? 0u : ((hi >> 31) ? ((0u - c) & ((1u << f.nbits) - 1u)) : c);
+}
+
 // 128-bit word as four 32-bit limbs (sign extension from W bits, |q| by xor +
 // carry chain, leading limb selected, top 32 bits by one funnel shift).
 __device__ __forceinline__ uint32_t q_to_posit_lut(const PositFmt& f, unsigned __int128 q,

@@ -185,6 +185,13 @@ __global__ void __launch_bounds__(ImplGeo<D, NT_, CPS, ACC, DA, DB>::THREADS, CP
     for (int i = threadIdx.x; i < kZeroBytes / 16; i += kIThreads)
         reinterpret_cast<int4*>(zero_tile)[i] = make_int4(0, 0, 0, 0);
     build_pack_lut(fixed_fmt<FMT>(a.f), s_lut, threadIdx.x, kIThreads);
+    // 8-bit outputs from 64-bit words: the rounding as one table (epilogue.cuh)
+    constexpr bool kTab8 = sizeof(CodeT) == 1 && QW == 2;
+    __shared__ uint8_t s_tab8[kTab8 ? kTab8Bytes : 1];
+    if constexpr (kTab8) {
+        __syncthreads();
+        build_pack_tab8(fixed_fmt<FMT>(a.f), s_lut, s_tab8, threadIdx.x, kIThreads);
+    }
     if (warp == 0 && lane == 0) {
         ptx::tma_prefetch_desc(&tmA);
         ptx::tma_prefetch_desc(&tmB);
@@ -460,11 +467,13 @@ __global__ void __launch_bounds__(ImplGeo<D, NT_, CPS, ACC, DA, DB>::THREADS, CP
                     if (a.nowrap) {
 #pragma unroll
                         for (int x = 0; x < 8; ++x)
-                            codes[x] = q_to_posit_lut_f64x<true, true>(f, uint64_t(q[c0 + x]), s_lut);
+                            codes[x] = kTab8 ? q_to_posit_tab8<true, true>(f, uint64_t(q[c0 + x]), s_tab8)
+                                             : q_to_posit_lut_f64x<true, true>(f, uint64_t(q[c0 + x]), s_lut);
                     } else {
 #pragma unroll
                         for (int x = 0; x < 8; ++x)
-                            codes[x] = q_to_posit_lut_f64x<true, false>(f, uint64_t(q[c0 + x]), s_lut);
+                            codes[x] = kTab8 ? q_to_posit_tab8<true, false>(f, uint64_t(q[c0 + x]), s_tab8)
+                                             : q_to_posit_lut_f64x<true, false>(f, uint64_t(q[c0 + x]), s_lut);
                     }
                     if (cn != 0) {  // (warp-uniform: the flags are per column)
 #pragma unroll
@@ -475,8 +484,13 @@ __global__ void __launch_bounds__(ImplGeo<D, NT_, CPS, ACC, DA, DB>::THREADS, CP
 #endif
                 {
 #pragma unroll
-                    for (int x = 0; x < 8; ++x)
-                        codes[x] = PNN_EPI_DEBUG(1) ? uint32_t(q[c0 + x]) : epi_round(f, q[c0 + x], s_lut);
+                    for (int x = 0; x < 8; ++x) {
+                        if constexpr (kTab8)
+                            codes[x] = PNN_EPI_DEBUG(1) ? uint32_t(q[c0 + x])
+                                                        : q_to_posit_tab8<false, false>(f, uint64_t(q[c0 + x]), s_tab8);
+                        else
+                            codes[x] = PNN_EPI_DEBUG(1) ? uint32_t(q[c0 + x]) : epi_round(f, q[c0 + x], s_lut);
+                    }
                     if (cn != 0) {  // (warp-uniform: the flags are per column)
 #pragma unroll
                         for (int x = 0; x < 8; ++x)
