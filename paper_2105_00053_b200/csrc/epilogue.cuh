@@ -151,7 +151,8 @@ __device__ __forceinline__ uint32_t q_to_posit_lut_f64x(const PositFmt& f, uint6
 // build_pack_lut and a barrier).  (scale index, top bits) is one field of the
 // double's high word: (hi >> (20 - FB)) minus a constant, clamped -- the rows at
 // both ends are the constant minpos / maxpos saturations.
-constexpr int kTab8Bytes = kPackLutEntries * 64 * 2;
+// (2R + 2) * 2^FB * 2 = (12 * 2^es + 2) * 2^(7 - es) <= 1792 entries for nbits <= 8
+constexpr int kTab8Bytes = 2048;
 __device__ __forceinline__ void build_pack_tab8(const PositFmt& f, const uint4* lut, uint8_t* tab, int tid,
                                                 int nthr) {
     const int FB = 6 - f.es, rows = 2 * f.R + 2;
@@ -181,6 +182,26 @@ __device__ __forceinline__ uint32_t q_to_posit_tab8(const PositFmt& f, uint64_t 
     const uint32_t c = tab[2 * idx + int(rest != 0)];
     if constexpr (kRelu) return int32_t(hi) > 0 ? c : 0u;
     else return hi == 0 ? 0u : ((hi >> 31) ? ((0u - c) & ((1u << f.nbits) - 1u)) : c);
+}
+
+// 32-bit quire word (W <= 32) -> 8-bit posit code: the same table through the
+// FP32 converter (24-bit significand, toward zero; a value of 2^24 or more
+// saturates whenever 3R <= 23, otherwise the dropped bits join the rest bit).
+template <bool kRelu>
+__device__ __forceinline__ uint32_t q32_to_posit_tab8(const PositFmt& f, uint32_t q, const uint8_t* tab) {
+    const int32_t v = f.W < 32 ? int32_t(q << (32 - f.W)) >> (32 - f.W) : int32_t(q);
+    const float fl = __int2float_rz(v);
+    const uint32_t bits = __float_as_uint(fl);
+    const int FB = 6 - f.es;
+    const bool lost = 3 * f.R > 23 && __float2int_rz(fl) != v;
+    const uint32_t mag = kRelu ? bits : (bits & 0x7FFFFFFFu);
+    int idx = int(mag >> (23 - FB)) - ((127 + f.R - 1) << FB);
+    const int last = ((2 * f.R + 2) << FB) - 1;
+    idx = idx < 0 ? 0 : (idx > last ? last : idx);
+    const uint32_t rest = (bits & ((1u << (23 - FB)) - 1u)) | uint32_t(lost);
+    const uint32_t c = tab[2 * idx + int(rest != 0)];
+    if constexpr (kRelu) return int32_t(bits) > 0 ? c : 0u;
+    else return bits == 0 ? 0u : ((bits >> 31) ? ((0u - c) & ((1u << f.nbits) - 1u)) : c);
 }
 
 // 128-bit word as four 32-bit limbs (sign extension from W bits, |q| by xor +

@@ -132,7 +132,7 @@ __device__ __forceinline__ void itile_coords(int64_t t64, const IgemmArgs& a, in
 // widths through the integer paths
 #ifndef PNN_EPI_INT_ROUND
 __device__ __forceinline__ uint32_t epi_round(const PositFmt& f, uint64_t q, const uint4* lut) {
-    return q_to_posit_lut_f64(f, q, lut);
+    return q_to_posit_lut_f64x<false, false>(f, q, lut);
 }
 #else
 __device__ __forceinline__ uint32_t epi_round(const PositFmt& f, uint64_t q, const uint4* lut) {
@@ -186,7 +186,7 @@ __global__ void __launch_bounds__(ImplGeo<D, NT_, CPS, ACC, DA, DB>::THREADS, CP
         reinterpret_cast<int4*>(zero_tile)[i] = make_int4(0, 0, 0, 0);
     build_pack_lut(fixed_fmt<FMT>(a.f), s_lut, threadIdx.x, kIThreads);
     // 8-bit outputs from 64-bit words: the rounding as one table (epilogue.cuh)
-    constexpr bool kTab8 = sizeof(CodeT) == 1 && QW == 2;
+    constexpr bool kTab8 = sizeof(CodeT) == 1 && QW <= 2;
     __shared__ uint8_t s_tab8[kTab8 ? kTab8Bytes : 1];
     if constexpr (kTab8) {
         __syncthreads();
@@ -462,8 +462,16 @@ __global__ void __launch_bounds__(ImplGeo<D, NT_, CPS, ACC, DA, DB>::THREADS, CP
                 uint32_t codes[8];
 #ifndef PNN_EPI_INT_ROUND
                 // relu(y) is the only output: magnitude-only rounding, NaR -> 0
-                const bool relu_only = MODE == 0 && QW == 2 && a.relu && a.pre_out == nullptr;
-                if (QW == 2 && relu_only && !PNN_EPI_DEBUG(1)) {
+                const bool relu_only = MODE == 0 && (QW == 2 || kTab8) && a.relu && a.pre_out == nullptr;
+                if (QW == 1 && kTab8 && relu_only && !PNN_EPI_DEBUG(1)) {
+#pragma unroll
+                    for (int x = 0; x < 8; ++x) codes[x] = q32_to_posit_tab8<true>(f, uint32_t(q[c0 + x]), s_tab8);
+                    if (cn != 0) {  // (warp-uniform: the flags are per column)
+#pragma unroll
+                        for (int x = 0; x < 8; ++x)
+                            if ((cn >> (8 * x)) & 0xFF) codes[x] = 0u;
+                    }
+                } else if (QW == 2 && relu_only && !PNN_EPI_DEBUG(1)) {
                     if (a.nowrap) {
 #pragma unroll
                         for (int x = 0; x < 8; ++x)
@@ -485,7 +493,10 @@ __global__ void __launch_bounds__(ImplGeo<D, NT_, CPS, ACC, DA, DB>::THREADS, CP
                 {
 #pragma unroll
                     for (int x = 0; x < 8; ++x) {
-                        if constexpr (kTab8)
+                        if constexpr (kTab8 && QW == 1)
+                            codes[x] = PNN_EPI_DEBUG(1) ? uint32_t(q[c0 + x])
+                                                        : q32_to_posit_tab8<false>(f, uint32_t(q[c0 + x]), s_tab8);
+                        else if constexpr (kTab8)
                             codes[x] = PNN_EPI_DEBUG(1) ? uint32_t(q[c0 + x])
                                                         : q_to_posit_tab8<false, false>(f, uint64_t(q[c0 + x]), s_tab8);
                         else

@@ -783,6 +783,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     // (epilogue.cuh q_to_posit_lut_f64: the word is the exact value, any W)
     __shared__ uint4 s_lut[QW == 2 ? kPackLutEntries : 1];
     if constexpr (QW == 2) build_pack_lut(f, s_lut, threadIdx.x, kThreads);
+    // 8-bit outputs: the rounding as one table lookup (epilogue.cuh)
+    constexpr bool kTab8 = sizeof(CodeT) == 1 && QW == 2;
+    __shared__ uint8_t s_tab8[kTab8 ? kTab8Bytes : 1];
+    if constexpr (kTab8) {
+        __syncthreads();
+        build_pack_tab8(f, s_lut, s_tab8, threadIdx.x, kThreads);
+    }
     uint8_t* zero_tile = smem + STAGES * Geo::STAGE_BYTES;
     uint64_t* full = reinterpret_cast<uint64_t*>(zero_tile + kZeroBytes);
     uint64_t* empty = full + STAGES;
@@ -998,7 +1005,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int x = 0; x < 8; ++x) {
                     const bool nar = rnar || ((cn >> (8 * x)) & 0xFF) != 0;
                     uint32_t c;
-                    if constexpr (QW == 2) c = q_to_posit_lut_f64(f, uint64_t(q[c0 + x]), s_lut);
+                    if constexpr (kTab8) c = q_to_posit_tab8<false, false>(f, uint64_t(q[c0 + x]), s_tab8);
+                    else if constexpr (QW == 2) c = q_to_posit_lut_f64x<false, false>(f, uint64_t(q[c0 + x]), s_lut);
                     else c = quire_word_to_posit_bf(f, q[c0 + x]);
                     codes[x] = nar ? (1u << (f.nbits - 1)) : c;
                 }
