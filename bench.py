@@ -485,7 +485,9 @@ def main():
                          "traffic_source": traffic["source"] if traffic else None,
                          "note": f"int8 tensor ops (2/MAC) on tcgen05 kind::i8, {D}x{D} digit "
                                  f"MMAs per posit MAC; peak = {peak_src}"},
-            "gpu_launches": args.steps * len(FORMATS) * 3,
+            # per step: 2 packs + MMA kernel per format, + the posit(16,1) 4-digit variant
+            # (launched, exits on the device flag); profiles/launches_r02_bench.json
+            "gpu_launches": args.steps * (len(FORMATS) * 3 + 1),
             "clocks": clk.summary(),
         }
         if e2e:
