@@ -70,11 +70,16 @@ constexpr int kZeroBytes = kBM * 32;
 // DR < D: the reduced-digit variant -- operands use only their first DR digit
 // planes (every value within DR balanced digits, flags from the pack kernels);
 // the packed images keep D planes per chunk (IMG_*), stages hold DR.
-template <int D, int DR = D>
+// CPS = 2: two CTAs per SM (reduced-digit variants whose groups fit 256 TMEM
+// columns): half the stages and half the TMEM each, so one CTA's TMEM drain and
+// rounding overlap the other's MMAs -- the short-K GEMMs of the Linear layers
+// are bound by that per-tile serial chain, not by the tensor pipe.
+template <int D, int DR = D, int CPS = 1>
 struct Geometry {
     static constexpr int NT = TileCfg<D>::NT;
     static constexpr int KB = TileCfg<D>::KB;
-    static constexpr int STAGES = TileCfg<D>::STAGES * D / DR > 12 ? 12 : TileCfg<D>::STAGES * D / DR;
+    static constexpr int STAGES1 = TileCfg<D>::STAGES * D / DR > 12 ? 12 : TileCfg<D>::STAGES * D / DR;
+    static constexpr int STAGES = CPS == 2 ? STAGES1 / 2 : STAGES1;
     static constexpr int G = 2 * DR - 1;
     static constexpr int NMMA = DR * NT;
     static constexpr int A_BYTES = DR * kBM * KB;
@@ -84,8 +89,9 @@ struct Geometry {
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
     static constexpr int SMEM = STAGES * STAGE_BYTES + kZeroBytes + 256;
     static_assert((NT / 2) % 8 == 0, "epilogue column split");
-    static constexpr uint32_t TMEM_COLS = 512;
-    static_assert(G * NT <= 512, "TMEM overflow");
+    static constexpr uint32_t TMEM_COLS = CPS == 2 ? 256 : 512;
+    static_assert(G * NT <= int(TMEM_COLS), "TMEM overflow");
+    static_assert(STAGES >= 2, "pipeline depth");
     static_assert(NMMA % 16 == 0 && NMMA <= 256, "bad UMMA N");
     static_assert(KB % 32 == 0, "KB must hold whole i8 MMA k-steps");
 };
@@ -757,8 +763,8 @@ __device__ __forceinline__ void tile_coords(int64_t t64, int64_t mtiles64, int64
 // issuer, warps 2..9 = epilogue (2 warps per TMEM lane quarter, each owning
 // half of the tile's columns).  The epilogue drains TMEM into registers,
 // releases it (tmem_empty), and rounds/stores while the next tile's MMAs run.
-template <int D, int QW, typename CodeT, bool kPair, int FMT = 0, int DR = D>
-__global__ void __launch_bounds__(kThreads, 1)
+template <int D, int QW, typename CodeT, bool kPair, int FMT = 0, int DR = D, int CPS = 1>
+__global__ void __launch_bounds__(kThreads, CPS)
     quire_gemm_tc_kernel(const int8_t* __restrict__ a_img, const int8_t* __restrict__ b_img,
                          int64_t kbt, int64_t kb_per_split, const uint8_t* __restrict__ row_nar,
                          const uint8_t* __restrict__ col_nar, OutMap<CodeT> out, int64_t M,
@@ -771,7 +777,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // digit plane; each CTA stages its own 128-row A tile and HALF of the
     // concatenated B rows, halving each SM's shared-memory operand traffic.
     const PositFmt f = fixed_fmt<FMT>(f_arg);  // compile-time for the BASELINE formats
-    using Geo = Geometry<D, DR>;
+    using Geo = Geometry<D, DR, CPS>;
     using QT = typename QuireWord<QW>::T;
     constexpr int NT = Geo::NT, KB = Geo::KB, STAGES = Geo::STAGES, G = Geo::G;
     constexpr int COLS = NT / 2;                 // columns per epilogue thread
@@ -1538,18 +1544,22 @@ cudaError_t launch_generic(const QuireGemmPlan& p, const GemmArgs& g, FA fa, FB 
         const int grid = int(tiles < num_sms() ? tiles : num_sms());
         if constexpr ((D == 6 || D == 8) && sizeof(CodeT) == 2 || D == 4 && sizeof(CodeT) == 1) {
             if (reduced) {  // both launched; the pack flags let exactly one run
-                using GR = Geometry<D, kRed>;
+                // 64-bit-word variants whose 2 kRed - 1 groups fit 256 TMEM columns: two CTAs per SM
+                constexpr int kCps = (D == 6 && (2 * kRed - 1) * Geo::NT <= 256) ? 2 : 1;
+                using GR = Geometry<D, kRed, kCps>;
                 // (128-bit word: this epilogue's quire_word_to_posit_bf takes W <= word bits)
                 constexpr int kFmt = D == 4 ? 2 : D == 6 ? 3 : 4;
                 // 64-bit words: posit(8,1)-class (W <= 64) and the 3-digit posit(12,1)-class
                 // variant (|X| < 2^23: |sum| < 2^46 * K <= 2^61 per split, exact as int64)
                 constexpr int kQW = D == 8 ? 4 : 2;
-                KernFn kr = fixed_fmt_id(f) == kFmt ? quire_gemm_tc_kernel<D, kQW, CodeT, false, kFmt, kRed>
-                                                    : quire_gemm_tc_kernel<D, kQW, CodeT, false, 0, kRed>;
+                KernFn kr = fixed_fmt_id(f) == kFmt ? quire_gemm_tc_kernel<D, kQW, CodeT, false, kFmt, kRed, kCps>
+                                                    : quire_gemm_tc_kernel<D, kQW, CodeT, false, 0, kRed, kCps>;
+                const int64_t slots = int64_t(kCps) * num_sms();
+                const int rgrid = int(tiles < slots ? tiles : slots);
                 if ((e = cudaFuncSetAttribute(kr, cudaFuncAttributeMaxDynamicSharedMemorySize, GR::SMEM)) !=
                     cudaSuccess)
                     return e;
-                launch_pdl(kr, dim3(grid), dim3(kThreads), GR::SMEM, st, a_img, b_img, p.kbt, p.kb_per_split, rn, cn, out, g.M,
+                launch_pdl(kr, dim3(rgrid), dim3(kThreads), GR::SMEM, st, a_img, b_img, p.kbt, p.kb_per_split, rn, cn, out, g.M,
                                                      g.N, f, partial, p.mtiles, p.ntiles, p.splits, flags + 2, 1,
                                                      tmA, tmB);
             }
