@@ -333,6 +333,39 @@ def test_fwd_reduced_digits(cuda, po, wide, shape):
         assert (host(y).reshape(want.shape) == want).all()
 
 
+@pytest.mark.parametrize("shape", [(2, 32, 8, 8, 32, 3, 1), (1, 64, 8, 8, 64, 3, 1)])
+def test_fwd_relu_only_three_digit_extremes(cuda, po, shape):
+    """posit(8,1) operands at the edge of the 3-digit variant (|x| <= 1024: X = 2^22)
+    with equal or random signs: the largest exact sums the reduced kernel can see
+    (K = 288: no W-bit wrap possible, the epilogue skips the sign extension; K = 576:
+    it does not), partial cancellations down to minpos terms, relu of negative sums."""
+    N, C, H, W, F, K, pad = shape
+    big, one = po.from_float64(8, 1, 1024.0), po.from_float64(8, 1, 1.0)
+    neg = lambda c: (-c) & 0xFF
+    pool = np.array([big, big, neg(big), one, neg(one), 1, neg(1), 0], np.uint64)
+    for seed, same_sign in ((1, True), (2, False)):
+        rng = np.random.default_rng(seed)
+        xa = np.full((N, C, H, W), big, np.uint64) if same_sign else pool[rng.integers(0, 8, (N, C, H, W))]
+        wa = pool[rng.integers(0, 8, (F, C, K, K))]
+        if same_sign:
+            wa[: F // 2] = big        # all-positive sums of K * 2^44
+            wa[F // 2:] = neg(big)    # all-negative
+        ba = pool[rng.integers(0, 8, (F,))]
+        x, w, b = dev(P81, xa), dev(P81, wa), dev(P81, ba)
+        prev = ops.conv_algo(1)
+        try:
+            ref = ops.conv2d(P81, x, w, b, 1, pad)
+        finally:
+            ops.conv_algo(prev)
+        yo, none = ops.conv2d_fwd_layer(P81, x, w, b, 1, pad, None, relu=True, want_pre=False)
+        assert none is None and torch.equal(yo, ops.relu_fwd(P81, ref))
+        y, pre = ops.conv2d_fwd_layer(P81, x, w, b, 1, pad, None, relu=True, want_pre=True)
+        assert torch.equal(pre, ref) and torch.equal(y, yo)
+        if C <= 32:
+            want = po.conv2d(8, 1, xa, wa, ba, 1, pad)
+            assert (host(pre).reshape(want.shape) == want).all()
+
+
 @pytest.mark.parametrize("cfg", [P80, P81])
 @pytest.mark.parametrize("shape", [(2, 32, 8, 8, 32, 3, 1), (1, 64, 8, 8, 64, 3, 1)])
 def test_fwd_relu_only_extremes(cuda, po, cfg, shape):
