@@ -335,6 +335,15 @@ constexpr int acc_of() { return 1; }
 template <int MODE, int D>
 constexpr int nt_of() { return cps_of<MODE, D>() == 2 ? small_nt(D) : TileCfg<D>::NT; }
 
+// PNN_WGRAD_NT64=0: the reduced weight gradient on 32-column tiles for wide layers too (A/B)
+inline bool wgrad_nt64() {
+    static const bool on = [] {
+        const char* v = getenv("PNN_WGRAD_NT64");
+        return v == nullptr || v[0] != '0';
+    }();
+    return on;
+}
+
 // PNN_IGEMM_ACC2=1: the reduced-digit forward / input-gradient kernels as ONE CTA
 // per SM with two TMEM accumulator buffers and 16 epilogue warps (instead of
 // two single-buffer CTAs): the MMA thread runs a whole tile ahead of the epilogue
@@ -949,10 +958,29 @@ int run_wgrad(const ImplPlan& p, const ConvGeom& g, const void* dy, const PositF
         a.vflag2 = dy_wide;
         a.vexpect = a.vexpect2 = 0;
         if constexpr (sizeof(CodeT) == 2) {
-            const cudaError_t er =
-                p.D == 8 ? launch_kernel<8, CodeT, 2, 4, 0, 4, 4>(tA3, tB3, a, out, st)
-                : p.OFF == 1 ? launch_kernel<6, CodeT, 2, kDgradDB, 1, kDgradDB, 4>(tA3, tB3, a, out, st)
-                             : launch_kernel<6, CodeT, 2, kDgradDB, 0, kDgradDB, 4>(tA3, tB3, a, out, st);
+            cudaError_t er;
+            // 64 output channels or more: the 3-digit variant on 64-column tiles (5 groups x
+            // 64 = 320 TMEM columns, one CTA per SM) reads each A box once per 64 channels
+            // instead of once per 32 -- the pass is L2 -> shared-memory traffic bound.
+            // Same splits and partial layout, so the finalize pass does not care which ran.
+            if (p.D == 6 && p.Fpw % 64 == 0 && p.NT == 32 && wgrad_nt64()) {
+                IgemmArgs a2 = a;
+                a2.ntiles = p.Fpw / 64;
+                a2.fd_split = FastDiv(uint32_t(a2.mtiles * a2.ntiles));
+                a2.fd_group = FastDiv(uint32_t(kGroupM * a2.ntiles));
+                CUtensorMap tB64;
+                uint32_t boxB64[5];
+                for (int i = 0; i < 5; ++i) boxB64[i] = boxB3[i];
+                boxB64[3] = 4;  // 64 channels = 4 slices
+                if (!map_act(&tB64, bdig, p.D, g.N, g.OH, g.OW, p.Fpw, boxB64)) return 5;
+                er = p.OFF == 1
+                         ? launch_kernel_geo<6, CodeT, 2, kDgradDB, 1, kDgradDB, 4, 64, 1, 1>(tA3, tB64, a2, out, st)
+                         : launch_kernel_geo<6, CodeT, 2, kDgradDB, 0, kDgradDB, 4, 64, 1, 1>(tA3, tB64, a2, out, st);
+            } else {
+                er = p.D == 8 ? launch_kernel<8, CodeT, 2, 4, 0, 4, 4>(tA3, tB3, a, out, st)
+                     : p.OFF == 1 ? launch_kernel<6, CodeT, 2, kDgradDB, 1, kDgradDB, 4>(tA3, tB3, a, out, st)
+                                  : launch_kernel<6, CodeT, 2, kDgradDB, 0, kDgradDB, 4>(tA3, tB3, a, out, st);
+            }
             if (er != cudaSuccess) return 4;
         }
         a.vor = 1;
