@@ -268,7 +268,10 @@ def test_dgrad_reduced_weight_digits(cuda, po, big, shape, dy_small):
 
 
 @pytest.mark.parametrize("wide", ["none", "x", "dy"])
-@pytest.mark.parametrize("shape", [(2, 32, 8, 8, 32, 3, 1), (3, 64, 16, 16, 64, 3, 1), (2, 3, 32, 32, 32, 3, 1)])
+@pytest.mark.parametrize("shape", [(2, 32, 8, 8, 32, 3, 1), (3, 64, 16, 16, 64, 3, 1), (2, 3, 32, 32, 32, 3, 1),
+                                   # 128 output channels: two 64-column tiles; 96: not a multiple of 64,
+                                   # the 32-column kernel
+                                   (2, 32, 8, 8, 128, 3, 1), (2, 32, 8, 8, 96, 3, 1)])
 def test_wgrad_reduced_digits(cuda, po, wide, shape):
     """Config-3 stages with activation / gradient values within 3 digits: the
     weight gradient takes the device-selected 3 x 3 digit kernel (saved (8,1)
