@@ -760,9 +760,27 @@ int run_fwd(const ImplPlan& p, const ConvGeom& g, const CodeT* x, const CodeT* w
         a.vflag = xwide;
         a.vflag2 = wwide;
         a.vexpect = a.vexpect2 = 0;
-        if constexpr (sizeof(CodeT) == 1)
-            if ((e = launch_kernel<4, CodeT, 0, kDgradDB, 0, kDgradDB>(tA3, tB3, a, out, st)) != cudaSuccess)
-                return 4;
+        if constexpr (sizeof(CodeT) == 1) {
+            // >= 64 output channels: 64-column tiles on one CTA per SM read each activation
+            // box once per 64 channels (conv3 / conv4 of the CIFAR CNN: 56.2 -> 53.3 and
+            // 82.8 -> 80.1 us); PNN_FWD_NT64=0: 32-column tiles on two CTAs per SM
+            static const bool nt64 = [] {
+                const char* v = getenv("PNN_FWD_NT64");
+                return v == nullptr || v[0] != '0';
+            }();
+            if (nt64 && p.D == 4 && p.NT == 32 && a.ntiles % 2 == 0 && a.splits == 1) {
+                IgemmArgs a2 = a;
+                a2.ntiles = a.ntiles / 2;
+                a2.fd_split = FastDiv(uint32_t(a2.mtiles * a2.ntiles));
+                a2.fd_group = FastDiv(uint32_t(kGroupM * a2.ntiles));
+                CUtensorMap tB64;
+                if (!map_weights(&tB64, bdig, p.D, p.brows, taps * p.Kp, 64, RP)) return 5;
+                e = launch_kernel_geo<4, CodeT, 0, kDgradDB, 0, kDgradDB, 0, 64, 1, 1>(tA3, tB64, a2, out, st);
+            } else {
+                e = launch_kernel<4, CodeT, 0, kDgradDB, 0, kDgradDB>(tA3, tB3, a, out, st);
+            }
+            if (e != cudaSuccess) return 4;
+        }
         if constexpr (sizeof(CodeT) == 2) {
             if (p.D == 6) {  // 64-bit quire word when a single chunk's exact sum fits
                 const bool narrow_word = a.splits == 1 && a.kb_per_split * kIKB < (int64_t(1) << 17);
